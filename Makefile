@@ -1,0 +1,34 @@
+# Builds the B200 library in-tree (travels to the GPU box with the snapshot).
+#   make            -> paper_2504_12471_b200/libd2ft_b200.so + oracle/_build/liboracle.so
+#   make ref        -> also oracle/_ref/libd2ft_ref.so (needs /root/reference)
+NVCC     ?= /usr/local/cuda/bin/nvcc
+PKG      := paper_2504_12471_b200
+CSRC     := $(PKG)/csrc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+            --expt-relaxed-constexpr -Iinclude -Xptxas -v
+OBJDIR   := build/obj
+SRCS     := $(wildcard $(CSRC)/*.cu)
+OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
+HDRS     := $(wildcard $(CSRC)/*.cuh) include/d2ft_b200.h
+LIB      := $(PKG)/libd2ft_b200.so
+
+.PHONY: all ref oracle clean
+all: $(LIB) oracle
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcuda -ldl
+
+oracle:
+	$(MAKE) -s -C oracle
+
+ref: all
+	$(MAKE) -s -j8 -C oracle ref
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean

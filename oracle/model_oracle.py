@@ -1,0 +1,267 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY — the CPU checker for the step numerics.
+
+numpy fp64 restatement of the reference's subnet model, forward/backward and
+trainer batch body.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline leg may import it; the product path never does.
+
+Pinned against the unmodified reference (oracle/_ref/libd2ft_ref.so) to ~1e-12
+relative in tests/test_oracle_vs_ref.py.
+
+Parameters use the reference's canonical flat order (model.hpp:117-153):
+  Embed: w_embed[d,d], b_embed[d], pos[T,d]
+  Block(l,h) block-major/head-minor: wq,wk,wv[d,dh], wo[dh,d], w1[d,fs], b1[fs],
+                                      w2[fs,d], b2[d/H]
+  Head: w_cls[d,C], b_cls[C]
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+import math
+
+import numpy as np
+from scipy.special import erf as _erf
+
+LN_EPS = 1e-5  # model.hpp:32
+
+
+@dataclass(frozen=True)
+class Config:
+    L: int
+    H: int
+    d: int
+    ffn: int
+    T: int
+    C: int
+
+    @property
+    def dh(self) -> int:
+        return self.d // self.H
+
+    @property
+    def fs(self) -> int:
+        return self.ffn // self.H
+
+    @property
+    def K(self) -> int:
+        return self.L * self.H
+
+
+def unpack(cfg: Config, flat: np.ndarray) -> dict:
+    """Views into the canonical flat vector (no copies)."""
+    d, dh, fs, T, C, H = cfg.d, cfg.dh, cfg.fs, cfg.T, cfg.C, cfg.H
+    off = 0
+
+    def take(*shape):
+        nonlocal off
+        n = int(np.prod(shape))
+        v = flat[off:off + n].reshape(shape)
+        off += n
+        return v
+
+    p = {"w_embed": take(d, d), "b_embed": take(d), "pos": take(T, d), "blocks": []}
+    for _ in range(cfg.K):
+        p["blocks"].append({
+            "wq": take(d, dh), "wk": take(d, dh), "wv": take(d, dh), "wo": take(dh, d),
+            "w1": take(d, fs), "b1": take(fs), "w2": take(fs, d), "b2": take(d // H)})
+    p["w_cls"] = take(d, C)
+    p["b_cls"] = take(C)
+    assert off == flat.size
+    return p
+
+
+def param_count(cfg: Config) -> int:
+    d, dh, fs = cfg.d, cfg.dh, cfg.fs
+    return d * d + d + cfg.T * d + cfg.K * (3 * d * dh + dh * d + d * fs + fs + fs * d + d // cfg.H) \
+        + d * cfg.C + cfg.C
+
+
+def subnet_slices(cfg: Config):
+    """(start, stop) of each subnet (embed, K blocks, head) in the flat vector."""
+    d, dh, fs = cfg.d, cfg.dh, cfg.fs
+    e = d * d + d + cfg.T * d
+    b = 3 * d * dh + dh * d + d * fs + fs + fs * d + d // cfg.H
+    out = [(0, e)]
+    for k in range(cfg.K):
+        out.append((e + k * b, e + (k + 1) * b))
+    out.append((e + cfg.K * b, e + cfg.K * b + d * cfg.C + cfg.C))
+    return out
+
+
+# linalg.cpp:133-151 (no affine)
+def layer_norm(x):
+    mean = x.mean(axis=1, keepdims=True)
+    var = ((x - mean) ** 2).mean(axis=1, keepdims=True)
+    inv = 1.0 / np.sqrt(var + LN_EPS)
+    return (x - mean) * inv
+
+
+# linalg.cpp:153-180
+def layer_norm_backward(x, dy):
+    n = x.shape[1]
+    mean = x.mean(axis=1, keepdims=True)
+    var = ((x - mean) ** 2).mean(axis=1, keepdims=True)
+    inv = 1.0 / np.sqrt(var + LN_EPS)
+    y = (x - mean) * inv
+    dy_mean = dy.sum(axis=1, keepdims=True) / n
+    dy_dot = (dy * y).sum(axis=1, keepdims=True) / n
+    return (dy - dy_mean - y * dy_dot) * inv
+
+
+# linalg.cpp:182-188 (exact-erf GELU and its derivative)
+def gelu(z):
+    return 0.5 * z * (1.0 + _erf(z * 0.70710678118654752440))
+
+
+def gelu_grad(z):
+    return 0.5 * (1.0 + _erf(z * 0.70710678118654752440)) + z * 0.39894228040143267794 * np.exp(-0.5 * z * z)
+
+
+def softmax_rows(s):
+    m = s.max(axis=1, keepdims=True)
+    e = np.exp(s - m)
+    return e / e.sum(axis=1, keepdims=True)
+
+
+def block_contribution(cfg, blk, h, xn, cache=None):
+    """model.cpp:197-241 (h is 0-based here; b2 offset = h*d/H, model.cpp:222)."""
+    q, k, v = xn @ blk["wq"], xn @ blk["wk"], xn @ blk["wv"]
+    probs = softmax_rows((q @ k.T) * (1.0 / math.sqrt(cfg.dh)))
+    headout = probs @ v
+    contrib = headout @ blk["wo"]
+    z = xn @ blk["w1"] + blk["b1"]
+    g = gelu(z)
+    ffn = g @ blk["w2"]
+    w = cfg.d // cfg.H
+    ffn[:, h * w:(h + 1) * w] += blk["b2"]
+    contrib = contrib + ffn
+    if cache is not None:
+        cache.update(xn=xn, q=q, k=k, v=v, probs=probs, headout=headout, z=z, g=g)
+    return contrib
+
+
+def contribution_backward(cfg, blk, h, c, dc, dxn, gb):
+    """model.cpp:243-303 (non-LoRA)."""
+    dg = dc @ blk["w2"].T
+    gb["w2"] += c["g"].T @ dc
+    w = cfg.d // cfg.H
+    gb["b2"] += dc[:, h * w:(h + 1) * w].sum(axis=0)
+    dz = dg * gelu_grad(c["z"])
+    gb["w1"] += c["xn"].T @ dz
+    gb["b1"] += dz.sum(axis=0)
+    dxn += dz @ blk["w1"].T
+    dheadout = dc @ blk["wo"].T
+    gb["wo"] += c["headout"].T @ dc
+    dprobs = dheadout @ c["v"].T
+    dv = c["probs"].T @ dheadout
+    dot = (c["probs"] * dprobs).sum(axis=1, keepdims=True)
+    dscores = c["probs"] * (dprobs - dot)
+    sc = 1.0 / math.sqrt(cfg.dh)
+    dq = (dscores @ c["k"]) * sc
+    dk = (dscores.T @ c["q"]) * sc
+    for dproj, wname in ((dq, "wq"), (dk, "wk"), (dv, "wv")):
+        gb[wname] += c["xn"].T @ dproj
+        dxn += dproj @ blk[wname].T
+
+
+def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trace=None):
+    """SubnetModel::forward_backward, model.cpp:416-520.
+
+    Returns (loss, grads_flat, engaged[K+2]).  `trace`, if a dict, receives the
+    block inputs per sample (for activation-level parity checks)."""
+    p = unpack(cfg, flat)
+    grads = np.zeros_like(flat)
+    g = unpack(cfg, grads)
+    column = list(column)
+    engaged = np.zeros(cfg.K + 2, dtype=np.uint8)
+    engaged[0] = engaged[-1] = 1
+    for r in range(cfg.K):
+        if column[r] == 1:
+            engaged[1 + r] = 1
+    n = len(inputs)
+    inv_n = 1.0 / n
+    loss = 0.0
+    L, H = cfg.L, cfg.H
+    for si in range(n):
+        inp = np.asarray(inputs[si], dtype=np.float64)
+        x = inp @ p["w_embed"] + p["b_embed"] + p["pos"]
+        xs = [x]
+        caches = [None] * cfg.K
+        for l in range(L):
+            xin = xs[-1]
+            xn = layer_norm(xin)
+            acc = xin.copy()
+            for h in range(H):
+                r = l * H + h
+                op = column[r]
+                if op == 3:
+                    continue
+                cache = {} if op == 1 else None
+                acc += block_contribution(cfg, p["blocks"][r], h, xn, cache)
+                caches[r] = cache
+            xs.append(acc)
+        if trace is not None:
+            trace.setdefault("block_inputs", []).append([a.copy() for a in xs])
+        fx = xs[-1]
+        xn_h = layer_norm(fx)
+        pooled = xn_h.mean(axis=0)
+        logits = pooled @ p["w_cls"] + p["b_cls"]
+        mx = logits.max()
+        e = np.exp(logits - mx)
+        ssum = e.sum()
+        lab = int(labels[si])
+        loss += (math.log(ssum) - (logits[lab] - mx)) * inv_n  # model.cpp:400-414
+        dlogits = e / ssum
+        dlogits[lab] -= 1.0
+        dlogits *= inv_n
+        if trace is not None:
+            trace.setdefault("logits", []).append(logits.copy())
+        g["w_cls"] += np.outer(pooled, dlogits)
+        g["b_cls"] += dlogits
+        dpooled = dlogits @ p["w_cls"].T
+        dxn_h = np.broadcast_to(dpooled / cfg.T, fx.shape)
+        dx = layer_norm_backward(fx, dxn_h)
+        for l in range(L - 1, -1, -1):
+            xin = xs[l]
+            dxn = np.zeros_like(xin)
+            anyf = False
+            for h in range(H):
+                r = l * H + h
+                if column[r] != 1:
+                    continue
+                contribution_backward(cfg, p["blocks"][r], h, caches[r], dx, dxn, g["blocks"][r])
+                anyf = True
+            if anyf:
+                dx = dx + layer_norm_backward(xin, dxn)
+        g["w_embed"] += inp.T @ dx
+        g["b_embed"] += dx.sum(axis=0)
+        g["pos"] += dx
+    return loss, grads, engaged
+
+
+def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, labels, codes, mbs,
+                lr, momentum):
+    """Trainer batch body, trainer.cpp:247-268, updating flat/velocity in place.
+
+    inputs: n_mb*mbs samples in unit order; codes: K x n_mb table."""
+    codes = np.asarray(codes, dtype=np.uint8).reshape(cfg.K, -1)
+    n_mb = codes.shape[1]
+    inv_mb = 1.0 / n_mb
+    accum = np.zeros_like(flat)
+    touched = np.zeros(cfg.K + 2, dtype=bool)
+    batch_loss = 0.0
+    for j in range(n_mb):
+        xs = inputs[j * mbs:(j + 1) * mbs]
+        ls = labels[j * mbs:(j + 1) * mbs]
+        loss, gr, eng = forward_backward(cfg, flat, xs, ls, codes[:, j])
+        batch_loss += loss * inv_mb
+        accum += gr * inv_mb
+        touched |= eng.astype(bool)
+    for si, (a, b) in enumerate(subnet_slices(cfg)):
+        if not touched[si]:
+            continue  # trainer.cpp:264-268: untouched subnets keep p and v
+        g = accum[a:b]
+        if not np.all(np.isfinite(g)):
+            raise FloatingPointError("sgd: non-finite gradient")  # trainer.cpp:118
+        velocity[a:b] = momentum * velocity[a:b] + g
+        flat[a:b] -= lr * velocity[a:b]
+    return batch_loss, touched

@@ -1,0 +1,359 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" wrapper around the UNMODIFIED reference C++ library, compiled
+// from the sources where they lie under /root/reference/proj/core/src by
+// oracle/Makefile into oracle/_ref/libd2ft_ref.so.  Only tests/, smoke() and
+// bench.py's cpu_baseline / --impl reference leg may load it.
+//
+// Every entry point calls the reference's own public API:
+//   scheduler   proj/core/include/d2ft/scheduler.hpp:135-207
+//   model       proj/core/include/d2ft/model.hpp:216-265
+//   trainer     proj/core/include/d2ft/trainer.hpp:71-98, body of train()
+//               at proj/core/src/trainer.cpp:247-268 (composed here with the
+//               same public calls, in the same order)
+//   rng         proj/core/include/d2ft/rng.hpp:16-59
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "d2ft/data.hpp"
+#include "d2ft/model.hpp"
+#include "d2ft/rng.hpp"
+#include "d2ft/scheduler.hpp"
+#include "d2ft/scoring.hpp"
+#include "d2ft/trainer.hpp"
+
+using namespace d2ft;
+
+namespace {
+
+thread_local std::string g_err;
+
+int code_of(const Error& e) {
+  switch (e.kind()) {
+    case errc::config: return 1;
+    case errc::input: return 2;
+    case errc::dimension: return 3;
+    case errc::state: return 4;
+    case errc::numeric: return 5;
+    case errc::size: return 6;
+  }
+  return 99;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 99;
+  }
+}
+
+std::vector<std::vector<double>> rows_d(const double* p, int K, int N) {
+  std::vector<std::vector<double>> r(static_cast<std::size_t>(K));
+  for (int k = 0; k < K; ++k) r[k].assign(p + static_cast<std::size_t>(k) * N, p + static_cast<std::size_t>(k + 1) * N);
+  return r;
+}
+std::vector<std::vector<int>> rows_i(const int32_t* p, int K, int N) {
+  std::vector<std::vector<int>> r(static_cast<std::size_t>(K));
+  for (int k = 0; k < K; ++k) r[k].assign(p + static_cast<std::size_t>(k) * N, p + static_cast<std::size_t>(k + 1) * N);
+  return r;
+}
+
+ScoreTable make_table(const double* bwd, const double* fwd, int K, int N) {
+  ScoreTable t;
+  t.subnets = K;
+  t.micro_batches = N;
+  t.backward = rows_d(bwd, K, N);
+  t.forward = rows_d(fwd, K, N);
+  return t;
+}
+
+CostModel make_cost(int cf, int cb, const int32_t* cf_dev, const int32_t* cb_dev, int K) {
+  CostModel cm;
+  cm.forward_cost = cf;
+  cm.backward_cost = cb;
+  if (cf_dev) cm.forward_cost_per_device.assign(cf_dev, cf_dev + K);
+  if (cb_dev) cm.backward_cost_per_device.assign(cb_dev, cb_dev + K);
+  return cm;
+}
+
+struct RefModel {
+  SubnetModel model;
+  std::vector<Subnet> velocity;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- rng
+// n draws of uniform_double from make_rng(seed, stream) (rng.hpp:24-31).
+void ref_uniform_stream(uint64_t seed, uint64_t stream, int n, double* out) {
+  auto rng = make_rng(seed, stream);
+  for (int i = 0; i < n; ++i) out[i] = uniform_double(rng);
+}
+void ref_gaussian_stream(uint64_t seed, uint64_t stream, int n, double* out) {
+  auto rng = make_rng(seed, stream);
+  for (int i = 0; i < n; ++i) out[i] = gaussian(rng);
+}
+void ref_shuffle_iota(uint64_t seed, uint64_t stream, int n, int32_t* out) {
+  auto rng = make_rng(seed, stream);
+  std::vector<int> v(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) v[i] = i;
+  shuffle(v, rng);
+  for (int i = 0; i < n; ++i) out[i] = v[i];
+}
+
+// ---------------------------------------------------------------- scheduler
+int ref_dp_search(const double* scores, const int32_t* weights, const int32_t* caps, int K, int N,
+                  int threads, uint8_t* sel_out, double* obj_out) {
+  return guarded([&] {
+    std::vector<int> c(caps, caps + K);
+    DpResult r = dp_search(rows_d(scores, K, N), rows_i(weights, K, N), c, threads);
+    for (int k = 0; k < K; ++k) {
+      obj_out[k] = r.objective[k];
+      std::memcpy(sel_out + static_cast<std::size_t>(k) * N, r.selection[k].data(), N);
+    }
+  });
+}
+
+int ref_merge_selections(const uint8_t* full_sel, const uint8_t* fwd_sel, int K, int N, uint8_t* codes) {
+  return guarded([&] {
+    std::vector<std::vector<uint8_t>> a(K), b(K);
+    for (int k = 0; k < K; ++k) {
+      a[k].assign(full_sel + static_cast<std::size_t>(k) * N, full_sel + static_cast<std::size_t>(k + 1) * N);
+      b[k].assign(fwd_sel + static_cast<std::size_t>(k) * N, fwd_sel + static_cast<std::size_t>(k + 1) * N);
+    }
+    ScheduleTable t = merge_selections(a, b);
+    std::memcpy(codes, t.codes.data(), t.codes.size());
+  });
+}
+
+int ref_knapsack_schedule(const double* bwd, const double* fwd, int cf, int cb, const int32_t* cf_dev,
+                          const int32_t* cb_dev, const int32_t* cap_full, const int32_t* cap_fwd, int K,
+                          int N, int threads, uint8_t* codes) {
+  return guarded([&] {
+    Capacities caps;
+    caps.full.assign(cap_full, cap_full + K);
+    caps.fwd.assign(cap_fwd, cap_fwd + K);
+    ScheduleTable t = knapsack_schedule(make_table(bwd, fwd, K, N), make_cost(cf, cb, cf_dev, cb_dev, K), caps, threads);
+    std::memcpy(codes, t.codes.data(), t.codes.size());
+  });
+}
+
+int ref_brute_force_schedule(const double* bwd, const double* fwd, int cf, int cb, const int32_t* cap_full,
+                             const int32_t* cap_fwd, int K, int N, uint8_t* codes) {
+  return guarded([&] {
+    Capacities caps;
+    caps.full.assign(cap_full, cap_full + K);
+    caps.fwd.assign(cap_fwd, cap_fwd + K);
+    ScheduleTable t = brute_force_schedule(make_table(bwd, fwd, K, N), make_cost(cf, cb, nullptr, nullptr, K), caps);
+    std::memcpy(codes, t.codes.data(), t.codes.size());
+  });
+}
+
+// mode: 0 Max, 1 Min, 2 Constant (scheduler.hpp:118-127)
+int ref_scaler_schedule(const double* bwd, const double* fwd, int cf, int cb, const int32_t* total_cap, int K,
+                        int N, int mode, double lambda, int threads, uint8_t* codes, double* lambda_used,
+                        int* fell_back) {
+  return guarded([&] {
+    ScalerConfig sc;
+    sc.mode = mode == 0 ? ScalerConfig::Mode::Max : mode == 1 ? ScalerConfig::Mode::Min : ScalerConfig::Mode::Constant;
+    sc.lambda = lambda;
+    std::vector<int> tc(total_cap, total_cap + K);
+    ScalerResult r = scaler_schedule(make_table(bwd, fwd, K, N), make_cost(cf, cb, nullptr, nullptr, K), tc, sc, threads);
+    std::memcpy(codes, r.table.codes.data(), r.table.codes.size());
+    *lambda_used = r.lambda_used;
+    *fell_back = r.fell_back ? 1 : 0;
+  });
+}
+
+int ref_capacities_from_budget(int n_full, int n_fwd, const int32_t* ovr, int n_ovr, int cf, int cb, int K, int N,
+                               int32_t* cap_full, int32_t* cap_fwd) {
+  return guarded([&] {
+    BudgetSpec b;
+    b.n_full = n_full;
+    b.n_fwd = n_fwd;
+    for (int i = 0; i < n_ovr; ++i) b.overrides.push_back({ovr[3 * i], ovr[3 * i + 1], ovr[3 * i + 2]});
+    Capacities c = capacities_from_budget(b, make_cost(cf, cb, nullptr, nullptr, K), K, N);
+    for (int k = 0; k < K; ++k) {
+      cap_full[k] = c.full[k];
+      cap_fwd[k] = c.fwd[k];
+    }
+  });
+}
+
+// ---------------------------------------------------------------- model
+void* ref_model_create(int L, int H, int d, int ffn, int T, int C, uint64_t seed) {
+  try {
+    ModelConfig cfg;
+    cfg.num_blocks = L;
+    cfg.heads_per_block = H;
+    cfg.model_dim = d;
+    cfg.ffn_hidden = ffn;
+    cfg.seq_len = T;
+    cfg.num_classes = C;
+    cfg.seed = seed;
+    auto* m = new RefModel{SubnetModel(cfg), {}};
+    for (const Subnet& s : m->model.subnets()) m->velocity.push_back(zeros_like(s));
+    return m;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
+
+uint64_t ref_model_param_count(void* h) { return static_cast<RefModel*>(h)->model.parameter_count(); }
+
+// canonical order (model.hpp:117-153), identical to parameter_bytes()
+void ref_model_get_params(void* h, double* out) {
+  auto* m = static_cast<RefModel*>(h);
+  std::vector<uint8_t> b = m->model.parameter_bytes(true);
+  std::memcpy(out, b.data(), b.size());
+}
+
+void ref_model_set_params(void* h, const double* in) {
+  auto* m = static_cast<RefModel*>(h);
+  std::size_t off = 0;
+  for (Subnet& s : m->model.subnets()) {
+    visit_tensors(s, [&](const char*, Matrix& mat) {
+      std::memcpy(mat.data.data(), in + off, mat.data.size() * sizeof(double));
+      off += mat.data.size();
+    });
+  }
+}
+
+void ref_model_get_velocity(void* h, double* out) {
+  auto* m = static_cast<RefModel*>(h);
+  std::size_t off = 0;
+  for (Subnet& s : m->velocity) {
+    visit_tensors(s, [&](const char*, Matrix& mat) {
+      std::memcpy(out + off, mat.data.data(), mat.data.size() * sizeof(double));
+      off += mat.data.size();
+    });
+  }
+}
+
+static void fill_inputs(const RefModel* m, const double* inputs, int n, std::vector<Matrix>& xs) {
+  const ModelConfig& c = m->model.config();
+  for (int i = 0; i < n; ++i) {
+    Matrix x(c.seq_len, c.model_dim);
+    std::memcpy(x.data.data(), inputs + static_cast<std::size_t>(i) * c.seq_len * c.model_dim,
+                x.data.size() * sizeof(double));
+    xs.push_back(std::move(x));
+  }
+}
+
+// SubnetModel::forward_backward (model.cpp:416-520). grads_flat receives the
+// canonical-order gradient of every subnet (zeros where not engaged).
+int ref_forward_backward(void* h, const double* inputs, const int32_t* labels, int n, const uint8_t* column,
+                         double* loss, double* grads_flat, uint8_t* engaged) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    std::vector<Matrix> xs;
+    fill_inputs(m, inputs, n, xs);
+    std::vector<int> lab(labels, labels + n);
+    std::vector<OperationKind> col(static_cast<std::size_t>(m->model.scheduled_count()));
+    for (std::size_t r = 0; r < col.size(); ++r) col[r] = static_cast<OperationKind>(column[r]);
+    ForwardBackwardResult fb = m->model.forward_backward(xs, lab, col);
+    *loss = fb.loss;
+    std::size_t off = 0;
+    for (std::size_t si = 0; si < fb.grads.size(); ++si) {
+      const Subnet& s = m->model.subnets()[si];
+      engaged[si] = fb.grads[si].has_value() ? 1 : 0;
+      visit_tensors(s, [&](const char* name, const Matrix& mat) {
+        if (fb.grads[si]) {
+          visit_tensors(*fb.grads[si], [&](const char* gname, const Matrix& g) {
+            if (std::strcmp(name, gname) == 0) std::memcpy(grads_flat + off, g.data.data(), g.data.size() * sizeof(double));
+          });
+        } else {
+          std::memset(grads_flat + off, 0, mat.data.size() * sizeof(double));
+        }
+        off += mat.data.size();
+      });
+    }
+  });
+}
+
+// One D2FT batch exactly as the body of train() (trainer.cpp:247-268):
+// forward_backward per micro-batch under table.column(j), accumulate with
+// 1/n_mb in micro-batch order, sgd_momentum_step on subnets with accum.
+// `inputs` holds the n_mb*mbs samples in unit order; codes is K x n_mb.
+int ref_train_batch(void* h, const double* inputs, const int32_t* labels, int n_mb, int mbs, const uint8_t* codes,
+                    double lr, double momentum, double* batch_loss) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    SubnetModel& model = m->model;
+    const int K = model.scheduled_count();
+    ScheduleTable table(K, n_mb);
+    std::memcpy(table.codes.data(), codes, table.codes.size());
+    table.validate();
+    const ModelConfig& c = model.config();
+    const double inv_mb = 1.0 / static_cast<double>(n_mb);
+    std::vector<std::optional<Subnet>> accum(model.subnets().size());
+    double loss = 0.0;
+    for (int j = 0; j < n_mb; ++j) {
+      std::vector<Matrix> xs;
+      fill_inputs(m, inputs + static_cast<std::size_t>(j) * mbs * c.seq_len * c.model_dim, mbs, xs);
+      std::vector<int> lab(labels + static_cast<std::size_t>(j) * mbs, labels + static_cast<std::size_t>(j + 1) * mbs);
+      ForwardBackwardResult fb = model.forward_backward(xs, lab, table.column(j));
+      loss += fb.loss * inv_mb;
+      for (std::size_t si = 0; si < fb.grads.size(); ++si) {
+        if (!fb.grads[si]) continue;
+        if (!accum[si]) accum[si].emplace(zeros_like(model.subnet(static_cast<int>(si))));
+        accumulate(*accum[si], *fb.grads[si], inv_mb);
+      }
+    }
+    for (std::size_t si = 0; si < accum.size(); ++si) {
+      if (!accum[si]) continue;
+      sgd_momentum_step(model.subnet(static_cast<int>(si)), *accum[si], m->velocity[si], lr, momentum,
+                        model.lora_enabled());
+    }
+    *batch_loss = loss;
+  });
+}
+
+int ref_logits(void* h, const double* input, double* out) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    std::vector<Matrix> xs;
+    fill_inputs(m, input, 1, xs);
+    Matrix lg = m->model.logits(xs[0]);
+    std::memcpy(out, lg.data.data(), lg.data.size() * sizeof(double));
+  });
+}
+
+// make_synthetic_dataset (trainer.cpp:83-111)
+int ref_make_dataset(int num_samples, int C, int d, int T, double noise, uint64_t seed, double* samples,
+                     int32_t* labels) {
+  return guarded([&] {
+    SynthDatasetSpec spec;
+    spec.num_samples = num_samples;
+    spec.num_classes = C;
+    spec.token_dim = d;
+    spec.seq_len = T;
+    spec.noise_level = noise;
+    spec.seed = seed;
+    Dataset ds = make_synthetic_dataset(spec);
+    for (int i = 0; i < num_samples; ++i) {
+      std::memcpy(samples + static_cast<std::size_t>(i) * T * d, ds.samples[i].data.data(),
+                  static_cast<std::size_t>(T) * d * sizeof(double));
+      labels[i] = ds.labels[i];
+    }
+  });
+}
+
+}  // extern "C"

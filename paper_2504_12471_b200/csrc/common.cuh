@@ -1,0 +1,59 @@
+// Shared helpers for the d2ft B200 library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace d2ft_b200 {
+
+// Status codes of the C-ABI (include/d2ft_b200.h).  1..6 mirror the
+// reference's errc categories in declaration order (error.hpp:12-19).
+enum Status : int {
+  kOk = 0,
+  kConfig = 1,
+  kInput = 2,
+  kDimension = 3,
+  kState = 4,
+  kNumeric = 5,
+  kSize = 6,
+  kCuda = 7,
+};
+
+void set_error(const std::string& msg);
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define D2FT_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t e__ = (call);                                                            \
+    if (e__ != cudaSuccess)                                                              \
+      throw ::d2ft_b200::Fail{::d2ft_b200::kCuda,                                        \
+                              std::string(#call) + ": " + cudaGetErrorString(e__)};      \
+  } while (0)
+
+#define D2FT_REQUIRE(cond, code, msg)                     \
+  do {                                                    \
+    if (!(cond)) throw ::d2ft_b200::Fail{(code), (msg)}; \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const Fail& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return kInput;
+  }
+}
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace d2ft_b200

@@ -1,0 +1,520 @@
+// D2FT scheduler and compaction kernels for sm_100a.
+//
+// Bit-exactness contract (SURVEY.md §7 "Hard parts" 1): the reference's
+// dp_search (scheduler.cpp:121-189) fills T[i][w] = max(T[i-1][w],
+// T[i-1][w-wt] + s) with a STRICT `take > skip` and backtracks with
+// `T[i][w] != T[i-1][w]`.  Two exact rewrites make it GPU-shaped:
+//  (1) decision bits: select(i,w) == (take > skip) at (i,w), so the backtrack
+//      needs one bit per cell instead of the fp64 table;
+//  (2) count compression: build_cost_tables (scheduler.cpp:104-119) gives every
+//      item of a row the same weight wt, so T[i][w] == U[i][floor(w/wt)] with
+//      the same fp64 operations in the same order; columns beyond i are equal
+//      to column i, so only min(cap/wt, N)+1 columns are needed.
+// Every fp64 operation is an add (__dadd_rn) or a compare: no contraction.
+#include "common.cuh"
+#include "sched.cuh"
+
+namespace d2ft_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;  // 8 warps: the maximum warps one row uses
+constexpr int kCMax = 8;       // DP values per thread: up to 2048 columns in registers
+constexpr size_t kSmemCap = 220 * 1024;
+
+__device__ __forceinline__ void named_sync(int nthreads) {
+  if (nthreads == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+  }
+}
+
+__host__ __device__ inline void row_geometry(int ncols, int* nw, int* C) {
+  int w = (ncols + 127) / 128;
+  w = w < 1 ? 1 : (w > 8 ? 8 : w);
+  *nw = w;
+  *C = (ncols + 32 * w - 1) / (32 * w);
+}
+
+__host__ __device__ inline int row_words(int ncols) {
+  int nw, C;
+  row_geometry(ncols, &nw, &C);
+  return nw * C;
+}
+
+__device__ inline void set_err(int32_t* err, int code) {
+  if (err) atomicCAS(err, 0, code);
+}
+
+// Count-compressed 0/1 knapsack of one row (all threads of the block call it
+// with block-uniform arguments).  s_scores: the row's N scores in shared
+// memory.  Writes sel[i] in {0,1} (shared or global) and returns the
+// objective T[N][cap] in thread 0.
+__device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, uint32_t* bits, double* xch,
+                               uint8_t* sel, double* s_obj) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Mp = (wt == 0) ? 0 : min(cap / wt, N);  // last stored column
+  const int ncols = Mp + 1;
+  int nw, C;
+  row_geometry(ncols, &nw, &C);
+  const int nthr = nw * 32;
+  const int words = nw * C;
+  const bool active = tid < nthr;
+  double v[kCMax];
+#pragma unroll
+  for (int j = 0; j < kCMax; ++j) v[j] = 0.0;
+  if (active && lane == 31) {
+#pragma unroll
+    for (int j = 0; j < kCMax; ++j) xch[warp * kCMax + j] = 0.0;  // parity 0
+  }
+  __syncthreads();
+  int p = 0;
+  if (active) {
+    for (int i = 0; i < N; ++i) {
+      const double s = s_scores[i];
+      const double* xin = xch + p * (8 * kCMax);
+      double* xout = xch + (p ^ 1) * (8 * kCMax);
+#pragma unroll
+      for (int j = 0; j < kCMax; ++j) {
+        if (j < C) {
+          const int m = j * nthr + warp * 32 + lane;
+          double prev = __shfl_up_sync(0xffffffffu, v[j], 1);
+          if (lane == 0) {
+            if (warp > 0) prev = xin[(warp - 1) * kCMax + j];
+            else prev = (j > 0) ? xin[(nw - 1) * kCMax + (j - 1)] : 0.0;
+          }
+          bool ok;
+          if (wt == 0) {  // zero weight: take reads the same column
+            prev = v[j];
+            ok = (m == 0);
+          } else {
+            ok = (m >= 1) && (m <= Mp);
+          }
+          const double take = __dadd_rn(prev, s);
+          const bool d = ok && (take > v[j]);  // scheduler.cpp:167 strict >
+          if (d) v[j] = take;
+          const unsigned ball = __ballot_sync(0xffffffffu, d);
+          if (lane == 0) bits[(size_t)i * words + j * nw + warp] = ball;
+          if (lane == 31) xout[warp * kCMax + j] = v[j];
+        }
+      }
+      p ^= 1;
+      named_sync(nthr);
+    }
+    // objective = U[N][Mp]
+#pragma unroll
+    for (int j = 0; j < kCMax; ++j) {
+      if (j < C && j * nthr + warp * 32 + lane == Mp) *s_obj = v[j];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long m = (wt == 0) ? 0 : (long long)(cap / wt);
+    for (int i = N; i > 0; --i) {
+      const long long colll = (wt == 0) ? 0 : (m < i ? m : i);
+      const int col = (int)colll;
+      const unsigned b = (bits[(size_t)(i - 1) * words + (col >> 5)] >> (col & 31)) & 1u;
+      sel[i - 1] = (uint8_t)b;
+      if (b && wt > 0) m -= 1;
+    }
+  }
+  __syncthreads();
+  return *s_obj;
+}
+
+struct KnapsackArgs {
+  const double* bwd;
+  const double* fwd;
+  const int32_t* cf;
+  const int32_t* cb;
+  const int32_t* cap_full;
+  const int32_t* cap_fwd;
+  int K, N, H;
+  uint8_t* codes;
+  CompactLists lists;
+  bool have_lists;
+  SchedWorkspace ws;
+  bool bits_in_smem;
+  int words_max;
+  bool validate;
+};
+
+// Warp 0 writes the ascending index lists of one row (codes in smem).
+__device__ void row_lists(const uint8_t* s_codes, int N, int32_t* fwd_idx, int32_t* fwd_cnt, int32_t* full_idx,
+                          int32_t* full_cnt) {
+  const int lane = threadIdx.x & 31;
+  int a = 0, f = 0;
+  for (int base = 0; base < N; base += 32) {
+    const int i = base + lane;
+    const uint8_t c = i < N ? s_codes[i] : 3;
+    const unsigned ma = __ballot_sync(0xffffffffu, c == 1 || c == 2);
+    const unsigned mf = __ballot_sync(0xffffffffu, c == 1);
+    const unsigned lt = (1u << lane) - 1u;
+    if (c == 1 || c == 2) fwd_idx[a + __popc(ma & lt)] = i;
+    if (c == 1) full_idx[f + __popc(mf & lt)] = i;
+    a += __popc(ma);
+    f += __popc(mf);
+  }
+  if (lane == 0) {
+    *fwd_cnt = a;
+    *full_cnt = f;
+  }
+}
+
+// Per-(micro-batch, block) head lists; thread per cell, heads ascending.
+__device__ void column_lists(const uint8_t* codes, int K, int N, int H, const CompactLists& L, int tid0,
+                             int stride) {
+  const int nb = K / H;
+  for (int cell = tid0; cell < N * nb; cell += stride) {
+    const int i = cell / nb, l = cell % nb;
+    int a = 0, f = 0;
+    for (int h = 0; h < H; ++h) {
+      const uint8_t c = __ldcg(codes + (size_t)(l * H + h) * N + i);
+      if (c == 1 || c == 2) L.act_heads[(size_t)cell * H + a++] = h;
+      if (c == 1) L.full_heads[(size_t)cell * H + f++] = h;
+    }
+    L.act_cnt[cell] = a;
+    L.full_hcnt[cell] = f;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int k = blockIdx.x;
+  const int N = A.N;
+  double* s_scores = reinterpret_cast<double*>(smem);
+  double* xch = s_scores + N;                    // 2 x 8 x kCMax
+  double* s_obj = xch + 2 * 8 * kCMax;           // 1 (+pad)
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 2);
+  uint8_t* s_sel = s_codes + ((N + 15) & ~15);
+  uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + ((N + 15) & ~15))
+                                  : A.ws.bits_global + (size_t)k * N * A.words_max;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+
+  const int cfk = A.cf[k], cbk = A.cb[k];
+  if (A.validate) {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double b = A.bwd[(size_t)k * N + i], f = A.fwd[(size_t)k * N + i];
+      if (!isfinite(b) || !isfinite(f) || b < 0.0 || f < 0.0) s_bad = kNumeric;  // scoring.cpp:38-41
+    }
+    if (threadIdx.x == 0 && (A.cap_full[k] < 0 || A.cap_fwd[k] < 0)) s_bad = kInput;
+    if (threadIdx.x == 0 && (cfk < 0 || cbk < 0)) s_bad = kConfig;
+    __syncthreads();
+    if (s_bad) {
+      if (threadIdx.x == 0) set_err(A.ws.err_flag, s_bad);
+      for (int i = threadIdx.x; i < N; i += blockDim.x) A.codes[(size_t)k * N + i] = 3;
+      // fall through to the compaction epilogue with an all-shortcut row
+    }
+  }
+  if (!s_bad) {
+    // pass 1: Full pool on backward scores, weight cf+cb (scheduler.cpp:233)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.bwd[(size_t)k * N + i];
+    __syncthreads();
+    dp_row_const(s_scores, N, cfk + cbk, A.cap_full[k], bits, xch, s_sel, s_obj);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_codes[i] = s_sel[i] ? 1 : 3;
+    // pass 2: Forward pool on forward scores, weight cf (scheduler.cpp:234)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.fwd[(size_t)k * N + i];
+    __syncthreads();
+    dp_row_const(s_scores, N, cfk, A.cap_fwd[k], bits, xch, s_sel, s_obj);
+    // merge (scheduler.cpp:205-216): full wins, then forward, else shortcut
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const uint8_t c = s_codes[i] == 1 ? 1 : (s_sel[i] ? 2 : 3);
+      s_codes[i] = c;
+      A.codes[(size_t)k * N + i] = c;
+    }
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_codes[i] = 3;
+  }
+  __syncthreads();
+  if (!A.have_lists) return;
+  if (threadIdx.x < 32)
+    row_lists(s_codes, N, A.lists.fwd_idx + (size_t)k * N, A.lists.fwd_cnt + k, A.lists.full_idx + (size_t)k * N,
+              A.lists.full_cnt + k);
+  // last CTA to finish builds the per-(micro-batch, block) head lists
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(A.ws.done_counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    column_lists(A.codes, A.K, N, A.H, A.lists, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0) *A.ws.done_counter = 0u;  // re-arm for the next launch
+  }
+}
+
+struct DpConstArgs {
+  const double* scores;
+  const int32_t* row_wt;
+  const int32_t* caps;
+  const int32_t* rows;
+  int N;
+  uint8_t* sel;
+  double* obj;
+  SchedWorkspace ws;
+  bool bits_in_smem;
+  int words_max;
+};
+
+__global__ void __launch_bounds__(kThreads) dp_const_kernel(DpConstArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int k = A.rows[blockIdx.x];
+  const int N = A.N;
+  double* s_scores = reinterpret_cast<double*>(smem);
+  double* xch = s_scores + N;
+  double* s_obj = xch + 2 * 8 * kCMax;
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 2);
+  uint8_t* s_sel = s_codes + ((N + 15) & ~15);
+  uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + ((N + 15) & ~15))
+                                  : A.ws.bits_global + (size_t)blockIdx.x * N * A.words_max;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.scores[(size_t)k * N + i];
+  __syncthreads();
+  const double obj = dp_row_const(s_scores, N, A.row_wt[k], A.caps[k], bits, xch, s_sel, s_obj);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) A.sel[(size_t)k * N + i] = s_sel[i];
+  if (threadIdx.x == 0) A.obj[k] = obj;
+}
+
+// General-weight row (dp_search with non-constant weights): values over
+// w in [0, cap] double-buffered in global/shared memory, one bit per cell.
+__global__ void __launch_bounds__(kThreads) dp_general_kernel(const double* scores, const int32_t* weights,
+                                                               const int32_t* caps, const int32_t* rows, int N,
+                                                               int max_cap, uint8_t* sel, double* obj,
+                                                               uint32_t* bits_global, double* vals_global) {
+  const int k = rows[blockIdx.x];
+  const int cap = caps[k];
+  const int W = cap + 1;
+  const int wordsW = (max_cap + 1 + 31) / 32;
+  uint32_t* bits = bits_global + (size_t)blockIdx.x * N * wordsW;
+  double* va = vals_global + (size_t)blockIdx.x * 2 * (max_cap + 1);
+  double* vb = va + (max_cap + 1);
+  const double* s = scores + (size_t)k * N;
+  const int32_t* wt = weights + (size_t)k * N;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) va[w] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < N; ++i) {
+    const int wi = wt[i];
+    const double si = s[i];
+    for (int base = 0; base < W; base += blockDim.x) {
+      const int w = base + threadIdx.x;
+      bool d = false;
+      if (w < W) {
+        const double skip = va[w];
+        double nv = skip;
+        if (w >= wi) {
+          const double take = __dadd_rn(va[w - wi], si);
+          d = take > skip;
+          if (d) nv = take;
+        }
+        vb[w] = nv;
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, d);
+      if ((threadIdx.x & 31) == 0 && w < W) bits[(size_t)i * wordsW + (w >> 5)] = ball;
+    }
+    __syncthreads();
+    double* t = va;
+    va = vb;
+    vb = t;
+  }
+  if (threadIdx.x == 0) {
+    obj[k] = va[cap];
+    int w = cap;
+    for (int i = N; i > 0; --i) {
+      const unsigned b = (__ldcg(bits + (size_t)(i - 1) * wordsW + (w >> 5)) >> (w & 31)) & 1u;
+      sel[(size_t)k * N + i - 1] = (uint8_t)b;
+      if (b) w -= wt[i - 1];
+    }
+  }
+}
+
+__global__ void merge_kernel(const uint8_t* a, const uint8_t* b, size_t n, uint8_t* codes) {
+  for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < n; c += (size_t)gridDim.x * blockDim.x)
+    codes[c] = a[c] ? 1 : (b[c] ? 2 : 3);
+}
+
+__global__ void compact_rows_kernel(const uint8_t* codes, int N, CompactLists L) {
+  extern __shared__ uint8_t s_codes[];
+  const int k = blockIdx.x;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) s_codes[i] = codes[(size_t)k * N + i];
+  __syncthreads();
+  if (threadIdx.x < 32)
+    row_lists(s_codes, N, L.fwd_idx + (size_t)k * N, L.fwd_cnt + k, L.full_idx + (size_t)k * N, L.full_cnt + k);
+}
+
+__global__ void compact_cols_kernel(const uint8_t* codes, int K, int N, int H, CompactLists L) {
+  column_lists(codes, K, N, H, L, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+// scaler_schedule row DP (scheduler.cpp:379-424).  Choices p_s, then p_o
+// (value lambda*f via __dmul_rn, weight cf), then p_f (value b, weight cf+cb),
+// each replacing the incumbent only on strict improvement.
+__global__ void __launch_bounds__(kThreads) scaler_kernel(const double* bwd, const double* fwd, const int32_t* cf,
+                                                          const int32_t* cb, const int32_t* total_cap, int N,
+                                                          const double* lambda_dev, int max_cap, uint8_t* codes,
+                                                          uint8_t* choice_global, double* vals_global) {
+  const int k = blockIdx.x;
+  const int cap = total_cap[k];
+  const int W = cap + 1;
+  const int w_fwd = cf[k], w_full = cf[k] + cb[k];
+  const double lam = *lambda_dev;
+  uint8_t* ch = choice_global + (size_t)k * N * (max_cap + 1);
+  double* va = vals_global + (size_t)k * 2 * (max_cap + 1);
+  double* vb = va + (max_cap + 1);
+  for (int w = threadIdx.x; w < W; w += blockDim.x) va[w] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < N; ++i) {
+    const double v_fwd = __dmul_rn(lam, fwd[(size_t)k * N + i]);
+    const double v_full = bwd[(size_t)k * N + i];
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+      double best = va[w];
+      uint8_t c = 3;
+      if (w >= w_fwd) {
+        const double cand = __dadd_rn(va[w - w_fwd], v_fwd);
+        if (cand > best) {
+          best = cand;
+          c = 2;
+        }
+      }
+      if (w >= w_full) {
+        const double cand = __dadd_rn(va[w - w_full], v_full);
+        if (cand > best) {
+          best = cand;
+          c = 1;
+        }
+      }
+      vb[w] = best;
+      ch[(size_t)i * (max_cap + 1) + w] = c;
+    }
+    __syncthreads();
+    double* t = va;
+    va = vb;
+    vb = t;
+  }
+  if (threadIdx.x == 0) {
+    int w = cap;
+    for (int i = N; i > 0; --i) {
+      const uint8_t c = __ldcg(ch + (size_t)(i - 1) * (max_cap + 1) + w);
+      codes[(size_t)k * N + i - 1] = c;
+      if (c == 1) w -= w_full;
+      else if (c == 2) w -= w_fwd;
+    }
+  }
+}
+
+}  // namespace
+
+size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
+  const int words = (max_cols + 31) / 32 + 8;
+  const size_t Np = (size_t)((N + 15) & ~15);
+  const size_t base = (size_t)N * 8 + 2 * 8 * kCMax * 8 + 16 + 2 * Np;
+  const size_t with_bits = base + (size_t)N * words * 4;
+  if (with_bits <= kSmemCap) {
+    *bits_in_smem = true;
+    return with_bits;
+  }
+  *bits_in_smem = false;
+  return base;
+}
+
+size_t knapsack_global_bits_words(int K, int N, int max_cols) {
+  const int words = (max_cols + 31) / 32 + 8;
+  return (size_t)K * N * words;
+}
+
+void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                              const int32_t* cap_full, const int32_t* cap_fwd, int K, int N, int H, int max_cols,
+                              uint8_t* codes, const CompactLists* lists, const SchedWorkspace& ws, bool validate,
+                              cudaStream_t stream) {
+  D2FT_REQUIRE(max_cols <= kThreads * kCMax, kSize, "knapsack: more than 2048 DP columns per row");
+  KnapsackArgs A{};
+  A.bwd = bwd;
+  A.fwd = fwd;
+  A.cf = cf;
+  A.cb = cb;
+  A.cap_full = cap_full;
+  A.cap_fwd = cap_fwd;
+  A.K = K;
+  A.N = N;
+  A.H = H;
+  A.codes = codes;
+  A.have_lists = lists != nullptr;
+  if (lists) A.lists = *lists;
+  A.ws = ws;
+  A.validate = validate;
+  A.words_max = (max_cols + 31) / 32 + 8;
+  const size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
+  if (!A.bits_in_smem)
+    D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(K, N, max_cols), kState,
+                 "knapsack: global decision-bit workspace too small");
+  static bool attr_done = false;
+  if (!attr_done) {
+    D2FT_CUDA(cudaFuncSetAttribute(knapsack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+    D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+    attr_done = true;
+  }
+  knapsack_kernel<<<K, kThreads, smem, stream>>>(A);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_dp_const(const double* scores, const int32_t* row_wt, const int32_t* caps, const int32_t* rows,
+                     int nrows, int N, int max_cols, uint8_t* sel, double* obj, const SchedWorkspace& ws,
+                     cudaStream_t stream) {
+  if (nrows == 0) return;
+  D2FT_REQUIRE(max_cols <= kThreads * kCMax, kSize, "dp_search: more than 2048 DP columns per row");
+  DpConstArgs A{};
+  A.scores = scores;
+  A.row_wt = row_wt;
+  A.caps = caps;
+  A.rows = rows;
+  A.N = N;
+  A.sel = sel;
+  A.obj = obj;
+  A.ws = ws;
+  A.words_max = (max_cols + 31) / 32 + 8;
+  const size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
+  if (!A.bits_in_smem)
+    D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(nrows, N, max_cols), kState,
+                 "dp_search: global decision-bit workspace too small");
+  D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+  dp_const_kernel<<<nrows, kThreads, smem, stream>>>(A);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_dp_general(const double* scores, const int32_t* weights, const int32_t* caps, const int32_t* rows,
+                       int nrows, int N, int max_cap, uint8_t* sel, double* obj, uint32_t* bits_global,
+                       double* vals_global, cudaStream_t stream) {
+  if (nrows == 0) return;
+  dp_general_kernel<<<nrows, kThreads, 0, stream>>>(scores, weights, caps, rows, N, max_cap, sel, obj, bits_global,
+                                                    vals_global);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_merge(const uint8_t* full_sel, const uint8_t* fwd_sel, size_t n, uint8_t* codes, cudaStream_t s) {
+  if (n == 0) return;
+  const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+  merge_kernel<<<blocks, 256, 0, s>>>(full_sel, fwd_sel, n, codes);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_compact(const uint8_t* codes, int K, int N, int H, const CompactLists& lists, cudaStream_t s) {
+  compact_rows_kernel<<<K, 128, (size_t)N, s>>>(codes, N, lists);
+  D2FT_CUDA(cudaGetLastError());
+  const int cells = N * (K / H);
+  compact_cols_kernel<<<(cells + 255) / 256, 256, 0, s>>>(codes, K, N, H, lists);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_scaler(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                   const int32_t* total_cap, int K, int N, const double* lambda_dev, int max_cap, uint8_t* codes,
+                   uint8_t* choice_global, double* vals_global, cudaStream_t s) {
+  scaler_kernel<<<K, kThreads, 0, s>>>(bwd, fwd, cf, cb, total_cap, N, lambda_dev, max_cap, codes, choice_global,
+                                       vals_global);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+}  // namespace d2ft_b200

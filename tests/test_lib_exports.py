@@ -1,0 +1,43 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h declares
+(no compute calls without a GPU)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(d2ft_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert "d2ft_knapsack_schedule" in names and "d2ft_dp_search" in names and "d2ft_compact" in names
+    assert len(names) >= 10
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2504_12471_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.fail("libd2ft_b200.so not built — run __graft_entry__.build()")
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_only():
+    from paper_2504_12471_b200 import _lib
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out, out
+    assert all("sm_100a" in line for line in out.splitlines() if ".cubin" in line)
