@@ -1,0 +1,263 @@
+// Host helpers for the tcgen05 GEMM: TMA descriptor encoding, SM count, and
+// self-test entry points (include/d2ft_b200_testing.h) that exercise the
+// three operand shapes the step uses.
+#include <cuda.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/d2ft_b200_testing.h"
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+
+namespace d2ft_b200 {
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  D2FT_REQUIRE(fn, kCuda, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+}  // namespace
+
+CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                              uint64_t stride2_bytes, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  const cuuint32_t box[3] = {64, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  D2FT_REQUIRE(stride1_bytes % 16 == 0 && stride2_bytes % 16 == 0, kInput, "tensor map strides must be 16B multiples");
+  D2FT_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, kInput, "tensor map base must be 16B aligned");
+  const CUresult r =
+      encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  D2FT_REQUIRE(r == CUDA_SUCCESS, kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    D2FT_CUDA(cudaGetDevice(&dev));
+    D2FT_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+namespace {
+
+// D[m][n] = sum_k A[m][k] B[n][k]; A, B 2-D row-major bf16 (K contiguous).
+template <int BN>
+struct DenseProb {
+  int M, N, K;
+  float* D;
+  struct Tile {
+    int nkb, mt, nt;
+  };
+  struct Row {};
+  __device__ int ntn() const { return (N + BN - 1) / BN; }
+  __device__ int ntiles() const { return ((M + 127) / 128) * ntn(); }
+  __device__ void tile(int t, Tile& c) const {
+    c.mt = t / ntn();
+    c.nt = t % ntn();
+    c.nkb = (K + 63) / 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, 0, kb * 64, c.nt * BN, 0};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = c.nt * BN + col0 + i;
+      if (n < N) D[(size_t)m * N + n] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// Tokens as N: D[p][m][t] = sum_k A[m][k] X[p][t][k], t < T (box of BN rows, OOB zero).
+template <int BN>
+struct PlanesProb {
+  int M, T, K, P;
+  float* D;
+  struct Tile {
+    int nkb, mt, p;
+  };
+  struct Row {};
+  __device__ int ntiles() const { return ((M + 127) / 128) * P; }
+  __device__ void tile(int t, Tile& c) const {
+    c.p = t / ((M + 127) / 128);
+    c.mt = t % ((M + 127) / 128);
+    c.nkb = (K + 63) / 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, 0, kb * 64, 0, c.p};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int t = col0 + i;
+      if (t < T) D[((size_t)c.p * M + m) * T + t] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// K = tokens of P planes: D[m][n] = sum_p sum_t XT[p][m][t] YT[p][n][t]
+// (token-innermost buffers with pitch TP; the tensor maps stop at T, so the
+// 64-token block that straddles T reads zeros).
+template <int BN>
+struct TokenKProb {
+  int M, N, T, P;
+  float* D;
+  struct Tile {
+    int nkb, mt, nt;
+  };
+  struct Row {};
+  __device__ int ntn() const { return (N + BN - 1) / BN; }
+  __device__ int ntiles() const { return ((M + 127) / 128) * ntn(); }
+  __device__ void tile(int t, Tile& c) const {
+    c.mt = t / ntn();
+    c.nt = t % ntn();
+    c.nkb = P * ((T + 63) / 64);
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int tb = (T + 63) / 64;
+    const int p = kb / tb, t0 = (kb % tb) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, p, t0, c.nt * BN, p};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = c.nt * BN + col0 + i;
+      if (n < N) D[(size_t)m * N + n] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+template <typename T>
+struct Dev {
+  T* p = nullptr;
+  explicit Dev(size_t n) { D2FT_CUDA(cudaMalloc(&p, n * sizeof(T) + 256)); }
+  ~Dev() { cudaFree(p); }
+};
+
+}  // namespace
+}  // namespace d2ft_b200
+
+using namespace d2ft_b200;
+
+extern "C" {
+
+int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int K, int bn, float* D) {
+  return guarded([&] {
+    D2FT_REQUIRE(K % 8 == 0, kInput, "K must be a multiple of 8");
+    Dev<uint16_t> dA((size_t)M * K), dB((size_t)N * K);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(dB.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
+    if (bn == 256) {
+      using S = GemmShape<256, 4>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 256);
+      launch_gemm<DenseProb<256>, S>(a, b, DenseProb<256>{M, N, K, dD.p}, 0, nullptr);
+    } else if (bn == 208) {
+      using S = GemmShape<208, 5>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 208);
+      launch_gemm<DenseProb<208>, S>(a, b, DenseProb<208>{M, N, K, dD.p}, 0, nullptr);
+    } else {
+      using S = GemmShape<160, 6>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 160);
+      launch_gemm<DenseProb<160>, S>(a, b, DenseProb<160>{M, N, K, dD.p}, 0, nullptr);
+    }
+    D2FT_CUDA(cudaDeviceSynchronize());
+    D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, int K, int P, float* D) {
+  return guarded([&] {
+    Dev<uint16_t> dA((size_t)M * K), dX((size_t)P * T * K + 256 * K);
+    Dev<float> dD((size_t)P * M * T);
+    D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(dX.p, X, (size_t)P * T * K * 2, cudaMemcpyHostToDevice));
+    using S = GemmShape<208, 5>;
+    CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dX.p, K, T, P, (uint64_t)K * 2, (uint64_t)K * T * 2, 208);
+    launch_gemm<PlanesProb<208>, S>(a, b, PlanesProb<208>{M, T, K, P, dD.p}, 0, nullptr);
+    D2FT_CUDA(cudaDeviceSynchronize());
+    D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)P * M * T * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int d2ft_test_gemm_tokenk(const uint16_t* XT, const uint16_t* YT, int M, int N, int T, int TP, int P, float* D) {
+  return guarded([&] {
+    Dev<uint16_t> dX((size_t)P * M * TP), dY((size_t)P * N * TP);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemcpy(dX.p, XT, (size_t)P * M * TP * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(dY.p, YT, (size_t)P * N * TP * 2, cudaMemcpyHostToDevice));
+    using S = GemmShape<256, 4>;
+    CUtensorMap a = make_tmap_bf16_3d(dX.p, T, M, P, (uint64_t)TP * 2, (uint64_t)TP * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dY.p, T, N, P, (uint64_t)TP * 2, (uint64_t)TP * N * 2, 256);
+    launch_gemm<TokenKProb<256>, S>(a, b, TokenKProb<256>{M, N, T, P, dD.p}, 0, nullptr);
+    D2FT_CUDA(cudaDeviceSynchronize());
+    D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Times `iters` launches of a dense M x N x K GEMM (device-resident random
+// data) with CUDA events; returns ms per launch.
+int d2ft_test_gemm_bench(int M, int N, int K, int iters, double* ms_per) {
+  return guarded([&] {
+    Dev<uint16_t> dA((size_t)M * K), dB((size_t)N * K);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemset(dA.p, 0x3c, (size_t)M * K * 2));
+    D2FT_CUDA(cudaMemset(dB.p, 0x3c, (size_t)N * K * 2));
+    using S = GemmShape<256, 4>;
+    CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 256);
+    DenseProb<256> prob{M, N, K, dD.p};
+    for (int i = 0; i < 3; ++i) launch_gemm<DenseProb<256>, S>(a, b, prob, 0, nullptr);
+    cudaEvent_t e0, e1;
+    D2FT_CUDA(cudaEventCreate(&e0));
+    D2FT_CUDA(cudaEventCreate(&e1));
+    D2FT_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) launch_gemm<DenseProb<256>, S>(a, b, prob, 0, nullptr);
+    D2FT_CUDA(cudaEventRecord(e1));
+    D2FT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    D2FT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+}  // extern "C"

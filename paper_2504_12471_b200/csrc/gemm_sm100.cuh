@@ -1,0 +1,203 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   D[m][n] = sum_k A[m][k] * B[n][k]     (bf16 operands, fp32 accumulate in TMEM)
+//
+// Both operands are K-major and arrive by TMA (128-byte swizzle) from 3-D
+// tensor maps, so a problem can gather rows from anywhere (per-head weight
+// units, per-sample token planes) and K can be a concatenation of segments
+// (active heads of a sample, Full micro-batches of a head).  Out-of-range rows
+// or tokens are zero-filled by TMA.  A problem policy P supplies the tile list,
+// the per-k-block TMA coordinates and a fused epilogue:
+//
+//   struct P {
+//     struct Tile { int nkb; ... };                 // nkb == 0: accumulator is zero
+//     struct Row { ... };                            // per-thread epilogue state
+//     __device__ int ntiles() const;
+//     __device__ void tile(int t, Tile&) const;
+//     __device__ KCoord kcoord(const Tile&, int kb) const;
+//     __device__ void row_begin(const Tile&, int row, Row&) const;
+//     __device__ void chunk(const Tile&, int row, int col0, const float (&v)[16], Row&) const;
+//     __device__ void row_end(const Tile&, int row, Row&) const;
+//   };
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
+// thread), warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM lane quarter
+// = warp % 4).  Tile M = 128 (two 64-row A boxes), N = BN, K-block = 64.
+// Two TMEM accumulators (columns 0 and 256) let the epilogue of tile i
+// overlap the MMAs of tile i+1.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace d2ft_b200 {
+
+struct KCoord {
+  int ax, ay0, ay1, az;  // A: k offset, row of the first/second 64-row half, plane
+  int bx, by, bz;        // B: k offset, first row, plane
+};
+
+template <int BN_, int STAGES_>
+struct GemmShape {
+  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
+  static_assert(B_BYTES % 1024 == 0, "B stage must keep 1024-byte swizzle alignment");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+};
+
+template <class P, class S>
+__global__ void __launch_bounds__(256, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const P prob) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* tfull = empty + S::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int i = 0; i < S::STAGES; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntiles = prob.ntiles();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        typename P::Tile c;
+        prob.tile(t, c);
+        for (int kb = 0; kb < c.nkb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          const KCoord k = prob.kcoord(c, kb);
+          uint8_t* a = sA + stage * S::A_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+          ptx::tma_load_3d(a, &tmA, &full[stage], k.ax, k.ay0, k.az);
+          ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ax, k.ay1, k.az);
+          ptx::tma_load_3d(sB + stage * S::B_BYTES, &tmB, &full[stage], k.bx, k.by, k.bz);
+          if (++stage == S::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_m128(S::BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        typename P::Tile c;
+        prob.tile(t, c);
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + acc * 256;
+        for (int kb = 0; kb < c.nkb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t ad = ptx::desc_sw128(ptx::smem_u32(sA + stage * S::A_BYTES));
+          const uint64_t bd = ptx::desc_sw128(ptx::smem_u32(sB + stage * S::B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < S::BK / 16; ++kk)
+            ptx::umma_bf16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == S::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      typename P::Tile c;
+      prob.tile(t, c);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      typename P::Row st;
+      prob.row_begin(c, row, st);
+      const uint32_t base = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int col0 = 0; col0 < S::BN; col0 += 16) {
+        float v[16];
+        if (c.nkb > 0) {
+          ptx::tmem_ld16(base + col0, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        prob.chunk(c, row, col0, v, st);
+      }
+      prob.row_end(c, row, st);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// Host side -----------------------------------------------------------------
+// 3-D bf16 tensor map: dim0 contiguous (elements), dim1 rows, dim2 planes;
+// strides in bytes (multiples of 16); box = 64 x box_rows x 1, 128-byte
+// swizzle, zero fill out of bounds.
+CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                              uint64_t stride2_bytes, uint32_t box_rows);
+
+int num_sms();
+
+template <class P, class S>
+void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int max_ctas, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    D2FT_CUDA(cudaFuncSetAttribute(gemm_sm100_kernel<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   S::SMEM_BYTES));
+    attr = true;
+  }
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (grid < 1) grid = 1;
+  gemm_sm100_kernel<P, S><<<grid, 256, S::SMEM_BYTES, stream>>>(a, b, prob);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+}  // namespace d2ft_b200

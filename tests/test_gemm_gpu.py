@@ -1,0 +1,73 @@
+"""GPU: the tcgen05/TMEM/TMA GEMM core against a plain fp32 reference of the
+same op (bf16-rounded operands, fp64 accumulation on the host)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2504_12471_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16(x):
+    """round-to-nearest-even bf16 bits and the rounded fp32 values"""
+    f = np.ascontiguousarray(x, np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    back = (r.astype(np.uint32) << 16).view(np.float32)
+    return r, back
+
+
+def _call(name, *args):
+    fn = getattr(_lib.lib(), name)
+    _lib.check(fn(*args))
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (256, 512, 768, 256), (200, 300, 320, 208),
+                                      (384, 320, 448, 160), (1000, 700, 1024, 256)])
+def test_dense(M, N, K, bn):
+    rng = np.random.default_rng(M + N + K)
+    A, Af = bf16(rng.standard_normal((M, K)))
+    B, Bf = bf16(rng.standard_normal((N, K)))
+    D = np.zeros((M, N), np.float32)
+    _call("d2ft_test_gemm_dense", _lib.ptr(A), _lib.ptr(B), C.c_int(M), C.c_int(N), C.c_int(K), C.c_int(bn),
+          _lib.ptr(D))
+    ref = Af.astype(np.float64) @ Bf.astype(np.float64).T
+    err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+
+
+def test_planes_tokens_as_n():
+    M, T, K, P = 448, 197, 768, 5
+    rng = np.random.default_rng(1)
+    A, Af = bf16(rng.standard_normal((M, K)))
+    X, Xf = bf16(rng.standard_normal((P, T, K)))
+    D = np.zeros((P, M, T), np.float32)
+    _call("d2ft_test_gemm_planes", _lib.ptr(A), _lib.ptr(X), C.c_int(M), C.c_int(T), C.c_int(K), C.c_int(P),
+          _lib.ptr(D))
+    ref = np.einsum("mk,ptk->pmt", Af.astype(np.float64), Xf.astype(np.float64))
+    err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+
+
+def test_tokens_as_k_zero_fill():
+    M, N, T, TP, P = 320, 768, 197, 208, 6
+    rng = np.random.default_rng(2)
+    XT, XTf = bf16(rng.standard_normal((P, M, TP)))
+    YT, YTf = bf16(rng.standard_normal((P, N, TP)))
+    D = np.zeros((M, N), np.float32)
+    _call("d2ft_test_gemm_tokenk", _lib.ptr(XT), _lib.ptr(YT), C.c_int(M), C.c_int(N), C.c_int(T), C.c_int(TP),
+          C.c_int(P), _lib.ptr(D))
+    ref = np.einsum("pmt,pnt->mn", XTf[:, :, :T].astype(np.float64), YTf[:, :, :T].astype(np.float64))
+    err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+
+
+def test_dense_throughput_reported():
+    ms = C.c_double()
+    M = N = K = 8192
+    _call("d2ft_test_gemm_bench", C.c_int(M), C.c_int(N), C.c_int(K), C.c_int(10), C.byref(ms))
+    tflops = 2.0 * M * N * K / (ms.value * 1e-3) / 1e12
+    print(f"dense 8192^3 bf16 tcgen05: {ms.value:.3f} ms = {tflops:.0f} TFLOP/s")
+    assert tflops > 100
