@@ -1,0 +1,92 @@
+/* d2ft_b200 — C-ABI of the D2FT step engine (one B200).
+ *
+ * Replaces, for the D2FT policy, the batch body of
+ *   d2ft::train()                     core/src/trainer.cpp:214-292
+ * i.e. knapsack_schedule (scheduler.cpp:222-236) -> per micro-batch
+ *   SubnetModel::forward_backward     core/src/model.cpp:416-520
+ * -> 1/n_mb accumulation (trainer.cpp:247-260) -> sgd_momentum_step on the
+ * subnets that received gradients (trainer.cpp:113-134, 264-268).
+ * Status codes as in d2ft_b200.h.  Parameters cross the boundary in the
+ * reference's canonical fp64 order (model.hpp:117-153, the order of
+ * SubnetModel::parameter_bytes / the checkpoint); the engine keeps fp32
+ * masters + velocity and bf16 operand copies on the device.
+ */
+#ifndef D2FT_B200_ENGINE_H
+#define D2FT_B200_ENGINE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ModelConfig (model.hpp:43-57).  The B200 engine requires model_dim % 128 == 0,
+ * model_dim <= 1024, head_dim (d/H) in {32, 64}, seq_len <= 256, <= 64 classes. */
+typedef struct {
+  int num_blocks, heads_per_block, model_dim, ffn_hidden, seq_len, num_classes;
+  uint64_t seed;
+} d2ft_model_config;
+
+typedef struct d2ft_engine d2ft_engine;
+
+int d2ft_engine_create(const d2ft_model_config* cfg, int max_batch, d2ft_engine** out);
+int d2ft_engine_destroy(d2ft_engine* e);
+/* number of fp64 values in the canonical flat parameter vector */
+int64_t d2ft_engine_param_count(d2ft_engine* e);
+/* load parameters (canonical fp64 order); resets the momentum to zero */
+int d2ft_engine_set_params(d2ft_engine* e, const double* flat);
+int d2ft_engine_get_params(d2ft_engine* e, double* flat);
+/* momentum buffers, canonical order (the trainer's `velocity`, trainer.cpp:194-196) */
+int d2ft_engine_get_velocity(d2ft_engine* e, double* flat);
+/* gradients of the last forward_backward / step, canonical order; subnets
+ * without a Full cell hold stale values (check the schedule) */
+int d2ft_engine_get_grads(d2ft_engine* e, double* flat);
+
+/* SubnetModel::forward_backward (model.cpp:416-520) for n samples of one
+ * micro-batch under one schedule column (K = L*H codes).  Loss = mean CE;
+ * gradients (scaled 1/n) readable with d2ft_engine_get_grads. */
+int d2ft_engine_forward_backward(d2ft_engine* e, const float* samples, const int32_t* labels, int n,
+                                 const uint8_t* column, double* loss_out);
+
+/* One trainer batch with an explicit K x n_mb schedule table (Standard policy
+ * = all 1).  samples: (n_mb*mbs) x T x d fp32 in micro-batch order; loss_out
+ * = batch loss as trainer.cpp:254. */
+int d2ft_engine_step_codes(d2ft_engine* e, const float* samples, const int32_t* labels, const uint8_t* codes,
+                           int n_mb, int mbs, double lr, double momentum, double* loss_out);
+
+/* One D2FT batch: schedule from the batch's score slice (K x n_mb fp64,
+ * ScoreTable::backward / forward of trainer.cpp:139-154) with per-row costs
+ * cf/cb and capacities, then forward/backward/SGD.  codes_out (K x n_mb,
+ * may be NULL) receives the schedule.  Host buffers; synchronous. */
+int d2ft_engine_step(d2ft_engine* e, const float* samples, const int32_t* labels, const double* bwd_scores,
+                     const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                     const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, double* loss_out,
+                     uint8_t* codes_out);
+
+/* Benchmark path: stage inputs once on the device, then run device-resident
+ * steps (asynchronous on d2ft_engine_stream) and d2ft_engine_sync. */
+int d2ft_engine_stage_device(d2ft_engine* e, const float* samples, const int32_t* labels, const double* bwd_scores,
+                             const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                             const int32_t* cap_fwd, int n_mb, int mbs);
+int d2ft_engine_step_resident(d2ft_engine* e, int n_mb, int mbs, double lr, double momentum);
+int d2ft_engine_sync(d2ft_engine* e, double* loss_out);
+void* d2ft_engine_stream(d2ft_engine* e);
+
+/* Per-phase device time (CUDA events between phases) accumulated while
+ * profiling is on: sched, embed, ln, G1, attn_fwd, G3, head, G4, attn_bwd,
+ * G5, G7, G8, bias, ln_bwd, embed_wgrad, sgd. */
+int d2ft_engine_set_profiling(d2ft_engine* e, int on);
+int d2ft_engine_phase_ms(d2ft_engine* e, double* ms_out, int n, int* steps);
+/* per-sample schedule codes of the last step, K x max_batch */
+int d2ft_engine_codes(d2ft_engine* e, uint8_t* codes_exp_out);
+
+/* partition_model (model.cpp:140-156): canonical fp64 flat initial
+ * parameters, bit-identical to the reference for the same config/seed. */
+int d2ft_partition_model(const d2ft_model_config* cfg, double* out);
+/* make_synthetic_dataset (trainer.cpp:83-111), samples returned as fp32
+ * (the engine's input precision; the fp64 draws are rounded once). */
+int d2ft_make_synthetic_dataset(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
+                                uint64_t seed, float* samples, int32_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

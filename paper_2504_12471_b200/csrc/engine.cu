@@ -1,0 +1,772 @@
+// D2FT step engine: one fine-tuning step of the subnet-partitioned model on
+// one B200 (trainer.cpp:214-292 for the D2FT policy), device resident.
+//
+//   schedule (fused knapsack kernel) -> expand to per-sample codes -> compaction
+//   -> embed GEMM -> L x [LN, G1, attention, G3] -> head/CE
+//   -> L x [G4, attention bwd, G5, G7, G8, bias sums, LN bwd]
+//   -> embed wgrad -> SGD-momentum on touched subnets (+ bf16 operand copies)
+//
+// Parameters live as fp32 masters in an arena laid out for the GEMMs (see
+// DESIGN.md §3); the canonical fp64 flat vector of the reference
+// (model.hpp:117-153) is the interchange format at the C-ABI.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/d2ft_b200.h"
+#include "../../include/d2ft_b200_engine.h"
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+#include "sched.cuh"
+#include "step_common.cuh"
+#include "step_gemms.cuh"
+#include "step_kernels.cuh"
+
+namespace d2ft_b200 {
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  D2FT_CUDA(cudaMalloc(&p, n * sizeof(T) + 256));
+  D2FT_CUDA(cudaMemset(p, 0, n * sizeof(T) + 256));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+// Phases timed when profiling is on (d2ft_engine_phase_ms).
+enum Phase {
+  PH_SCHED,
+  PH_EMBED,
+  PH_LN,
+  PH_G1,
+  PH_ATTN_F,
+  PH_G3,
+  PH_HEAD,
+  PH_G4,
+  PH_ATTN_B,
+  PH_G5,
+  PH_G7,
+  PH_G8,
+  PH_BIAS,
+  PH_LN_BWD,
+  PH_EMBED_W,
+  PH_SGD,
+  PH_COUNT
+};
+
+}  // namespace
+
+struct Engine {
+  Dims D{};
+  int Kmax_mb;  // scheduler items capacity (= Bmax)
+  int KS = 8;   // embed wgrad split
+  int BNt;      // token tile (UMMA N) of the tokens-as-N GEMMs
+  std::vector<void*> owned;
+  cudaStream_t st = nullptr;
+
+  // parameter arena segments (fp32 masters, velocity, gradient share offsets)
+  struct Seg {
+    size_t off, n;
+    long long outer, inner;
+  };
+  enum { S_W1T, S_B1, S_W2T, S_B2, S_WET, S_BE, S_POS, S_WC, S_BC, S_N };
+  Seg seg[S_N];
+  size_t nparam = 0;
+  float *P = nullptr, *V = nullptr, *G = nullptr;
+  bf16 *W1T_bf, *W1_bf, *W2T_bf, *W2_bf, *WeT_bf;
+
+  // activations
+  float* x;       // [L+1][Bmax][T][d]
+  float* stats;   // [L][Bmax][T][2]
+  bf16 *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
+  bf16 *Y1, *OG, *OGT;
+  float* lse;     // [L][Bmax][H][T]
+  bf16 *inp, *inpT;
+  float* samples_dev;
+  int* labels_dev;
+  // backward scratch
+  float *dX, *dxn, *part_cs, *part_db1, *part_ew;
+  bf16 *dC, *dCT, *dO, *dY1, *dY1T;
+  double *loss_s, *loss;
+  float *pooled, *dlog;
+  // schedule / compaction
+  double *bwd_dev, *fwd_dev;
+  int32_t *cf_dev, *cb_dev, *capf_dev, *capo_dev;
+  uint8_t *codes_mb, *codes_exp;
+  int32_t* lists_mem;
+  CompactLists lists{};
+  int *g1_tiles, *g1_count, *g4_tiles, *g4_count;
+  uint32_t* sched_bits = nullptr;
+  size_t sched_bits_words = 0;
+  unsigned int* sched_counter;
+  int* err;
+  int sched_max_cols = 0;
+  // pinned staging
+  float* h_samples = nullptr;
+  int* h_labels = nullptr;
+  double* h_scores = nullptr;
+  double* h_loss = nullptr;
+  int* h_err = nullptr;
+  uint8_t* h_codes = nullptr;
+
+  // tensor maps
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_OG, tm_W2, tm_dC, tm_dCT, tm_OGT, tm_dY1T, tm_xnT, tm_W1,
+      tm_dY1, tm_inpT;
+
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_phase;
+  double phase_ms[PH_COUNT] = {};
+  int profiled_steps = 0;
+
+  void mark(int ph) {
+    if (!profiling) return;
+    cudaEvent_t e;
+    D2FT_CUDA(cudaEventCreate(&e));
+    D2FT_CUDA(cudaEventRecord(e, st));
+    ev.push_back(e);
+    ev_phase.push_back(ph);
+  }
+  void collect() {
+    if (!profiling || ev.empty()) return;
+    D2FT_CUDA(cudaEventSynchronize(ev.back()));
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      D2FT_CUDA(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+      if (ev_phase[i - 1] < PH_COUNT) phase_ms[ev_phase[i - 1]] += ms;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    ev_phase.clear();
+    ++profiled_steps;
+  }
+
+  Engine(const d2ft_model_config& c, int Bmax) {
+    D2FT_REQUIRE(c.num_blocks >= 1 && c.heads_per_block >= 1 && c.model_dim >= 1 && c.ffn_hidden >= 1 &&
+                     c.seq_len >= 1 && c.num_classes >= 1,
+                 kConfig, "model config: all dimensions must be >= 1");
+    D2FT_REQUIRE(c.model_dim % c.heads_per_block == 0, kConfig,
+                 "model config: model_dim must be divisible by heads_per_block");
+    D2FT_REQUIRE(c.ffn_hidden % c.heads_per_block == 0, kConfig,
+                 "model config: ffn_hidden must be divisible by heads_per_block");
+    D.L = c.num_blocks;
+    D.H = c.heads_per_block;
+    D.d = c.model_dim;
+    D.ffn = c.ffn_hidden;
+    D.T = c.seq_len;
+    D.C = c.num_classes;
+    D.dh = D.d / D.H;
+    D.fs = D.ffn / D.H;
+    D2FT_REQUIRE(D.d % 128 == 0 && D.d <= 1024, kConfig, "b200 engine: model_dim must be a multiple of 128, <= 1024");
+    D2FT_REQUIRE(D.dh == 32 || D.dh == 64, kConfig, "b200 engine: head_dim (d/H) must be 32 or 64");
+    D2FT_REQUIRE(D.fs % 8 == 0, kConfig, "b200 engine: ffn slice must be a multiple of 8");
+    D2FT_REQUIRE(D.T <= 256, kConfig, "b200 engine: seq_len must be <= 256");
+    D2FT_REQUIRE(D.C <= 64, kConfig, "b200 engine: at most 64 classes");
+    D2FT_REQUIRE(Bmax >= 1 && Bmax <= 1024, kConfig, "b200 engine: batch capacity must be in [1, 1024]");
+    D.PQ = 3 * D.dh + D.fs;
+    D.PO = D.dh + D.fs;
+    D.UQ = (D.PQ + 63) / 64;
+    D.UO = (D.PO + 63) / 64;
+    D.TP = (D.T + 7) / 8 * 8;
+    D.TQ = (D.T + 15) / 16 * 16;
+    D.TB = (D.T + 63) / 64;
+    D.Bmax = Bmax;
+    D.B = Bmax;
+    Kmax_mb = Bmax;
+    BNt = D.T <= 64 ? 64 : D.T <= 128 ? 128 : D.T <= 208 ? 208 : 256;
+    KS = std::min(8, Bmax);
+    D2FT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    alloc_all();
+    make_maps();
+  }
+
+  ~Engine() {
+    for (auto e : ev) cudaEventDestroy(e);
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : owned) cudaFree(p);
+    if (h_samples) cudaFreeHost(h_samples);
+    if (h_labels) cudaFreeHost(h_labels);
+    if (h_scores) cudaFreeHost(h_scores);
+    if (h_loss) cudaFreeHost(h_loss);
+    if (h_err) cudaFreeHost(h_err);
+    if (h_codes) cudaFreeHost(h_codes);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void alloc_all() {
+    const size_t L = D.L, H = D.H, d = D.d, T = D.T, Bm = D.Bmax, PQ = D.PQ, PO = D.PO, TP = D.TP, fs = D.fs;
+    size_t off = 0;
+    auto add = [&](int id, size_t n, long long outer, long long inner) {
+      seg[id] = Seg{off, n, outer, inner};
+      off += (n + 63) / 64 * 64;
+    };
+    add(S_W1T, L * H * PQ * d, (long long)(H * PQ * d), (long long)(PQ * d));
+    add(S_B1, L * H * fs, (long long)(H * fs), (long long)fs);
+    add(S_W2T, L * d * H * PO, (long long)(d * H * PO), (long long)PO);
+    add(S_B2, L * d, (long long)d, (long long)(d / H));
+    add(S_WET, d * d, 0, 1);
+    add(S_BE, d, 0, 1);
+    add(S_POS, T * d, 0, 1);
+    add(S_WC, d * D.C, 0, 1);
+    add(S_BC, D.C, 0, 1);
+    nparam = off;
+    P = dalloc<float>(nparam, owned);
+    V = dalloc<float>(nparam, owned);
+    G = dalloc<float>(nparam, owned);
+    W1T_bf = dalloc<bf16>(L * H * PQ * d, owned);
+    W1_bf = dalloc<bf16>(L * H * PQ * d, owned);
+    W2T_bf = dalloc<bf16>(L * d * H * PO, owned);
+    W2_bf = dalloc<bf16>(L * d * H * PO, owned);
+    WeT_bf = dalloc<bf16>(d * d, owned);
+
+    x = dalloc<float>((L + 1) * Bm * T * d, owned);
+    stats = dalloc<float>(L * Bm * T * 2, owned);
+    xn = dalloc<bf16>(L * Bm * T * d, owned);
+    xnT = dalloc<bf16>(L * Bm * d * TP, owned);
+    Y1 = dalloc<bf16>(L * Bm * H * T * PQ, owned);
+    OG = dalloc<bf16>(L * Bm * H * T * PO, owned);
+    OGT = dalloc<bf16>(L * Bm * H * PO * TP, owned);
+    lse = dalloc<float>(L * Bm * H * T, owned);
+    inp = dalloc<bf16>(Bm * T * d, owned);
+    inpT = dalloc<bf16>(Bm * d * TP, owned);
+    samples_dev = dalloc<float>(Bm * T * d, owned);
+    labels_dev = dalloc<int>(Bm, owned);
+
+    dX = dalloc<float>(Bm * T * d, owned);
+    dxn = dalloc<float>(Bm * T * d, owned);
+    const size_t ntile = (T + 31) / 32;
+    part_cs = dalloc<float>(Bm * ntile * d, owned);
+    part_db1 = dalloc<float>(Bm * H * fs, owned);
+    part_ew = dalloc<float>((size_t)KS * d * d, owned);
+    dC = dalloc<bf16>(Bm * T * d, owned);
+    dCT = dalloc<bf16>(Bm * d * TP, owned);
+    dO = dalloc<bf16>(Bm * H * T * D.dh, owned);
+    dY1 = dalloc<bf16>(Bm * H * T * PQ, owned);
+    dY1T = dalloc<bf16>(Bm * H * PQ * TP, owned);
+    loss_s = dalloc<double>(Bm, owned);
+    loss = dalloc<double>(1, owned);
+    pooled = dalloc<float>(Bm * d, owned);
+    dlog = dalloc<float>(Bm * D.C, owned);
+
+    const size_t K = (size_t)D.K();
+    bwd_dev = dalloc<double>(K * Bm, owned);
+    fwd_dev = dalloc<double>(K * Bm, owned);
+    cf_dev = dalloc<int32_t>(K, owned);
+    cb_dev = dalloc<int32_t>(K, owned);
+    capf_dev = dalloc<int32_t>(K, owned);
+    capo_dev = dalloc<int32_t>(K, owned);
+    codes_mb = dalloc<uint8_t>(K * Bm, owned);
+    codes_exp = dalloc<uint8_t>(K * Bm, owned);
+    const size_t cells = Bm * L;
+    lists_mem = dalloc<int32_t>(2 * K * Bm + 2 * K + 2 * cells * H + 2 * cells, owned);
+    int32_t* p = lists_mem;
+    lists.fwd_idx = p;
+    p += K * Bm;
+    lists.full_idx = p;
+    p += K * Bm;
+    lists.fwd_cnt = p;
+    p += K;
+    lists.full_cnt = p;
+    p += K;
+    lists.act_heads = p;
+    p += cells * H;
+    lists.full_heads = p;
+    p += cells * H;
+    lists.act_cnt = p;
+    p += cells;
+    lists.full_hcnt = p;
+    g1_tiles = dalloc<int>(L * Bm * ((D.UQ * H + 1) / 2), owned);
+    g4_tiles = dalloc<int>(L * Bm * ((D.UO * H + 1) / 2), owned);
+    g1_count = dalloc<int>(L, owned);
+    g4_count = dalloc<int>(L, owned);
+    sched_counter = dalloc<unsigned int>(1, owned);
+    err = dalloc<int>(1, owned);
+
+    D2FT_CUDA(cudaMallocHost(&h_samples, Bm * T * d * sizeof(float)));
+    D2FT_CUDA(cudaMallocHost(&h_labels, Bm * sizeof(int)));
+    D2FT_CUDA(cudaMallocHost(&h_scores, 2 * K * Bm * sizeof(double)));
+    D2FT_CUDA(cudaMallocHost(&h_loss, sizeof(double)));
+    D2FT_CUDA(cudaMallocHost(&h_err, sizeof(int)));
+    D2FT_CUDA(cudaMallocHost(&h_codes, K * Bm));
+  }
+
+  void make_maps() {
+    const uint64_t L = D.L, H = D.H, d = D.d, T = D.T, Bm = D.Bmax, PQ = D.PQ, PO = D.PO, TP = D.TP;
+    // A operands (box 64 rows)
+    tm_WeT = make_tmap_bf16_3d(WeT_bf, d, d, 1, d * 2, d * d * 2, 64);
+    tm_W1T = make_tmap_bf16_3d(W1T_bf, d, H * PQ, L, d * 2, H * PQ * d * 2, 64);
+    tm_W2T = make_tmap_bf16_3d(W2T_bf, H * PO, d, L, H * PO * 2, d * H * PO * 2, 64);
+    tm_W2 = make_tmap_bf16_3d(W2_bf, d, H * PO, L, d * 2, H * PO * d * 2, 64);
+    tm_W1 = make_tmap_bf16_3d(W1_bf, H * PQ, d, L, H * PQ * 2, d * H * PQ * 2, 64);
+    tm_dCT = make_tmap_bf16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
+    tm_dY1T = make_tmap_bf16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
+    // B operands, tokens as N (box BNt)
+    tm_inp = make_tmap_bf16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt);
+    tm_xn = make_tmap_bf16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt);
+    tm_OG = make_tmap_bf16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt);
+    tm_dC = make_tmap_bf16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt);
+    tm_dY1 = make_tmap_bf16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt);
+    // B operands, tokens as K
+    tm_OGT = make_tmap_bf16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 160);
+    tm_xnT = make_tmap_bf16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 256);
+    tm_inpT = make_tmap_bf16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 256);
+  }
+
+  // ---------------------------------------------------------------- params
+  // canonical flat (model.hpp:117-153) <-> arena
+  template <bool kToArena>
+  void convert(double* flat, std::vector<float>& a) const {
+    const int L = D.L, H = D.H, d = D.d, dh = D.dh, fs = D.fs, T = D.T, C = D.C, PQ = D.PQ, PO = D.PO;
+    size_t o = 0;
+    auto mv = [&](size_t ai) {
+      if (kToArena) a[ai] = (float)flat[o++];
+      else flat[o++] = a[ai];
+    };
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) mv(seg[S_WET].off + (size_t)j * d + i);  // w_embed[i][j] -> WeT[j][i]
+    for (int j = 0; j < d; ++j) mv(seg[S_BE].off + j);
+    for (int t = 0; t < T; ++t)
+      for (int j = 0; j < d; ++j) mv(seg[S_POS].off + (size_t)t * d + j);
+    for (int l = 0; l < L; ++l)
+      for (int h = 0; h < H; ++h) {
+        const size_t w1 = seg[S_W1T].off + ((size_t)(l * H + h) * PQ) * d;
+        const size_t w2 = seg[S_W2T].off + (size_t)l * d * H * PO + (size_t)h * PO;
+        for (int q = 0; q < 3; ++q)  // wq, wk, wv [d][dh] -> W1T rows q*dh + j
+          for (int i = 0; i < d; ++i)
+            for (int j = 0; j < dh; ++j) mv(w1 + (size_t)(q * dh + j) * d + i);
+        for (int j = 0; j < dh; ++j)  // wo [dh][d] -> W2T[m][h*PO + j]
+          for (int m = 0; m < d; ++m) mv(w2 + (size_t)m * H * PO + j);
+        for (int i = 0; i < d; ++i)  // w1 [d][fs] -> W1T rows 3dh + j
+          for (int j = 0; j < fs; ++j) mv(w1 + (size_t)(3 * dh + j) * d + i);
+        for (int j = 0; j < fs; ++j) mv(seg[S_B1].off + (size_t)(l * H + h) * fs + j);
+        for (int j = 0; j < fs; ++j)  // w2 [fs][d] -> W2T[m][h*PO + dh + j]
+          for (int m = 0; m < d; ++m) mv(w2 + (size_t)m * H * PO + dh + j);
+        for (int j = 0; j < d / H; ++j) mv(seg[S_B2].off + (size_t)l * d + h * (d / H) + j);
+      }
+    for (int i = 0; i < d; ++i)
+      for (int c = 0; c < C; ++c) mv(seg[S_WC].off + (size_t)i * C + c);
+    for (int c = 0; c < C; ++c) mv(seg[S_BC].off + c);
+  }
+
+  size_t canonical_count() const {
+    const size_t d = D.d, dh = D.dh, fs = D.fs, H = D.H;
+    return d * d + d + (size_t)D.T * d + (size_t)D.L * H * (3 * d * dh + dh * d + d * fs + fs + fs * d + d / H) +
+           d * D.C + D.C;
+  }
+
+  void refresh_bf16_all() {
+    launch_f32_to_bf16(P + seg[S_W1T].off, W1T_bf, seg[S_W1T].n, st);
+    launch_f32_to_bf16(P + seg[S_W2T].off, W2T_bf, seg[S_W2T].n, st);
+    launch_f32_to_bf16(P + seg[S_WET].off, WeT_bf, seg[S_WET].n, st);
+    refresh_transposes(nullptr);
+  }
+  void refresh_transposes(const int* full_cnt) {
+    // W1_bf[l][m][h*PQ+f] = W1T_bf[l][h*PQ+f][m];  W2_bf[l][h*PO+f][m] = W2T_bf[l][m][h*PO+f]
+    launch_transpose_bf16(W1T_bf, W1_bf, D.L, D.H * D.PQ, D.d, D.PQ, D.H, full_cnt, st);
+    launch_transpose_bf16_colheads(W2T_bf, W2_bf, D.L, D.d, D.H * D.PO, D.PO, D.H, full_cnt, st);
+  }
+
+  void set_params(const double* flat) {
+    std::vector<float> a(nparam, 0.f);
+    convert<true>(const_cast<double*>(flat), a);
+    D2FT_CUDA(cudaMemcpyAsync(P, a.data(), nparam * 4, cudaMemcpyHostToDevice, st));
+    refresh_bf16_all();
+    D2FT_CUDA(cudaStreamSynchronize(st));
+  }
+  void get_arena(float* src, double* flat) {
+    std::vector<float> a(nparam);
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    D2FT_CUDA(cudaMemcpy(a.data(), src, nparam * 4, cudaMemcpyDeviceToHost));
+    convert<false>(flat, a);
+  }
+
+  // ---------------------------------------------------------------- GEMM dispatch
+  template <template <int> class Prob, class... Args>
+  void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
+    switch (BNt) {
+      case 64:
+        launch_gemm<Prob<64>, GemmShape<64, 8>>(a, b, Prob<64>{args...}, 0, st);
+        break;
+      case 128:
+        launch_gemm<Prob<128>, GemmShape<128, 6>>(a, b, Prob<128>{args...}, 0, st);
+        break;
+      case 208:
+        launch_gemm<Prob<208>, GemmShape<208, 5>>(a, b, Prob<208>{args...}, 0, st);
+        break;
+      default:
+        launch_gemm<Prob<256>, GemmShape<256, 4>>(a, b, Prob<256>{args...}, 0, st);
+        break;
+    }
+  }
+
+  // ---------------------------------------------------------------- the step
+  // Requires codes_exp + compaction lists + plan for this batch.
+  void run_forward_backward() {
+    const size_t L = D.L, Bm = D.Bmax, T = D.T, d = D.d, H = D.H;
+    const size_t xs = Bm * T * d;
+    mark(PH_EMBED);
+    launch_prep_input(D, samples_dev, inp, inpT, st);
+    gemm_tokN<EmbedFwd>(tm_WeT, tm_inp, D, P + seg[S_BE].off, P + seg[S_POS].off, x);
+    for (int l = 0; l < D.L; ++l) {
+      mark(PH_LN);
+      launch_ln_fwd(D, x + l * xs, xn + l * xs, xnT + (size_t)l * Bm * d * D.TP, stats + (size_t)l * Bm * T * 2, st);
+      mark(PH_G1);
+      bf16* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      bf16* OGl = OG + (size_t)l * Bm * H * T * D.PO;
+      bf16* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
+      const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
+      gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, Y1l, OGl, OGTl);
+      mark(PH_ATTN_F);
+      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, Y1l, OGl, OGTl, lse + (size_t)l * Bm * H * T, st);
+      mark(PH_G3);
+      gemm_tokN<G3>(tm_W2T, tm_OG, D, l, lists.act_heads, lists.act_cnt, codes_exp, P + seg[S_B2].off + (size_t)l * d,
+                    x + l * xs, x + (l + 1) * xs);
+    }
+    mark(PH_HEAD);
+    launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off, 1.0f / (float)D.B, loss_s, pooled,
+                dlog, dX, st);
+    launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
+    mark(PH_LN_BWD);
+    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, dCT, part_cs, st);
+    for (int l = D.L - 1; l >= 0; --l) {
+      bf16* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      bf16* OGl = OG + (size_t)l * Bm * H * T * D.PO;
+      mark(PH_G4);
+      const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
+      gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt, Y1l, dO,
+                    dY1, dY1T, part_db1);
+      mark(PH_ATTN_B);
+      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, Y1l, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
+                      st);
+      mark(PH_G5);
+      launch_gemm<G5<160>, GemmShape<160, 6>>(
+          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO},
+          0, st);
+      mark(PH_G7);
+      launch_gemm<G7<256>, GemmShape<256, 4>>(
+          tm_dY1T, tm_xnT,
+          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d}, 0, st);
+      mark(PH_G8);
+      gemm_tokN<G8>(tm_W1, tm_dY1, D, l, lists.full_heads, lists.full_hcnt, dxn);
+      mark(PH_BIAS);
+      launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
+                         G + seg[S_B2].off + (size_t)l * d, st);
+      mark(PH_LN_BWD);
+      launch_ln_bwd_prep(D, l, lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, dCT, part_cs,
+                         st);
+    }
+    mark(PH_EMBED_W);
+    launch_gemm<EmbedW<256>, GemmShape<256, 4>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew}, 0, st);
+    launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
+  }
+
+  void run_sgd(float lr, float mom) {
+    mark(PH_SGD);
+    const int* fc = lists.full_cnt;
+    auto sgd = [&](int id, bf16* pbf, const int* touch) {
+      const Seg& s = seg[id];
+      launch_sgd(P + s.off, V + s.off, G + s.off, pbf, s.n, s.outer, s.inner, D.H, touch, lr, mom, err, st);
+    };
+    sgd(S_W1T, W1T_bf, fc);
+    sgd(S_B1, nullptr, fc);
+    sgd(S_W2T, W2T_bf, fc);
+    sgd(S_B2, nullptr, fc);
+    sgd(S_WET, WeT_bf, nullptr);
+    sgd(S_BE, nullptr, nullptr);
+    sgd(S_POS, nullptr, nullptr);
+    sgd(S_WC, nullptr, nullptr);
+    sgd(S_BC, nullptr, nullptr);
+    refresh_transposes(fc);
+  }
+
+  // per-sample codes already in codes_exp: compaction + plan
+  void compact_and_plan() {
+    launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
+    launch_plan(D, lists.act_cnt, lists.full_hcnt, g1_tiles, g1_count, g4_tiles, g4_count, st);
+  }
+
+  void ensure_sched(int max_cols) {
+    if (max_cols <= sched_max_cols) return;
+    sched_max_cols = max_cols;
+    bool in_smem = true;
+    knapsack_smem_bytes(D.Bmax, max_cols, &in_smem);
+    if (!in_smem) {
+      const size_t w = knapsack_global_bits_words(D.K(), D.Bmax, max_cols);
+      if (w > sched_bits_words) {
+        D2FT_CUDA(cudaStreamSynchronize(st));
+        void* p = nullptr;
+        D2FT_CUDA(cudaMalloc(&p, w * 4));
+        owned.push_back(p);
+        sched_bits = static_cast<uint32_t*>(p);
+        sched_bits_words = w;
+      }
+    }
+  }
+
+  // D2FT schedule of n_mb micro-batches from device scores/costs.
+  void schedule_device(int n_mb, int mbs) {
+    mark(PH_SCHED);
+    SchedWorkspace ws{};
+    ws.bits_global = sched_bits;
+    ws.bits_global_words = sched_bits_words;
+    ws.done_counter = sched_counter;
+    ws.err_flag = err;
+    launch_knapsack_schedule(bwd_dev, fwd_dev, cf_dev, cb_dev, capf_dev, capo_dev, D.K(), n_mb, D.H, sched_max_cols,
+                             codes_mb, nullptr, ws, true, st);
+    launch_expand_codes(codes_mb, D.K(), n_mb, mbs, D.B, D.Bmax, codes_exp, st);
+    compact_and_plan();
+  }
+
+  void begin_step(int B) {
+    D2FT_REQUIRE(B >= 1 && B <= D.Bmax, kSize, "step: batch exceeds the engine capacity");
+    D.B = B;
+    D2FT_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  }
+
+  int finish_and_check() {
+    mark(PH_COUNT);
+    D2FT_CUDA(cudaMemcpyAsync(h_loss, loss, sizeof(double), cudaMemcpyDeviceToHost, st));
+    D2FT_CUDA(cudaMemcpyAsync(h_err, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    collect();
+    return *h_err;
+  }
+};
+
+}  // namespace d2ft_b200
+
+using namespace d2ft_b200;
+
+struct d2ft_engine {
+  Engine* e;
+};
+
+namespace {
+
+void validate_labels(const int32_t* labels, int B, int C) {
+  for (int i = 0; i < B; ++i) D2FT_REQUIRE(labels[i] >= 0 && labels[i] < C, kInput, "label out of range");
+}
+
+void validate_sched_inputs(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                           const int32_t* cap_full, const int32_t* cap_fwd, int K, int N) {
+  const double* sides[2] = {fwd, bwd};
+  for (int s = 0; s < 2; ++s)
+    for (size_t c = 0; c < (size_t)K * N; ++c) {
+      D2FT_REQUIRE(std::isfinite(sides[s][c]), kNumeric, "score table contains non-finite entries");
+      D2FT_REQUIRE(sides[s][c] >= 0.0, kNumeric, "score table contains negative entries");
+    }
+  for (int k = 0; k < K; ++k) D2FT_REQUIRE(cap_full[k] >= 0, kInput, "capacities: negative full capacity");
+  for (int k = 0; k < K; ++k) D2FT_REQUIRE(cap_fwd[k] >= 0, kInput, "capacities: negative forward capacity");
+  for (int k = 0; k < K; ++k)
+    D2FT_REQUIRE(cf[k] >= 0 && cb[k] >= 0, kConfig, "cost model: costs must be nonnegative integers");
+}
+
+int max_cols_of(const int32_t* cf, const int32_t* cb, const int32_t* capf, const int32_t* capo, int K, int N) {
+  auto cols = [N](int wt, int cap) { return wt == 0 ? 1 : std::min(cap / wt, N) + 1; };
+  int mc = 1;
+  for (int k = 0; k < K; ++k) mc = std::max(mc, std::max(cols(cf[k] + cb[k], capf[k]), cols(cf[k], capo[k])));
+  return mc;
+}
+
+void check_status(int e) {
+  if (e) throw Fail{e, e == kNumeric ? "non-finite score or gradient detected on the device"
+                                     : "device-side validation failed"};
+}
+
+}  // namespace
+
+extern "C" {
+
+int d2ft_engine_create(const d2ft_model_config* cfg, int max_batch, d2ft_engine** out) {
+  return guarded([&] {
+    D2FT_REQUIRE(cfg && out, kInput, "engine_create: null argument");
+    *out = new d2ft_engine{new Engine(*cfg, max_batch)};
+  });
+}
+
+int d2ft_engine_destroy(d2ft_engine* e) {
+  return guarded([&] {
+    if (e) {
+      delete e->e;
+      delete e;
+    }
+  });
+}
+
+int64_t d2ft_engine_param_count(d2ft_engine* e) { return e && e->e ? (int64_t)e->e->canonical_count() : -1; }
+
+int d2ft_engine_set_params(d2ft_engine* e, const double* flat) {
+  return guarded([&] {
+    D2FT_REQUIRE(e && e->e && flat, kInput, "set_params: null argument");
+    e->e->set_params(flat);
+    D2FT_CUDA(cudaMemsetAsync(e->e->V, 0, e->e->nparam * 4, e->e->st));
+    D2FT_CUDA(cudaStreamSynchronize(e->e->st));
+  });
+}
+
+int d2ft_engine_get_params(d2ft_engine* e, double* flat) {
+  return guarded([&] { e->e->get_arena(e->e->P, flat); });
+}
+
+int d2ft_engine_get_velocity(d2ft_engine* e, double* flat) {
+  return guarded([&] { e->e->get_arena(e->e->V, flat); });
+}
+
+int d2ft_engine_get_grads(d2ft_engine* e, double* flat) {
+  return guarded([&] { e->e->get_arena(e->e->G, flat); });
+}
+
+int d2ft_engine_forward_backward(d2ft_engine* h, const float* samples, const int32_t* labels, int n,
+                                 const uint8_t* column, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_REQUIRE(n >= 1, kInput, "micro-batch inputs and labels must be non-empty and aligned");
+    for (int k = 0; k < E.D.K(); ++k)
+      D2FT_REQUIRE(column[k] >= 1 && column[k] <= 3, kInput, "schedule table: code out of range");
+    validate_labels(labels, n, E.D.C);
+    E.begin_step(n);
+    const size_t xs = (size_t)n * E.D.T * E.D.d;
+    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, samples, xs * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, n * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, column, E.D.K(), cudaMemcpyHostToDevice, E.st));
+    launch_expand_codes(E.codes_mb, E.D.K(), 1, n, n, E.D.Bmax, E.codes_exp, E.st);
+    E.compact_and_plan();
+    E.run_forward_backward();
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+  });
+}
+
+int d2ft_engine_step_codes(d2ft_engine* h, const float* samples, const int32_t* labels, const uint8_t* codes,
+                           int n_mb, int mbs, double lr, double momentum, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
+    const int B = n_mb * mbs;
+    for (size_t c = 0; c < (size_t)E.D.K() * n_mb; ++c)
+      D2FT_REQUIRE(codes[c] >= 1 && codes[c] <= 3, kInput, "schedule table: code out of range");
+    validate_labels(labels, B, E.D.C);
+    E.begin_step(B);
+    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, samples, (size_t)B * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, B * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, codes, (size_t)E.D.K() * n_mb, cudaMemcpyHostToDevice, E.st));
+    launch_expand_codes(E.codes_mb, E.D.K(), n_mb, mbs, B, E.D.Bmax, E.codes_exp, E.st);
+    E.compact_and_plan();
+    E.run_forward_backward();
+    E.run_sgd((float)lr, (float)momentum);
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+  });
+}
+
+int d2ft_engine_step(d2ft_engine* h, const float* samples, const int32_t* labels, const double* bwd_scores,
+                     const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                     const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, double* loss_out,
+                     uint8_t* codes_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    const int K = E.D.K();
+    D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
+    const int B = n_mb * mbs;
+    validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
+    validate_labels(labels, B, E.D.C);
+    E.begin_step(B);
+    E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+    const size_t KN = (size_t)K * n_mb;
+    std::memcpy(E.h_samples, samples, (size_t)B * E.D.T * E.D.d * 4);
+    std::memcpy(E.h_scores, bwd_scores, KN * 8);
+    std::memcpy(E.h_scores + KN, fwd_scores, KN * 8);
+    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, E.h_samples, (size_t)B * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, B * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.bwd_dev, E.h_scores, KN * 8, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.fwd_dev, E.h_scores + KN, KN * 8, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.cf_dev, cf, K * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.cb_dev, cb, K * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, E.st));
+    E.schedule_device(n_mb, mbs);
+    E.run_forward_backward();
+    E.run_sgd((float)lr, (float)momentum);
+    if (codes_out) D2FT_CUDA(cudaMemcpyAsync(E.h_codes, E.codes_mb, KN, cudaMemcpyDeviceToHost, E.st));
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+    if (codes_out) std::memcpy(codes_out, E.h_codes, KN);
+  });
+}
+
+int d2ft_engine_stage_device(d2ft_engine* h, const float* samples, const int32_t* labels, const double* bwd_scores,
+                             const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                             const int32_t* cap_fwd, int n_mb, int mbs) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    const int K = E.D.K();
+    const int B = n_mb * mbs;
+    D2FT_REQUIRE(B >= 1 && B <= E.D.Bmax, kSize, "stage: batch exceeds the engine capacity");
+    validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
+    validate_labels(labels, B, E.D.C);
+    E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+    const size_t KN = (size_t)K * n_mb;
+    D2FT_CUDA(cudaMemcpy(E.samples_dev, samples, (size_t)B * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.labels_dev, labels, B * 4, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.bwd_dev, bwd_scores, KN * 8, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.fwd_dev, fwd_scores, KN * 8, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.cf_dev, cf, K * 4, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.cb_dev, cb, K * 4, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(E.capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+// Device-resident step on the staged inputs: no host copies, no sync.
+int d2ft_engine_step_resident(d2ft_engine* h, int n_mb, int mbs, double lr, double momentum) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    E.begin_step(n_mb * mbs);
+    E.schedule_device(n_mb, mbs);
+    E.run_forward_backward();
+    E.run_sgd((float)lr, (float)momentum);
+  });
+}
+
+int d2ft_engine_sync(d2ft_engine* h, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    check_status(E.finish_and_check());
+    if (loss_out) *loss_out = *E.h_loss;
+  });
+}
+
+void* d2ft_engine_stream(d2ft_engine* h) { return h && h->e ? (void*)h->e->st : nullptr; }
+
+int d2ft_engine_set_profiling(d2ft_engine* h, int on) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    E.profiling = on != 0;
+    for (double& v : E.phase_ms) v = 0.0;
+    E.profiled_steps = 0;
+  });
+}
+
+int d2ft_engine_phase_ms(d2ft_engine* h, double* ms_out, int n, int* steps) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    for (int i = 0; i < n && i < PH_COUNT; ++i) ms_out[i] = E.phase_ms[i];
+    if (steps) *steps = E.profiled_steps;
+  });
+}
+
+int d2ft_engine_codes(d2ft_engine* h, uint8_t* codes_exp_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_CUDA(cudaStreamSynchronize(E.st));
+    D2FT_CUDA(cudaMemcpy(codes_exp_out, E.codes_exp, (size_t)E.D.K() * E.D.Bmax, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

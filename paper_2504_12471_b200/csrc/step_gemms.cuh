@@ -1,0 +1,429 @@
+// GEMM problem policies of the D2FT step (GEMM table G1-G8).
+// Orientation: "tokens as N" — a sample's T tokens are the UMMA N dimension
+// (one TMA box of BN token rows, zero-filled past T), weight features are M
+// in 64-row units gathered per active head, so no tile ever straddles two
+// samples.  Weight gradients use "tokens as K" over the Full micro-batches of
+// a head.  All operands are K-major bf16; accumulation is fp32 in TMEM.
+#pragma once
+#include "gemm_sm100.cuh"
+#include "step_common.cuh"
+
+namespace d2ft_b200 {
+
+struct NoRow {};
+
+// ---------------------------------------------------------------- embed fwd
+// x0[s][t][m] = sum_j inp[s][t][j] w_embed[j][m] + b_embed[m] + pos[t][m]
+// (model.cpp:313-317).  A = WeT (d x d), B = inp (plane s).
+template <int BN>
+struct EmbedFwd {
+  Dims D;
+  const float* be;
+  const float* pos;
+  float* x0;
+  struct Tile {
+    int nkb, s, mt;
+  };
+  using Row = NoRow;
+  __device__ int ntiles() const { return D.B * (D.d / 128); }
+  __device__ void tile(int t, Tile& c) const {
+    c.s = t / (D.d / 128);
+    c.mt = t % (D.d / 128);
+    c.nkb = D.d / 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, 0, kb * 64, 0, c.s};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    const float b = be[m];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int t = col0 + i;
+      if (t < D.T) x0[((size_t)c.s * D.T + t) * D.d + m] = v[i] + b + pos[(size_t)t * D.d + m];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- G1
+// [q|k|v|z] = xn . [Wq|Wk|Wv|W1]  per (sample, active head)  (model.cpp:200-202, 218-220)
+// A = W1T (plane l, rows h*PQ + f), B = xn (plane l*Bmax + s).  Epilogue:
+// q,k,v,z -> Y1 (token-major); g = gelu(z + b1) -> OG (token-major, G3's B)
+// and OGT (feature-major, G5's B).
+template <int BN>
+struct G1 {
+  Dims D;
+  int l;
+  const int* tiles;
+  const int* count;
+  const int* act_heads;
+  const int* act_cnt;
+  const float* b1;  // block l: [H][fs]
+  bf16* Y1;         // block l: [Bmax][H][T][PQ]
+  bf16* OG;         // block l: [Bmax][H][T][PO]
+  bf16* OGT;        // block l: [Bmax][H][PO][TP]
+  struct Tile {
+    int nkb, s, u0, nu;
+  };
+  struct Row {
+    int valid, h, f;
+    float bias;
+  };
+  __device__ int ntiles() const { return *count; }
+  __device__ void tile(int t, Tile& c) const {
+    const int p = tiles[t];
+    c.s = p >> 16;
+    c.u0 = p & 0xffff;
+    c.nu = D.UQ * act_cnt[c.s * D.L + l];
+    c.nkb = D.d / 64;
+  }
+  __device__ int unit_row(const Tile& c, int u) const {
+    const int h = act_heads[(c.s * D.L + l) * D.H + u / D.UQ];
+    return h * D.PQ + (u % D.UQ) * 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int u1 = c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0;
+    return KCoord{kb * 64, unit_row(c, c.u0), unit_row(c, u1), l, kb * 64, 0, l * D.Bmax + c.s};
+  }
+  __device__ void row_begin(const Tile& c, int row, Row& r) const {
+    const int u = c.u0 + (row >> 6);
+    r.valid = u < c.nu;
+    if (!r.valid) return;
+    r.h = act_heads[(c.s * D.L + l) * D.H + u / D.UQ];
+    r.f = (u % D.UQ) * 64 + (row & 63);
+    r.valid = r.f < D.PQ;
+    r.bias = (r.valid && r.f >= 3 * D.dh) ? b1[r.h * D.fs + (r.f - 3 * D.dh)] : 0.f;
+  }
+  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
+    if (!r.valid || col0 >= D.T) return;
+    const size_t sh = (size_t)c.s * D.H + r.h;
+    bf16* y = Y1 + sh * D.T * D.PQ + r.f;
+    if (r.f < 3 * D.dh) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col0 + i < D.T) y[(size_t)(col0 + i) * D.PQ] = __float2bfloat16_rn(v[i]);
+      return;
+    }
+    const int j = r.f - 3 * D.dh;
+    float g[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float z = v[i] + r.bias;
+      g[i] = gelu_f(z);
+      if (col0 + i < D.T) {
+        y[(size_t)(col0 + i) * D.PQ] = __float2bfloat16_rn(z);
+        OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = __float2bfloat16_rn(g[i]);
+      }
+    }
+    bf16* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
+    if (col0 + 8 <= D.TP) st_bf16x8(gt, g);
+    if (col0 + 16 <= D.TP) st_bf16x8(gt + 8, g + 8);
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- G3
+// x_{l+1} = x_l + sum_{active h} ( [O_h|g_h] . [Wo_h;W2_h] + b2_h on its slice )
+// (model.cpp:216, 221-225, 454-468).  A = W2T (plane l, K offset h*PO),
+// B = OG (plane (l*Bmax+s)*H+h).  K = concatenation over the sample's active
+// heads; the sum over heads happens inside TMEM in head order.
+template <int BN>
+struct G3 {
+  Dims D;
+  int l;
+  const int* act_heads;
+  const int* act_cnt;
+  const uint8_t* codes;  // expanded K x Bmax
+  const float* b2;       // block l: [d]
+  const float* xin;
+  float* xout;
+  struct Tile {
+    int nkb, s, mt;
+  };
+  struct Row {
+    float bias;
+  };
+  __device__ int ntiles() const { return D.B * (D.d / 128); }
+  __device__ void tile(int t, Tile& c) const {
+    c.s = t / (D.d / 128);
+    c.mt = t % (D.d / 128);
+    c.nkb = D.UO * act_cnt[c.s * D.L + l];
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int a = kb / D.UO, kk = kb % D.UO;
+    const int h = act_heads[(c.s * D.L + l) * D.H + a];
+    return KCoord{h * D.PO + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, (l * D.Bmax + c.s) * D.H + h};
+  }
+  __device__ void row_begin(const Tile& c, int row, Row& r) const {
+    const int m = c.mt * 128 + row;
+    const int hm = m / (D.d / D.H);
+    const uint8_t code = codes[(size_t)(l * D.H + hm) * D.Bmax + c.s];
+    r.bias = (code == 1 || code == 2) ? b2[m] : 0.f;  // p_s adds nothing (model.cpp:458)
+  }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
+    const int m = c.mt * 128 + row;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int t = col0 + i;
+      if (t < D.T) {
+        const size_t o = ((size_t)c.s * D.T + t) * D.d + m;
+        xout[o] = xin[o] + v[i] + r.bias;
+      }
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- G4
+// d[O|g] = dC . [Wo;W2]^T per (sample, Full head)  (model.cpp:247, 262);
+// epilogue dz = dg * gelu'(z) (model.cpp:254), db1 row sums (model.cpp:257).
+// A = W2 (plane l, rows h*PO + f), B = dC (plane s).
+template <int BN>
+struct G4 {
+  Dims D;
+  int l;
+  const int* tiles;
+  const int* count;
+  const int* full_heads;
+  const int* full_hcnt;
+  const bf16* Y1;  // block l
+  bf16* dO;        // [Bmax][H][T][dh]
+  bf16* dY1;       // [Bmax][H][T][PQ]
+  bf16* dY1T;      // [Bmax][H][PQ][TP]
+  float* part_db1; // [Bmax][H][fs]
+  struct Tile {
+    int nkb, s, u0, nu;
+  };
+  struct Row {
+    int valid, h, f;
+    float db;
+  };
+  __device__ int ntiles() const { return *count; }
+  __device__ void tile(int t, Tile& c) const {
+    const int p = tiles[t];
+    c.s = p >> 16;
+    c.u0 = p & 0xffff;
+    c.nu = D.UO * full_hcnt[c.s * D.L + l];
+    c.nkb = D.d / 64;
+  }
+  __device__ int unit_row(const Tile& c, int u) const {
+    const int h = full_heads[(c.s * D.L + l) * D.H + u / D.UO];
+    return h * D.PO + (u % D.UO) * 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int u1 = c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0;
+    return KCoord{kb * 64, unit_row(c, c.u0), unit_row(c, u1), l, kb * 64, 0, c.s};
+  }
+  __device__ void row_begin(const Tile& c, int row, Row& r) const {
+    const int u = c.u0 + (row >> 6);
+    r.valid = u < c.nu;
+    r.db = 0.f;
+    if (!r.valid) return;
+    r.h = full_heads[(c.s * D.L + l) * D.H + u / D.UO];
+    r.f = (u % D.UO) * 64 + (row & 63);
+    r.valid = r.f < D.PO;
+  }
+  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
+    if (!r.valid || col0 >= D.T) return;
+    const size_t sh = (size_t)c.s * D.H + r.h;
+    if (r.f < D.dh) {
+      bf16* o = dO + sh * D.T * D.dh + r.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col0 + i < D.T) o[(size_t)(col0 + i) * D.dh] = __float2bfloat16_rn(v[i]);
+      return;
+    }
+    const int j = r.f - D.dh;
+    const int fq = 3 * D.dh + j;
+    const bf16* z = Y1 + sh * D.T * D.PQ + fq;
+    bf16* dy = dY1 + sh * D.T * D.PQ + fq;
+    float dz[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int t = col0 + i;
+      dz[i] = 0.f;
+      if (t < D.T) {
+        dz[i] = v[i] * gelu_grad_f(__bfloat162float(z[(size_t)t * D.PQ]));
+        dy[(size_t)t * D.PQ] = __float2bfloat16_rn(dz[i]);
+        r.db += dz[i];
+      }
+    }
+    bf16* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
+    if (col0 + 8 <= D.TP) st_bf16x8(dt, dz);
+    if (col0 + 16 <= D.TP) st_bf16x8(dt + 8, dz + 8);
+  }
+  __device__ void row_end(const Tile& c, int, Row& r) const {
+    if (r.valid && r.f >= D.dh) part_db1[((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)] = r.db;
+  }
+};
+
+// ---------------------------------------------------------------- G5
+// dW2T[l][m][h*PO + f] = sum_{s in Full(h)} sum_t dC[s][t][m] [O|g][s][h][t][f]
+// (model.cpp:249, 263).  A = dCT (plane s), B = OGT (plane (l*Bmax+s)*H+h).
+template <int BN>
+struct G5 {
+  Dims D;
+  int l;
+  const int* full_idx;  // row k: Bmax entries
+  const int* full_cnt;
+  float* dW2T;  // block l: [d][H*PO]
+  struct Tile {
+    int nkb, h, mt, nt;
+  };
+  using Row = NoRow;
+  __device__ int ntn() const { return (D.PO + BN - 1) / BN; }
+  __device__ int ntiles() const { return D.H * (D.d / 128) * ntn(); }
+  __device__ void tile(int t, Tile& c) const {
+    const int per = (D.d / 128) * ntn();
+    c.h = t / per;
+    const int r = t % per;
+    c.mt = r / ntn();
+    c.nt = r % ntn();
+    c.nkb = D.TB * full_cnt[l * D.H + c.h];
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int s = full_idx[(size_t)(l * D.H + c.h) * D.Bmax + kb / D.TB];
+    const int t0 = (kb % D.TB) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s, t0, c.nt * BN, (l * D.Bmax + s) * D.H + c.h};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int f = c.nt * BN + col0 + i;
+      if (f < D.PO) out[f] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- G7
+// dW1T[l][h][f][m] = sum_{s in Full(h)} sum_t d[q|k|v|z][s][h][t][f] xn[s][t][m]
+// (model.cpp:256, 286).  A = dY1T (plane s*H+h), B = xnT (plane l*Bmax+s).
+template <int BN>
+struct G7 {
+  Dims D;
+  int l;
+  const int* full_idx;
+  const int* full_cnt;
+  float* dW1T;  // block l: [H][PQ][d]
+  struct Tile {
+    int nkb, h, mt, nt;
+  };
+  using Row = NoRow;
+  __device__ int ntm() const { return (D.PQ + 127) / 128; }
+  __device__ int ntn() const { return (D.d + BN - 1) / BN; }
+  __device__ int ntiles() const { return D.H * ntm() * ntn(); }
+  __device__ void tile(int t, Tile& c) const {
+    const int per = ntm() * ntn();
+    c.h = t / per;
+    const int r = t % per;
+    c.mt = r / ntn();
+    c.nt = r % ntn();
+    c.nkb = D.TB * full_cnt[l * D.H + c.h];
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int s = full_idx[(size_t)(l * D.H + c.h) * D.Bmax + kb / D.TB];
+    const int t0 = (kb % D.TB) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s * D.H + c.h, t0, c.nt * BN, l * D.Bmax + s};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int f = c.mt * 128 + row;
+    if (f >= D.PQ) return;
+    float* out = dW1T + ((size_t)c.h * D.PQ + f) * D.d;
+    const int n0 = c.nt * BN + col0;
+    if (n0 + 16 <= D.d) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(out + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n0 + i < D.d) out[n0 + i] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- G8
+// dxn[s] = sum_{Full h} d[q|k|v|z]_h . [Wq|Wk|Wv|W1]_h^T  (model.cpp:259, 288)
+// A = W1 (plane l, K offset h*PQ), B = dY1 (plane s*H+h).
+template <int BN>
+struct G8 {
+  Dims D;
+  int l;
+  const int* full_heads;
+  const int* full_hcnt;
+  float* dxn;  // [Bmax][T][d]
+  struct Tile {
+    int nkb, s, mt;
+  };
+  using Row = NoRow;
+  __device__ int ntiles() const { return D.B * (D.d / 128); }
+  __device__ void tile(int t, Tile& c) const {
+    c.s = t / (D.d / 128);
+    c.mt = t % (D.d / 128);
+    c.nkb = D.UQ * full_hcnt[c.s * D.L + l];
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int a = kb / D.UQ, kk = kb % D.UQ;
+    const int h = full_heads[(c.s * D.L + l) * D.H + a];
+    return KCoord{h * D.PQ + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, c.s * D.H + h};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int t = col0 + i;
+      if (t < D.T) dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+// ---------------------------------------------------------------- embed wgrad
+// dWeT[m][j] = sum_s sum_t dx0[s][t][m] inp[s][t][j]  (model.cpp:514), split
+// over KS sample groups into partial sums (reduced deterministically later).
+template <int BN>
+struct EmbedW {
+  Dims D;
+  int KS;
+  float* part;  // [KS][d][d]
+  struct Tile {
+    int nkb, ks, mt, nt, s0;
+  };
+  using Row = NoRow;
+  __device__ int ntn() const { return (D.d + BN - 1) / BN; }
+  __device__ int ntiles() const { return KS * (D.d / 128) * ntn(); }
+  __device__ void tile(int t, Tile& c) const {
+    const int per = (D.d / 128) * ntn();
+    c.ks = t / per;
+    const int r = t % per;
+    c.mt = r / ntn();
+    c.nt = r % ntn();
+    c.s0 = c.ks * D.B / KS;
+    c.nkb = D.TB * ((c.ks + 1) * D.B / KS - c.s0);
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int s = c.s0 + kb / D.TB;
+    const int t0 = (kb % D.TB) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s, t0, c.nt * BN, s};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    float* out = part + ((size_t)c.ks * D.d + m) * D.d;
+    const int n0 = c.nt * BN + col0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (n0 + i < D.d) out[n0 + i] = v[i];
+  }
+  __device__ void row_end(const Tile&, int, Row&) const {}
+};
+
+}  // namespace d2ft_b200

@@ -1,0 +1,954 @@
+// Non-GEMM kernels of the D2FT step for sm_100a.
+#include "common.cuh"
+#include "step_kernels.cuh"
+
+namespace d2ft_b200 {
+
+namespace {
+
+constexpr float kLnEps = 1e-5f;  // model.hpp:32
+constexpr int kMaxVec = 32;      // d <= 1024: values per lane of a row
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ codes / plan
+__global__ void expand_codes_kernel(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out) {
+  const size_t n = (size_t)K * Bmax;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / Bmax), s = (int)(i % Bmax);
+    out[i] = s < B ? codes[(size_t)k * n_mb + s / mbs] : (uint8_t)3;
+  }
+}
+
+__global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count,
+                            int* g4_tiles, int* g4_count) {
+  const int l = blockIdx.x;
+  __shared__ int s1[1024], s4[1024];
+  int c1 = 0, c4 = 0;
+  const int s = threadIdx.x;
+  if (s < D.B) {
+    c1 = (D.UQ * act_cnt[s * D.L + l] + 1) / 2;
+    c4 = (D.UO * full_hcnt[s * D.L + l] + 1) / 2;
+  }
+  s1[threadIdx.x] = c1;
+  s4[threadIdx.x] = c4;
+  __syncthreads();
+  for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
+    int a1 = 0, a4 = 0;
+    if ((int)threadIdx.x >= o) {
+      a1 = s1[threadIdx.x - o];
+      a4 = s4[threadIdx.x - o];
+    }
+    __syncthreads();
+    s1[threadIdx.x] += a1;
+    s4[threadIdx.x] += a4;
+    __syncthreads();
+  }
+  const size_t cap = (size_t)D.Bmax * ((D.UQ * D.H + 1) / 2);
+  const size_t cap4 = (size_t)D.Bmax * ((D.UO * D.H + 1) / 2);
+  if (s < D.B) {
+    const int b1 = s1[s] - c1, b4 = s4[s] - c4;
+    for (int i = 0; i < c1; ++i) g1_tiles[l * cap + b1 + i] = (s << 16) | (2 * i);
+    for (int i = 0; i < c4; ++i) g4_tiles[l * cap4 + b4 + i] = (s << 16) | (2 * i);
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    g1_count[l] = s1[threadIdx.x];
+    g4_count[l] = s4[threadIdx.x];
+  }
+}
+
+// ------------------------------------------------------------------ row-tile kernels
+// One CTA = 32 tokens of one sample, 8 warps, warp per row.  Shared tile
+// [32][d+2] bf16 (odd word pitch: conflict-free transposed reads).
+
+__device__ __forceinline__ void write_transposed(const bf16* tile, int pitch, int d, int t0, int TP, bf16* outT) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (t0 + lane >= TP) return;
+  for (int m = warp; m < d; m += 8) outT[(size_t)m * TP + t0 + lane] = tile[lane * pitch + m];
+}
+
+__global__ void prep_input_kernel(Dims D, const float* x, bf16* inp, bf16* inpT) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  bf16* tile = reinterpret_cast<bf16*>(smem);
+  const int pitch = D.d + 2;
+  const int s = blockIdx.y, t0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < 32; r += 8) {
+    const int t = t0 + r;
+    for (int m = lane; m < D.d; m += 32) {
+      const float v = t < D.T ? x[((size_t)s * D.T + t) * D.d + m] : 0.f;
+      const bf16 b = __float2bfloat16_rn(v);
+      tile[r * pitch + m] = b;
+      if (t < D.T) inp[((size_t)s * D.T + t) * D.d + m] = b;
+    }
+  }
+  __syncthreads();
+  write_transposed(tile, pitch, D.d, t0, D.TP, inpT + (size_t)s * D.d * D.TP);
+}
+
+__global__ void ln_fwd_kernel(Dims D, const float* x, bf16* xn, bf16* xnT, float* stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  bf16* tile = reinterpret_cast<bf16*>(smem);
+  const int pitch = D.d + 2;
+  const int s = blockIdx.y, t0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = D.d / 32;
+  for (int r = warp; r < 32; r += 8) {
+    const int t = t0 + r;
+    if (t >= D.T) {
+      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = __float2bfloat16_rn(0.f);
+      continue;
+    }
+    const float* row = x + ((size_t)s * D.T + t) * D.d;
+    float v[kMaxVec];
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        v[j] = row[lane + 32 * j];
+        sum += v[j];
+      }
+    const float mean = warp_sum(sum) / D.d;  // linalg.cpp:136-139, two-pass
+    float sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        const float dv = v[j] - mean;
+        sq += dv * dv;
+      }
+    const float var = warp_sum(sq) / D.d;
+    const float rstd = 1.0f / sqrtf(var + kLnEps);
+    bf16* out = xn + ((size_t)s * D.T + t) * D.d;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        const bf16 b = __float2bfloat16_rn((v[j] - mean) * rstd);
+        out[lane + 32 * j] = b;
+        tile[r * pitch + lane + 32 * j] = b;
+      }
+    if (lane == 0) {
+      stats[((size_t)s * D.T + t) * 2] = mean;
+      stats[((size_t)s * D.T + t) * 2 + 1] = rstd;
+    }
+  }
+  __syncthreads();
+  write_transposed(tile, pitch, D.d, t0, D.TP, xnT + (size_t)s * D.d * D.TP);
+}
+
+__global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
+                                   const float* dxn, float* dX, bf16* dC, bf16* dCT, float* part_cs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  bf16* tile = reinterpret_cast<bf16*>(smem);
+  const int pitch = D.d + 2;
+  float* cs = reinterpret_cast<float*>(smem + (size_t)32 * pitch * 2 + 16);  // [8][d]
+  const int s = blockIdx.y, t0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = D.d / 32;
+  const bool do_ln = l >= 0 && full_hcnt[s * D.L + l] > 0;  // model.cpp:508
+  float acc[kMaxVec];
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j) acc[j] = 0.f;
+  for (int r = warp; r < 32; r += 8) {
+    const int t = t0 + r;
+    if (t >= D.T) {
+      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = __float2bfloat16_rn(0.f);
+      continue;
+    }
+    const size_t ro = ((size_t)s * D.T + t) * D.d;
+    float v[kMaxVec];
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) v[j] = dX[ro + lane + 32 * j];
+    if (do_ln) {  // linalg.cpp:153-180
+      const float mean = stats_l[((size_t)s * D.T + t) * 2], rstd = stats_l[((size_t)s * D.T + t) * 2 + 1];
+      float y[kMaxVec], dy[kMaxVec];
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxVec; ++j)
+        if (j < nv) {
+          y[j] = (x_l[ro + lane + 32 * j] - mean) * rstd;
+          dy[j] = dxn[ro + lane + 32 * j];
+          s1 += dy[j];
+          s2 += dy[j] * y[j];
+        }
+      const float dmean = warp_sum(s1) / D.d, ddot = warp_sum(s2) / D.d;
+#pragma unroll
+      for (int j = 0; j < kMaxVec; ++j)
+        if (j < nv) v[j] += (dy[j] - dmean - y[j] * ddot) * rstd;
+#pragma unroll
+      for (int j = 0; j < kMaxVec; ++j)
+        if (j < nv) dX[ro + lane + 32 * j] = v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        const bf16 b = __float2bfloat16_rn(v[j]);
+        dC[ro + lane + 32 * j] = b;
+        tile[r * pitch + lane + 32 * j] = b;
+        acc[j] += v[j];
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j)
+    if (j < nv) cs[warp * D.d + lane + 32 * j] = acc[j];
+  __syncthreads();
+  write_transposed(tile, pitch, D.d, t0, D.TP, dCT + (size_t)s * D.d * D.TP);
+  const int ntile = (D.T + 31) / 32;
+  for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
+    float c = 0.f;
+    for (int w = 0; w < 8; ++w) c += cs[w * D.d + m];
+    part_cs[((size_t)s * ntile + blockIdx.x) * D.d + m] = c;
+  }
+}
+
+// ------------------------------------------------------------------ head
+// LN -> mean over tokens -> linear -> cross-entropy (model.cpp:342-355,
+// 400-414, 470-492); backward to dX = dL/dx_L.  One CTA per sample.
+__global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
+                            double* loss_s, float* pooled_out, float* dlog_out, float* dX) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* part = reinterpret_cast<float*>(smem);  // [8][d]
+  float* pooled = part + 8 * D.d;                // [d]
+  float* dpooled = pooled + D.d;                 // [d]
+  float* rowstat = dpooled + D.d;                // [T][2]
+  __shared__ float logits[64], dlog[64];
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = D.d / 32;
+  float acc[kMaxVec];
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j) acc[j] = 0.f;
+  for (int t = warp; t < D.T; t += 8) {
+    const float* row = xL + ((size_t)s * D.T + t) * D.d;
+    float v[kMaxVec];
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        v[j] = row[lane + 32 * j];
+        sum += v[j];
+      }
+    const float mean = warp_sum(sum) / D.d;
+    float sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) sq += (v[j] - mean) * (v[j] - mean);
+    const float rstd = 1.0f / sqrtf(warp_sum(sq) / D.d + kLnEps);
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) acc[j] += (v[j] - mean) * rstd;
+    if (lane == 0) {
+      rowstat[2 * t] = mean;
+      rowstat[2 * t + 1] = rstd;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j)
+    if (j < nv) part[warp * D.d + lane + 32 * j] = acc[j];
+  __syncthreads();
+  for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
+    float p = 0.f;
+    for (int w = 0; w < 8; ++w) p += part[w * D.d + m];
+    pooled[m] = p / D.T;  // row_mean (linalg.cpp:101-105)
+    pooled_out[(size_t)s * D.d + m] = pooled[m];
+  }
+  __syncthreads();
+  for (int c = warp; c < D.C; c += 8) {
+    float z = 0.f;
+    for (int m = lane; m < D.d; m += 32) z += pooled[m] * Wc[(size_t)m * D.C + c];
+    z = warp_sum(z);
+    if (lane == 0) logits[c] = z + bc[c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // cross_entropy, model.cpp:400-414 (fp64 reduction)
+    const int lab = labels[s];
+    double mx = logits[0];
+    for (int c = 1; c < D.C; ++c) mx = fmax(mx, (double)logits[c]);
+    double sum = 0.0;
+    for (int c = 0; c < D.C; ++c) sum += exp((double)logits[c] - mx);
+    loss_s[s] = log(sum) - ((double)logits[lab] - mx);
+    for (int c = 0; c < D.C; ++c) {
+      double p = exp((double)logits[c] - mx) / sum;
+      if (c == lab) p -= 1.0;
+      dlog[c] = (float)(p * scale);
+      dlog_out[(size_t)s * D.C + c] = dlog[c];
+    }
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
+    float z = 0.f;
+    for (int c = 0; c < D.C; ++c) z += dlog[c] * Wc[(size_t)m * D.C + c];
+    dpooled[m] = z / D.T;  // dxn_h = dpooled / T (model.cpp:489-491)
+  }
+  __syncthreads();
+  float dmean_l = 0.f;
+  for (int m = lane; m < D.d; m += 32) dmean_l += dpooled[m];
+  const float dmean = warp_sum(dmean_l) / D.d;
+  for (int t = warp; t < D.T; t += 8) {
+    const size_t ro = ((size_t)s * D.T + t) * D.d;
+    const float mean = rowstat[2 * t], rstd = rowstat[2 * t + 1];
+    float y[kMaxVec];
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) {
+        y[j] = (xL[ro + lane + 32 * j] - mean) * rstd;
+        s2 += dpooled[lane + 32 * j] * y[j];
+      }
+    const float ddot = warp_sum(s2) / D.d;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j)
+      if (j < nv) dX[ro + lane + 32 * j] = (dpooled[lane + 32 * j] - dmean - y[j] * ddot) * rstd;
+  }
+}
+
+__global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
+                                   float* dbc, double* loss) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < D.d * D.C) {
+    const int m = i / D.C, c = i % D.C;
+    float a = 0.f;
+    for (int s = 0; s < D.B; ++s) a += pooled[(size_t)s * D.d + m] * dlog[(size_t)s * D.C + c];
+    dWc[i] = a;
+  } else if (i < D.d * D.C + D.C) {
+    const int c = i - D.d * D.C;
+    float a = 0.f;
+    for (int s = 0; s < D.B; ++s) a += dlog[(size_t)s * D.C + c];
+    dbc[c] = a;
+  } else if (i == D.d * D.C + D.C) {
+    double a = 0.0;
+    for (int s = 0; s < D.B; ++s) a += loss_s[s];
+    *loss = a / D.B;
+  }
+}
+
+// ------------------------------------------------------------------ bias / embed reductions
+__global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
+                                   float* db1_l, float* db2_l) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntile = (D.T + 31) / 32;
+  if (i < D.d) {  // db2 (model.cpp:250-252): Full samples of head m/(d/H)
+    const int m = i, h = m / (D.d / D.H);
+    const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
+    float a = 0.f;
+    for (int s = 0; s < D.B; ++s)
+      if (row[s] == 1)
+        for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
+    db2_l[m] = a;
+  } else if (i < D.d + D.H * D.fs) {  // db1 (model.cpp:257)
+    const int q = i - D.d, h = q / D.fs, j = q % D.fs;
+    const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
+    float a = 0.f;
+    for (int s = 0; s < D.B; ++s)
+      if (row[s] == 1) a += part_db1[((size_t)s * D.H + h) * D.fs + j];
+    db1_l[q] = a;
+  }
+}
+
+__global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const float* part_cs, const float* dX,
+                                    float* dWeT, float* dbe, float* dpos) {
+  const size_t dd = (size_t)D.d * D.d;
+  const size_t td = (size_t)D.T * D.d;
+  const int ntile = (D.T + 31) / 32;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd + td + D.d;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (i < dd) {
+      float a = 0.f;
+      for (int k = 0; k < KS; ++k) a += part[k * dd + i];
+      dWeT[i] = a;
+    } else if (i < dd + td) {
+      const size_t q = i - dd;
+      float a = 0.f;
+      for (int s = 0; s < D.B; ++s) a += dX[(size_t)s * td + q];
+      dpos[q] = a;
+    } else {
+      const int m = (int)(i - dd - td);
+      float a = 0.f;
+      for (int s = 0; s < D.B; ++s)
+        for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
+      dbe[m] = a;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SGD / copies
+__global__ void sgd_kernel(float* p, float* v, const float* g, bf16* pbf, size_t n, long long outer, long long inner,
+                           int H, const int* full_cnt, float lr, float mom, int* err) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    if (outer > 0 && full_cnt) {
+      const long long k = ((long long)i / outer) * H + ((long long)i / inner) % H;
+      if (full_cnt[k] == 0) continue;  // trainer.cpp:264-268: untouched subnets keep p and v
+    }
+    const float gi = g[i];
+    if (!isfinite(gi)) {
+      atomicCAS(err, 0, (int)kNumeric);  // trainer.cpp:118
+      continue;
+    }
+    const float vi = mom * v[i] + gi;  // trainer.cpp:119-120
+    v[i] = vi;
+    const float pi = p[i] - lr * vi;
+    p[i] = pi;
+    if (pbf) pbf[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+template <bool kColHeads>
+__global__ void transpose_bf16_kernel(const bf16* in, bf16* out, int rows, int cols, int head_span, int H,
+                                      const int* full_cnt) {
+  __shared__ bf16 tile[32][34];
+  const int b = blockIdx.z;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  if (full_cnt) {
+    const int h = kColHeads ? c0 / head_span : r0 / head_span;
+    if (h < H && full_cnt[b * H + h] == 0) return;
+  }
+  const bf16* src = in + (size_t)b * rows * cols;
+  bf16* dst = out + (size_t)b * rows * cols;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[(size_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[(size_t)c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* in, bf16* out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// ------------------------------------------------------------------ attention (mma.sync, FA2 style)
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t ld32(const bf16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// A fragment (16 x 16) from row-major X (pitch p): rows r0.., cols k0..
+__device__ __forceinline__ void lda(uint32_t (&a)[4], const bf16* X, int p, int r0, int k0, int g, int c) {
+  a[0] = ld32(X + (size_t)(r0 + g) * p + k0 + 2 * c);
+  a[1] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 2 * c);
+  a[2] = ld32(X + (size_t)(r0 + g) * p + k0 + 8 + 2 * c);
+  a[3] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 8 + 2 * c);
+}
+// B fragment (16 x 8) from n-major Y[n][k] (pitch p)
+__device__ __forceinline__ void ldb(uint32_t& b0, uint32_t& b1, const bf16* Y, int p, int n0, int k0, int g, int c) {
+  b0 = ld32(Y + (size_t)(n0 + g) * p + k0 + 2 * c);
+  b1 = ld32(Y + (size_t)(n0 + g) * p + k0 + 8 + 2 * c);
+}
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Loads rows [0,T) of a [T][pitch_g] slice (cols off..off+DH) into row-major
+// smem [TQ][DH+8] (rows >= T zero) and optionally its transpose [DH][TQ+8].
+template <int DH>
+__device__ void load_tile(const bf16* g, int pitch_g, int off, int T, int TQ, bf16* rowm, bf16* trans) {
+  const int P = DH + 8, PT = TQ + 8;
+  for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
+    const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
+    uint32_t v = 0;
+    if (t < T) v = ld32(g + (size_t)t * pitch_g + off + f);
+    *reinterpret_cast<uint32_t*>(rowm + t * P + f) = v;
+    if (trans) {
+      const bf16* h = reinterpret_cast<const bf16*>(&v);
+      trans[f * PT + t] = h[0];
+      trans[(f + 1) * PT + t] = h[1];
+    }
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
+                                                       const bf16* Y1, bf16* OG, bf16* OGT, float* lse) {
+  const int s = blockIdx.y, a = blockIdx.x;
+  if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
+  const int h = act_heads[(s * D.L + l) * D.H + a];
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
+  bf16* Ks = reinterpret_cast<bf16*>(smem);  // [TQ][P]
+  bf16* Vt = Ks + TQ * P;                    // [DH][PT]
+  bf16* Qs = Vt + DH * PT;                   // [TQ][P]
+  const size_t sh = (size_t)s * D.H + h;
+  const bf16* y = Y1 + sh * D.T * D.PQ;
+  load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, nullptr);
+  {
+    // K row-major, V transposed only
+    for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
+      const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
+      uint32_t kv = 0, vv = 0;
+      if (t < D.T) {
+        kv = ld32(y + (size_t)t * D.PQ + DH + f);
+        vv = ld32(y + (size_t)t * D.PQ + 2 * DH + f);
+      }
+      *reinterpret_cast<uint32_t*>(Ks + t * P + f) = kv;
+      const bf16* hv = reinterpret_cast<const bf16*>(&vv);
+      Vt[f * PT + t] = hv[0];
+      Vt[(f + 1) * PT + t] = hv[1];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
+  const float sl2 = kLog2e / sqrtf((float)DH);  // 1/sqrt(dh) (model.cpp:213) in log2 units
+  for (int strip = warp; strip < TQ / 16; strip += 4) {
+    const int r0 = strip * 16;
+    uint32_t qa[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) lda(qa[ks], Qs, P, r0, ks * 16, g, c);
+    float o[DH / 8][4];
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) o[nf][0] = o[nf][1] = o[nf][2] = o[nf][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int kc = 0; kc < TQ; kc += 64) {
+      float sc[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = -INFINITY;
+        if (kc + nt * 8 < TQ) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(acc, qa[ks], b0, b1);
+          }
+          const int key = kc + nt * 8 + 2 * c;
+          sc[nt][0] = key < D.T ? acc[0] * sl2 : -INFINITY;
+          sc[nt][1] = key + 1 < D.T ? acc[1] * sl2 : -INFINITY;
+          sc[nt][2] = key < D.T ? acc[2] * sl2 : -INFINITY;
+          sc[nt][3] = key + 1 < D.T ? acc[3] * sl2 : -INFINITY;
+        }
+      }
+      float mx0 = m0, mx1 = m1;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
+        mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float cr0 = m0 == -INFINITY ? 0.f : exp2f(m0 - mx0);
+      const float cr1 = m1 == -INFINITY ? 0.f : exp2f(m1 - mx1);
+      m0 = mx0;
+      m1 = mx1;
+      l0 *= cr0;
+      l1 *= cr1;
+#pragma unroll
+      for (int nf = 0; nf < DH / 8; ++nf) {
+        o[nf][0] *= cr0;
+        o[nf][1] *= cr0;
+        o[nf][2] *= cr1;
+        o[nf][3] *= cr1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        sc[nt][0] = exp2f(sc[nt][0] - m0);
+        sc[nt][1] = exp2f(sc[nt][1] - m0);
+        sc[nt][2] = exp2f(sc[nt][2] - m1);
+        sc[nt][3] = exp2f(sc[nt][3] - m1);
+        l0 += sc[nt][0] + sc[nt][1];
+        l1 += sc[nt][2] + sc[nt][3];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (kc + j * 16 < TQ) {
+          uint32_t pa[4] = {pack2(sc[2 * j][0], sc[2 * j][1]), pack2(sc[2 * j][2], sc[2 * j][3]),
+                            pack2(sc[2 * j + 1][0], sc[2 * j + 1][1]), pack2(sc[2 * j + 1][2], sc[2 * j + 1][3])};
+#pragma unroll
+          for (int nf = 0; nf < DH / 8; ++nf) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Vt, PT, nf * 8, kc + j * 16, g, c);
+            mma16816(o[nf], pa, b0, b1);
+          }
+        }
+      }
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+    const int t0 = r0 + g, t1 = r0 + g + 8;
+    bf16* og = OG + sh * D.T * D.PO;
+    bf16* ogt = OGT + sh * D.PO * D.TP;
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) {
+      const int f = nf * 8 + 2 * c;
+      if (t0 < D.T) {
+        const float a0 = o[nf][0] * i0, a1 = o[nf][1] * i0;
+        *reinterpret_cast<uint32_t*>(og + (size_t)t0 * D.PO + f) = pack2(a0, a1);
+        ogt[(size_t)f * D.TP + t0] = __float2bfloat16_rn(a0);
+        ogt[(size_t)(f + 1) * D.TP + t0] = __float2bfloat16_rn(a1);
+      }
+      if (t1 < D.T) {
+        const float a2 = o[nf][2] * i1, a3 = o[nf][3] * i1;
+        *reinterpret_cast<uint32_t*>(og + (size_t)t1 * D.PO + f) = pack2(a2, a3);
+        ogt[(size_t)f * D.TP + t1] = __float2bfloat16_rn(a2);
+        ogt[(size_t)(f + 1) * D.TP + t1] = __float2bfloat16_rn(a3);
+      }
+    }
+    if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
+      if (t0 < D.T) lse[sh * D.T + t0] = m0 + log2f(l0);
+      if (t1 < D.T) lse[sh * D.T + t1] = m1 + log2f(l1);
+    }
+  }
+}
+
+// Backward (model.cpp:262-271): pass A over key strips -> dK, dV; pass B over
+// query strips -> dQ (scores recomputed from q, k and the saved LSE).
+template <int DH>
+__global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
+                                                       const bf16* Y1, const bf16* OG, const bf16* dO,
+                                                       const float* lse, bf16* dY1, bf16* dY1T) {
+  const int s = blockIdx.y, a = blockIdx.x;
+  if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
+  const int h = full_heads[(s * D.L + l) * D.H + a];
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
+  bf16* Qs = reinterpret_cast<bf16*>(smem);
+  bf16* Ks = Qs + TQ * P;
+  bf16* Vs = Ks + TQ * P;
+  bf16* dOs = Vs + TQ * P;
+  bf16* Qt = dOs + TQ * P;
+  bf16* Kt = Qt + DH * PT;
+  bf16* dOt = Kt + DH * PT;
+  float* Dv = reinterpret_cast<float*>(dOt + DH * PT);
+  float* L2 = Dv + TQ;
+  const size_t sh = (size_t)s * D.H + h;
+  const bf16* y = Y1 + sh * D.T * D.PQ;
+  const bf16* og = OG + sh * D.T * D.PO;
+  const bf16* dog = dO + sh * D.T * D.dh;
+  load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, Qt);
+  load_tile<DH>(y, D.PQ, DH, D.T, TQ, Ks, Kt);
+  load_tile<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs, nullptr);
+  load_tile<DH>(dog, D.dh, 0, D.T, TQ, dOs, dOt);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
+  for (int t = warp; t < TQ; t += 4) {  // D_i = rowsum(dO . O)
+    float acc = 0.f;
+    if (t < D.T)
+      for (int f = lane; f < DH; f += 32)
+        acc += __bfloat162float(dog[(size_t)t * D.dh + f]) * __bfloat162float(og[(size_t)t * D.PO + f]);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      Dv[t] = acc;
+      L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+    }
+  }
+  __syncthreads();
+  const float scale = 1.0f / sqrtf((float)DH);
+  const float sl2 = kLog2e * scale;
+  bf16* dy = dY1 + sh * D.T * D.PQ;
+  bf16* dyt = dY1T + sh * D.PQ * D.TP;
+
+  // ---- pass A: key strip j -> dK_j, dV_j
+  for (int strip = warp; strip < TQ / 16; strip += 4) {
+    const int k0 = strip * 16;
+    uint32_t ka[DH / 16][4], va[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      lda(ka[ks], Ks, P, k0, ks * 16, g, c);
+      lda(va[ks], Vs, P, k0, ks * 16, g, c);
+    }
+    float dk[DH / 8][4], dv[DH / 8][4];
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dk[nf][e] = dv[nf][e] = 0.f;
+    const bool key0 = k0 + g < D.T, key1 = k0 + g + 8 < D.T;
+    for (int qc = 0; qc < TQ; qc += 64) {
+      float pt[8][4], ds[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pt[nt][e] = ds[nt][e] = 0.f;
+        if (qc + nt * 8 < TQ) {
+          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Qs, P, qc + nt * 8, ks * 16, g, c);
+            mma16816(st, ka[ks], b0, b1);
+            ldb(b0, b1, dOs, P, qc + nt * 8, ks * 16, g, c);
+            mma16816(dp, va[ks], b0, b1);
+          }
+          const int q = qc + nt * 8 + 2 * c;
+          const float l2a = L2[q], l2b = L2[q + 1], da = Dv[q], db = Dv[q + 1];
+          pt[nt][0] = key0 ? exp2f(st[0] * sl2 - l2a) : 0.f;
+          pt[nt][1] = key0 ? exp2f(st[1] * sl2 - l2b) : 0.f;
+          pt[nt][2] = key1 ? exp2f(st[2] * sl2 - l2a) : 0.f;
+          pt[nt][3] = key1 ? exp2f(st[3] * sl2 - l2b) : 0.f;
+          ds[nt][0] = pt[nt][0] * (dp[0] - da);
+          ds[nt][1] = pt[nt][1] * (dp[1] - db);
+          ds[nt][2] = pt[nt][2] * (dp[2] - da);
+          ds[nt][3] = pt[nt][3] * (dp[3] - db);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (qc + j * 16 < TQ) {
+          uint32_t pa[4] = {pack2(pt[2 * j][0], pt[2 * j][1]), pack2(pt[2 * j][2], pt[2 * j][3]),
+                            pack2(pt[2 * j + 1][0], pt[2 * j + 1][1]), pack2(pt[2 * j + 1][2], pt[2 * j + 1][3])};
+          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
+                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
+#pragma unroll
+          for (int nf = 0; nf < DH / 8; ++nf) {
+            uint32_t b0, b1;
+            ldb(b0, b1, dOt, PT, nf * 8, qc + j * 16, g, c);
+            mma16816(dv[nf], pa, b0, b1);
+            ldb(b0, b1, Qt, PT, nf * 8, qc + j * 16, g, c);
+            mma16816(dk[nf], sa, b0, b1);
+          }
+        }
+      }
+    }
+    const int t0 = k0 + g, t1 = k0 + g + 8;
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) {
+      const int f = nf * 8 + 2 * c;
+      if (t0 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + DH + f) = pack2(dk[nf][0] * scale, dk[nf][1] * scale);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0], dv[nf][1]);
+        dyt[(size_t)(DH + f) * D.TP + t0] = __float2bfloat16_rn(dk[nf][0] * scale);
+        dyt[(size_t)(DH + f + 1) * D.TP + t0] = __float2bfloat16_rn(dk[nf][1] * scale);
+        dyt[(size_t)(2 * DH + f) * D.TP + t0] = __float2bfloat16_rn(dv[nf][0]);
+        dyt[(size_t)(2 * DH + f + 1) * D.TP + t0] = __float2bfloat16_rn(dv[nf][1]);
+      }
+      if (t1 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + DH + f) = pack2(dk[nf][2] * scale, dk[nf][3] * scale);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2], dv[nf][3]);
+        dyt[(size_t)(DH + f) * D.TP + t1] = __float2bfloat16_rn(dk[nf][2] * scale);
+        dyt[(size_t)(DH + f + 1) * D.TP + t1] = __float2bfloat16_rn(dk[nf][3] * scale);
+        dyt[(size_t)(2 * DH + f) * D.TP + t1] = __float2bfloat16_rn(dv[nf][2]);
+        dyt[(size_t)(2 * DH + f + 1) * D.TP + t1] = __float2bfloat16_rn(dv[nf][3]);
+      }
+    }
+  }
+
+  // ---- pass B: query strip i -> dQ_i
+  for (int strip = warp; strip < TQ / 16; strip += 4) {
+    const int r0 = strip * 16;
+    uint32_t qa[DH / 16][4], da_[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      lda(qa[ks], Qs, P, r0, ks * 16, g, c);
+      lda(da_[ks], dOs, P, r0, ks * 16, g, c);
+    }
+    const float l20 = L2[r0 + g], l21 = L2[r0 + g + 8], d0 = Dv[r0 + g], d1 = Dv[r0 + g + 8];
+    float dq[DH / 8][4];
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
+    for (int kc = 0; kc < TQ; kc += 64) {
+      float ds[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        ds[nt][0] = ds[nt][1] = ds[nt][2] = ds[nt][3] = 0.f;
+        if (kc + nt * 8 < TQ) {
+          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(st, qa[ks], b0, b1);
+            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(dp, da_[ks], b0, b1);
+          }
+          const int key = kc + nt * 8 + 2 * c;
+          const bool ka = key < D.T, kb = key + 1 < D.T;
+          ds[nt][0] = ka ? exp2f(st[0] * sl2 - l20) * (dp[0] - d0) : 0.f;
+          ds[nt][1] = kb ? exp2f(st[1] * sl2 - l20) * (dp[1] - d0) : 0.f;
+          ds[nt][2] = ka ? exp2f(st[2] * sl2 - l21) * (dp[2] - d1) : 0.f;
+          ds[nt][3] = kb ? exp2f(st[3] * sl2 - l21) * (dp[3] - d1) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (kc + j * 16 < TQ) {
+          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
+                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
+#pragma unroll
+          for (int nf = 0; nf < DH / 8; ++nf) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Kt, PT, nf * 8, kc + j * 16, g, c);
+            mma16816(dq[nf], sa, b0, b1);
+          }
+        }
+      }
+    }
+    const int t0 = r0 + g, t1 = r0 + g + 8;
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) {
+      const int f = nf * 8 + 2 * c;
+      if (t0 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
+        dyt[(size_t)f * D.TP + t0] = __float2bfloat16_rn(dq[nf][0] * scale);
+        dyt[(size_t)(f + 1) * D.TP + t0] = __float2bfloat16_rn(dq[nf][1] * scale);
+      }
+      if (t1 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
+        dyt[(size_t)f * D.TP + t1] = __float2bfloat16_rn(dq[nf][2] * scale);
+        dyt[(size_t)(f + 1) * D.TP + t1] = __float2bfloat16_rn(dq[nf][3] * scale);
+      }
+    }
+  }
+}
+
+size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(2 * TQ * (DH + 8) + DH * (TQ + 8)) * 2; }
+size_t attn_bwd_smem(int DH, int TQ) {
+  return (size_t)(4 * TQ * (DH + 8) + 3 * DH * (TQ + 8)) * 2 + (size_t)2 * TQ * 4;
+}
+
+int grid_for(size_t n, int threads) {
+  size_t b = (n + threads - 1) / threads;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
+                         cudaStream_t st) {
+  expand_codes_kernel<<<grid_for((size_t)K * Bmax, 256), 256, 0, st>>>(codes, K, n_mb, mbs, B, Bmax, out);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count, int* g4_tiles,
+                 int* g4_count, cudaStream_t st) {
+  int threads = 32;
+  while (threads < D.B) threads <<= 1;
+  D2FT_REQUIRE(threads <= 1024, kSize, "plan: batch above 1024 samples");
+  plan_kernel<<<D.L, threads, 0, st>>>(D, act_cnt, full_hcnt, g1_tiles, g1_count, g4_tiles, g4_count);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+static size_t tile_smem(const Dims& D) { return (size_t)32 * (D.d + 2) * 2 + 16; }
+
+void launch_prep_input(const Dims& D, const float* x, bf16* inp, bf16* inpT, cudaStream_t st) {
+  dim3 grid((D.T + 31) / 32, D.B);
+  const size_t sm = tile_smem(D);
+  D2FT_CUDA(cudaFuncSetAttribute(prep_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  prep_input_kernel<<<grid, 256, sm, st>>>(D, x, inp, inpT);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_ln_fwd(const Dims& D, const float* x, bf16* xn, bf16* xnT, float* stats, cudaStream_t st) {
+  dim3 grid((D.T + 31) / 32, D.B);
+  const size_t sm = tile_smem(D);
+  D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  ln_fwd_kernel<<<grid, 256, sm, st>>>(D, x, xn, xnT, stats);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
+                        const float* dxn, float* dX, bf16* dC, bf16* dCT, float* part_cs, cudaStream_t st) {
+  dim3 grid((D.T + 31) / 32, D.B);
+  const size_t sm = tile_smem(D) + (size_t)8 * D.d * 4;
+  D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  ln_bwd_prep_kernel<<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const bf16* Y1, bf16* OG,
+                     bf16* OGT, float* lse, cudaStream_t st) {
+  dim3 grid(D.H, D.B);
+  if (D.dh == 64) {
+    const size_t sm = attn_fwd_smem(64, D.TQ) + (size_t)D.TQ * 72 * 2;
+    D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_fwd_kernel<64><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+  } else if (D.dh == 32) {
+    const size_t sm = attn_fwd_smem(32, D.TQ) + (size_t)D.TQ * 40 * 2;
+    D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_fwd_kernel<32><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+  } else {
+    throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
+  }
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const bf16* Y1, const bf16* OG,
+                     const bf16* dO, const float* lse, bf16* dY1, bf16* dY1T, cudaStream_t st) {
+  dim3 grid(D.H, D.B);
+  if (D.dh == 64) {
+    const size_t sm = attn_bwd_smem(64, D.TQ);
+    D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_bwd_kernel<64><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+  } else if (D.dh == 32) {
+    const size_t sm = attn_bwd_smem(32, D.TQ);
+    D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_bwd_kernel<32><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+  } else {
+    throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
+  }
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
+                 double* loss_s, float* pooled, float* dlog, float* dX, cudaStream_t st) {
+  D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
+  const size_t sm = (size_t)(10 * D.d + 2 * D.T) * 4;
+  D2FT_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  head_kernel<<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
+                        float* dbc, double* loss, cudaStream_t st) {
+  const int n = D.d * D.C + D.C + 1;
+  head_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, loss_s, pooled, dlog, dWc, dbc, loss);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
+                        float* db1_l, float* db2_l, cudaStream_t st) {
+  const int n = D.d + D.H * D.fs;
+  bias_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
+                         float* dbe, float* dpos, cudaStream_t st) {
+  const size_t n = (size_t)D.d * D.d + (size_t)D.T * D.d + D.d;
+  embed_reduce_kernel<<<grid_for(n, 256), 256, 0, st>>>(D, KS, part, part_cs, dX, dWeT, dbe, dpos);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_sgd(float* p, float* v, const float* g, bf16* pbf, size_t n, long long outer, long long inner, int H,
+                const int* full_cnt, float lr, float mom, int* err, cudaStream_t st) {
+  if (!n) return;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, v, g, pbf, n, outer, inner, H, full_cnt, lr, mom, err);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_transpose_bf16(const bf16* in, bf16* out, int batches, int rows, int cols, int head_rows, int H,
+                           const int* full_cnt, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
+  transpose_bf16_kernel<false><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_rows, H, full_cnt);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_transpose_bf16_colheads(const bf16* in, bf16* out, int batches, int rows, int cols, int head_cols, int H,
+                                    const int* full_cnt, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
+  transpose_bf16_kernel<true><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_cols, H, full_cnt);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_f32_to_bf16(const float* in, bf16* out, size_t n, cudaStream_t st) {
+  f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
+  D2FT_CUDA(cudaGetLastError());
+}
+
+}  // namespace d2ft_b200

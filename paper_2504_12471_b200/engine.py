@@ -1,0 +1,259 @@
+"""Host mirror of the reference model/trainer interface for the D2FT step.
+
+Names follow the reference: ModelConfig (model.hpp:43-57), partition_model
+(model.cpp:140-156), SubnetModel.forward_backward (model.cpp:416-520),
+make_synthetic_dataset (trainer.cpp:83-111), and `d2ft_step`, the batch body
+of train() for the D2FT policy (trainer.cpp:214-292).  All compute runs in the
+sm_100a kernels behind include/d2ft_b200_engine.h; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import Error, check, f64, i32, lib, ptr, u8
+from .scheduler import Capacities, CostModel, ScheduleTable, ScoreTable
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("num_blocks", C.c_int), ("heads_per_block", C.c_int), ("model_dim", C.c_int),
+                ("ffn_hidden", C.c_int), ("seq_len", C.c_int), ("num_classes", C.c_int), ("seed", C.c_uint64)]
+
+
+@dataclass
+class ModelConfig:
+    """model.hpp:43-57 (defaults as the reference)."""
+    num_blocks: int = 2
+    heads_per_block: int = 2
+    model_dim: int = 16
+    ffn_hidden: int = 32
+    seq_len: int = 8
+    num_classes: int = 4
+    seed: int = 1
+
+    def head_dim(self) -> int:
+        return self.model_dim // self.heads_per_block
+
+    def ffn_slice_dim(self) -> int:
+        return self.ffn_hidden // self.heads_per_block
+
+    def subnet_count(self) -> int:
+        return self.num_blocks * self.heads_per_block + 2
+
+    def scheduled_subnet_count(self) -> int:
+        return self.num_blocks * self.heads_per_block
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.num_blocks, self.heads_per_block, self.model_dim, self.ffn_hidden, self.seq_len,
+                    self.num_classes, self.seed)
+
+
+# presets of BASELINE.json
+TINY = ModelConfig(2, 4, 128, 512, 64, 4, 1)
+VIT_B16 = ModelConfig(12, 12, 768, 3072, 197, 8, 1)
+VIT_L16 = ModelConfig(24, 16, 1024, 4096, 197, 8, 1)
+
+
+def param_count(cfg: ModelConfig) -> int:
+    d, H, dh, fs = cfg.model_dim, cfg.heads_per_block, cfg.head_dim(), cfg.ffn_slice_dim()
+    block = 3 * d * dh + dh * d + d * fs + fs + fs * d + d // H
+    return d * d + d + cfg.seq_len * d + cfg.num_blocks * H * block + d * cfg.num_classes + cfg.num_classes
+
+
+def subnet_slices(cfg: ModelConfig):
+    """[(start, stop)] of embed, the L*H block subnets, head in the canonical flat vector."""
+    d, H, dh, fs = cfg.model_dim, cfg.heads_per_block, cfg.head_dim(), cfg.ffn_slice_dim()
+    e = d * d + d + cfg.seq_len * d
+    b = 3 * d * dh + dh * d + d * fs + fs + fs * d + d // H
+    out = [(0, e)] + [(e + k * b, e + (k + 1) * b) for k in range(cfg.num_blocks * H)]
+    out.append((e + cfg.num_blocks * H * b, e + cfg.num_blocks * H * b + d * cfg.num_classes + cfg.num_classes))
+    return out
+
+
+def partition_model(cfg: ModelConfig) -> np.ndarray:
+    """Canonical fp64 initial parameters (model.cpp:140-156), bit-identical to the reference."""
+    out = np.empty(param_count(cfg), np.float64)
+    c = cfg._c()
+    check(lib().d2ft_partition_model(C.byref(c), ptr(out)))
+    return out
+
+
+def make_synthetic_dataset(num_samples, num_classes, token_dim, seq_len, noise_level=0.5, seed=7):
+    """trainer.cpp:83-111; samples as fp32 [n][T][d], labels int32."""
+    x = np.empty((num_samples, seq_len, token_dim), np.float32)
+    y = np.empty(num_samples, np.int32)
+    check(lib().d2ft_make_synthetic_dataset(C.c_int(num_samples), C.c_int(num_classes), C.c_int(token_dim),
+                                            C.c_int(seq_len), C.c_double(noise_level), C.c_uint64(seed), ptr(x),
+                                            ptr(y)))
+    return x, y
+
+
+class SubnetModel:
+    """Device-resident subnet model + optimizer state on one B200."""
+
+    def __init__(self, config: ModelConfig, max_batch: int, params: np.ndarray | None = None):
+        self.config = config
+        self.max_batch = max_batch
+        self._h = C.c_void_p()
+        c = config._c()
+        L = lib()
+        L.d2ft_engine_param_count.restype = C.c_int64
+        L.d2ft_engine_stream.restype = C.c_void_p
+        check(L.d2ft_engine_create(C.byref(c), C.c_int(max_batch), C.byref(self._h)))
+        self.n = int(L.d2ft_engine_param_count(self._h))
+        self.set_params(partition_model(config) if params is None else params)
+
+    def close(self):
+        if self._h:
+            lib().d2ft_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def scheduled_count(self) -> int:
+        return self.config.scheduled_subnet_count()
+
+    def parameter_count(self) -> int:
+        return self.n
+
+    def set_params(self, flat) -> None:
+        a = f64(flat)
+        if a.size != self.n:
+            raise Error(3, f"set_params: expected {self.n} values, got {a.size}")
+        check(lib().d2ft_engine_set_params(self._h, ptr(a)))
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        check(lib().d2ft_engine_get_params(self._h, ptr(out)))
+        return out
+
+    def velocity(self) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        check(lib().d2ft_engine_get_velocity(self._h, ptr(out)))
+        return out
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        check(lib().d2ft_engine_get_grads(self._h, ptr(out)))
+        return out
+
+    def forward_backward(self, inputs, labels, schedule_column):
+        """model.cpp:416-520: returns (loss, grads_flat, engaged).  Gradients of
+        subnets that are not engaged are zeroed here, mirroring the reference's
+        disengaged optionals."""
+        x = np.ascontiguousarray(inputs, np.float32)
+        y = i32(labels)
+        col = u8(schedule_column)
+        if col.size != self.scheduled_count():
+            raise Error(2, "schedule column must have one operation per scheduled subnet")
+        loss = C.c_double()
+        check(lib().d2ft_engine_forward_backward(self._h, ptr(x), ptr(y), C.c_int(len(y)), ptr(col), C.byref(loss)))
+        g = self.grads()
+        engaged = np.zeros(self.scheduled_count() + 2, np.uint8)
+        engaged[0] = engaged[-1] = 1
+        engaged[1:-1] = (col == 1)
+        for si, (a, b) in enumerate(subnet_slices(self.config)):
+            if not engaged[si]:
+                g[a:b] = 0.0
+        return loss.value, g, engaged
+
+    def step_codes(self, samples, labels, codes, mbs=1, lr=0.05, momentum=0.9) -> float:
+        """Trainer batch with an explicit K x n_mb schedule table."""
+        x = np.ascontiguousarray(samples, np.float32)
+        y = i32(labels)
+        c = u8(codes.codes if isinstance(codes, ScheduleTable) else codes)
+        n_mb = c.shape[1]
+        loss = C.c_double()
+        check(lib().d2ft_engine_step_codes(self._h, ptr(x), ptr(y), ptr(c), C.c_int(n_mb), C.c_int(mbs),
+                                           C.c_double(lr), C.c_double(momentum), C.byref(loss)))
+        return loss.value
+
+    def d2ft_step(self, samples, labels, scores: ScoreTable, cost_model: CostModel, capacities: Capacities,
+                  mbs=1, lr=0.05, momentum=0.9):
+        """One D2FT batch (trainer.cpp:214-292): GPU knapsack schedule from the
+        batch's score slice, forward/backward of the active heads, SGD.
+        Returns (batch_loss, ScheduleTable)."""
+        K, n_mb = scores.subnets, scores.micro_batches
+        if K != self.scheduled_count():
+            raise Error(2, "knapsack_schedule: capacities device count mismatch")
+        scores.validate()
+        capacities.validate()
+        cost_model.validate()
+        cf, cb = cost_model.row_arrays(K)
+        x = np.ascontiguousarray(samples, np.float32)
+        y = i32(labels)
+        codes = np.zeros((K, n_mb), np.uint8)
+        loss = C.c_double()
+        check(lib().d2ft_engine_step(self._h, ptr(x), ptr(y), ptr(scores.backward), ptr(scores.forward), ptr(cf),
+                                     ptr(cb), ptr(i32(capacities.full)), ptr(i32(capacities.fwd)), C.c_int(n_mb),
+                                     C.c_int(mbs), C.c_double(lr), C.c_double(momentum), C.byref(loss), ptr(codes)))
+        return loss.value, ScheduleTable(K, n_mb, codes)
+
+    # -- bench path -------------------------------------------------------
+    def stage(self, samples, labels, scores: ScoreTable, cost_model: CostModel, capacities: Capacities, mbs=1):
+        K, n_mb = scores.subnets, scores.micro_batches
+        cf, cb = cost_model.row_arrays(K)
+        x = np.ascontiguousarray(samples, np.float32)
+        check(lib().d2ft_engine_stage_device(self._h, ptr(x), ptr(i32(labels)), ptr(scores.backward),
+                                             ptr(scores.forward), ptr(cf), ptr(cb), ptr(i32(capacities.full)),
+                                             ptr(i32(capacities.fwd)), C.c_int(n_mb), C.c_int(mbs)))
+        self._staged = (n_mb, mbs)
+
+    def step_resident(self, lr=0.05, momentum=0.9):
+        n_mb, mbs = self._staged
+        check(lib().d2ft_engine_step_resident(self._h, C.c_int(n_mb), C.c_int(mbs), C.c_double(lr),
+                                              C.c_double(momentum)))
+
+    def sync(self) -> float:
+        loss = C.c_double()
+        check(lib().d2ft_engine_sync(self._h, C.byref(loss)))
+        return loss.value
+
+    def stream(self) -> int:
+        return lib().d2ft_engine_stream(self._h)
+
+    def set_profiling(self, on: bool):
+        check(lib().d2ft_engine_set_profiling(self._h, C.c_int(1 if on else 0)))
+
+    PHASES = ("sched", "embed", "ln", "G1", "attn_fwd", "G3", "head", "G4", "attn_bwd", "G5", "G7", "G8", "bias",
+              "ln_bwd", "embed_wgrad", "sgd")
+
+    def phase_ms(self):
+        out = np.zeros(len(self.PHASES))
+        steps = C.c_int()
+        check(lib().d2ft_engine_phase_ms(self._h, ptr(out), C.c_int(len(out)), C.byref(steps)))
+        n = max(1, steps.value)
+        return {k: float(v) / n for k, v in zip(self.PHASES, out)}
+
+
+def smoke_step() -> None:
+    """__graft_entry__.smoke(): one tiny D2FT step on cuda:0 vs the fp64 oracle."""
+    from oracle import lib as O
+    from oracle import model_oracle as MO
+    cfg = ModelConfig(2, 4, 128, 256, 64, 4, 1)
+    B = 8
+    x, y = make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    K = cfg.scheduled_subnet_count()
+    b, f = O.bench_scores(K, B, 3)
+    caps = Capacities([(2 * B // 5) * 5] * K, [(2 * B // 5) * 2] * K)
+    m = SubnetModel(cfg, B)
+    p0 = m.params()
+    loss, table = m.d2ft_step(x, y, ScoreTable(K, B, f, b), CostModel(), caps, 1, 0.05, 0.9)
+    ref_codes = O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd)
+    assert np.array_equal(table.codes, ref_codes), "smoke: GPU schedule differs from the oracle"
+    oc = MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
+                   cfg.num_classes)
+    pr = p0.copy()
+    v = np.zeros_like(pr)
+    ref_loss, _ = MO.train_batch(oc, pr, v, x.astype(np.float64), y, ref_codes, 1, 0.05, 0.9)
+    assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss), (loss, ref_loss)
+    dp, dr = m.params() - p0, pr - p0
+    rel = np.max(np.abs(dp - dr)) / np.max(np.abs(dr))
+    assert rel <= 1e-2, rel
+    m.close()
