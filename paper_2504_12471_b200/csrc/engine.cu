@@ -4,7 +4,7 @@
 //   schedule (fused knapsack kernel) -> expand to per-sample codes -> compaction
 //   -> embed GEMM -> L x [LN, G1, attention, G3] -> head/CE
 //   -> L x [G4, attention bwd, G5, G7, G8, bias sums, LN bwd]
-//   -> embed wgrad -> SGD-momentum on touched subnets (+ bf16 operand copies)
+//   -> embed wgrad -> SGD-momentum on touched subnets (+ act_t operand copies)
 //
 // Parameters live as fp32 masters in an arena laid out for the GEMMs (see
 // DESIGN.md §3); the canonical fp64 flat vector of the reference
@@ -77,20 +77,20 @@ struct Engine {
   Seg seg[S_N];
   size_t nparam = 0;
   float *P = nullptr, *V = nullptr, *G = nullptr;
-  bf16 *W1T_bf, *W1_bf, *W2T_bf, *W2_bf, *WeT_bf;
+  act_t *W1T_bf, *W1_bf, *W2T_bf, *W2_bf, *WeT_bf;
 
   // activations
   float* x;       // [L+1][Bmax][T][d]
   float* stats;   // [L][Bmax][T][2]
-  bf16 *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
-  bf16 *Y1, *OG, *OGT;
+  act_t *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
+  act_t *Y1, *OG, *OGT;
   float* lse;     // [L][Bmax][H][T]
-  bf16 *inp, *inpT;
+  act_t *inp, *inpT;
   float* samples_dev;
   int* labels_dev;
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
-  bf16 *dC, *dCT, *dO, *dY1, *dY1T;
+  act_t *dC, *dCT, *dO, *dY1, *dY1T;
   double *loss_s, *loss;
   float *pooled, *dlog;
   // schedule / compaction
@@ -104,6 +104,7 @@ struct Engine {
   size_t sched_bits_words = 0;
   unsigned int* sched_counter;
   int* err;
+  float* gmax;  // running max |dX_L| -> gradient scale S
   int sched_max_cols = 0;
   // pinned staging
   float* h_samples = nullptr;
@@ -218,22 +219,22 @@ struct Engine {
     P = dalloc<float>(nparam, owned);
     V = dalloc<float>(nparam, owned);
     G = dalloc<float>(nparam, owned);
-    W1T_bf = dalloc<bf16>(L * H * PQ * d, owned);
-    W1_bf = dalloc<bf16>(L * H * PQ * d, owned);
-    W2T_bf = dalloc<bf16>(L * d * H * PO, owned);
-    W2_bf = dalloc<bf16>(L * d * H * PO, owned);
-    WeT_bf = dalloc<bf16>(d * d, owned);
+    W1T_bf = dalloc<act_t>(L * H * PQ * d, owned);
+    W1_bf = dalloc<act_t>(L * H * PQ * d, owned);
+    W2T_bf = dalloc<act_t>(L * d * H * PO, owned);
+    W2_bf = dalloc<act_t>(L * d * H * PO, owned);
+    WeT_bf = dalloc<act_t>(d * d, owned);
 
     x = dalloc<float>((L + 1) * Bm * T * d, owned);
     stats = dalloc<float>(L * Bm * T * 2, owned);
-    xn = dalloc<bf16>(L * Bm * T * d, owned);
-    xnT = dalloc<bf16>(L * Bm * d * TP, owned);
-    Y1 = dalloc<bf16>(L * Bm * H * T * PQ, owned);
-    OG = dalloc<bf16>(L * Bm * H * T * PO, owned);
-    OGT = dalloc<bf16>(L * Bm * H * PO * TP, owned);
+    xn = dalloc<act_t>(L * Bm * T * d, owned);
+    xnT = dalloc<act_t>(L * Bm * d * TP, owned);
+    Y1 = dalloc<act_t>(L * Bm * H * T * PQ, owned);
+    OG = dalloc<act_t>(L * Bm * H * T * PO, owned);
+    OGT = dalloc<act_t>(L * Bm * H * PO * TP, owned);
     lse = dalloc<float>(L * Bm * H * T, owned);
-    inp = dalloc<bf16>(Bm * T * d, owned);
-    inpT = dalloc<bf16>(Bm * d * TP, owned);
+    inp = dalloc<act_t>(Bm * T * d, owned);
+    inpT = dalloc<act_t>(Bm * d * TP, owned);
     samples_dev = dalloc<float>(Bm * T * d, owned);
     labels_dev = dalloc<int>(Bm, owned);
 
@@ -243,11 +244,11 @@ struct Engine {
     part_cs = dalloc<float>(Bm * ntile * d, owned);
     part_db1 = dalloc<float>(Bm * H * fs, owned);
     part_ew = dalloc<float>((size_t)KS * d * d, owned);
-    dC = dalloc<bf16>(Bm * T * d, owned);
-    dCT = dalloc<bf16>(Bm * d * TP, owned);
-    dO = dalloc<bf16>(Bm * H * T * D.dh, owned);
-    dY1 = dalloc<bf16>(Bm * H * T * PQ, owned);
-    dY1T = dalloc<bf16>(Bm * H * PQ * TP, owned);
+    dC = dalloc<act_t>(Bm * T * d, owned);
+    dCT = dalloc<act_t>(Bm * d * TP, owned);
+    dO = dalloc<act_t>(Bm * H * T * D.dh, owned);
+    dY1 = dalloc<act_t>(Bm * H * T * PQ, owned);
+    dY1T = dalloc<act_t>(Bm * H * PQ * TP, owned);
     loss_s = dalloc<double>(Bm, owned);
     loss = dalloc<double>(1, owned);
     pooled = dalloc<float>(Bm * d, owned);
@@ -286,6 +287,7 @@ struct Engine {
     g4_count = dalloc<int>(L, owned);
     sched_counter = dalloc<unsigned int>(1, owned);
     err = dalloc<int>(1, owned);
+    gmax = dalloc<float>(1, owned);
 
     D2FT_CUDA(cudaMallocHost(&h_samples, Bm * T * d * sizeof(float)));
     D2FT_CUDA(cudaMallocHost(&h_labels, Bm * sizeof(int)));
@@ -298,23 +300,23 @@ struct Engine {
   void make_maps() {
     const uint64_t L = D.L, H = D.H, d = D.d, T = D.T, Bm = D.Bmax, PQ = D.PQ, PO = D.PO, TP = D.TP;
     // A operands (box 64 rows)
-    tm_WeT = make_tmap_bf16_3d(WeT_bf, d, d, 1, d * 2, d * d * 2, 64);
-    tm_W1T = make_tmap_bf16_3d(W1T_bf, d, H * PQ, L, d * 2, H * PQ * d * 2, 64);
-    tm_W2T = make_tmap_bf16_3d(W2T_bf, H * PO, d, L, H * PO * 2, d * H * PO * 2, 64);
-    tm_W2 = make_tmap_bf16_3d(W2_bf, d, H * PO, L, d * 2, H * PO * d * 2, 64);
-    tm_W1 = make_tmap_bf16_3d(W1_bf, H * PQ, d, L, H * PQ * 2, d * H * PQ * 2, 64);
-    tm_dCT = make_tmap_bf16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
-    tm_dY1T = make_tmap_bf16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
+    tm_WeT = make_tmap_f16_3d(WeT_bf, d, d, 1, d * 2, d * d * 2, 64);
+    tm_W1T = make_tmap_f16_3d(W1T_bf, d, H * PQ, L, d * 2, H * PQ * d * 2, 64);
+    tm_W2T = make_tmap_f16_3d(W2T_bf, H * PO, d, L, H * PO * 2, d * H * PO * 2, 64);
+    tm_W2 = make_tmap_f16_3d(W2_bf, d, H * PO, L, d * 2, H * PO * d * 2, 64);
+    tm_W1 = make_tmap_f16_3d(W1_bf, H * PQ, d, L, H * PQ * 2, d * H * PQ * 2, 64);
+    tm_dCT = make_tmap_f16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
+    tm_dY1T = make_tmap_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
     // B operands, tokens as N (box BNt)
-    tm_inp = make_tmap_bf16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt);
-    tm_xn = make_tmap_bf16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt);
-    tm_OG = make_tmap_bf16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt);
-    tm_dC = make_tmap_bf16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt);
-    tm_dY1 = make_tmap_bf16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt);
+    tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt);
+    tm_xn = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt);
+    tm_OG = make_tmap_f16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt);
+    tm_dC = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt);
+    tm_dY1 = make_tmap_f16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt);
     // B operands, tokens as K
-    tm_OGT = make_tmap_bf16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 160);
-    tm_xnT = make_tmap_bf16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 256);
-    tm_inpT = make_tmap_bf16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 256);
+    tm_OGT = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 160);
+    tm_xnT = make_tmap_f16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 256);
+    tm_inpT = make_tmap_f16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 256);
   }
 
   // ---------------------------------------------------------------- params
@@ -360,9 +362,9 @@ struct Engine {
   }
 
   void refresh_bf16_all() {
-    launch_f32_to_bf16(P + seg[S_W1T].off, W1T_bf, seg[S_W1T].n, st);
-    launch_f32_to_bf16(P + seg[S_W2T].off, W2T_bf, seg[S_W2T].n, st);
-    launch_f32_to_bf16(P + seg[S_WET].off, WeT_bf, seg[S_WET].n, st);
+    launch_f32_to_act(P + seg[S_W1T].off, W1T_bf, seg[S_W1T].n, st);
+    launch_f32_to_act(P + seg[S_W2T].off, W2T_bf, seg[S_W2T].n, st);
+    launch_f32_to_act(P + seg[S_WET].off, WeT_bf, seg[S_WET].n, st);
     refresh_transposes(nullptr);
   }
   void refresh_transposes(const int* full_cnt) {
@@ -416,9 +418,9 @@ struct Engine {
       mark(PH_LN);
       launch_ln_fwd(D, x + l * xs, xn + l * xs, xnT + (size_t)l * Bm * d * D.TP, stats + (size_t)l * Bm * T * 2, st);
       mark(PH_G1);
-      bf16* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
-      bf16* OGl = OG + (size_t)l * Bm * H * T * D.PO;
-      bf16* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
+      act_t* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
+      act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
       gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
                     P + seg[S_B1].off + (size_t)l * H * D.fs, Y1l, OGl, OGTl);
@@ -429,47 +431,48 @@ struct Engine {
                     x + l * xs, x + (l + 1) * xs);
     }
     mark(PH_HEAD);
+    D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
     launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off, 1.0f / (float)D.B, loss_s, pooled,
-                dlog, dX, st);
+                dlog, dX, gmax, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
-    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, dCT, part_cs, st);
+    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, dCT, part_cs, gmax, st);
     for (int l = D.L - 1; l >= 0; --l) {
-      bf16* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
-      bf16* OGl = OG + (size_t)l * Bm * H * T * D.PO;
+      act_t* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt, Y1l, dO,
-                    dY1, dY1T, part_db1);
+                    dY1, dY1T, part_db1, (const float*)gmax);
       mark(PH_ATTN_B);
       launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, Y1l, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
                       st);
       mark(PH_G5);
       launch_gemm<G5<160>, GemmShape<160, 6>>(
-          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO},
+          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax},
           0, st);
       mark(PH_G7);
       launch_gemm<G7<256>, GemmShape<256, 4>>(
           tm_dY1T, tm_xnT,
-          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d}, 0, st);
+          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax}, 0, st);
       mark(PH_G8);
-      gemm_tokN<G8>(tm_W1, tm_dY1, D, l, lists.full_heads, lists.full_hcnt, dxn);
+      gemm_tokN<G8>(tm_W1, tm_dY1, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax);
       mark(PH_BIAS);
       launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
                          G + seg[S_B2].off + (size_t)l * d, st);
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, dCT, part_cs,
-                         st);
+                         gmax, st);
     }
     mark(PH_EMBED_W);
-    launch_gemm<EmbedW<256>, GemmShape<256, 4>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew}, 0, st);
+    launch_gemm<EmbedW<256>, GemmShape<256, 4>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
   }
 
   void run_sgd(float lr, float mom) {
     mark(PH_SGD);
     const int* fc = lists.full_cnt;
-    auto sgd = [&](int id, bf16* pbf, const int* touch) {
+    auto sgd = [&](int id, act_t* pbf, const int* touch) {
       const Seg& s = seg[id];
       launch_sgd(P + s.off, V + s.off, G + s.off, pbf, s.n, s.outer, s.inner, D.H, touch, lr, mom, err, st);
     };

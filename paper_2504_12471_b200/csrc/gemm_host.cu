@@ -31,8 +31,8 @@ EncodeFn encode_fn() {
 }
 }  // namespace
 
-CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
-                              uint64_t stride2_bytes, uint32_t box_rows) {
+CUtensorMap make_tmap_16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                            uint64_t stride2_bytes, uint32_t box_rows, bool is_bf16) {
   CUtensorMap m;
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
@@ -41,7 +41,7 @@ CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64
   D2FT_REQUIRE(stride1_bytes % 16 == 0 && stride2_bytes % 16 == 0, kInput, "tensor map strides must be 16B multiples");
   D2FT_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, kInput, "tensor map base must be 16B aligned");
   const CUresult r =
-      encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+      encode_fn()(&m, is_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   D2FT_REQUIRE(r == CUDA_SUCCESS, kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -182,17 +182,17 @@ int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int
     D2FT_CUDA(cudaMemcpy(dB.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
     if (bn == 256) {
-      using S = GemmShape<256, 4>;
+      using S = GemmShape<256, 4, 1>;
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 256);
       launch_gemm<DenseProb<256>, S>(a, b, DenseProb<256>{M, N, K, dD.p}, 0, nullptr);
     } else if (bn == 208) {
-      using S = GemmShape<208, 5>;
+      using S = GemmShape<208, 5, 1>;
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 208);
       launch_gemm<DenseProb<208>, S>(a, b, DenseProb<208>{M, N, K, dD.p}, 0, nullptr);
     } else {
-      using S = GemmShape<160, 6>;
+      using S = GemmShape<160, 6, 1>;
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 160);
       launch_gemm<DenseProb<160>, S>(a, b, DenseProb<160>{M, N, K, dD.p}, 0, nullptr);
@@ -208,7 +208,7 @@ int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, in
     Dev<float> dD((size_t)P * M * T);
     D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemcpy(dX.p, X, (size_t)P * T * K * 2, cudaMemcpyHostToDevice));
-    using S = GemmShape<208, 5>;
+    using S = GemmShape<208, 5, 1>;
     CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
     CUtensorMap b = make_tmap_bf16_3d(dX.p, K, T, P, (uint64_t)K * 2, (uint64_t)K * T * 2, 208);
     launch_gemm<PlanesProb<208>, S>(a, b, PlanesProb<208>{M, T, K, P, dD.p}, 0, nullptr);
@@ -223,7 +223,7 @@ int d2ft_test_gemm_tokenk(const uint16_t* XT, const uint16_t* YT, int M, int N, 
     Dev<float> dD((size_t)M * N);
     D2FT_CUDA(cudaMemcpy(dX.p, XT, (size_t)P * M * TP * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemcpy(dY.p, YT, (size_t)P * N * TP * 2, cudaMemcpyHostToDevice));
-    using S = GemmShape<256, 4>;
+    using S = GemmShape<256, 4, 1>;
     CUtensorMap a = make_tmap_bf16_3d(dX.p, T, M, P, (uint64_t)TP * 2, (uint64_t)TP * M * 2, 64);
     CUtensorMap b = make_tmap_bf16_3d(dY.p, T, N, P, (uint64_t)TP * 2, (uint64_t)TP * N * 2, 256);
     launch_gemm<TokenKProb<256>, S>(a, b, TokenKProb<256>{M, N, T, P, dD.p}, 0, nullptr);
@@ -240,7 +240,7 @@ int d2ft_test_gemm_bench(int M, int N, int K, int iters, double* ms_per) {
     Dev<float> dD((size_t)M * N);
     D2FT_CUDA(cudaMemset(dA.p, 0x3c, (size_t)M * K * 2));
     D2FT_CUDA(cudaMemset(dB.p, 0x3c, (size_t)N * K * 2));
-    using S = GemmShape<256, 4>;
+    using S = GemmShape<256, 4, 1>;
     CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
     CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 256);
     DenseProb<256> prob{M, N, K, dD.p};

@@ -38,9 +38,10 @@ struct KCoord {
   int bx, by, bz;        // B: k offset, first row, plane
 };
 
-template <int BN_, int STAGES_>
+// FMT: operand format, 0 = fp16 (the step), 1 = bf16 (self-tests)
+template <int BN_, int STAGES_, int FMT_ = 0>
 struct GemmShape {
-  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_;
+  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_m128(S::BN);
+      constexpr uint32_t idesc = ptx::idesc_f16_m128(S::BN, S::FMT);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -177,11 +178,19 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // Host side -----------------------------------------------------------------
-// 3-D bf16 tensor map: dim0 contiguous (elements), dim1 rows, dim2 planes;
+// 3-D 16-bit tensor map: dim0 contiguous (elements), dim1 rows, dim2 planes;
 // strides in bytes (multiples of 16); box = 64 x box_rows x 1, 128-byte
-// swizzle, zero fill out of bounds.
-CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
-                              uint64_t stride2_bytes, uint32_t box_rows);
+// swizzle, zero fill out of bounds.  fp16 (step operands) or bf16.
+CUtensorMap make_tmap_16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                            uint64_t stride2_bytes, uint32_t box_rows, bool bf16);
+inline CUtensorMap make_tmap_bf16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                                     uint64_t s2, uint32_t box_rows) {
+  return make_tmap_16_3d(base, d0, d1, d2, s1, s2, box_rows, true);
+}
+inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                                    uint64_t s2, uint32_t box_rows) {
+  return make_tmap_16_3d(base, d0, d1, d2, s1, s2, box_rows, false);
+}
 
 int num_sms();
 

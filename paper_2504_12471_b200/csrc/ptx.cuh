@@ -105,9 +105,11 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
-// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, M=128.
-__host__ __device__ constexpr uint32_t idesc_bf16_m128(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// Instruction descriptor: kind::f16, D=f32, both K-major, M=128; operand
+// format fmt: 0 = fp16, 1 = bf16 (A and B share it).
+__host__ __device__ constexpr uint32_t idesc_f16_m128(int n, int fmt) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t elect_one() {

@@ -1,11 +1,25 @@
 // Shared dimensions and device helpers of the D2FT step engine.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace d2ft_b200 {
 
 using bf16 = __nv_bfloat16;
+// GEMM / attention operand type of the step.  fp16 (10-bit mantissa): the same
+// tcgen05 rate as bf16, 4x finer rounding (the wq/wk gradients are
+// ill-conditioned on token-similar inputs).  Gradient operands
+// carry a per-step power-of-two scale so they stay inside the fp16 range.
+using act_t = __half;
+__device__ __forceinline__ act_t to_act(float v) { return __float2half_rn(v); }
+__device__ __forceinline__ float act_to_f(act_t v) { return __half2float(v); }
+// Power-of-two gradient scale S (max|S*dX_L| in (1/2, 1]) from the running max
+// written by the head kernel; every consumer derives the identical S.
+__device__ __forceinline__ float grad_scale(const float* gmax) {
+  const float m = *gmax;
+  return m > 0.f ? exp2f(-ceilf(log2f(m))) : 1.f;
+}
 
 // Model/step geometry (ModelConfig, model.hpp:43-57, plus the B200 layout).
 struct Dims {
@@ -26,10 +40,10 @@ __device__ __forceinline__ float gelu_grad_f(float z) {
   return 0.5f * (1.0f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * __expf(-0.5f * z * z);
 }
 
-__device__ __forceinline__ void st_bf16x8(bf16* dst, const float* v) {
-  __align__(16) __nv_bfloat162 h[4];
+__device__ __forceinline__ void st_act_x8(act_t* dst, const float* v) {
+  __align__(16) __half2 h[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
   *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
 }
 

@@ -3,9 +3,12 @@
 // (one TMA box of BN token rows, zero-filled past T), weight features are M
 // in 64-row units gathered per active head, so no tile ever straddles two
 // samples.  Weight gradients use "tokens as K" over the Full micro-batches of
-// a head.  All operands are K-major bf16; accumulation is fp32 in TMEM.
+// a head.  All operands are K-major fp16 (act_t); accumulation is fp32 in TMEM;
+// gradient operands carry the step's power-of-two scale S (step_common.cuh).
 #pragma once
 #include "gemm_sm100.cuh"
+#include <cuda_fp16.h>
+
 #include "step_common.cuh"
 
 namespace d2ft_b200 {
@@ -61,9 +64,9 @@ struct G1 {
   const int* act_heads;
   const int* act_cnt;
   const float* b1;  // block l: [H][fs]
-  bf16* Y1;         // block l: [Bmax][H][T][PQ]
-  bf16* OG;         // block l: [Bmax][H][T][PO]
-  bf16* OGT;        // block l: [Bmax][H][PO][TP]
+  act_t* Y1;         // block l: [Bmax][H][T][PQ]
+  act_t* OG;         // block l: [Bmax][H][T][PO]
+  act_t* OGT;        // block l: [Bmax][H][PO][TP]
   struct Tile {
     int nkb, s, u0, nu;
   };
@@ -99,11 +102,11 @@ struct G1 {
   __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
     if (!r.valid || col0 >= D.T) return;
     const size_t sh = (size_t)c.s * D.H + r.h;
-    bf16* y = Y1 + sh * D.T * D.PQ + r.f;
-    if (r.f < 3 * D.dh) {
+    act_t* y = Y1 + sh * D.T * D.PQ + r.f;
+    if (r.f < 3 * D.dh) {  // q, k, v: fp16 operands of the attention kernels
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (col0 + i < D.T) y[(size_t)(col0 + i) * D.PQ] = __float2bfloat16_rn(v[i]);
+        if (col0 + i < D.T) y[(size_t)(col0 + i) * D.PQ] = to_act(v[i]);
       return;
     }
     const int j = r.f - 3 * D.dh;
@@ -113,13 +116,13 @@ struct G1 {
       const float z = v[i] + r.bias;
       g[i] = gelu_f(z);
       if (col0 + i < D.T) {
-        y[(size_t)(col0 + i) * D.PQ] = __float2bfloat16_rn(z);
-        OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = __float2bfloat16_rn(g[i]);
+        y[(size_t)(col0 + i) * D.PQ] = to_act(z);
+        OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = to_act(g[i]);
       }
     }
-    bf16* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
-    if (col0 + 8 <= D.TP) st_bf16x8(gt, g);
-    if (col0 + 16 <= D.TP) st_bf16x8(gt + 8, g + 8);
+    act_t* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
+    if (col0 + 8 <= D.TP) st_act_x8(gt, g);
+    if (col0 + 16 <= D.TP) st_act_x8(gt + 8, g + 8);
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
 };
@@ -188,11 +191,12 @@ struct G4 {
   const int* count;
   const int* full_heads;
   const int* full_hcnt;
-  const bf16* Y1;  // block l
-  bf16* dO;        // [Bmax][H][T][dh]
-  bf16* dY1;       // [Bmax][H][T][PQ]
-  bf16* dY1T;      // [Bmax][H][PQ][TP]
+  const act_t* Y1;  // block l
+  act_t* dO;        // [Bmax][H][T][dh]
+  act_t* dY1;       // [Bmax][H][T][PQ]
+  act_t* dY1T;      // [Bmax][H][PQ][TP]
   float* part_db1; // [Bmax][H][fs]
+  const float* gmax;
   struct Tile {
     int nkb, s, u0, nu;
   };
@@ -229,33 +233,34 @@ struct G4 {
     if (!r.valid || col0 >= D.T) return;
     const size_t sh = (size_t)c.s * D.H + r.h;
     if (r.f < D.dh) {
-      bf16* o = dO + sh * D.T * D.dh + r.f;
+      act_t* o = dO + sh * D.T * D.dh + r.f;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (col0 + i < D.T) o[(size_t)(col0 + i) * D.dh] = __float2bfloat16_rn(v[i]);
+        if (col0 + i < D.T) o[(size_t)(col0 + i) * D.dh] = to_act(v[i]);
       return;
     }
     const int j = r.f - D.dh;
     const int fq = 3 * D.dh + j;
-    const bf16* z = Y1 + sh * D.T * D.PQ + fq;
-    bf16* dy = dY1 + sh * D.T * D.PQ + fq;
+    const act_t* z = Y1 + sh * D.T * D.PQ + fq;
+    act_t* dy = dY1 + sh * D.T * D.PQ + fq;
     float dz[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int t = col0 + i;
       dz[i] = 0.f;
       if (t < D.T) {
-        dz[i] = v[i] * gelu_grad_f(__bfloat162float(z[(size_t)t * D.PQ]));
-        dy[(size_t)t * D.PQ] = __float2bfloat16_rn(dz[i]);
+        dz[i] = v[i] * gelu_grad_f(act_to_f(z[(size_t)t * D.PQ]));
+        dy[(size_t)t * D.PQ] = to_act(dz[i]);
         r.db += dz[i];
       }
     }
-    bf16* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
-    if (col0 + 8 <= D.TP) st_bf16x8(dt, dz);
-    if (col0 + 16 <= D.TP) st_bf16x8(dt + 8, dz + 8);
+    act_t* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
+    if (col0 + 8 <= D.TP) st_act_x8(dt, dz);
+    if (col0 + 16 <= D.TP) st_act_x8(dt + 8, dz + 8);
   }
   __device__ void row_end(const Tile& c, int, Row& r) const {
-    if (r.valid && r.f >= D.dh) part_db1[((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)] = r.db;
+    if (r.valid && r.f >= D.dh)
+      part_db1[((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)] = r.db / grad_scale(gmax);
   }
 };
 
@@ -269,10 +274,13 @@ struct G5 {
   const int* full_idx;  // row k: Bmax entries
   const int* full_cnt;
   float* dW2T;  // block l: [d][H*PO]
+  const float* gmax;
   struct Tile {
     int nkb, h, mt, nt;
   };
-  using Row = NoRow;
+  struct Row {
+    float inv;
+  };
   __device__ int ntn() const { return (D.PO + BN - 1) / BN; }
   __device__ int ntiles() const { return D.H * (D.d / 128) * ntn(); }
   __device__ void tile(int t, Tile& c) const {
@@ -288,14 +296,14 @@ struct G5 {
     const int t0 = (kb % D.TB) * 64;
     return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s, t0, c.nt * BN, (l * D.Bmax + s) * D.H + c.h};
   }
-  __device__ void row_begin(const Tile&, int, Row&) const {}
-  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+  __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
     float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int f = c.nt * BN + col0 + i;
-      if (f < D.PO) out[f] = v[i];
+      if (f < D.PO) out[f] = v[i] * r.inv;
     }
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
@@ -311,10 +319,13 @@ struct G7 {
   const int* full_idx;
   const int* full_cnt;
   float* dW1T;  // block l: [H][PQ][d]
+  const float* gmax;
   struct Tile {
     int nkb, h, mt, nt;
   };
-  using Row = NoRow;
+  struct Row {
+    float inv;
+  };
   __device__ int ntm() const { return (D.PQ + 127) / 128; }
   __device__ int ntn() const { return (D.d + BN - 1) / BN; }
   __device__ int ntiles() const { return D.H * ntm() * ntn(); }
@@ -331,19 +342,21 @@ struct G7 {
     const int t0 = (kb % D.TB) * 64;
     return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s * D.H + c.h, t0, c.nt * BN, l * D.Bmax + s};
   }
-  __device__ void row_begin(const Tile&, int, Row&) const {}
-  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+  __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int f = c.mt * 128 + row;
     if (f >= D.PQ) return;
     float* out = dW1T + ((size_t)c.h * D.PQ + f) * D.d;
     const int n0 = c.nt * BN + col0;
+    const float k = r.inv;
     if (n0 + 16 <= D.d) {
 #pragma unroll
-      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(out + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 16; i += 4)
+        *reinterpret_cast<float4*>(out + n0 + i) = make_float4(v[i] * k, v[i + 1] * k, v[i + 2] * k, v[i + 3] * k);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (n0 + i < D.d) out[n0 + i] = v[i];
+        if (n0 + i < D.d) out[n0 + i] = v[i] * k;
     }
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
@@ -359,10 +372,13 @@ struct G8 {
   const int* full_heads;
   const int* full_hcnt;
   float* dxn;  // [Bmax][T][d]
+  const float* gmax;
   struct Tile {
     int nkb, s, mt;
   };
-  using Row = NoRow;
+  struct Row {
+    float inv;
+  };
   __device__ int ntiles() const { return D.B * (D.d / 128); }
   __device__ void tile(int t, Tile& c) const {
     c.s = t / (D.d / 128);
@@ -374,13 +390,13 @@ struct G8 {
     const int h = full_heads[(c.s * D.L + l) * D.H + a];
     return KCoord{h * D.PQ + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, c.s * D.H + h};
   }
-  __device__ void row_begin(const Tile&, int, Row&) const {}
-  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+  __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int t = col0 + i;
-      if (t < D.T) dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i];
+      if (t < D.T) dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i] * r.inv;
     }
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
@@ -394,10 +410,13 @@ struct EmbedW {
   Dims D;
   int KS;
   float* part;  // [KS][d][d]
+  const float* gmax;
   struct Tile {
     int nkb, ks, mt, nt, s0;
   };
-  using Row = NoRow;
+  struct Row {
+    float inv;
+  };
   __device__ int ntn() const { return (D.d + BN - 1) / BN; }
   __device__ int ntiles() const { return KS * (D.d / 128) * ntn(); }
   __device__ void tile(int t, Tile& c) const {
@@ -414,14 +433,14 @@ struct EmbedW {
     const int t0 = (kb % D.TB) * 64;
     return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s, t0, c.nt * BN, s};
   }
-  __device__ void row_begin(const Tile&, int, Row&) const {}
-  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+  __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
     float* out = part + ((size_t)c.ks * D.d + m) * D.d;
     const int n0 = c.nt * BN + col0;
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-      if (n0 + i < D.d) out[n0 + i] = v[i];
+      if (n0 + i < D.d) out[n0 + i] = v[i] * r.inv;
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
 };

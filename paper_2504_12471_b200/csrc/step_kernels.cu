@@ -63,17 +63,17 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, in
 
 // ------------------------------------------------------------------ row-tile kernels
 // One CTA = 32 tokens of one sample, 8 warps, warp per row.  Shared tile
-// [32][d+2] bf16 (odd word pitch: conflict-free transposed reads).
+// [32][d+2] act_t (odd word pitch: conflict-free transposed reads).
 
-__device__ __forceinline__ void write_transposed(const bf16* tile, int pitch, int d, int t0, int TP, bf16* outT) {
+__device__ __forceinline__ void write_transposed(const act_t* tile, int pitch, int d, int t0, int TP, act_t* outT) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (t0 + lane >= TP) return;
   for (int m = warp; m < d; m += 8) outT[(size_t)m * TP + t0 + lane] = tile[lane * pitch + m];
 }
 
-__global__ void prep_input_kernel(Dims D, const float* x, bf16* inp, bf16* inpT) {
+__global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inpT) {
   extern __shared__ __align__(16) unsigned char smem[];
-  bf16* tile = reinterpret_cast<bf16*>(smem);
+  act_t* tile = reinterpret_cast<act_t*>(smem);
   const int pitch = D.d + 2;
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -81,7 +81,7 @@ __global__ void prep_input_kernel(Dims D, const float* x, bf16* inp, bf16* inpT)
     const int t = t0 + r;
     for (int m = lane; m < D.d; m += 32) {
       const float v = t < D.T ? x[((size_t)s * D.T + t) * D.d + m] : 0.f;
-      const bf16 b = __float2bfloat16_rn(v);
+      const act_t b = to_act(v);
       tile[r * pitch + m] = b;
       if (t < D.T) inp[((size_t)s * D.T + t) * D.d + m] = b;
     }
@@ -90,9 +90,9 @@ __global__ void prep_input_kernel(Dims D, const float* x, bf16* inp, bf16* inpT)
   write_transposed(tile, pitch, D.d, t0, D.TP, inpT + (size_t)s * D.d * D.TP);
 }
 
-__global__ void ln_fwd_kernel(Dims D, const float* x, bf16* xn, bf16* xnT, float* stats) {
+__global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, float* stats) {
   extern __shared__ __align__(16) unsigned char smem[];
-  bf16* tile = reinterpret_cast<bf16*>(smem);
+  act_t* tile = reinterpret_cast<act_t*>(smem);
   const int pitch = D.d + 2;
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -100,7 +100,7 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, bf16* xn, bf16* xnT, float
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
     if (t >= D.T) {
-      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = __float2bfloat16_rn(0.f);
+      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = to_act(0.f);
       continue;
     }
     const float* row = x + ((size_t)s * D.T + t) * D.d;
@@ -122,11 +122,11 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, bf16* xn, bf16* xnT, float
       }
     const float var = warp_sum(sq) / D.d;
     const float rstd = 1.0f / sqrtf(var + kLnEps);
-    bf16* out = xn + ((size_t)s * D.T + t) * D.d;
+    act_t* out = xn + ((size_t)s * D.T + t) * D.d;
 #pragma unroll
     for (int j = 0; j < kMaxVec; ++j)
       if (j < nv) {
-        const bf16 b = __float2bfloat16_rn((v[j] - mean) * rstd);
+        const act_t b = to_act((v[j] - mean) * rstd);
         out[lane + 32 * j] = b;
         tile[r * pitch + lane + 32 * j] = b;
       }
@@ -140,9 +140,10 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, bf16* xn, bf16* xnT, float
 }
 
 __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                                   const float* dxn, float* dX, bf16* dC, bf16* dCT, float* part_cs) {
+                                   const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs,
+                                   const float* gmax) {
   extern __shared__ __align__(16) unsigned char smem[];
-  bf16* tile = reinterpret_cast<bf16*>(smem);
+  act_t* tile = reinterpret_cast<act_t*>(smem);
   const int pitch = D.d + 2;
   float* cs = reinterpret_cast<float*>(smem + (size_t)32 * pitch * 2 + 16);  // [8][d]
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
@@ -155,7 +156,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
     if (t >= D.T) {
-      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = __float2bfloat16_rn(0.f);
+      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = to_act(0.f);
       continue;
     }
     const size_t ro = ((size_t)s * D.T + t) * D.d;
@@ -183,10 +184,11 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
       for (int j = 0; j < kMaxVec; ++j)
         if (j < nv) dX[ro + lane + 32 * j] = v[j];
     }
+    const float S = grad_scale(gmax);  // fp16 gradient operands carry S
 #pragma unroll
     for (int j = 0; j < kMaxVec; ++j)
       if (j < nv) {
-        const bf16 b = __float2bfloat16_rn(v[j]);
+        const act_t b = to_act(v[j] * S);
         dC[ro + lane + 32 * j] = b;
         tile[r * pitch + lane + 32 * j] = b;
         acc[j] += v[j];
@@ -209,7 +211,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
 // LN -> mean over tokens -> linear -> cross-entropy (model.cpp:342-355,
 // 400-414, 470-492); backward to dX = dL/dx_L.  One CTA per sample.
 __global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                            double* loss_s, float* pooled_out, float* dlog_out, float* dX) {
+                            double* loss_s, float* pooled_out, float* dlog_out, float* dX, float* gmax) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* part = reinterpret_cast<float*>(smem);  // [8][d]
   float* pooled = part + 8 * D.d;                // [d]
@@ -300,9 +302,17 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
         s2 += dpooled[lane + 32 * j] * y[j];
       }
     const float ddot = warp_sum(s2) / D.d;
+    float amax = 0.f;
 #pragma unroll
     for (int j = 0; j < kMaxVec; ++j)
-      if (j < nv) dX[ro + lane + 32 * j] = (dpooled[lane + 32 * j] - dmean - y[j] * ddot) * rstd;
+      if (j < nv) {
+        const float g = (dpooled[lane + 32 * j] - dmean - y[j] * ddot) * rstd;
+        dX[ro + lane + 32 * j] = g;
+        amax = fmaxf(amax, fabsf(g));
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(gmax), __float_as_uint(amax));  // >= 0: int order
   }
 }
 
@@ -376,7 +386,7 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
 }
 
 // ------------------------------------------------------------------ SGD / copies
-__global__ void sgd_kernel(float* p, float* v, const float* g, bf16* pbf, size_t n, long long outer, long long inner,
+__global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner,
                            int H, const int* full_cnt, float lr, float mom, int* err) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     if (outer > 0 && full_cnt) {
@@ -392,22 +402,22 @@ __global__ void sgd_kernel(float* p, float* v, const float* g, bf16* pbf, size_t
     v[i] = vi;
     const float pi = p[i] - lr * vi;
     p[i] = pi;
-    if (pbf) pbf[i] = __float2bfloat16_rn(pi);
+    if (pbf) pbf[i] = to_act(pi);
   }
 }
 
 template <bool kColHeads>
-__global__ void transpose_bf16_kernel(const bf16* in, bf16* out, int rows, int cols, int head_span, int H,
+__global__ void transpose_bf16_kernel(const act_t* in, act_t* out, int rows, int cols, int head_span, int H,
                                       const int* full_cnt) {
-  __shared__ bf16 tile[32][34];
+  __shared__ act_t tile[32][34];
   const int b = blockIdx.z;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   if (full_cnt) {
     const int h = kColHeads ? c0 / head_span : r0 / head_span;
     if (h < H && full_cnt[b * H + h] == 0) return;
   }
-  const bf16* src = in + (size_t)b * rows * cols;
-  bf16* dst = out + (size_t)b * rows * cols;
+  const act_t* src = in + (size_t)b * rows * cols;
+  act_t* dst = out + (size_t)b * rows * cols;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[i][threadIdx.x] = src[(size_t)r * cols + c];
@@ -419,33 +429,36 @@ __global__ void transpose_bf16_kernel(const bf16* in, bf16* out, int rows, int c
   }
 }
 
-__global__ void f32_to_bf16_kernel(const float* in, bf16* out, size_t n) {
+__global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16_rn(in[i]);
+    out[i] = to_act(in[i]);
 }
 
 // ------------------------------------------------------------------ attention (mma.sync, FA2 style)
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t ld32(const bf16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ uint32_t ld32(const act_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
+// attention operands are fp16 (q, k, v written by G1; P, dS, scaled dO here):
+// 10-bit mantissa keeps the recomputed softmax and dS 4x closer to fp64 than act_t
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+
 // A fragment (16 x 16) from row-major X (pitch p): rows r0.., cols k0..
-__device__ __forceinline__ void lda(uint32_t (&a)[4], const bf16* X, int p, int r0, int k0, int g, int c) {
+__device__ __forceinline__ void lda(uint32_t (&a)[4], const act_t* X, int p, int r0, int k0, int g, int c) {
   a[0] = ld32(X + (size_t)(r0 + g) * p + k0 + 2 * c);
   a[1] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 2 * c);
   a[2] = ld32(X + (size_t)(r0 + g) * p + k0 + 8 + 2 * c);
   a[3] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 8 + 2 * c);
 }
 // B fragment (16 x 8) from n-major Y[n][k] (pitch p)
-__device__ __forceinline__ void ldb(uint32_t& b0, uint32_t& b1, const bf16* Y, int p, int n0, int k0, int g, int c) {
+__device__ __forceinline__ void ldb(uint32_t& b0, uint32_t& b1, const act_t* Y, int p, int n0, int k0, int g, int c) {
   b0 = ld32(Y + (size_t)(n0 + g) * p + k0 + 2 * c);
   b1 = ld32(Y + (size_t)(n0 + g) * p + k0 + 8 + 2 * c);
 }
@@ -455,7 +468,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Loads rows [0,T) of a [T][pitch_g] slice (cols off..off+DH) into row-major
 // smem [TQ][DH+8] (rows >= T zero) and optionally its transpose [DH][TQ+8].
 template <int DH>
-__device__ void load_tile(const bf16* g, int pitch_g, int off, int T, int TQ, bf16* rowm, bf16* trans) {
+__device__ void load_tile(const act_t* g, int pitch_g, int off, int T, int TQ, act_t* rowm, act_t* trans) {
   const int P = DH + 8, PT = TQ + 8;
   for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
     const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
@@ -463,7 +476,7 @@ __device__ void load_tile(const bf16* g, int pitch_g, int off, int T, int TQ, bf
     if (t < T) v = ld32(g + (size_t)t * pitch_g + off + f);
     *reinterpret_cast<uint32_t*>(rowm + t * P + f) = v;
     if (trans) {
-      const bf16* h = reinterpret_cast<const bf16*>(&v);
+      const act_t* h = reinterpret_cast<const act_t*>(&v);
       trans[f * PT + t] = h[0];
       trans[(f + 1) * PT + t] = h[1];
     }
@@ -472,17 +485,17 @@ __device__ void load_tile(const bf16* g, int pitch_g, int off, int T, int TQ, bf
 
 template <int DH>
 __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
-                                                       const bf16* Y1, bf16* OG, bf16* OGT, float* lse) {
+                                                       const act_t* Y1, act_t* OG, act_t* OGT, float* lse) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
   const int h = act_heads[(s * D.L + l) * D.H + a];
   extern __shared__ __align__(16) unsigned char smem[];
   const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
-  bf16* Ks = reinterpret_cast<bf16*>(smem);  // [TQ][P]
-  bf16* Vt = Ks + TQ * P;                    // [DH][PT]
-  bf16* Qs = Vt + DH * PT;                   // [TQ][P]
+  act_t* Ks = reinterpret_cast<act_t*>(smem);  // [TQ][P]
+  act_t* Vt = Ks + TQ * P;                    // [DH][PT]
+  act_t* Qs = Vt + DH * PT;                   // [TQ][P]
   const size_t sh = (size_t)s * D.H + h;
-  const bf16* y = Y1 + sh * D.T * D.PQ;
+  const act_t* y = Y1 + sh * D.T * D.PQ;
   load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, nullptr);
   {
     // K row-major, V transposed only
@@ -494,7 +507,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
         vv = ld32(y + (size_t)t * D.PQ + 2 * DH + f);
       }
       *reinterpret_cast<uint32_t*>(Ks + t * P + f) = kv;
-      const bf16* hv = reinterpret_cast<const bf16*>(&vv);
+      const act_t* hv = reinterpret_cast<const act_t*>(&vv);
       Vt[f * PT + t] = hv[0];
       Vt[(f + 1) * PT + t] = hv[1];
     }
@@ -583,22 +596,22 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
     const float i0 = 1.f / l0, i1 = 1.f / l1;
     const int t0 = r0 + g, t1 = r0 + g + 8;
-    bf16* og = OG + sh * D.T * D.PO;
-    bf16* ogt = OGT + sh * D.PO * D.TP;
+    act_t* og = OG + sh * D.T * D.PO;
+    act_t* ogt = OGT + sh * D.PO * D.TP;
 #pragma unroll
     for (int nf = 0; nf < DH / 8; ++nf) {
       const int f = nf * 8 + 2 * c;
       if (t0 < D.T) {
         const float a0 = o[nf][0] * i0, a1 = o[nf][1] * i0;
         *reinterpret_cast<uint32_t*>(og + (size_t)t0 * D.PO + f) = pack2(a0, a1);
-        ogt[(size_t)f * D.TP + t0] = __float2bfloat16_rn(a0);
-        ogt[(size_t)(f + 1) * D.TP + t0] = __float2bfloat16_rn(a1);
+        ogt[(size_t)f * D.TP + t0] = to_act(a0);
+        ogt[(size_t)(f + 1) * D.TP + t0] = to_act(a1);
       }
       if (t1 < D.T) {
         const float a2 = o[nf][2] * i1, a3 = o[nf][3] * i1;
         *reinterpret_cast<uint32_t*>(og + (size_t)t1 * D.PO + f) = pack2(a2, a3);
-        ogt[(size_t)f * D.TP + t1] = __float2bfloat16_rn(a2);
-        ogt[(size_t)(f + 1) * D.TP + t1] = __float2bfloat16_rn(a3);
+        ogt[(size_t)f * D.TP + t1] = to_act(a2);
+        ogt[(size_t)(f + 1) * D.TP + t1] = to_act(a3);
       }
     }
     if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
@@ -612,47 +625,159 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
 // query strips -> dQ (scores recomputed from q, k and the saved LSE).
 template <int DH>
 __global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
-                                                       const bf16* Y1, const bf16* OG, const bf16* dO,
-                                                       const float* lse, bf16* dY1, bf16* dY1T) {
+                                                       const act_t* Y1, const act_t* OG, const act_t* dO,
+                                                       const float* lse, act_t* dY1, act_t* dY1T) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
   const int h = full_heads[(s * D.L + l) * D.H + a];
   extern __shared__ __align__(16) unsigned char smem[];
   const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
-  bf16* Qs = reinterpret_cast<bf16*>(smem);
-  bf16* Ks = Qs + TQ * P;
-  bf16* Vs = Ks + TQ * P;
-  bf16* dOs = Vs + TQ * P;
-  bf16* Qt = dOs + TQ * P;
-  bf16* Kt = Qt + DH * PT;
-  bf16* dOt = Kt + DH * PT;
+  act_t* Qs = reinterpret_cast<act_t*>(smem);
+  act_t* Ks = Qs + TQ * P;
+  act_t* Vs = Ks + TQ * P;
+  act_t* dOs = Vs + TQ * P;
+  act_t* Qt = dOs + TQ * P;
+  act_t* Kt = Qt + DH * PT;
+  act_t* dOt = Kt + DH * PT;
   float* Dv = reinterpret_cast<float*>(dOt + DH * PT);
   float* L2 = Dv + TQ;
   const size_t sh = (size_t)s * D.H + h;
-  const bf16* y = Y1 + sh * D.T * D.PQ;
-  const bf16* og = OG + sh * D.T * D.PO;
-  const bf16* dog = dO + sh * D.T * D.dh;
+  const act_t* y = Y1 + sh * D.T * D.PQ;
+  const act_t* og = OG + sh * D.T * D.PO;
+  const act_t* dog = dO + sh * D.T * D.dh;
   load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, Qt);
   load_tile<DH>(y, D.PQ, DH, D.T, TQ, Ks, Kt);
   load_tile<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs, nullptr);
-  load_tile<DH>(dog, D.dh, 0, D.T, TQ, dOs, dOt);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
-  for (int t = warp; t < TQ; t += 4) {  // D_i = rowsum(dO . O)
-    float acc = 0.f;
-    if (t < D.T)
-      for (int f = lane; f < DH; f += 32)
-        acc += __bfloat162float(dog[(size_t)t * D.dh + f]) * __bfloat162float(og[(size_t)t * D.PO + f]);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      Dv[t] = acc;
-      L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+  // dO arrives in act_t (G4); rescale by a power of two alpha so max|alpha*dO| is in
+  // [1, 2) and convert exactly to fp16; outputs are unscaled by 1/alpha.
+  __shared__ float s_red[4];
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < D.T * DH; i += blockDim.x)
+    mx = fmaxf(mx, fabsf(act_to_f(dog[(size_t)(i / DH) * D.dh + i % DH])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_red[warp] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
+  const float alpha = mx > 0.f ? exp2f(-floorf(log2f(mx))) : 1.f;
+  const float ia = 1.f / alpha;
+  for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
+    const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
+    float v0 = 0.f, v1 = 0.f;
+    if (t < D.T) {
+      v0 = act_to_f(dog[(size_t)t * D.dh + f]) * alpha;
+      v1 = act_to_f(dog[(size_t)t * D.dh + f + 1]) * alpha;
+    }
+    *reinterpret_cast<uint32_t*>(dOs + t * P + f) = pack2(v0, v1);
+    reinterpret_cast<__half*>(dOt)[f * PT + t] = __float2half_rn(v0);
+    reinterpret_cast<__half*>(dOt)[(f + 1) * PT + t] = __float2half_rn(v1);
+  }
+  for (int t = threadIdx.x; t < TQ; t += blockDim.x) L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+  __syncthreads();
+  const float sl2 = kLog2e / sqrtf((float)DH);
+  const float scale = ia / sqrtf((float)DH);  // 1/sqrt(dh) and the dO unscale
+  act_t* dy = dY1 + sh * D.T * D.PQ;
+  act_t* dyt = dY1T + sh * D.PQ * D.TP;
+
+  // ---- pass B: query strip i -> D_i, dQ_i
+  for (int strip = warp; strip < TQ / 16; strip += 4) {
+    const int r0 = strip * 16;
+    uint32_t qa[DH / 16][4], da_[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      lda(qa[ks], Qs, P, r0, ks * 16, g, c);
+      lda(da_[ks], dOs, P, r0, ks * 16, g, c);
+    }
+    const float l20 = L2[r0 + g], l21 = L2[r0 + g + 8];
+    // D_i = sum_j P_ij dP_ij from the very P and dP used below (softmax_rows_backward,
+    // linalg.cpp:118-128): keeps sum_j dS_ij = 0 exactly as the reference does
+    float d0 = 0.f, d1 = 0.f;
+    for (int kc = 0; kc < TQ; kc += 64) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        if (kc + nt * 8 < TQ) {
+          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(st, qa[ks], b0, b1);
+            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(dp, da_[ks], b0, b1);
+          }
+          const int key = kc + nt * 8 + 2 * c;
+          const bool ka = key < D.T, kb = key + 1 < D.T;
+          d0 += (ka ? exp2f(st[0] * sl2 - l20) * dp[0] : 0.f) + (kb ? exp2f(st[1] * sl2 - l20) * dp[1] : 0.f);
+          d1 += (ka ? exp2f(st[2] * sl2 - l21) * dp[2] : 0.f) + (kb ? exp2f(st[3] * sl2 - l21) * dp[3] : 0.f);
+        }
+      }
+    }
+    d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+    d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+    d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
+    d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
+    if (c == 0) {
+      Dv[r0 + g] = d0;
+      Dv[r0 + g + 8] = d1;
+    }
+    float dq[DH / 8][4];
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
+    for (int kc = 0; kc < TQ; kc += 64) {
+      float ds[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        ds[nt][0] = ds[nt][1] = ds[nt][2] = ds[nt][3] = 0.f;
+        if (kc + nt * 8 < TQ) {
+          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(st, qa[ks], b0, b1);
+            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
+            mma16816(dp, da_[ks], b0, b1);
+          }
+          const int key = kc + nt * 8 + 2 * c;
+          const bool ka = key < D.T, kb = key + 1 < D.T;
+          ds[nt][0] = ka ? exp2f(st[0] * sl2 - l20) * (dp[0] - d0) : 0.f;
+          ds[nt][1] = kb ? exp2f(st[1] * sl2 - l20) * (dp[1] - d0) : 0.f;
+          ds[nt][2] = ka ? exp2f(st[2] * sl2 - l21) * (dp[2] - d1) : 0.f;
+          ds[nt][3] = kb ? exp2f(st[3] * sl2 - l21) * (dp[3] - d1) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (kc + j * 16 < TQ) {
+          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
+                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
+#pragma unroll
+          for (int nf = 0; nf < DH / 8; ++nf) {
+            uint32_t b0, b1;
+            ldb(b0, b1, Kt, PT, nf * 8, kc + j * 16, g, c);
+            mma16816(dq[nf], sa, b0, b1);
+          }
+        }
+      }
+    }
+    const int t0 = r0 + g, t1 = r0 + g + 8;
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) {
+      const int f = nf * 8 + 2 * c;
+      if (t0 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
+        dyt[(size_t)f * D.TP + t0] = to_act(dq[nf][0] * scale);
+        dyt[(size_t)(f + 1) * D.TP + t0] = to_act(dq[nf][1] * scale);
+      }
+      if (t1 < D.T) {
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
+        dyt[(size_t)f * D.TP + t1] = to_act(dq[nf][2] * scale);
+        dyt[(size_t)(f + 1) * D.TP + t1] = to_act(dq[nf][3] * scale);
+      }
     }
   }
   __syncthreads();
-  const float scale = 1.0f / sqrtf((float)DH);
-  const float sl2 = kLog2e * scale;
-  bf16* dy = dY1 + sh * D.T * D.PQ;
-  bf16* dyt = dY1T + sh * D.PQ * D.TP;
 
   // ---- pass A: key strip j -> dK_j, dV_j
   for (int strip = warp; strip < TQ / 16; strip += 4) {
@@ -721,89 +846,23 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int*
       const int f = nf * 8 + 2 * c;
       if (t0 < D.T) {
         *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + DH + f) = pack2(dk[nf][0] * scale, dk[nf][1] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0], dv[nf][1]);
-        dyt[(size_t)(DH + f) * D.TP + t0] = __float2bfloat16_rn(dk[nf][0] * scale);
-        dyt[(size_t)(DH + f + 1) * D.TP + t0] = __float2bfloat16_rn(dk[nf][1] * scale);
-        dyt[(size_t)(2 * DH + f) * D.TP + t0] = __float2bfloat16_rn(dv[nf][0]);
-        dyt[(size_t)(2 * DH + f + 1) * D.TP + t0] = __float2bfloat16_rn(dv[nf][1]);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0] * ia, dv[nf][1] * ia);
+        dyt[(size_t)(DH + f) * D.TP + t0] = to_act(dk[nf][0] * scale);
+        dyt[(size_t)(DH + f + 1) * D.TP + t0] = to_act(dk[nf][1] * scale);
+        dyt[(size_t)(2 * DH + f) * D.TP + t0] = to_act(dv[nf][0] * ia);
+        dyt[(size_t)(2 * DH + f + 1) * D.TP + t0] = to_act(dv[nf][1] * ia);
       }
       if (t1 < D.T) {
         *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + DH + f) = pack2(dk[nf][2] * scale, dk[nf][3] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2], dv[nf][3]);
-        dyt[(size_t)(DH + f) * D.TP + t1] = __float2bfloat16_rn(dk[nf][2] * scale);
-        dyt[(size_t)(DH + f + 1) * D.TP + t1] = __float2bfloat16_rn(dk[nf][3] * scale);
-        dyt[(size_t)(2 * DH + f) * D.TP + t1] = __float2bfloat16_rn(dv[nf][2]);
-        dyt[(size_t)(2 * DH + f + 1) * D.TP + t1] = __float2bfloat16_rn(dv[nf][3]);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2] * ia, dv[nf][3] * ia);
+        dyt[(size_t)(DH + f) * D.TP + t1] = to_act(dk[nf][2] * scale);
+        dyt[(size_t)(DH + f + 1) * D.TP + t1] = to_act(dk[nf][3] * scale);
+        dyt[(size_t)(2 * DH + f) * D.TP + t1] = to_act(dv[nf][2] * ia);
+        dyt[(size_t)(2 * DH + f + 1) * D.TP + t1] = to_act(dv[nf][3] * ia);
       }
     }
   }
 
-  // ---- pass B: query strip i -> dQ_i
-  for (int strip = warp; strip < TQ / 16; strip += 4) {
-    const int r0 = strip * 16;
-    uint32_t qa[DH / 16][4], da_[DH / 16][4];
-#pragma unroll
-    for (int ks = 0; ks < DH / 16; ++ks) {
-      lda(qa[ks], Qs, P, r0, ks * 16, g, c);
-      lda(da_[ks], dOs, P, r0, ks * 16, g, c);
-    }
-    const float l20 = L2[r0 + g], l21 = L2[r0 + g + 8], d0 = Dv[r0 + g], d1 = Dv[r0 + g + 8];
-    float dq[DH / 8][4];
-#pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
-    for (int kc = 0; kc < TQ; kc += 64) {
-      float ds[8][4];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        ds[nt][0] = ds[nt][1] = ds[nt][2] = ds[nt][3] = 0.f;
-        if (kc + nt * 8 < TQ) {
-          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(st, qa[ks], b0, b1);
-            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(dp, da_[ks], b0, b1);
-          }
-          const int key = kc + nt * 8 + 2 * c;
-          const bool ka = key < D.T, kb = key + 1 < D.T;
-          ds[nt][0] = ka ? exp2f(st[0] * sl2 - l20) * (dp[0] - d0) : 0.f;
-          ds[nt][1] = kb ? exp2f(st[1] * sl2 - l20) * (dp[1] - d0) : 0.f;
-          ds[nt][2] = ka ? exp2f(st[2] * sl2 - l21) * (dp[2] - d1) : 0.f;
-          ds[nt][3] = kb ? exp2f(st[3] * sl2 - l21) * (dp[3] - d1) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (kc + j * 16 < TQ) {
-          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
-                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
-#pragma unroll
-          for (int nf = 0; nf < DH / 8; ++nf) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Kt, PT, nf * 8, kc + j * 16, g, c);
-            mma16816(dq[nf], sa, b0, b1);
-          }
-        }
-      }
-    }
-    const int t0 = r0 + g, t1 = r0 + g + 8;
-#pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) {
-      const int f = nf * 8 + 2 * c;
-      if (t0 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
-        dyt[(size_t)f * D.TP + t0] = __float2bfloat16_rn(dq[nf][0] * scale);
-        dyt[(size_t)(f + 1) * D.TP + t0] = __float2bfloat16_rn(dq[nf][1] * scale);
-      }
-      if (t1 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
-        dyt[(size_t)f * D.TP + t1] = __float2bfloat16_rn(dq[nf][2] * scale);
-        dyt[(size_t)(f + 1) * D.TP + t1] = __float2bfloat16_rn(dq[nf][3] * scale);
-      }
-    }
-  }
 }
 
 size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(2 * TQ * (DH + 8) + DH * (TQ + 8)) * 2; }
@@ -836,7 +895,7 @@ void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g
 
 static size_t tile_smem(const Dims& D) { return (size_t)32 * (D.d + 2) * 2 + 16; }
 
-void launch_prep_input(const Dims& D, const float* x, bf16* inp, bf16* inpT, cudaStream_t st) {
+void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D);
   D2FT_CUDA(cudaFuncSetAttribute(prep_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -844,7 +903,7 @@ void launch_prep_input(const Dims& D, const float* x, bf16* inp, bf16* inpT, cud
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_ln_fwd(const Dims& D, const float* x, bf16* xn, bf16* xnT, float* stats, cudaStream_t st) {
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D);
   D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -853,16 +912,17 @@ void launch_ln_fwd(const Dims& D, const float* x, bf16* xn, bf16* xnT, float* st
 }
 
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, bf16* dC, bf16* dCT, float* part_cs, cudaStream_t st) {
+                        const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs, const float* gmax,
+                        cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D) + (size_t)8 * D.d * 4;
   D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  ln_bwd_prep_kernel<<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs);
+  ln_bwd_prep_kernel<<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs, gmax);
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const bf16* Y1, bf16* OG,
-                     bf16* OGT, float* lse, cudaStream_t st) {
+void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OG,
+                     act_t* OGT, float* lse, cudaStream_t st) {
   dim3 grid(D.H, D.B);
   if (D.dh == 64) {
     const size_t sm = attn_fwd_smem(64, D.TQ) + (size_t)D.TQ * 72 * 2;
@@ -878,8 +938,8 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const bf16* Y1, const bf16* OG,
-                     const bf16* dO, const float* lse, bf16* dY1, bf16* dY1T, cudaStream_t st) {
+void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1, const act_t* OG,
+                     const act_t* dO, const float* lse, act_t* dY1, act_t* dY1T, cudaStream_t st) {
   dim3 grid(D.H, D.B);
   if (D.dh == 64) {
     const size_t sm = attn_bwd_smem(64, D.TQ);
@@ -896,11 +956,11 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 }
 
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                 double* loss_s, float* pooled, float* dlog, float* dX, cudaStream_t st) {
+                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
   const size_t sm = (size_t)(10 * D.d + 2 * D.T) * 4;
   D2FT_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  head_kernel<<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX);
+  head_kernel<<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -925,28 +985,28 @@ void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* 
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_sgd(float* p, float* v, const float* g, bf16* pbf, size_t n, long long outer, long long inner, int H,
+void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner, int H,
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st) {
   if (!n) return;
   sgd_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, v, g, pbf, n, outer, inner, H, full_cnt, lr, mom, err);
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_transpose_bf16(const bf16* in, bf16* out, int batches, int rows, int cols, int head_rows, int H,
+void launch_transpose_bf16(const act_t* in, act_t* out, int batches, int rows, int cols, int head_rows, int H,
                            const int* full_cnt, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
   transpose_bf16_kernel<false><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_rows, H, full_cnt);
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_transpose_bf16_colheads(const bf16* in, bf16* out, int batches, int rows, int cols, int head_cols, int H,
+void launch_transpose_bf16_colheads(const act_t* in, act_t* out, int batches, int rows, int cols, int head_cols, int H,
                                     const int* full_cnt, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
   transpose_bf16_kernel<true><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_cols, H, full_cnt);
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_f32_to_bf16(const float* in, bf16* out, size_t n, cudaStream_t st) {
+void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
   D2FT_CUDA(cudaGetLastError());
 }

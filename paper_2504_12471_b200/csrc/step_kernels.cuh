@@ -12,41 +12,42 @@ void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, 
 // per block: G1 / G4 tile lists over (sample, 64-row unit pair)
 void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count,
                  int* g4_tiles, int* g4_count, cudaStream_t st);
-// fp32 samples [B][T][d] -> bf16 token-major + feature-major copies
-void launch_prep_input(const Dims& D, const float* x, bf16* inp, bf16* inpT, cudaStream_t st);
+// fp32 samples [B][T][d] -> act_t token-major + feature-major copies
+void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st);
 // LayerNorm (no affine, eps 1e-5) of x -> xn (token-major), xnT (feature-major), stats (mean, rstd)
-void launch_ln_fwd(const Dims& D, const float* x, bf16* xn, bf16* xnT, float* stats, cudaStream_t st);
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st);
 // attention forward / backward (one CTA per (sample, active|Full head) slot)
-void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const bf16* Y1, bf16* OG,
-                     bf16* OGT, float* lse, cudaStream_t st);
-void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const bf16* Y1, const bf16* OG,
-                     const bf16* dO, const float* lse, bf16* dY1, bf16* dY1T, cudaStream_t st);
+void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OG,
+                     act_t* OGT, float* lse, cudaStream_t st);
+void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1, const act_t* OG,
+                     const act_t* dO, const float* lse, act_t* dY1, act_t* dY1T, cudaStream_t st);
 // head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, dlogits, and dX = dL/dx_L
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                 double* loss_s, float* pooled, float* dlog, float* dX, cudaStream_t st);
+                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st);
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                         float* dbc, double* loss, cudaStream_t st);
 // dX += LN_bwd(x_l, dxn) for samples with a Full head in block l (if l >= 0), then
-// emit dC (bf16 token-major), dCT (feature-major) and per-tile column sums.
+// emit dC (act_t token-major), dCT (feature-major) and per-tile column sums.
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, bf16* dC, bf16* dCT, float* part_cs, cudaStream_t st);
+                        const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs, const float* gmax,
+                        cudaStream_t st);
 void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
                         float* db1_l, float* db2_l, cudaStream_t st);
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
                          float* dbe, float* dpos, cudaStream_t st);
 // SGD with momentum (trainer.cpp:113-134) on one tensor; elements whose
 // scheduled row k = (i/outer)*H + (i/inner)%H has full_cnt[k] == 0 are skipped
-// (outer == 0: always touched).  pbf (may be null) receives the bf16 copy.
-void launch_sgd(float* p, float* v, const float* g, bf16* pbf, size_t n, long long outer, long long inner, int H,
+// (outer == 0: always touched).  pbf (may be null) receives the act_t copy.
+void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner, int H,
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st);
-// batched bf16 transpose: out[b][c][r] = in[b][r][c]; rows r are grouped in
+// batched act_t transpose: out[b][c][r] = in[b][r][c]; rows r are grouped in
 // heads of `head_rows` (skip the tile when full_cnt[b*H + r/head_rows] == 0,
 // or never when full_cnt is null)
-void launch_transpose_bf16(const bf16* in, bf16* out, int batches, int rows, int cols, int head_rows, int H,
+void launch_transpose_bf16(const act_t* in, act_t* out, int batches, int rows, int cols, int head_rows, int H,
                            const int* full_cnt, cudaStream_t st);
 // same, with the head grouping on the column index (for W2T -> W2)
-void launch_transpose_bf16_colheads(const bf16* in, bf16* out, int batches, int rows, int cols, int head_cols, int H,
+void launch_transpose_bf16_colheads(const act_t* in, act_t* out, int batches, int rows, int cols, int head_cols, int H,
                                     const int* full_cnt, cudaStream_t st);
-void launch_f32_to_bf16(const float* in, bf16* out, size_t n, cudaStream_t st);
+void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st);
 
 }  // namespace d2ft_b200

@@ -253,7 +253,7 @@ def smoke_step() -> None:
     v = np.zeros_like(pr)
     ref_loss, _ = MO.train_batch(oc, pr, v, x.astype(np.float64), y, ref_codes, 1, 0.05, 0.9)
     assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss), (loss, ref_loss)
-    dp, dr = m.params() - p0, pr - p0
+    dp, dr = m.params() - p0.astype(np.float32).astype(np.float64), pr - p0
     rel = np.max(np.abs(dp - dr)) / np.max(np.abs(dr))
     assert rel <= 1e-2, rel
     m.close()
