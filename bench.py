@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""bench.py — D2FT ViT-B/16 fine-tuning step on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One "step" = one D2FT batch of the reference's trainer body
+(trainer.cpp:214-292): GPU knapsack schedule of the batch's score slice,
+forward of the active heads, backward of the Full heads, SGD-momentum on the
+touched subnets.  Workload (BASELINE.json configs[1]): ViT-B/16 dims
+(L12 H12 d768 ffn3072 T197, 8 classes), batch 64, micro_batch 1 (per-sample
+schedule, N = 64 items per row), budget floor(2N/5) p_f + floor(2N/5) p_o,
+cf=2, cb=3, ragged synthetic scores U[0,10) (bench_scheduler.cpp:13-27 recipe),
+weights partition_model(seed 1), data make_synthetic_dataset(noise 0.5, seed 7).
+
+value : samples/s with inputs resident in HBM, CUDA-event timed on the engine
+        stream (max over ranks).  The step's working set (weights, activations,
+        >4 GB) exceeds the 126 MB L2, so no explicit flush is needed.
+e2e   : the same metric through the C-ABI host-buffer call d2ft_engine_step
+        (H2D of samples/labels/scores from pinned memory, D2H of loss+codes,
+        host sync, every step).
+--impl reference: the unmodified reference (oracle/_ref, built from
+        /root/reference) on the host cores, a bounded sample per step.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = {"hbm_gbs": 6505.6, "bf16_tflops": 1664.7, "bf16_tflops_sustained": 1389.1}
+PEAK_SRC = "fallback"
+try:
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        PEAKS.update(json.load(f))
+        PEAK_SRC = "measured"
+except Exception:
+    pass
+
+L, H, D, FFN, T, NCLS = 12, 12, 768, 3072, 197, 8
+PQ, PO = 3 * (D // H) + FFN // H, D // H + FFN // H
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, text=True)
+        except Exception:
+            return
+        self.proc = p
+        for line in p.stdout:
+            if self._stop.is_set():
+                break
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        p = getattr(self, "proc", None)
+        if p:
+            p.terminate()
+            try:
+                p.wait(timeout=2)
+            except Exception:
+                p.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload(B):
+    """Synthetic inputs of the benchmark (product-side generators)."""
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    K = L * H
+    x, y = E.make_synthetic_dataset(B, NCLS, D, T, 0.5, 7)
+    u = np.empty(2 * K * B)
+    _lib.check(_lib.lib().d2ft_uniform_stream(C.c_uint64(1), C.c_uint64(0), C.c_int(u.size), _lib.ptr(u)))
+    u = u.reshape(K, B, 2) * 10.0
+    fwd, bwd = np.ascontiguousarray(u[:, :, 0]), np.ascontiguousarray(u[:, :, 1])
+    nb = (2 * B) // 5
+    capf = np.full(K, nb * 5, np.int32)
+    capo = np.full(K, nb * 2, np.int32)
+    return x, y, bwd, fwd, capf, capo
+
+
+def gemm_flops(codes_exp, B):
+    """Algorithmic FLOPs of the active-head GEMMs per kind."""
+    c = codes_exp[:, :B].reshape(L, H, B)
+    act = (c == 1) | (c == 2)
+    full = c == 1
+    a_l = act.sum(axis=(1, 2)).astype(np.float64)
+    f_l = full.sum(axis=(1, 2)).astype(np.float64)
+    fl = {
+        "G1": 2.0 * T * D * PQ * a_l.sum(), "G3": 2.0 * T * PO * D * a_l.sum(),
+        "G4": 2.0 * T * D * PO * f_l.sum(), "G5": 2.0 * T * D * PO * f_l.sum(),
+        "G7": 2.0 * T * PQ * D * f_l.sum(), "G8": 2.0 * T * PQ * D * f_l.sum(),
+        "embed": 2.0 * B * T * D * D, "embed_wgrad": 2.0 * B * T * D * D,
+    }
+    dh = D // H
+    fl["attn_fwd"] = 4.0 * T * T * dh * act.sum()
+    fl["attn_bwd"] = 8.0 * T * T * dh * full.sum()
+    total_alg = 0.0
+    for cell_full, cell_act in ((full.sum(), act.sum()),):
+        Fk = 2.0 * T * (4 * D * dh + 2 * T * dh + 2 * D * (FFN // H))
+        total_alg = (3 * Fk * cell_full + Fk * (cell_act - cell_full)) + 4.0 * T * D * D * B
+    return fl, total_alg
+
+
+def cpu_baseline(codes_mb, threads, steps=1, warmup=0, lr=0.05, momentum=0.9):
+    """The unmodified reference's trainer body on the host cores, bounded sample:
+    `threads` micro-batches (mbs=1) per step, each a ViT-B/16-width model
+    truncated to 2 of the 12 blocks (rows = the first 24 of the step's schedule);
+    samples/s is extrapolated x(2/12) (embed/head then counted 6x:
+    conservative for the reference by ~5%)."""
+    from oracle import lib as O
+    kind = "reference" if O.ref_available() else None
+    if kind is None:
+        return None
+    Ls = 2
+    x, y = O.ref_make_dataset(threads if threads % NCLS == 0 else NCLS * ((threads + NCLS - 1) // NCLS), NCLS, D, T,
+                              0.5, 7)
+    x, y = x[:threads], y[:threads]
+    codes = np.ascontiguousarray(codes_mb[: Ls * H, :threads])
+    m = O.RefModel(Ls, H, D, FFN, T, NCLS, 1)
+    for _ in range(warmup):
+        m.train_batch_parallel(x, y, codes, 1, lr, momentum, threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        m.train_batch_parallel(x, y, codes, 1, lr, momentum, threads)
+    dt = (time.perf_counter() - t0) / steps
+    sps = threads / (dt * (L / Ls))
+    return {"value": sps, "unit": "samples/s", "cores": threads, "kind": kind,
+            "sample": f"{threads} micro-batches (mbs=1) per step on {threads} threads through the reference "
+                      f"trainer body (forward_backward per micro-batch, ordered 1/n_mb accumulation, "
+                      f"sgd_momentum_step) of a ViT-B/16-width model truncated to {Ls}/{L} blocks, "
+                      f"{dt:.2f} s/step, extrapolated x{L // Ls}",
+            "seconds_per_step": dt}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from oracle import lib as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    B = args.batch
+    x, y, bwd, fwd, capf, capo = workload(B)
+    codes = O.ref_knapsack_schedule(bwd, fwd, 2, 3, capf, capo, threads=os.cpu_count() or 1)
+    threads = os.cpu_count() or 1
+    cb = cpu_baseline(codes, threads, steps=args.steps, warmup=min(args.warmup, 1))
+    v = cb["value"]
+    line = {"metric": "D2FT ViT-B/16 samples/s", "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3 * (L / 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": {"workload": "ViT-B/16 D2FT step, batch 64, per-sample schedule",
+                                             "global_batch": B, "seq_len": T, "parallelism": "host threads"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    rank, local, world = dist_env()
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    from paper_2504_12471_b200 import scheduler as S
+    lib = _lib.lib()
+    _lib.check(lib.d2ft_set_device(C.c_int(local)))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    B = args.batch
+    K = L * H
+    x, y, bwd, fwd, capf, capo = workload(B)
+    cfg = E.VIT_B16
+    m = E.SubnetModel(cfg, B)
+    cm = S.CostModel()
+    st = S.ScoreTable(K, B, fwd, bwd)
+    caps = S.Capacities(capf.tolist(), capo.tolist())
+    m.stage(x, y, st, cm, caps)
+    lib.d2ft_launch_count.restype = C.c_ulonglong
+    # ---- device-resident timed region (profiling events inside it)
+    m.set_profiling(True)
+    ms = C.c_double()
+    loss = C.c_double()
+    if dist:
+        dist.barrier()
+    with Clocks(local) as clk:
+        l0 = lib.d2ft_launch_count()
+        _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+                                                C.c_int(args.warmup), C.c_int(args.steps), C.byref(ms),
+                                                C.byref(loss)))
+        l1 = lib.d2ft_launch_count()
+    phases = m.phase_ms()
+    m.set_profiling(False)
+    ms_step = ms.value / args.steps
+    if dist:
+        import torch
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    launches = (l1 - l0) * args.steps // (args.steps + args.warmup) if args.steps + args.warmup else 0
+    value = world * B / (ms_step * 1e-3)
+    codes_exp = np.zeros((K, B), np.uint8)
+    _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes_exp)))
+    fl, alg_total = gemm_flops(codes_exp, B)
+    # ---- end to end through the C-ABI with pinned host buffers
+    lib.d2ft_host_alloc.restype = C.c_void_p
+    nbytes = x.nbytes
+    hx = lib.d2ft_host_alloc(C.c_size_t(nbytes))
+    px = np.frombuffer((C.c_char * nbytes).from_address(hx), np.float32).reshape(x.shape)
+    px[...] = x
+    hs = lib.d2ft_host_alloc(C.c_size_t(bwd.nbytes * 2 + y.nbytes + 4 * 4 * K))
+    buf = (C.c_char * (bwd.nbytes * 2 + y.nbytes + 16 * K)).from_address(hs)
+    pb = np.frombuffer(buf, np.float64, count=bwd.size, offset=0).reshape(bwd.shape)
+    pf = np.frombuffer(buf, np.float64, count=fwd.size, offset=bwd.nbytes).reshape(fwd.shape)
+    py = np.frombuffer(buf, np.int32, count=y.size, offset=2 * bwd.nbytes)
+    pc = np.frombuffer(buf, np.int32, count=4 * K, offset=2 * bwd.nbytes + y.nbytes).reshape(4, K)
+    pb[...] = bwd
+    pf[...] = fwd
+    py[...] = y
+    pc[0], pc[1], pc[2], pc[3] = 2, 3, capf, capo
+    ms_e2e = C.c_double()
+    if dist:
+        dist.barrier()
+    with Clocks(local) as clk2:
+        _lib.check(lib.d2ft_engine_bench_e2e(
+            m._h, _lib.ptr(px), _lib.ptr(py), _lib.ptr(pb), _lib.ptr(pf), _lib.ptr(pc[0]), _lib.ptr(pc[1]),
+            _lib.ptr(pc[2]), _lib.ptr(pc[3]), C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+            C.c_int(1), C.c_int(args.steps), C.byref(ms_e2e), C.byref(loss)))
+    e2e_step = ms_e2e.value / args.steps
+    if dist:
+        import torch
+        t = torch.tensor([e2e_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    h2d = x.nbytes + y.nbytes + 2 * bwd.nbytes + 4 * 4 * K
+    d2h = 8 + K * B
+    # ---- scheduler latency at the training shape and the 144 x 1024 sweep
+    sched = {}
+    for tag, N in (("vitb_144x64", B), ("sweep_144x1024_r1", 1024)):
+        u = np.empty(2 * K * N)
+        _lib.check(lib.d2ft_uniform_stream(C.c_uint64(1), C.c_uint64(0), C.c_int(u.size), _lib.ptr(u)))
+        u = u.reshape(K, N, 2) * 10.0
+        nb = (2 * N) // 5 if N == B else N
+        cf_, co_ = np.full(K, nb * 5, np.int32), np.full(K, nb * 2, np.int32)
+        sc = S.Scheduler(K, N, H, S.max_cols_for(2, 3, cf_, co_, N))
+        us_dev, us_e2e, _ = sc.bench(u[:, :, 1], u[:, :, 0], 2, 3, cf_, co_, warmup=3, iters=20)
+        sched[tag] = {"us_device": round(us_dev, 2), "us_e2e": round(us_e2e, 2),
+                      "in_gbs": round(2 * K * N * 8 / (us_dev * 1e-6) / 1e9, 2)}
+        sc.close()
+    # ---- roofline: dominant kernel = the G1 grouped GEMM
+    peak = PEAKS["bf16_tflops_sustained"]
+    g1_tflops = fl["G1"] / (phases["G1"] * 1e-3) / 1e12 if phases["G1"] > 0 else 0.0
+    gemm_keys = ["G1", "G3", "G4", "G5", "G7", "G8"]
+    gemm_ms = sum(phases[k] for k in gemm_keys)
+    gemm_tf = sum(fl[k] for k in gemm_keys) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    step_tf = alg_total / (ms_step * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("G1_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import lib as O
+        codes = O.ref_knapsack_schedule(bwd, fwd, 2, 3, capf, capo) if O.ref_available() else None
+        if codes is not None:
+            r = cpu_baseline(codes, os.cpu_count() or 1)
+            cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        line = {
+            "metric": "D2FT ViT-B/16 samples/s", "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic (make_synthetic_dataset noise 0.5 seed 7; scores U[0,10) make_rng(1,0))",
+            "config": {"workload": "ViT-B/16 D2FT fine-tune step, batch 64, per-sample schedule (BASELINE configs[1])",
+                       "model": "ViT-B/16 subnet transformer (L12 H12 d768 ffn3072 T197, 144 head-subnets)",
+                       "global_batch": B * world, "seq_len": T,
+                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas (head-partitioned exchange: DESIGN.md §6)",
+                       "budget": f"{(2 * B) // 5} p_f + {(2 * B) // 5} p_o of {B} per row, cf=2 cb=3",
+                       "l2": "working set > 126 MB L2 (no flush needed)"},
+            "loss": loss.value,
+            "e2e": {"value": world * B / (e2e_step * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": "G1 grouped tcgen05 GEMM ([Wq|Wk|Wv|W1] x xn, active heads)",
+                         "achieved": round(g1_tflops, 1), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(g1_tflops / peak, 4), "traffic": traffic,
+                         "peak_source": f"{PEAK_SRC} bf16 dense sustained (fp16 kind::f16 runs at the same rate)",
+                         "flops_per_launch": fl["G1"] / L, "ms_per_launch": phases["G1"] / L,
+                         "active_head_gemms": {"achieved": round(gemm_tf, 1), "frac": round(gemm_tf / peak, 4),
+                                               "ms_per_step": round(gemm_ms, 3)},
+                         "step_algorithmic": {"tflop_per_step": alg_total / 1e12, "achieved": round(step_tf, 1),
+                                              "frac": round(step_tf / peak, 4)}},
+            "phase_ms": {k: round(v, 4) for k, v in phases.items()},
+            "schedule_latency_us": sched,
+            "clocks": clk.summary(),
+            "cpu_baseline": cb,
+        }
+        print(json.dumps(line))
+    m.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

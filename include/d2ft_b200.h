@@ -38,6 +38,11 @@ extern "C" {
 #define D2FT_ERR_CUDA 7
 
 const char* d2ft_last_error(void);
+/* kernels launched by this library so far (bench.py's gpu_launches) */
+unsigned long long d2ft_launch_count(void);
+/* page-locked host buffers (full-speed H2D for the end-to-end path) */
+void* d2ft_host_alloc(size_t bytes);
+void d2ft_host_free(void* p);
 /* Library build tag and the sm arch the kernels were built for (100 = sm_100a). */
 int d2ft_build_info(int* sm_arch, int* abi_version);
 

@@ -68,6 +68,16 @@ int d2ft_engine_stage_device(d2ft_engine* e, const float* samples, const int32_t
                              const int32_t* cap_fwd, int n_mb, int mbs);
 int d2ft_engine_step_resident(d2ft_engine* e, int n_mb, int mbs, double lr, double momentum);
 int d2ft_engine_sync(d2ft_engine* e, double* loss_out);
+/* Timed loops for bench.py: device-resident steps on the staged inputs, and
+ * end-to-end host-buffer steps (H2D of samples/labels/scores + D2H of loss and
+ * codes + host sync inside every step).  CUDA events on the engine stream;
+ * ms_out = total ms over `steps`. */
+int d2ft_engine_bench_device(d2ft_engine* e, int n_mb, int mbs, double lr, double momentum, int warmup, int steps,
+                             double* ms_out, double* loss_out);
+int d2ft_engine_bench_e2e(d2ft_engine* e, const float* samples, const int32_t* labels, const double* bwd_scores,
+                          const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                          const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, int warmup,
+                          int steps, double* ms_out, double* loss_out);
 void* d2ft_engine_stream(d2ft_engine* e);
 
 /* Per-phase device time (CUDA events between phases) accumulated while
@@ -78,6 +88,10 @@ int d2ft_engine_phase_ms(d2ft_engine* e, double* ms_out, int n, int* steps);
 /* per-sample schedule codes of the last step, K x max_batch */
 int d2ft_engine_codes(d2ft_engine* e, uint8_t* codes_exp_out);
 
+/* n draws of uniform_double(make_rng(seed, stream)) (rng.hpp:24-31) */
+int d2ft_uniform_stream(uint64_t seed, uint64_t stream, int n, double* out);
+/* select the CUDA device for subsequent engine/scheduler creation on this thread */
+int d2ft_set_device(int device);
 /* partition_model (model.cpp:140-156): canonical fp64 flat initial
  * parameters, bit-identical to the reference for the same config/seed. */
 int d2ft_partition_model(const d2ft_model_config* cfg, double* out);

@@ -274,6 +274,17 @@ class RefModel:
             raise OracleError(rc, self.lib.ref_last_error().decode())
         return loss.value, grads, eng
 
+    def train_batch_parallel(self, inputs, labels, codes, mbs, lr, momentum, threads):
+        x = np.ascontiguousarray(inputs, np.float64)
+        lab = np.ascontiguousarray(labels, np.int32)
+        c = np.ascontiguousarray(codes, np.uint8)
+        loss = C.c_double()
+        rc = self.lib.ref_train_batch_parallel(C.c_void_p(self.h), _ptr(x), _ptr(lab), _I(c.shape[1]), _I(mbs),
+                                               _ptr(c), _D(lr), _D(momentum), _I(threads), C.byref(loss))
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+        return loss.value
+
     def train_batch(self, inputs, labels, codes, mbs, lr, momentum):
         x = np.ascontiguousarray(inputs, np.float64)
         lab = np.ascontiguousarray(labels, np.int32)

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <exception>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "d2ft/data.hpp"
@@ -315,6 +316,59 @@ int ref_train_batch(void* h, const double* inputs, const int32_t* labels, int n_
         if (!fb.grads[si]) continue;
         if (!accum[si]) accum[si].emplace(zeros_like(model.subnet(static_cast<int>(si))));
         accumulate(*accum[si], *fb.grads[si], inv_mb);
+      }
+    }
+    for (std::size_t si = 0; si < accum.size(); ++si) {
+      if (!accum[si]) continue;
+      sgd_momentum_step(model.subnet(static_cast<int>(si)), *accum[si], m->velocity[si], lr, momentum,
+                        model.lora_enabled());
+    }
+    *batch_loss = loss;
+  });
+}
+
+// Same batch body, with the per-micro-batch forward_backward calls (const,
+// independent) spread over `threads` host threads; accumulation and the SGD
+// step stay sequential in micro-batch order, so results are identical to
+// ref_train_batch (the harness-level parallel loop SURVEY.md §7 names).
+int ref_train_batch_parallel(void* h, const double* inputs, const int32_t* labels, int n_mb, int mbs,
+                             const uint8_t* codes, double lr, double momentum, int threads, double* batch_loss) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    SubnetModel& model = m->model;
+    const int K = model.scheduled_count();
+    ScheduleTable table(K, n_mb);
+    std::memcpy(table.codes.data(), codes, table.codes.size());
+    table.validate();
+    const ModelConfig& c = model.config();
+    std::vector<ForwardBackwardResult> res(static_cast<std::size_t>(n_mb));
+    std::vector<std::string> errs(static_cast<std::size_t>(n_mb));
+    auto work = [&](int t) {
+      for (int j = t; j < n_mb; j += threads) {
+        try {
+          std::vector<Matrix> xs;
+          fill_inputs(m, inputs + static_cast<std::size_t>(j) * mbs * c.seq_len * c.model_dim, mbs, xs);
+          std::vector<int> lab(labels + static_cast<std::size_t>(j) * mbs, labels + static_cast<std::size_t>(j + 1) * mbs);
+          res[j] = model.forward_backward(xs, lab, table.column(j));
+        } catch (const std::exception& e) {
+          errs[j] = e.what();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw input_error(e);
+    const double inv_mb = 1.0 / static_cast<double>(n_mb);
+    std::vector<std::optional<Subnet>> accum(model.subnets().size());
+    double loss = 0.0;
+    for (int j = 0; j < n_mb; ++j) {
+      loss += res[j].loss * inv_mb;
+      for (std::size_t si = 0; si < res[j].grads.size(); ++si) {
+        if (!res[j].grads[si]) continue;
+        if (!accum[si]) accum[si].emplace(zeros_like(model.subnet(static_cast<int>(si))));
+        accumulate(*accum[si], *res[j].grads[si], inv_mb);
       }
     }
     for (std::size_t si = 0; si < accum.size(); ++si) {

@@ -12,6 +12,7 @@ namespace d2ft_b200 {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+unsigned long long g_launches = 0;
 
 namespace {
 
@@ -176,6 +177,17 @@ struct d2ft_sched {
 extern "C" {
 
 const char* d2ft_last_error(void) { return g_last_error.c_str(); }
+
+unsigned long long d2ft_launch_count(void) { return g_launches; }
+
+void* d2ft_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+void d2ft_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
 
 int d2ft_build_info(int* sm_arch, int* abi_version) {
   if (sm_arch) *sm_arch = 100;

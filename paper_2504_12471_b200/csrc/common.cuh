@@ -22,6 +22,10 @@ enum Status : int {
 
 void set_error(const std::string& msg);
 
+// Count of kernels this library launched (bench.py's gpu_launches).
+extern unsigned long long g_launches;
+inline void count_launch() { ++g_launches; }
+
 struct Fail {
   int code;
   std::string msg;

@@ -125,10 +125,15 @@ struct Engine {
   double phase_ms[PH_COUNT] = {};
   int profiled_steps = 0;
 
+  std::vector<cudaEvent_t> pool;
   void mark(int ph) {
     if (!profiling) return;
-    cudaEvent_t e;
-    D2FT_CUDA(cudaEventCreate(&e));
+    if (ev.size() >= pool.size()) {
+      cudaEvent_t e;
+      D2FT_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    cudaEvent_t e = pool[ev.size()];
     D2FT_CUDA(cudaEventRecord(e, st));
     ev.push_back(e);
     ev_phase.push_back(ph);
@@ -141,7 +146,6 @@ struct Engine {
       D2FT_CUDA(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
       if (ev_phase[i - 1] < PH_COUNT) phase_ms[ev_phase[i - 1]] += ms;
     }
-    for (auto e : ev) cudaEventDestroy(e);
     ev.clear();
     ev_phase.clear();
     ++profiled_steps;
@@ -187,7 +191,7 @@ struct Engine {
   }
 
   ~Engine() {
-    for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : pool) cudaEventDestroy(e);
     if (st) cudaStreamSynchronize(st);
     for (void* p : owned) cudaFree(p);
     if (h_samples) cudaFreeHost(h_samples);
@@ -526,6 +530,29 @@ struct Engine {
     compact_and_plan();
   }
 
+  // One D2FT batch from host buffers (pinned for full-speed DMA): H2D of the
+  // samples, labels and score slice, schedule, step, D2H of loss and codes.
+  void host_step(const float* samples, const int32_t* labels, const double* bwd_scores, const double* fwd_scores,
+                 const int32_t* cf, const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb,
+                 int mbs, double lr, double momentum) {
+    const int K = D.K();
+    const int B = n_mb * mbs;
+    begin_step(B);
+    const size_t KN = (size_t)K * n_mb;
+    D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(labels_dev, labels, B * 4, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(bwd_dev, bwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(fwd_dev, fwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(cf_dev, cf, K * 4, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(cb_dev, cb, K * 4, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, st));
+    schedule_device(n_mb, mbs);
+    run_forward_backward();
+    run_sgd((float)lr, (float)momentum);
+    D2FT_CUDA(cudaMemcpyAsync(h_codes, codes_mb, KN, cudaMemcpyDeviceToHost, st));
+  }
+
   void begin_step(int B) {
     D2FT_REQUIRE(B >= 1 && B <= D.Bmax, kSize, "step: batch exceeds the engine capacity");
     D.B = B;
@@ -676,30 +703,84 @@ int d2ft_engine_step(d2ft_engine* h, const float* samples, const int32_t* labels
     Engine& E = *h->e;
     const int K = E.D.K();
     D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
-    const int B = n_mb * mbs;
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
-    validate_labels(labels, B, E.D.C);
-    E.begin_step(B);
+    validate_labels(labels, n_mb * mbs, E.D.C);
     E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
-    const size_t KN = (size_t)K * n_mb;
-    std::memcpy(E.h_samples, samples, (size_t)B * E.D.T * E.D.d * 4);
-    std::memcpy(E.h_scores, bwd_scores, KN * 8);
-    std::memcpy(E.h_scores + KN, fwd_scores, KN * 8);
-    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, E.h_samples, (size_t)B * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, B * 4, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.bwd_dev, E.h_scores, KN * 8, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.fwd_dev, E.h_scores + KN, KN * 8, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.cf_dev, cf, K * 4, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.cb_dev, cb, K * 4, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, E.st));
-    D2FT_CUDA(cudaMemcpyAsync(E.capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, E.st));
-    E.schedule_device(n_mb, mbs);
-    E.run_forward_backward();
-    E.run_sgd((float)lr, (float)momentum);
-    if (codes_out) D2FT_CUDA(cudaMemcpyAsync(E.h_codes, E.codes_mb, KN, cudaMemcpyDeviceToHost, E.st));
+    E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
-    if (codes_out) std::memcpy(codes_out, E.h_codes, KN);
+    if (codes_out) std::memcpy(codes_out, E.h_codes, (size_t)K * n_mb);
+  });
+}
+
+// bench.py's e2e leg: `steps` host-buffer steps (after `warmup`), each with its
+// H2D copies and the loss/codes D2H and a host sync, CUDA-event timed on the
+// engine stream.  ms_out = total milliseconds of the timed steps.
+int d2ft_engine_bench_e2e(d2ft_engine* h, const float* samples, const int32_t* labels, const double* bwd_scores,
+                          const double* fwd_scores, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                          const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, int warmup,
+                          int steps, double* ms_out, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    const int K = E.D.K();
+    validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
+    validate_labels(labels, n_mb * mbs, E.D.C);
+    E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+    for (int i = 0; i < warmup; ++i) {
+      E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
+      check_status(E.finish_and_check());
+    }
+    cudaEvent_t e0, e1;
+    D2FT_CUDA(cudaEventCreate(&e0));
+    D2FT_CUDA(cudaEventCreate(&e1));
+    D2FT_CUDA(cudaEventRecord(e0, E.st));
+    for (int i = 0; i < steps; ++i) {
+      E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
+      check_status(E.finish_and_check());
+    }
+    D2FT_CUDA(cudaEventRecord(e1, E.st));
+    D2FT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    D2FT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms;
+    if (loss_out) *loss_out = *E.h_loss;
+  });
+}
+
+// bench.py's device leg: `steps` device-resident steps on the staged inputs,
+// CUDA-event timed on the engine stream (inputs already in HBM).
+int d2ft_engine_bench_device(d2ft_engine* h, int n_mb, int mbs, double lr, double momentum, int warmup, int steps,
+                             double* ms_out, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    for (int i = 0; i < warmup; ++i) {
+      E.begin_step(n_mb * mbs);
+      E.schedule_device(n_mb, mbs);
+      E.run_forward_backward();
+      E.run_sgd((float)lr, (float)momentum);
+    }
+    check_status(E.finish_and_check());
+    cudaEvent_t e0, e1;
+    D2FT_CUDA(cudaEventCreate(&e0));
+    D2FT_CUDA(cudaEventCreate(&e1));
+    D2FT_CUDA(cudaEventRecord(e0, E.st));
+    for (int i = 0; i < steps; ++i) {
+      E.begin_step(n_mb * mbs);
+      E.schedule_device(n_mb, mbs);
+      E.run_forward_backward();
+      E.run_sgd((float)lr, (float)momentum);
+    }
+    D2FT_CUDA(cudaEventRecord(e1, E.st));
+    D2FT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    D2FT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms;
+    check_status(E.finish_and_check());
+    if (loss_out) *loss_out = *E.h_loss;
   });
 }
 

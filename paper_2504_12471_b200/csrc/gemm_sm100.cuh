@@ -206,6 +206,7 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int 
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid < 1) grid = 1;
   gemm_sm100_kernel<P, S><<<grid, 256, S::SMEM_BYTES, stream>>>(a, b, prob);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 

@@ -79,6 +79,19 @@ int d2ft_partition_model(const d2ft_model_config* c, double* out) {
   });
 }
 
+// rng.hpp:29-31: n draws of uniform_double from make_rng(seed, stream)
+// (bench_scheduler.cpp:13-27 draws the synthetic score tables this way).
+int d2ft_uniform_stream(uint64_t seed, uint64_t stream, int n, double* out) {
+  return guarded([&] {
+    auto g = stream_rng(seed, stream);
+    for (int i = 0; i < n; ++i) out[i] = unit(g);
+  });
+}
+
+int d2ft_set_device(int device) {
+  return guarded([&] { D2FT_CUDA(cudaSetDevice(device)); });
+}
+
 int d2ft_make_synthetic_dataset(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
                                 uint64_t seed, float* samples, int32_t* labels) {
   return guarded([&] {

@@ -458,6 +458,7 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
     attr_done = true;
   }
   knapsack_kernel<<<K, kThreads, smem, stream>>>(A);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -482,6 +483,7 @@ void launch_dp_const(const double* scores, const int32_t* row_wt, const int32_t*
                  "dp_search: global decision-bit workspace too small");
   D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
   dp_const_kernel<<<nrows, kThreads, smem, stream>>>(A);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -491,6 +493,7 @@ void launch_dp_general(const double* scores, const int32_t* weights, const int32
   if (nrows == 0) return;
   dp_general_kernel<<<nrows, kThreads, 0, stream>>>(scores, weights, caps, rows, N, max_cap, sel, obj, bits_global,
                                                     vals_global);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -498,14 +501,17 @@ void launch_merge(const uint8_t* full_sel, const uint8_t* fwd_sel, size_t n, uin
   if (n == 0) return;
   const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
   merge_kernel<<<blocks, 256, 0, s>>>(full_sel, fwd_sel, n, codes);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 void launch_compact(const uint8_t* codes, int K, int N, int H, const CompactLists& lists, cudaStream_t s) {
   compact_rows_kernel<<<K, 128, (size_t)N, s>>>(codes, N, lists);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
   const int cells = N * (K / H);
   compact_cols_kernel<<<(cells + 255) / 256, 256, 0, s>>>(codes, K, N, H, lists);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -514,6 +520,7 @@ void launch_scaler(const double* bwd, const double* fwd, const int32_t* cf, cons
                    uint8_t* choice_global, double* vals_global, cudaStream_t s) {
   scaler_kernel<<<K, kThreads, 0, s>>>(bwd, fwd, cf, cb, total_cap, N, lambda_dev, max_cap, codes, choice_global,
                                        vals_global);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 

@@ -881,6 +881,7 @@ int grid_for(size_t n, int threads) {
 void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
                          cudaStream_t st) {
   expand_codes_kernel<<<grid_for((size_t)K * Bmax, 256), 256, 0, st>>>(codes, K, n_mb, mbs, B, Bmax, out);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -890,6 +891,7 @@ void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g
   while (threads < D.B) threads <<= 1;
   D2FT_REQUIRE(threads <= 1024, kSize, "plan: batch above 1024 samples");
   plan_kernel<<<D.L, threads, 0, st>>>(D, act_cnt, full_hcnt, g1_tiles, g1_count, g4_tiles, g4_count);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -900,6 +902,7 @@ void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, c
   const size_t sm = tile_smem(D);
   D2FT_CUDA(cudaFuncSetAttribute(prep_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   prep_input_kernel<<<grid, 256, sm, st>>>(D, x, inp, inpT);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -908,6 +911,7 @@ void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* 
   const size_t sm = tile_smem(D);
   D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   ln_fwd_kernel<<<grid, 256, sm, st>>>(D, x, xn, xnT, stats);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -918,6 +922,7 @@ void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float*
   const size_t sm = tile_smem(D) + (size_t)8 * D.d * 4;
   D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   ln_bwd_prep_kernel<<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs, gmax);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -928,10 +933,12 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
     const size_t sm = attn_fwd_smem(64, D.TQ) + (size_t)D.TQ * 72 * 2;
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attn_fwd_kernel<64><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_fwd_smem(32, D.TQ) + (size_t)D.TQ * 40 * 2;
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attn_fwd_kernel<32><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
   }
@@ -945,10 +952,12 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
     const size_t sm = attn_bwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attn_bwd_kernel<64><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_bwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attn_bwd_kernel<32><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
   }
@@ -961,6 +970,7 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
   const size_t sm = (size_t)(10 * D.d + 2 * D.T) * 4;
   D2FT_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   head_kernel<<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -968,6 +978,7 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
                         float* dbc, double* loss, cudaStream_t st) {
   const int n = D.d * D.C + D.C + 1;
   head_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, loss_s, pooled, dlog, dWc, dbc, loss);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -975,6 +986,7 @@ void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float*
                         float* db1_l, float* db2_l, cudaStream_t st) {
   const int n = D.d + D.H * D.fs;
   bias_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -982,6 +994,7 @@ void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* 
                          float* dbe, float* dpos, cudaStream_t st) {
   const size_t n = (size_t)D.d * D.d + (size_t)D.T * D.d + D.d;
   embed_reduce_kernel<<<grid_for(n, 256), 256, 0, st>>>(D, KS, part, part_cs, dX, dWeT, dbe, dpos);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -989,6 +1002,7 @@ void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long l
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st) {
   if (!n) return;
   sgd_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, v, g, pbf, n, outer, inner, H, full_cnt, lr, mom, err);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -996,6 +1010,7 @@ void launch_transpose_bf16(const act_t* in, act_t* out, int batches, int rows, i
                            const int* full_cnt, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
   transpose_bf16_kernel<false><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_rows, H, full_cnt);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
@@ -1003,11 +1018,13 @@ void launch_transpose_bf16_colheads(const act_t* in, act_t* out, int batches, in
                                     const int* full_cnt, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
   transpose_bf16_kernel<true><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_cols, H, full_cnt);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
+  count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
