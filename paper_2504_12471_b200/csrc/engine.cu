@@ -148,7 +148,6 @@ struct Engine {
     }
     ev.clear();
     ev_phase.clear();
-    ++profiled_steps;
   }
 
   Engine(const d2ft_model_config& c, int Bmax) {
@@ -555,6 +554,7 @@ struct Engine {
 
   void begin_step(int B) {
     D2FT_REQUIRE(B >= 1 && B <= D.Bmax, kSize, "step: batch exceeds the engine capacity");
+    if (profiling) ++profiled_steps;
     D.B = B;
     D2FT_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
   }
