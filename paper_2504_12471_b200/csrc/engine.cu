@@ -170,6 +170,7 @@ struct Engine {
     D2FT_REQUIRE(D.dh == 32 || D.dh == 64, kConfig, "b200 engine: head_dim (d/H) must be 32 or 64");
     D2FT_REQUIRE(D.fs % 8 == 0, kConfig, "b200 engine: ffn slice must be a multiple of 8");
     D2FT_REQUIRE(D.T <= 256, kConfig, "b200 engine: seq_len must be <= 256");
+    D2FT_REQUIRE(D.H <= 16, kConfig, "b200 engine: at most 16 heads per block");
     D2FT_REQUIRE(D.C <= 64, kConfig, "b200 engine: at most 64 classes");
     D2FT_REQUIRE(Bmax >= 1 && Bmax <= 1024, kConfig, "b200 engine: batch capacity must be in [1, 1024]");
     D.PQ = 3 * D.dh + D.fs;

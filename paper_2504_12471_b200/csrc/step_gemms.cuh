@@ -41,10 +41,13 @@ struct EmbedFwd {
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
     const int m = c.mt * 128 + row;
     const float b = be[m];
+    float p[16];  // all loads first: the stores below may alias as far as the compiler knows
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = col0 + i < D.T ? __ldg(pos + (size_t)(col0 + i) * D.d + m) : 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int t = col0 + i;
-      if (t < D.T) x0[((size_t)c.s * D.T + t) * D.d + m] = v[i] + b + pos[(size_t)t * D.d + m];
+      if (t < D.T) x0[((size_t)c.s * D.T + t) * D.d + m] = v[i] + b + p[i];
     }
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
@@ -68,27 +71,28 @@ struct G1 {
   act_t* OG;         // block l: [Bmax][H][T][PO]
   act_t* OGT;        // block l: [Bmax][H][PO][TP]
   struct Tile {
-    int nkb, s, u0, nu;
+    int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
   struct Row {
     int valid, h, f;
     float bias;
   };
   __device__ int ntiles() const { return *count; }
+  __device__ int unit_row(int s, int u) const {
+    const int h = act_heads[(s * D.L + l) * D.H + u / D.UQ];
+    return h * D.PQ + (u % D.UQ) * 64;
+  }
   __device__ void tile(int t, Tile& c) const {
     const int p = tiles[t];
     c.s = p >> 16;
     c.u0 = p & 0xffff;
     c.nu = D.UQ * act_cnt[c.s * D.L + l];
     c.nkb = D.d / 64;
-  }
-  __device__ int unit_row(const Tile& c, int u) const {
-    const int h = act_heads[(c.s * D.L + l) * D.H + u / D.UQ];
-    return h * D.PQ + (u % D.UQ) * 64;
+    c.r0 = unit_row(c.s, c.u0);
+    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0);
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
-    const int u1 = c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0;
-    return KCoord{kb * 64, unit_row(c, c.u0), unit_row(c, u1), l, kb * 64, 0, l * D.Bmax + c.s};
+    return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, l * D.Bmax + c.s};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
     const int u = c.u0 + (row >> 6);
@@ -144,6 +148,7 @@ struct G3 {
   float* xout;
   struct Tile {
     int nkb, s, mt;
+    int heads[16];  // the sample's active heads in block l (cached once per tile)
   };
   struct Row {
     float bias;
@@ -152,11 +157,15 @@ struct G3 {
   __device__ void tile(int t, Tile& c) const {
     c.s = t / (D.d / 128);
     c.mt = t % (D.d / 128);
-    c.nkb = D.UO * act_cnt[c.s * D.L + l];
+    const int n = act_cnt[c.s * D.L + l];
+    c.nkb = D.UO * n;
+    const int* hp = act_heads + (c.s * D.L + l) * D.H;
+#pragma unroll
+    for (int a = 0; a < 16; ++a) c.heads[a] = a < n ? hp[a] : 0;
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int a = kb / D.UO, kk = kb % D.UO;
-    const int h = act_heads[(c.s * D.L + l) * D.H + a];
+    const int h = c.heads[a];
     return KCoord{h * D.PO + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, (l * D.Bmax + c.s) * D.H + h};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
@@ -167,14 +176,13 @@ struct G3 {
   }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
+    const size_t o0 = ((size_t)c.s * D.T + col0) * D.d + m;
+    float xi[16];  // batch the residual loads ahead of the stores
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int t = col0 + i;
-      if (t < D.T) {
-        const size_t o = ((size_t)c.s * D.T + t) * D.d + m;
-        xout[o] = xin[o] + v[i] + r.bias;
-      }
-    }
+    for (int i = 0; i < 16; ++i) xi[i] = col0 + i < D.T ? __ldg(xin + o0 + (size_t)i * D.d) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col0 + i < D.T) xout[o0 + (size_t)i * D.d] = xi[i] + v[i] + r.bias;
   }
   __device__ void row_end(const Tile&, int, Row&) const {}
 };
@@ -198,27 +206,28 @@ struct G4 {
   float* part_db1; // [Bmax][H][fs]
   const float* gmax;
   struct Tile {
-    int nkb, s, u0, nu;
+    int nkb, s, u0, nu, r0, r1;
   };
   struct Row {
     int valid, h, f;
     float db;
   };
   __device__ int ntiles() const { return *count; }
+  __device__ int unit_row(int s, int u) const {
+    const int h = full_heads[(s * D.L + l) * D.H + u / D.UO];
+    return h * D.PO + (u % D.UO) * 64;
+  }
   __device__ void tile(int t, Tile& c) const {
     const int p = tiles[t];
     c.s = p >> 16;
     c.u0 = p & 0xffff;
     c.nu = D.UO * full_hcnt[c.s * D.L + l];
     c.nkb = D.d / 64;
-  }
-  __device__ int unit_row(const Tile& c, int u) const {
-    const int h = full_heads[(c.s * D.L + l) * D.H + u / D.UO];
-    return h * D.PO + (u % D.UO) * 64;
+    c.r0 = unit_row(c.s, c.u0);
+    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0);
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
-    const int u1 = c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0;
-    return KCoord{kb * 64, unit_row(c, c.u0), unit_row(c, u1), l, kb * 64, 0, c.s};
+    return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, c.s};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
     const int u = c.u0 + (row >> 6);
@@ -245,15 +254,16 @@ struct G4 {
     act_t* dy = dY1 + sh * D.T * D.PQ + fq;
     float dz[16];
 #pragma unroll
+    for (int i = 0; i < 16; ++i)  // loads first (no load->store serialisation)
+      dz[i] = col0 + i < D.T ? act_to_f(z[(size_t)(col0 + i) * D.PQ]) : 0.f;
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int t = col0 + i;
-      dz[i] = 0.f;
-      if (t < D.T) {
-        dz[i] = v[i] * gelu_grad_f(act_to_f(z[(size_t)t * D.PQ]));
-        dy[(size_t)t * D.PQ] = to_act(dz[i]);
-        r.db += dz[i];
-      }
+      dz[i] = col0 + i < D.T ? v[i] * gelu_grad_f(dz[i]) : 0.f;
+      r.db += dz[i];
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col0 + i < D.T) dy[(size_t)(col0 + i) * D.PQ] = to_act(dz[i]);
     act_t* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
     if (col0 + 8 <= D.TP) st_act_x8(dt, dz);
     if (col0 + 16 <= D.TP) st_act_x8(dt + 8, dz + 8);
@@ -375,6 +385,7 @@ struct G8 {
   const float* gmax;
   struct Tile {
     int nkb, s, mt;
+    int heads[16];
   };
   struct Row {
     float inv;
@@ -383,11 +394,15 @@ struct G8 {
   __device__ void tile(int t, Tile& c) const {
     c.s = t / (D.d / 128);
     c.mt = t % (D.d / 128);
-    c.nkb = D.UQ * full_hcnt[c.s * D.L + l];
+    const int n = full_hcnt[c.s * D.L + l];
+    c.nkb = D.UQ * n;
+    const int* hp = full_heads + (c.s * D.L + l) * D.H;
+#pragma unroll
+    for (int a = 0; a < 16; ++a) c.heads[a] = a < n ? hp[a] : 0;
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int a = kb / D.UQ, kk = kb % D.UQ;
-    const int h = full_heads[(c.s * D.L + l) * D.H + a];
+    const int h = c.heads[a];
     return KCoord{h * D.PQ + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, c.s * D.H + h};
   }
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }

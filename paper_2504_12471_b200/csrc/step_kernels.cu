@@ -435,6 +435,13 @@ __global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
 }
 
 // ------------------------------------------------------------------ attention (mma.sync, FA2 style)
+// One CTA per (sample, head) slot, 8 warps, 16-row strips.  q, k, v, dO are
+// fp16 (G1 / G4 epilogues), staged with cp.async (zero-filled past T) into
+// row-major shared tiles with a 16-byte pad (conflict-free ldmatrix); A and B
+// fragments come from ldmatrix / ldmatrix.trans, so no transposed copies.
+constexpr int kAttnWarps = 8;
+constexpr float kLog2e = 1.4426950408889634f;
+
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -442,84 +449,107 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t ld32(const act_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
-// attention operands are fp16 (q, k, v written by G1; P, dS, scaled dO here):
-// 10-bit mantissa keeps the recomputed softmax and dS 4x closer to fp64 than act_t
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-
-// A fragment (16 x 16) from row-major X (pitch p): rows r0.., cols k0..
-__device__ __forceinline__ void lda(uint32_t (&a)[4], const act_t* X, int p, int r0, int k0, int g, int c) {
-  a[0] = ld32(X + (size_t)(r0 + g) * p + k0 + 2 * c);
-  a[1] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 2 * c);
-  a[2] = ld32(X + (size_t)(r0 + g) * p + k0 + 8 + 2 * c);
-  a[3] = ld32(X + (size_t)(r0 + g + 8) * p + k0 + 8 + 2 * c);
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
 }
-// B fragment (16 x 8) from n-major Y[n][k] (pitch p)
-__device__ __forceinline__ void ldb(uint32_t& b0, uint32_t& b1, const act_t* Y, int p, int n0, int k0, int g, int c) {
-  b0 = ld32(Y + (size_t)(n0 + g) * p + k0 + 2 * c);
-  b1 = ld32(Y + (size_t)(n0 + g) * p + k0 + 8 + 2 * c);
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
 }
+// A (16x16) at (r0, k0) of row-major X[row][k], pitch P halves
+__device__ __forceinline__ void frag_a(uint32_t (&a)[4], const act_t* X, int P, int r0, int k0, int lane) {
+  ldsm_x4(a, X + (size_t)(r0 + (lane & 15)) * P + k0 + (lane >> 4) * 8);
+}
+// B for two n8 tiles (n0, n0+8) x k16 from n-major Y[n][k]: {b0,b1} of n0, {b0,b1} of n0+8
+__device__ __forceinline__ void frag_b_n(uint32_t (&b)[4], const act_t* Y, int P, int n0, int k0, int lane) {
+  ldsm_x4(b, Y + (size_t)(n0 + (lane & 7) + ((lane >> 4) << 3)) * P + k0 + ((lane >> 3) & 1) * 8);
+}
+// B for two n8 tiles x k16 from k-major X[k][n] (transposed load)
+__device__ __forceinline__ void frag_b_k(uint32_t (&b)[4], const act_t* X, int P, int n0, int k0, int lane) {
+  ldsm_x4_t(b, X + (size_t)(k0 + (lane & 7) + (((lane >> 3) & 1) << 3)) * P + n0 + (lane >> 4) * 8);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-constexpr float kLog2e = 1.4426950408889634f;
-
-// Loads rows [0,T) of a [T][pitch_g] slice (cols off..off+DH) into row-major
-// smem [TQ][DH+8] (rows >= T zero) and optionally its transpose [DH][TQ+8].
+// rows [0,TQ) of cols [off, off+DH) of a [T][pitch] fp16 slice -> smem [TQ][DH+8]
 template <int DH>
-__device__ void load_tile(const act_t* g, int pitch_g, int off, int T, int TQ, act_t* rowm, act_t* trans) {
-  const int P = DH + 8, PT = TQ + 8;
-  for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
-    const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
-    uint32_t v = 0;
-    if (t < T) v = ld32(g + (size_t)t * pitch_g + off + f);
-    *reinterpret_cast<uint32_t*>(rowm + t * P + f) = v;
-    if (trans) {
-      const act_t* h = reinterpret_cast<const act_t*>(&v);
-      trans[f * PT + t] = h[0];
-      trans[(f + 1) * PT + t] = h[1];
-    }
+__device__ void stage_rows(const act_t* g, int pitch, int off, int T, int TQ, act_t* dst) {
+  constexpr int CH = DH / 8;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < TQ * CH; i += blockDim.x) {
+    const int t = i / CH, c = i % CH;
+    const bool v = t < T;
+    cp_async16(dst + t * (DH + 8) + c * 8, g + (size_t)(v ? t : 0) * pitch + off + c * 8, v);
   }
 }
+// 16 x DH fp32 fragment block of one warp -> fp16 feature-major rows
+// outT[f][t0 .. t0+15] (staged through the warp's shared scratch)
+template <int DH>
+__device__ void store_transposed(const float (&o)[DH / 8][4], float sc, act_t* scratch, act_t* outT, int TP, int t0,
+                                 int T, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+#pragma unroll
+  for (int nf = 0; nf < DH / 8; ++nf) {  // scratch[f][row], pitch 24 halves
+    const int f = nf * 8 + 2 * c;
+    scratch[f * 24 + g] = __float2half_rn(o[nf][0] * sc);
+    scratch[(f + 1) * 24 + g] = __float2half_rn(o[nf][1] * sc);
+    scratch[f * 24 + g + 8] = __float2half_rn(o[nf][2] * sc);
+    scratch[(f + 1) * 24 + g + 8] = __float2half_rn(o[nf][3] * sc);
+  }
+  __syncwarp();
+  for (int f = lane; f < DH; f += 32) {
+    act_t* dst = outT + (size_t)f * TP + t0;
+    const act_t* src = scratch + f * 24;
+    if (t0 + 16 <= TP) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      *reinterpret_cast<uint4*>(dst + 8) = *reinterpret_cast<const uint4*>(src + 8);
+    } else {
+      for (int r = 0; r < 16 && t0 + r < TP; ++r) dst[r] = src[r];
+    }
+  }
+  __syncwarp();
+  (void)T;
+}
 
 template <int DH>
-__global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
-                                                       const act_t* Y1, act_t* OG, act_t* OGT, float* lse) {
+__global__ void __launch_bounds__(kAttnWarps * 32) attn_fwd_kernel(Dims D, int l, const int* act_heads,
+                                                                  const int* act_cnt, const act_t* Y1, act_t* OG,
+                                                                  act_t* OGT, float* lse) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
   const int h = act_heads[(s * D.L + l) * D.H + a];
   extern __shared__ __align__(16) unsigned char smem[];
-  const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
-  act_t* Ks = reinterpret_cast<act_t*>(smem);  // [TQ][P]
-  act_t* Vt = Ks + TQ * P;                    // [DH][PT]
-  act_t* Qs = Vt + DH * PT;                   // [TQ][P]
+  const int TQ = D.TQ;
+  constexpr int P = DH + 8;
+  act_t* Qs = reinterpret_cast<act_t*>(smem);  // [TQ][P]
+  act_t* Ks = Qs + TQ * P;
+  act_t* Vs = Ks + TQ * P;
+  act_t* scr = Vs + TQ * P;  // kAttnWarps x [DH][24]
   const size_t sh = (size_t)s * D.H + h;
   const act_t* y = Y1 + sh * D.T * D.PQ;
-  load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, nullptr);
-  {
-    // K row-major, V transposed only
-    for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
-      const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
-      uint32_t kv = 0, vv = 0;
-      if (t < D.T) {
-        kv = ld32(y + (size_t)t * D.PQ + DH + f);
-        vv = ld32(y + (size_t)t * D.PQ + 2 * DH + f);
-      }
-      *reinterpret_cast<uint32_t*>(Ks + t * P + f) = kv;
-      const act_t* hv = reinterpret_cast<const act_t*>(&vv);
-      Vt[f * PT + t] = hv[0];
-      Vt[(f + 1) * PT + t] = hv[1];
-    }
-  }
+  stage_rows<DH>(y, D.PQ, 0, D.T, TQ, Qs);
+  stage_rows<DH>(y, D.PQ, DH, D.T, TQ, Ks);
+  stage_rows<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs);
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
+  act_t* myscr = scr + warp * DH * 24;
   const float sl2 = kLog2e / sqrtf((float)DH);  // 1/sqrt(dh) (model.cpp:213) in log2 units
-  for (int strip = warp; strip < TQ / 16; strip += 4) {
+  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
     const int r0 = strip * 16;
     uint32_t qa[DH / 16][4];
 #pragma unroll
-    for (int ks = 0; ks < DH / 16; ++ks) lda(qa[ks], Qs, P, r0, ks * 16, g, c);
+    for (int ks = 0; ks < DH / 16; ++ks) frag_a(qa[ks], Qs, P, r0, ks * 16, lane);
     float o[DH / 8][4];
 #pragma unroll
     for (int nf = 0; nf < DH / 8; ++nf) o[nf][0] = o[nf][1] = o[nf][2] = o[nf][3] = 0.f;
@@ -527,22 +557,26 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
     for (int kc = 0; kc < TQ; kc += 64) {
       float sc[8][4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = -INFINITY;
-        if (kc + nt * 8 < TQ) {
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int np = 0; np < 4; ++np) {  // pairs of n8 key tiles
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[2 * np][e] = sc[2 * np + 1][e] = 0.f;
+        if (kc + np * 16 < TQ) {
 #pragma unroll
           for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(acc, qa[ks], b0, b1);
+            uint32_t b[4];
+            frag_b_n(b, Ks, P, kc + np * 16, ks * 16, lane);
+            mma16816(sc[2 * np], qa[ks], b[0], b[1]);
+            mma16816(sc[2 * np + 1], qa[ks], b[2], b[3]);
           }
-          const int key = kc + nt * 8 + 2 * c;
-          sc[nt][0] = key < D.T ? acc[0] * sl2 : -INFINITY;
-          sc[nt][1] = key + 1 < D.T ? acc[1] * sl2 : -INFINITY;
-          sc[nt][2] = key < D.T ? acc[2] * sl2 : -INFINITY;
-          sc[nt][3] = key + 1 < D.T ? acc[3] * sl2 : -INFINITY;
         }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int key = kc + nt * 8 + 2 * c;
+        sc[nt][0] = key < D.T ? sc[nt][0] * sl2 : -INFINITY;
+        sc[nt][1] = key + 1 < D.T ? sc[nt][1] * sl2 : -INFINITY;
+        sc[nt][2] = key < D.T ? sc[nt][2] * sl2 : -INFINITY;
+        sc[nt][3] = key + 1 < D.T ? sc[nt][3] * sl2 : -INFINITY;
       }
       float mx0 = m0, mx1 = m1;
 #pragma unroll
@@ -582,10 +616,11 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
           uint32_t pa[4] = {pack2(sc[2 * j][0], sc[2 * j][1]), pack2(sc[2 * j][2], sc[2 * j][3]),
                             pack2(sc[2 * j + 1][0], sc[2 * j + 1][1]), pack2(sc[2 * j + 1][2], sc[2 * j + 1][3])};
 #pragma unroll
-          for (int nf = 0; nf < DH / 8; ++nf) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Vt, PT, nf * 8, kc + j * 16, g, c);
-            mma16816(o[nf], pa, b0, b1);
+          for (int nf = 0; nf < DH / 8; nf += 2) {
+            uint32_t b[4];
+            frag_b_k(b, Vs, P, nf * 8, kc + j * 16, lane);
+            mma16816(o[nf], pa, b[0], b[1]);
+            mma16816(o[nf + 1], pa, b[2], b[3]);
           }
         }
       }
@@ -595,25 +630,22 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
     const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int nf = 0; nf < DH / 8; ++nf) {
+      o[nf][0] *= i0;
+      o[nf][1] *= i0;
+      o[nf][2] *= i1;
+      o[nf][3] *= i1;
+    }
     const int t0 = r0 + g, t1 = r0 + g + 8;
     act_t* og = OG + sh * D.T * D.PO;
-    act_t* ogt = OGT + sh * D.PO * D.TP;
 #pragma unroll
     for (int nf = 0; nf < DH / 8; ++nf) {
       const int f = nf * 8 + 2 * c;
-      if (t0 < D.T) {
-        const float a0 = o[nf][0] * i0, a1 = o[nf][1] * i0;
-        *reinterpret_cast<uint32_t*>(og + (size_t)t0 * D.PO + f) = pack2(a0, a1);
-        ogt[(size_t)f * D.TP + t0] = to_act(a0);
-        ogt[(size_t)(f + 1) * D.TP + t0] = to_act(a1);
-      }
-      if (t1 < D.T) {
-        const float a2 = o[nf][2] * i1, a3 = o[nf][3] * i1;
-        *reinterpret_cast<uint32_t*>(og + (size_t)t1 * D.PO + f) = pack2(a2, a3);
-        ogt[(size_t)f * D.TP + t1] = to_act(a2);
-        ogt[(size_t)(f + 1) * D.TP + t1] = to_act(a3);
-      }
+      if (t0 < D.T) *reinterpret_cast<uint32_t*>(og + (size_t)t0 * D.PO + f) = pack2(o[nf][0], o[nf][1]);
+      if (t1 < D.T) *reinterpret_cast<uint32_t*>(og + (size_t)t1 * D.PO + f) = pack2(o[nf][2], o[nf][3]);
     }
+    store_transposed<DH>(o, 1.f, myscr, OGT + sh * D.PO * D.TP, D.TP, r0, D.T, lane);
     if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
       if (t0 < D.T) lse[sh * D.T + t0] = m0 + log2f(l0);
       if (t1 < D.T) lse[sh * D.T + t1] = m1 + log2f(l1);
@@ -621,172 +653,145 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(Dims D, int l, const int*
   }
 }
 
-// Backward (model.cpp:262-271): pass A over key strips -> dK, dV; pass B over
-// query strips -> dQ (scores recomputed from q, k and the saved LSE).
+// Backward (model.cpp:262-271).  Pass B (query strips) first: D_i =
+// rowdot(P_i, dP_i) from the very P and dP used for dS (softmax_rows_backward,
+// linalg.cpp:118-128), then dQ.  Pass A (key strips): dK, dV.
 template <int DH>
-__global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
-                                                       const act_t* Y1, const act_t* OG, const act_t* dO,
-                                                       const float* lse, act_t* dY1, act_t* dY1T) {
+__global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_kernel(Dims D, int l, const int* full_heads,
+                                                                  const int* full_hcnt, const act_t* Y1,
+                                                                  const act_t* dO, const float* lse, act_t* dY1,
+                                                                  act_t* dY1T) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
   const int h = full_heads[(s * D.L + l) * D.H + a];
   extern __shared__ __align__(16) unsigned char smem[];
-  const int TQ = D.TQ, P = DH + 8, PT = TQ + 8;
+  const int TQ = D.TQ;
+  constexpr int P = DH + 8;
   act_t* Qs = reinterpret_cast<act_t*>(smem);
   act_t* Ks = Qs + TQ * P;
   act_t* Vs = Ks + TQ * P;
   act_t* dOs = Vs + TQ * P;
-  act_t* Qt = dOs + TQ * P;
-  act_t* Kt = Qt + DH * PT;
-  act_t* dOt = Kt + DH * PT;
-  float* Dv = reinterpret_cast<float*>(dOt + DH * PT);
+  act_t* scr = dOs + TQ * P;  // kAttnWarps x [DH][24]
+  float* Dv = reinterpret_cast<float*>(scr + kAttnWarps * DH * 24);
   float* L2 = Dv + TQ;
   const size_t sh = (size_t)s * D.H + h;
   const act_t* y = Y1 + sh * D.T * D.PQ;
-  const act_t* og = OG + sh * D.T * D.PO;
-  const act_t* dog = dO + sh * D.T * D.dh;
-  load_tile<DH>(y, D.PQ, 0, D.T, TQ, Qs, Qt);
-  load_tile<DH>(y, D.PQ, DH, D.T, TQ, Ks, Kt);
-  load_tile<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs, nullptr);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
-  // dO arrives in act_t (G4); rescale by a power of two alpha so max|alpha*dO| is in
-  // [1, 2) and convert exactly to fp16; outputs are unscaled by 1/alpha.
-  __shared__ float s_red[4];
-  float mx = 0.f;
-  for (int i = threadIdx.x; i < D.T * DH; i += blockDim.x)
-    mx = fmaxf(mx, fabsf(act_to_f(dog[(size_t)(i / DH) * D.dh + i % DH])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_red[warp] = mx;
-  __syncthreads();
-  mx = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
-  const float alpha = mx > 0.f ? exp2f(-floorf(log2f(mx))) : 1.f;
-  const float ia = 1.f / alpha;
-  for (int i = threadIdx.x; i < TQ * (DH / 2); i += blockDim.x) {
-    const int t = i / (DH / 2), f = (i % (DH / 2)) * 2;
-    float v0 = 0.f, v1 = 0.f;
-    if (t < D.T) {
-      v0 = act_to_f(dog[(size_t)t * D.dh + f]) * alpha;
-      v1 = act_to_f(dog[(size_t)t * D.dh + f + 1]) * alpha;
-    }
-    *reinterpret_cast<uint32_t*>(dOs + t * P + f) = pack2(v0, v1);
-    reinterpret_cast<__half*>(dOt)[f * PT + t] = __float2half_rn(v0);
-    reinterpret_cast<__half*>(dOt)[(f + 1) * PT + t] = __float2half_rn(v1);
-  }
+  stage_rows<DH>(y, D.PQ, 0, D.T, TQ, Qs);
+  stage_rows<DH>(y, D.PQ, DH, D.T, TQ, Ks);
+  stage_rows<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs);
+  stage_rows<DH>(dO + sh * D.T * D.dh, D.dh, 0, D.T, TQ, dOs);
   for (int t = threadIdx.x; t < TQ; t += blockDim.x) L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+  cp_async_wait_all();
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
+  act_t* myscr = scr + warp * DH * 24;
   const float sl2 = kLog2e / sqrtf((float)DH);
-  const float scale = ia / sqrtf((float)DH);  // 1/sqrt(dh) and the dO unscale
+  const float scale = 1.0f / sqrtf((float)DH);
   act_t* dy = dY1 + sh * D.T * D.PQ;
   act_t* dyt = dY1T + sh * D.PQ * D.TP;
 
   // ---- pass B: query strip i -> D_i, dQ_i
-  for (int strip = warp; strip < TQ / 16; strip += 4) {
+  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
     const int r0 = strip * 16;
-    uint32_t qa[DH / 16][4], da_[DH / 16][4];
+    uint32_t qa[DH / 16][4], oa[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
-      lda(qa[ks], Qs, P, r0, ks * 16, g, c);
-      lda(da_[ks], dOs, P, r0, ks * 16, g, c);
+      frag_a(qa[ks], Qs, P, r0, ks * 16, lane);
+      frag_a(oa[ks], dOs, P, r0, ks * 16, lane);
     }
     const float l20 = L2[r0 + g], l21 = L2[r0 + g + 8];
-    // D_i = sum_j P_ij dP_ij from the very P and dP used below (softmax_rows_backward,
-    // linalg.cpp:118-128): keeps sum_j dS_ij = 0 exactly as the reference does
     float d0 = 0.f, d1 = 0.f;
-    for (int kc = 0; kc < TQ; kc += 64) {
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      float dq[DH / 8][4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        if (kc + nt * 8 < TQ) {
-          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
+      for (int kc = 0; kc < TQ; kc += 64) {
+        float ds[8][4];
 #pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(st, qa[ks], b0, b1);
-            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(dp, da_[ks], b0, b1);
+        for (int np = 0; np < 4; ++np) {
+          float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};
+          float dp0[4] = {0.f, 0.f, 0.f, 0.f}, dp1[4] = {0.f, 0.f, 0.f, 0.f};
+          if (kc + np * 16 < TQ) {
+#pragma unroll
+            for (int ks = 0; ks < DH / 16; ++ks) {
+              uint32_t b[4];
+              frag_b_n(b, Ks, P, kc + np * 16, ks * 16, lane);
+              mma16816(st0, qa[ks], b[0], b[1]);
+              mma16816(st1, qa[ks], b[2], b[3]);
+              frag_b_n(b, Vs, P, kc + np * 16, ks * 16, lane);
+              mma16816(dp0, oa[ks], b[0], b[1]);
+              mma16816(dp1, oa[ks], b[2], b[3]);
+            }
           }
-          const int key = kc + nt * 8 + 2 * c;
-          const bool ka = key < D.T, kb = key + 1 < D.T;
-          d0 += (ka ? exp2f(st[0] * sl2 - l20) * dp[0] : 0.f) + (kb ? exp2f(st[1] * sl2 - l20) * dp[1] : 0.f);
-          d1 += (ka ? exp2f(st[2] * sl2 - l21) * dp[2] : 0.f) + (kb ? exp2f(st[3] * sl2 - l21) * dp[3] : 0.f);
-        }
-      }
-    }
-    d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
-    d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
-    d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
-    d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
-    if (c == 0) {
-      Dv[r0 + g] = d0;
-      Dv[r0 + g + 8] = d1;
-    }
-    float dq[DH / 8][4];
 #pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
-    for (int kc = 0; kc < TQ; kc += 64) {
-      float ds[8][4];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        ds[nt][0] = ds[nt][1] = ds[nt][2] = ds[nt][3] = 0.f;
-        if (kc + nt * 8 < TQ) {
-          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Ks, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(st, qa[ks], b0, b1);
-            ldb(b0, b1, Vs, P, kc + nt * 8, ks * 16, g, c);
-            mma16816(dp, da_[ks], b0, b1);
+          for (int hh = 0; hh < 2; ++hh) {
+            const float* st = hh ? st1 : st0;
+            const float* dp = hh ? dp1 : dp0;
+            const int key = kc + np * 16 + hh * 8 + 2 * c;
+            const bool ka = key < D.T, kb = key + 1 < D.T;
+            const float p0 = ka ? exp2f(st[0] * sl2 - l20) : 0.f, p1 = kb ? exp2f(st[1] * sl2 - l20) : 0.f;
+            const float p2 = ka ? exp2f(st[2] * sl2 - l21) : 0.f, p3 = kb ? exp2f(st[3] * sl2 - l21) : 0.f;
+            if (sweep == 0) {
+              d0 += p0 * dp[0] + p1 * dp[1];
+              d1 += p2 * dp[2] + p3 * dp[3];
+            }
+            ds[2 * np + hh][0] = p0 * (dp[0] - d0);
+            ds[2 * np + hh][1] = p1 * (dp[1] - d0);
+            ds[2 * np + hh][2] = p2 * (dp[2] - d1);
+            ds[2 * np + hh][3] = p3 * (dp[3] - d1);
           }
-          const int key = kc + nt * 8 + 2 * c;
-          const bool ka = key < D.T, kb = key + 1 < D.T;
-          ds[nt][0] = ka ? exp2f(st[0] * sl2 - l20) * (dp[0] - d0) : 0.f;
-          ds[nt][1] = kb ? exp2f(st[1] * sl2 - l20) * (dp[1] - d0) : 0.f;
-          ds[nt][2] = ka ? exp2f(st[2] * sl2 - l21) * (dp[2] - d1) : 0.f;
-          ds[nt][3] = kb ? exp2f(st[3] * sl2 - l21) * (dp[3] - d1) : 0.f;
         }
-      }
+        if (sweep == 1) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (kc + j * 16 < TQ) {
-          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
-                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
+          for (int j = 0; j < 4; ++j) {
+            if (kc + j * 16 < TQ) {
+              uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
+                                pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]),
+                                pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
 #pragma unroll
-          for (int nf = 0; nf < DH / 8; ++nf) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Kt, PT, nf * 8, kc + j * 16, g, c);
-            mma16816(dq[nf], sa, b0, b1);
+              for (int nf = 0; nf < DH / 8; nf += 2) {
+                uint32_t b[4];
+                frag_b_k(b, Ks, P, nf * 8, kc + j * 16, lane);
+                mma16816(dq[nf], sa, b[0], b[1]);
+                mma16816(dq[nf + 1], sa, b[2], b[3]);
+              }
+            }
           }
         }
       }
-    }
-    const int t0 = r0 + g, t1 = r0 + g + 8;
+      if (sweep == 0) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
+        if (c == 0) {
+          Dv[r0 + g] = d0;
+          Dv[r0 + g + 8] = d1;
+        }
+      } else {
+        const int t0 = r0 + g, t1 = r0 + g + 8;
 #pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) {
-      const int f = nf * 8 + 2 * c;
-      if (t0 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
-        dyt[(size_t)f * D.TP + t0] = to_act(dq[nf][0] * scale);
-        dyt[(size_t)(f + 1) * D.TP + t0] = to_act(dq[nf][1] * scale);
-      }
-      if (t1 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
-        dyt[(size_t)f * D.TP + t1] = to_act(dq[nf][2] * scale);
-        dyt[(size_t)(f + 1) * D.TP + t1] = to_act(dq[nf][3] * scale);
+        for (int nf = 0; nf < DH / 8; ++nf) {
+          const int f = nf * 8 + 2 * c;
+          if (t0 < D.T)
+            *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
+          if (t1 < D.T)
+            *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
+        }
+        store_transposed<DH>(dq, scale, myscr, dyt, D.TP, r0, D.T, lane);
       }
     }
   }
   __syncthreads();
 
   // ---- pass A: key strip j -> dK_j, dV_j
-  for (int strip = warp; strip < TQ / 16; strip += 4) {
+  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
     const int k0 = strip * 16;
-    uint32_t ka[DH / 16][4], va[DH / 16][4];
+    uint32_t ka_[DH / 16][4], va[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
-      lda(ka[ks], Ks, P, k0, ks * 16, g, c);
-      lda(va[ks], Vs, P, k0, ks * 16, g, c);
+      frag_a(ka_[ks], Ks, P, k0, ks * 16, lane);
+      frag_a(va[ks], Vs, P, k0, ks * 16, lane);
     }
     float dk[DH / 8][4], dv[DH / 8][4];
 #pragma unroll
@@ -797,29 +802,38 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int*
     for (int qc = 0; qc < TQ; qc += 64) {
       float pt[8][4], ds[8][4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) pt[nt][e] = ds[nt][e] = 0.f;
-        if (qc + nt * 8 < TQ) {
-          float st[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int np = 0; np < 4; ++np) {
+        float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};
+        float dp0[4] = {0.f, 0.f, 0.f, 0.f}, dp1[4] = {0.f, 0.f, 0.f, 0.f};
+        if (qc + np * 16 < TQ) {
 #pragma unroll
           for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b0, b1;
-            ldb(b0, b1, Qs, P, qc + nt * 8, ks * 16, g, c);
-            mma16816(st, ka[ks], b0, b1);
-            ldb(b0, b1, dOs, P, qc + nt * 8, ks * 16, g, c);
-            mma16816(dp, va[ks], b0, b1);
+            uint32_t b[4];
+            frag_b_n(b, Qs, P, qc + np * 16, ks * 16, lane);
+            mma16816(st0, ka_[ks], b[0], b[1]);
+            mma16816(st1, ka_[ks], b[2], b[3]);
+            frag_b_n(b, dOs, P, qc + np * 16, ks * 16, lane);
+            mma16816(dp0, va[ks], b[0], b[1]);
+            mma16816(dp1, va[ks], b[2], b[3]);
           }
-          const int q = qc + nt * 8 + 2 * c;
-          const float l2a = L2[q], l2b = L2[q + 1], da = Dv[q], db = Dv[q + 1];
-          pt[nt][0] = key0 ? exp2f(st[0] * sl2 - l2a) : 0.f;
-          pt[nt][1] = key0 ? exp2f(st[1] * sl2 - l2b) : 0.f;
-          pt[nt][2] = key1 ? exp2f(st[2] * sl2 - l2a) : 0.f;
-          pt[nt][3] = key1 ? exp2f(st[3] * sl2 - l2b) : 0.f;
-          ds[nt][0] = pt[nt][0] * (dp[0] - da);
-          ds[nt][1] = pt[nt][1] * (dp[1] - db);
-          ds[nt][2] = pt[nt][2] * (dp[2] - da);
-          ds[nt][3] = pt[nt][3] * (dp[3] - db);
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float* st = hh ? st1 : st0;
+          const float* dp = hh ? dp1 : dp0;
+          const int q = qc + np * 16 + hh * 8 + 2 * c;
+          const float l2a = q < TQ ? L2[q] : INFINITY, l2b = q + 1 < TQ ? L2[q + 1] : INFINITY;
+          const float da = q < TQ ? Dv[q] : 0.f, db = q + 1 < TQ ? Dv[q + 1] : 0.f;
+          float* P_ = pt[2 * np + hh];
+          float* S_ = ds[2 * np + hh];
+          P_[0] = key0 ? exp2f(st[0] * sl2 - l2a) : 0.f;
+          P_[1] = key0 ? exp2f(st[1] * sl2 - l2b) : 0.f;
+          P_[2] = key1 ? exp2f(st[2] * sl2 - l2a) : 0.f;
+          P_[3] = key1 ? exp2f(st[3] * sl2 - l2b) : 0.f;
+          S_[0] = P_[0] * (dp[0] - da);
+          S_[1] = P_[1] * (dp[1] - db);
+          S_[2] = P_[2] * (dp[2] - da);
+          S_[3] = P_[3] * (dp[3] - db);
         }
       }
 #pragma unroll
@@ -830,12 +844,14 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int*
           uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
                             pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
 #pragma unroll
-          for (int nf = 0; nf < DH / 8; ++nf) {
-            uint32_t b0, b1;
-            ldb(b0, b1, dOt, PT, nf * 8, qc + j * 16, g, c);
-            mma16816(dv[nf], pa, b0, b1);
-            ldb(b0, b1, Qt, PT, nf * 8, qc + j * 16, g, c);
-            mma16816(dk[nf], sa, b0, b1);
+          for (int nf = 0; nf < DH / 8; nf += 2) {
+            uint32_t b[4];
+            frag_b_k(b, dOs, P, nf * 8, qc + j * 16, lane);
+            mma16816(dv[nf], pa, b[0], b[1]);
+            mma16816(dv[nf + 1], pa, b[2], b[3]);
+            frag_b_k(b, Qs, P, nf * 8, qc + j * 16, lane);
+            mma16816(dk[nf], sa, b[0], b[1]);
+            mma16816(dk[nf + 1], sa, b[2], b[3]);
           }
         }
       }
@@ -846,28 +862,21 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(Dims D, int l, const int*
       const int f = nf * 8 + 2 * c;
       if (t0 < D.T) {
         *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + DH + f) = pack2(dk[nf][0] * scale, dk[nf][1] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0] * ia, dv[nf][1] * ia);
-        dyt[(size_t)(DH + f) * D.TP + t0] = to_act(dk[nf][0] * scale);
-        dyt[(size_t)(DH + f + 1) * D.TP + t0] = to_act(dk[nf][1] * scale);
-        dyt[(size_t)(2 * DH + f) * D.TP + t0] = to_act(dv[nf][0] * ia);
-        dyt[(size_t)(2 * DH + f + 1) * D.TP + t0] = to_act(dv[nf][1] * ia);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0], dv[nf][1]);
       }
       if (t1 < D.T) {
         *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + DH + f) = pack2(dk[nf][2] * scale, dk[nf][3] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2] * ia, dv[nf][3] * ia);
-        dyt[(size_t)(DH + f) * D.TP + t1] = to_act(dk[nf][2] * scale);
-        dyt[(size_t)(DH + f + 1) * D.TP + t1] = to_act(dk[nf][3] * scale);
-        dyt[(size_t)(2 * DH + f) * D.TP + t1] = to_act(dv[nf][2] * ia);
-        dyt[(size_t)(2 * DH + f + 1) * D.TP + t1] = to_act(dv[nf][3] * ia);
+        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2], dv[nf][3]);
       }
     }
+    store_transposed<DH>(dk, scale, myscr, dyt + (size_t)DH * D.TP, D.TP, k0, D.T, lane);
+    store_transposed<DH>(dv, 1.f, myscr, dyt + (size_t)2 * DH * D.TP, D.TP, k0, D.T, lane);
   }
-
 }
 
-size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(2 * TQ * (DH + 8) + DH * (TQ + 8)) * 2; }
+size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(3 * TQ * (DH + 8) + kAttnWarps * DH * 24) * 2; }
 size_t attn_bwd_smem(int DH, int TQ) {
-  return (size_t)(4 * TQ * (DH + 8) + 3 * DH * (TQ + 8)) * 2 + (size_t)2 * TQ * 4;
+  return (size_t)(4 * TQ * (DH + 8) + kAttnWarps * DH * 24) * 2 + (size_t)2 * TQ * 4;
 }
 
 int grid_for(size_t n, int threads) {
@@ -930,14 +939,14 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
                      act_t* OGT, float* lse, cudaStream_t st) {
   dim3 grid(D.H, D.B);
   if (D.dh == 64) {
-    const size_t sm = attn_fwd_smem(64, D.TQ) + (size_t)D.TQ * 72 * 2;
+    const size_t sm = attn_fwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<64><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<64><<<grid, kAttnWarps * 32, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
     count_launch();
   } else if (D.dh == 32) {
-    const size_t sm = attn_fwd_smem(32, D.TQ) + (size_t)D.TQ * 40 * 2;
+    const size_t sm = attn_fwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<32><<<grid, 128, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<32><<<grid, kAttnWarps * 32, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
@@ -951,12 +960,12 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
   if (D.dh == 64) {
     const size_t sm = attn_bwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<64><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<64><<<grid, kAttnWarps * 32, sm, st>>>(D, l, full_heads, full_hcnt, Y1, dO, lse, dY1, dY1T);
     count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_bwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<32><<<grid, 128, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<32><<<grid, kAttnWarps * 32, sm, st>>>(D, l, full_heads, full_hcnt, Y1, dO, lse, dY1, dY1T);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
