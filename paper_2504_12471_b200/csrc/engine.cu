@@ -83,7 +83,7 @@ struct Engine {
   float* x;       // [L+1][Bmax][T][d]
   float* stats;   // [L][Bmax][T][2]
   act_t *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
-  act_t *Y1, *OG, *OGT;
+  act_t *QKV, *ZT, *OG, *OGT;
   float* lse;     // [L][Bmax][H][T]
   act_t *inp, *inpT;
   float* samples_dev;
@@ -233,7 +233,8 @@ struct Engine {
     stats = dalloc<float>(L * Bm * T * 2, owned);
     xn = dalloc<act_t>(L * Bm * T * d, owned);
     xnT = dalloc<act_t>(L * Bm * d * TP, owned);
-    Y1 = dalloc<act_t>(L * Bm * H * T * PQ, owned);
+    QKV = dalloc<act_t>(L * Bm * H * T * 3 * D.dh, owned);
+    ZT = dalloc<act_t>(L * Bm * H * fs * TP, owned);
     OG = dalloc<act_t>(L * Bm * H * T * PO, owned);
     OGT = dalloc<act_t>(L * Bm * H * PO * TP, owned);
     lse = dalloc<float>(L * Bm * H * T, owned);
@@ -246,7 +247,7 @@ struct Engine {
     dxn = dalloc<float>(Bm * T * d, owned);
     const size_t ntile = (T + 31) / 32;
     part_cs = dalloc<float>(Bm * ntile * d, owned);
-    part_db1 = dalloc<float>(Bm * H * fs, owned);
+    part_db1 = dalloc<float>((size_t)kEpiGroups * Bm * H * fs, owned);
     part_ew = dalloc<float>((size_t)KS * d * d, owned);
     dC = dalloc<act_t>(Bm * T * d, owned);
     dCT = dalloc<act_t>(Bm * d * TP, owned);
@@ -422,14 +423,15 @@ struct Engine {
       mark(PH_LN);
       launch_ln_fwd(D, x + l * xs, xn + l * xs, xnT + (size_t)l * Bm * d * D.TP, stats + (size_t)l * Bm * T * 2, st);
       mark(PH_G1);
-      act_t* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
+      act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
       gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
-                    P + seg[S_B1].off + (size_t)l * H * D.fs, Y1l, OGl, OGTl);
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGl, OGTl);
       mark(PH_ATTN_F);
-      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, Y1l, OGl, OGTl, lse + (size_t)l * Bm * H * T, st);
+      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
       gemm_tokN<G3>(tm_W2T, tm_OG, D, l, lists.act_heads, lists.act_cnt, codes_exp, P + seg[S_B2].off + (size_t)l * d,
                     x + l * xs, x + (l + 1) * xs);
@@ -442,14 +444,15 @@ struct Engine {
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, dCT, part_cs, gmax, st);
     for (int l = D.L - 1; l >= 0; --l) {
-      act_t* Y1l = Y1 + (size_t)l * Bm * H * T * D.PQ;
+      act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
+      act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
-      gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt, Y1l, dO,
-                    dY1, dY1T, part_db1, (const float*)gmax);
+      gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
+                    (const act_t*)ZTl, dO, dY1, dY1T, part_db1, (const float*)gmax);
       mark(PH_ATTN_B);
-      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, Y1l, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
+      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
                       st);
       mark(PH_G5);
       launch_gemm<G5<160>, GemmShape<160, 6>>(

@@ -89,7 +89,7 @@ struct DenseProb {
       if (n < N) D[(size_t)m * N + n] = v[i];
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // Tokens as N: D[p][m][t] = sum_k A[m][k] X[p][t][k], t < T (box of BN rows, OOB zero).
@@ -120,7 +120,7 @@ struct PlanesProb {
       if (t < T) D[((size_t)c.p * M + m) * T + t] = v[i];
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // K = tokens of P planes: D[m][n] = sum_p sum_t XT[p][m][t] YT[p][n][t]
@@ -156,7 +156,7 @@ struct TokenKProb {
       if (n < N) D[(size_t)m * N + n] = v[i];
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 template <typename T>

@@ -17,12 +17,12 @@
 //     __device__ KCoord kcoord(const Tile&, int kb) const;
 //     __device__ void row_begin(const Tile&, int row, Row&) const;
 //     __device__ void chunk(const Tile&, int row, int col0, const float (&v)[16], Row&) const;
-//     __device__ void row_end(const Tile&, int row, Row&) const;
+//     __device__ void row_end(const Tile&, int row, int group, Row&) const;
 //   };
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
-// thread), warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM lane quarter
-// = warp % 4).  Tile M = 128 (two 64-row A boxes), N = BN, K-block = 64.
+// Roles: warp 0 = TMA producer, warp 1 = MMA issuer (one thread), warp 2 =
+// TMEM allocator, warps 4.. = EPI epilogue warpgroups (TMEM lane quarter =
+// warp % 4, column group = (warp - 4) / 4).  Tile M = 128 (two 64-row A boxes), N = BN, K-block = 64.
 // Two TMEM accumulators (columns 0 and 256) let the epilogue of tile i
 // overlap the MMAs of tile i+1.
 #pragma once
@@ -38,10 +38,13 @@ struct KCoord {
   int bx, by, bz;        // B: k offset, first row, plane
 };
 
-// FMT: operand format, 0 = fp16 (the step), 1 = bf16 (self-tests)
-template <int BN_, int STAGES_, int FMT_ = 0>
+// FMT: operand format, 0 = fp16 (the step), 1 = bf16 (self-tests).
+// EPI: epilogue warpgroups; group e drains column chunks e, e+EPI, ... of the
+// accumulator, so EPI x more epilogue loads/stores are in flight per SM.
+template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4>
 struct GemmShape {
-  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_;
+  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_;
+  static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -52,7 +55,7 @@ struct GemmShape {
 };
 
 template <class P, class S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(S::THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const P prob) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4);
+      ptx::mbar_init(&tempty[i], 4 * S::EPI);
     }
     ptx::fence_barrier_init();
   }
@@ -138,7 +141,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;  // TMEM lane quarter
+    const int q = warp & 3;            // TMEM lane quarter
+    const int e = (warp - 4) >> 2;     // column group
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(256, 1)
       prob.row_begin(c, row, st);
       const uint32_t base = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int col0 = 0; col0 < S::BN; col0 += 16) {
+      for (int col0 = 16 * e; col0 < S::BN; col0 += 16 * S::EPI) {
         float v[16];
         if (c.nkb > 0) {
           ptx::tmem_ld16(base + col0, v);
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         prob.chunk(c, row, col0, v, st);
       }
-      prob.row_end(c, row, st);
+      prob.row_end(c, row, e, st);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -205,7 +209,7 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int 
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid < 1) grid = 1;
-  gemm_sm100_kernel<P, S><<<grid, 256, S::SMEM_BYTES, stream>>>(a, b, prob);
+  gemm_sm100_kernel<P, S><<<grid, S::THREADS, S::SMEM_BYTES, stream>>>(a, b, prob);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

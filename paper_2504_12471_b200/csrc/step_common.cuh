@@ -21,6 +21,9 @@ __device__ __forceinline__ float grad_scale(const float* gmax) {
   return m > 0.f ? exp2f(-ceilf(log2f(m))) : 1.f;
 }
 
+// epilogue warpgroups of the step GEMMs (GemmShape::EPI) — G4's db1 partials
+constexpr int kEpiGroups = 4;
+
 // Model/step geometry (ModelConfig, model.hpp:43-57, plus the B200 layout).
 struct Dims {
   int L, H, d, ffn, T, C;  // reference config

@@ -50,7 +50,7 @@ struct EmbedFwd {
       if (t < D.T) x0[((size_t)c.s * D.T + t) * D.d + m] = v[i] + b + p[i];
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- G1
@@ -67,9 +67,10 @@ struct G1 {
   const int* act_heads;
   const int* act_cnt;
   const float* b1;  // block l: [H][fs]
-  act_t* Y1;         // block l: [Bmax][H][T][PQ]
-  act_t* OG;         // block l: [Bmax][H][T][PO]
-  act_t* OGT;        // block l: [Bmax][H][PO][TP]
+  act_t* QKV;       // block l: [Bmax][H][T][3dh]   q|k|v, token-major (attention operands)
+  act_t* ZT;        // block l: [Bmax][H][fs][TP]   z + b1, feature-major (G4's GELU')
+  act_t* OG;        // block l: [Bmax][H][T][PO]    [O|g] token-major (G3's B)
+  act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G5's B)
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
@@ -106,29 +107,35 @@ struct G1 {
   __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
     if (!r.valid || col0 >= D.T) return;
     const size_t sh = (size_t)c.s * D.H + r.h;
-    act_t* y = Y1 + sh * D.T * D.PQ + r.f;
     if (r.f < 3 * D.dh) {  // q, k, v: fp16 operands of the attention kernels
+      act_t* y = QKV + sh * D.T * (3 * D.dh) + r.f;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (col0 + i < D.T) y[(size_t)(col0 + i) * D.PQ] = to_act(v[i]);
+        if (col0 + i < D.T) y[(size_t)(col0 + i) * (3 * D.dh)] = to_act(v[i]);
       return;
     }
     const int j = r.f - 3 * D.dh;
-    float g[16];
+    float z[16], g[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float z = v[i] + r.bias;
-      g[i] = gelu_f(z);
-      if (col0 + i < D.T) {
-        y[(size_t)(col0 + i) * D.PQ] = to_act(z);
-        OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = to_act(g[i]);
-      }
+      z[i] = v[i] + r.bias;
+      g[i] = gelu_f(z[i]);
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col0 + i < D.T) OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = to_act(g[i]);
+    act_t* zt = ZT + (sh * D.fs + j) * D.TP + col0;
     act_t* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
-    if (col0 + 8 <= D.TP) st_act_x8(gt, g);
-    if (col0 + 16 <= D.TP) st_act_x8(gt + 8, g + 8);
+    if (col0 + 8 <= D.TP) {
+      st_act_x8(zt, z);
+      st_act_x8(gt, g);
+    }
+    if (col0 + 16 <= D.TP) {
+      st_act_x8(zt + 8, z + 8);
+      st_act_x8(gt + 8, g + 8);
+    }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- G3
@@ -184,7 +191,7 @@ struct G3 {
     for (int i = 0; i < 16; ++i)
       if (col0 + i < D.T) xout[o0 + (size_t)i * D.d] = xi[i] + v[i] + r.bias;
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- G4
@@ -199,11 +206,11 @@ struct G4 {
   const int* count;
   const int* full_heads;
   const int* full_hcnt;
-  const act_t* Y1;  // block l
+  const act_t* ZT;  // block l: [Bmax][H][fs][TP]
   act_t* dO;        // [Bmax][H][T][dh]
   act_t* dY1;       // [Bmax][H][T][PQ]
   act_t* dY1T;      // [Bmax][H][PQ][TP]
-  float* part_db1; // [Bmax][H][fs]
+  float* part_db1; // [EPI][Bmax][H][fs]
   const float* gmax;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;
@@ -250,12 +257,17 @@ struct G4 {
     }
     const int j = r.f - D.dh;
     const int fq = 3 * D.dh + j;
-    const act_t* z = Y1 + sh * D.T * D.PQ + fq;
     act_t* dy = dY1 + sh * D.T * D.PQ + fq;
     float dz[16];
+    {  // z row of this feature: 16 contiguous tokens (two 16-byte loads)
+      const act_t* z = ZT + (sh * D.fs + j) * D.TP + col0;
+      __align__(16) act_t zz[16];
+      *reinterpret_cast<uint4*>(zz) = col0 + 8 <= D.TP ? *reinterpret_cast<const uint4*>(z) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(zz + 8) =
+          col0 + 16 <= D.TP ? *reinterpret_cast<const uint4*>(z + 8) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int i = 0; i < 16; ++i)  // loads first (no load->store serialisation)
-      dz[i] = col0 + i < D.T ? act_to_f(z[(size_t)(col0 + i) * D.PQ]) : 0.f;
+      for (int i = 0; i < 16; ++i) dz[i] = act_to_f(zz[i]);
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       dz[i] = col0 + i < D.T ? v[i] * gelu_grad_f(dz[i]) : 0.f;
@@ -268,9 +280,10 @@ struct G4 {
     if (col0 + 8 <= D.TP) st_act_x8(dt, dz);
     if (col0 + 16 <= D.TP) st_act_x8(dt + 8, dz + 8);
   }
-  __device__ void row_end(const Tile& c, int, Row& r) const {
+  // one partial per column group (summed in fixed order by bias_reduce)
+  __device__ void row_end(const Tile& c, int, int group, Row& r) const {
     if (r.valid && r.f >= D.dh)
-      part_db1[((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)] = r.db / grad_scale(gmax);
+      part_db1[(((size_t)group * D.Bmax + c.s) * D.H + r.h) * D.fs + (r.f - D.dh)] = r.db / grad_scale(gmax);
   }
 };
 
@@ -316,7 +329,7 @@ struct G5 {
       if (f < D.PO) out[f] = v[i] * r.inv;
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- G7
@@ -369,7 +382,7 @@ struct G7 {
         if (n0 + i < D.d) out[n0 + i] = v[i] * k;
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- G8
@@ -414,7 +427,7 @@ struct G8 {
       if (t < D.T) dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i] * r.inv;
     }
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 // ---------------------------------------------------------------- embed wgrad
@@ -457,7 +470,7 @@ struct EmbedW {
     for (int i = 0; i < 16; ++i)
       if (n0 + i < D.d) out[n0 + i] = v[i] * r.inv;
   }
-  __device__ void row_end(const Tile&, int, Row&) const {}
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
 }  // namespace d2ft_b200

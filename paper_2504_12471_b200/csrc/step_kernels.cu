@@ -7,7 +7,6 @@ namespace d2ft_b200 {
 namespace {
 
 constexpr float kLnEps = 1e-5f;  // model.hpp:32
-constexpr int kMaxVec = 32;      // d <= 1024: values per lane of a row
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -90,13 +89,14 @@ __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inp
   write_transposed(tile, pitch, D.d, t0, D.TP, inpT + (size_t)s * D.d * D.TP);
 }
 
+template <int NV>
 __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, float* stats) {
   extern __shared__ __align__(16) unsigned char smem[];
   act_t* tile = reinterpret_cast<act_t*>(smem);
   const int pitch = D.d + 2;
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = D.d / 32;
+  constexpr int nv = NV;
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
     if (t >= D.T) {
@@ -104,10 +104,10 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, flo
       continue;
     }
     const float* row = x + ((size_t)s * D.T + t) * D.d;
-    float v[kMaxVec];
+    float v[NV];
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         v[j] = row[lane + 32 * j];
         sum += v[j];
@@ -115,7 +115,7 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, flo
     const float mean = warp_sum(sum) / D.d;  // linalg.cpp:136-139, two-pass
     float sq = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         const float dv = v[j] - mean;
         sq += dv * dv;
@@ -124,7 +124,7 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, flo
     const float rstd = 1.0f / sqrtf(var + kLnEps);
     act_t* out = xn + ((size_t)s * D.T + t) * D.d;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         const act_t b = to_act((v[j] - mean) * rstd);
         out[lane + 32 * j] = b;
@@ -139,6 +139,7 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, flo
   write_transposed(tile, pitch, D.d, t0, D.TP, xnT + (size_t)s * D.d * D.TP);
 }
 
+template <int NV>
 __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
                                    const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs,
                                    const float* gmax) {
@@ -148,11 +149,11 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
   float* cs = reinterpret_cast<float*>(smem + (size_t)32 * pitch * 2 + 16);  // [8][d]
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = D.d / 32;
+  constexpr int nv = NV;
   const bool do_ln = l >= 0 && full_hcnt[s * D.L + l] > 0;  // model.cpp:508
-  float acc[kMaxVec];
+  float acc[NV];
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j) acc[j] = 0.f;
+  for (int j = 0; j < NV; ++j) acc[j] = 0.f;
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
     if (t >= D.T) {
@@ -160,16 +161,16 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
       continue;
     }
     const size_t ro = ((size_t)s * D.T + t) * D.d;
-    float v[kMaxVec];
+    float v[NV];
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) v[j] = dX[ro + lane + 32 * j];
     if (do_ln) {  // linalg.cpp:153-180
       const float mean = stats_l[((size_t)s * D.T + t) * 2], rstd = stats_l[((size_t)s * D.T + t) * 2 + 1];
-      float y[kMaxVec], dy[kMaxVec];
+      float y[NV], dy[NV];
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-      for (int j = 0; j < kMaxVec; ++j)
+      for (int j = 0; j < NV; ++j)
         if (j < nv) {
           y[j] = (x_l[ro + lane + 32 * j] - mean) * rstd;
           dy[j] = dxn[ro + lane + 32 * j];
@@ -178,15 +179,15 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
         }
       const float dmean = warp_sum(s1) / D.d, ddot = warp_sum(s2) / D.d;
 #pragma unroll
-      for (int j = 0; j < kMaxVec; ++j)
+      for (int j = 0; j < NV; ++j)
         if (j < nv) v[j] += (dy[j] - dmean - y[j] * ddot) * rstd;
 #pragma unroll
-      for (int j = 0; j < kMaxVec; ++j)
+      for (int j = 0; j < NV; ++j)
         if (j < nv) dX[ro + lane + 32 * j] = v[j];
     }
     const float S = grad_scale(gmax);  // fp16 gradient operands carry S
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         const act_t b = to_act(v[j] * S);
         dC[ro + lane + 32 * j] = b;
@@ -195,7 +196,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
       }
   }
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j)
+  for (int j = 0; j < NV; ++j)
     if (j < nv) cs[warp * D.d + lane + 32 * j] = acc[j];
   __syncthreads();
   write_transposed(tile, pitch, D.d, t0, D.TP, dCT + (size_t)s * D.d * D.TP);
@@ -210,6 +211,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
 // ------------------------------------------------------------------ head
 // LN -> mean over tokens -> linear -> cross-entropy (model.cpp:342-355,
 // 400-414, 470-492); backward to dX = dL/dx_L.  One CTA per sample.
+template <int NV>
 __global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                             double* loss_s, float* pooled_out, float* dlog_out, float* dX, float* gmax) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -220,16 +222,16 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   __shared__ float logits[64], dlog[64];
   const int s = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = D.d / 32;
-  float acc[kMaxVec];
+  constexpr int nv = NV;
+  float acc[NV];
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j) acc[j] = 0.f;
+  for (int j = 0; j < NV; ++j) acc[j] = 0.f;
   for (int t = warp; t < D.T; t += 8) {
     const float* row = xL + ((size_t)s * D.T + t) * D.d;
-    float v[kMaxVec];
+    float v[NV];
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         v[j] = row[lane + 32 * j];
         sum += v[j];
@@ -237,11 +239,11 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
     const float mean = warp_sum(sum) / D.d;
     float sq = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) sq += (v[j] - mean) * (v[j] - mean);
     const float rstd = 1.0f / sqrtf(warp_sum(sq) / D.d + kLnEps);
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) acc[j] += (v[j] - mean) * rstd;
     if (lane == 0) {
       rowstat[2 * t] = mean;
@@ -249,7 +251,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
     }
   }
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j)
+  for (int j = 0; j < NV; ++j)
     if (j < nv) part[warp * D.d + lane + 32 * j] = acc[j];
   __syncthreads();
   for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
@@ -293,10 +295,10 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   for (int t = warp; t < D.T; t += 8) {
     const size_t ro = ((size_t)s * D.T + t) * D.d;
     const float mean = rowstat[2 * t], rstd = rowstat[2 * t + 1];
-    float y[kMaxVec];
+    float y[NV];
     float s2 = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         y[j] = (xL[ro + lane + 32 * j] - mean) * rstd;
         s2 += dpooled[lane + 32 * j] * y[j];
@@ -304,7 +306,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
     const float ddot = warp_sum(s2) / D.d;
     float amax = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
       if (j < nv) {
         const float g = (dpooled[lane + 32 * j] - dmean - y[j] * ddot) * rstd;
         dX[ro + lane + 32 * j] = g;
@@ -337,25 +339,42 @@ __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* po
 }
 
 // ------------------------------------------------------------------ bias / embed reductions
+// db2 (model.cpp:250-252) and db1 (model.cpp:257) of block l: sums over the
+// Full samples of each head.  32 outputs per CTA (lane), samples split over
+// the 8 warps, warp partials combined in fixed order (deterministic).
 __global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
                                    float* db1_l, float* db2_l) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   const int ntile = (D.T + 31) / 32;
-  if (i < D.d) {  // db2 (model.cpp:250-252): Full samples of head m/(d/H)
-    const int m = i, h = m / (D.d / D.H);
-    const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
-    float a = 0.f;
-    for (int s = 0; s < D.B; ++s)
-      if (row[s] == 1)
-        for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
-    db2_l[m] = a;
-  } else if (i < D.d + D.H * D.fs) {  // db1 (model.cpp:257)
-    const int q = i - D.d, h = q / D.fs, j = q % D.fs;
-    const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
-    float a = 0.f;
-    for (int s = 0; s < D.B; ++s)
-      if (row[s] == 1) a += part_db1[((size_t)s * D.H + h) * D.fs + j];
-    db1_l[q] = a;
+  const int nout = D.d + D.H * D.fs;
+  float a = 0.f;
+  if (i < nout) {
+    if (i < D.d) {
+      const int m = i, h = m / (D.d / D.H);
+      const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
+      for (int s = warp; s < D.B; s += 8)
+        if (row[s] == 1) {
+#pragma unroll 4
+          for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
+        }
+    } else {
+      const int q = i - D.d, h = q / D.fs, j = q % D.fs;
+      const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
+      for (int s = warp; s < D.B; s += 8)
+        if (row[s] == 1)
+#pragma unroll
+          for (int e = 0; e < kEpiGroups; ++e) a += part_db1[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
+    }
+  }
+  red[warp][lane] = a;
+  __syncthreads();
+  if (warp == 0 && i < nout) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    if (i < D.d) db2_l[i] = t;
+    else db1_l[i - D.d] = t;
   }
 }
 
@@ -366,19 +385,20 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
   const int ntile = (D.T + 31) / 32;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd + td + D.d;
        i += (size_t)gridDim.x * blockDim.x) {
-    if (i < dd) {
-      float a = 0.f;
+    float a = 0.f;
+    if (i < dd) {  // dW_embed (model.cpp:514), sum of the split-K partials
+#pragma unroll 8
       for (int k = 0; k < KS; ++k) a += part[k * dd + i];
       dWeT[i] = a;
-    } else if (i < dd + td) {
+    } else if (i < dd + td) {  // dpos (model.cpp:516)
       const size_t q = i - dd;
-      float a = 0.f;
+#pragma unroll 8
       for (int s = 0; s < D.B; ++s) a += dX[(size_t)s * td + q];
       dpos[q] = a;
-    } else {
+    } else {  // db_embed (model.cpp:515)
       const int m = (int)(i - dd - td);
-      float a = 0.f;
       for (int s = 0; s < D.B; ++s)
+#pragma unroll 4
         for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
       dbe[m] = a;
     }
@@ -388,21 +408,50 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
 // ------------------------------------------------------------------ SGD / copies
 __global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner,
                            int H, const int* full_cnt, float lr, float mom, int* err) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+  // 4 consecutive elements per thread (every segment's `inner` is a multiple of 4)
+  const size_t n4 = n / 4;
+  for (size_t i4 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i4 < n4 + (n % 4 ? 1 : 0);
+       i4 += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = i4 * 4;
     if (outer > 0 && full_cnt) {
       const long long k = ((long long)i / outer) * H + ((long long)i / inner) % H;
       if (full_cnt[k] == 0) continue;  // trainer.cpp:264-268: untouched subnets keep p and v
     }
-    const float gi = g[i];
-    if (!isfinite(gi)) {
-      atomicCAS(err, 0, (int)kNumeric);  // trainer.cpp:118
-      continue;
+    if (i + 4 <= n) {
+      const float4 gi = *reinterpret_cast<const float4*>(g + i);
+      float4 vi = *reinterpret_cast<const float4*>(v + i);
+      float4 pi = *reinterpret_cast<const float4*>(p + i);
+      if (!isfinite(gi.x) || !isfinite(gi.y) || !isfinite(gi.z) || !isfinite(gi.w)) {
+        atomicCAS(err, 0, (int)kNumeric);  // trainer.cpp:118
+        continue;
+      }
+      vi.x = mom * vi.x + gi.x;  // trainer.cpp:119-120
+      vi.y = mom * vi.y + gi.y;
+      vi.z = mom * vi.z + gi.z;
+      vi.w = mom * vi.w + gi.w;
+      pi.x -= lr * vi.x;
+      pi.y -= lr * vi.y;
+      pi.z -= lr * vi.z;
+      pi.w -= lr * vi.w;
+      *reinterpret_cast<float4*>(v + i) = vi;
+      *reinterpret_cast<float4*>(p + i) = pi;
+      if (pbf) {
+        __align__(8) __half2 h[2] = {__floats2half2_rn(pi.x, pi.y), __floats2half2_rn(pi.z, pi.w)};
+        *reinterpret_cast<uint2*>(pbf + i) = *reinterpret_cast<const uint2*>(h);
+      }
+    } else {
+      for (size_t j = i; j < n; ++j) {
+        const float gi = g[j];
+        if (!isfinite(gi)) {
+          atomicCAS(err, 0, (int)kNumeric);
+          continue;
+        }
+        const float vi = mom * v[j] + gi;
+        v[j] = vi;
+        p[j] -= lr * vi;
+        if (pbf) pbf[j] = to_act(p[j]);
+      }
     }
-    const float vi = mom * v[i] + gi;  // trainer.cpp:119-120
-    v[i] = vi;
-    const float pi = p[i] - lr * vi;
-    p[i] = pi;
-    if (pbf) pbf[i] = to_act(pi);
   }
 }
 
@@ -435,11 +484,10 @@ __global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
 }
 
 // ------------------------------------------------------------------ attention (mma.sync, FA2 style)
-// One CTA per (sample, head) slot, 8 warps, 16-row strips.  q, k, v, dO are
+// One CTA per (sample, head) slot, one warp per 16-row strip.  q, k, v, dO are
 // fp16 (G1 / G4 epilogues), staged with cp.async (zero-filled past T) into
 // row-major shared tiles with a 16-byte pad (conflict-free ldmatrix); A and B
 // fragments come from ldmatrix / ldmatrix.trans, so no transposed copies.
-constexpr int kAttnWarps = 8;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -492,39 +540,41 @@ __device__ void stage_rows(const act_t* g, int pitch, int off, int T, int TQ, ac
     cp_async16(dst + t * (DH + 8) + c * 8, g + (size_t)(v ? t : 0) * pitch + off + c * 8, v);
   }
 }
-// 16 x DH fp32 fragment block of one warp -> fp16 feature-major rows
-// outT[f][t0 .. t0+15] (staged through the warp's shared scratch)
+// Scalar feature-major stores of a 16 x DH fragment block: outT[f][t0 + row]
 template <int DH>
-__device__ void store_transposed(const float (&o)[DH / 8][4], float sc, act_t* scratch, act_t* outT, int TP, int t0,
-                                 int T, int lane) {
-  const int g = lane >> 2, c = lane & 3;
+__device__ __forceinline__ void store_frag_T(const float (&o)[DH / 8][4], float sc, act_t* outT, int TP, int t0,
+                                             int T, int g, int c) {
+  const int ta = t0 + g, tb = t0 + g + 8;
 #pragma unroll
-  for (int nf = 0; nf < DH / 8; ++nf) {  // scratch[f][row], pitch 24 halves
+  for (int nf = 0; nf < DH / 8; ++nf) {
     const int f = nf * 8 + 2 * c;
-    scratch[f * 24 + g] = __float2half_rn(o[nf][0] * sc);
-    scratch[(f + 1) * 24 + g] = __float2half_rn(o[nf][1] * sc);
-    scratch[f * 24 + g + 8] = __float2half_rn(o[nf][2] * sc);
-    scratch[(f + 1) * 24 + g + 8] = __float2half_rn(o[nf][3] * sc);
-  }
-  __syncwarp();
-  for (int f = lane; f < DH; f += 32) {
-    act_t* dst = outT + (size_t)f * TP + t0;
-    const act_t* src = scratch + f * 24;
-    if (t0 + 16 <= TP) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
-      *reinterpret_cast<uint4*>(dst + 8) = *reinterpret_cast<const uint4*>(src + 8);
-    } else {
-      for (int r = 0; r < 16 && t0 + r < TP; ++r) dst[r] = src[r];
+    if (ta < T) {
+      outT[(size_t)f * TP + ta] = __float2half_rn(o[nf][0] * sc);
+      outT[(size_t)(f + 1) * TP + ta] = __float2half_rn(o[nf][1] * sc);
+    }
+    if (tb < T) {
+      outT[(size_t)f * TP + tb] = __float2half_rn(o[nf][2] * sc);
+      outT[(size_t)(f + 1) * TP + tb] = __float2half_rn(o[nf][3] * sc);
     }
   }
-  __syncwarp();
-  (void)T;
+}
+template <int DH>
+__device__ __forceinline__ void store_frag(const float (&o)[DH / 8][4], float sc, act_t* out, int pitch, int t0, int T,
+                                           int g, int c) {
+  const int ta = t0 + g, tb = t0 + g + 8;
+#pragma unroll
+  for (int nf = 0; nf < DH / 8; ++nf) {
+    const int f = nf * 8 + 2 * c;
+    if (ta < T) *reinterpret_cast<uint32_t*>(out + (size_t)ta * pitch + f) = pack2(o[nf][0] * sc, o[nf][1] * sc);
+    if (tb < T) *reinterpret_cast<uint32_t*>(out + (size_t)tb * pitch + f) = pack2(o[nf][2] * sc, o[nf][3] * sc);
+  }
 }
 
+// Forward: one warp per 16-query strip (blockDim = 32 * TQ/16), online softmax
+// over 32-key chunks.
 template <int DH>
-__global__ void __launch_bounds__(kAttnWarps * 32) attn_fwd_kernel(Dims D, int l, const int* act_heads,
-                                                                  const int* act_cnt, const act_t* Y1, act_t* OG,
-                                                                  act_t* OGT, float* lse) {
+__global__ void __launch_bounds__(512) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
+                                                       const act_t* QKV, act_t* OG, act_t* OGT, float* lse) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
   const int h = act_heads[(s * D.L + l) * D.H + a];
@@ -534,259 +584,173 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_fwd_kernel(Dims D, int l
   act_t* Qs = reinterpret_cast<act_t*>(smem);  // [TQ][P]
   act_t* Ks = Qs + TQ * P;
   act_t* Vs = Ks + TQ * P;
-  act_t* scr = Vs + TQ * P;  // kAttnWarps x [DH][24]
   const size_t sh = (size_t)s * D.H + h;
-  const act_t* y = Y1 + sh * D.T * D.PQ;
-  stage_rows<DH>(y, D.PQ, 0, D.T, TQ, Qs);
-  stage_rows<DH>(y, D.PQ, DH, D.T, TQ, Ks);
-  stage_rows<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs);
+  const act_t* y = QKV + sh * D.T * (3 * DH);
+  stage_rows<DH>(y, 3 * DH, 0, D.T, TQ, Qs);
+  stage_rows<DH>(y, 3 * DH, DH, D.T, TQ, Ks);
+  stage_rows<DH>(y, 3 * DH, 2 * DH, D.T, TQ, Vs);
   cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
-  act_t* myscr = scr + warp * DH * 24;
   const float sl2 = kLog2e / sqrtf((float)DH);  // 1/sqrt(dh) (model.cpp:213) in log2 units
-  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
-    const int r0 = strip * 16;
-    uint32_t qa[DH / 16][4];
+  const int r0 = warp * 16;
+  uint32_t qa[DH / 16][4];
 #pragma unroll
-    for (int ks = 0; ks < DH / 16; ++ks) frag_a(qa[ks], Qs, P, r0, ks * 16, lane);
-    float o[DH / 8][4];
+  for (int ks = 0; ks < DH / 16; ++ks) frag_a(qa[ks], Qs, P, r0, ks * 16, lane);
+  float o[DH / 8][4];
 #pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) o[nf][0] = o[nf][1] = o[nf][2] = o[nf][3] = 0.f;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    for (int kc = 0; kc < TQ; kc += 64) {
-      float sc[8][4];
+  for (int nf = 0; nf < DH / 8; ++nf) o[nf][0] = o[nf][1] = o[nf][2] = o[nf][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  for (int kc = 0; kc < TQ; kc += 32) {
+    float sc[4][4];
 #pragma unroll
-      for (int np = 0; np < 4; ++np) {  // pairs of n8 key tiles
+    for (int np = 0; np < 2; ++np) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) sc[2 * np][e] = sc[2 * np + 1][e] = 0.f;
-        if (kc + np * 16 < TQ) {
+      for (int e = 0; e < 4; ++e) sc[2 * np][e] = sc[2 * np + 1][e] = 0.f;
+      if (kc + np * 16 < TQ) {
 #pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b[4];
-            frag_b_n(b, Ks, P, kc + np * 16, ks * 16, lane);
-            mma16816(sc[2 * np], qa[ks], b[0], b[1]);
-            mma16816(sc[2 * np + 1], qa[ks], b[2], b[3]);
-          }
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const int key = kc + nt * 8 + 2 * c;
-        sc[nt][0] = key < D.T ? sc[nt][0] * sl2 : -INFINITY;
-        sc[nt][1] = key + 1 < D.T ? sc[nt][1] * sl2 : -INFINITY;
-        sc[nt][2] = key < D.T ? sc[nt][2] * sl2 : -INFINITY;
-        sc[nt][3] = key + 1 < D.T ? sc[nt][3] * sl2 : -INFINITY;
-      }
-      float mx0 = m0, mx1 = m1;
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
-        mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
-      }
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-      const float cr0 = m0 == -INFINITY ? 0.f : exp2f(m0 - mx0);
-      const float cr1 = m1 == -INFINITY ? 0.f : exp2f(m1 - mx1);
-      m0 = mx0;
-      m1 = mx1;
-      l0 *= cr0;
-      l1 *= cr1;
-#pragma unroll
-      for (int nf = 0; nf < DH / 8; ++nf) {
-        o[nf][0] *= cr0;
-        o[nf][1] *= cr0;
-        o[nf][2] *= cr1;
-        o[nf][3] *= cr1;
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        sc[nt][0] = exp2f(sc[nt][0] - m0);
-        sc[nt][1] = exp2f(sc[nt][1] - m0);
-        sc[nt][2] = exp2f(sc[nt][2] - m1);
-        sc[nt][3] = exp2f(sc[nt][3] - m1);
-        l0 += sc[nt][0] + sc[nt][1];
-        l1 += sc[nt][2] + sc[nt][3];
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (kc + j * 16 < TQ) {
-          uint32_t pa[4] = {pack2(sc[2 * j][0], sc[2 * j][1]), pack2(sc[2 * j][2], sc[2 * j][3]),
-                            pack2(sc[2 * j + 1][0], sc[2 * j + 1][1]), pack2(sc[2 * j + 1][2], sc[2 * j + 1][3])};
-#pragma unroll
-          for (int nf = 0; nf < DH / 8; nf += 2) {
-            uint32_t b[4];
-            frag_b_k(b, Vs, P, nf * 8, kc + j * 16, lane);
-            mma16816(o[nf], pa, b[0], b[1]);
-            mma16816(o[nf + 1], pa, b[2], b[3]);
-          }
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          uint32_t b[4];
+          frag_b_n(b, Ks, P, kc + np * 16, ks * 16, lane);
+          mma16816(sc[2 * np], qa[ks], b[0], b[1]);
+          mma16816(sc[2 * np + 1], qa[ks], b[2], b[3]);
         }
       }
     }
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int key = kc + nt * 8 + 2 * c;
+      sc[nt][0] = key < D.T ? sc[nt][0] * sl2 : -INFINITY;
+      sc[nt][1] = key + 1 < D.T ? sc[nt][1] * sl2 : -INFINITY;
+      sc[nt][2] = key < D.T ? sc[nt][2] * sl2 : -INFINITY;
+      sc[nt][3] = key + 1 < D.T ? sc[nt][3] * sl2 : -INFINITY;
+    }
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float cr0 = m0 == -INFINITY ? 0.f : exp2f(m0 - mx0);
+    const float cr1 = m1 == -INFINITY ? 0.f : exp2f(m1 - mx1);
+    m0 = mx0;
+    m1 = mx1;
+    l0 *= cr0;
+    l1 *= cr1;
 #pragma unroll
     for (int nf = 0; nf < DH / 8; ++nf) {
-      o[nf][0] *= i0;
-      o[nf][1] *= i0;
-      o[nf][2] *= i1;
-      o[nf][3] *= i1;
+      o[nf][0] *= cr0;
+      o[nf][1] *= cr0;
+      o[nf][2] *= cr1;
+      o[nf][3] *= cr1;
     }
-    const int t0 = r0 + g, t1 = r0 + g + 8;
-    act_t* og = OG + sh * D.T * D.PO;
 #pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) {
-      const int f = nf * 8 + 2 * c;
-      if (t0 < D.T) *reinterpret_cast<uint32_t*>(og + (size_t)t0 * D.PO + f) = pack2(o[nf][0], o[nf][1]);
-      if (t1 < D.T) *reinterpret_cast<uint32_t*>(og + (size_t)t1 * D.PO + f) = pack2(o[nf][2], o[nf][3]);
+    for (int nt = 0; nt < 4; ++nt) {
+      sc[nt][0] = exp2f(sc[nt][0] - m0);
+      sc[nt][1] = exp2f(sc[nt][1] - m0);
+      sc[nt][2] = exp2f(sc[nt][2] - m1);
+      sc[nt][3] = exp2f(sc[nt][3] - m1);
+      l0 += sc[nt][0] + sc[nt][1];
+      l1 += sc[nt][2] + sc[nt][3];
     }
-    store_transposed<DH>(o, 1.f, myscr, OGT + sh * D.PO * D.TP, D.TP, r0, D.T, lane);
-    if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
-      if (t0 < D.T) lse[sh * D.T + t0] = m0 + log2f(l0);
-      if (t1 < D.T) lse[sh * D.T + t1] = m1 + log2f(l1);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (kc + j * 16 < TQ) {
+        uint32_t pa[4] = {pack2(sc[2 * j][0], sc[2 * j][1]), pack2(sc[2 * j][2], sc[2 * j][3]),
+                          pack2(sc[2 * j + 1][0], sc[2 * j + 1][1]), pack2(sc[2 * j + 1][2], sc[2 * j + 1][3])};
+#pragma unroll
+        for (int nf = 0; nf < DH / 8; nf += 2) {
+          uint32_t b[4];
+          frag_b_k(b, Vs, P, nf * 8, kc + j * 16, lane);
+          mma16816(o[nf], pa, b[0], b[1]);
+          mma16816(o[nf + 1], pa, b[2], b[3]);
+        }
+      }
     }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+  for (int nf = 0; nf < DH / 8; ++nf) {
+    o[nf][0] *= i0;
+    o[nf][1] *= i0;
+    o[nf][2] *= i1;
+    o[nf][3] *= i1;
+  }
+  store_frag<DH>(o, 1.f, OG + sh * D.T * D.PO, D.PO, r0, D.T, g, c);
+  store_frag_T<DH>(o, 1.f, OGT + sh * D.PO * D.TP, D.TP, r0, D.T, g, c);
+  if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
+    if (r0 + g < D.T) lse[sh * D.T + r0 + g] = m0 + log2f(l0);
+    if (r0 + g + 8 < D.T) lse[sh * D.T + r0 + g + 8] = m1 + log2f(l1);
   }
 }
 
-// Backward (model.cpp:262-271).  Pass B (query strips) first: D_i =
-// rowdot(P_i, dP_i) from the very P and dP used for dS (softmax_rows_backward,
-// linalg.cpp:118-128), then dQ.  Pass A (key strips): dK, dV.
+// A fragment (16x16 at (i0, k0)) of A[i][k] held transposed as X[k][i]
+__device__ __forceinline__ void frag_a_t(uint32_t (&a)[4], const act_t* X, int P, int i0, int k0, int lane) {
+  ldsm_x4_t(a, X + (size_t)(k0 + (lane & 7) + ((lane >> 4) << 3)) * P + i0 + ((lane >> 3) & 1) * 8);
+}
+
+// Backward (model.cpp:262-271), FA2 order, deterministic.  D_i = rowsum(dO.O)
+// (fp16 O; == rowdot(P, dP) of softmax_rows_backward, linalg.cpp:118-128).
+// Phase 1, one warp per 16-key strip: S^T, P^T, dP^T, dS^T -> dV, dK, and
+// dS^T kept in shared memory; phase 2, one warp per 16-query strip: dQ = dS.K.
 template <int DH>
-__global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_kernel(Dims D, int l, const int* full_heads,
-                                                                  const int* full_hcnt, const act_t* Y1,
-                                                                  const act_t* dO, const float* lse, act_t* dY1,
-                                                                  act_t* dY1T) {
+__global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
+                                                       const act_t* QKV, const act_t* OG, const act_t* dO,
+                                                       const float* lse, act_t* dY1, act_t* dY1T) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
   const int h = full_heads[(s * D.L + l) * D.H + a];
   extern __shared__ __align__(16) unsigned char smem[];
   const int TQ = D.TQ;
   constexpr int P = DH + 8;
+  const int PS = TQ + 8;
   act_t* Qs = reinterpret_cast<act_t*>(smem);
   act_t* Ks = Qs + TQ * P;
   act_t* Vs = Ks + TQ * P;
   act_t* dOs = Vs + TQ * P;
-  act_t* scr = dOs + TQ * P;  // kAttnWarps x [DH][24]
-  float* Dv = reinterpret_cast<float*>(scr + kAttnWarps * DH * 24);
+  act_t* dST = dOs + TQ * P;  // [TQ keys][TQ+8 queries]
+  float* Dv = reinterpret_cast<float*>(dST + TQ * PS);
   float* L2 = Dv + TQ;
   const size_t sh = (size_t)s * D.H + h;
-  const act_t* y = Y1 + sh * D.T * D.PQ;
-  stage_rows<DH>(y, D.PQ, 0, D.T, TQ, Qs);
-  stage_rows<DH>(y, D.PQ, DH, D.T, TQ, Ks);
-  stage_rows<DH>(y, D.PQ, 2 * DH, D.T, TQ, Vs);
+  const act_t* y = QKV + sh * D.T * (3 * DH);
+  stage_rows<DH>(y, 3 * DH, 0, D.T, TQ, Qs);
+  stage_rows<DH>(y, 3 * DH, DH, D.T, TQ, Ks);
+  stage_rows<DH>(y, 3 * DH, 2 * DH, D.T, TQ, Vs);
   stage_rows<DH>(dO + sh * D.T * D.dh, D.dh, 0, D.T, TQ, dOs);
-  for (int t = threadIdx.x; t < TQ; t += blockDim.x) L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
+  {  // D_i and L2_i for this warp's 16 rows (rows >= T: D = 0, L2 = +inf -> P = 0)
+    const act_t* og = OG + sh * D.T * D.PO;
+    const act_t* dog = dO + sh * D.T * D.dh;
+    for (int r = 0; r < 16; ++r) {
+      const int t = warp * 16 + r;
+      float acc = 0.f;
+      if (t < D.T)
+        for (int f = lane; f < DH; f += 32)
+          acc += __half2float(dog[(size_t)t * D.dh + f]) * __half2float(og[(size_t)t * D.PO + f]);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        Dv[t] = acc;
+        L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+      }
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
-  act_t* myscr = scr + warp * DH * 24;
   const float sl2 = kLog2e / sqrtf((float)DH);
   const float scale = 1.0f / sqrtf((float)DH);
   act_t* dy = dY1 + sh * D.T * D.PQ;
   act_t* dyt = dY1T + sh * D.PQ * D.TP;
 
-  // ---- pass B: query strip i -> D_i, dQ_i
-  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
-    const int r0 = strip * 16;
-    uint32_t qa[DH / 16][4], oa[DH / 16][4];
-#pragma unroll
-    for (int ks = 0; ks < DH / 16; ++ks) {
-      frag_a(qa[ks], Qs, P, r0, ks * 16, lane);
-      frag_a(oa[ks], dOs, P, r0, ks * 16, lane);
-    }
-    const float l20 = L2[r0 + g], l21 = L2[r0 + g + 8];
-    float d0 = 0.f, d1 = 0.f;
-    for (int sweep = 0; sweep < 2; ++sweep) {
-      float dq[DH / 8][4];
-#pragma unroll
-      for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
-      for (int kc = 0; kc < TQ; kc += 64) {
-        float ds[8][4];
-#pragma unroll
-        for (int np = 0; np < 4; ++np) {
-          float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};
-          float dp0[4] = {0.f, 0.f, 0.f, 0.f}, dp1[4] = {0.f, 0.f, 0.f, 0.f};
-          if (kc + np * 16 < TQ) {
-#pragma unroll
-            for (int ks = 0; ks < DH / 16; ++ks) {
-              uint32_t b[4];
-              frag_b_n(b, Ks, P, kc + np * 16, ks * 16, lane);
-              mma16816(st0, qa[ks], b[0], b[1]);
-              mma16816(st1, qa[ks], b[2], b[3]);
-              frag_b_n(b, Vs, P, kc + np * 16, ks * 16, lane);
-              mma16816(dp0, oa[ks], b[0], b[1]);
-              mma16816(dp1, oa[ks], b[2], b[3]);
-            }
-          }
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const float* st = hh ? st1 : st0;
-            const float* dp = hh ? dp1 : dp0;
-            const int key = kc + np * 16 + hh * 8 + 2 * c;
-            const bool ka = key < D.T, kb = key + 1 < D.T;
-            const float p0 = ka ? exp2f(st[0] * sl2 - l20) : 0.f, p1 = kb ? exp2f(st[1] * sl2 - l20) : 0.f;
-            const float p2 = ka ? exp2f(st[2] * sl2 - l21) : 0.f, p3 = kb ? exp2f(st[3] * sl2 - l21) : 0.f;
-            if (sweep == 0) {
-              d0 += p0 * dp[0] + p1 * dp[1];
-              d1 += p2 * dp[2] + p3 * dp[3];
-            }
-            ds[2 * np + hh][0] = p0 * (dp[0] - d0);
-            ds[2 * np + hh][1] = p1 * (dp[1] - d0);
-            ds[2 * np + hh][2] = p2 * (dp[2] - d1);
-            ds[2 * np + hh][3] = p3 * (dp[3] - d1);
-          }
-        }
-        if (sweep == 1) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (kc + j * 16 < TQ) {
-              uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
-                                pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]),
-                                pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
-#pragma unroll
-              for (int nf = 0; nf < DH / 8; nf += 2) {
-                uint32_t b[4];
-                frag_b_k(b, Ks, P, nf * 8, kc + j * 16, lane);
-                mma16816(dq[nf], sa, b[0], b[1]);
-                mma16816(dq[nf + 1], sa, b[2], b[3]);
-              }
-            }
-          }
-        }
-      }
-      if (sweep == 0) {
-        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
-        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
-        if (c == 0) {
-          Dv[r0 + g] = d0;
-          Dv[r0 + g + 8] = d1;
-        }
-      } else {
-        const int t0 = r0 + g, t1 = r0 + g + 8;
-#pragma unroll
-        for (int nf = 0; nf < DH / 8; ++nf) {
-          const int f = nf * 8 + 2 * c;
-          if (t0 < D.T)
-            *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + f) = pack2(dq[nf][0] * scale, dq[nf][1] * scale);
-          if (t1 < D.T)
-            *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + f) = pack2(dq[nf][2] * scale, dq[nf][3] * scale);
-        }
-        store_transposed<DH>(dq, scale, myscr, dyt, D.TP, r0, D.T, lane);
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- pass A: key strip j -> dK_j, dV_j
-  for (int strip = warp; strip < TQ / 16; strip += kAttnWarps) {
-    const int k0 = strip * 16;
+  {  // ---- phase 1: key strip -> dK, dV, dS^T
+    const int k0 = warp * 16;
     uint32_t ka_[DH / 16][4], va[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
@@ -799,85 +763,93 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_kernel(Dims D, int l
 #pragma unroll
       for (int e = 0; e < 4; ++e) dk[nf][e] = dv[nf][e] = 0.f;
     const bool key0 = k0 + g < D.T, key1 = k0 + g + 8 < D.T;
-    for (int qc = 0; qc < TQ; qc += 64) {
-      float pt[8][4], ds[8][4];
+    for (int qc = 0; qc < TQ; qc += 16) {
+      float st[2][4] = {}, dp[2][4] = {};
 #pragma unroll
-      for (int np = 0; np < 4; ++np) {
-        float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};
-        float dp0[4] = {0.f, 0.f, 0.f, 0.f}, dp1[4] = {0.f, 0.f, 0.f, 0.f};
-        if (qc + np * 16 < TQ) {
-#pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            uint32_t b[4];
-            frag_b_n(b, Qs, P, qc + np * 16, ks * 16, lane);
-            mma16816(st0, ka_[ks], b[0], b[1]);
-            mma16816(st1, ka_[ks], b[2], b[3]);
-            frag_b_n(b, dOs, P, qc + np * 16, ks * 16, lane);
-            mma16816(dp0, va[ks], b[0], b[1]);
-            mma16816(dp1, va[ks], b[2], b[3]);
-          }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const float* st = hh ? st1 : st0;
-          const float* dp = hh ? dp1 : dp0;
-          const int q = qc + np * 16 + hh * 8 + 2 * c;
-          const float l2a = q < TQ ? L2[q] : INFINITY, l2b = q + 1 < TQ ? L2[q + 1] : INFINITY;
-          const float da = q < TQ ? Dv[q] : 0.f, db = q + 1 < TQ ? Dv[q + 1] : 0.f;
-          float* P_ = pt[2 * np + hh];
-          float* S_ = ds[2 * np + hh];
-          P_[0] = key0 ? exp2f(st[0] * sl2 - l2a) : 0.f;
-          P_[1] = key0 ? exp2f(st[1] * sl2 - l2b) : 0.f;
-          P_[2] = key1 ? exp2f(st[2] * sl2 - l2a) : 0.f;
-          P_[3] = key1 ? exp2f(st[3] * sl2 - l2b) : 0.f;
-          S_[0] = P_[0] * (dp[0] - da);
-          S_[1] = P_[1] * (dp[1] - db);
-          S_[2] = P_[2] * (dp[2] - da);
-          S_[3] = P_[3] * (dp[3] - db);
-        }
+      for (int ks = 0; ks < DH / 16; ++ks) {
+        uint32_t b[4];
+        frag_b_n(b, Qs, P, qc, ks * 16, lane);
+        mma16816(st[0], ka_[ks], b[0], b[1]);
+        mma16816(st[1], ka_[ks], b[2], b[3]);
+        frag_b_n(b, dOs, P, qc, ks * 16, lane);
+        mma16816(dp[0], va[ks], b[0], b[1]);
+        mma16816(dp[1], va[ks], b[2], b[3]);
       }
+      float pt[2][4], ds[2][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (qc + j * 16 < TQ) {
-          uint32_t pa[4] = {pack2(pt[2 * j][0], pt[2 * j][1]), pack2(pt[2 * j][2], pt[2 * j][3]),
-                            pack2(pt[2 * j + 1][0], pt[2 * j + 1][1]), pack2(pt[2 * j + 1][2], pt[2 * j + 1][3])};
-          uint32_t sa[4] = {pack2(ds[2 * j][0], ds[2 * j][1]), pack2(ds[2 * j][2], ds[2 * j][3]),
-                            pack2(ds[2 * j + 1][0], ds[2 * j + 1][1]), pack2(ds[2 * j + 1][2], ds[2 * j + 1][3])};
+      for (int hh = 0; hh < 2; ++hh) {
+        const int q = qc + hh * 8 + 2 * c;
+        const float l2a = L2[q], l2b = L2[q + 1], da = Dv[q], db = Dv[q + 1];
+        pt[hh][0] = key0 ? exp2f(st[hh][0] * sl2 - l2a) : 0.f;
+        pt[hh][1] = key0 ? exp2f(st[hh][1] * sl2 - l2b) : 0.f;
+        pt[hh][2] = key1 ? exp2f(st[hh][2] * sl2 - l2a) : 0.f;
+        pt[hh][3] = key1 ? exp2f(st[hh][3] * sl2 - l2b) : 0.f;
+        ds[hh][0] = pt[hh][0] * (dp[hh][0] - da);
+        ds[hh][1] = pt[hh][1] * (dp[hh][1] - db);
+        ds[hh][2] = pt[hh][2] * (dp[hh][2] - da);
+        ds[hh][3] = pt[hh][3] * (dp[hh][3] - db);
+        *reinterpret_cast<uint32_t*>(dST + (size_t)(k0 + g) * PS + q) = pack2(ds[hh][0], ds[hh][1]);
+        *reinterpret_cast<uint32_t*>(dST + (size_t)(k0 + g + 8) * PS + q) = pack2(ds[hh][2], ds[hh][3]);
+      }
+      const uint32_t pa[4] = {pack2(pt[0][0], pt[0][1]), pack2(pt[0][2], pt[0][3]), pack2(pt[1][0], pt[1][1]),
+                              pack2(pt[1][2], pt[1][3])};
+      const uint32_t sa[4] = {pack2(ds[0][0], ds[0][1]), pack2(ds[0][2], ds[0][3]), pack2(ds[1][0], ds[1][1]),
+                              pack2(ds[1][2], ds[1][3])};
 #pragma unroll
-          for (int nf = 0; nf < DH / 8; nf += 2) {
-            uint32_t b[4];
-            frag_b_k(b, dOs, P, nf * 8, qc + j * 16, lane);
-            mma16816(dv[nf], pa, b[0], b[1]);
-            mma16816(dv[nf + 1], pa, b[2], b[3]);
-            frag_b_k(b, Qs, P, nf * 8, qc + j * 16, lane);
-            mma16816(dk[nf], sa, b[0], b[1]);
-            mma16816(dk[nf + 1], sa, b[2], b[3]);
-          }
-        }
+      for (int nf = 0; nf < DH / 8; nf += 2) {
+        uint32_t b[4];
+        frag_b_k(b, dOs, P, nf * 8, qc, lane);
+        mma16816(dv[nf], pa, b[0], b[1]);
+        mma16816(dv[nf + 1], pa, b[2], b[3]);
+        frag_b_k(b, Qs, P, nf * 8, qc, lane);
+        mma16816(dk[nf], sa, b[0], b[1]);
+        mma16816(dk[nf + 1], sa, b[2], b[3]);
       }
     }
-    const int t0 = k0 + g, t1 = k0 + g + 8;
+    store_frag<DH>(dk, scale, dy + DH, D.PQ, k0, D.T, g, c);
+    store_frag<DH>(dv, 1.f, dy + 2 * DH, D.PQ, k0, D.T, g, c);
+    store_frag_T<DH>(dk, scale, dyt + (size_t)DH * D.TP, D.TP, k0, D.T, g, c);
+    store_frag_T<DH>(dv, 1.f, dyt + (size_t)2 * DH * D.TP, D.TP, k0, D.T, g, c);
+  }
+  __syncthreads();
+  {  // ---- phase 2: query strip -> dQ = dS . K
+    const int i0 = warp * 16;
+    float dq[DH / 8][4];
 #pragma unroll
-    for (int nf = 0; nf < DH / 8; ++nf) {
-      const int f = nf * 8 + 2 * c;
-      if (t0 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + DH + f) = pack2(dk[nf][0] * scale, dk[nf][1] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t0 * D.PQ + 2 * DH + f) = pack2(dv[nf][0], dv[nf][1]);
-      }
-      if (t1 < D.T) {
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + DH + f) = pack2(dk[nf][2] * scale, dk[nf][3] * scale);
-        *reinterpret_cast<uint32_t*>(dy + (size_t)t1 * D.PQ + 2 * DH + f) = pack2(dv[nf][2], dv[nf][3]);
+    for (int nf = 0; nf < DH / 8; ++nf) dq[nf][0] = dq[nf][1] = dq[nf][2] = dq[nf][3] = 0.f;
+    for (int kc = 0; kc < TQ; kc += 16) {
+      uint32_t sa[4];
+      frag_a_t(sa, dST, PS, i0, kc, lane);
+#pragma unroll
+      for (int nf = 0; nf < DH / 8; nf += 2) {
+        uint32_t b[4];
+        frag_b_k(b, Ks, P, nf * 8, kc, lane);
+        mma16816(dq[nf], sa, b[0], b[1]);
+        mma16816(dq[nf + 1], sa, b[2], b[3]);
       }
     }
-    store_transposed<DH>(dk, scale, myscr, dyt + (size_t)DH * D.TP, D.TP, k0, D.T, lane);
-    store_transposed<DH>(dv, 1.f, myscr, dyt + (size_t)2 * DH * D.TP, D.TP, k0, D.T, lane);
+    store_frag<DH>(dq, scale, dy, D.PQ, i0, D.T, g, c);
+    store_frag_T<DH>(dq, scale, dyt, D.TP, i0, D.T, g, c);
   }
 }
 
-size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(3 * TQ * (DH + 8) + kAttnWarps * DH * 24) * 2; }
+size_t attn_fwd_smem(int DH, int TQ) { return (size_t)(3 * TQ * (DH + 8)) * 2; }
 size_t attn_bwd_smem(int DH, int TQ) {
-  return (size_t)(4 * TQ * (DH + 8) + kAttnWarps * DH * 24) * 2 + (size_t)2 * TQ * 4;
+  return (size_t)(4 * TQ * (DH + 8) + TQ * (TQ + 8)) * 2 + (size_t)2 * TQ * 4;
 }
+
+// d = 32 * NV: instantiate the row kernels for the supported model widths
+#define D2FT_NV_DISPATCH(d, ...)                                                     \
+  do {                                                                              \
+    switch ((d) / 32) {                                                             \
+      case 4: { constexpr int NV = 4; __VA_ARGS__ } break;                          \
+      case 8: { constexpr int NV = 8; __VA_ARGS__ } break;                          \
+      case 16: { constexpr int NV = 16; __VA_ARGS__ } break;                        \
+      case 24: { constexpr int NV = 24; __VA_ARGS__ } break;                        \
+      case 32: { constexpr int NV = 32; __VA_ARGS__ } break;                        \
+      default: throw Fail{kConfig, "row kernels: model_dim must be 128, 256, 512, 768 or 1024"}; \
+    }                                                                               \
+  } while (0)
 
 int grid_for(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
@@ -918,8 +890,10 @@ void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, c
 void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D);
-  D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  ln_fwd_kernel<<<grid, 256, sm, st>>>(D, x, xn, xnT, stats);
+  D2FT_NV_DISPATCH(D.d, {
+    D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ln_fwd_kernel<NV><<<grid, 256, sm, st>>>(D, x, xn, xnT, stats);
+  });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -929,8 +903,10 @@ void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float*
                         cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D) + (size_t)8 * D.d * 4;
-  D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  ln_bwd_prep_kernel<<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs, gmax);
+  D2FT_NV_DISPATCH(D.d, {
+    D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs, gmax);
+  });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -941,12 +917,12 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
   if (D.dh == 64) {
     const size_t sm = attn_fwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<64><<<grid, kAttnWarps * 32, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
     count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_fwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<32><<<grid, kAttnWarps * 32, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
@@ -960,12 +936,12 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
   if (D.dh == 64) {
     const size_t sm = attn_bwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<64><<<grid, kAttnWarps * 32, sm, st>>>(D, l, full_heads, full_hcnt, Y1, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
     count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_bwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<32><<<grid, kAttnWarps * 32, sm, st>>>(D, l, full_heads, full_hcnt, Y1, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
@@ -977,8 +953,10 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
   const size_t sm = (size_t)(10 * D.d + 2 * D.T) * 4;
-  D2FT_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  head_kernel<<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
+  D2FT_NV_DISPATCH(D.d, {
+    D2FT_CUDA(cudaFuncSetAttribute(head_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    head_kernel<NV><<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
+  });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -994,7 +972,7 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
 void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
                         float* db1_l, float* db2_l, cudaStream_t st) {
   const int n = D.d + D.H * D.fs;
-  bias_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
+  bias_reduce_kernel<<<(n + 31) / 32, 256, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -1002,7 +980,7 @@ void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float*
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
                          float* dbe, float* dpos, cudaStream_t st) {
   const size_t n = (size_t)D.d * D.d + (size_t)D.T * D.d + D.d;
-  embed_reduce_kernel<<<grid_for(n, 256), 256, 0, st>>>(D, KS, part, part_cs, dX, dWeT, dbe, dpos);
+  embed_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(D, KS, part, part_cs, dX, dWeT, dbe, dpos);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -1010,7 +988,7 @@ void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* 
 void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner, int H,
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st) {
   if (!n) return;
-  sgd_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, v, g, pbf, n, outer, inner, H, full_cnt, lr, mom, err);
+  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, st>>>(p, v, g, pbf, n, outer, inner, H, full_cnt, lr, mom, err);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
