@@ -71,6 +71,11 @@ int d2ft_scaler_schedule(const double* bwd, const double* fwd, const int32_t* cf
                          const int32_t* total_cap, int K, int N, int mode, double lambda, uint8_t* codes_out,
                          double* lambda_used, int* fell_back);
 
+/* brute_force_schedule — scheduler.hpp:162-163, scheduler.cpp:248-302:
+ * exhaustive per-row optimum over 3^N assignments (N <= 14, else status 6). */
+int d2ft_brute_force_schedule(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                              const int32_t* cap_full, const int32_t* cap_fwd, int K, int N, uint8_t* codes_out);
+
 /* Compaction of a code table (the implicit skips of model.cpp:431-436,
  * 455-466, 499-508 made explicit).  H = heads per block (K % H == 0),
  * L = K / H.  Outputs (host):

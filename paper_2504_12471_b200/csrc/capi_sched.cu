@@ -355,6 +355,32 @@ int d2ft_scaler_schedule(const double* bwd, const double* fwd, const int32_t* cf
   });
 }
 
+int d2ft_brute_force_schedule(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                              const int32_t* cap_full, const int32_t* cap_fwd, int K, int N, uint8_t* codes_out) {
+  return guarded([&] {
+    D2FT_REQUIRE(K >= 0 && N >= 0, kInput, "brute_force_schedule: negative dimensions");
+    const size_t KN = (size_t)K * N;
+    validate_scores(bwd, fwd, KN);  // scheduler.cpp:250
+    for (int k = 0; k < K; ++k) D2FT_REQUIRE(cap_full[k] >= 0, kInput, "capacities: negative full capacity");
+    for (int k = 0; k < K; ++k) D2FT_REQUIRE(cap_fwd[k] >= 0, kInput, "capacities: negative forward capacity");
+    D2FT_REQUIRE(N <= 14, kSize,
+                 "brute_force_schedule: " + std::to_string(N) + " micro-batches exceeds the 3^N enumeration bound (N <= 14)");
+    if (K == 0) return;
+    DevBuf<double> d_b(KN ? KN : 1), d_f(KN ? KN : 1);
+    DevBuf<int32_t> d_cf(K), d_cb(K), d_cfu(K), d_cfw(K);
+    DevBuf<uint8_t> d_codes(KN ? KN : 1);
+    d_b.upload(bwd, KN);
+    d_f.upload(fwd, KN);
+    d_cf.upload(cf, K);
+    d_cb.upload(cb, K);
+    d_cfu.upload(cap_full, K);
+    d_cfw.upload(cap_fwd, K);
+    launch_brute_force(d_b.p, d_f.p, d_cf.p, d_cb.p, d_cfu.p, d_cfw.p, K, N, d_codes.p, nullptr);
+    D2FT_CUDA(cudaDeviceSynchronize());
+    d_codes.download(codes_out, KN);
+  });
+}
+
 int d2ft_compact(const uint8_t* codes, int K, int N, int H, int32_t* fwd_idx, int32_t* fwd_cnt, int32_t* full_idx,
                  int32_t* full_cnt, int32_t* act_heads, int32_t* act_cnt, int32_t* full_heads, int32_t* full_hcnt) {
   return guarded([&] {

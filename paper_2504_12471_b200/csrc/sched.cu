@@ -406,7 +406,77 @@ __global__ void __launch_bounds__(kThreads) scaler_kernel(const double* bwd, con
   }
 }
 
+// brute_force_schedule (scheduler.cpp:248-302): one CTA per row enumerates
+// all 3^N assignments (digit 0 = p_s, 1 = p_o, 2 = p_f; value summed in item
+// order with the reference's early exit on cost > cap), keeping the maximum
+// value and, among equal values, the smallest assignment index — exactly the
+// reference's sequential "first found strict maximum".
+__global__ void __launch_bounds__(kThreads) brute_kernel(const double* bwd, const double* fwd, const int32_t* cf,
+                                                         const int32_t* cb, const int32_t* cap_full,
+                                                         const int32_t* cap_fwd, int N, int total, uint8_t* codes) {
+  const int k = blockIdx.x;
+  const int cap = cap_full[k] + cap_fwd[k];
+  const int c_full = cf[k] + cb[k], c_fwd = cf[k];
+  const double* b = bwd + (size_t)k * N;
+  const double* f = fwd + (size_t)k * N;
+  double best = -1.0;
+  int best_a = 0x7fffffff;
+  for (int a = threadIdx.x; a < total; a += blockDim.x) {
+    int cost = 0, rest = a;
+    double value = 0.0;
+    for (int i = 0; i < N && cost <= cap; ++i) {
+      const int digit = rest % 3;
+      rest /= 3;
+      if (digit == 2) {
+        cost += c_full;
+        value = __dadd_rn(value, __dadd_rn(b[i], f[i]));
+      } else if (digit == 1) {
+        cost += c_fwd;
+        value = __dadd_rn(value, f[i]);
+      }
+    }
+    if (cost <= cap && (value > best || (value == best && a < best_a))) {
+      best = value;
+      best_a = a;
+    }
+  }
+  __shared__ double sv[kThreads];
+  __shared__ int sa[kThreads];
+  sv[threadIdx.x] = best;
+  sa[threadIdx.x] = best_a;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int a2 = sa[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && a2 < sa[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        sa[threadIdx.x] = a2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int rest = sa[0] == 0x7fffffff ? 0 : sa[0];
+    for (int i = 0; i < N; ++i) {
+      const int digit = rest % 3;
+      rest /= 3;
+      codes[(size_t)k * N + i] = digit == 2 ? 1 : digit == 1 ? 2 : 3;
+    }
+  }
+}
+
 }  // namespace
+
+void launch_brute_force(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                        const int32_t* cap_full, const int32_t* cap_fwd, int K, int N, uint8_t* codes,
+                        cudaStream_t s) {
+  int total = 1;
+  for (int i = 0; i < N; ++i) total *= 3;
+  brute_kernel<<<K, kThreads, 0, s>>>(bwd, fwd, cf, cb, cap_full, cap_fwd, N, total, codes);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
 
 size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
   const int words = (max_cols + 31) / 32 + 8;

@@ -64,4 +64,9 @@ void launch_scaler(const double* bwd, const double* fwd, const int32_t* cf, cons
                    const int32_t* total_cap, int K, int N, const double* lambda_dev, int max_cap,
                    uint8_t* codes, uint8_t* choice_global, double* vals_global, cudaStream_t s);
 
+// brute_force_schedule (scheduler.cpp:248-302), N <= 14
+void launch_brute_force(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
+                        const int32_t* cap_full, const int32_t* cap_fwd, int K, int N, uint8_t* codes,
+                        cudaStream_t s);
+
 }  // namespace d2ft_b200

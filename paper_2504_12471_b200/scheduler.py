@@ -363,6 +363,22 @@ def check_shared_budget(table: ScheduleTable, cost_model: CostModel, capacities:
     return SharedBudgetReport(devs, viol)
 
 
+def brute_force_schedule(scores: ScoreTable, cost_model: CostModel, capacities: Capacities,
+                         threads: int = 1) -> ScheduleTable:
+    """scheduler.cpp:248-302 on the GPU (3^N enumeration per row, N <= 14)."""
+    scores.validate()
+    capacities.validate()
+    K, N = scores.subnets, scores.micro_batches
+    if capacities.devices() != K:
+        raise Error(2, "brute_force_schedule: capacities device count mismatch")
+    cf, cb = cost_model.row_arrays(K)
+    codes = np.zeros((K, N), np.uint8)
+    check(lib().d2ft_brute_force_schedule(ptr(scores.backward), ptr(scores.forward), ptr(cf), ptr(cb),
+                                          ptr(i32(capacities.full)), ptr(i32(capacities.fwd)), C.c_int(K),
+                                          C.c_int(N), ptr(codes)))
+    return ScheduleTable(K, N, codes)
+
+
 def schedule_objective(table: ScheduleTable, scores: ScoreTable) -> np.ndarray:
     """scheduler.cpp:304-319 (per-row realised value; host accounting)."""
     if table.devices != scores.subnets or table.micro_batches != scores.micro_batches:

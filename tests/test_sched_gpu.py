@@ -167,3 +167,23 @@ def test_merge_exhaustive():
             b = np.array([[(fb >> i) & 1 for i in range(n)]] * (1 << n), np.uint8)
             got = P.merge_selections(a, b).codes
             assert np.array_equal(got, np.where(a == 1, 1, np.where(b == 1, 2, 3)))
+
+
+def test_brute_force_vs_oracle_and_dominance():
+    # test_scheduler.cpp:201-250: exhaustive optimum dominates the bi-level result
+    rng = np.random.default_rng(21)
+    cm = P.CostModel()
+    for trial in range(12):
+        K, N = int(rng.integers(1, 4)), int(rng.integers(1, 9))
+        b, f = O.random_score_table(K, N, 500 + trial)
+        capf = rng.integers(0, 18, K).astype(np.int32)
+        capo = rng.integers(0, 7, K).astype(np.int32)
+        t = _table(b, f)
+        caps = P.Capacities(capf.tolist(), capo.tolist())
+        got = P.brute_force_schedule(t, cm, caps)
+        assert np.array_equal(got.codes, O.brute_force_schedule(b, f, 2, 3, capf, capo)), trial
+        heur = P.knapsack_schedule(t, cm, caps)
+        assert np.all(P.schedule_objective(got, t) >= P.schedule_objective(heur, t))
+    with pytest.raises(P.Error) as e:
+        P.brute_force_schedule(P.ScoreTable(1, 15, np.ones((1, 15)), np.ones((1, 15))), cm, P.Capacities([10], [2]))
+    assert e.value.kind == "size"
