@@ -10,7 +10,7 @@
 extern "C" {
 #endif
 
-/* D[m][n] = sum_k A[m][k] B[n][k]; bn selects the tile width (160, 208, 256). */
+/* D[m][n] = sum_k A[m][k] B[n][k]; bn selects the tile width (160, 208, 256; -208 / -160 = CTA pair with multicast B). */
 int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int K, int bn, float* D);
 /* Tokens as N: D[p][m][t] = sum_k A[m][k] X[p][t][k] for t < T (T-row planes). */
 int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, int K, int P, float* D);

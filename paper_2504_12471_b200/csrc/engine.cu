@@ -312,16 +312,16 @@ struct Engine {
     tm_W1 = make_tmap_f16_3d(W1_bf, H * PQ, d, L, H * PQ * 2, d * H * PQ * 2, 64);
     tm_dCT = make_tmap_f16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
     tm_dY1T = make_tmap_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
-    // B operands, tokens as N (box BNt)
-    tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt);
-    tm_xn = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt);
-    tm_OG = make_tmap_f16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt);
-    tm_dC = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt);
-    tm_dY1 = make_tmap_f16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt);
-    // B operands, tokens as K
-    tm_OGT = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 160);
-    tm_xnT = make_tmap_f16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 256);
-    tm_inpT = make_tmap_f16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 256);
+    // B operands, tokens as N (box BNt/2: each CTA of a pair loads half, multicast)
+    tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt / 2);
+    tm_xn = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt / 2);
+    tm_OG = make_tmap_f16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt / 2);
+    tm_dC = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt / 2);
+    tm_dY1 = make_tmap_f16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt / 2);
+    // B operands, tokens as K (half boxes, multicast)
+    tm_OGT = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 80);
+    tm_xnT = make_tmap_f16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 128);
+    tm_inpT = make_tmap_f16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 128);
   }
 
   // ---------------------------------------------------------------- params
@@ -397,16 +397,16 @@ struct Engine {
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, 6>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        launch_gemm<Prob<208>, GemmShape<208, 5>>(a, b, Prob<208>{args...}, 0, st);
+        launch_gemm<Prob<208>, GemmShape<208, 5, 0, 4, 2>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, 4>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
@@ -455,11 +455,11 @@ struct Engine {
       launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
                       st);
       mark(PH_G5);
-      launch_gemm<G5<160>, GemmShape<160, 6>>(
+      launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2>>(
           tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax},
           0, st);
       mark(PH_G7);
-      launch_gemm<G7<256>, GemmShape<256, 4>>(
+      launch_gemm<G7<256>, GemmShape<256, 4, 0, 4, 2>>(
           tm_dY1T, tm_xnT,
           G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax}, 0, st);
       mark(PH_G8);
@@ -472,7 +472,7 @@ struct Engine {
                          gmax, st);
     }
     mark(PH_EMBED_W);
-    launch_gemm<EmbedW<256>, GemmShape<256, 4>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
+    launch_gemm<EmbedW<256>, GemmShape<256, 4, 0, 4, 2>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
   }
 

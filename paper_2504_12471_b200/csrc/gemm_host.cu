@@ -71,7 +71,7 @@ struct DenseProb {
   struct Row {};
   __device__ int ntn() const { return (N + BN - 1) / BN; }
   __device__ int ntiles() const { return ((M + 127) / 128) * ntn(); }
-  __device__ void tile(int t, Tile& c) const {
+  __device__ void tile(int t, int, Tile& c) const {
     c.mt = t / ntn();
     c.nt = t % ntn();
     c.nkb = (K + 63) / 64;
@@ -102,7 +102,7 @@ struct PlanesProb {
   };
   struct Row {};
   __device__ int ntiles() const { return ((M + 127) / 128) * P; }
-  __device__ void tile(int t, Tile& c) const {
+  __device__ void tile(int t, int, Tile& c) const {
     c.p = t / ((M + 127) / 128);
     c.mt = t % ((M + 127) / 128);
     c.nkb = (K + 63) / 64;
@@ -136,7 +136,7 @@ struct TokenKProb {
   struct Row {};
   __device__ int ntn() const { return (N + BN - 1) / BN; }
   __device__ int ntiles() const { return ((M + 127) / 128) * ntn(); }
-  __device__ void tile(int t, Tile& c) const {
+  __device__ void tile(int t, int, Tile& c) const {
     c.mt = t / ntn();
     c.nt = t % ntn();
     c.nkb = P * ((T + 63) / 64);
@@ -145,6 +145,39 @@ struct TokenKProb {
     const int tb = (T + 63) / 64;
     const int p = kb / tb, t0 = (kb % tb) * 64;
     return KCoord{t0, c.mt * 128, c.mt * 128 + 64, p, t0, c.nt * BN, p};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = c.nt * BN + col0 + i;
+      if (n < N) D[(size_t)m * N + n] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
+};
+
+// CTA-pair variant of DenseProb: the two CTAs of a cluster take m-tiles 2p and
+// 2p+1 of the same n-tile and share (multicast) its B rows.
+template <int BN>
+struct DensePairProb {
+  int M, N, K;
+  float* D;
+  struct Tile {
+    int nkb, mt, nt;
+  };
+  struct Row {};
+  __device__ int ntn() const { return (N + BN - 1) / BN; }
+  __device__ int ntiles() const { return (((M + 127) / 128 + 1) / 2) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.mt = 2 * (t / ntn()) + rank;
+    c.nt = t % ntn();
+    c.nkb = (K + 63) / 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, 0, kb * 64, c.nt * BN, 0};
   }
   __device__ void row_begin(const Tile&, int, Row&) const {}
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
@@ -181,7 +214,17 @@ int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int
     D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemcpy(dB.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
-    if (bn == 256) {
+    if (bn == -208) {  // CTA pair, B multicast
+      using S = GemmShape<208, 5, 1, 4, 2>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 104);
+      launch_gemm<DensePairProb<208>, S>(a, b, DensePairProb<208>{M, N, K, dD.p}, 0, nullptr);
+    } else if (bn == -160) {
+      using S = GemmShape<160, 6, 1, 4, 2>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 80);
+      launch_gemm<DensePairProb<160>, S>(a, b, DensePairProb<160>{M, N, K, dD.p}, 0, nullptr);
+    } else if (bn == 256) {
       using S = GemmShape<256, 4, 1>;
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 256);

@@ -1,6 +1,6 @@
 // Persistent, warp-specialised tcgen05 GEMM for sm_100a.
 //
-//   D[m][n] = sum_k A[m][k] * B[n][k]     (bf16 operands, fp32 accumulate in TMEM)
+//   D[m][n] = sum_k A[m][k] * B[n][k]     (fp16/bf16 operands, fp32 accumulate in TMEM)
 //
 // Both operands are K-major and arrive by TMA (128-byte swizzle) from 3-D
 // tensor maps, so a problem can gather rows from anywhere (per-head weight
@@ -12,19 +12,26 @@
 //   struct P {
 //     struct Tile { int nkb; ... };                 // nkb == 0: accumulator is zero
 //     struct Row { ... };                            // per-thread epilogue state
-//     __device__ int ntiles() const;
-//     __device__ void tile(int t, Tile&) const;
+//     __device__ int ntiles() const;                 // tile slots (pairs when CLUSTER == 2)
+//     __device__ void tile(int t, int rank, Tile&) const;
 //     __device__ KCoord kcoord(const Tile&, int kb) const;
 //     __device__ void row_begin(const Tile&, int row, Row&) const;
 //     __device__ void chunk(const Tile&, int row, int col0, const float (&v)[16], Row&) const;
 //     __device__ void row_end(const Tile&, int row, int group, Row&) const;
 //   };
 //
+// CLUSTER == 2: the two CTAs of a cluster work on the two tiles of a slot,
+// which share the B operand (same sample / plane) and the k-block count.  Each
+// CTA loads its own A and HALF of B, multicast to both CTAs; MMA completion is
+// committed to both CTAs' empty barriers.  Per CTA this cuts the TMA operand
+// traffic from A+B to A+B/2 per k-block (the single-CTA kernel is L2->SM
+// operand-feed bound).
+//
 // Roles: warp 0 = TMA producer, warp 1 = MMA issuer (one thread), warp 2 =
 // TMEM allocator, warps 4.. = EPI epilogue warpgroups (TMEM lane quarter =
-// warp % 4, column group = (warp - 4) / 4).  Tile M = 128 (two 64-row A boxes), N = BN, K-block = 64.
-// Two TMEM accumulators (columns 0 and 256) let the epilogue of tile i
-// overlap the MMAs of tile i+1.
+// warp % 4, column group = (warp - 4) / 4).  Tile M = 128 (two 64-row A
+// boxes), N = BN, K-block = 64.  Two TMEM accumulators (columns 0 and 256) let
+// the epilogue of tile i overlap the MMAs of tile i+1.
 #pragma once
 #include <cuda.h>
 
@@ -35,22 +42,25 @@ namespace d2ft_b200 {
 
 struct KCoord {
   int ax, ay0, ay1, az;  // A: k offset, row of the first/second 64-row half, plane
-  int bx, by, bz;        // B: k offset, first row, plane
+  int bx, by, bz;        // B: k offset, first row of the (full) B tile, plane
 };
 
 // FMT: operand format, 0 = fp16 (the step), 1 = bf16 (self-tests).
 // EPI: epilogue warpgroups; group e drains column chunks e, e+EPI, ... of the
 // accumulator, so EPI x more epilogue loads/stores are in flight per SM.
-template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4>
+// CLUSTER: 1, or 2 for the B-sharing CTA pair.
+template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1>
 struct GemmShape {
-  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_;
+  static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_PART = B_BYTES / CLUSTER;  // bytes of B each CTA loads
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
-  static_assert(B_BYTES % 1024 == 0, "B stage must keep 1024-byte swizzle alignment");
+  static_assert(B_BYTES % 1024 == 0 && B_PART % 1024 == 0, "B stage parts must keep 1024-byte swizzle alignment");
+  static_assert(CLUSTER == 1 || CLUSTER == 2, "cluster of 1 or 2");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 
@@ -68,12 +78,15 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = S::CLUSTER == 2 ? (int)ptx::cluster_rank() : 0;
+  const int slot0 = blockIdx.x / S::CLUSTER, nslots = gridDim.x / S::CLUSTER;
+  constexpr uint16_t kPair = 0x3;
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
     for (int i = 0; i < S::STAGES; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&empty[i], S::CLUSTER);  // both CTAs' MMAs read the stage (multicast B)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -83,7 +96,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
-  __syncthreads();
+  if (S::CLUSTER == 2) ptx::cluster_sync();  // peers' barriers exist before any multicast
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ntiles = prob.ntiles();
@@ -92,9 +106,9 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = slot0; t < ntiles; t += nslots) {
         typename P::Tile c;
-        prob.tile(t, c);
+        prob.tile(t, rank, c);
         for (int kb = 0; kb < c.nkb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           const KCoord k = prob.kcoord(c, kb);
@@ -102,7 +116,12 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
           ptx::tma_load_3d(a, &tmA, &full[stage], k.ax, k.ay0, k.az);
           ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ax, k.ay1, k.az);
-          ptx::tma_load_3d(sB + stage * S::B_BYTES, &tmB, &full[stage], k.bx, k.by, k.bz);
+          if (S::CLUSTER == 2) {
+            ptx::tma_load_3d_mc(sB + stage * S::B_BYTES + rank * S::B_PART, &tmB, &full[stage], k.bx,
+                                k.by + rank * (S::BN / 2), k.bz, kPair);
+          } else {
+            ptx::tma_load_3d(sB + stage * S::B_BYTES, &tmB, &full[stage], k.bx, k.by, k.bz);
+          }
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -115,9 +134,9 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       constexpr uint32_t idesc = ptx::idesc_f16_m128(S::BN, S::FMT);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = slot0; t < ntiles; t += nslots) {
         typename P::Tile c;
-        prob.tile(t, c);
+        prob.tile(t, rank, c);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem + acc * 256;
@@ -129,7 +148,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
             ptx::umma_bf16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
-          ptx::umma_commit(&empty[stage]);
+          if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
+          else ptx::umma_commit(&empty[stage]);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -141,14 +161,14 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;            // TMEM lane quarter
-    const int e = (warp - 4) >> 2;     // column group
+    const int q = warp & 3;         // TMEM lane quarter
+    const int e = (warp - 4) >> 2;  // column group
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = slot0; t < ntiles; t += nslots) {
       typename P::Tile c;
-      prob.tile(t, c);
+      prob.tile(t, rank, c);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       typename P::Row st;
@@ -174,7 +194,9 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  // the peer may still commit into our empty barriers / multicast into our smem
+  if (S::CLUSTER == 2) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
@@ -198,6 +220,8 @@ inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, 
 
 int num_sms();
 
+// Launch: persistent grid of ~one CTA (CLUSTER == 2: one CTA pair per two
+// SMs) per SM.  The B tensor map's box must be BN / CLUSTER rows.
 template <class P, class S>
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int max_ctas, cudaStream_t stream) {
   static bool attr = false;
@@ -208,8 +232,25 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int 
   }
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (grid < 1) grid = 1;
-  gemm_sm100_kernel<P, S><<<grid, S::THREADS, S::SMEM_BYTES, stream>>>(a, b, prob);
+  grid -= grid % S::CLUSTER;
+  if (grid < S::CLUSTER) grid = S::CLUSTER;
+  if (S::CLUSTER == 1) {
+    gemm_sm100_kernel<P, S><<<grid, S::THREADS, S::SMEM_BYTES, stream>>>(a, b, prob);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(S::THREADS);
+    cfg.dynamicSmemBytes = S::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = S::CLUSTER;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    D2FT_CUDA(cudaLaunchKernelEx(&cfg, gemm_sm100_kernel<P, S>, a, b, prob));
+  }
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

@@ -15,6 +15,11 @@ namespace d2ft_b200 {
 
 struct NoRow {};
 
+// The step GEMMs run as CTA pairs (GemmShape CLUSTER = 2): a tile slot holds
+// two tiles that share the B operand; `rank` selects the CTA's tile.
+__host__ __device__ inline int mpairs(int mtiles) { return (mtiles + 1) / 2; }
+constexpr int kUnitsPerSlot = 4;  // G1/G4: 2 x 64-row units per CTA
+
 // ---------------------------------------------------------------- embed fwd
 // x0[s][t][m] = sum_j inp[s][t][j] w_embed[j][m] + b_embed[m] + pos[t][m]
 // (model.cpp:313-317).  A = WeT (d x d), B = inp (plane s).
@@ -28,10 +33,11 @@ struct EmbedFwd {
     int nkb, s, mt;
   };
   using Row = NoRow;
-  __device__ int ntiles() const { return D.B * (D.d / 128); }
-  __device__ void tile(int t, Tile& c) const {
-    c.s = t / (D.d / 128);
-    c.mt = t % (D.d / 128);
+  // slot = (sample, pair of 128-row m-tiles); both CTAs share the sample's tokens (B)
+  __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.s = t / mpairs(D.d / 128);
+    c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
     c.nkb = D.d / 64;
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
@@ -40,6 +46,7 @@ struct EmbedFwd {
   __device__ void row_begin(const Tile&, int, Row&) const {}
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
     const float b = be[m];
     float p[16];  // all loads first: the stores below may alias as far as the compiler knows
 #pragma unroll
@@ -83,14 +90,14 @@ struct G1 {
     const int h = act_heads[(s * D.L + l) * D.H + u / D.UQ];
     return h * D.PQ + (u % D.UQ) * 64;
   }
-  __device__ void tile(int t, Tile& c) const {
+  __device__ void tile(int t, int rank, Tile& c) const {
     const int p = tiles[t];
     c.s = p >> 16;
-    c.u0 = p & 0xffff;
+    c.u0 = (p & 0xffff) + 2 * rank;
     c.nu = D.UQ * act_cnt[c.s * D.L + l];
     c.nkb = D.d / 64;
-    c.r0 = unit_row(c.s, c.u0);
-    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0);
+    c.r0 = unit_row(c.s, c.u0 < c.nu ? c.u0 : c.nu - 1);  // units past nu: valid rows, ignored rows
+    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.nu - 1);
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, l * D.Bmax + c.s};
@@ -160,10 +167,10 @@ struct G3 {
   struct Row {
     float bias;
   };
-  __device__ int ntiles() const { return D.B * (D.d / 128); }
-  __device__ void tile(int t, Tile& c) const {
-    c.s = t / (D.d / 128);
-    c.mt = t % (D.d / 128);
+  __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.s = t / mpairs(D.d / 128);
+    c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
     const int n = act_cnt[c.s * D.L + l];
     c.nkb = D.UO * n;
     const int* hp = act_heads + (c.s * D.L + l) * D.H;
@@ -177,12 +184,14 @@ struct G3 {
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
     const int hm = m / (D.d / D.H);
     const uint8_t code = codes[(size_t)(l * D.H + hm) * D.Bmax + c.s];
     r.bias = (code == 1 || code == 2) ? b2[m] : 0.f;  // p_s adds nothing (model.cpp:458)
   }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
     const size_t o0 = ((size_t)c.s * D.T + col0) * D.d + m;
     float xi[16];  // batch the residual loads ahead of the stores
 #pragma unroll
@@ -224,14 +233,14 @@ struct G4 {
     const int h = full_heads[(s * D.L + l) * D.H + u / D.UO];
     return h * D.PO + (u % D.UO) * 64;
   }
-  __device__ void tile(int t, Tile& c) const {
+  __device__ void tile(int t, int rank, Tile& c) const {
     const int p = tiles[t];
     c.s = p >> 16;
-    c.u0 = p & 0xffff;
+    c.u0 = (p & 0xffff) + 2 * rank;
     c.nu = D.UO * full_hcnt[c.s * D.L + l];
     c.nkb = D.d / 64;
-    c.r0 = unit_row(c.s, c.u0);
-    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.u0);
+    c.r0 = unit_row(c.s, c.u0 < c.nu ? c.u0 : c.nu - 1);
+    c.r1 = unit_row(c.s, c.u0 + 1 < c.nu ? c.u0 + 1 : c.nu - 1);
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, c.s};
@@ -305,12 +314,13 @@ struct G5 {
     float inv;
   };
   __device__ int ntn() const { return (D.PO + BN - 1) / BN; }
-  __device__ int ntiles() const { return D.H * (D.d / 128) * ntn(); }
-  __device__ void tile(int t, Tile& c) const {
-    const int per = (D.d / 128) * ntn();
+  // slot = (head, m-tile pair, n-tile): the pair shares B = [O|g]^T of (s, h)
+  __device__ int ntiles() const { return D.H * mpairs(D.d / 128) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int per = mpairs(D.d / 128) * ntn();
     c.h = t / per;
     const int r = t % per;
-    c.mt = r / ntn();
+    c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
     c.nkb = D.TB * full_cnt[l * D.H + c.h];
   }
@@ -322,6 +332,7 @@ struct G5 {
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
     float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -351,12 +362,13 @@ struct G7 {
   };
   __device__ int ntm() const { return (D.PQ + 127) / 128; }
   __device__ int ntn() const { return (D.d + BN - 1) / BN; }
-  __device__ int ntiles() const { return D.H * ntm() * ntn(); }
-  __device__ void tile(int t, Tile& c) const {
-    const int per = ntm() * ntn();
+  // slot = (head, m-tile pair, n-tile): the pair shares B = xn^T of sample s
+  __device__ int ntiles() const { return D.H * mpairs(ntm()) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int per = mpairs(ntm()) * ntn();
     c.h = t / per;
     const int r = t % per;
-    c.mt = r / ntn();
+    c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
     c.nkb = D.TB * full_cnt[l * D.H + c.h];
   }
@@ -403,10 +415,10 @@ struct G8 {
   struct Row {
     float inv;
   };
-  __device__ int ntiles() const { return D.B * (D.d / 128); }
-  __device__ void tile(int t, Tile& c) const {
-    c.s = t / (D.d / 128);
-    c.mt = t % (D.d / 128);
+  __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.s = t / mpairs(D.d / 128);
+    c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
     const int n = full_hcnt[c.s * D.L + l];
     c.nkb = D.UQ * n;
     const int* hp = full_heads + (c.s * D.L + l) * D.H;
@@ -421,6 +433,7 @@ struct G8 {
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int t = col0 + i;
@@ -446,12 +459,12 @@ struct EmbedW {
     float inv;
   };
   __device__ int ntn() const { return (D.d + BN - 1) / BN; }
-  __device__ int ntiles() const { return KS * (D.d / 128) * ntn(); }
-  __device__ void tile(int t, Tile& c) const {
-    const int per = (D.d / 128) * ntn();
+  __device__ int ntiles() const { return KS * mpairs(D.d / 128) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int per = mpairs(D.d / 128) * ntn();
     c.ks = t / per;
     const int r = t % per;
-    c.mt = r / ntn();
+    c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
     c.s0 = c.ks * D.B / KS;
     c.nkb = D.TB * ((c.ks + 1) * D.B / KS - c.s0);
@@ -464,6 +477,7 @@ struct EmbedW {
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
     float* out = part + ((size_t)c.ks * D.d + m) * D.d;
     const int n0 = c.nt * BN + col0;
 #pragma unroll

@@ -30,8 +30,8 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, in
   int c1 = 0, c4 = 0;
   const int s = threadIdx.x;
   if (s < D.B) {
-    c1 = (D.UQ * act_cnt[s * D.L + l] + 1) / 2;
-    c4 = (D.UO * full_hcnt[s * D.L + l] + 1) / 2;
+    c1 = (D.UQ * act_cnt[s * D.L + l] + 3) / 4;  // slots of 4 units (2 per CTA of the pair)
+    c4 = (D.UO * full_hcnt[s * D.L + l] + 3) / 4;
   }
   s1[threadIdx.x] = c1;
   s4[threadIdx.x] = c4;
@@ -51,8 +51,8 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, in
   const size_t cap4 = (size_t)D.Bmax * ((D.UO * D.H + 1) / 2);
   if (s < D.B) {
     const int b1 = s1[s] - c1, b4 = s4[s] - c4;
-    for (int i = 0; i < c1; ++i) g1_tiles[l * cap + b1 + i] = (s << 16) | (2 * i);
-    for (int i = 0; i < c4; ++i) g4_tiles[l * cap4 + b4 + i] = (s << 16) | (2 * i);
+    for (int i = 0; i < c1; ++i) g1_tiles[l * cap + b1 + i] = (s << 16) | (4 * i);
+    for (int i = 0; i < c4; ++i) g4_tiles[l * cap4 + b4 + i] = (s << 16) | (4 * i);
   }
   if (threadIdx.x == blockDim.x - 1) {
     g1_count[l] = s1[threadIdx.x];
