@@ -1,17 +1,19 @@
 # Builds the B200 library in-tree (travels to the GPU box with the snapshot).
 #   make            -> paper_2504_12471_b200/libd2ft_b200.so + oracle/_build/liboracle.so
 #   make ref        -> also oracle/_ref/libd2ft_ref.so (needs /root/reference)
+#   make OBJDIR=build/var/x/obj LIB=build/var/x/libd2ft_b200.so EXTRA=-D...  -> experiment build
+#                      (load it with D2FT_B200_LIB=...)
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2504_12471_b200
 CSRC     := $(PKG)/csrc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-            --expt-relaxed-constexpr -Iinclude -Xptxas -v
-OBJDIR   := build/obj
+            --expt-relaxed-constexpr -Iinclude -Xptxas -v $(EXTRA)
+OBJDIR   ?= build/obj
 SRCS     := $(wildcard $(CSRC)/*.cu)
 OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/d2ft_b200.h
-LIB      := $(PKG)/libd2ft_b200.so
+LIB      ?= $(PKG)/libd2ft_b200.so
 
 .PHONY: all ref oracle clean
 all: $(LIB) oracle

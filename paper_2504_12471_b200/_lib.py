@@ -10,7 +10,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libd2ft_b200.so")
+# D2FT_B200_LIB lets profiling experiments load an alternative build of the
+# same library (never a CPU path: every build is the sm_100a library).
+LIB_PATH = os.environ.get("D2FT_B200_LIB", os.path.join(HERE, "libd2ft_b200.so"))
 
 # d2ft::errc (error.hpp:12-19) + cuda
 ERRC = {1: "config", 2: "input", 3: "dimension", 4: "state", 5: "numeric", 6: "size", 7: "cuda"}

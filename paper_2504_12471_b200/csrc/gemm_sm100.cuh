@@ -37,6 +37,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include <type_traits>
 
 namespace d2ft_b200 {
 
@@ -49,6 +50,15 @@ struct KCoord {
 // EPI: epilogue warpgroups; group e drains column chunks e, e+EPI, ... of the
 // accumulator, so EPI x more epilogue loads/stores are in flight per SM.
 // CLUSTER: 1, or 2 for the B-sharing CTA pair.
+// Optional epilogue hook P::prefetch(tile, row, col0, row_state): issued for
+// the warp's first chunk right after the tile's accumulator wait (before the
+// TMEM load), so a problem that reads a per-element operand in its epilogue
+// can keep that load one chunk ahead.
+template <class P, class = void>
+struct has_prefetch : std::false_type {};
+template <class P>
+struct has_prefetch<P, std::void_t<decltype(&P::prefetch)>> : std::true_type {};
+
 template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1>
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
@@ -174,21 +184,60 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       typename P::Row st;
       prob.row_begin(c, row, st);
       const uint32_t base = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int col0 = 16 * e; col0 < S::BN; col0 += 16 * S::EPI) {
+      // Chunks of this warp: 16*e + i*16*EPI.  The accumulator is released to
+      // the MMA warp as soon as the warp's last TMEM load has landed.
+      const bool have = c.nkb > 0;
+      const int nch = (S::BN - 16 * e + 16 * S::EPI - 1) / (16 * S::EPI);
+      auto col_of = [&](int i) { return 16 * e + i * 16 * S::EPI; };
+      auto release = [&]() {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      };
+      auto process = [&](uint32_t (&r)[16], int i) {
         float v[16];
-        if (c.nkb > 0) {
-          ptx::tmem_ld16(base + col0, v);
-        } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        for (int j = 0; j < 16; ++j) v[j] = have ? __uint_as_float(r[j]) : 0.f;
+#ifndef D2FT_EXP_NOEPI
+        prob.chunk(c, row, col_of(i), v, st);
+#else
+        if (v[0] == 12345.f) prob.chunk(c, row, col_of(i), v, st);  // experiment: epilogue stores off
+#endif
+      };
+#ifdef D2FT_EXP_DB
+      uint32_t b0[16], b1[16];
+      if (have && nch > 0) ptx::tmem_ld16_async(base + col_of(0), b0);
+      if (nch == 0) release();
+#pragma unroll 1
+      for (int i = 0; i < nch; i += 2) {
+        if (have) ptx::tmem_ld_wait(b0);
+        if (have && i + 1 < nch) ptx::tmem_ld16_async(base + col_of(i + 1), b1);
+        if (i + 1 >= nch) release();
+        process(b0, i);
+        if (i + 1 < nch) {
+          if (have) ptx::tmem_ld_wait(b1);
+          if (have && i + 2 < nch) ptx::tmem_ld16_async(base + col_of(i + 2), b0);
+          if (i + 2 >= nch) release();
+          process(b1, i + 1);
         }
-        prob.chunk(c, row, col0, v, st);
       }
+#else
+      if constexpr (has_prefetch<P>::value) {
+        if (nch > 0) prob.prefetch(c, row, col_of(0), st);
+      }
+#pragma unroll 1
+      for (int i = 0; i < nch; ++i) {
+        uint32_t b0[16];
+        if (have) {
+          ptx::tmem_ld16_async(base + col_of(i), b0);
+          ptx::tmem_ld_wait(b0);
+        }
+        if (i + 1 == nch) release();
+        process(b0, i);
+      }
+      if (nch == 0) release();
+#endif
       prob.row_end(c, row, e, st);
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

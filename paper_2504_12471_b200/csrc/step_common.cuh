@@ -39,6 +39,12 @@ struct Dims {
 };
 
 __device__ __forceinline__ float gelu_f(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
+// GELU and its derivative sharing one erf evaluation.
+__device__ __forceinline__ void gelu_and_grad(float z, float& g, float& gp) {
+  const float cdf = 0.5f * (1.0f + erff(z * 0.70710678118654752f));
+  g = z * cdf;
+  gp = cdf + z * 0.39894228040143268f * __expf(-0.5f * z * z);
+}
 __device__ __forceinline__ float gelu_grad_f(float z) {
   return 0.5f * (1.0f + erff(z * 0.70710678118654752f)) + z * 0.39894228040143268f * __expf(-0.5f * z * z);
 }

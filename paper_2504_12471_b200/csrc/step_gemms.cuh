@@ -75,7 +75,7 @@ struct G1 {
   const int* act_cnt;
   const float* b1;  // block l: [H][fs]
   act_t* QKV;       // block l: [Bmax][H][T][3dh]   q|k|v, token-major (attention operands)
-  act_t* ZT;        // block l: [Bmax][H][fs][TP]   z + b1, feature-major (G4's GELU')
+  act_t* ZT;        // block l: [Bmax][H][fs][TP]   GELU'(z + b1), feature-major (G4's dz)
   act_t* OG;        // block l: [Bmax][H][T][PO]    [O|g] token-major (G3's B)
   act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G5's B)
   struct Tile {
@@ -115,22 +115,32 @@ struct G1 {
     if (!r.valid || col0 >= D.T) return;
     const size_t sh = (size_t)c.s * D.H + r.h;
     if (r.f < 3 * D.dh) {  // q, k, v: fp16 operands of the attention kernels
+#ifndef D2FT_EXP_G1_NOQKV
       act_t* y = QKV + sh * D.T * (3 * D.dh) + r.f;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         if (col0 + i < D.T) y[(size_t)(col0 + i) * (3 * D.dh)] = to_act(v[i]);
+#endif
       return;
     }
     const int j = r.f - 3 * D.dh;
-    float z[16], g[16];
+    float z[16], g[16];  // z becomes GELU'(z) (stored for G4), g = GELU(z)
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      z[i] = v[i] + r.bias;
-      g[i] = gelu_f(z[i]);
+      const float zz = v[i] + r.bias;
+#ifndef D2FT_EXP_G1_NOGELU
+      gelu_and_grad(zz, g[i], z[i]);
+#else
+      g[i] = zz;
+      z[i] = zz;
+#endif
     }
+#ifndef D2FT_EXP_G1_NOOG
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (col0 + i < D.T) OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = to_act(g[i]);
+#endif
+#ifndef D2FT_EXP_G1_NOT
     act_t* zt = ZT + (sh * D.fs + j) * D.TP + col0;
     act_t* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
     if (col0 + 8 <= D.TP) {
@@ -141,6 +151,7 @@ struct G1 {
       st_act_x8(zt + 8, z + 8);
       st_act_x8(gt + 8, g + 8);
     }
+#endif
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
@@ -215,7 +226,7 @@ struct G4 {
   const int* count;
   const int* full_heads;
   const int* full_hcnt;
-  const act_t* ZT;  // block l: [Bmax][H][fs][TP]
+  const act_t* ZT;  // block l: [Bmax][H][fs][TP]  GELU'(z), written by G1
   act_t* dO;        // [Bmax][H][T][dh]
   act_t* dY1;       // [Bmax][H][T][PQ]
   act_t* dY1T;      // [Bmax][H][PQ][TP]
@@ -227,6 +238,7 @@ struct G4 {
   struct Row {
     int valid, h, f;
     float db;
+    uint4 gp0, gp1;  // GELU'(z) of the warp's next chunk (prefetched one chunk ahead)
   };
   __device__ int ntiles() const { return *count; }
   __device__ int unit_row(int s, int u) const {
@@ -254,7 +266,15 @@ struct G4 {
     r.f = (u % D.UO) * 64 + (row & 63);
     r.valid = r.f < D.PO;
   }
-  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
+  // GELU' row of this feature, 16 contiguous tokens from col0 (two 16-byte
+  // loads), issued a chunk ahead so their latency hides behind the MMA wait.
+  __device__ void prefetch(const Tile& c, int, int col0, Row& r) const {
+    if (!r.valid || r.f < D.dh || col0 >= D.T) return;
+    const act_t* z = ZT + (((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)) * D.TP + col0;
+    r.gp0 = col0 + 8 <= D.TP ? *reinterpret_cast<const uint4*>(z) : make_uint4(0, 0, 0, 0);
+    r.gp1 = col0 + 16 <= D.TP ? *reinterpret_cast<const uint4*>(z + 8) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     if (!r.valid || col0 >= D.T) return;
     const size_t sh = (size_t)c.s * D.H + r.h;
     if (r.f < D.dh) {
@@ -268,18 +288,17 @@ struct G4 {
     const int fq = 3 * D.dh + j;
     act_t* dy = dY1 + sh * D.T * D.PQ + fq;
     float dz[16];
-    {  // z row of this feature: 16 contiguous tokens (two 16-byte loads)
-      const act_t* z = ZT + (sh * D.fs + j) * D.TP + col0;
+    {
       __align__(16) act_t zz[16];
-      *reinterpret_cast<uint4*>(zz) = col0 + 8 <= D.TP ? *reinterpret_cast<const uint4*>(z) : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(zz + 8) =
-          col0 + 16 <= D.TP ? *reinterpret_cast<const uint4*>(z + 8) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(zz) = r.gp0;
+      *reinterpret_cast<uint4*>(zz + 8) = r.gp1;
 #pragma unroll
       for (int i = 0; i < 16; ++i) dz[i] = act_to_f(zz[i]);
     }
+    prefetch(c, row, col0 + 16 * kEpiGroups, r);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      dz[i] = col0 + i < D.T ? v[i] * gelu_grad_f(dz[i]) : 0.f;
+      dz[i] = col0 + i < D.T ? v[i] * dz[i] : 0.f;
       r.db += dz[i];
     }
 #pragma unroll
@@ -334,10 +353,16 @@ struct G5 {
     const int m = c.mt * 128 + row;
     if (m >= D.d) return;
     float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
+    const int f0 = c.nt * BN + col0;
+    if (f0 + 16 <= D.PO) {  // 16 contiguous fp32 of this row: four 16-byte stores
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int f = c.nt * BN + col0 + i;
-      if (f < D.PO) out[f] = v[i] * r.inv;
+      for (int i = 0; i < 16; i += 4)
+        *reinterpret_cast<float4*>(out + f0 + i) =
+            make_float4(v[i] * r.inv, v[i + 1] * r.inv, v[i + 2] * r.inv, v[i + 3] * r.inv);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (f0 + i < D.PO) out[f0 + i] = v[i] * r.inv;
     }
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}
