@@ -83,14 +83,14 @@ struct Engine {
   float* x;       // [L+1][Bmax][T][d]
   float* stats;   // [L][Bmax][T][2]
   act_t *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
-  act_t *QKV, *ZT, *OG, *OGT;
+  act_t *QKV, *ZT, *OGT;
   float* lse;     // [L][Bmax][H][T]
   act_t *inp, *inpT;
   float* samples_dev;
   int* labels_dev;
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
-  act_t *dC, *dCT, *dO, *dY1, *dY1T;
+  act_t *dC, *dCT, *dO, *dY1T;
   double *loss_s, *loss;
   float *pooled, *dlog;
   // schedule / compaction
@@ -100,6 +100,11 @@ struct Engine {
   int32_t* lists_mem;
   CompactLists lists{};
   int *g1_tiles, *g1_count, *g4_tiles, *g4_count;
+  int *ord_act, *ord_full, *ord_head;  // cost orders (plan_kernel)
+  int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
+                                       // (the variable-K GEMMs; uniform ones stay static)
+  enum { C_G3, C_G5, C_G7, C_G8 };
+  int* ctr(int l, int kind) { return ctrs + (l < 0 ? (size_t)D.L * 8 : (size_t)l * 8) + kind; }
   uint32_t* sched_bits = nullptr;
   size_t sched_bits_words = 0;
   unsigned int* sched_counter;
@@ -115,8 +120,8 @@ struct Engine {
   uint8_t* h_codes = nullptr;
 
   // tensor maps
-  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_OG, tm_W2, tm_dC, tm_dCT, tm_OGT, tm_dY1T, tm_xnT, tm_W1,
-      tm_dY1, tm_inpT;
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_W2, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_W1,
+      tm_inpT;
 
   // profiling
   bool profiling = false;
@@ -235,7 +240,6 @@ struct Engine {
     xnT = dalloc<act_t>(L * Bm * d * TP, owned);
     QKV = dalloc<act_t>(L * Bm * H * T * 3 * D.dh, owned);
     ZT = dalloc<act_t>(L * Bm * H * fs * TP, owned);
-    OG = dalloc<act_t>(L * Bm * H * T * PO, owned);
     OGT = dalloc<act_t>(L * Bm * H * PO * TP, owned);
     lse = dalloc<float>(L * Bm * H * T, owned);
     inp = dalloc<act_t>(Bm * T * d, owned);
@@ -252,7 +256,6 @@ struct Engine {
     dC = dalloc<act_t>(Bm * T * d, owned);
     dCT = dalloc<act_t>(Bm * d * TP, owned);
     dO = dalloc<act_t>(Bm * H * T * D.dh, owned);
-    dY1 = dalloc<act_t>(Bm * H * T * PQ, owned);
     dY1T = dalloc<act_t>(Bm * H * PQ * TP, owned);
     loss_s = dalloc<double>(Bm, owned);
     loss = dalloc<double>(1, owned);
@@ -290,6 +293,10 @@ struct Engine {
     g4_tiles = dalloc<int>(L * Bm * ((D.UO * H + 1) / 2), owned);
     g1_count = dalloc<int>(L, owned);
     g4_count = dalloc<int>(L, owned);
+    ord_act = dalloc<int>(L * Bm, owned);
+    ord_full = dalloc<int>(L * Bm, owned);
+    ord_head = dalloc<int>(L * H, owned);
+    ctrs = dalloc<int>((L + 1) * 8, owned);
     sched_counter = dalloc<unsigned int>(1, owned);
     err = dalloc<int>(1, owned);
     gmax = dalloc<float>(1, owned);
@@ -315,9 +322,10 @@ struct Engine {
     // B operands, tokens as N (box BNt/2: each CTA of a pair loads half, multicast)
     tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt / 2);
     tm_xn = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt / 2);
-    tm_OG = make_tmap_f16_3d(OG, PO, T, L * Bm * H, PO * 2, T * PO * 2, BNt / 2);
     tm_dC = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt / 2);
-    tm_dY1 = make_tmap_f16_3d(dY1, PQ, T, Bm * H, PQ * 2, T * PQ * 2, BNt / 2);
+    // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
+    tm_OGT64 = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 64);
+    // (tm_dY1T above doubles as G8's MN-major B)
     // B operands, tokens as K (half boxes, multicast)
     tm_OGT = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 80);
     tm_xnT = make_tmap_f16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 128);
@@ -393,20 +401,22 @@ struct Engine {
   }
 
   // ---------------------------------------------------------------- GEMM dispatch
-  template <template <int> class Prob, class... Args>
+  // Tokens-as-N GEMMs on CTA pairs; BMN = 1: B is a feature-major buffer
+  // read MN-major (its 64-token blocks cost more shared memory per stage).
+  template <template <int> class Prob, int BMN = 0, class... Args>
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2, BMN>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2, BMN>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        launch_gemm<Prob<208>, GemmShape<208, 5, 0, 4, 2>>(a, b, Prob<208>{args...}, 0, st);
+        launch_gemm<Prob<208>, GemmShape<208, BMN ? 4 : 5, 0, 4, 2, BMN>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2, BMN>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
@@ -417,6 +427,7 @@ struct Engine {
     const size_t L = D.L, Bm = D.Bmax, T = D.T, d = D.d, H = D.H;
     const size_t xs = Bm * T * d;
     mark(PH_EMBED);
+    D2FT_CUDA(cudaMemsetAsync(ctrs, 0, (L + 1) * 8 * sizeof(int), st));
     launch_prep_input(D, samples_dev, inp, inpT, st);
     gemm_tokN<EmbedFwd>(tm_WeT, tm_inp, D, P + seg[S_BE].off, P + seg[S_POS].off, x);
     for (int l = 0; l < D.L; ++l) {
@@ -425,16 +436,15 @@ struct Engine {
       mark(PH_G1);
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
-      act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
       gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
-                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGl, OGTl);
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl);
       mark(PH_ATTN_F);
-      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGl, OGTl, lse + (size_t)l * Bm * H * T, st);
+      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
-      gemm_tokN<G3>(tm_W2T, tm_OG, D, l, lists.act_heads, lists.act_cnt, codes_exp, P + seg[S_B2].off + (size_t)l * d,
-                    x + l * xs, x + (l + 1) * xs);
+      gemm_tokN<G3, 1>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
+                       P + seg[S_B2].off + (size_t)l * d, x + l * xs, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
     }
     mark(PH_HEAD);
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
@@ -446,24 +456,27 @@ struct Engine {
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
-      act_t* OGl = OG + (size_t)l * Bm * H * T * D.PO;
+      const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
-                    (const act_t*)ZTl, dO, dY1, dY1T, part_db1, (const float*)gmax);
+                    (const act_t*)ZTl, dO, dY1T, part_db1, (const float*)gmax);
       mark(PH_ATTN_B);
-      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGl, dO, lse + (size_t)l * Bm * H * T, dY1, dY1T,
-                      st);
+      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T, st);
       mark(PH_G5);
       launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2>>(
-          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax},
+          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
+                  ord_head + l * H, ctr(l, C_G5)},
           0, st);
       mark(PH_G7);
       launch_gemm<G7<256>, GemmShape<256, 4, 0, 4, 2>>(
           tm_dY1T, tm_xnT,
-          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax}, 0, st);
+          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                  ord_head + l * H, ctr(l, C_G7)},
+          0, st);
       mark(PH_G8);
-      gemm_tokN<G8>(tm_W1, tm_dY1, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax);
+      gemm_tokN<G8, 1>(tm_W1, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
+                       ord_full + l * Bm, ctr(l, C_G8));
       mark(PH_BIAS);
       launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
                          G + seg[S_B2].off + (size_t)l * d, st);
@@ -498,7 +511,8 @@ struct Engine {
   // per-sample codes already in codes_exp: compaction + plan
   void compact_and_plan() {
     launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
-    launch_plan(D, lists.act_cnt, lists.full_hcnt, g1_tiles, g1_count, g4_tiles, g4_count, st);
+    launch_plan(D, lists.act_cnt, lists.full_hcnt, lists.full_cnt,
+                Plan{g1_tiles, g1_count, g4_tiles, g4_count, ord_act, ord_full, ord_head}, st);
   }
 
   void ensure_sched(int max_cols) {

@@ -192,6 +192,39 @@ struct DensePairProb {
   __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
 
+// MN-major B: D[m][n] = sum_k A[m][k] BT[k][n]; BT row-major [K][N] (N contiguous).
+template <int BN>
+struct DenseMNProb {
+  int M, N, K, pair;
+  float* D;
+  struct Tile {
+    int nkb, mt, nt;
+  };
+  struct Row {};
+  __device__ int ntn() const { return (N + BN - 1) / BN; }
+  __device__ int mts() const { return pair ? (((M + 127) / 128 + 1) / 2) : (M + 127) / 128; }
+  __device__ int ntiles() const { return mts() * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.mt = pair ? 2 * (t / ntn()) + rank : t / ntn();
+    c.nt = t % ntn();
+    c.nkb = (K + 63) / 64;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, 0, c.nt * BN, kb * 64, 0};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (m >= M) return;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = c.nt * BN + col0 + i;
+      if (n < N) D[(size_t)m * N + n] = v[i];
+    }
+  }
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
+};
+
 template <typename T>
 struct Dev {
   T* p = nullptr;
@@ -239,6 +272,32 @@ int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 160);
       launch_gemm<DenseProb<160>, S>(a, b, DenseProb<160>{M, N, K, dD.p}, 0, nullptr);
+    }
+    D2FT_CUDA(cudaDeviceSynchronize());
+    D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int d2ft_test_gemm_mn(const uint16_t* A, const uint16_t* BT, int M, int N, int K, int bn, float* D) {
+  return guarded([&] {
+    D2FT_REQUIRE(K % 8 == 0 && N % 8 == 0, kInput, "K and N must be multiples of 8");
+    Dev<uint16_t> dA((size_t)M * K), dB((size_t)K * N);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(dB.p, BT, (size_t)K * N * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
+    CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dB.p, N, K, 1, (uint64_t)N * 2, (uint64_t)K * N * 2, 64);
+    if (bn == -208) {
+      launch_gemm<DenseMNProb<208>, GemmShape<208, 4, 1, 4, 2, 1>>(a, b, DenseMNProb<208>{M, N, K, 1, dD.p}, 0,
+                                                                    nullptr);
+    } else if (bn == 64) {
+      launch_gemm<DenseMNProb<64>, GemmShape<64, 8, 1, 4, 1, 1>>(a, b, DenseMNProb<64>{M, N, K, 0, dD.p}, 0, nullptr);
+    } else if (bn == -64) {
+      launch_gemm<DenseMNProb<64>, GemmShape<64, 8, 1, 4, 2, 1>>(a, b, DenseMNProb<64>{M, N, K, 1, dD.p}, 0, nullptr);
+    } else {
+      launch_gemm<DenseMNProb<208>, GemmShape<208, 4, 1, 4, 1, 1>>(a, b, DenseMNProb<208>{M, N, K, 0, dD.p}, 0,
+                                                                    nullptr);
     }
     D2FT_CUDA(cudaDeviceSynchronize());
     D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));

@@ -38,6 +38,7 @@
 #include "common.cuh"
 #include "ptx.cuh"
 #include <type_traits>
+#include <utility>
 
 namespace d2ft_b200 {
 
@@ -59,17 +60,35 @@ struct has_prefetch : std::false_type {};
 template <class P>
 struct has_prefetch<P, std::void_t<decltype(&P::prefetch)>> : std::true_type {};
 
-template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1>
+// BMN: B operand layout.  0 = K-major (rows of B are the N index, K
+// contiguous; one TMA box of BK x BN, or BK x BN/2 per CTA of a pair).
+// 1 = MN-major (B stored as [K][N] with N contiguous, e.g. a feature-major
+// activation whose N is tokens): the stage holds ceil(BN/64) blocks of
+// 64 K-rows x 64 N-elements (one 8 KB TMA box of 64 N x 64 K each, 128-byte
+// swizzle), read by UMMA with LBO = 8 KB (next 64-element N block) and
+// SBO = 1 KB (next 8 K-rows); the CTAs of a pair load alternate blocks.
+// Optional member `int* ctr` (zeroed before the launch): dynamic tile
+// scheduling instead of the static slot0 + i*nslots striding.
+template <class P, class = void>
+struct has_counter : std::false_type {};
+template <class P>
+struct has_counter<P, std::void_t<decltype(std::declval<P>().ctr)>> : std::true_type {};
+constexpr int kTileQ = 4;
+
+template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0>
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
+  static constexpr int BMN = BMN_;
+  static constexpr int NBLK = (BN + 63) / 64;  // MN-major B: 64-wide N blocks
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int B_PART = B_BYTES / CLUSTER;  // bytes of B each CTA loads
+  static constexpr int B_BYTES = BMN ? NBLK * 64 * BK * 2 : BN * BK * 2;
+  static constexpr int B_PART = B_BYTES / CLUSTER;  // bytes of B each CTA loads (K-major)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
-  static_assert(B_BYTES % 1024 == 0 && B_PART % 1024 == 0, "B stage parts must keep 1024-byte swizzle alignment");
+  static_assert(BMN || (B_BYTES % 1024 == 0 && B_PART % 1024 == 0),
+                "B stage parts must keep 1024-byte swizzle alignment");
   static_assert(CLUSTER == 1 || CLUSTER == 2, "cluster of 1 or 2");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
@@ -85,12 +104,16 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tq_full = tempty + 2;        // tile queue (dynamic scheduling)
+  uint64_t* tq_empty = tq_full + kTileQ;
+  int* tq = reinterpret_cast<int*>(tq_empty + kTileQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTileQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = S::CLUSTER == 2 ? (int)ptx::cluster_rank() : 0;
   const int slot0 = blockIdx.x / S::CLUSTER, nslots = gridDim.x / S::CLUSTER;
   constexpr uint16_t kPair = 0x3;
+  constexpr bool kDyn = has_counter<P>::value;
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
@@ -102,6 +125,11 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 4 * S::EPI);
     }
+    for (int i = 0; i < kTileQ; ++i) {
+      ptx::mbar_init(&tq_full[i], 1);
+      // consumers of both CTAs (MMA thread + epilogue warps) and the peer's producer
+      ptx::mbar_init(&tq_empty[i], S::CLUSTER * (1 + 4 * S::EPI) + (S::CLUSTER - 1));
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
@@ -112,11 +140,41 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int ntiles = prob.ntiles();
 
+  // Tile sequence.  Static: slot0, slot0 + nslots, ...  Dynamic (P has `ctr`):
+  // rank 0's producer claims slots with atomicAdd on prob.ctr (the problem
+  // orders its slots by decreasing cost) and publishes each id through the
+  // kTileQ-deep queue to every role of both CTAs; ids >= ntiles end the loop.
+  auto tq_publish = [&](int i, int t) {
+    const int q = i % kTileQ;
+    ptx::mbar_wait_cluster(&tq_empty[q], ((i / kTileQ) & 1) ^ 1);
+    for (int r = 0; r < S::CLUSTER; ++r) ptx::st_cluster_u32(ptx::mapa(&tq[q], r), (uint32_t)t);
+    for (int r = 0; r < S::CLUSTER; ++r) ptx::mbar_arrive_cluster(ptx::mapa(&tq_full[q], r));
+  };
+  auto tq_take = [&](int i, bool leader) {
+    const int q = i % kTileQ;
+    ptx::mbar_wait_cluster(&tq_full[q], (i / kTileQ) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&tq[q]);
+    __syncwarp(__activemask());
+    if (leader) ptx::mbar_arrive_cluster(ptx::mapa(&tq_empty[q], 0));
+    return t;
+  };
+  auto for_each_tile = [&](bool leader, auto&& body) {
+    if constexpr (kDyn) {
+      for (int i = 0;; ++i) {
+        const int t = tq_take(i, leader);
+        if (t >= ntiles) break;
+        body(t);
+      }
+    } else {
+      for (int t = slot0; t < ntiles; t += nslots) body(t);
+    }
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = slot0; t < ntiles; t += nslots) {
+      auto load_tile = [&](int t) {
         typename P::Tile c;
         prob.tile(t, rank, c);
         for (int kb = 0; kb < c.nkb; ++kb) {
@@ -126,7 +184,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
           ptx::tma_load_3d(a, &tmA, &full[stage], k.ax, k.ay0, k.az);
           ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ax, k.ay1, k.az);
-          if (S::CLUSTER == 2) {
+          if constexpr (S::BMN) {  // k.bx = first N element, k.by = first K row
+            for (int j = rank; j < S::NBLK; j += S::CLUSTER) {
+              uint8_t* b = sB + stage * S::B_BYTES + j * (64 * S::BK * 2);
+              if (S::CLUSTER == 2) ptx::tma_load_3d_mc(b, &tmB, &full[stage], k.bx + 64 * j, k.by, k.bz, kPair);
+              else ptx::tma_load_3d(b, &tmB, &full[stage], k.bx + 64 * j, k.by, k.bz);
+            }
+          } else if (S::CLUSTER == 2) {
             ptx::tma_load_3d_mc(sB + stage * S::B_BYTES + rank * S::B_PART, &tmB, &full[stage], k.bx,
                                 k.by + rank * (S::BN / 2), k.bz, kPair);
           } else {
@@ -137,14 +201,30 @@ __global__ void __launch_bounds__(S::THREADS, 1)
             phase ^= 1;
           }
         }
+      };
+      if constexpr (kDyn) {
+        if (rank == 0) {
+          int cur = atomicAdd(prob.ctr, 1);
+          for (int i = 0;; ++i) {
+            tq_publish(i, cur);
+            if (cur >= ntiles) break;
+            const int nxt = atomicAdd(prob.ctr, 1);  // claimed now, used after this tile's loads
+            load_tile(cur);
+            cur = nxt;
+          }
+        } else {
+          for_each_tile(true, load_tile);
+        }
+      } else {
+        for_each_tile(true, load_tile);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_m128(S::BN, S::FMT);
+      constexpr uint32_t idesc = ptx::idesc_f16_m128(S::BN, S::FMT) | (S::BMN ? (1u << 16) : 0u);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = slot0; t < ntiles; t += nslots) {
+      for_each_tile(true, [&](int t) {
         typename P::Tile c;
         prob.tile(t, rank, c);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -154,10 +234,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ad = ptx::desc_sw128(ptx::smem_u32(sA + stage * S::A_BYTES));
-          const uint64_t bd = ptx::desc_sw128(ptx::smem_u32(sB + stage * S::B_BYTES));
+          const uint32_t bs = ptx::smem_u32(sB + stage * S::B_BYTES);
+          const uint64_t bd = S::BMN ? ptx::desc_sw128_mn(bs, 64 * S::BK * 2) : ptx::desc_sw128(bs);
+          // K step of 16: +32 B along a K-major row, or +16 rows (2 KB) of an MN-major block
+          constexpr uint64_t bstep = S::BMN ? (16 * 128) >> 4 : 2;
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
-            ptx::umma_bf16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            ptx::umma_bf16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
           if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
           else ptx::umma_commit(&empty[stage]);
           if (++stage == S::STAGES) {
@@ -168,7 +251,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         ptx::umma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
+      });
     }
   } else if (warp >= 4) {
     const int q = warp & 3;         // TMEM lane quarter
@@ -176,7 +259,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = slot0; t < ntiles; t += nslots) {
+    for_each_tile(lane == 0, [&](int t) {
       typename P::Tile c;
       prob.tile(t, rank, c);
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -240,7 +323,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       prob.row_end(c, row, e, st);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   }
   ptx::tc_fence_before();
   // the peer may still commit into our empty barriers / multicast into our smem

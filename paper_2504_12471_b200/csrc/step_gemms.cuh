@@ -63,8 +63,8 @@ struct EmbedFwd {
 // ---------------------------------------------------------------- G1
 // [q|k|v|z] = xn . [Wq|Wk|Wv|W1]  per (sample, active head)  (model.cpp:200-202, 218-220)
 // A = W1T (plane l, rows h*PQ + f), B = xn (plane l*Bmax + s).  Epilogue:
-// q,k,v,z -> Y1 (token-major); g = gelu(z + b1) -> OG (token-major, G3's B)
-// and OGT (feature-major, G5's B).
+// q,k,v -> QKV (token-major, attention operands); g = gelu(z + b1) -> OGT
+// (feature-major: G3's MN-major B and G5's B); GELU'(z + b1) -> ZT (G4).
 template <int BN>
 struct G1 {
   Dims D;
@@ -76,8 +76,7 @@ struct G1 {
   const float* b1;  // block l: [H][fs]
   act_t* QKV;       // block l: [Bmax][H][T][3dh]   q|k|v, token-major (attention operands)
   act_t* ZT;        // block l: [Bmax][H][fs][TP]   GELU'(z + b1), feature-major (G4's dz)
-  act_t* OG;        // block l: [Bmax][H][T][PO]    [O|g] token-major (G3's B)
-  act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G5's B)
+  act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G3's and G5's B)
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
@@ -135,11 +134,6 @@ struct G1 {
       z[i] = zz;
 #endif
     }
-#ifndef D2FT_EXP_G1_NOOG
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (col0 + i < D.T) OG[(sh * D.T + col0 + i) * D.PO + D.dh + j] = to_act(g[i]);
-#endif
 #ifndef D2FT_EXP_G1_NOT
     act_t* zt = ZT + (sh * D.fs + j) * D.TP + col0;
     act_t* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
@@ -159,8 +153,9 @@ struct G1 {
 // ---------------------------------------------------------------- G3
 // x_{l+1} = x_l + sum_{active h} ( [O_h|g_h] . [Wo_h;W2_h] + b2_h on its slice )
 // (model.cpp:216, 221-225, 454-468).  A = W2T (plane l, K offset h*PO),
-// B = OG (plane (l*Bmax+s)*H+h).  K = concatenation over the sample's active
-// heads; the sum over heads happens inside TMEM in head order.
+// B = OGT read MN-major (plane (l*Bmax+s)*H+h, rows = K features, tokens
+// contiguous).  K = concatenation over the sample's active heads; the sum over
+// heads happens inside TMEM in head order.
 template <int BN>
 struct G3 {
   Dims D;
@@ -171,6 +166,8 @@ struct G3 {
   const float* b2;       // block l: [d]
   const float* xin;
   float* xout;
+  const int* order;  // block l: samples by decreasing active-head count (slot order)
+  int* ctr;          // dynamic tile counter (gemm_sm100.cuh): K varies by sample
   struct Tile {
     int nkb, s, mt;
     int heads[16];  // the sample's active heads in block l (cached once per tile)
@@ -180,7 +177,7 @@ struct G3 {
   };
   __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
   __device__ void tile(int t, int rank, Tile& c) const {
-    c.s = t / mpairs(D.d / 128);
+    c.s = order[t / mpairs(D.d / 128)];
     c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
     const int n = act_cnt[c.s * D.L + l];
     c.nkb = D.UO * n;
@@ -191,7 +188,7 @@ struct G3 {
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int a = kb / D.UO, kk = kb % D.UO;
     const int h = c.heads[a];
-    return KCoord{h * D.PO + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, (l * D.Bmax + c.s) * D.H + h};
+    return KCoord{h * D.PO + kk * 64, c.mt * 128, c.mt * 128 + 64, l, 0, kk * 64, (l * D.Bmax + c.s) * D.H + h};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
     const int m = c.mt * 128 + row;
@@ -228,8 +225,7 @@ struct G4 {
   const int* full_hcnt;
   const act_t* ZT;  // block l: [Bmax][H][fs][TP]  GELU'(z), written by G1
   act_t* dO;        // [Bmax][H][T][dh]
-  act_t* dY1;       // [Bmax][H][T][PQ]
-  act_t* dY1T;      // [Bmax][H][PQ][TP]
+  act_t* dY1T;      // [Bmax][H][PQ][TP]  d[q|k|v|z], feature-major (G7's and G8's operand)
   float* part_db1; // [EPI][Bmax][H][fs]
   const float* gmax;
   struct Tile {
@@ -286,7 +282,6 @@ struct G4 {
     }
     const int j = r.f - D.dh;
     const int fq = 3 * D.dh + j;
-    act_t* dy = dY1 + sh * D.T * D.PQ + fq;
     float dz[16];
     {
       __align__(16) act_t zz[16];
@@ -301,9 +296,6 @@ struct G4 {
       dz[i] = col0 + i < D.T ? v[i] * dz[i] : 0.f;
       r.db += dz[i];
     }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (col0 + i < D.T) dy[(size_t)(col0 + i) * D.PQ] = to_act(dz[i]);
     act_t* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
     if (col0 + 8 <= D.TP) st_act_x8(dt, dz);
     if (col0 + 16 <= D.TP) st_act_x8(dt + 8, dz + 8);
@@ -326,6 +318,8 @@ struct G5 {
   const int* full_cnt;
   float* dW2T;  // block l: [d][H*PO]
   const float* gmax;
+  const int* order;  // block l: heads by decreasing Full-sample count
+  int* ctr;
   struct Tile {
     int nkb, h, mt, nt;
   };
@@ -337,7 +331,7 @@ struct G5 {
   __device__ int ntiles() const { return D.H * mpairs(D.d / 128) * ntn(); }
   __device__ void tile(int t, int rank, Tile& c) const {
     const int per = mpairs(D.d / 128) * ntn();
-    c.h = t / per;
+    c.h = order[t / per];
     const int r = t % per;
     c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
@@ -379,6 +373,8 @@ struct G7 {
   const int* full_cnt;
   float* dW1T;  // block l: [H][PQ][d]
   const float* gmax;
+  const int* order;  // block l: heads by decreasing Full-sample count
+  int* ctr;
   struct Tile {
     int nkb, h, mt, nt;
   };
@@ -391,7 +387,7 @@ struct G7 {
   __device__ int ntiles() const { return D.H * mpairs(ntm()) * ntn(); }
   __device__ void tile(int t, int rank, Tile& c) const {
     const int per = mpairs(ntm()) * ntn();
-    c.h = t / per;
+    c.h = order[t / per];
     const int r = t % per;
     c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
@@ -424,7 +420,7 @@ struct G7 {
 
 // ---------------------------------------------------------------- G8
 // dxn[s] = sum_{Full h} d[q|k|v|z]_h . [Wq|Wk|Wv|W1]_h^T  (model.cpp:259, 288)
-// A = W1 (plane l, K offset h*PQ), B = dY1 (plane s*H+h).
+// A = W1 (plane l, K offset h*PQ), B = dY1T read MN-major (plane s*H+h).
 template <int BN>
 struct G8 {
   Dims D;
@@ -433,6 +429,8 @@ struct G8 {
   const int* full_hcnt;
   float* dxn;  // [Bmax][T][d]
   const float* gmax;
+  const int* order;  // block l: samples by decreasing Full-head count
+  int* ctr;
   struct Tile {
     int nkb, s, mt;
     int heads[16];
@@ -442,7 +440,7 @@ struct G8 {
   };
   __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
   __device__ void tile(int t, int rank, Tile& c) const {
-    c.s = t / mpairs(D.d / 128);
+    c.s = order[t / mpairs(D.d / 128)];
     c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
     const int n = full_hcnt[c.s * D.L + l];
     c.nkb = D.UQ * n;
@@ -453,7 +451,7 @@ struct G8 {
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int a = kb / D.UQ, kk = kb % D.UQ;
     const int h = c.heads[a];
-    return KCoord{h * D.PQ + kk * 64, c.mt * 128, c.mt * 128 + 64, l, kk * 64, 0, c.s * D.H + h};
+    return KCoord{h * D.PQ + kk * 64, c.mt * 128, c.mt * 128 + 64, l, 0, kk * 64, c.s * D.H + h};
   }
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {

@@ -23,19 +23,36 @@ __global__ void expand_codes_kernel(const uint8_t* codes, int K, int n_mb, int m
   }
 }
 
-__global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count,
-                            int* g4_tiles, int* g4_count) {
+// rank of v[i] in decreasing order, ties by index (a stable counting rank)
+__device__ __forceinline__ int desc_rank(const int* v, int n, int i) {
+  const int x = v[i];
+  int r = 0;
+  for (int j = 0; j < n; ++j) r += (v[j] > x) | ((v[j] == x) & (j < i));
+  return r;
+}
+
+__global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, Plan pl) {
   const int l = blockIdx.x;
-  __shared__ int s1[1024], s4[1024];
+  __shared__ int s1[1024], s4[1024], va[1024], vf[1024], vh[64];
   int c1 = 0, c4 = 0;
   const int s = threadIdx.x;
   if (s < D.B) {
-    c1 = (D.UQ * act_cnt[s * D.L + l] + 3) / 4;  // slots of 4 units (2 per CTA of the pair)
-    c4 = (D.UO * full_hcnt[s * D.L + l] + 3) / 4;
+    va[s] = act_cnt[s * D.L + l];
+    vf[s] = full_hcnt[s * D.L + l];
+    c1 = (D.UQ * va[s] + 3) / 4;  // slots of 4 units (2 per CTA of the pair)
+    c4 = (D.UO * vf[s] + 3) / 4;
   }
+  if (s < D.H) vh[s] = full_cnt[l * D.H + s];
   s1[threadIdx.x] = c1;
   s4[threadIdx.x] = c4;
   __syncthreads();
+  // cost orders of the dynamically scheduled GEMMs: samples by active / Full
+  // head count (G3, G8), heads by Full sample count (G5, G7), largest first
+  if (s < D.B) {
+    pl.ord_act[l * D.Bmax + desc_rank(va, D.B, s)] = s;
+    pl.ord_full[l * D.Bmax + desc_rank(vf, D.B, s)] = s;
+  }
+  if (s < D.H) pl.ord_head[l * D.H + desc_rank(vh, D.H, s)] = s;
   for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
     int a1 = 0, a4 = 0;
     if ((int)threadIdx.x >= o) {
@@ -51,12 +68,12 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, in
   const size_t cap4 = (size_t)D.Bmax * ((D.UO * D.H + 1) / 2);
   if (s < D.B) {
     const int b1 = s1[s] - c1, b4 = s4[s] - c4;
-    for (int i = 0; i < c1; ++i) g1_tiles[l * cap + b1 + i] = (s << 16) | (4 * i);
-    for (int i = 0; i < c4; ++i) g4_tiles[l * cap4 + b4 + i] = (s << 16) | (4 * i);
+    for (int i = 0; i < c1; ++i) pl.g1_tiles[l * cap + b1 + i] = (s << 16) | (4 * i);
+    for (int i = 0; i < c4; ++i) pl.g4_tiles[l * cap4 + b4 + i] = (s << 16) | (4 * i);
   }
   if (threadIdx.x == blockDim.x - 1) {
-    g1_count[l] = s1[threadIdx.x];
-    g4_count[l] = s4[threadIdx.x];
+    pl.g1_count[l] = s1[threadIdx.x];
+    pl.g4_count[l] = s4[threadIdx.x];
   }
 }
 
@@ -558,23 +575,12 @@ __device__ __forceinline__ void store_frag_T(const float (&o)[DH / 8][4], float 
     }
   }
 }
-template <int DH>
-__device__ __forceinline__ void store_frag(const float (&o)[DH / 8][4], float sc, act_t* out, int pitch, int t0, int T,
-                                           int g, int c) {
-  const int ta = t0 + g, tb = t0 + g + 8;
-#pragma unroll
-  for (int nf = 0; nf < DH / 8; ++nf) {
-    const int f = nf * 8 + 2 * c;
-    if (ta < T) *reinterpret_cast<uint32_t*>(out + (size_t)ta * pitch + f) = pack2(o[nf][0] * sc, o[nf][1] * sc);
-    if (tb < T) *reinterpret_cast<uint32_t*>(out + (size_t)tb * pitch + f) = pack2(o[nf][2] * sc, o[nf][3] * sc);
-  }
-}
 
 // Forward: one warp per 16-query strip (blockDim = 32 * TQ/16), online softmax
 // over 32-key chunks.
 template <int DH>
 __global__ void __launch_bounds__(512) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
-                                                       const act_t* QKV, act_t* OG, act_t* OGT, float* lse) {
+                                                       const act_t* QKV, act_t* OGT, float* lse) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
   const int h = act_heads[(s * D.L + l) * D.H + a];
@@ -684,7 +690,6 @@ __global__ void __launch_bounds__(512) attn_fwd_kernel(Dims D, int l, const int*
     o[nf][2] *= i1;
     o[nf][3] *= i1;
   }
-  store_frag<DH>(o, 1.f, OG + sh * D.T * D.PO, D.PO, r0, D.T, g, c);
   store_frag_T<DH>(o, 1.f, OGT + sh * D.PO * D.TP, D.TP, r0, D.T, g, c);
   if (c == 0) {  // log2-domain log-sum-exp of the scaled scores
     if (r0 + g < D.T) lse[sh * D.T + r0 + g] = m0 + log2f(l0);
@@ -703,8 +708,8 @@ __device__ __forceinline__ void frag_a_t(uint32_t (&a)[4], const act_t* X, int P
 // dS^T kept in shared memory; phase 2, one warp per 16-query strip: dQ = dS.K.
 template <int DH>
 __global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
-                                                       const act_t* QKV, const act_t* OG, const act_t* dO,
-                                                       const float* lse, act_t* dY1, act_t* dY1T) {
+                                                       const act_t* QKV, const act_t* OGT, const act_t* dO,
+                                                       const float* lse, act_t* dY1T) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
   const int h = full_heads[(s * D.L + l) * D.H + a];
@@ -726,27 +731,28 @@ __global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int*
   stage_rows<DH>(y, 3 * DH, 2 * DH, D.T, TQ, Vs);
   stage_rows<DH>(dO + sh * D.T * D.dh, D.dh, 0, D.T, TQ, dOs);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, c = lane & 3;
-  {  // D_i and L2_i for this warp's 16 rows (rows >= T: D = 0, L2 = +inf -> P = 0)
-    const act_t* og = OG + sh * D.T * D.PO;
-    const act_t* dog = dO + sh * D.T * D.dh;
-    for (int r = 0; r < 16; ++r) {
-      const int t = warp * 16 + r;
-      float acc = 0.f;
-      if (t < D.T)
-        for (int f = lane; f < DH; f += 32)
-          acc += __half2float(dog[(size_t)t * D.dh + f]) * __half2float(og[(size_t)t * D.PO + f]);
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        Dv[t] = acc;
-        L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
+  // D_i and L2_i per query row (rows >= T: D = 0, L2 = +inf -> P = 0); O is
+  // read feature-major from OGT (coalesced over t), dO row-wise (16-byte loads)
+  for (int t = threadIdx.x; t < TQ; t += blockDim.x) {
+    float acc = 0.f;
+    if (t < D.T) {
+      const act_t* o = OGT + sh * D.PO * D.TP + t;
+      const act_t* dor = dO + (sh * D.T + t) * D.dh;
+#pragma unroll
+      for (int f0 = 0; f0 < DH; f0 += 8) {
+        __align__(16) act_t v[8];
+        *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(dor + f0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += __half2float(v[i]) * __half2float(o[(size_t)(f0 + i) * D.TP]);
       }
     }
+    Dv[t] = acc;
+    L2[t] = t < D.T ? lse[sh * D.T + t] : INFINITY;
   }
   cp_async_wait_all();
   __syncthreads();
   const float sl2 = kLog2e / sqrtf((float)DH);
   const float scale = 1.0f / sqrtf((float)DH);
-  act_t* dy = dY1 + sh * D.T * D.PQ;
   act_t* dyt = dY1T + sh * D.PQ * D.TP;
 
   {  // ---- phase 1: key strip -> dK, dV, dS^T
@@ -806,8 +812,6 @@ __global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int*
         mma16816(dk[nf + 1], sa, b[2], b[3]);
       }
     }
-    store_frag<DH>(dk, scale, dy + DH, D.PQ, k0, D.T, g, c);
-    store_frag<DH>(dv, 1.f, dy + 2 * DH, D.PQ, k0, D.T, g, c);
     store_frag_T<DH>(dk, scale, dyt + (size_t)DH * D.TP, D.TP, k0, D.T, g, c);
     store_frag_T<DH>(dv, 1.f, dyt + (size_t)2 * DH * D.TP, D.TP, k0, D.T, g, c);
   }
@@ -828,7 +832,6 @@ __global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int*
         mma16816(dq[nf + 1], sa, b[2], b[3]);
       }
     }
-    store_frag<DH>(dq, scale, dy, D.PQ, i0, D.T, g, c);
     store_frag_T<DH>(dq, scale, dyt, D.TP, i0, D.T, g, c);
   }
 }
@@ -866,12 +869,13 @@ void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, 
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count, int* g4_tiles,
-                 int* g4_count, cudaStream_t st) {
+void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, const Plan& pl,
+                 cudaStream_t st) {
   int threads = 32;
   while (threads < D.B) threads <<= 1;
   D2FT_REQUIRE(threads <= 1024, kSize, "plan: batch above 1024 samples");
-  plan_kernel<<<D.L, threads, 0, st>>>(D, act_cnt, full_hcnt, g1_tiles, g1_count, g4_tiles, g4_count);
+  D2FT_REQUIRE(D.H <= 64, kSize, "plan: at most 64 heads");
+  plan_kernel<<<D.L, threads, 0, st>>>(D, act_cnt, full_hcnt, full_cnt, pl);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -911,18 +915,18 @@ void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float*
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OG,
-                     act_t* OGT, float* lse, cudaStream_t st) {
+void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OGT,
+                     float* lse, cudaStream_t st) {
   dim3 grid(D.H, D.B);
   if (D.dh == 64) {
     const size_t sm = attn_fwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OGT, lse);
     count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_fwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OG, OGT, lse);
+    attn_fwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OGT, lse);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
@@ -930,18 +934,18 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1, const act_t* OG,
-                     const act_t* dO, const float* lse, act_t* dY1, act_t* dY1T, cudaStream_t st) {
+void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1,
+                     const act_t* OGT, const act_t* dO, const float* lse, act_t* dY1T, cudaStream_t st) {
   dim3 grid(D.H, D.B);
   if (D.dh == 64) {
     const size_t sm = attn_bwd_smem(64, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OGT, dO, lse, dY1T);
     count_launch();
   } else if (D.dh == 32) {
     const size_t sm = attn_bwd_smem(32, D.TQ);
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OG, dO, lse, dY1, dY1T);
+    attn_bwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, full_heads, full_hcnt, Y1, OGT, dO, lse, dY1T);
     count_launch();
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};

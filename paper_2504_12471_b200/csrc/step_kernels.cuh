@@ -9,18 +9,26 @@ namespace d2ft_b200 {
 // codes [K][n_mb] -> per-sample codes [K][Bmax] (sample s uses column s / mbs; s >= B -> 3)
 void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
                          cudaStream_t st);
-// per block: G1 / G4 tile lists over (sample, 64-row unit pair)
-void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, int* g1_tiles, int* g1_count,
-                 int* g4_tiles, int* g4_count, cudaStream_t st);
+// Per-block GEMM plan of one batch: G1 / G4 tile lists over (sample, 64-row
+// unit pair) and the cost orders of the dynamically scheduled GEMMs.
+struct Plan {
+  int *g1_tiles, *g1_count, *g4_tiles, *g4_count;
+  int* ord_act;   // [L][Bmax] samples by decreasing active-head count (G3)
+  int* ord_full;  // [L][Bmax] samples by decreasing Full-head count (G8)
+  int* ord_head;  // [L][H] heads by decreasing Full-sample count (G5, G7)
+};
+void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, const Plan& pl,
+                 cudaStream_t st);
 // fp32 samples [B][T][d] -> act_t token-major + feature-major copies
 void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st);
 // LayerNorm (no affine, eps 1e-5) of x -> xn (token-major), xnT (feature-major), stats (mean, rstd)
 void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st);
 // attention forward / backward (one CTA per (sample, active|Full head) slot)
-void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OG,
-                     act_t* OGT, float* lse, cudaStream_t st);
-void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1, const act_t* OG,
-                     const act_t* dO, const float* lse, act_t* dY1, act_t* dY1T, cudaStream_t st);
+// (O feature-major into OGT rows 0..dh-1; dq|dk|dv feature-major into dY1T rows 0..3dh-1)
+void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OGT,
+                     float* lse, cudaStream_t st);
+void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1,
+                     const act_t* OGT, const act_t* dO, const float* lse, act_t* dY1T, cudaStream_t st);
 // head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, dlogits, and dX = dL/dx_L
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st);

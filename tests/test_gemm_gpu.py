@@ -39,6 +39,22 @@ def test_dense(M, N, K, bn):
     assert err < 1e-5, err
 
 
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 208, 448, 208), (384, 416, 320, 208),
+                                      (200, 200, 768, 208), (512, 624, 320, -208), (384, 128, 192, -64),
+                                      (130, 96, 128, 64)])
+def test_mn_major_b(M, N, K, bn):
+    """B stored [K][N] (N contiguous) and read by UMMA as an MN-major operand."""
+    rng = np.random.default_rng(M * 3 + N + K)
+    A, Af = bf16(rng.standard_normal((M, K)))
+    BT, BTf = bf16(rng.standard_normal((K, N)))
+    D = np.zeros((M, N), np.float32)
+    _call("d2ft_test_gemm_mn", _lib.ptr(A), _lib.ptr(BT), C.c_int(M), C.c_int(N), C.c_int(K), C.c_int(bn),
+          _lib.ptr(D))
+    ref = Af.astype(np.float64) @ BTf.astype(np.float64)
+    err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+
+
 def test_planes_tokens_as_n():
     M, T, K, P = 448, 197, 768, 5
     rng = np.random.default_rng(1)
