@@ -90,6 +90,25 @@ int d2ft_engine_codes(d2ft_engine* e, uint8_t* codes_exp_out);
 
 /* n draws of uniform_double(make_rng(seed, stream)) (rng.hpp:24-31) */
 int d2ft_uniform_stream(uint64_t seed, uint64_t stream, int n, double* out);
+/* ---- head partition across GPUs (no reference counterpart:
+ * the reference runs every subnet in one process).  Rank r of `world` owns
+ * heads h with h % world == r of every block: it schedules every row (rows
+ * are independent, so all ranks derive the same table), keeps its own rows,
+ * and after each block's forward (partial block outputs) and backward (dxn
+ * partials) the ranks sum their partials, the one data-path exchange.  The
+ * embedding and classifier are replicated.  Parameters and gradients of a
+ * head are authoritative on its owner only. */
+typedef struct d2ft_local_group d2ft_local_group;
+/* 128-byte NCCL unique id (rank 0 creates it, all ranks pass it below) */
+int d2ft_nccl_unique_id(uint8_t* id_out);
+/* join an NCCL group: one process per GPU, exchange = ncclAllReduce(sum) */
+int d2ft_engine_partition_nccl(d2ft_engine* e, int rank, int world, const uint8_t* id);
+/* in-process group of `world` engines on one device, stepped from `world`
+ * host threads; exchange = fixed-order device sum (single-GPU test harness) */
+int d2ft_local_group_create(int world, d2ft_local_group** out);
+int d2ft_local_group_destroy(d2ft_local_group* g);
+int d2ft_engine_partition_local(d2ft_engine* e, d2ft_local_group* g, int rank);
+
 /* select the CUDA device for subsequent engine/scheduler creation on this thread */
 int d2ft_set_device(int device);
 /* partition_model (model.cpp:140-156): canonical fp64 flat initial

@@ -12,7 +12,7 @@ namespace d2ft_b200 {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
 
 namespace {
 
@@ -178,7 +178,7 @@ extern "C" {
 
 const char* d2ft_last_error(void) { return g_last_error.c_str(); }
 
-unsigned long long d2ft_launch_count(void) { return g_launches; }
+unsigned long long d2ft_launch_count(void) { return g_launches.load(); }
 
 void* d2ft_host_alloc(size_t bytes) {
   void* p = nullptr;

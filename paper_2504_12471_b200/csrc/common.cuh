@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 namespace d2ft_b200 {
@@ -23,8 +24,9 @@ enum Status : int {
 void set_error(const std::string& msg);
 
 // Count of kernels this library launched (bench.py's gpu_launches).
-extern unsigned long long g_launches;
-inline void count_launch() { ++g_launches; }
+// (atomic: engines of an in-process partition group step on separate threads)
+extern std::atomic<unsigned long long> g_launches;
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct Fail {
   int code;

@@ -11,12 +11,14 @@
 // (model.hpp:117-153) is the interchange format at the C-ABI.
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/d2ft_b200.h"
 #include "../../include/d2ft_b200_engine.h"
 #include "common.cuh"
+#include "exchange.cuh"
 #include "gemm_sm100.cuh"
 #include "sched.cuh"
 #include "step_common.cuh"
@@ -55,6 +57,7 @@ enum Phase {
   PH_LN_BWD,
   PH_EMBED_W,
   PH_SGD,
+  PH_EXCH,  // head-partition exchange (partitioned engines only)
   PH_COUNT
 };
 
@@ -101,6 +104,10 @@ struct Engine {
   CompactLists lists{};
   int *g1_tiles, *g1_count, *g4_tiles, *g4_count;
   int *ord_act, *ord_full, *ord_head;  // cost orders (plan_kernel)
+  // head partition (exchange.cuh): null = the whole model on this GPU
+  std::unique_ptr<Exchange> ex;
+  int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
+  bool partitioned() const { return ex && ex->world > 1; }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
                                        // (the variable-K GEMMs; uniform ones stay static)
   enum { C_G3, C_G5, C_G7, C_G8 };
@@ -297,6 +304,7 @@ struct Engine {
     ord_full = dalloc<int>(L * Bm, owned);
     ord_head = dalloc<int>(L * H, owned);
     ctrs = dalloc<int>((L + 1) * 8, owned);
+    full_any = dalloc<int>(L * Bm, owned);
     sched_counter = dalloc<unsigned int>(1, owned);
     err = dalloc<int>(1, owned);
     gmax = dalloc<float>(1, owned);
@@ -443,8 +451,14 @@ struct Engine {
       mark(PH_ATTN_F);
       launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
+      // partitioned: partial block output, residual added once (rank 0), then summed across ranks
+      const float* xres = partitioned() && ex->rank != 0 ? nullptr : x + l * xs;
       gemm_tokN<G3, 1>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
-                       P + seg[S_B2].off + (size_t)l * d, x + l * xs, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
+                       P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
+      if (partitioned()) {
+        mark(PH_EXCH);
+        ex->allreduce_sum(x + (l + 1) * xs, (size_t)D.B * T * d, st);
+      }
     }
     mark(PH_HEAD);
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
@@ -477,11 +491,15 @@ struct Engine {
       mark(PH_G8);
       gemm_tokN<G8, 1>(tm_W1, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
                        ord_full + l * Bm, ctr(l, C_G8));
+      if (partitioned()) {
+        mark(PH_EXCH);
+        ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
+      }
       mark(PH_BIAS);
       launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
                          G + seg[S_B2].off + (size_t)l * d, st);
       mark(PH_LN_BWD);
-      launch_ln_bwd_prep(D, l, lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, dCT, part_cs,
+      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, dCT, part_cs,
                          gmax, st);
     }
     mark(PH_EMBED_W);
@@ -510,6 +528,12 @@ struct Engine {
 
   // per-sample codes already in codes_exp: compaction + plan
   void compact_and_plan() {
+    if (partitioned()) {  // keep the global Full counts, then drop the heads other ranks own
+      launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
+      D2FT_CUDA(cudaMemcpyAsync(full_any, lists.full_hcnt, (size_t)D.L * D.Bmax * sizeof(int),
+                                cudaMemcpyDeviceToDevice, st));
+      launch_mask_rows(codes_exp, D.K(), D.Bmax, D.H, ex->rank, ex->world, st);
+    }
     launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
     launch_plan(D, lists.act_cnt, lists.full_hcnt, lists.full_cnt,
                 Plan{g1_tiles, g1_count, g4_tiles, g4_count, ord_act, ord_full, ord_head}, st);
@@ -668,6 +692,52 @@ int d2ft_engine_get_velocity(d2ft_engine* e, double* flat) {
 
 int d2ft_engine_get_grads(d2ft_engine* e, double* flat) {
   return guarded([&] { e->e->get_arena(e->e->G, flat); });
+}
+
+int d2ft_nccl_unique_id(uint8_t* id_out) {
+  return guarded([&] {
+    D2FT_REQUIRE(id_out, kInput, "nccl_unique_id: null argument");
+    nccl_unique_id(id_out);
+  });
+}
+
+int d2ft_engine_partition_nccl(d2ft_engine* h, int rank, int world, const uint8_t* id) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && id, kInput, "partition: null argument");
+    D2FT_REQUIRE(world >= 1 && rank >= 0 && rank < world, kConfig, "partition: rank out of range");
+    Engine& E = *h->e;
+    D2FT_CUDA(cudaStreamSynchronize(E.st));
+    E.ex = make_nccl_exchange(rank, world, id);
+  });
+}
+
+struct d2ft_local_group {
+  LocalGroup* g;
+};
+
+int d2ft_local_group_create(int world, d2ft_local_group** out) {
+  return guarded([&] {
+    D2FT_REQUIRE(out, kInput, "local_group_create: null argument");
+    *out = new d2ft_local_group{local_group_create(world)};
+  });
+}
+
+int d2ft_local_group_destroy(d2ft_local_group* g) {
+  return guarded([&] {
+    if (g) {
+      local_group_destroy(g->g);
+      delete g;
+    }
+  });
+}
+
+int d2ft_engine_partition_local(d2ft_engine* h, d2ft_local_group* g, int rank) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && g, kInput, "partition: null argument");
+    Engine& E = *h->e;
+    D2FT_CUDA(cudaStreamSynchronize(E.st));
+    E.ex = make_local_exchange(g->g, rank);
+  });
 }
 
 int d2ft_engine_forward_backward(d2ft_engine* h, const float* samples, const int32_t* labels, int n,

@@ -174,6 +174,7 @@ struct G3 {
   };
   struct Row {
     float bias;
+    float xi[16];  // residual of the warp's next chunk (prefetched one chunk ahead)
   };
   __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
   __device__ void tile(int t, int rank, Tile& c) const {
@@ -197,13 +198,23 @@ struct G3 {
     const uint8_t code = codes[(size_t)(l * D.H + hm) * D.Bmax + c.s];
     r.bias = (code == 1 || code == 2) ? b2[m] : 0.f;  // p_s adds nothing (model.cpp:458)
   }
+  // xin == nullptr: partial block output of a head partition (the residual is
+  // added by partition rank 0 only, so the exchange sum carries it once)
+  __device__ void prefetch(const Tile& c, int row, int col0, Row& r) const {
+    const int m = c.mt * 128 + row;
+    if (m >= D.d || col0 >= D.T) return;
+    const size_t o0 = ((size_t)c.s * D.T + col0) * D.d + m;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r.xi[i] = (xin && col0 + i < D.T) ? __ldg(xin + o0 + (size_t)i * D.d) : 0.f;
+  }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
-    if (m >= D.d) return;
+    if (m >= D.d || col0 >= D.T) return;
     const size_t o0 = ((size_t)c.s * D.T + col0) * D.d + m;
-    float xi[16];  // batch the residual loads ahead of the stores
+    float xi[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) xi[i] = col0 + i < D.T ? __ldg(xin + o0 + (size_t)i * D.d) : 0.f;
+    for (int i = 0; i < 16; ++i) xi[i] = r.xi[i];
+    prefetch(c, row, col0 + 16 * kEpiGroups, r);
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (col0 + i < D.T) xout[o0 + (size_t)i * D.d] = xi[i] + v[i] + r.bias;

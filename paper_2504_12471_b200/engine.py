@@ -96,6 +96,7 @@ class SubnetModel:
     def __init__(self, config: ModelConfig, max_batch: int, params: np.ndarray | None = None):
         self.config = config
         self.max_batch = max_batch
+        self.partition = None  # partition.HeadPartition once joined to a head partition
         self._h = C.c_void_p()
         c = config._c()
         L = lib()
@@ -222,7 +223,7 @@ class SubnetModel:
         check(lib().d2ft_engine_set_profiling(self._h, C.c_int(1 if on else 0)))
 
     PHASES = ("sched", "embed", "ln", "G1", "attn_fwd", "G3", "head", "G4", "attn_bwd", "G5", "G7", "G8", "bias",
-              "ln_bwd", "embed_wgrad", "sgd")
+              "ln_bwd", "embed_wgrad", "sgd", "exchange")
 
     def phase_ms(self):
         out = np.zeros(len(self.PHASES))
