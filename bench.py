@@ -211,6 +211,14 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def global_codes(bwd, fwd, capf, capo, B):
+    """Global K x B schedule for the partition's cost-unit balance report (the
+    GPU schedule is bit-identical to it, tests/test_sched_gpu.py)."""
+    from paper_2504_12471_b200 import scheduler as S
+    return S.knapsack_schedule(S.ScoreTable(L * H, B, fwd, bwd), S.CostModel(),
+                               S.Capacities(capf.tolist(), capo.tolist())).codes
+
+
 def run_ours(args):
     rank, local, world = dist_env()
     from paper_2504_12471_b200 import _lib
@@ -225,11 +233,19 @@ def run_ours(args):
         torch.cuda.set_device(local)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
-    B = args.batch
+    # N > 1: head partition (partition.py), weak scaling: the
+    # global batch grows with N so each rank's share of head-sample cells stays
+    # that of the 1-GPU batch; every rank holds the whole batch.
+    B = args.batch * world
     K = L * H
     x, y, bwd, fwd, capf, capo = workload(B)
     cfg = E.VIT_B16
     m = E.SubnetModel(cfg, B)
+    part = None
+    if dist:
+        from paper_2504_12471_b200 import partition as PT
+        part = PT.HeadPartition(H, rank, world)
+        PT.join_nccl(m, part)
     cm = S.CostModel()
     st = S.ScoreTable(K, B, fwd, bwd)
     caps = S.Capacities(capf.tolist(), capo.tolist())
@@ -256,10 +272,27 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     launches = (l1 - l0) * args.steps // (args.steps + args.warmup) if args.steps + args.warmup else 0
-    value = world * B / (ms_step * 1e-3)
+    value = B / (ms_step * 1e-3)
+    part_info = None
+    if dist:  # per-rank busy time (step minus time spent inside the exchange) -> max / mean
+        import torch
+        busy = torch.tensor([ms.value / args.steps - phases.get("exchange", 0.0)], device="cuda")
+        allb = [torch.zeros_like(busy) for _ in range(world)]
+        dist.all_gather(allb, busy)
+        bl = [float(b.item()) for b in allb]
     codes_exp = np.zeros((K, B), np.uint8)
-    _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes_exp)))
+    _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes_exp)))  # this rank's rows (others: p_s)
     fl, alg_total = gemm_flops(codes_exp, B)
+    if dist:
+        glob = global_codes(bwd, fwd, capf, capo, B)
+        _, unit_ratio = PT.busy_units(glob, H, world)
+        part_info = {"mapping": "head h -> rank h % N (tensor parallel over heads)",
+                     "heads_per_rank": [len(PT.HeadPartition(H, r, world).owned_heads()) for r in range(world)],
+                     "busy_ms_per_rank": [round(b, 3) for b in bl],
+                     "busy_max_over_mean": round(max(bl) / (sum(bl) / len(bl)), 4),
+                     "cost_units_max_over_mean": round(unit_ratio, 4),
+                     "exchange_ms_per_step": round(phases.get("exchange", 0.0), 3),
+                     "exchange_bytes_per_step": 2 * L * B * T * D * 4}
     # ---- end to end through the C-ABI with pinned host buffers
     lib.d2ft_host_alloc.restype = C.c_void_p
     nbytes = x.nbytes
@@ -332,14 +365,15 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "fp16",
             "data": "synthetic (make_synthetic_dataset noise 0.5 seed 7; scores U[0,10) make_rng(1,0))",
-            "config": {"workload": "ViT-B/16 D2FT fine-tune step, batch 64, per-sample schedule (BASELINE configs[1])",
+            "config": {"workload": f"ViT-B/16 D2FT fine-tune step, batch {B}, per-sample schedule (BASELINE configs[1])",
                        "model": "ViT-B/16 subnet transformer (L12 H12 d768 ffn3072 T197, 144 head-subnets)",
-                       "global_batch": B * world, "seq_len": T,
-                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas (head-partitioned exchange: DESIGN.md §6)",
+                       "global_batch": B, "seq_len": T,
+                       "parallelism": "1 GPU" if world == 1 else f"head partition over {world} GPUs, NCCL all-reduce of "
+                                                                   "per-block partial outputs / dxn (DESIGN.md §6)",
                        "budget": f"{(2 * B) // 5} p_f + {(2 * B) // 5} p_o of {B} per row, cf=2 cb=3",
                        "l2": "working set > 126 MB L2 (no flush needed)"},
             "loss": loss.value,
-            "e2e": {"value": world * B / (e2e_step * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": B / (e2e_step * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": "G1 grouped tcgen05 GEMM ([Wq|Wk|Wv|W1] x xn, active heads)",
@@ -356,6 +390,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cb,
         }
+        if part_info:
+            line["partition"] = part_info
         print(json.dumps(line))
     m.close()
     if dist:
