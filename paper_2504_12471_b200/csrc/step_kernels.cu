@@ -578,8 +578,9 @@ __device__ __forceinline__ void store_frag_T(const float (&o)[DH / 8][4], float 
 
 // Forward: one warp per 16-query strip (blockDim = 32 * TQ/16), online softmax
 // over 32-key chunks.
-template <int DH>
-__global__ void __launch_bounds__(512) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
+// MINB = 2: two CTAs per SM (T <= 208, 416 threads, <= 72 registers)
+template <int DH, int MINB>
+__global__ void __launch_bounds__(MINB == 2 ? 416 : 512, MINB) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
                                                        const act_t* QKV, act_t* OGT, float* lse) {
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
@@ -918,16 +919,19 @@ void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float*
 void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OGT,
                      float* lse, cudaStream_t st) {
   dim3 grid(D.H, D.B);
+  auto go = [&](auto kern, int dh) {
+    const size_t sm = attn_fwd_smem(dh, D.TQ);
+    D2FT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OGT, lse);
+    count_launch();
+  };
+  const bool two = D.TQ * 2 <= 416;
   if (D.dh == 64) {
-    const size_t sm = attn_fwd_smem(64, D.TQ);
-    D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<64><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OGT, lse);
-    count_launch();
+    if (two) go(attn_fwd_kernel<64, 2>, 64);
+    else go(attn_fwd_kernel<64, 1>, 64);
   } else if (D.dh == 32) {
-    const size_t sm = attn_fwd_smem(32, D.TQ);
-    D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<32><<<grid, D.TQ * 2, sm, st>>>(D, l, act_heads, act_cnt, Y1, OGT, lse);
-    count_launch();
+    if (two) go(attn_fwd_kernel<32, 2>, 32);
+    else go(attn_fwd_kernel<32, 1>, 32);
   } else {
     throw Fail{kConfig, "attention: head_dim must be 32 or 64"};
   }
