@@ -14,6 +14,8 @@ extern "C" {
 int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int K, int bn, float* D);
 /* MN-major B: D[m][n] = sum_k A[m][k] BT[k][n] (BT row-major K x N); bn 208 / 64, negative = CTA pair. */
 int d2ft_test_gemm_mn(const uint16_t* A, const uint16_t* BT, int M, int N, int K, int bn, float* D);
+/* Both MN-major: D[m][n] = sum_k AT[k][m] BT[k][n] (CTA pair, BN 208). */
+int d2ft_test_gemm_mn_ab(const uint16_t* AT, const uint16_t* BT, int M, int N, int K, float* D);
 /* Tokens as N: D[p][m][t] = sum_k A[m][k] X[p][t][k] for t < T (T-row planes). */
 int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, int K, int P, float* D);
 /* Tokens as K: D[m][n] = sum_p sum_{t<T} XT[p][m][t] YT[p][n][t]; pitch TP >= T. */

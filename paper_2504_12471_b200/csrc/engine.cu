@@ -80,7 +80,7 @@ struct Engine {
   Seg seg[S_N];
   size_t nparam = 0;
   float *P = nullptr, *V = nullptr, *G = nullptr;
-  act_t *W1T_bf, *W1_bf, *W2T_bf, *W2_bf, *WeT_bf;
+  act_t *W1T_bf, *W2T_bf, *WeT_bf;  // fp16 operand copies (G4 / G8 read W2T / W1T MN-major)
 
   // activations
   float* x;       // [L+1][Bmax][T][d]
@@ -127,7 +127,7 @@ struct Engine {
   uint8_t* h_codes = nullptr;
 
   // tensor maps
-  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_W2, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_W1,
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT,
       tm_inpT;
 
   // profiling
@@ -236,9 +236,7 @@ struct Engine {
     V = dalloc<float>(nparam, owned);
     G = dalloc<float>(nparam, owned);
     W1T_bf = dalloc<act_t>(L * H * PQ * d, owned);
-    W1_bf = dalloc<act_t>(L * H * PQ * d, owned);
     W2T_bf = dalloc<act_t>(L * d * H * PO, owned);
-    W2_bf = dalloc<act_t>(L * d * H * PO, owned);
     WeT_bf = dalloc<act_t>(d * d, owned);
 
     x = dalloc<float>((L + 1) * Bm * T * d, owned);
@@ -323,8 +321,6 @@ struct Engine {
     tm_WeT = make_tmap_f16_3d(WeT_bf, d, d, 1, d * 2, d * d * 2, 64);
     tm_W1T = make_tmap_f16_3d(W1T_bf, d, H * PQ, L, d * 2, H * PQ * d * 2, 64);
     tm_W2T = make_tmap_f16_3d(W2T_bf, H * PO, d, L, H * PO * 2, d * H * PO * 2, 64);
-    tm_W2 = make_tmap_f16_3d(W2_bf, d, H * PO, L, d * 2, H * PO * d * 2, 64);
-    tm_W1 = make_tmap_f16_3d(W1_bf, H * PQ, d, L, H * PQ * 2, d * H * PQ * 2, 64);
     tm_dCT = make_tmap_f16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
     tm_dY1T = make_tmap_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
     // B operands, tokens as N (box BNt/2: each CTA of a pair loads half, multicast)
@@ -386,12 +382,6 @@ struct Engine {
     launch_f32_to_act(P + seg[S_W1T].off, W1T_bf, seg[S_W1T].n, st);
     launch_f32_to_act(P + seg[S_W2T].off, W2T_bf, seg[S_W2T].n, st);
     launch_f32_to_act(P + seg[S_WET].off, WeT_bf, seg[S_WET].n, st);
-    refresh_transposes(nullptr);
-  }
-  void refresh_transposes(const int* full_cnt) {
-    // W1_bf[l][m][h*PQ+f] = W1T_bf[l][h*PQ+f][m];  W2_bf[l][h*PO+f][m] = W2T_bf[l][m][h*PO+f]
-    launch_transpose_bf16(W1T_bf, W1_bf, D.L, D.H * D.PQ, D.d, D.PQ, D.H, full_cnt, st);
-    launch_transpose_bf16_colheads(W2T_bf, W2_bf, D.L, D.d, D.H * D.PO, D.PO, D.H, full_cnt, st);
   }
 
   void set_params(const double* flat) {
@@ -411,20 +401,21 @@ struct Engine {
   // ---------------------------------------------------------------- GEMM dispatch
   // Tokens-as-N GEMMs on CTA pairs; BMN = 1: B is a feature-major buffer
   // read MN-major (its 64-token blocks cost more shared memory per stage).
-  template <template <int> class Prob, int BMN = 0, class... Args>
+  // AMN = 1: A (weights) read MN-major from the other GEMM's copy.
+  template <template <int> class Prob, int BMN = 0, int AMN = 0, class... Args>
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2, BMN>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2, BMN, AMN>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2, BMN>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2, BMN, AMN>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        launch_gemm<Prob<208>, GemmShape<208, BMN ? 4 : 5, 0, 4, 2, BMN>>(a, b, Prob<208>{args...}, 0, st);
+        launch_gemm<Prob<208>, GemmShape<208, BMN ? 4 : 5, 0, 4, 2, BMN, AMN>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2, BMN>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2, BMN, AMN>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
@@ -473,7 +464,7 @@ struct Engine {
       const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
-      gemm_tokN<G4>(tm_W2, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
+      gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
                     (const act_t*)ZTl, dO, dY1T, part_db1, (const float*)gmax);
       mark(PH_ATTN_B);
       launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T, st);
@@ -489,7 +480,7 @@ struct Engine {
                   ord_head + l * H, ctr(l, C_G7)},
           0, st);
       mark(PH_G8);
-      gemm_tokN<G8, 1>(tm_W1, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
+      gemm_tokN<G8, 1, 1>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
                        ord_full + l * Bm, ctr(l, C_G8));
       if (partitioned()) {
         mark(PH_EXCH);
@@ -523,7 +514,6 @@ struct Engine {
     sgd(S_POS, nullptr, nullptr);
     sgd(S_WC, nullptr, nullptr);
     sgd(S_BC, nullptr, nullptr);
-    refresh_transposes(fc);
   }
 
   // per-sample codes already in codes_exp: compaction + plan

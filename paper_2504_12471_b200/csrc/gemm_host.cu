@@ -304,6 +304,23 @@ int d2ft_test_gemm_mn(const uint16_t* A, const uint16_t* BT, int M, int N, int K
   });
 }
 
+int d2ft_test_gemm_mn_ab(const uint16_t* AT, const uint16_t* BT, int M, int N, int K, float* D) {
+  return guarded([&] {
+    D2FT_REQUIRE(K % 8 == 0 && N % 8 == 0 && M % 8 == 0, kInput, "M, N and K must be multiples of 8");
+    Dev<uint16_t> dA((size_t)K * M), dB((size_t)K * N);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemcpy(dA.p, AT, (size_t)K * M * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(dB.p, BT, (size_t)K * N * 2, cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
+    CUtensorMap a = make_tmap_bf16_3d(dA.p, M, K, 1, (uint64_t)M * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dB.p, N, K, 1, (uint64_t)N * 2, (uint64_t)K * N * 2, 64);
+    launch_gemm<DenseMNProb<208>, GemmShape<208, 4, 1, 4, 2, 1, 1>>(a, b, DenseMNProb<208>{M, N, K, 1, dD.p}, 0,
+                                                                     nullptr);
+    D2FT_CUDA(cudaDeviceSynchronize());
+    D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
 int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, int K, int P, float* D) {
   return guarded([&] {
     Dev<uint16_t> dA((size_t)M * K), dX((size_t)P * T * K + 256 * K);

@@ -75,10 +75,13 @@ template <class P>
 struct has_counter<P, std::void_t<decltype(std::declval<P>().ctr)>> : std::true_type {};
 constexpr int kTileQ = 4;
 
-template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0>
+// AMN: A operand layout.  0 = K-major; 1 = MN-major (A stored [K][M] with M
+// contiguous, e.g. a weight matrix kept in the other GEMM's orientation): the
+// two 64-row halves of the tile are two 64(M) x 64(K) boxes, LBO = 8 KB.
+template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0, int AMN_ = 0>
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
-  static constexpr int BMN = BMN_;
+  static constexpr int BMN = BMN_, AMN = AMN_;
   static constexpr int NBLK = (BN + 63) / 64;  // MN-major B: 64-wide N blocks
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
@@ -182,8 +185,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           const KCoord k = prob.kcoord(c, kb);
           uint8_t* a = sA + stage * S::A_BYTES;
           ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-          ptx::tma_load_3d(a, &tmA, &full[stage], k.ax, k.ay0, k.az);
-          ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ax, k.ay1, k.az);
+          if constexpr (S::AMN) {  // boxes of 64 M (inner) x 64 K rows
+            ptx::tma_load_3d(a, &tmA, &full[stage], k.ay0, k.ax, k.az);
+            ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ay1, k.ax, k.az);
+          } else {
+            ptx::tma_load_3d(a, &tmA, &full[stage], k.ax, k.ay0, k.az);
+            ptx::tma_load_3d(a + S::A_BYTES / 2, &tmA, &full[stage], k.ax, k.ay1, k.az);
+          }
           if constexpr (S::BMN) {  // k.bx = first N element, k.by = first K row
             for (int j = rank; j < S::NBLK; j += S::CLUSTER) {
               uint8_t* b = sB + stage * S::B_BYTES + j * (64 * S::BK * 2);
@@ -220,39 +228,47 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_m128(S::BN, S::FMT) | (S::BMN ? (1u << 16) : 0u);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for_each_tile(true, [&](int t) {
-        typename P::Tile c;
-        prob.tile(t, rank, c);
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // The whole warp runs the MMA loop (warp-uniform control flow keeps the
+    // descriptors in uniform registers); one elected lane issues the UMMAs
+    // and commits.
+    constexpr uint32_t idesc =
+        ptx::idesc_f16_m128(S::BN, S::FMT) | (S::AMN ? (1u << 15) : 0u) | (S::BMN ? (1u << 16) : 0u);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for_each_tile(lane == 0, [&](int t) {
+      typename P::Tile c;
+      prob.tile(t, rank, c);
+      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem + acc * 256;
+      for (int kb = 0; kb < c.nkb; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t d = tmem + acc * 256;
-        for (int kb = 0; kb < c.nkb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint64_t ad = ptx::desc_sw128(ptx::smem_u32(sA + stage * S::A_BYTES));
-          const uint32_t bs = ptx::smem_u32(sB + stage * S::B_BYTES);
-          const uint64_t bd = S::BMN ? ptx::desc_sw128_mn(bs, 64 * S::BK * 2) : ptx::desc_sw128(bs);
-          // K step of 16: +32 B along a K-major row, or +16 rows (2 KB) of an MN-major block
-          constexpr uint64_t bstep = S::BMN ? (16 * 128) >> 4 : 2;
+        const uint32_t as = ptx::smem_u32(sA + stage * S::A_BYTES);
+        const uint64_t ad = S::AMN ? ptx::desc_sw128_mn(as, S::A_BYTES / 2) : ptx::desc_sw128(as);
+        const uint32_t bs = ptx::smem_u32(sB + stage * S::B_BYTES);
+        const uint64_t bd = S::BMN ? ptx::desc_sw128_mn(bs, 64 * S::BK * 2) : ptx::desc_sw128(bs);
+        // K step of 16: +32 B along a K-major row, or +16 rows (2 KB) of an MN-major block
+        constexpr uint64_t astep = S::AMN ? (16 * 128) >> 4 : 2;
+        constexpr uint64_t bstep = S::BMN ? (16 * 128) >> 4 : 2;
+        if (ptx::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
-            ptx::umma_bf16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
+            ptx::umma_bf16(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
           if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
           else ptx::umma_commit(&empty[stage]);
-          if (++stage == S::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        ptx::umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      });
-    }
+        __syncwarp();
+        if (++stage == S::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    });
   } else if (warp >= 4) {
     const int q = warp & 3;         // TMEM lane quarter
     const int e = (warp - 4) >> 2;  // column group
@@ -262,16 +278,21 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     for_each_tile(lane == 0, [&](int t) {
       typename P::Tile c;
       prob.tile(t, rank, c);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      typename P::Row st;
-      prob.row_begin(c, row, st);
-      const uint32_t base = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
-      // Chunks of this warp: 16*e + i*16*EPI.  The accumulator is released to
-      // the MMA warp as soon as the warp's last TMEM load has landed.
+      // Chunks of this warp: 16*e + i*16*EPI.  Row state and the first
+      // chunk's epilogue operands are loaded before the accumulator wait (they
+      // do not depend on it), and the accumulator is released to the MMA warp
+      // as soon as the warp's last TMEM load has landed.
       const bool have = c.nkb > 0;
       const int nch = (S::BN - 16 * e + 16 * S::EPI - 1) / (16 * S::EPI);
       auto col_of = [&](int i) { return 16 * e + i * 16 * S::EPI; };
+      typename P::Row st;
+      prob.row_begin(c, row, st);
+      if constexpr (has_prefetch<P>::value) {
+        if (nch > 0) prob.prefetch(c, row, col_of(0), st);
+      }
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t base = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
       auto release = [&]() {
         ptx::tc_fence_before();
         __syncwarp();
@@ -287,27 +308,6 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         if (v[0] == 12345.f) prob.chunk(c, row, col_of(i), v, st);  // experiment: epilogue stores off
 #endif
       };
-#ifdef D2FT_EXP_DB
-      uint32_t b0[16], b1[16];
-      if (have && nch > 0) ptx::tmem_ld16_async(base + col_of(0), b0);
-      if (nch == 0) release();
-#pragma unroll 1
-      for (int i = 0; i < nch; i += 2) {
-        if (have) ptx::tmem_ld_wait(b0);
-        if (have && i + 1 < nch) ptx::tmem_ld16_async(base + col_of(i + 1), b1);
-        if (i + 1 >= nch) release();
-        process(b0, i);
-        if (i + 1 < nch) {
-          if (have) ptx::tmem_ld_wait(b1);
-          if (have && i + 2 < nch) ptx::tmem_ld16_async(base + col_of(i + 2), b0);
-          if (i + 2 >= nch) release();
-          process(b1, i + 1);
-        }
-      }
-#else
-      if constexpr (has_prefetch<P>::value) {
-        if (nch > 0) prob.prefetch(c, row, col_of(0), st);
-      }
 #pragma unroll 1
       for (int i = 0; i < nch; ++i) {
         uint32_t b0[16];
@@ -319,7 +319,6 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         process(b0, i);
       }
       if (nch == 0) release();
-#endif
       prob.row_end(c, row, e, st);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -472,29 +472,6 @@ __global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_
   }
 }
 
-template <bool kColHeads>
-__global__ void transpose_bf16_kernel(const act_t* in, act_t* out, int rows, int cols, int head_span, int H,
-                                      const int* full_cnt) {
-  __shared__ act_t tile[32][34];
-  const int b = blockIdx.z;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  if (full_cnt) {
-    const int h = kColHeads ? c0 / head_span : r0 / head_span;
-    if (h < H && full_cnt[b * H + h] == 0) return;
-  }
-  const act_t* src = in + (size_t)b * rows * cols;
-  act_t* dst = out + (size_t)b * rows * cols;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = r0 + i, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[i][threadIdx.x] = src[(size_t)r * cols + c];
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) dst[(size_t)c * rows + r] = tile[threadIdx.x][i];
-  }
-}
-
 __global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = to_act(in[i]);
@@ -1001,21 +978,6 @@ void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long l
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_transpose_bf16(const act_t* in, act_t* out, int batches, int rows, int cols, int head_rows, int H,
-                           const int* full_cnt, cudaStream_t st) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
-  transpose_bf16_kernel<false><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_rows, H, full_cnt);
-  count_launch();
-  D2FT_CUDA(cudaGetLastError());
-}
-
-void launch_transpose_bf16_colheads(const act_t* in, act_t* out, int batches, int rows, int cols, int head_cols, int H,
-                                    const int* full_cnt, cudaStream_t st) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batches);
-  transpose_bf16_kernel<true><<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, head_cols, H, full_cnt);
-  count_launch();
-  D2FT_CUDA(cudaGetLastError());
-}
 
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);

@@ -48,14 +48,6 @@ void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* 
 // (outer == 0: always touched).  pbf (may be null) receives the act_t copy.
 void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner, int H,
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st);
-// batched act_t transpose: out[b][c][r] = in[b][r][c]; rows r are grouped in
-// heads of `head_rows` (skip the tile when full_cnt[b*H + r/head_rows] == 0,
-// or never when full_cnt is null)
-void launch_transpose_bf16(const act_t* in, act_t* out, int batches, int rows, int cols, int head_rows, int H,
-                           const int* full_cnt, cudaStream_t st);
-// same, with the head grouping on the column index (for W2T -> W2)
-void launch_transpose_bf16_colheads(const act_t* in, act_t* out, int batches, int rows, int cols, int head_cols, int H,
-                                    const int* full_cnt, cudaStream_t st);
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st);
 
 }  // namespace d2ft_b200

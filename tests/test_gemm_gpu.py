@@ -55,6 +55,19 @@ def test_mn_major_b(M, N, K, bn):
     assert err < 1e-5, err
 
 
+@pytest.mark.parametrize("M,N,K", [(128, 208, 64), (384, 416, 448), (264, 200, 320)])
+def test_mn_major_a_and_b(M, N, K):
+    """A stored [K][M] and B stored [K][N], both read MN-major."""
+    rng = np.random.default_rng(M + 7 * N + K)
+    AT, ATf = bf16(rng.standard_normal((K, M)))
+    BT, BTf = bf16(rng.standard_normal((K, N)))
+    D = np.zeros((M, N), np.float32)
+    _call("d2ft_test_gemm_mn_ab", _lib.ptr(AT), _lib.ptr(BT), C.c_int(M), C.c_int(N), C.c_int(K), _lib.ptr(D))
+    ref = ATf.astype(np.float64).T @ BTf.astype(np.float64)
+    err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+    assert err < 1e-5, err
+
+
 def test_planes_tokens_as_n():
     M, T, K, P = 448, 197, 768, 5
     rng = np.random.default_rng(1)
