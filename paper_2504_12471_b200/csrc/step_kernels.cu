@@ -359,9 +359,12 @@ __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* po
 // db2 (model.cpp:250-252) and db1 (model.cpp:257) of block l: sums over the
 // Full samples of each head.  32 outputs per CTA (lane), samples split over
 // the 8 warps, warp partials combined in fixed order (deterministic).
-__global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
-                                   float* db1_l, float* db2_l) {
-  __shared__ float red[8][33];
+// 32 outputs per CTA, 32 warps striding over the samples (fixed order: warp
+// partials then lanes' sum over warps), so the per-layer reduction runs at
+// full memory parallelism despite only (d + H*fs)/32 CTAs.
+__global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs,
+                                                           const float* part_db1, float* db1_l, float* db2_l) {
+  __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   const int ntile = (D.T + 31) / 32;
@@ -371,7 +374,7 @@ __global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const fl
     if (i < D.d) {
       const int m = i, h = m / (D.d / D.H);
       const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
-      for (int s = warp; s < D.B; s += 8)
+      for (int s = warp; s < D.B; s += 32)
         if (row[s] == 1) {
 #pragma unroll 4
           for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
@@ -379,7 +382,7 @@ __global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const fl
     } else {
       const int q = i - D.d, h = q / D.fs, j = q % D.fs;
       const uint8_t* row = codes + (size_t)(l * D.H + h) * D.Bmax;
-      for (int s = warp; s < D.B; s += 8)
+      for (int s = warp; s < D.B; s += 32)
         if (row[s] == 1)
 #pragma unroll
           for (int e = 0; e < kEpiGroups; ++e) a += part_db1[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
@@ -389,7 +392,7 @@ __global__ void bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const fl
   __syncthreads();
   if (warp == 0 && i < nout) {
     float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
     if (i < D.d) db2_l[i] = t;
     else db1_l[i - D.d] = t;
   }
@@ -957,7 +960,7 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
 void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
                         float* db1_l, float* db2_l, cudaStream_t st) {
   const int n = D.d + D.H * D.fs;
-  bias_reduce_kernel<<<(n + 31) / 32, 256, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
+  bias_reduce_kernel<<<(n + 31) / 32, 1024, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
