@@ -127,7 +127,7 @@ struct Engine {
   uint8_t* h_codes = nullptr;
 
   // tensor maps
-  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT,
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_Q, tm_K, tm_V,
       tm_inpT;
 
   // profiling
@@ -327,6 +327,13 @@ struct Engine {
     tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt / 2);
     tm_xn = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, BNt / 2);
     tm_dC = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, BNt / 2);
+    // attention operands (tcgen05 path, dh = 64): Q / K / V column blocks of the QKV rows
+    if (D.dh == 64) {
+      const uint64_t W = 3 * D.dh;
+      tm_Q = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 128);
+      tm_K = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, D.TQ);
+      tm_V = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 64);
+    }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
     tm_OGT64 = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 64);
     // (tm_dY1T above doubles as G8's MN-major B)
@@ -440,7 +447,11 @@ struct Engine {
       gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
                     P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl);
       mark(PH_ATTN_F);
-      launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
+      if (D.dh == 64 && D.TQ <= 256)
+        launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, lists.act_heads, lists.act_cnt, OGTl, lse + (size_t)l * Bm * H * T,
+                           st);
+      else
+        launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
       // partitioned: partial block output, residual added once (rank 0), then summed across ranks
       const float* xres = partitioned() && ex->rank != 0 ? nullptr : x + l * xs;

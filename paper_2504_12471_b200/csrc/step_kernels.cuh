@@ -1,5 +1,6 @@
 // Non-GEMM kernels of the D2FT step (launch wrappers).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "step_common.cuh"
@@ -29,6 +30,12 @@ void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_
                      float* lse, cudaStream_t st);
 void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* full_hcnt, const act_t* Y1,
                      const act_t* OGT, const act_t* dO, const float* lse, act_t* dY1T, cudaStream_t st);
+// tcgen05 attention forward (attn_sm100.cu), dh = 64: tensor maps over the
+// whole QKV buffer [L][Bmax][H][T][3dh] with boxes of 64 x 128 (Q), 64 x TQ
+// (K), 64 x 64 (V) rows; planes (l*Bmax + s)*H + h
+void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
+                        const int* act_heads, const int* act_cnt, act_t* OGT, float* lse, cudaStream_t st);
+int sm_max_attn();
 // head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, dlogits, and dX = dL/dx_L
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st);
