@@ -181,7 +181,234 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
+// Backward, one CTA (4 warps) per (sample, Full head), keys as M (model.cpp
+// 262-271; FA2 order, deterministic):
+//   TMA: Q, K, V, dO tiles ([TQ rows][64], 128-byte swizzle).  Each tile is both
+//   a K-major operand (rows = M or N) and an MN-major B operand (rows = K,
+//   N = dh), so no transposed copies exist.
+//   D_q = rowsum(dO . O) (O from OGT), lse in log2 units -> shared vectors.
+//   per key tile (128 keys = TMEM lanes):
+//     S^T = K Q^T, dP^T = V dO^T          -> TMEM [0, TQ), [256, 256+TQ)
+//     P^T = exp2(S^T sl2 - lse), dS^T = P^T (dP^T - D): fp16, written back over
+//     the scores (A operands from TMEM) and dS^T also into shared memory
+//     dV = P^T dO, dK = dS^T Q / sqrt(dh)  -> TMEM [128,192), [384,448) -> dY1T
+//   dQ = dS K / sqrt(dh): A = dS^T from shared memory read MN-major (queries
+//   contiguous in 64-wide blocks), B = K  -> TMEM [0,64), [64,128) -> dY1T
+struct AttnBwdArgs {
+  Dims D;
+  int l;
+  const int* full_heads;
+  const int* full_hcnt;
+  const act_t* OGT;  // block l
+  const float* lse;  // block l
+  act_t* dY1T;       // [Bmax][H][PQ][TP]
+};
+
+__host__ __device__ inline int attn_bwd_tc_smem(int TQ) {
+  return 4 * TQ * 128 + 4 * TQ * 128 + 2 * TQ * 4 + 1024 + 64;
+}
+
+__global__ void __launch_bounds__(128, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmdO,
+                       const AttnBwdArgs a) {
+  const Dims& D = a.D;
+  const int s = blockIdx.y, slot = blockIdx.x;
+  if (s >= D.B || slot >= a.full_hcnt[s * D.L + a.l]) return;
+  const int h = a.full_heads[(s * D.L + a.l) * D.H + slot];
+  const int plane = (a.l * D.Bmax + s) * D.H + h;
+  const int TQ = D.TQ, T = D.T;
+  const int nkt = (T + kQTile - 1) / kQTile;
+  const size_t sh = (size_t)s * D.H + h;
+  const uint32_t tile_bytes = (uint32_t)TQ * 128;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + tile_bytes;
+  uint8_t* sV = sK + tile_bytes;
+  uint8_t* sdO = sV + tile_bytes;
+  uint8_t* sDS = sdO + tile_bytes;  // 4 query blocks x [TQ keys][128 B]
+  float* lse2 = reinterpret_cast<float*>(sDS + 4 * tile_bytes);
+  float* Dv = lse2 + TQ;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Dv + TQ);  // 0 load, 1 S/dP, 2 dV/dK, 3 dQ
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmQKV);
+    ptx::tma_prefetch(&tmdO);
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(&bar[i], 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc(tslot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bar[0], 4 * tile_bytes);
+    ptx::tma_load_3d(sQ, &tmQKV, &bar[0], 0, 0, plane);
+    ptx::tma_load_3d(sK, &tmQKV, &bar[0], 64, 0, plane);
+    ptx::tma_load_3d(sV, &tmQKV, &bar[0], 128, 0, plane);
+    ptx::tma_load_3d(sdO, &tmdO, &bar[0], 0, 0, (int)sh);
+  }
+  // lse (log2 units; +inf past T so P = 0) while the tiles land
+  for (int q = threadIdx.x; q < TQ; q += blockDim.x) lse2[q] = q < T ? a.lse[sh * T + q] : INFINITY;
+  ptx::mbar_wait(&bar[0], 0);
+  // D_q = sum_f dO[q][f] O[q][f]: dO row from the swizzled tile, O from OGT (coalesced over q)
+  for (int q = threadIdx.x; q < TQ; q += blockDim.x) {
+    float acc = 0.f;
+    if (q < T) {
+      const act_t* o = a.OGT + sh * D.PO * D.TP + q;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(sdO + q * 128 + ((c ^ (q & 7)) << 4));
+        const act_t* hv = reinterpret_cast<const act_t*>(&raw);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * __half2float(o[(size_t)(c * 8 + i) * D.TP]);
+      }
+    }
+    Dv[q] = acc;
+  }
+  __syncthreads();
+
+  const float sl2 = kLog2eF * 0.125f;
+  const float scale = 0.125f;  // 1 / sqrt(64)
+  const uint32_t idS = ptx::idesc_f16_m128(TQ, 0);                 // K-major A and B
+  const uint32_t idG = ptx::idesc_f16_m128(64, 0) | (1u << 16);    // B (dh-wide tile) MN-major
+  const uint32_t idQ = ptx::idesc_f16_m128(64, 0) | (1u << 15) | (1u << 16);  // A and B MN-major
+  const uint32_t lrow = (uint32_t)(warp * 32) << 16;
+  const uint32_t SA = 0, SB = 256;
+  act_t* dyt = a.dY1T + sh * D.PQ * D.TP;
+  const uint32_t sds = ptx::smem_u32(sDS);
+  for (int kt = 0; kt < nkt; ++kt) {
+    if (threadIdx.x == 0) {
+      ptx::tc_fence_after();
+      const uint64_t kd = ptx::desc_sw128(ptx::smem_u32(sK + kt * kQTile * 128));
+      const uint64_t vd = ptx::desc_sw128(ptx::smem_u32(sV + kt * kQTile * 128));
+      const uint64_t qd = ptx::desc_sw128(ptx::smem_u32(sQ));
+      const uint64_t od = ptx::desc_sw128(ptx::smem_u32(sdO));
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        ptx::umma_bf16(tmem + SA, kd + (uint64_t)(kk * 2), qd + (uint64_t)(kk * 2), idS, kk);
+        ptx::umma_bf16(tmem + SB, vd + (uint64_t)(kk * 2), od + (uint64_t)(kk * 2), idS, kk);
+      }
+      ptx::umma_commit(&bar[1]);
+    }
+    ptx::mbar_wait(&bar[1], kt & 1);
+    ptx::tc_fence_after();
+    const int k = kt * kQTile + threadIdx.x;  // this thread's key (TMEM lane)
+    const bool kv = k < T;
+    for (int c0 = 0; c0 < TQ; c0 += 16) {
+      float sv[16], dp[16];
+      ptx::tmem_ld16(tmem + lrow + SA + c0, sv);
+      ptx::tmem_ld16(tmem + lrow + SB + c0, dp);
+      float p[16], ds[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        p[i] = kv ? fast_exp2(fmaf(sv[i], sl2, -lse2[c0 + i])) : 0.f;
+        ds[i] = p[i] * (dp[i] - Dv[c0 + i]);
+      }
+      uint32_t pp[8], pd[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        __half2 a2 = __floats2half2_rn(p[2 * i], p[2 * i + 1]);
+        __half2 b2 = __floats2half2_rn(ds[2 * i], ds[2 * i + 1]);
+        pp[i] = *reinterpret_cast<uint32_t*>(&a2);
+        pd[i] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      ptx::tmem_st8(tmem + lrow + SA + (c0 >> 1), pp);
+      ptx::tmem_st8(tmem + lrow + SB + (c0 >> 1), pd);
+      // dS^T row k, queries c0..c0+15 -> query block c0/64, 16-byte chunks (c0%64)/8 (+1), swizzled
+      if (k < TQ) {  // rows past TQ would run into the next query block
+        const uint32_t rb = sds + (uint32_t)(c0 >> 6) * tile_bytes + (uint32_t)k * 128;
+        const int ch = (c0 & 63) >> 3;
+        ptx::st_shared_v4(rb + ((ch ^ (k & 7)) << 4), pd[0], pd[1], pd[2], pd[3]);
+        ptx::st_shared_v4(rb + (((ch + 1) ^ (k & 7)) << 4), pd[4], pd[5], pd[6], pd[7]);
+      }
+    }
+    ptx::tmem_st_wait();
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ptx::tc_fence_after();
+      for (int kk = 0; kk < TQ / 16; ++kk) {
+        const uint64_t od = ptx::desc_sw128_mn(ptx::smem_u32(sdO) + kk * 2048, 8192);
+        const uint64_t qd = ptx::desc_sw128_mn(ptx::smem_u32(sQ) + kk * 2048, 8192);
+        ptx::umma_ts(tmem + SA + 128, tmem + SA + kk * 8, od, idG, kk);  // dV += P^T dO
+        ptx::umma_ts(tmem + SB + 128, tmem + SB + kk * 8, qd, idG, kk);  // dK += dS^T Q
+      }
+      ptx::umma_commit(&bar[2]);
+    }
+    ptx::mbar_wait(&bar[2], kt & 1);
+    ptx::tc_fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float dv[16], dk[16];
+      ptx::tmem_ld16(tmem + lrow + SA + 128 + c0, dv);
+      ptx::tmem_ld16(tmem + lrow + SB + 128 + c0, dk);
+      if (kv) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          dyt[(size_t)(D.dh + c0 + i) * D.TP + k] = to_act(dk[i] * scale);
+          dyt[(size_t)(2 * D.dh + c0 + i) * D.TP + k] = to_act(dv[i]);
+        }
+      }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();  // TMEM regions free for the next key tile
+  }
+  // dQ = dS K: query tiles of 128 (two 64-wide MN-major blocks of dS^T each)
+  if (threadIdx.x == 0) {
+    ptx::tc_fence_after();
+    for (int qt = 0; qt < nkt; ++qt)
+      for (int kk = 0; kk < TQ / 16; ++kk) {
+        const uint64_t ad = ptx::desc_sw128_mn(sds + (uint32_t)(2 * qt) * tile_bytes + kk * 2048, tile_bytes);
+        const uint64_t bd = ptx::desc_sw128_mn(ptx::smem_u32(sK) + kk * 2048, 8192);
+        ptx::umma_bf16(tmem + 64 * qt, ad, bd, idQ, kk);
+      }
+    ptx::umma_commit(&bar[3]);
+  }
+  ptx::mbar_wait(&bar[3], 0);
+  ptx::tc_fence_after();
+  for (int qt = 0; qt < nkt; ++qt) {
+    const int q = qt * kQTile + threadIdx.x;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float dq[16];
+      ptx::tmem_ld16(tmem + lrow + 64 * qt + c0, dq);
+      if (q < T) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dyt[(size_t)(c0 + i) * D.TP + q] = to_act(dq[i] * scale);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
+
+void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const Dims& D, int l, const int* full_heads,
+                        const int* full_hcnt, const act_t* OGT, const float* lse, act_t* dY1T, cudaStream_t st) {
+  D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
+  const int sm = attn_bwd_tc_smem(D.TQ);
+  D2FT_REQUIRE(attn_bwd_tc_fits(D.TQ), kConfig, "tcgen05 attention backward: shared memory");
+  static bool attr = false;
+  if (!attr) {
+    D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  dim3 grid(D.H, D.B);
+  attn_bwd_tc_kernel<<<grid, 128, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, OGT, lse, dY1T});
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
 
 void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
                         const int* act_heads, const int* act_cnt, act_t* OGT, float* lse, cudaStream_t st) {
@@ -199,5 +426,6 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
 }
 
 int sm_max_attn() { return attn_tc_smem(256); }
+bool attn_bwd_tc_fits(int TQ) { return attn_bwd_tc_smem(TQ) <= 227 * 1024; }
 
 }  // namespace d2ft_b200

@@ -127,7 +127,7 @@ struct Engine {
   uint8_t* h_codes = nullptr;
 
   // tensor maps
-  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_Q, tm_K, tm_V,
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_Q, tm_K, tm_V, tm_dO,
       tm_inpT;
 
   // profiling
@@ -333,6 +333,7 @@ struct Engine {
       tm_Q = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 128);
       tm_K = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, D.TQ);
       tm_V = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 64);
+      tm_dO = make_tmap_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, D.TQ);
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
     tm_OGT64 = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 64);
@@ -478,7 +479,12 @@ struct Engine {
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
                     (const act_t*)ZTl, dO, dY1T, part_db1, (const float*)gmax);
       mark(PH_ATTN_B);
-      launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T, st);
+      if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
+        launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, OGTl, lse + (size_t)l * Bm * H * T,
+                           dY1T, st);
+      else
+        launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
+                        st);
       mark(PH_G5);
       launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2>>(
           tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
