@@ -205,7 +205,7 @@ struct AttnBwdArgs {
 };
 
 __host__ __device__ inline int attn_bwd_tc_smem(int TQ) {
-  return 4 * TQ * 128 + 4 * TQ * 128 + 2 * TQ * 4 + 1024 + 64;
+  return 4 * TQ * 128 + 4 * TQ * 128 + 1024;
 }
 
 __global__ void __launch_bounds__(128, 1)
@@ -228,10 +228,9 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* sV = sK + tile_bytes;
   uint8_t* sdO = sV + tile_bytes;
   uint8_t* sDS = sdO + tile_bytes;  // 4 query blocks x [TQ keys][128 B]
-  float* lse2 = reinterpret_cast<float*>(sDS + 4 * tile_bytes);
-  float* Dv = lse2 + TQ;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Dv + TQ);  // 0 load, 1 S/dP, 2 dV/dK, 3 dQ
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  __shared__ float lse2[256], Dv[256];  // statically shared: LDS, not generic loads
+  __shared__ uint64_t bar[4];             // 0 load, 1 S/dP, 2 dV/dK, 3 dQ
+  __shared__ uint32_t tslot[1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -252,23 +251,29 @@ __global__ void __launch_bounds__(128, 1)
     ptx::tma_load_3d(sV, &tmQKV, &bar[0], 128, 0, plane);
     ptx::tma_load_3d(sdO, &tmdO, &bar[0], 0, 0, (int)sh);
   }
-  // lse (log2 units; +inf past T so P = 0) while the tiles land
+  // lse (log2 units; +inf past T so P = 0) and the O rows for D, loaded while the tiles land
   for (int q = threadIdx.x; q < TQ; q += blockDim.x) lse2[q] = q < T ? a.lse[sh * T + q] : INFINITY;
-  ptx::mbar_wait(&bar[0], 0);
-  // D_q = sum_f dO[q][f] O[q][f]: dO row from the swizzled tile, O from OGT (coalesced over q)
-  for (int q = threadIdx.x; q < TQ; q += blockDim.x) {
-    float acc = 0.f;
+  for (int q0 = 0; q0 < TQ; q0 += blockDim.x) {
+    const int q = q0 + threadIdx.x;
+    act_t ov[64];
     if (q < T) {
       const act_t* o = a.OGT + sh * D.PO * D.TP + q;
+#pragma unroll
+      for (int f = 0; f < 64; ++f) ov[f] = o[(size_t)f * D.TP];
+    }
+    ptx::mbar_wait(&bar[0], 0);
+    // D_q = sum_f dO[q][f] O[q][f]: dO row from the swizzled tile
+    float acc = 0.f;
+    if (q < T) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint4 raw = *reinterpret_cast<const uint4*>(sdO + q * 128 + ((c ^ (q & 7)) << 4));
         const act_t* hv = reinterpret_cast<const act_t*>(&raw);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * __half2float(o[(size_t)(c * 8 + i) * D.TP]);
+        for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * __half2float(ov[c * 8 + i]);
       }
     }
-    Dv[q] = acc;
+    if (q < TQ) Dv[q] = acc;
   }
   __syncthreads();
 
@@ -401,7 +406,7 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
   D2FT_REQUIRE(attn_bwd_tc_fits(D.TQ), kConfig, "tcgen05 attention backward: shared memory");
   static bool attr = false;
   if (!attr) {
-    D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 223 * 1024));
     attr = true;
   }
   dim3 grid(D.H, D.B);
@@ -426,6 +431,6 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
 }
 
 int sm_max_attn() { return attn_tc_smem(256); }
-bool attn_bwd_tc_fits(int TQ) { return attn_bwd_tc_smem(TQ) <= 227 * 1024; }
+bool attn_bwd_tc_fits(int TQ) { return attn_bwd_tc_smem(TQ) + 4096 <= 227 * 1024; }  // + static shared
 
 }  // namespace d2ft_b200
