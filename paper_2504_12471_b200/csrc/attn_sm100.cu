@@ -41,143 +41,191 @@ constexpr float kLog2eF = 1.4426950408889634f;
 struct AttnFwdArgs {
   Dims D;
   int l;
+  const int* items;  // block l: (sample << 8 | active slot), plan_kernel
+  const int* count;  // block l: number of items
   const int* act_heads;
-  const int* act_cnt;
   act_t* OGT;  // block l
   float* lse;  // block l
 };
 
-__host__ __device__ inline int attn_tc_smem(int TQ) {
-  const int nkv = (TQ + 63) / 64;
-  return 2 * kQTile * 128 + TQ * 128 + nkv * 8192 + 1024 + 64;
+__host__ __device__ inline int attn_fwd_stage_bytes(int TQ) {
+  const int b = 2 * kQTile * 128 + TQ * 128 + ((TQ + 63) / 64) * 8192;
+  return (b + 1023) & ~1023;
 }
+__host__ __device__ inline int attn_tc_smem(int TQ) { return 2 * attn_fwd_stage_bytes(TQ) + 1024; }
 
-__global__ void __launch_bounds__(128, 2)
+// Persistent, warp-specialised: warp 0 TMA (two item stages), warp 1 MMA,
+// warp 2 TMEM allocator, warps 4-7 / 8-11 = softmax+epilogue of query tile
+// 0 / 1 (TMEM columns [0,256) / [256,512)), so both tiles of an item run in
+// parallel and the next item's operands land during the current one.
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const AttnFwdArgs a) {
   const Dims& D = a.D;
-  const int s = blockIdx.y, slot = blockIdx.x;
-  if (s >= D.B || slot >= a.act_cnt[s * D.L + a.l]) return;
-  const int h = a.act_heads[(s * D.L + a.l) * D.H + slot];
-  const int plane = (a.l * D.Bmax + s) * D.H + h;
   const int TQ = D.TQ, T = D.T;
   const int nkv = (TQ + 63) / 64, nqt = (T + kQTile - 1) / kQTile;
+  const int nitems = *a.count;
+  const uint32_t stage = attn_fwd_stage_bytes(TQ);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                  // nqt x [128 rows][128 B]
-  uint8_t* sK = sQ + 2 * kQTile * 128;  // [TQ rows][128 B]
-  uint8_t* sV = sK + TQ * 128;          // nkv x [64 keys][128 B]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + nkv * 8192);  // 0 load, 1 S done, 2 O done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+  __shared__ uint64_t load_full[2], load_empty[2], s_full[2], p_full[2], o_full[2], tfree[2];
+  __shared__ uint32_t tslot[1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmQ);
     ptx::tma_prefetch(&tmK);
     ptx::tma_prefetch(&tmV);
-    for (int i = 0; i < 3; ++i) ptx::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&load_full[i], 1);
+      ptx::mbar_init(&load_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&o_full[i], 1);
+      ptx::mbar_init(&tfree[i], 4);
+    }
     ptx::fence_barrier_init();
   }
-  if (warp == 0) ptx::tmem_alloc(tslot, 256);
+  if (warp == 2) ptx::tmem_alloc(tslot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (threadIdx.x == 0) {
-    ptx::mbar_arrive_expect_tx(&bar[0], (uint32_t)(nqt * kQTile * 128 + TQ * 128 + nkv * 8192));
-    for (int qt = 0; qt < nqt; ++qt) ptx::tma_load_3d(sQ + qt * kQTile * 128, &tmQ, &bar[0], 0, qt * kQTile, plane);
-    ptx::tma_load_3d(sK, &tmK, &bar[0], 64, 0, plane);
-    for (int j = 0; j < nkv; ++j) ptx::tma_load_3d(sV + j * 8192, &tmV, &bar[0], 128, 64 * j, plane);
-    ptx::mbar_wait(&bar[0], 0);
-  }
-  const float sl2 = kLog2eF * 0.125f;  // log2(e) / sqrt(64)
-  const uint32_t idS = ptx::idesc_f16_m128(TQ, 0);
-  const uint32_t idO = ptx::idesc_f16_m128(64, 0) | (1u << 16);  // B = V, MN-major
-  const uint32_t lrow = (uint32_t)(warp * 32) << 16;               // this warp's TMEM lane quarter
-  const size_t sh = (size_t)s * D.H + h;
-  for (int qt = 0; qt < nqt; ++qt) {
-    if (threadIdx.x == 0) {
-      ptx::tc_fence_after();
-      const uint64_t qd = ptx::desc_sw128(ptx::smem_u32(sQ + qt * kQTile * 128));
-      const uint64_t kd = ptx::desc_sw128(ptx::smem_u32(sK));
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) ptx::umma_bf16(tmem, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idS, kk);
-      ptx::umma_commit(&bar[1]);
-    }
-    ptx::mbar_wait(&bar[1], qt & 1);
-    ptx::tc_fence_after();
-    // row max over the valid keys (scores in log2 units); only the chunk that
-    // straddles T needs the key mask
-    const int cfull = T & ~15;  // chunks [0, cfull) hold valid keys only
-    float mx = -INFINITY;
-    for (int c0 = 0; c0 < TQ; c0 += 16) {
-      float v[16];
-      ptx::tmem_ld16(tmem + lrow + c0, v);
-      if (c0 < cfull) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) mx = fmaxf(mx, v[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (c0 + i < T) mx = fmaxf(mx, v[i]);
-      }
-    }
-    mx *= sl2;
-    // P = exp2(S * sl2 - max), fp16 pairs written back over the scores
-    float sum = 0.f;
-    for (int c0 = 0; c0 < TQ; c0 += 16) {
-      float v[16];
-      ptx::tmem_ld16(tmem + lrow + c0, v);
-      float p[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) p[i] = fast_exp2(fmaf(v[i], sl2, -mx));
-      if (c0 >= cfull) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (c0 + i >= T) p[i] = 0.f;
-      }
-      uint32_t pk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        sum += p[2 * i] + p[2 * i + 1];
-        __half2 hp = __floats2half2_rn(p[2 * i], p[2 * i + 1]);
-        pk[i] = *reinterpret_cast<uint32_t*>(&hp);
-      }
-      ptx::tmem_st8(tmem + lrow + (c0 >> 1), pk);
-    }
-    ptx::tmem_st_wait();
-    const int t = qt * kQTile + threadIdx.x;
-    if (t < T) a.lse[sh * T + t] = mx + log2f(sum);
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      ptx::tc_fence_after();
-      for (int kk = 0; kk < TQ / 16; ++kk) {
-        const uint32_t vb = ptx::smem_u32(sV + (kk >> 2) * 8192) + (kk & 3) * 2048;
-        ptx::umma_ts(tmem + 128, tmem + kk * 8, ptx::desc_sw128_mn(vb, 8192), idO, kk);
-      }
-      ptx::umma_commit(&bar[2]);
-    }
-    ptx::mbar_wait(&bar[2], qt & 1);
-    ptx::tc_fence_after();
-    const float inv = 1.f / sum;
-    act_t* o = a.OGT + sh * D.PO * D.TP + t;
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      float v[16];
-      ptx::tmem_ld16(tmem + lrow + 128 + c0, v);
-      if (t < T) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) o[(size_t)(c0 + i) * D.TP] = to_act(v[i] * inv);
-      }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();  // O and P read before the next tile's S overwrites the columns
-  }
+  auto decode = [&](int i, int& s, int& h) {
+    const int it = a.items[i];
+    s = it >> 8;
+    h = a.act_heads[(s * D.L + a.l) * D.H + (it & 255)];
+  };
+
   if (warp == 0) {
+    if (lane == 0) {
+      for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
+        const int buf = it & 1;
+        ptx::mbar_wait(&load_empty[buf], ((it >> 1) & 1) ^ 1);
+        int s, h;
+        decode(i, s, h);
+        const int plane = (a.l * D.Bmax + s) * D.H + h;
+        uint8_t* sQ = smem + buf * stage;
+        uint8_t* sK = sQ + 2 * kQTile * 128;
+        uint8_t* sV = sK + TQ * 128;
+        ptx::mbar_arrive_expect_tx(&load_full[buf], (uint32_t)(nqt * kQTile * 128 + TQ * 128 + nkv * 8192));
+        for (int qt = 0; qt < nqt; ++qt)
+          ptx::tma_load_3d(sQ + qt * kQTile * 128, &tmQ, &load_full[buf], 0, qt * kQTile, plane);
+        ptx::tma_load_3d(sK, &tmK, &load_full[buf], 64, 0, plane);
+        for (int j = 0; j < nkv; ++j) ptx::tma_load_3d(sV + j * 8192, &tmV, &load_full[buf], 128, 64 * j, plane);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = ptx::idesc_f16_m128(TQ, 0);
+    const uint32_t idO = ptx::idesc_f16_m128(64, 0) | (1u << 16);  // B = V, MN-major
+    for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
+      const int buf = it & 1;
+      ptx::mbar_wait(&load_full[buf], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t qb = ptx::smem_u32(smem + buf * stage);
+      const uint32_t kb = qb + 2 * kQTile * 128, vb = kb + TQ * 128;
+      for (int t = 0; t < nqt; ++t) {
+        ptx::mbar_wait(&tfree[t], (it & 1) ^ 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          const uint64_t qd = ptx::desc_sw128(qb + t * kQTile * 128), kd = ptx::desc_sw128(kb);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::umma_bf16(tmem + 256 * t, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idS, kk);
+          ptx::umma_commit(&s_full[t]);
+        }
+        __syncwarp();
+      }
+      for (int t = 0; t < nqt; ++t) {
+        ptx::mbar_wait(&p_full[t], it & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          for (int kk = 0; kk < TQ / 16; ++kk)
+            ptx::umma_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8,
+                         ptx::desc_sw128_mn(vb + (kk >> 2) * 8192 + (kk & 3) * 2048, 8192), idO, kk);
+          ptx::umma_commit(&o_full[t]);
+        }
+        __syncwarp();
+      }
+      if (ptx::elect_one()) ptx::umma_commit(&load_empty[buf]);
+      __syncwarp();
+    }
+  } else if (warp >= 4 && (warp - 4) / 4 < nqt) {
+    const int t = (warp - 4) / 4, q4 = warp & 3;
+    const uint32_t base = tmem + 256 * t + ((uint32_t)(q4 * 32) << 16);
+    const float sl2 = kLog2eF * 0.125f;  // log2(e) / sqrt(64)
+    const int cfull = T & ~15;           // chunks [0, cfull) hold valid keys only
+    const int row = t * kQTile + q4 * 32 + lane;  // query
+    for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
+      int s, h;
+      decode(i, s, h);
+      const size_t sh = (size_t)s * D.H + h;
+      ptx::mbar_wait(&s_full[t], it & 1);
+      ptx::tc_fence_after();
+      float mx = -INFINITY;
+      for (int c0 = 0; c0 < TQ; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(base + c0, v);
+        if (c0 < cfull) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < T) mx = fmaxf(mx, v[j]);
+        }
+      }
+      mx *= sl2;
+      float sum = 0.f;
+      for (int c0 = 0; c0 < TQ; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(base + c0, v);
+        float p[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) p[j] = fast_exp2(fmaf(v[j], sl2, -mx));
+        if (c0 >= cfull) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j >= T) p[j] = 0.f;
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          sum += p[2 * j] + p[2 * j + 1];
+          __half2 hp = __floats2half2_rn(p[2 * j], p[2 * j + 1]);
+          pk[j] = *reinterpret_cast<uint32_t*>(&hp);
+        }
+        ptx::tmem_st8(base + (c0 >> 1), pk);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      if (row < T) a.lse[sh * T + row] = mx + log2f(sum);
+      ptx::mbar_wait(&o_full[t], it & 1);
+      ptx::tc_fence_after();
+      const float inv = 1.f / sum;
+      act_t* o = a.OGT + sh * D.PO * D.TP + row;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(base + 128 + c0, v);
+        if (row < T) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[(size_t)(c0 + j) * D.TP] = to_act(v[j] * inv);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 256);
+    ptx::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -416,7 +464,8 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
 }
 
 void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
-                        const int* act_heads, const int* act_cnt, act_t* OGT, float* lse, cudaStream_t st) {
+                        const int* items, const int* count, const int* act_heads, act_t* OGT, float* lse,
+                        cudaStream_t st) {
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_tc_smem(D.TQ);
   static bool attr = false;
@@ -424,8 +473,7 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max_attn()));
     attr = true;
   }
-  dim3 grid(D.H, D.B);
-  attn_fwd_tc_kernel<<<grid, 128, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, act_heads, act_cnt, OGT, lse});
+  attn_fwd_tc_kernel<<<num_sms(), 384, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse});
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

@@ -104,6 +104,7 @@ struct Engine {
   CompactLists lists{};
   int *g1_tiles, *g1_count, *g4_tiles, *g4_count;
   int *ord_act, *ord_full, *ord_head;  // cost orders (plan_kernel)
+  int *af_items, *af_count, *ab_items, *ab_count;  // attention work lists (plan_kernel)
   // head partition (exchange.cuh): null = the whole model on this GPU
   std::unique_ptr<Exchange> ex;
   int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
@@ -303,6 +304,10 @@ struct Engine {
     ord_head = dalloc<int>(L * H, owned);
     ctrs = dalloc<int>((L + 1) * 8, owned);
     full_any = dalloc<int>(L * Bm, owned);
+    af_items = dalloc<int>(L * Bm * H, owned);
+    ab_items = dalloc<int>(L * Bm * H, owned);
+    af_count = dalloc<int>(L, owned);
+    ab_count = dalloc<int>(L, owned);
     sched_counter = dalloc<unsigned int>(1, owned);
     err = dalloc<int>(1, owned);
     gmax = dalloc<float>(1, owned);
@@ -449,8 +454,8 @@ struct Engine {
                     P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl);
       mark(PH_ATTN_F);
       if (D.dh == 64 && D.TQ <= 256)
-        launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, lists.act_heads, lists.act_cnt, OGTl, lse + (size_t)l * Bm * H * T,
-                           st);
+        launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, af_items + l * Bm * H, af_count + l, lists.act_heads, OGTl,
+                           lse + (size_t)l * Bm * H * T, st);
       else
         launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
@@ -543,7 +548,8 @@ struct Engine {
     }
     launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
     launch_plan(D, lists.act_cnt, lists.full_hcnt, lists.full_cnt,
-                Plan{g1_tiles, g1_count, g4_tiles, g4_count, ord_act, ord_full, ord_head}, st);
+                Plan{g1_tiles, g1_count, g4_tiles, g4_count, ord_act, ord_full, ord_head, af_items, af_count, ab_items,
+                     ab_count}, st);
   }
 
   void ensure_sched(int max_cols) {

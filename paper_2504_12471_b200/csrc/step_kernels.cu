@@ -33,7 +33,7 @@ __device__ __forceinline__ int desc_rank(const int* v, int n, int i) {
 
 __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, Plan pl) {
   const int l = blockIdx.x;
-  __shared__ int s1[1024], s4[1024], va[1024], vf[1024], vh[64];
+  __shared__ int s1[1024], s4[1024], va[1024], vf[1024], sa[1024], sf[1024], vh[64];
   int c1 = 0, c4 = 0;
   const int s = threadIdx.x;
   if (s < D.B) {
@@ -45,6 +45,8 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, co
   if (s < D.H) vh[s] = full_cnt[l * D.H + s];
   s1[threadIdx.x] = c1;
   s4[threadIdx.x] = c4;
+  sa[threadIdx.x] = s < D.B ? va[s] : 0;
+  sf[threadIdx.x] = s < D.B ? vf[s] : 0;
   __syncthreads();
   // cost orders of the dynamically scheduled GEMMs: samples by active / Full
   // head count (G3, G8), heads by Full sample count (G5, G7), largest first
@@ -53,15 +55,19 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, co
     pl.ord_full[l * D.Bmax + desc_rank(vf, D.B, s)] = s;
   }
   if (s < D.H) pl.ord_head[l * D.H + desc_rank(vh, D.H, s)] = s;
-  for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
-    int a1 = 0, a4 = 0;
+  for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scans
+    int a1 = 0, a4 = 0, aa = 0, af = 0;
     if ((int)threadIdx.x >= o) {
       a1 = s1[threadIdx.x - o];
       a4 = s4[threadIdx.x - o];
+      aa = sa[threadIdx.x - o];
+      af = sf[threadIdx.x - o];
     }
     __syncthreads();
     s1[threadIdx.x] += a1;
     s4[threadIdx.x] += a4;
+    sa[threadIdx.x] += aa;
+    sf[threadIdx.x] += af;
     __syncthreads();
   }
   const size_t cap = (size_t)D.Bmax * ((D.UQ * D.H + 1) / 2);
@@ -70,10 +76,16 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, co
     const int b1 = s1[s] - c1, b4 = s4[s] - c4;
     for (int i = 0; i < c1; ++i) pl.g1_tiles[l * cap + b1 + i] = (s << 16) | (4 * i);
     for (int i = 0; i < c4; ++i) pl.g4_tiles[l * cap4 + b4 + i] = (s << 16) | (4 * i);
+    // attention work items (sample, active / Full head slot) in sample order
+    const size_t capa = (size_t)D.Bmax * D.H;
+    for (int a = 0, b = sa[s] - va[s]; a < va[s]; ++a) pl.af_items[l * capa + b + a] = (s << 8) | a;
+    for (int a = 0, b = sf[s] - vf[s]; a < vf[s]; ++a) pl.ab_items[l * capa + b + a] = (s << 8) | a;
   }
   if (threadIdx.x == blockDim.x - 1) {
     pl.g1_count[l] = s1[threadIdx.x];
     pl.g4_count[l] = s4[threadIdx.x];
+    pl.af_count[l] = sa[threadIdx.x];
+    pl.ab_count[l] = sf[threadIdx.x];
   }
 }
 

@@ -17,6 +17,8 @@ struct Plan {
   int* ord_act;   // [L][Bmax] samples by decreasing active-head count (G3)
   int* ord_full;  // [L][Bmax] samples by decreasing Full-head count (G8)
   int* ord_head;  // [L][H] heads by decreasing Full-sample count (G5, G7)
+  int *af_items, *af_count;  // [L][Bmax*H] (sample << 8 | active slot) of the attention forward
+  int *ab_items, *ab_count;  // [L][Bmax*H] (sample << 8 | Full slot) of the attention backward
 };
 void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, const Plan& pl,
                  cudaStream_t st);
@@ -34,7 +36,8 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 // whole QKV buffer [L][Bmax][H][T][3dh] with boxes of 64 x 128 (Q), 64 x TQ
 // (K), 64 x 64 (V) rows; planes (l*Bmax + s)*H + h
 void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
-                        const int* act_heads, const int* act_cnt, act_t* OGT, float* lse, cudaStream_t st);
+                        const int* items, const int* count, const int* act_heads, act_t* OGT, float* lse,
+                        cudaStream_t st);
 int sm_max_attn();
 // tcgen05 attention backward (attn_sm100.cu), dh = 64: tmQKV = the K map above
 // (box 64 x TQ), tmdO over dO [Bmax][H][T][dh] with box 64 x TQ
