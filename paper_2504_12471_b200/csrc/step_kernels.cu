@@ -99,6 +99,7 @@ __device__ __forceinline__ void write_transposed(const act_t* tile, int pitch, i
   for (int m = warp; m < d; m += 8) outT[(size_t)m * TP + t0 + lane] = tile[lane * pitch + m];
 }
 
+template <int NV>
 __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inpT) {
   extern __shared__ __align__(16) unsigned char smem[];
   act_t* tile = reinterpret_cast<act_t*>(smem);
@@ -107,11 +108,14 @@ __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
-    for (int m = lane; m < D.d; m += 32) {
-      const float v = t < D.T ? x[((size_t)s * D.T + t) * D.d + m] : 0.f;
-      const act_t b = to_act(v);
-      tile[r * pitch + m] = b;
-      if (t < D.T) inp[((size_t)s * D.T + t) * D.d + m] = b;
+    float v[NV];  // the row's loads all in flight before any use
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = t < D.T ? x[((size_t)s * D.T + t) * D.d + lane + 32 * j] : 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const act_t b = to_act(v[j]);
+      tile[r * pitch + lane + 32 * j] = b;
+      if (t < D.T) inp[((size_t)s * D.T + t) * D.d + lane + 32 * j] = b;
     }
   }
   __syncthreads();
@@ -244,8 +248,9 @@ template <int NV>
 __global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                             double* loss_s, float* pooled_out, float* dlog_out, float* dX, float* gmax) {
   extern __shared__ __align__(16) unsigned char smem[];
-  float* part = reinterpret_cast<float*>(smem);  // [8][d]
-  float* pooled = part + 8 * D.d;                // [d]
+  const int nw = blockDim.x >> 5;
+  float* part = reinterpret_cast<float*>(smem);  // [nw][d]
+  float* pooled = part + nw * D.d;               // [d]
   float* dpooled = pooled + D.d;                 // [d]
   float* rowstat = dpooled + D.d;                // [T][2]
   __shared__ float logits[64], dlog[64];
@@ -255,7 +260,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   float acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.f;
-  for (int t = warp; t < D.T; t += 8) {
+  for (int t = warp; t < D.T; t += nw) {
     const float* row = xL + ((size_t)s * D.T + t) * D.d;
     float v[NV];
     float sum = 0.f;
@@ -285,12 +290,12 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   __syncthreads();
   for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
     float p = 0.f;
-    for (int w = 0; w < 8; ++w) p += part[w * D.d + m];
+    for (int w = 0; w < nw; ++w) p += part[w * D.d + m];
     pooled[m] = p / D.T;  // row_mean (linalg.cpp:101-105)
     pooled_out[(size_t)s * D.d + m] = pooled[m];
   }
   __syncthreads();
-  for (int c = warp; c < D.C; c += 8) {
+  for (int c = warp; c < D.C; c += nw) {
     float z = 0.f;
     for (int m = lane; m < D.d; m += 32) z += pooled[m] * Wc[(size_t)m * D.C + c];
     z = warp_sum(z);
@@ -321,7 +326,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   float dmean_l = 0.f;
   for (int m = lane; m < D.d; m += 32) dmean_l += dpooled[m];
   const float dmean = warp_sum(dmean_l) / D.d;
-  for (int t = warp; t < D.T; t += 8) {
+  for (int t = warp; t < D.T; t += nw) {
     const size_t ro = ((size_t)s * D.T + t) * D.d;
     const float mean = rowstat[2 * t], rstd = rowstat[2 * t + 1];
     float y[NV];
@@ -415,7 +420,7 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
   const size_t dd = (size_t)D.d * D.d;
   const size_t td = (size_t)D.T * D.d;
   const int ntile = (D.T + 31) / 32;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd + td + D.d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd + td;
        i += (size_t)gridDim.x * blockDim.x) {
     float a = 0.f;
     if (i < dd) {  // dW_embed (model.cpp:514), sum of the split-K partials
@@ -427,13 +432,26 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
 #pragma unroll 8
       for (int s = 0; s < D.B; ++s) a += dX[(size_t)s * td + q];
       dpos[q] = a;
-    } else {  // db_embed (model.cpp:515)
-      const int m = (int)(i - dd - td);
-      for (int s = 0; s < D.B; ++s)
-#pragma unroll 4
-        for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
-      dbe[m] = a;
     }
+  }
+}
+
+// out[c] = sum_r in[r][c]: 32 columns per CTA, 32 warps striding the rows,
+// fixed-order combine (deterministic).  db_embed (model.cpp:515) from the
+// per-tile column sums of the LN-backward kernel.
+__global__ void __launch_bounds__(1024) colsum_kernel(const float* in, int rows, int cols, float* out) {
+  __shared__ float red[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float a = 0.f;
+  if (c < cols)
+    for (int r = warp; r < rows; r += 32) a += in[(size_t)r * cols + c];
+  red[warp][lane] = a;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    float t = 0.f;
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
+    out[c] = t;
   }
 }
 
@@ -878,8 +896,10 @@ static size_t tile_smem(const Dims& D) { return (size_t)32 * (D.d + 2) * 2 + 16;
 void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = tile_smem(D);
-  D2FT_CUDA(cudaFuncSetAttribute(prep_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  prep_input_kernel<<<grid, 256, sm, st>>>(D, x, inp, inpT);
+  D2FT_NV_DISPATCH(D.d, {
+    D2FT_CUDA(cudaFuncSetAttribute(prep_input_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    prep_input_kernel<NV><<<grid, 256, sm, st>>>(D, x, inp, inpT);
+  });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -952,10 +972,12 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
-  const size_t sm = (size_t)(10 * D.d + 2 * D.T) * 4;
+  // one CTA per sample, 16 warps (96 registers each): B (= 64) CTAs need many rows in flight each
+  const int threads = 512;
+  const size_t sm = (size_t)((threads / 32 + 2) * D.d + 2 * D.T) * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(head_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    head_kernel<NV><<<D.B, 256, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
+    head_kernel<NV><<<D.B, threads, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
@@ -979,8 +1001,11 @@ void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float*
 
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
                          float* dbe, float* dpos, cudaStream_t st) {
-  const size_t n = (size_t)D.d * D.d + (size_t)D.T * D.d + D.d;
+  const size_t n = (size_t)D.d * D.d + (size_t)D.T * D.d;
   embed_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(D, KS, part, part_cs, dX, dWeT, dbe, dpos);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+  colsum_kernel<<<(D.d + 31) / 32, 1024, 0, st>>>(part_cs, D.B * ((D.T + 31) / 32), D.d, dbe);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
