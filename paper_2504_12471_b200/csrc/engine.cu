@@ -25,6 +25,10 @@
 #include "step_gemms.cuh"
 #include "step_kernels.cuh"
 
+#ifndef D2FT_G1_EPI
+#define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
+#endif
+
 namespace d2ft_b200 {
 
 namespace {
@@ -107,6 +111,7 @@ struct Engine {
   int *af_items, *af_count, *ab_items, *ab_count;  // attention work lists (plan_kernel)
   // head partition (exchange.cuh): null = the whole model on this GPU
   std::unique_ptr<Exchange> ex;
+  CUtensorMap* store_maps;  // device copies: [0] ZT, [1] OGT bulk-store maps (G1 epilogue)
   int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
   bool partitioned() const { return ex && ex->world > 1; }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
@@ -304,6 +309,7 @@ struct Engine {
     ord_head = dalloc<int>(L * H, owned);
     ctrs = dalloc<int>((L + 1) * 8, owned);
     full_any = dalloc<int>(L * Bm, owned);
+    store_maps = dalloc<CUtensorMap>(2, owned);
     af_items = dalloc<int>(L * Bm * H, owned);
     ab_items = dalloc<int>(L * Bm * H, owned);
     af_count = dalloc<int>(L, owned);
@@ -339,6 +345,12 @@ struct Engine {
       tm_K = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, D.TQ);
       tm_V = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 64);
       tm_dO = make_tmap_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, D.TQ);
+    }
+    {  // G1 epilogue bulk stores: 16 tokens x 32 feature rows, clipped at T
+      CUtensorMap sm[2];
+      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 16, 32);
+      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 16, 32);
+      D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
     tm_OGT64 = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 64);
@@ -415,20 +427,22 @@ struct Engine {
   // Tokens-as-N GEMMs on CTA pairs; BMN = 1: B is a feature-major buffer
   // read MN-major (its 64-token blocks cost more shared memory per stage).
   // AMN = 1: A (weights) read MN-major from the other GEMM's copy.
-  template <template <int> class Prob, int BMN = 0, int AMN = 0, class... Args>
+  template <template <int> class Prob, int BMN = 0, int AMN = 0, int EPI = 4, class... Args>
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8, 0, 4, 2, BMN, AMN>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, 8, 0, EPI, 2, BMN, AMN>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, 6, 0, 4, 2, BMN, AMN>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, 6, 0, EPI, 2, BMN, AMN>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        launch_gemm<Prob<208>, GemmShape<208, BMN ? 4 : 5, 0, 4, 2, BMN, AMN>>(a, b, Prob<208>{args...}, 0, st);
+        // 4 stages when the B blocks are MN-major or the epilogue stages bulk stores
+        launch_gemm<Prob<208>, GemmShape<208, (BMN || epi_stage_bytes<Prob<208>>::value) ? 4 : 5, 0, EPI, 2, BMN, AMN>>(
+            a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, 4, 0, 4, 2, BMN, AMN>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, 4, 0, EPI, 2, BMN, AMN>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
@@ -450,8 +464,8 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
-      gemm_tokN<G1>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
-                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl);
+      gemm_tokN<G1, 0, 0, D2FT_G1_EPI>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl, store_maps, store_maps + 1);
       mark(PH_ATTN_F);
       if (D.dh == 64 && D.TQ <= 256)
         launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, af_items + l * Bm * H, af_count + l, lists.act_heads, OGTl,

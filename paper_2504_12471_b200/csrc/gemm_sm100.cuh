@@ -75,6 +75,19 @@ template <class P>
 struct has_counter<P, std::void_t<decltype(std::declval<P>().ctr)>> : std::true_type {};
 constexpr int kTileQ = 4;
 
+// Optional `static constexpr int kEpiStageBytes` (> 0): that many bytes of
+// shared memory per epilogue warp, handed to the problem as Row::stage before
+// row_begin (staging for bulk tensor stores); the kernel drains the warp's
+// bulk stores before exiting.
+template <class P, class = void>
+struct epi_stage_bytes : std::integral_constant<int, 0> {};
+template <class P>
+struct epi_stage_bytes<P, std::void_t<decltype(P::kEpiStageBytes)>> : std::integral_constant<int, P::kEpiStageBytes> {};
+template <class P, class S>
+constexpr int gemm_smem_bytes() {
+  return S::SMEM_BYTES + 4 * S::EPI * epi_stage_bytes<P>::value;
+}
+
 // AMN: A operand layout.  0 = K-major; 1 = MN-major (A stored [K][M] with M
 // contiguous, e.g. a weight matrix kept in the other GEMM's orientation): the
 // two 64-row halves of the tile are two 64(M) x 64(K) boxes, LBO = 8 KB.
@@ -111,6 +124,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint64_t* tq_empty = tq_full + kTileQ;
   int* tq = reinterpret_cast<int*>(tq_empty + kTileQ);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTileQ);
+  // per-epilogue-warp staging (epi_stage_bytes), 128-byte aligned, after the barriers
+  uint8_t* epi_stage = sB + S::STAGES * S::B_BYTES + 512;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = S::CLUSTER == 2 ? (int)ptx::cluster_rank() : 0;
@@ -286,6 +301,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       const int nch = (S::BN - 16 * e + 16 * S::EPI - 1) / (16 * S::EPI);
       auto col_of = [&](int i) { return 16 * e + i * 16 * S::EPI; };
       typename P::Row st;
+      if constexpr (epi_stage_bytes<P>::value > 0) st.stage = epi_stage + (warp - 4) * epi_stage_bytes<P>::value;
       prob.row_begin(c, row, st);
       if constexpr (has_prefetch<P>::value) {
         if (nch > 0) prob.prefetch(c, row, col_of(0), st);
@@ -323,6 +339,9 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     });
+    if constexpr (epi_stage_bytes<P>::value > 0) {
+      if (lane == 0) ptx::bulk_wait0();
+    }
   }
   ptx::tc_fence_before();
   // the peer may still commit into our empty barriers / multicast into our smem
@@ -348,6 +367,10 @@ inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, 
                                     uint64_t s2, uint32_t box_rows) {
   return make_tmap_16_3d(base, d0, d1, d2, s1, s2, box_rows, false);
 }
+// fp16 map for bulk tensor STORES: box = box0 x box1 x 1, no swizzle (the
+// staging tile is plain row-major [box1][box0]); writes past d0/d1 are clipped.
+CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                                   uint32_t box0, uint32_t box1);
 
 int num_sms();
 
@@ -355,10 +378,11 @@ int num_sms();
 // SMs) per SM.  The B tensor map's box must be BN / CLUSTER rows.
 template <class P, class S>
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int max_ctas, cudaStream_t stream) {
+  static_assert(gemm_smem_bytes<P, S>() <= 227 * 1024, "shared memory (stages + epilogue staging)");
   static bool attr = false;
   if (!attr) {
     D2FT_CUDA(cudaFuncSetAttribute(gemm_sm100_kernel<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   S::SMEM_BYTES));
+                                   gemm_smem_bytes<P, S>()));
     attr = true;
   }
   int grid = num_sms();
@@ -366,12 +390,12 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int 
   grid -= grid % S::CLUSTER;
   if (grid < S::CLUSTER) grid = S::CLUSTER;
   if (S::CLUSTER == 1) {
-    gemm_sm100_kernel<P, S><<<grid, S::THREADS, S::SMEM_BYTES, stream>>>(a, b, prob);
+    gemm_sm100_kernel<P, S><<<grid, S::THREADS, gemm_smem_bytes<P, S>(), stream>>>(a, b, prob);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(S::THREADS);
-    cfg.dynamicSmemBytes = S::SMEM_BYTES;
+    cfg.dynamicSmemBytes = gemm_smem_bytes<P, S>();
     cfg.stream = stream;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeClusterDimension;

@@ -77,12 +77,20 @@ struct G1 {
   act_t* QKV;       // block l: [Bmax][H][T][3dh]   q|k|v, token-major (attention operands)
   act_t* ZT;        // block l: [Bmax][H][fs][TP]   GELU'(z + b1), feature-major (G4's dz)
   act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G3's and G5's B)
+  // bulk-store maps (global memory) over the whole ZT / OGT buffers, box 16 tokens x 32 rows
+  const CUtensorMap* zt_store;
+  const CUtensorMap* ogt_store;
+  // The feature-major GELU'/GELU rows leave through shared memory and bulk
+  // tensor stores: per-lane 16-byte global stores to 32 rows touch 32 lines
+  // per instruction and made the LSU the limiter of this epilogue.
+  static constexpr int kEpiStageBytes = 2 * 32 * 16 * 2;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
   struct Row {
     int valid, h, f;
     float bias;
+    uint8_t* stage;  // this warp's staging (kEpiStageBytes)
   };
   __device__ int ntiles() const { return *count; }
   __device__ int unit_row(int s, int u) const {
@@ -135,15 +143,33 @@ struct G1 {
 #endif
     }
 #ifndef D2FT_EXP_G1_NOT
-    act_t* zt = ZT + (sh * D.fs + j) * D.TP + col0;
-    act_t* gt = OGT + (sh * D.PO + D.dh + j) * D.TP + col0;
-    if (col0 + 8 <= D.TP) {
-      st_act_x8(zt, z);
-      st_act_x8(gt, g);
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) ptx::bulk_wait_read0();  // the previous chunk's stores have read the staging
+    __syncwarp();
+    uint4 pz[2], pg[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      __align__(16) __half2 hz[4], hg[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        hz[i] = __floats2half2_rn(z[8 * q + 2 * i], z[8 * q + 2 * i + 1]);
+        hg[i] = __floats2half2_rn(g[8 * q + 2 * i], g[8 * q + 2 * i + 1]);
+      }
+      pz[q] = *reinterpret_cast<const uint4*>(hz);
+      pg[q] = *reinterpret_cast<const uint4*>(hg);
     }
-    if (col0 + 16 <= D.TP) {
-      st_act_x8(zt + 8, z + 8);
-      st_act_x8(gt + 8, g + 8);
+    const uint32_t sz = ptx::smem_u32(r.stage) + lane * 32, sg = sz + 1024;
+    ptx::st_shared_v4(sz, pz[0].x, pz[0].y, pz[0].z, pz[0].w);
+    ptx::st_shared_v4(sz + 16, pz[1].x, pz[1].y, pz[1].z, pz[1].w);
+    ptx::st_shared_v4(sg, pg[0].x, pg[0].y, pg[0].z, pg[0].w);
+    ptx::st_shared_v4(sg + 16, pg[1].x, pg[1].y, pg[1].z, pg[1].w);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {  // the warp's 32 rows start at this lane's row j
+      const int plane = (l * D.Bmax + c.s) * D.H + r.h;
+      ptx::tma_store_3d(zt_store, r.stage, col0, j, plane);
+      ptx::tma_store_3d(ogt_store, r.stage + 1024, col0, D.dh + j, plane);
+      ptx::bulk_commit();
     }
 #endif
   }
