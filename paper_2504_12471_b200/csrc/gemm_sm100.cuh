@@ -67,6 +67,14 @@ struct has_prefetch<P, std::void_t<decltype(&P::prefetch)>> : std::true_type {};
 // 64 K-rows x 64 N-elements (one 8 KB TMA box of 64 N x 64 K each, 128-byte
 // swizzle), read by UMMA with LBO = 8 KB (next 64-element N block) and
 // SBO = 1 KB (next 8 K-rows); the CTAs of a pair load alternate blocks.
+// Optional P::ksteps(tile, kb): number of 16-wide K steps of k-block kb that
+// carry data (1..4); the MMA skips the rest (tokens-as-K problems whose last
+// 64-token block of a sample holds T % 64 tokens).
+template <class P, class = void>
+struct has_ksteps : std::false_type {};
+template <class P>
+struct has_ksteps<P, std::void_t<decltype(&P::ksteps)>> : std::true_type {};
+
 // Optional member `int* ctr` (zeroed before the launch): dynamic tile
 // scheduling instead of the static slot0 + i*nslots striding.
 template <class P, class = void>
@@ -266,10 +274,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         // K step of 16: +32 B along a K-major row, or +16 rows (2 KB) of an MN-major block
         constexpr uint64_t astep = S::AMN ? (16 * 128) >> 4 : 2;
         constexpr uint64_t bstep = S::BMN ? (16 * 128) >> 4 : 2;
+        int nk = S::BK / 16;
+        if constexpr (has_ksteps<P>::value) nk = prob.ksteps(c, kb);
         if (ptx::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
-            ptx::umma_bf16(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
+            if (kk < nk)
+              ptx::umma_bf16(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
           if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
           else ptx::umma_commit(&empty[stage]);
         }

@@ -374,6 +374,10 @@ struct G5 {
     c.nt = r % ntn();
     c.nkb = D.TB * full_cnt[l * D.H + c.h];
   }
+  // the last 64-token block of a sample carries T - 64*(TB-1) tokens
+  __device__ int ksteps(const Tile&, int kb) const {
+    return kb % D.TB == D.TB - 1 ? (D.T - 64 * (D.TB - 1) + 15) / 16 : 4;
+  }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int s = full_idx[(size_t)(l * D.H + c.h) * D.Bmax + kb / D.TB];
     const int t0 = (kb % D.TB) * 64;
@@ -429,6 +433,10 @@ struct G7 {
     c.mt = 2 * (r / ntn()) + rank;
     c.nt = r % ntn();
     c.nkb = D.TB * full_cnt[l * D.H + c.h];
+  }
+  // the last 64-token block of a sample carries T - 64*(TB-1) tokens
+  __device__ int ksteps(const Tile&, int kb) const {
+    return kb % D.TB == D.TB - 1 ? (D.T - 64 * (D.TB - 1) + 15) / 16 : 4;
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int s = full_idx[(size_t)(l * D.H + c.h) * D.Bmax + kb / D.TB];
@@ -528,6 +536,10 @@ struct EmbedW {
     c.nt = r % ntn();
     c.s0 = c.ks * D.B / KS;
     c.nkb = D.TB * ((c.ks + 1) * D.B / KS - c.s0);
+  }
+  // the last 64-token block of a sample carries T - 64*(TB-1) tokens
+  __device__ int ksteps(const Tile&, int kb) const {
+    return kb % D.TB == D.TB - 1 ? (D.T - 64 * (D.TB - 1) + 15) / 16 : 4;
   }
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int s = c.s0 + kb / D.TB;
