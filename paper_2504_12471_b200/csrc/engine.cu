@@ -111,7 +111,7 @@ struct Engine {
   int *af_items, *af_count, *ab_items, *ab_count;  // attention work lists (plan_kernel)
   // head partition (exchange.cuh): null = the whole model on this GPU
   std::unique_ptr<Exchange> ex;
-  CUtensorMap* store_maps;  // device copies: [0] ZT, [1] OGT bulk-store maps (G1 epilogue)
+  CUtensorMap* store_maps;  // device copies of the epilogue bulk-store maps: [0] ZT, [1] OGT, [2] QKV (G1)
   int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
   bool partitioned() const { return ex && ex->world > 1; }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
@@ -186,7 +186,7 @@ struct Engine {
     D.fs = D.ffn / D.H;
     D2FT_REQUIRE(D.d % 128 == 0 && D.d <= 1024, kConfig, "b200 engine: model_dim must be a multiple of 128, <= 1024");
     D2FT_REQUIRE(D.dh == 32 || D.dh == 64, kConfig, "b200 engine: head_dim (d/H) must be 32 or 64");
-    D2FT_REQUIRE(D.fs % 8 == 0, kConfig, "b200 engine: ffn slice must be a multiple of 8");
+    D2FT_REQUIRE(D.fs % 32 == 0, kConfig, "b200 engine: ffn slice (ffn/H) must be a multiple of 32");
     D2FT_REQUIRE(D.T <= 256, kConfig, "b200 engine: seq_len must be <= 256");
     D2FT_REQUIRE(D.H <= 16, kConfig, "b200 engine: at most 16 heads per block");
     D2FT_REQUIRE(D.C <= 64, kConfig, "b200 engine: at most 64 classes");
@@ -309,7 +309,7 @@ struct Engine {
     ord_head = dalloc<int>(L * H, owned);
     ctrs = dalloc<int>((L + 1) * 8, owned);
     full_any = dalloc<int>(L * Bm, owned);
-    store_maps = dalloc<CUtensorMap>(2, owned);
+    store_maps = dalloc<CUtensorMap>(8, owned);
     af_items = dalloc<int>(L * Bm * H, owned);
     ab_items = dalloc<int>(L * Bm * H, owned);
     af_count = dalloc<int>(L, owned);
@@ -346,10 +346,12 @@ struct Engine {
       tm_V = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 64);
       tm_dO = make_tmap_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, D.TQ);
     }
-    {  // G1 epilogue bulk stores: 16 tokens x 32 feature rows, clipped at T
-      CUtensorMap sm[2];
+    {  // G1 epilogue bulk stores: 16 tokens x 32 feature rows (feature-major) or
+       // 32 features x 16 tokens (token-major QKV), clipped at T
+      CUtensorMap sm[3];
       sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 16, 32);
       sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 16, 32);
+      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, 16);
       D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
@@ -464,8 +466,9 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
-      gemm_tokN<G1, 0, 0, D2FT_G1_EPI>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt,
-                    P + seg[S_B1].off + (size_t)l * H * D.fs, QKVl, ZTl, OGTl, store_maps, store_maps + 1);
+      gemm_tokN<G1, 0, 0, D2FT_G1_EPI>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads,
+                                       lists.act_cnt, (const uint8_t*)codes_exp, P + seg[S_B1].off + (size_t)l * H * D.fs,
+                                       (const CUtensorMap*)store_maps);
       mark(PH_ATTN_F);
       if (D.dh == 64 && D.TQ <= 256)
         launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, af_items + l * Bm * H, af_count + l, lists.act_heads, OGTl,

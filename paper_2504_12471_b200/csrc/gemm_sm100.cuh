@@ -91,9 +91,38 @@ template <class P, class = void>
 struct epi_stage_bytes : std::integral_constant<int, 0> {};
 template <class P>
 struct epi_stage_bytes<P, std::void_t<decltype(P::kEpiStageBytes)>> : std::integral_constant<int, P::kEpiStageBytes> {};
+// Tile ring and k-block queue, both filled by warp 3 (the scheduler warp):
+// it resolves each tile's coordinates (prob.tile: the dependent global loads
+// of tile lists and head lists) up to kRing tiles ahead into the ring, and
+// every k-block's TMA coordinates (prob.kcoord, incl. its integer divisions
+// and list lookups) into the kKQ-deep k-block queue.  The producer then only
+// pops ready coordinates and issues TMA: ncu showed the producer thread busy
+// ~80% of G3 computing coordinates, with the MMA waiting on data ~60%.
+constexpr int kRing = 4;
+constexpr int kKQ = 16;
+template <class P>
+struct alignas(16) RingEntry {
+  int t;
+  typename P::Tile c;
+};
+struct alignas(16) KRec {
+  KCoord k;
+  int nk;  // 16-wide K steps of the k-block that carry data (P::ksteps)
+};
+template <class P>
+struct SchedSmem {
+  RingEntry<P> ring[kRing];
+  KRec kq[kKQ];
+  uint64_t ring_full[kRing], ring_empty[kRing], kq_full[kKQ], kq_empty[kKQ];
+};
+template <class P, class S>
+constexpr int gemm_sched_offset() {  // after the epilogue staging
+  return S::STAGES * S::STAGE_BYTES + 512 + 4 * S::EPI * epi_stage_bytes<P>::value;
+}
+
 template <class P, class S>
 constexpr int gemm_smem_bytes() {
-  return S::SMEM_BYTES + 4 * S::EPI * epi_stage_bytes<P>::value;
+  return S::SMEM_BYTES + 4 * S::EPI * epi_stage_bytes<P>::value + (int)sizeof(SchedSmem<P>);
 }
 
 // AMN: A operand layout.  0 = K-major; 1 = MN-major (A stored [K][M] with M
@@ -128,12 +157,19 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* tq_full = tempty + 2;        // tile queue (dynamic scheduling)
+  uint64_t* tq_full = tempty + 2;        // rank 0 -> rank 1 tile-id queue (dynamic scheduling)
   uint64_t* tq_empty = tq_full + kTileQ;
   int* tq = reinterpret_cast<int*>(tq_empty + kTileQ);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTileQ);
   // per-epilogue-warp staging (epi_stage_bytes), 128-byte aligned, after the barriers
   uint8_t* epi_stage = sB + S::STAGES * S::B_BYTES + 512;
+  SchedSmem<P>& sch = *reinterpret_cast<SchedSmem<P>*>(smem + gemm_sched_offset<P, S>());
+  RingEntry<P>* ring = sch.ring;
+  uint64_t* ring_full = sch.ring_full;
+  uint64_t* ring_empty = sch.ring_empty;
+  KRec* kq = sch.kq;
+  uint64_t* kq_full = sch.kq_full;
+  uint64_t* kq_empty = sch.kq_empty;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = S::CLUSTER == 2 ? (int)ptx::cluster_rank() : 0;
@@ -153,8 +189,15 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     }
     for (int i = 0; i < kTileQ; ++i) {
       ptx::mbar_init(&tq_full[i], 1);
-      // consumers of both CTAs (MMA thread + epilogue warps) and the peer's producer
-      ptx::mbar_init(&tq_empty[i], S::CLUSTER * (1 + 4 * S::EPI) + (S::CLUSTER - 1));
+      ptx::mbar_init(&tq_empty[i], 1);  // rank 1's scheduler
+    }
+    for (int i = 0; i < kRing; ++i) {
+      ptx::mbar_init(&ring_full[i], 1);
+      ptx::mbar_init(&ring_empty[i], 2 + 4 * S::EPI);  // producer, MMA warp, epilogue warps
+    }
+    for (int i = 0; i < kKQ; ++i) {
+      ptx::mbar_init(&kq_full[i], 1);
+      ptx::mbar_init(&kq_empty[i], has_ksteps<P>::value ? 2 : 1);  // producer (+ MMA warp for ksteps)
     }
     ptx::fence_barrier_init();
   }
@@ -166,46 +209,88 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int ntiles = prob.ntiles();
 
-  // Tile sequence.  Static: slot0, slot0 + nslots, ...  Dynamic (P has `ctr`):
-  // rank 0's producer claims slots with atomicAdd on prob.ctr (the problem
-  // orders its slots by decreasing cost) and publishes each id through the
-  // kTileQ-deep queue to every role of both CTAs; ids >= ntiles end the loop.
-  auto tq_publish = [&](int i, int t) {
-    const int q = i % kTileQ;
-    ptx::mbar_wait_cluster(&tq_empty[q], ((i / kTileQ) & 1) ^ 1);
-    for (int r = 0; r < S::CLUSTER; ++r) ptx::st_cluster_u32(ptx::mapa(&tq[q], r), (uint32_t)t);
-    for (int r = 0; r < S::CLUSTER; ++r) ptx::mbar_arrive_cluster(ptx::mapa(&tq_full[q], r));
-  };
-  auto tq_take = [&](int i, bool leader) {
-    const int q = i % kTileQ;
-    ptx::mbar_wait_cluster(&tq_full[q], (i / kTileQ) & 1);
-    const int t = *reinterpret_cast<volatile int*>(&tq[q]);
-    __syncwarp(__activemask());
-    if (leader) ptx::mbar_arrive_cluster(ptx::mapa(&tq_empty[q], 0));
-    return t;
-  };
+  // Tile sequence, produced by warp 3 into the ring.  Static: slot0, slot0 +
+  // nslots, ...  Dynamic (P has `ctr`): rank 0's scheduler claims slots with
+  // atomicAdd on prob.ctr (the problem orders its slots by decreasing cost)
+  // and hands each id to rank 1's scheduler through the kTileQ-deep queue;
+  // ids >= ntiles end every role's loop.
   auto for_each_tile = [&](bool leader, auto&& body) {
-    if constexpr (kDyn) {
-      for (int i = 0;; ++i) {
-        const int t = tq_take(i, leader);
-        if (t >= ntiles) break;
-        body(t);
-      }
-    } else {
-      for (int t = slot0; t < ntiles; t += nslots) body(t);
+    for (int i = 0;; ++i) {
+      const int q = i % kRing;
+      ptx::mbar_wait(&ring_full[q], (i / kRing) & 1);
+      if (ring[q].t >= ntiles) break;
+      body(static_cast<const typename P::Tile&>(ring[q].c));
+      __syncwarp(__activemask());
+      if (leader) ptx::mbar_arrive(&ring_empty[q]);
     }
   };
 
-  if (warp == 0) {
+  if (warp == 3) {
+    if (lane == 0) {
+      int kqi = 0;
+      auto push = [&](int i, int t) {
+        const int q = i % kRing;
+        typename P::Tile c{};
+        if (t < ntiles) prob.tile(t, rank, c);  // global loads resolve before the slot is needed
+        ptx::mbar_wait(&ring_empty[q], ((i / kRing) & 1) ^ 1);
+        ring[q].t = t;
+        ring[q].c = c;
+        ptx::mbar_arrive(&ring_full[q]);
+        if (t >= ntiles) return;
+        for (int kb = 0; kb < c.nkb; ++kb, ++kqi) {
+          KRec rec;
+          rec.k = prob.kcoord(c, kb);
+          rec.nk = S::BK / 16;
+          if constexpr (has_ksteps<P>::value) rec.nk = prob.ksteps(c, kb);
+          const int j = kqi % kKQ;
+          ptx::mbar_wait(&kq_empty[j], ((kqi / kKQ) & 1) ^ 1);
+          kq[j] = rec;
+          ptx::mbar_arrive(&kq_full[j]);
+        }
+      };
+      if constexpr (kDyn) {
+        for (int i = 0;; ++i) {
+          int t;
+          if (rank == 0) {
+            // claim only once the ring slot is free: claiming further ahead
+            // than the pipeline needs unbalances the end of the launch
+            ptx::mbar_wait(&ring_empty[i % kRing], ((i / kRing) & 1) ^ 1);
+            t = atomicAdd(prob.ctr, 1);
+            if (S::CLUSTER == 2) {
+              const int q = i % kTileQ;
+              ptx::mbar_wait_cluster(&tq_empty[q], ((i / kTileQ) & 1) ^ 1);
+              ptx::st_cluster_u32(ptx::mapa(&tq[q], 1), (uint32_t)t);
+              ptx::mbar_arrive_cluster(ptx::mapa(&tq_full[q], 1));
+            }
+          } else {
+            const int q = i % kTileQ;
+            ptx::mbar_wait_cluster(&tq_full[q], (i / kTileQ) & 1);
+            t = *reinterpret_cast<volatile int*>(&tq[q]);
+            ptx::mbar_arrive_cluster(ptx::mapa(&tq_empty[q], 0));
+          }
+          push(i, t);
+          if (t >= ntiles) break;
+        }
+      } else {
+        for (int i = 0;; ++i) {
+          const int t = slot0 + i * nslots;
+          push(i, t < ntiles ? t : ntiles);
+          if (t >= ntiles) break;
+        }
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      auto load_tile = [&](int t) {
-        typename P::Tile c;
-        prob.tile(t, rank, c);
-        for (int kb = 0; kb < c.nkb; ++kb) {
+      int kqi = 0;
+      for_each_tile(true, [&](const typename P::Tile& c) {
+        const int nkb = c.nkb;
+        for (int kb = 0; kb < nkb; ++kb, ++kqi) {
+          const int j = kqi % kKQ;
+          ptx::mbar_wait(&kq_full[j], (kqi / kKQ) & 1);
+          const KCoord k = kq[j].k;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          const KCoord k = prob.kcoord(c, kb);
           uint8_t* a = sA + stage * S::A_BYTES;
           ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
           if constexpr (S::AMN) {  // boxes of 64 M (inner) x 64 K rows
@@ -227,28 +312,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           } else {
             ptx::tma_load_3d(sB + stage * S::B_BYTES, &tmB, &full[stage], k.bx, k.by, k.bz);
           }
+          ptx::mbar_arrive(&kq_empty[j]);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-      };
-      if constexpr (kDyn) {
-        if (rank == 0) {
-          int cur = atomicAdd(prob.ctr, 1);
-          for (int i = 0;; ++i) {
-            tq_publish(i, cur);
-            if (cur >= ntiles) break;
-            const int nxt = atomicAdd(prob.ctr, 1);  // claimed now, used after this tile's loads
-            load_tile(cur);
-            cur = nxt;
-          }
-        } else {
-          for_each_tile(true, load_tile);
-        }
-      } else {
-        for_each_tile(true, load_tile);
-      }
+      });
     }
   } else if (warp == 1) {
     // The whole warp runs the MMA loop (warp-uniform control flow keeps the
@@ -256,11 +326,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     // and commits.
     constexpr uint32_t idesc =
         ptx::idesc_f16_m128(S::BN, S::FMT) | (S::AMN ? (1u << 15) : 0u) | (S::BMN ? (1u << 16) : 0u);
-    int stage = 0, acc = 0;
+    int stage = 0, acc = 0, kqm = 0;
     uint32_t phase = 0, acc_phase = 0;
-    for_each_tile(lane == 0, [&](int t) {
-      typename P::Tile c;
-      prob.tile(t, rank, c);
+    for_each_tile(lane == 0, [&](const typename P::Tile& cref) {
+      const typename P::Tile c = cref;  // registers (smem reads would be re-done around every store)
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem + acc * 256;
@@ -275,7 +344,14 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         constexpr uint64_t astep = S::AMN ? (16 * 128) >> 4 : 2;
         constexpr uint64_t bstep = S::BMN ? (16 * 128) >> 4 : 2;
         int nk = S::BK / 16;
-        if constexpr (has_ksteps<P>::value) nk = prob.ksteps(c, kb);
+        if constexpr (has_ksteps<P>::value) {
+          const int j = kqm % kKQ;
+          ptx::mbar_wait(&kq_full[j], (kqm / kKQ) & 1);
+          nk = kq[j].nk;
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&kq_empty[j]);
+          ++kqm;
+        }
         if (ptx::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
@@ -301,9 +377,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for_each_tile(lane == 0, [&](int t) {
-      typename P::Tile c;
-      prob.tile(t, rank, c);
+    for_each_tile(lane == 0, [&](const typename P::Tile& cref) {
+      const typename P::Tile c = cref;
       // Chunks of this warp: 16*e + i*16*EPI.  Row state and the first
       // chunk's epilogue operands are loaded before the accumulator wait (they
       // do not depend on it), and the accumulator is released to the MMA warp

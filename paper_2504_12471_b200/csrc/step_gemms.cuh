@@ -64,7 +64,16 @@ struct EmbedFwd {
 // [q|k|v|z] = xn . [Wq|Wk|Wv|W1]  per (sample, active head)  (model.cpp:200-202, 218-220)
 // A = W1T (plane l, rows h*PQ + f), B = xn (plane l*Bmax + s).  Epilogue:
 // q,k,v -> QKV (token-major, attention operands); g = gelu(z + b1) -> OGT
-// (feature-major: G3's MN-major B and G5's B); GELU'(z + b1) -> ZT (G4).
+// (feature-major: G3's MN-major B and G5's B); GELU'(z + b1) -> ZT (G4; only
+// for Full cells — p_o cells never run backward, model.cpp:501).
+//
+// Every output leaves through shared memory and bulk tensor stores: a warp's
+// 32 accumulator rows (one feature each, warp-uniform q / k / v / z section
+// since dh and fs are multiples of 32) x 16 tokens are staged and written by
+// one TMA store per destination.  Per-lane global stores (32 rows per
+// instruction) made the LSU the limiter of this epilogue.  The staging is
+// double-buffered per warp so the next chunk's math overlaps the previous
+// chunk's store.
 template <int BN>
 struct G1 {
   Dims D;
@@ -73,22 +82,15 @@ struct G1 {
   const int* count;
   const int* act_heads;
   const int* act_cnt;
+  const uint8_t* codes;  // expanded K x Bmax (code 1 = Full)
   const float* b1;  // block l: [H][fs]
-  act_t* QKV;       // block l: [Bmax][H][T][3dh]   q|k|v, token-major (attention operands)
-  act_t* ZT;        // block l: [Bmax][H][fs][TP]   GELU'(z + b1), feature-major (G4's dz)
-  act_t* OGT;       // block l: [Bmax][H][PO][TP]   [O|g] feature-major (G3's and G5's B)
-  // bulk-store maps (global memory) over the whole ZT / OGT buffers, box 16 tokens x 32 rows
-  const CUtensorMap* zt_store;
-  const CUtensorMap* ogt_store;
-  // The feature-major GELU'/GELU rows leave through shared memory and bulk
-  // tensor stores: per-lane 16-byte global stores to 32 rows touch 32 lines
-  // per instruction and made the LSU the limiter of this epilogue.
-  static constexpr int kEpiStageBytes = 2 * 32 * 16 * 2;
+  const CUtensorMap* maps;  // bulk-store maps: [0] ZT, [1] OGT (16 tokens x 32 rows), [2] QKV (32 features x 16 tokens)
+  static constexpr int kEpiStageBytes = 2 * 2048;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
   struct Row {
-    int valid, h, f;
+    int valid, h, f, full, buf;
     float bias;
     uint8_t* stage;  // this warp's staging (kEpiStageBytes)
   };
@@ -110,68 +112,70 @@ struct G1 {
     return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, l * D.Bmax + c.s};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
+    // the previous tile's stores have read the staging (buffer parity restarts)
+    if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read0();
+    r.buf = 0;
     const int u = c.u0 + (row >> 6);
     r.valid = u < c.nu;
     if (!r.valid) return;
     r.h = act_heads[(c.s * D.L + l) * D.H + u / D.UQ];
     r.f = (u % D.UQ) * 64 + (row & 63);
     r.valid = r.f < D.PQ;
+    r.full = codes[(size_t)(l * D.H + r.h) * D.Bmax + c.s] == 1;
     r.bias = (r.valid && r.f >= 3 * D.dh) ? b1[r.h * D.fs + (r.f - 3 * D.dh)] : 0.f;
   }
   __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
-    if (!r.valid || col0 >= D.T) return;
-    const size_t sh = (size_t)c.s * D.H + r.h;
-    if (r.f < 3 * D.dh) {  // q, k, v: fp16 operands of the attention kernels
-#ifndef D2FT_EXP_G1_NOQKV
-      act_t* y = QKV + sh * D.T * (3 * D.dh) + r.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (col0 + i < D.T) y[(size_t)(col0 + i) * (3 * D.dh)] = to_act(v[i]);
-#endif
-      return;
-    }
-    const int j = r.f - 3 * D.dh;
-    float z[16], g[16];  // z becomes GELU'(z) (stored for G4), g = GELU(z)
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float zz = v[i] + r.bias;
-#ifndef D2FT_EXP_G1_NOGELU
-      gelu_and_grad(zz, g[i], z[i]);
-#else
-      g[i] = zz;
-      z[i] = zz;
-#endif
-    }
-#ifndef D2FT_EXP_G1_NOT
+    if (!r.valid || col0 >= D.T) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
-    if (lane == 0) ptx::bulk_wait_read0();  // the previous chunk's stores have read the staging
+    if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used this buffer has read it
     __syncwarp();
-    uint4 pz[2], pg[2];
+    const uint32_t sb = ptx::smem_u32(r.stage) + r.buf * 2048;
+    const int plane = (l * D.Bmax + c.s) * D.H + r.h;
+    const int f0 = r.f - lane;  // the warp's first feature row
+    if (r.f < 3 * D.dh) {  // q, k, v: staged [16 tokens][32 features]
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      __align__(16) __half2 hz[4], hg[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        hz[i] = __floats2half2_rn(z[8 * q + 2 * i], z[8 * q + 2 * i + 1]);
-        hg[i] = __floats2half2_rn(g[8 * q + 2 * i], g[8 * q + 2 * i + 1]);
+      for (int i = 0; i < 16; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(maps + 2, r.stage + r.buf * 2048, f0, col0, plane);
+        ptx::bulk_commit();
       }
-      pz[q] = *reinterpret_cast<const uint4*>(hz);
-      pg[q] = *reinterpret_cast<const uint4*>(hg);
+    } else {
+      const int j0 = f0 - 3 * D.dh;
+      float z[16], g[16];  // z becomes GELU'(z) (stored for G4), g = GELU(z)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) gelu_and_grad(v[i] + r.bias, g[i], z[i]);
+      uint4 pz[2], pg[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        __align__(16) __half2 hz[4], hg[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          hz[i] = __floats2half2_rn(z[8 * q + 2 * i], z[8 * q + 2 * i + 1]);
+          hg[i] = __floats2half2_rn(g[8 * q + 2 * i], g[8 * q + 2 * i + 1]);
+        }
+        pz[q] = *reinterpret_cast<const uint4*>(hz);
+        pg[q] = *reinterpret_cast<const uint4*>(hg);
+      }
+      // [32 rows][16 tokens] tiles: g at +0, GELU' at +1024
+      const uint32_t sg = sb + lane * 32, sz = sg + 1024;
+      ptx::st_shared_v4(sg, pg[0].x, pg[0].y, pg[0].z, pg[0].w);
+      ptx::st_shared_v4(sg + 16, pg[1].x, pg[1].y, pg[1].z, pg[1].w);
+      if (r.full) {
+        ptx::st_shared_v4(sz, pz[0].x, pz[0].y, pz[0].z, pz[0].w);
+        ptx::st_shared_v4(sz + 16, pz[1].x, pz[1].y, pz[1].z, pz[1].w);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        uint8_t* st = r.stage + r.buf * 2048;
+        ptx::tma_store_3d(maps + 1, st, col0, D.dh + j0, plane);
+        if (r.full) ptx::tma_store_3d(maps + 0, st + 1024, col0, j0, plane);
+        ptx::bulk_commit();
+      }
     }
-    const uint32_t sz = ptx::smem_u32(r.stage) + lane * 32, sg = sz + 1024;
-    ptx::st_shared_v4(sz, pz[0].x, pz[0].y, pz[0].z, pz[0].w);
-    ptx::st_shared_v4(sz + 16, pz[1].x, pz[1].y, pz[1].z, pz[1].w);
-    ptx::st_shared_v4(sg, pg[0].x, pg[0].y, pg[0].z, pg[0].w);
-    ptx::st_shared_v4(sg + 16, pg[1].x, pg[1].y, pg[1].z, pg[1].w);
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {  // the warp's 32 rows start at this lane's row j
-      const int plane = (l * D.Bmax + c.s) * D.H + r.h;
-      ptx::tma_store_3d(zt_store, r.stage, col0, j, plane);
-      ptx::tma_store_3d(ogt_store, r.stage + 1024, col0, D.dh + j, plane);
-      ptx::bulk_commit();
-    }
-#endif
+    r.buf ^= 1;
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
