@@ -346,12 +346,12 @@ struct Engine {
       tm_V = make_tmap_f16_3d(QKV, W, T, L * Bm * H, W * 2, T * W * 2, 64);
       tm_dO = make_tmap_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, D.TQ);
     }
-    {  // G1 epilogue bulk stores: 16 tokens x 32 feature rows (feature-major) or
-       // 32 features x 16 tokens (token-major QKV), clipped at T
+    {  // G1 epilogue bulk stores: 32 tokens x 32 feature rows (feature-major) or
+       // 32 features x 32 tokens (token-major QKV), clipped at T
       CUtensorMap sm[3];
-      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 16, 32);
-      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 16, 32);
-      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, 16);
+      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 32, 32, true);
+      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 32, 32, true);
+      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, 32);
       D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)

@@ -91,6 +91,19 @@ template <class P, class = void>
 struct epi_stage_bytes : std::integral_constant<int, 0> {};
 template <class P>
 struct epi_stage_bytes<P, std::void_t<decltype(P::kEpiStageBytes)>> : std::integral_constant<int, P::kEpiStageBytes> {};
+// Optional `static constexpr int kChunk` (16 or 32): accumulator columns per
+// epilogue chunk (TMEM load + P::chunk call); default 16.  Optional
+// `static constexpr bool kNonEmpty = true`: no tile has nkb == 0 (skips the
+// zero-accumulator selects).
+template <class P, class = void>
+struct chunk_cols : std::integral_constant<int, 16> {};
+template <class P>
+struct chunk_cols<P, std::void_t<decltype(P::kChunk)>> : std::integral_constant<int, P::kChunk> {};
+template <class P, class = void>
+struct non_empty : std::false_type {};
+template <class P>
+struct non_empty<P, std::void_t<decltype(P::kNonEmpty)>> : std::integral_constant<bool, P::kNonEmpty> {};
+
 // Tile ring and k-block queue, both filled by warp 3 (the scheduler warp):
 // it resolves each tile's coordinates (prob.tile: the dependent global loads
 // of tile lists and head lists) up to kRing tiles ahead into the ring, and
@@ -383,9 +396,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       // chunk's epilogue operands are loaded before the accumulator wait (they
       // do not depend on it), and the accumulator is released to the MMA warp
       // as soon as the warp's last TMEM load has landed.
-      const bool have = c.nkb > 0;
-      const int nch = (S::BN - 16 * e + 16 * S::EPI - 1) / (16 * S::EPI);
-      auto col_of = [&](int i) { return 16 * e + i * 16 * S::EPI; };
+      constexpr int CW = chunk_cols<P>::value;
+      const bool have = non_empty<P>::value || c.nkb > 0;
+      const int nch = (S::BN - CW * e + CW * S::EPI - 1) / (CW * S::EPI);
+      auto col_of = [&](int i) { return CW * e + i * CW * S::EPI; };
       typename P::Row st;
       if constexpr (epi_stage_bytes<P>::value > 0) st.stage = epi_stage + (warp - 4) * epi_stage_bytes<P>::value;
       prob.row_begin(c, row, st);
@@ -400,25 +414,27 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       };
-      auto process = [&](uint32_t (&r)[16], int i) {
-        float v[16];
+#pragma unroll 1
+      for (int i = 0; i < nch; ++i) {
+        uint32_t b0[CW];
+        if (have) {
+          if constexpr (CW == 32) {
+            ptx::tmem_ld16_async(base + col_of(i), *reinterpret_cast<uint32_t(*)[16]>(&b0[0]));
+            ptx::tmem_ld16_async(base + col_of(i) + 16, *reinterpret_cast<uint32_t(*)[16]>(&b0[16]));
+          } else {
+            ptx::tmem_ld16_async(base + col_of(i), b0);
+          }
+          ptx::tmem_ld_wait(b0);
+        }
+        if (i + 1 == nch) release();
+        float v[CW];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = have ? __uint_as_float(r[j]) : 0.f;
+        for (int j = 0; j < CW; ++j) v[j] = have ? __uint_as_float(b0[j]) : 0.f;
 #ifndef D2FT_EXP_NOEPI
         prob.chunk(c, row, col_of(i), v, st);
 #else
         if (v[0] == 12345.f) prob.chunk(c, row, col_of(i), v, st);  // experiment: epilogue stores off
 #endif
-      };
-#pragma unroll 1
-      for (int i = 0; i < nch; ++i) {
-        uint32_t b0[16];
-        if (have) {
-          ptx::tmem_ld16_async(base + col_of(i), b0);
-          ptx::tmem_ld_wait(b0);
-        }
-        if (i + 1 == nch) release();
-        process(b0, i);
       }
       if (nch == 0) release();
       prob.row_end(c, row, e, st);
@@ -453,10 +469,11 @@ inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, 
                                     uint64_t s2, uint32_t box_rows) {
   return make_tmap_16_3d(base, d0, d1, d2, s1, s2, box_rows, false);
 }
-// fp16 map for bulk tensor STORES: box = box0 x box1 x 1, no swizzle (the
-// staging tile is plain row-major [box1][box0]); writes past d0/d1 are clipped.
+// fp16 map for bulk tensor STORES: box = box0 x box1 x 1; the staging tile is
+// row-major [box1][box0], plain or 64-byte swizzled (box0 * 2 == 64 bytes);
+// writes past d0/d1 are clipped.
 CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-                                   uint32_t box0, uint32_t box1);
+                                   uint32_t box0, uint32_t box1, bool swizzle64 = false);
 
 int num_sms();
 

@@ -67,13 +67,12 @@ struct EmbedFwd {
 // (feature-major: G3's MN-major B and G5's B); GELU'(z + b1) -> ZT (G4; only
 // for Full cells — p_o cells never run backward, model.cpp:501).
 //
-// Every output leaves through shared memory and bulk tensor stores: a warp's
-// 32 accumulator rows (one feature each, warp-uniform q / k / v / z section
-// since dh and fs are multiples of 32) x 16 tokens are staged and written by
-// one TMA store per destination.  Per-lane global stores (32 rows per
-// instruction) made the LSU the limiter of this epilogue.  The staging is
-// double-buffered per warp so the next chunk's math overlaps the previous
-// chunk's store.
+// Every output leaves through shared memory and bulk tensor stores, 32 tokens
+// per chunk: a warp's 32 accumulator rows (one feature each; the q / k / v /
+// z section is warp-uniform since dh and fs are multiples of 32) x 32 tokens
+// are staged and written by one TMA store per destination.  Per-lane global
+// stores (32 rows per instruction) made the LSU the limiter of this epilogue;
+// the GELU pair runs on packed fp32 (gelu_and_grad2).
 template <int BN>
 struct G1 {
   Dims D;
@@ -84,13 +83,17 @@ struct G1 {
   const int* act_cnt;
   const uint8_t* codes;  // expanded K x Bmax (code 1 = Full)
   const float* b1;  // block l: [H][fs]
-  const CUtensorMap* maps;  // bulk-store maps: [0] ZT, [1] OGT (16 tokens x 32 rows), [2] QKV (32 features x 16 tokens)
-  static constexpr int kEpiStageBytes = 2 * 2048;
+  const CUtensorMap* maps;  // bulk-store maps: [0] ZT, [1] OGT (32 tokens x 32 rows, 64B swizzle), [2] QKV (32 x 32)
+  static constexpr int kChunk = 32;
+  static constexpr bool kNonEmpty = true;
+  // g tile [32 rows][32 tokens] at +0, GELU' tile at +2048 (64B-swizzled);
+  // or the QKV tile [32 tokens][32 features] at +0
+  static constexpr int kEpiStageBytes = 4096;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
   struct Row {
-    int valid, h, f, full, buf;
+    int valid, h, f, full;
     float bias;
     uint8_t* stage;  // this warp's staging (kEpiStageBytes)
   };
@@ -112,9 +115,6 @@ struct G1 {
     return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, l * D.Bmax + c.s};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
-    // the previous tile's stores have read the staging (buffer parity restarts)
-    if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read0();
-    r.buf = 0;
     const int u = c.u0 + (row >> 6);
     r.valid = u < c.nu;
     if (!r.valid) return;
@@ -124,58 +124,52 @@ struct G1 {
     r.full = codes[(size_t)(l * D.H + r.h) * D.Bmax + c.s] == 1;
     r.bias = (r.valid && r.f >= 3 * D.dh) ? b1[r.h * D.fs + (r.f - 3 * D.dh)] : 0.f;
   }
-  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[16], Row& r) const {
+  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[32], Row& r) const {
     if (!r.valid || col0 >= D.T) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
-    if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used this buffer has read it
+    if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's stores have read the staging
     __syncwarp();
-    const uint32_t sb = ptx::smem_u32(r.stage) + r.buf * 2048;
+    const uint32_t sb = ptx::smem_u32(r.stage);
     const int plane = (l * D.Bmax + c.s) * D.H + r.h;
     const int f0 = r.f - lane;  // the warp's first feature row
-    if (r.f < 3 * D.dh) {  // q, k, v: staged [16 tokens][32 features]
+    if (r.f < 3 * D.dh) {  // q, k, v: staged [32 tokens][32 features]
 #pragma unroll
-      for (int i = 0; i < 16; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
+      for (int i = 0; i < 32; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::tma_store_3d(maps + 2, r.stage + r.buf * 2048, f0, col0, plane);
+        ptx::tma_store_3d(maps + 2, r.stage, f0, col0, plane);
         ptx::bulk_commit();
       }
-    } else {
-      const int j0 = f0 - 3 * D.dh;
-      float z[16], g[16];  // z becomes GELU'(z) (stored for G4), g = GELU(z)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) gelu_and_grad(v[i] + r.bias, g[i], z[i]);
-      uint4 pz[2], pg[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        __align__(16) __half2 hz[4], hg[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          hz[i] = __floats2half2_rn(z[8 * q + 2 * i], z[8 * q + 2 * i + 1]);
-          hg[i] = __floats2half2_rn(g[8 * q + 2 * i], g[8 * q + 2 * i + 1]);
-        }
-        pz[q] = *reinterpret_cast<const uint4*>(hz);
-        pg[q] = *reinterpret_cast<const uint4*>(hg);
-      }
-      // [32 rows][16 tokens] tiles: g at +0, GELU' at +1024
-      const uint32_t sg = sb + lane * 32, sz = sg + 1024;
-      ptx::st_shared_v4(sg, pg[0].x, pg[0].y, pg[0].z, pg[0].w);
-      ptx::st_shared_v4(sg + 16, pg[1].x, pg[1].y, pg[1].z, pg[1].w);
-      if (r.full) {
-        ptx::st_shared_v4(sz, pz[0].x, pz[0].y, pz[0].z, pz[0].w);
-        ptx::st_shared_v4(sz + 16, pz[1].x, pz[1].y, pz[1].z, pz[1].w);
-      }
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        uint8_t* st = r.stage + r.buf * 2048;
-        ptx::tma_store_3d(maps + 1, st, col0, D.dh + j0, plane);
-        if (r.full) ptx::tma_store_3d(maps + 0, st + 1024, col0, j0, plane);
-        ptx::bulk_commit();
-      }
+      return;
     }
-    r.buf ^= 1;
+    const int j0 = f0 - 3 * D.dh;
+    uint32_t hg[16], hz[16];  // half2 pairs of g = GELU(z) and GELU'(z), tokens 2i, 2i+1
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float g0, g1, d0, d1;
+      gelu_and_grad2(v[2 * i] + r.bias, v[2 * i + 1] + r.bias, g0, g1, d0, d1);
+      const __half2 a = __floats2half2_rn(g0, g1), b = __floats2half2_rn(d0, d1);
+      hg[i] = *reinterpret_cast<const uint32_t*>(&a);
+      hz[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    // row `lane` of a [32][32] fp16 tile is 64 B = four 16-byte chunks; the
+    // 64-byte swizzle (chunk ^ (row >> 1) & 3) keeps the 8 lanes of each
+    // store phase on distinct banks
+    const uint32_t rb = sb + lane * 64, sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t o = ((q ^ sw) << 4);
+      ptx::st_shared_v4(rb + o, hg[4 * q], hg[4 * q + 1], hg[4 * q + 2], hg[4 * q + 3]);
+      if (r.full) ptx::st_shared_v4(rb + 2048 + o, hz[4 * q], hz[4 * q + 1], hz[4 * q + 2], hz[4 * q + 3]);
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_3d(maps + 1, r.stage, col0, D.dh + j0, plane);
+      if (r.full) ptx::tma_store_3d(maps + 0, r.stage + 2048, col0, j0, plane);
+      ptx::bulk_commit();
+    }
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
