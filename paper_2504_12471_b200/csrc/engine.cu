@@ -111,7 +111,7 @@ struct Engine {
   int *af_items, *af_count, *ab_items, *ab_count;  // attention work lists (plan_kernel)
   // head partition (exchange.cuh): null = the whole model on this GPU
   std::unique_ptr<Exchange> ex;
-  CUtensorMap* store_maps;  // device copies of the epilogue bulk-store maps: [0] ZT, [1] OGT, [2] QKV (G1)
+  CUtensorMap* store_maps;  // device copies of the epilogue bulk-store maps: [0] ZT, [1] OGT, [2] QKV (G1), [3] dO, [4] dY1T (G4)
   int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
   bool partitioned() const { return ex && ex->world > 1; }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
@@ -348,10 +348,13 @@ struct Engine {
     }
     {  // G1 epilogue bulk stores: 32 tokens x 32 feature rows (feature-major) or
        // 32 features x 32 tokens (token-major QKV), clipped at T
-      CUtensorMap sm[3];
+      CUtensorMap sm[5];
       sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 32, 32, true);
       sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 32, 32, true);
       sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, 32);
+      // G4 epilogue: dO (token-major) and the dz rows of dY1T (feature-major)
+      sm[3] = make_tmap_store_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, 32, 32);
+      sm[4] = make_tmap_store_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 32, 32, true);
       D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
@@ -499,7 +502,7 @@ struct Engine {
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
-                    (const act_t*)ZTl, dO, dY1T, part_db1, (const float*)gmax);
+                          (const act_t*)ZTl, part_db1, (const float*)gmax, (const CUtensorMap*)store_maps);
       mark(PH_ATTN_B);
       if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
         launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, OGTl, lse + (size_t)l * Bm * H * T,

@@ -249,7 +249,8 @@ struct G3 {
 // ---------------------------------------------------------------- G4
 // d[O|g] = dC . [Wo;W2]^T per (sample, Full head)  (model.cpp:247, 262);
 // epilogue dz = dg * gelu'(z) (model.cpp:254), db1 row sums (model.cpp:257).
-// A = W2 (plane l, rows h*PO + f), B = dC (plane s).
+// A = W2 (plane l, rows h*PO + f), B = dC (plane s).  Outputs leave through
+// shared-memory staging and bulk tensor stores, 32 tokens per chunk (as G1).
 template <int BN>
 struct G4 {
   Dims D;
@@ -259,17 +260,20 @@ struct G4 {
   const int* full_heads;
   const int* full_hcnt;
   const act_t* ZT;  // block l: [Bmax][H][fs][TP]  GELU'(z), written by G1
-  act_t* dO;        // [Bmax][H][T][dh]
-  act_t* dY1T;      // [Bmax][H][PQ][TP]  d[q|k|v|z], feature-major (G7's and G8's operand)
   float* part_db1; // [EPI][Bmax][H][fs]
   const float* gmax;
+  const CUtensorMap* maps;  // bulk-store maps: [3] dO (32 features x 32 tokens), [4] dY1T (32 tokens x 32 rows, 64B swizzle)
+  static constexpr int kChunk = 32;
+  static constexpr bool kNonEmpty = true;
+  static constexpr int kEpiStageBytes = 2048;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;
   };
   struct Row {
     int valid, h, f;
     float db;
-    uint4 gp0, gp1;  // GELU'(z) of the warp's next chunk (prefetched one chunk ahead)
+    uint4 gp[4];  // GELU'(z) of the warp's next chunk (prefetched one chunk ahead)
+    uint8_t* stage;
   };
   __device__ int ntiles() const { return *count; }
   __device__ int unit_row(int s, int u) const {
@@ -297,43 +301,63 @@ struct G4 {
     r.f = (u % D.UO) * 64 + (row & 63);
     r.valid = r.f < D.PO;
   }
-  // GELU' row of this feature, 16 contiguous tokens from col0 (two 16-byte
+  // GELU' row of this feature, 32 contiguous tokens from col0 (four 16-byte
   // loads), issued a chunk ahead so their latency hides behind the MMA wait.
   __device__ void prefetch(const Tile& c, int, int col0, Row& r) const {
     if (!r.valid || r.f < D.dh || col0 >= D.T) return;
     const act_t* z = ZT + (((size_t)c.s * D.H + r.h) * D.fs + (r.f - D.dh)) * D.TP + col0;
-    r.gp0 = col0 + 8 <= D.TP ? *reinterpret_cast<const uint4*>(z) : make_uint4(0, 0, 0, 0);
-    r.gp1 = col0 + 16 <= D.TP ? *reinterpret_cast<const uint4*>(z + 8) : make_uint4(0, 0, 0, 0);
-  }
-  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
-    if (!r.valid || col0 >= D.T) return;
-    const size_t sh = (size_t)c.s * D.H + r.h;
-    if (r.f < D.dh) {
-      act_t* o = dO + sh * D.T * D.dh + r.f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (col0 + i < D.T) o[(size_t)(col0 + i) * D.dh] = to_act(v[i]);
+    for (int q = 0; q < 4; ++q)
+      r.gp[q] = col0 + 8 * q + 8 <= D.TP ? *reinterpret_cast<const uint4*>(z + 8 * q) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[32], Row& r) const {
+    if (!r.valid || col0 >= D.T) return;  // warp-uniform
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's store has read the staging
+    __syncwarp();
+    const uint32_t sb = ptx::smem_u32(r.stage);
+    const int plane = c.s * D.H + r.h;
+    const int f0 = r.f - lane;
+    if (r.f < D.dh) {  // dO: staged [32 tokens][32 features]
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(maps + 3, r.stage, f0, col0, plane);
+        ptx::bulk_commit();
+      }
       return;
     }
-    const int j = r.f - D.dh;
-    const int fq = 3 * D.dh + j;
-    float dz[16];
-    {
-      __align__(16) act_t zz[16];
-      *reinterpret_cast<uint4*>(zz) = r.gp0;
-      *reinterpret_cast<uint4*>(zz + 8) = r.gp1;
+    uint32_t gz[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dz[i] = act_to_f(zz[i]);
+    for (int q = 0; q < 4; ++q) {
+      gz[4 * q] = r.gp[q].x;
+      gz[4 * q + 1] = r.gp[q].y;
+      gz[4 * q + 2] = r.gp[q].z;
+      gz[4 * q + 3] = r.gp[q].w;
     }
-    prefetch(c, row, col0 + 16 * kEpiGroups, r);
+    prefetch(c, row, col0 + 32 * kEpiGroups, r);
+    uint32_t hz[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      dz[i] = col0 + i < D.T ? v[i] * dz[i] : 0.f;
-      r.db += dz[i];
+      const float2 gp = __half22float2(*reinterpret_cast<const __half2*>(&gz[i]));
+      const float d0 = col0 + 2 * i < D.T ? v[2 * i] * gp.x : 0.f;
+      const float d1 = col0 + 2 * i + 1 < D.T ? v[2 * i + 1] * gp.y : 0.f;
+      r.db += d0 + d1;
+      const __half2 h = __floats2half2_rn(d0, d1);
+      hz[i] = *reinterpret_cast<const uint32_t*>(&h);
     }
-    act_t* dt = dY1T + (sh * D.PQ + fq) * D.TP + col0;
-    if (col0 + 8 <= D.TP) st_act_x8(dt, dz);
-    if (col0 + 16 <= D.TP) st_act_x8(dt + 8, dz + 8);
+    const uint32_t rb = sb + lane * 64, sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      ptx::st_shared_v4(rb + ((q ^ sw) << 4), hz[4 * q], hz[4 * q + 1], hz[4 * q + 2], hz[4 * q + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_3d(maps + 4, r.stage, col0, 3 * D.dh + (f0 - D.dh), plane);
+      ptx::bulk_commit();
+    }
   }
   // one partial per column group (summed in fixed order by bias_reduce)
   __device__ void row_end(const Tile& c, int, int group, Row& r) const {
