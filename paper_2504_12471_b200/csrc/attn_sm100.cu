@@ -256,7 +256,12 @@ __host__ __device__ inline int attn_bwd_tc_smem(int TQ) {
   return 4 * TQ * 128 + 4 * TQ * 128 + 1024;
 }
 
-__global__ void __launch_bounds__(128, 1)
+// 16 warps: warp w owns TMEM lane quarter w % 4 (its 32 keys / queries) and
+// column group w / 4 of every elementwise pass (softmax backward over the
+// query columns, dV / dK / dQ drains), so the latency-bound per-element work
+// of a cell runs on 4x the warps of one-warp-per-lane-quarter.
+constexpr int kBwdWarps = 16;
+__global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmdO,
                        const AttnBwdArgs a) {
   const Dims& D = a.D;
@@ -268,6 +273,7 @@ __global__ void __launch_bounds__(128, 1)
   const int nkt = (T + kQTile - 1) / kQTile;
   const size_t sh = (size_t)s * D.H + h;
   const uint32_t tile_bytes = (uint32_t)TQ * 128;
+  constexpr int NT = 32 * kBwdWarps;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -281,6 +287,7 @@ __global__ void __launch_bounds__(128, 1)
   __shared__ uint32_t tslot[1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q4 = warp & 3, cg = warp >> 2;  // TMEM lane quarter, column group
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmQKV);
     ptx::tma_prefetch(&tmdO);
@@ -300,28 +307,30 @@ __global__ void __launch_bounds__(128, 1)
     ptx::tma_load_3d(sdO, &tmdO, &bar[0], 0, 0, (int)sh);
   }
   // lse (log2 units; +inf past T so P = 0) and the O rows for D, loaded while the tiles land
-  for (int q = threadIdx.x; q < TQ; q += blockDim.x) lse2[q] = q < T ? a.lse[sh * T + q] : INFINITY;
-  for (int q0 = 0; q0 < TQ; q0 += blockDim.x) {
-    const int q = q0 + threadIdx.x;
-    act_t ov[64];
+  for (int q = threadIdx.x; q < TQ; q += NT) lse2[q] = q < T ? a.lse[sh * T + q] : INFINITY;
+  {
+    // D_q = sum_f dO[q][f] O[q][f]: two threads per query, 32 features each
+    const int q = threadIdx.x >> 1, hf = threadIdx.x & 1;
+    act_t ov[32];
     if (q < T) {
-      const act_t* o = a.OGT + sh * D.PO * D.TP + q;
+      const act_t* o = a.OGT + sh * D.PO * D.TP + (size_t)(32 * hf) * D.TP + q;
 #pragma unroll
-      for (int f = 0; f < 64; ++f) ov[f] = o[(size_t)f * D.TP];
+      for (int f = 0; f < 32; ++f) ov[f] = o[(size_t)f * D.TP];
     }
     ptx::mbar_wait(&bar[0], 0);
-    // D_q = sum_f dO[q][f] O[q][f]: dO row from the swizzled tile
     float acc = 0.f;
     if (q < T) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(sdO + q * 128 + ((c ^ (q & 7)) << 4));
+      for (int c = 0; c < 4; ++c) {
+        const int cc = 4 * hf + c;
+        const uint4 raw = *reinterpret_cast<const uint4*>(sdO + q * 128 + ((cc ^ (q & 7)) << 4));
         const act_t* hv = reinterpret_cast<const act_t*>(&raw);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * __half2float(ov[c * 8 + i]);
       }
     }
-    if (q < TQ) Dv[q] = acc;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (hf == 0 && q < TQ) Dv[q] = acc;
   }
   __syncthreads();
 
@@ -330,10 +339,11 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t idS = ptx::idesc_f16_m128(TQ, 0);                 // K-major A and B
   const uint32_t idG = ptx::idesc_f16_m128(64, 0) | (1u << 16);    // B (dh-wide tile) MN-major
   const uint32_t idQ = ptx::idesc_f16_m128(64, 0) | (1u << 15) | (1u << 16);  // A and B MN-major
-  const uint32_t lrow = (uint32_t)(warp * 32) << 16;
+  const uint32_t lrow = (uint32_t)(q4 * 32) << 16;
   const uint32_t SA = 0, SB = 256;
   act_t* dyt = a.dY1T + sh * D.PQ * D.TP;
   const uint32_t sds = ptx::smem_u32(sDS);
+  const int nch = TQ / 16;
   for (int kt = 0; kt < nkt; ++kt) {
     if (threadIdx.x == 0) {
       ptx::tc_fence_after();
@@ -350,9 +360,10 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::mbar_wait(&bar[1], kt & 1);
     ptx::tc_fence_after();
-    const int k = kt * kQTile + threadIdx.x;  // this thread's key (TMEM lane)
+    const int k = kt * kQTile + q4 * 32 + lane;  // this thread's key (TMEM lane)
     const bool kv = k < T;
-    for (int c0 = 0; c0 < TQ; c0 += 16) {
+    for (int j = cg; j < nch; j += 4) {
+      const int c0 = 16 * j;
       float sv[16], dp[16];
       ptx::tmem_ld16(tmem + lrow + SA + c0, sv);
       ptx::tmem_ld16(tmem + lrow + SB + c0, dp);
@@ -396,8 +407,8 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::mbar_wait(&bar[2], kt & 1);
     ptx::tc_fence_after();
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+    {
+      const int c0 = 16 * cg;  // this warp's 16 of the 64 dV / dK columns
       float dv[16], dk[16];
       ptx::tmem_ld16(tmem + lrow + SA + 128 + c0, dv);
       ptx::tmem_ld16(tmem + lrow + SB + 128 + c0, dk);
@@ -426,15 +437,13 @@ __global__ void __launch_bounds__(128, 1)
   ptx::mbar_wait(&bar[3], 0);
   ptx::tc_fence_after();
   for (int qt = 0; qt < nkt; ++qt) {
-    const int q = qt * kQTile + threadIdx.x;
+    const int q = qt * kQTile + q4 * 32 + lane;
+    const int c0 = 16 * cg;
+    float dq[16];
+    ptx::tmem_ld16(tmem + lrow + 64 * qt + c0, dq);
+    if (q < T) {
 #pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      float dq[16];
-      ptx::tmem_ld16(tmem + lrow + 64 * qt + c0, dq);
-      if (q < T) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) dyt[(size_t)(c0 + i) * D.TP + q] = to_act(dq[i] * scale);
-      }
+      for (int i = 0; i < 16; ++i) dyt[(size_t)(c0 + i) * D.TP + q] = to_act(dq[i] * scale);
     }
   }
   ptx::tc_fence_before();
@@ -458,7 +467,7 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
     attr = true;
   }
   dim3 grid(D.H, D.B);
-  attn_bwd_tc_kernel<<<grid, 128, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, OGT, lse, dY1T});
+  attn_bwd_tc_kernel<<<grid, 32 * kBwdWarps, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, OGT, lse, dY1T});
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
