@@ -27,6 +27,9 @@ void set_error(const std::string& msg);
 // (atomic: engines of an in-process partition group step on separate threads)
 extern std::atomic<unsigned long long> g_launches;
 inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+inline unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+// a CUDA graph replay launches the kernels it captured
+inline void add_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 struct Fail {
   int code;

@@ -143,6 +143,16 @@ struct Engine {
   double phase_ms[PH_COUNT] = {};
   int profiled_steps = 0;
 
+  // CUDA graph of one compute step (schedule + forward/backward + SGD) for a
+  // fixed (batch, micro-batch size, lr, momentum): the ~150 launches of a
+  // step replay without host launch overhead or inter-kernel gaps.  Eager
+  // when profiling (per-phase events) or partitioned (host-side exchange).
+  cudaGraphExec_t gexec = nullptr;
+  int g_nmb = -1, g_mbs = -1;
+  float g_lr = 0.f, g_mom = 0.f;
+  unsigned long long g_kernels = 0;  // kernels per replay (for d2ft_launch_count)
+  bool use_graphs = getenv("D2FT_NO_GRAPH") == nullptr;
+
   std::vector<cudaEvent_t> pool;
   void mark(int ph) {
     if (!profiling) return;
@@ -210,6 +220,7 @@ struct Engine {
 
   ~Engine() {
     for (auto e : pool) cudaEventDestroy(e);
+    if (gexec) cudaGraphExecDestroy(gexec);
     if (st) cudaStreamSynchronize(st);
     for (void* p : owned) cudaFree(p);
     if (h_samples) cudaFreeHost(h_samples);
@@ -621,10 +632,41 @@ struct Engine {
     D2FT_CUDA(cudaMemcpyAsync(cb_dev, cb, K * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, st));
-    schedule_device(n_mb, mbs);
-    run_forward_backward();
-    run_sgd((float)lr, (float)momentum);
+    compute_step(n_mb, mbs, lr, momentum);
     D2FT_CUDA(cudaMemcpyAsync(h_codes, codes_mb, KN, cudaMemcpyDeviceToHost, st));
+  }
+
+  // schedule + forward/backward + SGD on the staged device inputs (after begin_step)
+  void compute_step(int n_mb, int mbs, double lr, double momentum) {
+    if (profiling || partitioned() || !use_graphs) {
+      schedule_device(n_mb, mbs);
+      run_forward_backward();
+      run_sgd((float)lr, (float)momentum);
+      return;
+    }
+    if (!gexec || g_nmb != n_mb || g_mbs != mbs || g_lr != (float)lr || g_mom != (float)momentum) {
+      if (gexec) {
+        D2FT_CUDA(cudaGraphExecDestroy(gexec));
+        gexec = nullptr;
+      }
+      cudaGraph_t g = nullptr;
+      const unsigned long long n0 = d2ft_b200::launch_count();
+      D2FT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      schedule_device(n_mb, mbs);
+      run_forward_backward();
+      run_sgd((float)lr, (float)momentum);
+      D2FT_CUDA(cudaStreamEndCapture(st, &g));
+      g_kernels = d2ft_b200::launch_count() - n0;
+      D2FT_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+      D2FT_CUDA(cudaGraphDestroy(g));
+      g_nmb = n_mb;
+      g_mbs = mbs;
+      g_lr = (float)lr;
+      g_mom = (float)momentum;
+    } else {
+      d2ft_b200::add_launches(g_kernels);
+    }
+    D2FT_CUDA(cudaGraphLaunch(gexec, st));
   }
 
   void begin_step(int B) {
@@ -878,9 +920,7 @@ int d2ft_engine_bench_device(d2ft_engine* h, int n_mb, int mbs, double lr, doubl
     Engine& E = *h->e;
     for (int i = 0; i < warmup; ++i) {
       E.begin_step(n_mb * mbs);
-      E.schedule_device(n_mb, mbs);
-      E.run_forward_backward();
-      E.run_sgd((float)lr, (float)momentum);
+      E.compute_step(n_mb, mbs, lr, momentum);
     }
     check_status(E.finish_and_check());
     cudaEvent_t e0, e1;
@@ -889,9 +929,7 @@ int d2ft_engine_bench_device(d2ft_engine* h, int n_mb, int mbs, double lr, doubl
     D2FT_CUDA(cudaEventRecord(e0, E.st));
     for (int i = 0; i < steps; ++i) {
       E.begin_step(n_mb * mbs);
-      E.schedule_device(n_mb, mbs);
-      E.run_forward_backward();
-      E.run_sgd((float)lr, (float)momentum);
+      E.compute_step(n_mb, mbs, lr, momentum);
     }
     D2FT_CUDA(cudaEventRecord(e1, E.st));
     D2FT_CUDA(cudaEventSynchronize(e1));
@@ -933,9 +971,7 @@ int d2ft_engine_step_resident(d2ft_engine* h, int n_mb, int mbs, double lr, doub
   return guarded([&] {
     Engine& E = *h->e;
     E.begin_step(n_mb * mbs);
-    E.schedule_device(n_mb, mbs);
-    E.run_forward_backward();
-    E.run_sgd((float)lr, (float)momentum);
+    E.compute_step(n_mb, mbs, lr, momentum);
   });
 }
 
