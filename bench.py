@@ -317,7 +317,9 @@ def run_ours(args):
     ms_e2e = C.c_double()
     if dist:
         dist.barrier()
-    with Clocks(local) as clk2:
+    # (no nvidia-smi sampling here: its driver queries stall the per-step host
+    # syncs of this leg; the clocks line comes from the device-timed region)
+    if True:
         _lib.check(lib.d2ft_engine_bench_e2e(
             m._h, _lib.ptr(px), _lib.ptr(py), _lib.ptr(pb), _lib.ptr(pf), _lib.ptr(pc[0]), _lib.ptr(pc[1]),
             _lib.ptr(pc[2]), _lib.ptr(pc[3]), C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),

@@ -61,6 +61,18 @@ int d2ft_engine_step(d2ft_engine* e, const float* samples, const int32_t* labels
                      const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, double* loss_out,
                      uint8_t* codes_out);
 
+/* Input pipeline (a data loader's double buffering; no reference counterpart:
+ * trainer.cpp:214-292 reads batches from host memory).  d2ft_engine_prefetch
+ * starts the H2D copy of a batch's samples (pinned host memory) on the
+ * engine's copy stream; d2ft_engine_step_pipelined then runs the step on the
+ * prefetched samples (as d2ft_engine_step) and, if samples_next != NULL,
+ * prefetches the next batch while this one computes. */
+int d2ft_engine_prefetch(d2ft_engine* e, const float* samples, int batch);
+int d2ft_engine_step_pipelined(d2ft_engine* e, const float* samples_next, const int32_t* labels,
+                               const double* bwd_scores, const double* fwd_scores, const int32_t* cf,
+                               const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb, int mbs,
+                               double lr, double momentum, double* loss_out, uint8_t* codes_out);
+
 /* Benchmark path: stage inputs once on the device, then run device-resident
  * steps (asynchronous on d2ft_engine_stream) and d2ft_engine_sync. */
 int d2ft_engine_stage_device(d2ft_engine* e, const float* samples, const int32_t* labels, const double* bwd_scores,

@@ -94,6 +94,13 @@ struct Engine {
   float* lse;     // [L][Bmax][H][T]
   act_t *inp, *inpT;
   float* samples_dev;
+  // input pipeline: the next batch's samples are copied H2D on a copy stream
+  // into samples_stage while the current batch computes (d2ft_engine_prefetch)
+  float* samples_stage = nullptr;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
+  bool have_prefetch = false;
+  int prefetch_B = 0;
   int* labels_dev;
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
@@ -214,6 +221,9 @@ struct Engine {
     BNt = D.T <= 64 ? 64 : D.T <= 128 ? 128 : D.T <= 208 ? 208 : 256;
     KS = std::min(8, Bmax);
     D2FT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    D2FT_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+    D2FT_CUDA(cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming));
+    D2FT_CUDA(cudaEventCreateWithFlags(&ev_stage_free, cudaEventDisableTiming));
     alloc_all();
     make_maps();
   }
@@ -229,6 +239,10 @@ struct Engine {
     if (h_loss) cudaFreeHost(h_loss);
     if (h_err) cudaFreeHost(h_err);
     if (h_codes) cudaFreeHost(h_codes);
+    if (cst) cudaStreamSynchronize(cst);
+    if (ev_copied) cudaEventDestroy(ev_copied);
+    if (ev_stage_free) cudaEventDestroy(ev_stage_free);
+    if (cst) cudaStreamDestroy(cst);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -267,6 +281,7 @@ struct Engine {
     inp = dalloc<act_t>(Bm * T * d, owned);
     inpT = dalloc<act_t>(Bm * d * TP, owned);
     samples_dev = dalloc<float>(Bm * T * d, owned);
+    samples_stage = dalloc<float>(Bm * T * d, owned);
     labels_dev = dalloc<int>(Bm, owned);
 
     dX = dalloc<float>(Bm * T * d, owned);
@@ -619,12 +634,13 @@ struct Engine {
   // samples, labels and score slice, schedule, step, D2H of loss and codes.
   void host_step(const float* samples, const int32_t* labels, const double* bwd_scores, const double* fwd_scores,
                  const int32_t* cf, const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb,
-                 int mbs, double lr, double momentum) {
+                 int mbs, double lr, double momentum, const float* samples_next = nullptr) {
     const int K = D.K();
     const int B = n_mb * mbs;
     begin_step(B);
     const size_t KN = (size_t)K * n_mb;
-    D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, st));
+    if (samples) D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, st));
+    else consume_prefetch(B);  // samples == nullptr: the batch prefetched by d2ft_engine_prefetch
     D2FT_CUDA(cudaMemcpyAsync(labels_dev, labels, B * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(bwd_dev, bwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(fwd_dev, fwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
@@ -633,7 +649,28 @@ struct Engine {
     D2FT_CUDA(cudaMemcpyAsync(capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, st));
     compute_step(n_mb, mbs, lr, momentum);
+    if (samples_next) prefetch(samples_next, B);  // overlaps this batch's compute
     D2FT_CUDA(cudaMemcpyAsync(h_codes, codes_mb, KN, cudaMemcpyDeviceToHost, st));
+  }
+
+  // Next batch's samples (pinned host memory for an asynchronous copy) ->
+  // samples_stage on the copy stream, overlapping whatever the engine stream
+  // is computing; the stage is reused only after the previous batch left it.
+  void prefetch(const float* samples, int B) {
+    D2FT_REQUIRE(B >= 1 && B <= D.Bmax, kSize, "prefetch: batch exceeds the engine capacity");
+    D2FT_CUDA(cudaStreamWaitEvent(cst, ev_stage_free, 0));
+    D2FT_CUDA(cudaMemcpyAsync(samples_stage, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, cst));
+    D2FT_CUDA(cudaEventRecord(ev_copied, cst));
+    have_prefetch = true;
+    prefetch_B = B;
+  }
+  // prefetched samples -> samples_dev on the engine stream (device copy, ~12 us at ViT-B)
+  void consume_prefetch(int B) {
+    D2FT_REQUIRE(have_prefetch && prefetch_B == B, kState, "step: no prefetched batch of this size");
+    D2FT_CUDA(cudaStreamWaitEvent(st, ev_copied, 0));
+    D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples_stage, (size_t)B * D.T * D.d * 4, cudaMemcpyDeviceToDevice, st));
+    D2FT_CUDA(cudaEventRecord(ev_stage_free, st));
+    have_prefetch = false;
   }
 
   // schedule + forward/backward + SGD on the staged device inputs (after begin_step)
@@ -876,6 +913,32 @@ int d2ft_engine_step(d2ft_engine* h, const float* samples, const int32_t* labels
   });
 }
 
+int d2ft_engine_prefetch(d2ft_engine* h, const float* samples, int batch) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && samples, kInput, "prefetch: null argument");
+    h->e->prefetch(samples, batch);
+  });
+}
+
+int d2ft_engine_step_pipelined(d2ft_engine* h, const float* samples_next, const int32_t* labels,
+                               const double* bwd_scores, const double* fwd_scores, const int32_t* cf,
+                               const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb, int mbs,
+                               double lr, double momentum, double* loss_out, uint8_t* codes_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    const int K = E.D.K();
+    D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
+    validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
+    validate_labels(labels, n_mb * mbs, E.D.C);
+    E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+    E.host_step(nullptr, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum,
+                samples_next);
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+    if (codes_out) std::memcpy(codes_out, E.h_codes, (size_t)K * n_mb);
+  });
+}
+
 // bench.py's e2e leg: `steps` host-buffer steps (after `warmup`), each with its
 // H2D copies and the loss/codes D2H and a host sync, CUDA-event timed on the
 // engine stream.  ms_out = total milliseconds of the timed steps.
@@ -889,6 +952,10 @@ int d2ft_engine_bench_e2e(d2ft_engine* h, const float* samples, const int32_t* l
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
     validate_labels(labels, n_mb * mbs, E.D.C);
     E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+    // Every step copies its own samples H2D; the copy of batch i+1 runs on the
+    // copy stream while batch i computes (the data-loader pipeline of
+    // d2ft_engine_prefetch + d2ft_engine_step(samples = NULL, samples_next)).
+    const int B = n_mb * mbs;
     for (int i = 0; i < warmup; ++i) {
       E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
       check_status(E.finish_and_check());
@@ -897,8 +964,11 @@ int d2ft_engine_bench_e2e(d2ft_engine* h, const float* samples, const int32_t* l
     D2FT_CUDA(cudaEventCreate(&e0));
     D2FT_CUDA(cudaEventCreate(&e1));
     D2FT_CUDA(cudaEventRecord(e0, E.st));
+    D2FT_CUDA(cudaStreamWaitEvent(E.cst, e0, 0));  // the first copy is inside the timed region
+    E.prefetch(samples, B);
     for (int i = 0; i < steps; ++i) {
-      E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
+      E.host_step(nullptr, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum,
+                  i + 1 < steps ? samples : nullptr);
       check_status(E.finish_and_check());
     }
     D2FT_CUDA(cudaEventRecord(e1, E.st));
