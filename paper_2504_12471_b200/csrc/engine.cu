@@ -25,6 +25,7 @@
 #include "step_gemms.cuh"
 #include "step_kernels.cuh"
 
+constexpr int kG7BN = 224;  // G7 N tile: PQ = 448 = 2 x 224 (ViT-B/L)
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
@@ -89,7 +90,7 @@ struct Engine {
   // activations
   float* x;       // [L+1][Bmax][T][d]
   float* stats;   // [L][Bmax][T][2]
-  act_t *xn, *xnT; // [L][Bmax][T][d], [L][Bmax][d][TP]
+  act_t* xn;  // [L][Bmax][T][d] (G1's B; G7's A read MN-major)
   act_t *QKV, *ZT, *OGT;
   float* lse;     // [L][Bmax][H][T]
   act_t *inp, *inpT;
@@ -104,7 +105,7 @@ struct Engine {
   int* labels_dev;
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
-  act_t *dC, *dCT, *dO, *dY1T;
+  act_t *dC, *dO, *dY1T;  // dC: G4's B, G5's / EmbedW's A (read MN-major)
   double *loss_s, *loss;
   float *pooled, *dlog;
   // schedule / compaction
@@ -140,8 +141,8 @@ struct Engine {
   uint8_t* h_codes = nullptr;
 
   // tensor maps
-  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_W2T, tm_dC, tm_dCT, tm_OGT, tm_OGT64, tm_dY1T, tm_xnT, tm_Q, tm_K, tm_V, tm_dO,
-      tm_inpT;
+  CUtensorMap tm_WeT, tm_inp, tm_W1T, tm_xn, tm_xn64, tm_W2T, tm_dC, tm_dC64, tm_OGT, tm_OGT64, tm_dY1T, tm_dY1Tb,
+      tm_Q, tm_K, tm_V, tm_dO, tm_inpT;
 
   // profiling
   bool profiling = false;
@@ -273,7 +274,6 @@ struct Engine {
     x = dalloc<float>((L + 1) * Bm * T * d, owned);
     stats = dalloc<float>(L * Bm * T * 2, owned);
     xn = dalloc<act_t>(L * Bm * T * d, owned);
-    xnT = dalloc<act_t>(L * Bm * d * TP, owned);
     QKV = dalloc<act_t>(L * Bm * H * T * 3 * D.dh, owned);
     ZT = dalloc<act_t>(L * Bm * H * fs * TP, owned);
     OGT = dalloc<act_t>(L * Bm * H * PO * TP, owned);
@@ -291,7 +291,6 @@ struct Engine {
     part_db1 = dalloc<float>((size_t)kEpiGroups * Bm * H * fs, owned);
     part_ew = dalloc<float>((size_t)KS * d * d, owned);
     dC = dalloc<act_t>(Bm * T * d, owned);
-    dCT = dalloc<act_t>(Bm * d * TP, owned);
     dO = dalloc<act_t>(Bm * H * T * D.dh, owned);
     dY1T = dalloc<act_t>(Bm * H * PQ * TP, owned);
     loss_s = dalloc<double>(Bm, owned);
@@ -358,7 +357,9 @@ struct Engine {
     tm_WeT = make_tmap_f16_3d(WeT_bf, d, d, 1, d * 2, d * d * 2, 64);
     tm_W1T = make_tmap_f16_3d(W1T_bf, d, H * PQ, L, d * 2, H * PQ * d * 2, 64);
     tm_W2T = make_tmap_f16_3d(W2T_bf, H * PO, d, L, H * PO * 2, d * H * PO * 2, 64);
-    tm_dCT = make_tmap_f16_3d(dCT, T, d, Bm, TP * 2, d * TP * 2, 64);
+    // MN-major A (64 M x 64 K boxes): dC for G5 / EmbedW, xn for G7
+    tm_dC64 = make_tmap_f16_3d(dC, d, T, Bm, d * 2, T * d * 2, 64);
+    tm_xn64 = make_tmap_f16_3d(xn, d, T, L * Bm, d * 2, T * d * 2, 64);
     tm_dY1T = make_tmap_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 64);
     // B operands, tokens as N (box BNt/2: each CTA of a pair loads half, multicast)
     tm_inp = make_tmap_f16_3d(inp, d, T, Bm, d * 2, T * d * 2, BNt / 2);
@@ -388,7 +389,7 @@ struct Engine {
     // (tm_dY1T above doubles as G8's MN-major B)
     // B operands, tokens as K (half boxes, multicast)
     tm_OGT = make_tmap_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 80);
-    tm_xnT = make_tmap_f16_3d(xnT, T, d, L * Bm, TP * 2, d * TP * 2, 128);
+    tm_dY1Tb = make_tmap_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, kG7BN / 2);  // G7's B (half per CTA)
     tm_inpT = make_tmap_f16_3d(inpT, T, d, Bm, TP * 2, d * TP * 2, 128);
   }
 
@@ -489,7 +490,7 @@ struct Engine {
     gemm_tokN<EmbedFwd>(tm_WeT, tm_inp, D, P + seg[S_BE].off, P + seg[S_POS].off, x);
     for (int l = 0; l < D.L; ++l) {
       mark(PH_LN);
-      launch_ln_fwd(D, x + l * xs, xn + l * xs, xnT + (size_t)l * Bm * d * D.TP, stats + (size_t)l * Bm * T * 2, st);
+      launch_ln_fwd(D, x + l * xs, xn + l * xs, stats + (size_t)l * Bm * T * 2, st);
       mark(PH_G1);
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
@@ -520,7 +521,7 @@ struct Engine {
                 dlog, dX, gmax, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
-    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, dCT, part_cs, gmax, st);
+    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, part_cs, gmax, st);
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
@@ -537,15 +538,15 @@ struct Engine {
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
       mark(PH_G5);
-      launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2>>(
-          tm_dCT, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
+      launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2, 0, 1>>(
+          tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
                   ord_head + l * H, ctr(l, C_G5)},
           0, st);
       mark(PH_G7);
-      launch_gemm<G7<256>, GemmShape<256, 4, 0, 4, 2>>(
-          tm_dY1T, tm_xnT,
-          G7<256>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
-                  ord_head + l * H, ctr(l, C_G7)},
+      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, 5, 0, 4, 2, 0, 1>>(
+          tm_xn64, tm_dY1Tb,
+          G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                    ord_head + l * H, ctr(l, C_G7)},
           0, st);
       mark(PH_G8);
       gemm_tokN<G8, 1, 1>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
@@ -558,11 +559,11 @@ struct Engine {
       launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
                          G + seg[S_B2].off + (size_t)l * d, st);
       mark(PH_LN_BWD);
-      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, dCT, part_cs,
+      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, part_cs,
                          gmax, st);
     }
     mark(PH_EMBED_W);
-    launch_gemm<EmbedW<256>, GemmShape<256, 4, 0, 4, 2>>(tm_dCT, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
+    launch_gemm<EmbedW<256>, GemmShape<256, 4, 0, 4, 2, 0, 1>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
   }
 

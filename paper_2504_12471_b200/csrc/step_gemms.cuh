@@ -368,7 +368,8 @@ struct G4 {
 
 // ---------------------------------------------------------------- G5
 // dW2T[l][m][h*PO + f] = sum_{s in Full(h)} sum_t dC[s][t][m] [O|g][s][h][t][f]
-// (model.cpp:249, 263).  A = dCT (plane s), B = OGT (plane (l*Bmax+s)*H+h).
+// (model.cpp:249, 263).  A = dC read MN-major (plane s, [t][m] as [K][M]),
+// B = OGT (plane (l*Bmax+s)*H+h).
 template <int BN>
 struct G5 {
   Dims D;
@@ -426,8 +427,10 @@ struct G5 {
 };
 
 // ---------------------------------------------------------------- G7
-// dW1T[l][h][f][m] = sum_{s in Full(h)} sum_t d[q|k|v|z][s][h][t][f] xn[s][t][m]
-// (model.cpp:256, 286).  A = dY1T (plane s*H+h), B = xnT (plane l*Bmax+s).
+// dW1T[l][h][f][m] = sum_{s in Full(h)} sum_t xn[s][t][m] d[q|k|v|z][s][h][f][t]
+// (model.cpp:256, 286).  M = model features m (d = 6 x 128: no padded rows),
+// N = the head's PQ = 2 x 224 features, K = tokens of the head's Full samples.
+// A = xn read MN-major (token-major [t][m] as [K][M]), B = dY1T (K-major).
 template <int BN>
 struct G7 {
   Dims D;
@@ -444,9 +447,9 @@ struct G7 {
   struct Row {
     float inv;
   };
-  __device__ int ntm() const { return (D.PQ + 127) / 128; }
-  __device__ int ntn() const { return (D.d + BN - 1) / BN; }
-  // slot = (head, m-tile pair, n-tile): the pair shares B = xn^T of sample s
+  __device__ int ntm() const { return (D.d + 127) / 128; }
+  __device__ int ntn() const { return (D.PQ + BN - 1) / BN; }
+  // slot = (head, m-tile pair, n-tile): the pair shares B = dY1T rows of (s, h)
   __device__ int ntiles() const { return D.H * mpairs(ntm()) * ntn(); }
   __device__ void tile(int t, int rank, Tile& c) const {
     const int per = mpairs(ntm()) * ntn();
@@ -463,24 +466,18 @@ struct G7 {
   __device__ KCoord kcoord(const Tile& c, int kb) const {
     const int s = full_idx[(size_t)(l * D.H + c.h) * D.Bmax + kb / D.TB];
     const int t0 = (kb % D.TB) * 64;
-    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s * D.H + c.h, t0, c.nt * BN, l * D.Bmax + s};
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, l * D.Bmax + s, t0, c.nt * BN, s * D.H + c.h};
   }
   __device__ void row_begin(const Tile&, int, Row& r) const { r.inv = 1.f / grad_scale(gmax); }
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
-    const int f = c.mt * 128 + row;
-    if (f >= D.PQ) return;
-    float* out = dW1T + ((size_t)c.h * D.PQ + f) * D.d;
-    const int n0 = c.nt * BN + col0;
-    const float k = r.inv;
-    if (n0 + 16 <= D.d) {
+    const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
+    const int f0 = c.nt * BN + col0;
+    // lanes hold consecutive m: each store instruction writes 128 contiguous bytes
+    float* out = dW1T + ((size_t)c.h * D.PQ + f0) * D.d + m;
 #pragma unroll
-      for (int i = 0; i < 16; i += 4)
-        *reinterpret_cast<float4*>(out + n0 + i) = make_float4(v[i] * k, v[i + 1] * k, v[i + 2] * k, v[i + 3] * k);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (n0 + i < D.d) out[n0 + i] = v[i] * k;
-    }
+    for (int i = 0; i < 16; ++i)
+      if (f0 + i < D.PQ) out[(size_t)i * D.d] = v[i] * r.inv;
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}
 };
@@ -536,6 +533,7 @@ struct G8 {
 // ---------------------------------------------------------------- embed wgrad
 // dWeT[m][j] = sum_s sum_t dx0[s][t][m] inp[s][t][j]  (model.cpp:514), split
 // over KS sample groups into partial sums (reduced deterministically later).
+// A = dC read MN-major, B = inpT.
 template <int BN>
 struct EmbedW {
   Dims D;

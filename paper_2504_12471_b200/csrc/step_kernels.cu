@@ -123,19 +123,13 @@ __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inp
 }
 
 template <int NV>
-__global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, float* stats) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  act_t* tile = reinterpret_cast<act_t*>(smem);
-  const int pitch = D.d + 2;
+__global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nv = NV;
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
-    if (t >= D.T) {
-      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = to_act(0.f);
-      continue;
-    }
+    if (t >= D.T) continue;
     const float* row = x + ((size_t)s * D.T + t) * D.d;
     float v[NV];
     float sum = 0.f;
@@ -158,28 +152,19 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, act_t* xnT, flo
     act_t* out = xn + ((size_t)s * D.T + t) * D.d;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
-      if (j < nv) {
-        const act_t b = to_act((v[j] - mean) * rstd);
-        out[lane + 32 * j] = b;
-        tile[r * pitch + lane + 32 * j] = b;
-      }
+      if (j < nv) out[lane + 32 * j] = to_act((v[j] - mean) * rstd);
     if (lane == 0) {
       stats[((size_t)s * D.T + t) * 2] = mean;
       stats[((size_t)s * D.T + t) * 2 + 1] = rstd;
     }
   }
-  __syncthreads();
-  write_transposed(tile, pitch, D.d, t0, D.TP, xnT + (size_t)s * D.d * D.TP);
 }
 
 template <int NV>
 __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                                   const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs,
-                                   const float* gmax) {
+                                   const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax) {
   extern __shared__ __align__(16) unsigned char smem[];
-  act_t* tile = reinterpret_cast<act_t*>(smem);
-  const int pitch = D.d + 2;
-  float* cs = reinterpret_cast<float*>(smem + (size_t)32 * pitch * 2 + 16);  // [8][d]
+  float* cs = reinterpret_cast<float*>(smem);  // [8][d]
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nv = NV;
@@ -189,10 +174,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
   for (int j = 0; j < NV; ++j) acc[j] = 0.f;
   for (int r = warp; r < 32; r += 8) {
     const int t = t0 + r;
-    if (t >= D.T) {
-      for (int m = lane; m < D.d; m += 32) tile[r * pitch + m] = to_act(0.f);
-      continue;
-    }
+    if (t >= D.T) continue;
     const size_t ro = ((size_t)s * D.T + t) * D.d;
     float v[NV];
 #pragma unroll
@@ -222,9 +204,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
 #pragma unroll
     for (int j = 0; j < NV; ++j)
       if (j < nv) {
-        const act_t b = to_act(v[j] * S);
-        dC[ro + lane + 32 * j] = b;
-        tile[r * pitch + lane + 32 * j] = b;
+        dC[ro + lane + 32 * j] = to_act(v[j] * S);
         acc[j] += v[j];
       }
   }
@@ -232,7 +212,6 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
   for (int j = 0; j < NV; ++j)
     if (j < nv) cs[warp * D.d + lane + 32 * j] = acc[j];
   __syncthreads();
-  write_transposed(tile, pitch, D.d, t0, D.TP, dCT + (size_t)s * D.d * D.TP);
   const int ntile = (D.T + 31) / 32;
   for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
     float c = 0.f;
@@ -904,25 +883,21 @@ void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, c
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st) {
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
-  const size_t sm = tile_smem(D);
-  D2FT_NV_DISPATCH(D.d, {
-    D2FT_CUDA(cudaFuncSetAttribute(ln_fwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ln_fwd_kernel<NV><<<grid, 256, sm, st>>>(D, x, xn, xnT, stats);
-  });
+  D2FT_NV_DISPATCH(D.d, { ln_fwd_kernel<NV><<<grid, 256, 0, st>>>(D, x, xn, stats); });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs, const float* gmax,
+                        const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax,
                         cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
-  const size_t sm = tile_smem(D) + (size_t)8 * D.d * 4;
+  const size_t sm = (size_t)8 * D.d * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, dCT, part_cs, gmax);
+    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, part_cs, gmax);
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());

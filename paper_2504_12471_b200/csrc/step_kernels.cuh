@@ -24,8 +24,8 @@ void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, const 
                  cudaStream_t st);
 // fp32 samples [B][T][d] -> act_t token-major + feature-major copies
 void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st);
-// LayerNorm (no affine, eps 1e-5) of x -> xn (token-major), xnT (feature-major), stats (mean, rstd)
-void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, act_t* xnT, float* stats, cudaStream_t st);
+// LayerNorm (no affine, eps 1e-5) of x -> xn (token-major fp16), stats (mean, rstd)
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st);
 // attention forward / backward (one CTA per (sample, active|Full head) slot)
 // (O feature-major into OGT rows 0..dh-1; dq|dk|dv feature-major into dY1T rows 0..3dh-1)
 void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OGT,
@@ -50,9 +50,9 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                         float* dbc, double* loss, cudaStream_t st);
 // dX += LN_bwd(x_l, dxn) for samples with a Full head in block l (if l >= 0), then
-// emit dC (act_t token-major), dCT (feature-major) and per-tile column sums.
+// emit dC (act_t token-major) and per-tile column sums.
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, act_t* dC, act_t* dCT, float* part_cs, const float* gmax,
+                        const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax,
                         cudaStream_t st);
 void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
                         float* db1_l, float* db2_l, cudaStream_t st);
