@@ -61,10 +61,10 @@ __host__ __device__ inline int attn_tc_smem(int TQ) { return 2 * attn_fwd_stage_
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const AttnFwdArgs a) {
+  pdl_trigger();
   const Dims& D = a.D;
   const int TQ = D.TQ, T = D.T;
   const int nkv = (TQ + 63) / 64, nqt = (T + kQTile - 1) / kQTile;
-  const int nitems = *a.count;
   const uint32_t stage = attn_fwd_stage_bytes(TQ);
 
   extern __shared__ uint8_t smem_raw[];
@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();
+  const int nitems = *a.count;
   auto decode = [&](int i, int& s, int& h) {
     const int it = a.items[i];
     s = it >> 8;
@@ -264,6 +266,7 @@ constexpr int kBwdWarps = 16;
 __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmdO,
                        const AttnBwdArgs a) {
+  D2FT_PDL_ENTRY();
   const Dims& D = a.D;
   const int s = blockIdx.y, slot = blockIdx.x;
   if (s >= D.B || slot >= a.full_hcnt[s * D.L + a.l]) return;

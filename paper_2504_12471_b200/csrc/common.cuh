@@ -31,6 +31,23 @@ inline unsigned long long launch_count() { return g_launches.load(std::memory_or
 // a CUDA graph replay launches the kernels it captured
 inline void add_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Programmatic dependent launch (the step's CUDA graph links consecutive
+// kernels with programmatic edges, Engine::compute_step): every kernel lets
+// its successor launch right away (pdl_trigger) and waits for its
+// predecessor's completion and memory (pdl_wait) before touching data the
+// predecessor may write.  Both are no-ops for an ordinary launch.
+#ifndef D2FT_NO_PDL_TRIGGER
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#else
+__device__ __forceinline__ void pdl_trigger() {}
+#endif
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define D2FT_PDL_ENTRY() \
+  do {                   \
+    ::d2ft_b200::pdl_trigger(); \
+    ::d2ft_b200::pdl_wait();    \
+  } while (0)
+
 struct Fail {
   int code;
   std::string msg;

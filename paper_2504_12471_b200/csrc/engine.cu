@@ -160,6 +160,34 @@ struct Engine {
   float g_lr = 0.f, g_mom = 0.f;
   unsigned long long g_kernels = 0;  // kernels per replay (for d2ft_launch_count)
   bool use_graphs = getenv("D2FT_NO_GRAPH") == nullptr;
+  // opt-in (D2FT_PDL=1): measured slower on the ViT-B step (6.13 / 5.96 ms with
+  // early / implicit trigger vs 5.88 ms plain graph edges)
+  bool use_pdl = getenv("D2FT_PDL") != nullptr;
+
+  // kernel -> kernel edges of the captured step become programmatic
+  // (programmatic dependent launch): the successor launches as soon as every
+  // CTA of its predecessor has started (pdl_trigger at kernel entry) and runs
+  // its prologue (barrier init, TMEM allocation, descriptor prefetch) on the
+  // SMs the predecessor's tail leaves idle; pdl_wait orders the data.
+  static void make_edges_programmatic(cudaGraph_t g) {
+    size_t n = 0;
+    D2FT_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &n));
+    std::vector<cudaGraphNode_t> from(n), to(n);
+    std::vector<cudaGraphEdgeData> ed(n);
+    D2FT_CUDA(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &n));
+    for (size_t i = 0; i < n; ++i) {
+      cudaGraphNodeType a, b;
+      D2FT_CUDA(cudaGraphNodeGetType(from[i], &a));
+      D2FT_CUDA(cudaGraphNodeGetType(to[i], &b));
+      if (a != cudaGraphNodeTypeKernel || b != cudaGraphNodeTypeKernel || ed[i].type != cudaGraphDependencyTypeDefault)
+        continue;
+      D2FT_CUDA(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1));
+      cudaGraphEdgeData e{};
+      e.from_port = cudaGraphKernelNodePortProgrammatic;
+      e.type = cudaGraphDependencyTypeProgrammatic;
+      D2FT_CUDA(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &e, 1));
+    }
+  }
 
   std::vector<cudaEvent_t> pool;
   void mark(int ph) {
@@ -695,6 +723,7 @@ struct Engine {
       run_sgd((float)lr, (float)momentum);
       D2FT_CUDA(cudaStreamEndCapture(st, &g));
       g_kernels = d2ft_b200::launch_count() - n0;
+      if (use_pdl) make_edges_programmatic(g);
       D2FT_CUDA(cudaGraphInstantiate(&gexec, g, 0));
       D2FT_CUDA(cudaGraphDestroy(g));
       g_nmb = n_mb;

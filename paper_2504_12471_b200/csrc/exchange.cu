@@ -86,6 +86,7 @@ struct Ptrs {
   const float* p[kMaxLocal];
 };
 __global__ void sum_ranks_kernel(Ptrs in, int world, size_t n, float* out) {
+  D2FT_PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     float acc = in.p[0][i];
     for (int r = 1; r < world; ++r) acc += in.p[r][i];  // fixed rank order on every rank
@@ -153,6 +154,7 @@ struct LocalExchange final : Exchange {
 };
 
 __global__ void mask_rows_kernel(uint8_t* codes, int K, int Bmax, int H, int rank, int world) {
+  D2FT_PDL_ENTRY();
   const size_t n = (size_t)K * Bmax;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / Bmax);

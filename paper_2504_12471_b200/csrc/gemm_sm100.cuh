@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint64_t* kq_full = sch.kq_full;
   uint64_t* kq_empty = sch.kq_empty;
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = S::CLUSTER == 2 ? (int)ptx::cluster_rank() : 0;
   const int slot0 = blockIdx.x / S::CLUSTER, nslots = gridDim.x / S::CLUSTER;
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the prologue above overlapped the previous kernel's tail
   const int ntiles = prob.ntiles();
 
   // Tile sequence, produced by warp 3 into the ring.  Static: slot0, slot0 +

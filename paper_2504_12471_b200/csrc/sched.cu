@@ -180,6 +180,7 @@ __device__ void column_lists(const uint8_t* codes, int K, int N, int H, const Co
 }
 
 __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
+  D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int k = blockIdx.x;
   const int N = A.N;
@@ -263,6 +264,7 @@ struct DpConstArgs {
 };
 
 __global__ void __launch_bounds__(kThreads) dp_const_kernel(DpConstArgs A) {
+  D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int k = A.rows[blockIdx.x];
   const int N = A.N;
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(kThreads) dp_general_kernel(const double* scor
                                                                const int32_t* caps, const int32_t* rows, int N,
                                                                int max_cap, uint8_t* sel, double* obj,
                                                                uint32_t* bits_global, double* vals_global) {
+  D2FT_PDL_ENTRY();
   const int k = rows[blockIdx.x];
   const int cap = caps[k];
   const int W = cap + 1;
@@ -333,11 +336,13 @@ __global__ void __launch_bounds__(kThreads) dp_general_kernel(const double* scor
 }
 
 __global__ void merge_kernel(const uint8_t* a, const uint8_t* b, size_t n, uint8_t* codes) {
+  D2FT_PDL_ENTRY();
   for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < n; c += (size_t)gridDim.x * blockDim.x)
     codes[c] = a[c] ? 1 : (b[c] ? 2 : 3);
 }
 
 __global__ void compact_rows_kernel(const uint8_t* codes, int N, CompactLists L) {
+  D2FT_PDL_ENTRY();
   extern __shared__ uint8_t s_codes[];
   const int k = blockIdx.x;
   for (int i = threadIdx.x; i < N; i += blockDim.x) s_codes[i] = codes[(size_t)k * N + i];
@@ -347,6 +352,7 @@ __global__ void compact_rows_kernel(const uint8_t* codes, int N, CompactLists L)
 }
 
 __global__ void compact_cols_kernel(const uint8_t* codes, int K, int N, int H, CompactLists L) {
+  D2FT_PDL_ENTRY();
   column_lists(codes, K, N, H, L, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
@@ -357,6 +363,7 @@ __global__ void __launch_bounds__(kThreads) scaler_kernel(const double* bwd, con
                                                           const int32_t* cb, const int32_t* total_cap, int N,
                                                           const double* lambda_dev, int max_cap, uint8_t* codes,
                                                           uint8_t* choice_global, double* vals_global) {
+  D2FT_PDL_ENTRY();
   const int k = blockIdx.x;
   const int cap = total_cap[k];
   const int W = cap + 1;
@@ -414,6 +421,7 @@ __global__ void __launch_bounds__(kThreads) scaler_kernel(const double* bwd, con
 __global__ void __launch_bounds__(kThreads) brute_kernel(const double* bwd, const double* fwd, const int32_t* cf,
                                                          const int32_t* cb, const int32_t* cap_full,
                                                          const int32_t* cap_fwd, int N, int total, uint8_t* codes) {
+  D2FT_PDL_ENTRY();
   const int k = blockIdx.x;
   const int cap = cap_full[k] + cap_fwd[k];
   const int c_full = cf[k] + cb[k], c_fwd = cf[k];

@@ -16,6 +16,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // ------------------------------------------------------------------ codes / plan
 __global__ void expand_codes_kernel(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out) {
+  D2FT_PDL_ENTRY();
   const size_t n = (size_t)K * Bmax;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / Bmax), s = (int)(i % Bmax);
@@ -32,6 +33,7 @@ __device__ __forceinline__ int desc_rank(const int* v, int n, int i) {
 }
 
 __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, Plan pl) {
+  D2FT_PDL_ENTRY();
   const int l = blockIdx.x;
   __shared__ int s1[1024], s4[1024], va[1024], vf[1024], sa[1024], sf[1024], vh[64];
   int c1 = 0, c4 = 0;
@@ -101,6 +103,7 @@ __device__ __forceinline__ void write_transposed(const act_t* tile, int pitch, i
 
 template <int NV>
 __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inpT) {
+  D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   act_t* tile = reinterpret_cast<act_t*>(smem);
   const int pitch = D.d + 2;
@@ -124,6 +127,7 @@ __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inp
 
 template <int NV>
 __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
+  D2FT_PDL_ENTRY();
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nv = NV;
@@ -163,6 +167,7 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
 template <int NV>
 __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
                                    const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax) {
+  D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   float* cs = reinterpret_cast<float*>(smem);  // [8][d]
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
@@ -226,6 +231,7 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
 template <int NV>
 __global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                             double* loss_s, float* pooled_out, float* dlog_out, float* dX, float* gmax) {
+  D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int nw = blockDim.x >> 5;
   float* part = reinterpret_cast<float*>(smem);  // [nw][d]
@@ -333,6 +339,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
 
 __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                                    float* dbc, double* loss) {
+  D2FT_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < D.d * D.C) {
     const int m = i / D.C, c = i % D.C;
@@ -360,6 +367,7 @@ __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* po
 // full memory parallelism despite only (d + H*fs)/32 CTAs.
 __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs,
                                                            const float* part_db1, float* db1_l, float* db2_l) {
+  D2FT_PDL_ENTRY();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const 
 
 __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const float* part_cs, const float* dX,
                                     float* dWeT, float* dbe, float* dpos) {
+  D2FT_PDL_ENTRY();
   const size_t dd = (size_t)D.d * D.d;
   const size_t td = (size_t)D.T * D.d;
   const int ntile = (D.T + 31) / 32;
@@ -419,6 +428,7 @@ __global__ void embed_reduce_kernel(Dims D, int KS, const float* part, const flo
 // fixed-order combine (deterministic).  db_embed (model.cpp:515) from the
 // per-tile column sums of the LN-backward kernel.
 __global__ void __launch_bounds__(1024) colsum_kernel(const float* in, int rows, int cols, float* out) {
+  D2FT_PDL_ENTRY();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -437,6 +447,7 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float* in, int rows,
 // ------------------------------------------------------------------ SGD / copies
 __global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner,
                            int H, const int* full_cnt, float lr, float mom, int* err) {
+  D2FT_PDL_ENTRY();
   // 4 consecutive elements per thread (every segment's `inner` is a multiple of 4)
   const size_t n4 = n / 4;
   for (size_t i4 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i4 < n4 + (n % 4 ? 1 : 0);
@@ -485,6 +496,7 @@ __global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_
 }
 
 __global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
+  D2FT_PDL_ENTRY();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = to_act(in[i]);
 }
@@ -571,6 +583,7 @@ __device__ __forceinline__ void store_frag_T(const float (&o)[DH / 8][4], float 
 template <int DH, int MINB>
 __global__ void __launch_bounds__(MINB == 2 ? 416 : 512, MINB) attn_fwd_kernel(Dims D, int l, const int* act_heads, const int* act_cnt,
                                                        const act_t* QKV, act_t* OGT, float* lse) {
+  D2FT_PDL_ENTRY();
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= act_cnt[s * D.L + l]) return;
   const int h = act_heads[(s * D.L + l) * D.H + a];
@@ -700,6 +713,7 @@ template <int DH>
 __global__ void __launch_bounds__(512) attn_bwd_kernel(Dims D, int l, const int* full_heads, const int* full_hcnt,
                                                        const act_t* QKV, const act_t* OGT, const act_t* dO,
                                                        const float* lse, act_t* dY1T) {
+  D2FT_PDL_ENTRY();
   const int s = blockIdx.y, a = blockIdx.x;
   if (s >= D.B || a >= full_hcnt[s * D.L + l]) return;
   const int h = full_heads[(s * D.L + l) * D.H + a];
