@@ -46,6 +46,8 @@ struct AttnFwdArgs {
   const int* act_heads;
   act_t* OGT;  // block l
   float* lse;  // block l
+  const uint8_t* codes;  // expanded K x Bmax (code 1 = Full)
+  float* O32T;           // block l: [Bmax][H][64][TP] fp32 O of Full cells (the backward's D)
 };
 
 __host__ __device__ inline int attn_fwd_stage_bytes(int TQ) {
@@ -209,6 +211,12 @@ __global__ void __launch_bounds__(384, 1)
       ptx::tc_fence_after();
       const float inv = 1.f / sum;
       act_t* o = a.OGT + sh * D.PO * D.TP + row;
+      // Full cells also keep O in fp32: the backward's D = rowsum(dO . O) must be
+      // consistent with its dP = dO V^T to the fp32 level (the softmax backward
+      // dP - D cancels strongly when tokens are alike; an fp16 O costs ~1e-2 on
+      // the wq/wk gradients at ViT-L)
+      const bool full = a.codes[(size_t)(a.l * D.H + h) * D.Bmax + s] == 1;
+      float* o32 = a.O32T + sh * 64 * D.TP + row;
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 16) {
         float v[16];
@@ -216,6 +224,10 @@ __global__ void __launch_bounds__(384, 1)
         if (row < T) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) o[(size_t)(c0 + j) * D.TP] = to_act(v[j] * inv);
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o32[(size_t)(c0 + j) * D.TP] = v[j] * inv;
+          }
         }
       }
       ptx::tc_fence_before();
@@ -249,9 +261,9 @@ struct AttnBwdArgs {
   int l;
   const int* full_heads;
   const int* full_hcnt;
-  const act_t* OGT;  // block l
-  const float* lse;  // block l
-  act_t* dY1T;       // [Bmax][H][PQ][TP]
+  const float* O32T;  // block l: [Bmax][H][64][TP] fp32 O (attention forward, Full cells)
+  const float* lse;   // block l
+  act_t* dY1T;        // [Bmax][H][PQ][TP]
 };
 
 __host__ __device__ inline int attn_bwd_tc_smem(int TQ) {
@@ -314,9 +326,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   {
     // D_q = sum_f dO[q][f] O[q][f]: two threads per query, 32 features each
     const int q = threadIdx.x >> 1, hf = threadIdx.x & 1;
-    act_t ov[32];
+    float ov[32];
     if (q < T) {
-      const act_t* o = a.OGT + sh * D.PO * D.TP + (size_t)(32 * hf) * D.TP + q;
+      const float* o = a.O32T + sh * 64 * D.TP + (size_t)(32 * hf) * D.TP + q;
 #pragma unroll
       for (int f = 0; f < 32; ++f) ov[f] = o[(size_t)f * D.TP];
     }
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const uint4 raw = *reinterpret_cast<const uint4*>(sdO + q * 128 + ((cc ^ (q & 7)) << 4));
         const act_t* hv = reinterpret_cast<const act_t*>(&raw);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * __half2float(ov[c * 8 + i]);
+        for (int i = 0; i < 8; ++i) acc += __half2float(hv[i]) * ov[c * 8 + i];
       }
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -460,7 +472,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
 }  // namespace
 
 void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const Dims& D, int l, const int* full_heads,
-                        const int* full_hcnt, const act_t* OGT, const float* lse, act_t* dY1T, cudaStream_t st) {
+                        const int* full_hcnt, const float* O32T, const float* lse, act_t* dY1T, cudaStream_t st) {
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_bwd_tc_smem(D.TQ);
   D2FT_REQUIRE(attn_bwd_tc_fits(D.TQ), kConfig, "tcgen05 attention backward: shared memory");
@@ -470,14 +482,14 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
     attr = true;
   }
   dim3 grid(D.H, D.B);
-  attn_bwd_tc_kernel<<<grid, 32 * kBwdWarps, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, OGT, lse, dY1T});
+  attn_bwd_tc_kernel<<<grid, 32 * kBwdWarps, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, O32T, lse, dY1T});
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
                         const int* items, const int* count, const int* act_heads, act_t* OGT, float* lse,
-                        cudaStream_t st) {
+                        const uint8_t* codes, float* O32T, cudaStream_t st) {
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_tc_smem(D.TQ);
   static bool attr = false;
@@ -485,7 +497,7 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max_attn()));
     attr = true;
   }
-  attn_fwd_tc_kernel<<<num_sms(), 384, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse});
+  attn_fwd_tc_kernel<<<num_sms(), 384, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse, codes, O32T});
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

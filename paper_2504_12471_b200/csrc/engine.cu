@@ -93,6 +93,7 @@ struct Engine {
   act_t* xn;  // [L][Bmax][T][d] (G1's B; G7's A read MN-major)
   act_t *QKV, *ZT, *OGT;
   float* lse;     // [L][Bmax][H][T]
+  float* O32T = nullptr;  // [L][Bmax][H][64][TP] fp32 attention output of Full cells (tcgen05 path)
   act_t *inp, *inpT;
   float* samples_dev;
   // input pipeline: the next batch's samples are copied H2D on a copy stream
@@ -306,6 +307,7 @@ struct Engine {
     ZT = dalloc<act_t>(L * Bm * H * fs * TP, owned);
     OGT = dalloc<act_t>(L * Bm * H * PO * TP, owned);
     lse = dalloc<float>(L * Bm * H * T, owned);
+    if (D.dh == 64) O32T = dalloc<float>(L * Bm * H * 64 * TP, owned);
     inp = dalloc<act_t>(Bm * T * d, owned);
     inpT = dalloc<act_t>(Bm * d * TP, owned);
     samples_dev = dalloc<float>(Bm * T * d, owned);
@@ -530,7 +532,7 @@ struct Engine {
       mark(PH_ATTN_F);
       if (D.dh == 64 && D.TQ <= 256)
         launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, af_items + l * Bm * H, af_count + l, lists.act_heads, OGTl,
-                           lse + (size_t)l * Bm * H * T, st);
+                           lse + (size_t)l * Bm * H * T, codes_exp, O32T + (size_t)l * Bm * H * 64 * D.TP, st);
       else
         launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
@@ -560,7 +562,8 @@ struct Engine {
                           (const act_t*)ZTl, part_db1, (const float*)gmax, (const CUtensorMap*)store_maps);
       mark(PH_ATTN_B);
       if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
-        launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, OGTl, lse + (size_t)l * Bm * H * T,
+        launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, O32T + (size_t)l * Bm * H * 64 * D.TP,
+                           lse + (size_t)l * Bm * H * T,
                            dY1T, st);
       else
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,

@@ -127,14 +127,28 @@ struct G1 {
   __device__ void chunk(const Tile& c, int, int col0, const float (&v)[32], Row& r) const {
     if (!r.valid || col0 >= D.T) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
-    if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's stores have read the staging
-    __syncwarp();
+    // the staging is single-buffered: the previous chunk's bulk stores must
+    // have read it; that wait comes after this chunk's math, which hides it
+    auto staging_free = [&]() {
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    };
     const uint32_t sb = ptx::smem_u32(r.stage);
     const int plane = (l * D.Bmax + c.s) * D.H + r.h;
     const int f0 = r.f - lane;  // the warp's first feature row
     if (r.f < 3 * D.dh) {  // q, k, v: staged [32 tokens][32 features]
+      uint32_t hv[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
+      for (int i = 0; i < 16; ++i) {
+        const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        hv[i] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      staging_free();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        ptx::st_shared_u16(sb + (2 * i) * 64 + lane * 2, (unsigned short)(hv[i] & 0xffffu));
+        ptx::st_shared_u16(sb + (2 * i + 1) * 64 + lane * 2, (unsigned short)(hv[i] >> 16));
+      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -157,6 +171,7 @@ struct G1 {
     // 64-byte swizzle (chunk ^ (row >> 1) & 3) keeps the 8 lanes of each
     // store phase on distinct banks
     const uint32_t rb = sb + lane * 64, sw = (lane >> 1) & 3;
+    staging_free();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t o = ((q ^ sw) << 4);
@@ -313,14 +328,26 @@ struct G4 {
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[32], Row& r) const {
     if (!r.valid || col0 >= D.T) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
-    if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's store has read the staging
-    __syncwarp();
+    auto staging_free = [&]() {  // the previous chunk's store has read the staging (after this chunk's math)
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    };
     const uint32_t sb = ptx::smem_u32(r.stage);
     const int plane = c.s * D.H + r.h;
     const int f0 = r.f - lane;
     if (r.f < D.dh) {  // dO: staged [32 tokens][32 features]
+      uint32_t hv[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) ptx::st_shared_u16(sb + i * 64 + lane * 2, __half_as_ushort(to_act(v[i])));
+      for (int i = 0; i < 16; ++i) {
+        const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        hv[i] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      staging_free();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        ptx::st_shared_u16(sb + (2 * i) * 64 + lane * 2, (unsigned short)(hv[i] & 0xffffu));
+        ptx::st_shared_u16(sb + (2 * i + 1) * 64 + lane * 2, (unsigned short)(hv[i] >> 16));
+      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -349,6 +376,7 @@ struct G4 {
       hz[i] = *reinterpret_cast<const uint32_t*>(&h);
     }
     const uint32_t rb = sb + lane * 64, sw = (lane >> 1) & 3;
+    staging_free();
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       ptx::st_shared_v4(rb + ((q ^ sw) << 4), hz[4 * q], hz[4 * q + 1], hz[4 * q + 2], hz[4 * q + 3]);

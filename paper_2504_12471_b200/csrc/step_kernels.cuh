@@ -37,12 +37,12 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 // (K), 64 x 64 (V) rows; planes (l*Bmax + s)*H + h
 void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV, const Dims& D, int l,
                         const int* items, const int* count, const int* act_heads, act_t* OGT, float* lse,
-                        cudaStream_t st);
+                        const uint8_t* codes, float* O32T, cudaStream_t st);
 int sm_max_attn();
 // tcgen05 attention backward (attn_sm100.cu), dh = 64: tmQKV = the K map above
 // (box 64 x TQ), tmdO over dO [Bmax][H][T][dh] with box 64 x TQ
 void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const Dims& D, int l, const int* full_heads,
-                        const int* full_hcnt, const act_t* OGT, const float* lse, act_t* dY1T, cudaStream_t st);
+                        const int* full_hcnt, const float* O32T, const float* lse, act_t* dY1T, cudaStream_t st);
 bool attn_bwd_tc_fits(int TQ);
 // head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, dlogits, and dX = dL/dx_L
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,

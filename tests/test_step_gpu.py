@@ -163,3 +163,47 @@ def test_vitb_full_batch_step_properties():
     assert np.array_equal(outs[0][1], O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd))
     assert np.isfinite(outs[0][0]) and outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_vitl_forward_backward_one_sample():
+    """ViT-L/16 dims (BASELINE configs[3]: 24x16, d=1024, ffn=4096, T=197; 16
+    heads = the widest head list of the GEMM tile caches), 1 sample, mixed
+    column, against the fp64 oracle."""
+    cfg = E.VIT_L16
+    oc, sl = _cfgs(cfg)
+    p = E.partition_model(cfg)
+    x, y = E.make_synthetic_dataset(8, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    x, y = x[:1], y[:1]
+    K = cfg.scheduled_subnet_count()
+    col = np.array([(1, 2, 3, 1, 2, 1, 3)[k % 7] for k in range(K)], np.uint8)
+    m = E.SubnetModel(cfg, 1, p)
+    loss, g, eng = m.forward_backward(x, y, col)
+    m.close()
+    rl, rg, reng = MO.forward_backward(oc, p, x.astype(np.float64), y, col)
+    assert np.array_equal(eng, reng)
+    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
+    bad = compare_tensors(g, rg, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+
+
+def test_vitl_batch_step_properties():
+    """ViT-L/16 batch 32 with ragged random scores (384 scheduled rows): the
+    schedule is bit-exact vs the oracle and the step is finite and
+    deterministic across two fresh engines."""
+    cfg = E.VIT_L16
+    B = 32
+    x, y = E.make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    K = cfg.scheduled_subnet_count()
+    b, f = O.bench_scores(K, B, 1)
+    nb = (2 * B) // 5
+    caps = P.Capacities([nb * 5] * K, [nb * 2] * K)
+    st = P.ScoreTable(K, B, f, b)
+    outs = []
+    for _ in range(2):
+        m = E.SubnetModel(cfg, B)
+        loss, table = m.d2ft_step(x, y, st, P.CostModel(), caps)
+        outs.append((loss, table.codes.copy(), m.params()))
+        m.close()
+    assert np.array_equal(outs[0][1], O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd))
+    assert np.isfinite(outs[0][0]) and outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][2], outs[1][2])
