@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-vitl", action="store_true", help="skip the ViT-L/16 batch-256 1-GPU leg")
     return ap.parse_args()
 
 
@@ -154,6 +155,48 @@ def gemm_flops(codes_exp, B):
         Fk = 2.0 * T * (4 * D * dh + 2 * T * dh + 2 * D * (FFN // H))
         total_alg = (3 * Fk * cell_full + Fk * (cell_act - cell_full)) + 4.0 * T * D * D * B
     return fl, total_alg
+
+
+def vitl_leg(steps=3, warmup=2, B=256):
+    """BASELINE configs[3]'s model and batch (ViT-L/16, L24 H16 d1024 ffn4096,
+    batch 256) on ONE B200: device-resident steps, same schedule recipe and
+    data generators as the headline.  The config names 8 B200 (head partition,
+    --gpus 8); this leg reports what a single GPU does with that batch."""
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    from paper_2504_12471_b200 import scheduler as S
+    lib = _lib.lib()
+    cfg = E.VIT_L16
+    Lq, Hq, Dq = cfg.num_blocks, cfg.heads_per_block, cfg.model_dim
+    dh, fs = Dq // Hq, cfg.ffn_hidden // Hq
+    K = Lq * Hq
+    x, y = E.make_synthetic_dataset(B, NCLS, Dq, T, 0.5, 7)
+    u = np.empty(2 * K * B)
+    _lib.check(lib.d2ft_uniform_stream(C.c_uint64(1), C.c_uint64(0), C.c_int(u.size), _lib.ptr(u)))
+    u = u.reshape(K, B, 2) * 10.0
+    fwd, bwd = np.ascontiguousarray(u[:, :, 0]), np.ascontiguousarray(u[:, :, 1])
+    nb = (2 * B) // 5
+    capf, capo = np.full(K, nb * 5, np.int32), np.full(K, nb * 2, np.int32)
+    m = E.SubnetModel(cfg, B)
+    m.stage(x, y, S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
+    ms, loss = C.c_double(), C.c_double()
+    _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+                                            C.c_int(warmup), C.c_int(steps), C.byref(ms), C.byref(loss)))
+    codes = np.zeros((K, B), np.uint8)
+    _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes)))
+    m.close()
+    full = float((codes == 1).sum())
+    act = float(((codes == 1) | (codes == 2)).sum())
+    Fk = 2.0 * T * (4 * Dq * dh + 2 * T * dh + 2 * Dq * fs)
+    alg = 3 * Fk * full + Fk * (act - full) + 4.0 * T * Dq * Dq * B
+    ms_step = ms.value / steps
+    tf = alg / (ms_step * 1e-3) / 1e12
+    peak = PEAKS["bf16_tflops_sustained"]
+    return {"workload": f"ViT-L/16 (L24 H16 d1024 ffn4096 T197, {K} head-subnets) D2FT step, batch {B}, "
+                        f"per-sample schedule, 1 B200 (BASELINE configs[3] names 8 B200)",
+            "value": B / (ms_step * 1e-3), "unit": "samples/s", "ms_per_step": ms_step, "steps": steps,
+            "warmup": warmup, "loss": loss.value, "tflop_per_step": alg / 1e12, "achieved_tflops": round(tf, 1),
+            "frac": round(tf / peak, 4)}
 
 
 def cpu_baseline(codes_mb, threads, steps=1, warmup=0, lr=0.05, momentum=0.9):
@@ -366,6 +409,12 @@ def run_ours(args):
         if codes is not None:
             r = cpu_baseline(codes, os.cpu_count() or 1)
             cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    vitl = None
+    if rank == 0 and world == 1 and not args.no_vitl:
+        try:
+            vitl = vitl_leg()
+        except Exception as e:  # reported, never fatal for the headline line
+            vitl = {"error": str(e)[:200]}
     if rank == 0:
         line = {
             "metric": "D2FT ViT-B/16 samples/s", "value": value, "unit": "samples/s", "n_gpus": world,
@@ -399,6 +448,8 @@ def run_ours(args):
         }
         if part_info:
             line["partition"] = part_info
+        if vitl:
+            line["vitl_1gpu"] = vitl
         print(json.dumps(line))
     m.close()
     if dist:
