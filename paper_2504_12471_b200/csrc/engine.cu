@@ -14,6 +14,7 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <chrono>
 
 #include "../../include/d2ft_b200.h"
 #include "../../include/d2ft_b200_engine.h"
@@ -671,8 +672,9 @@ struct Engine {
     const int B = n_mb * mbs;
     begin_step(B);
     const size_t KN = (size_t)K * n_mb;
-    if (samples) D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, st));
-    else consume_prefetch(B);  // samples == nullptr: the batch prefetched by d2ft_engine_prefetch
+    // the small H2D copies go first: the host->device copy engine serves
+    // transfers in submission order, so behind a prefetch of the next batch's
+    // samples (released by consume_prefetch below) they would wait ~0.7 ms
     D2FT_CUDA(cudaMemcpyAsync(labels_dev, labels, B * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(bwd_dev, bwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(fwd_dev, fwd_scores, KN * 8, cudaMemcpyHostToDevice, st));
@@ -680,6 +682,8 @@ struct Engine {
     D2FT_CUDA(cudaMemcpyAsync(cb_dev, cb, K * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(capf_dev, cap_full, K * 4, cudaMemcpyHostToDevice, st));
     D2FT_CUDA(cudaMemcpyAsync(capo_dev, cap_fwd, K * 4, cudaMemcpyHostToDevice, st));
+    if (samples) D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples, (size_t)B * D.T * D.d * 4, cudaMemcpyHostToDevice, st));
+    else consume_prefetch(B);  // samples == nullptr: the batch prefetched by d2ft_engine_prefetch
     compute_step(n_mb, mbs, lr, momentum);
     if (samples_next) prefetch(samples_next, B);  // overlaps this batch's compute
     D2FT_CUDA(cudaMemcpyAsync(h_codes, codes_mb, KN, cudaMemcpyDeviceToHost, st));
@@ -999,10 +1003,32 @@ int d2ft_engine_bench_e2e(d2ft_engine* h, const float* samples, const int32_t* l
     D2FT_CUDA(cudaEventRecord(e0, E.st));
     D2FT_CUDA(cudaStreamWaitEvent(E.cst, e0, 0));  // the first copy is inside the timed region
     E.prefetch(samples, B);
+    const bool trace = getenv("D2FT_E2E_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
     for (int i = 0; i < steps; ++i) {
+      const auto h0 = std::chrono::steady_clock::now();
+      if (trace) {
+        tev.emplace_back();
+        D2FT_CUDA(cudaEventCreate(&tev.back()));
+        D2FT_CUDA(cudaEventRecord(tev.back(), E.st));
+      }
       E.host_step(nullptr, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum,
                   i + 1 < steps ? samples : nullptr);
+      const auto h1 = std::chrono::steady_clock::now();
       check_status(E.finish_and_check());
+      const auto h2 = std::chrono::steady_clock::now();
+      if (trace)
+        fprintf(stderr, "e2e step %d: enqueue %.3f ms, sync %.3f ms\n", i,
+                std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                std::chrono::duration<double, std::milli>(h2 - h1).count());
+    }
+    if (trace) {
+      for (size_t i = 1; i < tev.size(); ++i) {
+        float ms = 0.f;
+        D2FT_CUDA(cudaEventElapsedTime(&ms, tev[i - 1], tev[i]));
+        fprintf(stderr, "e2e gpu step %zu: %.3f ms\n", i - 1, ms);
+      }
+      for (auto e : tev) cudaEventDestroy(e);
     }
     D2FT_CUDA(cudaEventRecord(e1, E.st));
     D2FT_CUDA(cudaEventSynchronize(e1));
