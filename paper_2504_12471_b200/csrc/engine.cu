@@ -27,6 +27,10 @@
 #include "step_kernels.cuh"
 
 constexpr int kG7BN = 224;  // G7 N tile: PQ = 448 = 2 x 224 (ViT-B/L)
+#ifndef D2FT_CG2
+#define D2FT_CG2 1  // pair UMMA (cta_group::2) for the K-major-B GEMMs; 0 = B multicast (experiment builds)
+#endif
+constexpr int kCG2 = D2FT_CG2;
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
@@ -490,22 +494,27 @@ struct Engine {
   // Tokens-as-N GEMMs on CTA pairs; BMN = 1: B is a feature-major buffer
   // read MN-major (its 64-token blocks cost more shared memory per stage).
   // AMN = 1: A (weights) read MN-major from the other GEMM's copy.
-  template <template <int> class Prob, int BMN = 0, int AMN = 0, int EPI = 4, class... Args>
+  template <template <int> class Prob, int BMN = 0, int AMN = 0, int EPI = 4, int PAIR_UMMA = 1, class... Args>
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
+    // K-major B: pair UMMA (cta_group::2, B split across the pair, deeper
+    // pipeline); MN-major B: B multicast to both CTAs of the pair.  G1 keeps
+    // multicast: its epilogue is the limiter and the pair UMMA couples the two
+    // CTAs' epilogues through one accumulator release (0.91 vs 0.95 ms).
+    constexpr int CG = (BMN || !PAIR_UMMA) ? 0 : kCG2;
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8, 0, EPI, 2, BMN, AMN>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, 8, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, 6, 0, EPI, 2, BMN, AMN>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, CG ? 8 : 6, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        // 4 stages when the B blocks are MN-major or the epilogue stages bulk stores
-        launch_gemm<Prob<208>, GemmShape<208, (BMN || epi_stage_bytes<Prob<208>>::value) ? 4 : 5, 0, EPI, 2, BMN, AMN>>(
-            a, b, Prob<208>{args...}, 0, st);
+        // 4 stages when the B blocks are MN-major or the epilogue stages bulk stores (multicast B)
+        launch_gemm<Prob<208>, GemmShape<208, CG ? 6 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? 4 : 5), 0, EPI, 2,
+                                         BMN, AMN, CG>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, 4, 0, EPI, 2, BMN, AMN>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, CG ? 5 : 4, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
@@ -527,7 +536,7 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
-      gemm_tokN<G1, 0, 0, D2FT_G1_EPI>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads,
+      gemm_tokN<G1, 0, 0, D2FT_G1_EPI, 0>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads,
                                        lists.act_cnt, (const uint8_t*)codes_exp, P + seg[S_B1].off + (size_t)l * H * D.fs,
                                        (const CUtensorMap*)store_maps);
       mark(PH_ATTN_F);
@@ -570,12 +579,12 @@ struct Engine {
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
       mark(PH_G5);
-      launch_gemm<G5<160>, GemmShape<160, 6, 0, 4, 2, 0, 1>>(
+      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
                   ord_head + l * H, ctr(l, C_G5)},
           0, st);
       mark(PH_G7);
-      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, 5, 0, 4, 2, 0, 1>>(
+      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
           tm_xn64, tm_dY1Tb,
           G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
                     ord_head + l * H, ctr(l, C_G7)},
@@ -595,7 +604,7 @@ struct Engine {
                          gmax, st);
     }
     mark(PH_EMBED_W);
-    launch_gemm<EmbedW<256>, GemmShape<256, 4, 0, 4, 2, 0, 1>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
+    launch_gemm<EmbedW<256>, GemmShape<256, kCG2 ? 6 : 4, 0, 4, 2, 0, 1, kCG2>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
   }
 

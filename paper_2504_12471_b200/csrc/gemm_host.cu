@@ -263,7 +263,12 @@ int d2ft_test_gemm_dense(const uint16_t* A, const uint16_t* B, int M, int N, int
     D2FT_CUDA(cudaMemcpy(dA.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemcpy(dB.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
     D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
-    if (bn == -208) {  // CTA pair, B multicast
+    if (bn == -2208) {  // CTA pair, pair UMMA (cta_group::2, B split)
+      using S = GemmShape<208, 6, 1, 4, 2, 0, 0, 1>;
+      CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+      CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 104);
+      launch_gemm<DensePairProb<208>, S>(a, b, DensePairProb<208>{M, N, K, dD.p}, 0, nullptr);
+    } else if (bn == -208) {  // CTA pair, B multicast
       using S = GemmShape<208, 5, 1, 4, 2>;
       CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
       CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 104);

@@ -141,15 +141,23 @@ constexpr int gemm_smem_bytes() {
 // AMN: A operand layout.  0 = K-major; 1 = MN-major (A stored [K][M] with M
 // contiguous, e.g. a weight matrix kept in the other GEMM's orientation): the
 // two 64-row halves of the tile are two 64(M) x 64(K) boxes, LBO = 8 KB.
-template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0, int AMN_ = 0>
+// CG2: pair UMMA (`tcgen05.mma.cta_group::2`, M = 256 across the CTA pair):
+// each CTA holds its own 128 A rows and HALF of B (N/2 rows) — B is split, not
+// multicast, so a stage is A + B/2 bytes per CTA and more stages fit; the even
+// CTA issues the MMAs for both, its mbarriers count both CTAs' TMA bytes, and
+// its commits arrive on both CTAs' barriers.  K-major B only.
+template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0, int AMN_ = 0,
+          int CG2_ = 0>
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
-  static constexpr int BMN = BMN_, AMN = AMN_;
+  static constexpr int BMN = BMN_, AMN = AMN_, CG2 = CG2_;
+  static_assert(!CG2 || (CLUSTER == 2 && !BMN), "pair UMMA needs a CTA pair and a K-major B");
   static constexpr int NBLK = (BN + 63) / 64;  // MN-major B: 64-wide N blocks
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BMN ? NBLK * 64 * BK * 2 : BN * BK * 2;
-  static constexpr int B_PART = B_BYTES / CLUSTER;  // bytes of B each CTA loads (K-major)
+  // B bytes held per CTA and stage (CG2: this CTA's N/2 rows)
+  static constexpr int B_BYTES = BMN ? NBLK * 64 * BK * 2 : (CG2 ? BN * BK : BN * BK * 2);
+  static constexpr int B_PART = CG2 ? B_BYTES : B_BYTES / CLUSTER;  // bytes of B each CTA loads (K-major)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
@@ -195,11 +203,12 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     ptx::tma_prefetch(&tmB);
     for (int i = 0; i < S::STAGES; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], S::CLUSTER);  // both CTAs' MMAs read the stage (multicast B)
+      // multicast B: both CTAs' MMAs read the stage; pair UMMA: the even CTA's commit
+      ptx::mbar_init(&empty[i], S::CG2 ? 1 : S::CLUSTER);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4 * S::EPI);
+      ptx::mbar_init(&tempty[i], 4 * S::EPI * (S::CG2 ? 2 : 1));  // pair UMMA: both CTAs' epilogues
     }
     for (int i = 0; i < kTileQ; ++i) {
       ptx::mbar_init(&tq_full[i], 1);
@@ -215,7 +224,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if constexpr (S::CG2) ptx::tmem_alloc_cg2(tmem_slot, 512);
+    else ptx::tmem_alloc(tmem_slot, 512);
+  }
   ptx::tc_fence_before();
   if (S::CLUSTER == 2) ptx::cluster_sync();  // peers' barriers exist before any multicast
   else __syncthreads();
@@ -307,6 +319,25 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           const KCoord k = kq[j].k;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * S::A_BYTES;
+          if constexpr (S::CG2) {
+            // both CTAs' bytes complete on the even CTA's full barrier
+            const uint32_t fb = ptx::mapa(&full[stage], 0);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+            if constexpr (S::AMN) {
+              ptx::tma_load_3d_cg2(a, &tmA, fb, k.ay0, k.ax, k.az);
+              ptx::tma_load_3d_cg2(a + S::A_BYTES / 2, &tmA, fb, k.ay1, k.ax, k.az);
+            } else {
+              ptx::tma_load_3d_cg2(a, &tmA, fb, k.ax, k.ay0, k.az);
+              ptx::tma_load_3d_cg2(a + S::A_BYTES / 2, &tmA, fb, k.ax, k.ay1, k.az);
+            }
+            ptx::tma_load_3d_cg2(sB + stage * S::B_BYTES, &tmB, fb, k.bx, k.by + rank * (S::BN / 2), k.bz);
+            ptx::mbar_arrive(&kq_empty[j]);
+            if (++stage == S::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
           if constexpr (S::AMN) {  // boxes of 64 M (inner) x 64 K rows
             ptx::tma_load_3d(a, &tmA, &full[stage], k.ay0, k.ax, k.az);
@@ -339,12 +370,25 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     // The whole warp runs the MMA loop (warp-uniform control flow keeps the
     // descriptors in uniform registers); one elected lane issues the UMMAs
     // and commits.
-    constexpr uint32_t idesc =
-        ptx::idesc_f16_m128(S::BN, S::FMT) | (S::AMN ? (1u << 15) : 0u) | (S::BMN ? (1u << 16) : 0u);
+    constexpr uint32_t idesc = ptx::idesc_f16(S::CG2 ? 256 : 128, S::BN, S::FMT) | (S::AMN ? (1u << 15) : 0u) |
+                               (S::BMN ? (1u << 16) : 0u);
+    // pair UMMA: the odd CTA's MMA warp only keeps the ring / k-block queue flowing
+    const bool issuer = !S::CG2 || rank == 0;
     int stage = 0, acc = 0, kqm = 0;
     uint32_t phase = 0, acc_phase = 0;
     for_each_tile(lane == 0, [&](const typename P::Tile& cref) {
       const typename P::Tile c = cref;  // registers (smem reads would be re-done around every store)
+      if (!issuer) {
+        if constexpr (has_ksteps<P>::value) {
+          for (int kb = 0; kb < c.nkb; ++kb, ++kqm) {
+            const int j = kqm % kKQ;
+            ptx::mbar_wait(&kq_full[j], (kqm / kKQ) & 1);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&kq_empty[j]);
+          }
+        }
+        return;
+      }
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem + acc * 256;
@@ -370,9 +414,14 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         if (ptx::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < S::BK / 16; ++kk)
-            if (kk < nk)
-              ptx::umma_bf16(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
-          if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
+            if (kk < nk) {
+              if constexpr (S::CG2)
+                ptx::umma_f16_cg2(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
+              else
+                ptx::umma_bf16(d, ad + (uint64_t)kk * astep, bd + (uint64_t)kk * bstep, idesc, (kb | kk) != 0);
+            }
+          if constexpr (S::CG2) ptx::umma_commit_cg2_mc(&empty[stage], kPair);
+          else if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
           else ptx::umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -381,7 +430,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           phase ^= 1;
         }
       }
-      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+      if (ptx::elect_one()) {
+        if constexpr (S::CG2) ptx::umma_commit_cg2_mc(&tfull[acc], kPair);  // both CTAs' epilogues
+        else ptx::umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -414,7 +466,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       auto release = [&]() {
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (S::CG2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(&tempty[acc], 0));  // the issuing CTA's
+          else ptx::mbar_arrive(&tempty[acc]);
+        }
       };
 #pragma unroll 1
       for (int i = 0; i < nch; ++i) {
@@ -453,7 +508,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 512);
+    if constexpr (S::CG2) ptx::tmem_dealloc_cg2(tmem, 512);
+    else ptx::tmem_dealloc(tmem, 512);
   }
 }
 

@@ -1,5 +1,6 @@
-"""GPU: the tcgen05/TMEM/TMA GEMM core (single CTA and B-multicast CTA pairs, bn < 0) against a plain fp32 reference of the
-same op (bf16-rounded operands, fp64 accumulation on the host)."""
+"""GPU: the tcgen05/TMEM/TMA GEMM core (single CTA, B-multicast CTA pairs bn < 0, and pair UMMA with
+cta_group::2, bn = -2208) against a plain fp32 reference of the same op (bf16-rounded operands, fp64
+accumulation on the host)."""
 import ctypes as C
 
 import numpy as np
@@ -26,7 +27,9 @@ def _call(name, *args):
 
 @pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (256, 512, 768, 256), (200, 300, 320, 208),
                                       (384, 320, 448, 160), (1000, 700, 1024, 256),
-                                      (640, 416, 768, -208), (384, 320, 448, -160), (130, 500, 128, -208)])
+                                      (640, 416, 768, -208), (384, 320, 448, -160), (130, 500, 128, -208),
+                                      (640, 416, 768, -2208), (256, 208, 64, -2208), (130, 500, 128, -2208),
+                                      (1000, 700, 1024, -2208)])
 def test_dense(M, N, K, bn):
     rng = np.random.default_rng(M + N + K)
     A, Af = bf16(rng.standard_normal((M, K)))
