@@ -31,6 +31,10 @@ constexpr int kG7BN = 224;  // G7 N tile: PQ = 448 = 2 x 224 (ViT-B/L)
 #define D2FT_CG2 1  // pair UMMA (cta_group::2) for the K-major-B GEMMs; 0 = B multicast (experiment builds)
 #endif
 constexpr int kCG2 = D2FT_CG2;
+#ifndef D2FT_CG2_BMN
+#define D2FT_CG2_BMN 1  // pair UMMA also for the MN-major-B GEMMs (G3, G8)
+#endif
+constexpr int kCG2Bmn = D2FT_CG2_BMN;
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
@@ -500,7 +504,7 @@ struct Engine {
     // pipeline); MN-major B: B multicast to both CTAs of the pair.  G1 keeps
     // multicast: its epilogue is the limiter and the pair UMMA couples the two
     // CTAs' epilogues through one accumulator release (0.91 vs 0.95 ms).
-    constexpr int CG = (BMN || !PAIR_UMMA) ? 0 : kCG2;
+    constexpr int CG = !PAIR_UMMA ? 0 : (BMN ? kCG2Bmn : kCG2);
     switch (BNt) {
       case 64:
         launch_gemm<Prob<64>, GemmShape<64, 8, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<64>{args...}, 0, st);
@@ -509,7 +513,7 @@ struct Engine {
         launch_gemm<Prob<128>, GemmShape<128, CG ? 8 : 6, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
-        // 4 stages when the B blocks are MN-major or the epilogue stages bulk stores (multicast B)
+        // multicast B: 4 stages when the B blocks are MN-major or the epilogue stages bulk stores
         launch_gemm<Prob<208>, GemmShape<208, CG ? 6 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? 4 : 5), 0, EPI, 2,
                                          BMN, AMN, CG>>(a, b, Prob<208>{args...}, 0, st);
         break;

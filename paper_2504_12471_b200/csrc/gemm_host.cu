@@ -309,7 +309,10 @@ int d2ft_test_gemm_mn(const uint16_t* A, const uint16_t* BT, int M, int N, int K
     D2FT_CUDA(cudaMemset(dD.p, 0, (size_t)M * N * 4));
     CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
     CUtensorMap b = make_tmap_bf16_3d(dB.p, N, K, 1, (uint64_t)N * 2, (uint64_t)K * N * 2, 64);
-    if (bn == -208) {
+    if (bn == -2208) {  // pair UMMA, MN-major B split across the pair
+      launch_gemm<DenseMNProb<208>, GemmShape<208, 6, 1, 4, 2, 1, 0, 1>>(a, b, DenseMNProb<208>{M, N, K, 1, dD.p}, 0,
+                                                                          nullptr);
+    } else if (bn == -208) {
       launch_gemm<DenseMNProb<208>, GemmShape<208, 4, 1, 4, 2, 1>>(a, b, DenseMNProb<208>{M, N, K, 1, dD.p}, 0,
                                                                     nullptr);
     } else if (bn == 64) {

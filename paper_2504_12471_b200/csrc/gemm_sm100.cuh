@@ -151,8 +151,9 @@ template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, in
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
   static constexpr int BMN = BMN_, AMN = AMN_, CG2 = CG2_;
-  static_assert(!CG2 || (CLUSTER == 2 && !BMN), "pair UMMA needs a CTA pair and a K-major B");
-  static constexpr int NBLK = (BN + 63) / 64;  // MN-major B: 64-wide N blocks
+  static_assert(!CG2 || CLUSTER == 2, "pair UMMA needs a CTA pair");
+  // MN-major B: 64-wide N blocks held per CTA (pair UMMA: of this CTA's N/2)
+  static constexpr int NBLK = CG2 ? (BN / 2 + 63) / 64 : (BN + 63) / 64;
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int A_BYTES = BM * BK * 2;
   // B bytes held per CTA and stage (CG2: this CTA's N/2 rows)
@@ -330,7 +331,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
               ptx::tma_load_3d_cg2(a, &tmA, fb, k.ax, k.ay0, k.az);
               ptx::tma_load_3d_cg2(a + S::A_BYTES / 2, &tmA, fb, k.ax, k.ay1, k.az);
             }
-            ptx::tma_load_3d_cg2(sB + stage * S::B_BYTES, &tmB, fb, k.bx, k.by + rank * (S::BN / 2), k.bz);
+            if constexpr (S::BMN) {  // this CTA's N/2 tokens from k.bx + rank * BN/2, 64 per box
+              for (int j2 = 0; j2 < S::NBLK; ++j2)
+                ptx::tma_load_3d_cg2(sB + stage * S::B_BYTES + j2 * (64 * S::BK * 2), &tmB, fb,
+                                     k.bx + rank * (S::BN / 2) + 64 * j2, k.by, k.bz);
+            } else {
+              ptx::tma_load_3d_cg2(sB + stage * S::B_BYTES, &tmB, fb, k.bx, k.by + rank * (S::BN / 2), k.bz);
+            }
             ptx::mbar_arrive(&kq_empty[j]);
             if (++stage == S::STAGES) {
               stage = 0;

@@ -44,7 +44,8 @@ def test_dense(M, N, K, bn):
 
 @pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 208, 448, 208), (384, 416, 320, 208),
                                       (200, 200, 768, 208), (512, 624, 320, -208), (384, 128, 192, -64),
-                                      (130, 96, 128, 64)])
+                                      (130, 96, 128, 64), (512, 624, 320, -2208), (256, 208, 768, -2208),
+                                      (130, 200, 128, -2208)])
 def test_mn_major_b(M, N, K, bn):
     """B stored [K][N] (N contiguous) and read by UMMA as an MN-major operand."""
     rng = np.random.default_rng(M * 3 + N + K)
