@@ -326,8 +326,11 @@ struct Engine {
     dX = dalloc<float>(Bm * T * d, owned);
     dxn = dalloc<float>(Bm * T * d, owned);
     const size_t ntile = (T + 31) / 32;
-    part_cs = dalloc<float>(Bm * ntile * d, owned);
-    part_db1 = dalloc<float>((size_t)kEpiGroups * Bm * H * fs, owned);
+    // per-slot partial sums, reduced for all blocks in one launch after the
+    // backward loop: part_cs slot l = column sums of the gradient entering
+    // block l (slot L: entering the embedding), part_db1 slot l = G4 partials
+    part_cs = dalloc<float>((L + 1) * Bm * ntile * d, owned);
+    part_db1 = dalloc<float>(L * (size_t)kEpiGroups * Bm * H * fs, owned);
     part_ew = dalloc<float>((size_t)KS * d * d, owned);
     dC = dalloc<act_t>(Bm * T * d, owned);
     dO = dalloc<act_t>(Bm * H * T * D.dh, owned);
@@ -565,7 +568,7 @@ struct Engine {
                 dlog, dX, gmax, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
-    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, part_cs, gmax, st);
+    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1), gmax, st);
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
@@ -573,7 +576,7 @@ struct Engine {
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
-                          (const act_t*)ZTl, part_db1, (const float*)gmax, (const CUtensorMap*)store_maps);
+                          (const act_t*)ZTl, db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps);
       mark(PH_ATTN_B);
       if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
         launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, O32T + (size_t)l * Bm * H * 64 * D.TP,
@@ -600,17 +603,19 @@ struct Engine {
         mark(PH_EXCH);
         ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
       }
-      mark(PH_BIAS);
-      launch_bias_reduce(D, l, codes_exp, part_cs, part_db1, G + seg[S_B1].off + (size_t)l * H * D.fs,
-                         G + seg[S_B2].off + (size_t)l * d, st);
       mark(PH_LN_BWD);
-      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2, dxn, dX, dC, part_cs,
-                         gmax, st);
+      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2,
+                         dxn, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
     mark(PH_EMBED_W);
     launch_gemm<EmbedW<256>, GemmShape<256, kCG2 ? 6 : 4, 0, 4, 2, 0, 1, kCG2>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
-    launch_embed_reduce(D, KS, part_ew, part_cs, dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
+    launch_embed_reduce(D, KS, part_ew, cs_slot(L), dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
+    mark(PH_BIAS);
+    launch_bias_reduce(D, codes_exp, part_cs, part_db1, G + seg[S_B1].off, G + seg[S_B2].off, st);
   }
+
+  float* cs_slot(int k) { return part_cs + (size_t)k * D.Bmax * ((D.T + 31) / 32) * D.d; }
+  float* db1_slot(int l) { return part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs; }
 
   void run_sgd(float lr, float mom) {
     mark(PH_SGD);

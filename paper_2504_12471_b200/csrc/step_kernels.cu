@@ -365,14 +365,21 @@ __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* po
 // 32 outputs per CTA, 32 warps striding over the samples (fixed order: warp
 // partials then lanes' sum over warps), so the per-layer reduction runs at
 // full memory parallelism despite only (d + H*fs)/32 CTAs.
-__global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const uint8_t* codes, const float* part_cs,
-                                                           const float* part_db1, float* db1_l, float* db2_l) {
+// db2 / db1 of every block in one launch (blockIdx.y = block): fixed-order
+// sums over the Full samples of each head of the per-tile column sums of the
+// incoming gradient (model.cpp:250-252) and of G4's per-column-group db1
+// partials (model.cpp:257).
+__global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, const uint8_t* codes, const float* part_cs,
+                                                           const float* part_db1, float* db1, float* db2) {
   D2FT_PDL_ENTRY();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int l = blockIdx.y;
   const int i = blockIdx.x * 32 + lane;
   const int ntile = (D.T + 31) / 32;
   const int nout = D.d + D.H * D.fs;
+  const float* pcs = part_cs + (size_t)l * D.Bmax * ntile * D.d;
+  const float* pdb = part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs;
   float a = 0.f;
   if (i < nout) {
     if (i < D.d) {
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const 
       for (int s = warp; s < D.B; s += 32)
         if (row[s] == 1) {
 #pragma unroll 4
-          for (int tt = 0; tt < ntile; ++tt) a += part_cs[((size_t)s * ntile + tt) * D.d + m];
+          for (int tt = 0; tt < ntile; ++tt) a += pcs[((size_t)s * ntile + tt) * D.d + m];
         }
     } else {
       const int q = i - D.d, h = q / D.fs, j = q % D.fs;
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const 
       for (int s = warp; s < D.B; s += 32)
         if (row[s] == 1)
 #pragma unroll
-          for (int e = 0; e < kEpiGroups; ++e) a += part_db1[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
+          for (int e = 0; e < kEpiGroups; ++e) a += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
     }
   }
   red[warp][lane] = a;
@@ -397,8 +404,8 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, int l, const 
   if (warp == 0 && i < nout) {
     float t = 0.f;
     for (int w = 0; w < 32; ++w) t += red[w][lane];
-    if (i < D.d) db2_l[i] = t;
-    else db1_l[i - D.d] = t;
+    if (i < D.d) db2[(size_t)l * D.d + i] = t;
+    else db1[(size_t)l * D.H * D.fs + (i - D.d)] = t;
   }
 }
 
@@ -980,10 +987,10 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
-                        float* db1_l, float* db2_l, cudaStream_t st) {
+void launch_bias_reduce(const Dims& D, const uint8_t* codes, const float* part_cs, const float* part_db1, float* db1,
+                        float* db2, cudaStream_t st) {
   const int n = D.d + D.H * D.fs;
-  bias_reduce_kernel<<<(n + 31) / 32, 1024, 0, st>>>(D, l, codes, part_cs, part_db1, db1_l, db2_l);
+  bias_reduce_kernel<<<dim3((n + 31) / 32, D.L), 1024, 0, st>>>(D, codes, part_cs, part_db1, db1, db2);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

@@ -54,8 +54,8 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
                         const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax,
                         cudaStream_t st);
-void launch_bias_reduce(const Dims& D, int l, const uint8_t* codes, const float* part_cs, const float* part_db1,
-                        float* db1_l, float* db2_l, cudaStream_t st);
+void launch_bias_reduce(const Dims& D, const uint8_t* codes, const float* part_cs, const float* part_db1, float* db1,
+                        float* db2, cudaStream_t st);
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
                          float* dbe, float* dpos, cudaStream_t st);
 // SGD with momentum (trainer.cpp:113-134) on one tensor; elements whose
