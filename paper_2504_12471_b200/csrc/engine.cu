@@ -568,7 +568,8 @@ struct Engine {
                 dlog, dX, gmax, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
-    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1), gmax, st);
+    launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
+                       gmax, st);
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
@@ -597,15 +598,20 @@ struct Engine {
                     ord_head + l * H, ctr(l, C_G7)},
           0, st);
       mark(PH_G8);
-      gemm_tokN<G8, 1, 1>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, (const float*)gmax,
-                       ord_full + l * Bm, ctr(l, C_G8));
+      // single engine: dxn leaves G8 as fp16 in gradient-scale units (half the
+      // bytes of G8's stores and the LN backward's reads); partitioned: fp32
+      // for the cross-rank sum
+      act_t* dxn_h = partitioned() ? nullptr : reinterpret_cast<act_t*>(dxn);
+      gemm_tokN<G8, 1, 1>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, dxn_h, (const float*)gmax,
+                          ord_full + l * Bm, ctr(l, C_G8));
       if (partitioned()) {
         mark(PH_EXCH);
         ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
       }
       mark(PH_LN_BWD);
-      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs, stats + (size_t)l * Bm * T * 2,
-                         dxn, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
+      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
+                         partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
+                         partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
     mark(PH_EMBED_W);
     launch_gemm<EmbedW<256>, GemmShape<256, kCG2 ? 6 : 4, 0, 4, 2, 0, 1, kCG2>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);

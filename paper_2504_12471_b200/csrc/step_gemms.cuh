@@ -519,7 +519,8 @@ struct G8 {
   int l;
   const int* full_heads;
   const int* full_hcnt;
-  float* dxn;  // [Bmax][T][d]
+  float* dxn;     // [Bmax][T][d] fp32 (head partition: the exchange sums it), or
+  act_t* dxn_h;   // [Bmax][T][d] fp16 in gradient-scale units (single engine; LN backward undoes S)
   const float* gmax;
   const int* order;  // block l: samples by decreasing Full-head count
   int* ctr;
@@ -552,7 +553,10 @@ struct G8 {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int t = col0 + i;
-      if (t < D.T) dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i] * r.inv;
+      if (t < D.T) {
+        if (dxn_h) dxn_h[((size_t)c.s * D.T + t) * D.d + m] = to_act(v[i]);
+        else dxn[((size_t)c.s * D.T + t) * D.d + m] = v[i] * r.inv;
+      }
     }
   }
   __device__ void row_end(const Tile&, int, int, Row&) const {}

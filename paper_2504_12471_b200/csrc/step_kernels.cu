@@ -165,8 +165,9 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
 }
 
 template <int NV>
-__global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                                   const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax) {
+__global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
+                                   const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
+                                   float* part_cs, const float* gmax) {
   D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   float* cs = reinterpret_cast<float*>(smem);  // [8][d]
@@ -189,11 +190,13 @@ __global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const fl
       const float mean = stats_l[((size_t)s * D.T + t) * 2], rstd = stats_l[((size_t)s * D.T + t) * 2 + 1];
       float y[NV], dy[NV];
       float s1 = 0.f, s2 = 0.f;
+      const float iS = 1.f / grad_scale(gmax);
 #pragma unroll
       for (int j = 0; j < NV; ++j)
         if (j < nv) {
-          y[j] = (x_l[ro + lane + 32 * j] - mean) * rstd;
-          dy[j] = dxn[ro + lane + 32 * j];
+          // fp16 inputs (single engine): y = the stored LN output, dxn in S units
+          y[j] = xn_l ? act_to_f(xn_l[ro + lane + 32 * j]) : (x_l[ro + lane + 32 * j] - mean) * rstd;
+          dy[j] = dxn_h ? act_to_f(dxn_h[ro + lane + 32 * j]) * iS : dxn[ro + lane + 32 * j];
           s1 += dy[j];
           s2 += dy[j] * y[j];
         }
@@ -911,14 +914,15 @@ void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaS
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax,
-                        cudaStream_t st) {
+void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
+                        const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
+                        float* part_cs, const float* gmax, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
   const size_t sm = (size_t)8 * D.d * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, stats_l, dxn, dX, dC, part_cs, gmax);
+    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, xn_l, stats_l, dxn, dxn_h, dX, dC, part_cs,
+                                                  gmax);
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());

@@ -51,9 +51,10 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
                         float* dbc, double* loss, cudaStream_t st);
 // dX += LN_bwd(x_l, dxn) for samples with a Full head in block l (if l >= 0), then
 // emit dC (act_t token-major) and per-tile column sums.
-void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const float* stats_l,
-                        const float* dxn, float* dX, act_t* dC, float* part_cs, const float* gmax,
-                        cudaStream_t st);
+// x_l (fp32) or xn_l (the stored fp16 LN output) for y; dxn (fp32) or dxn_h (fp16, gradient-scale units)
+void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
+                        const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
+                        float* part_cs, const float* gmax, cudaStream_t st);
 void launch_bias_reduce(const Dims& D, const uint8_t* codes, const float* part_cs, const float* part_db1, float* db1,
                         float* db2, cudaStream_t st);
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,
