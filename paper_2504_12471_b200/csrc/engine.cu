@@ -109,6 +109,14 @@ struct Engine {
   // into samples_stage while the current batch computes (d2ft_engine_prefetch)
   float* samples_stage = nullptr;
   cudaStream_t cst = nullptr;
+  // side stream: G5 (dW of [Wo;W2]) only needs the incoming gradient dC and
+  // the forward's [O|g], so it runs beside G4 / attention backward / G7 / G8
+  // and joins before the LN backward overwrites dC
+  cudaStream_t st2 = nullptr;
+  std::vector<cudaEvent_t> side_ev;  // [2L]: fork, join per block
+  // opt-in (D2FT_SIDE=1): measured 5.716 vs 5.733 ms per step — the
+  // persistent G5 CTAs that start in a tail hold their SMs until done
+  bool use_side = getenv("D2FT_SIDE") != nullptr;
   cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
   bool have_prefetch = false;
   int prefetch_B = 0;
@@ -259,7 +267,14 @@ struct Engine {
     Kmax_mb = Bmax;
     BNt = D.T <= 64 ? 64 : D.T <= 128 ? 128 : D.T <= 208 ? 208 : 256;
     KS = std::min(8, Bmax);
-    D2FT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {
+      int least = 0, greatest = 0;
+      D2FT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      // the step's critical path runs at the highest priority; the off-path
+      // weight-gradient GEMMs (side stream) fill the SMs it leaves idle
+      D2FT_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest));
+      D2FT_CUDA(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, least));
+    }
     D2FT_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
     D2FT_CUDA(cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming));
     D2FT_CUDA(cudaEventCreateWithFlags(&ev_stage_free, cudaEventDisableTiming));
@@ -282,6 +297,8 @@ struct Engine {
     if (ev_copied) cudaEventDestroy(ev_copied);
     if (ev_stage_free) cudaEventDestroy(ev_stage_free);
     if (cst) cudaStreamDestroy(cst);
+    for (auto e : side_ev) cudaEventDestroy(e);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -570,10 +587,23 @@ struct Engine {
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
+    const bool side = use_side && !profiling && !partitioned();
+    auto g5 = [&](int l, cudaStream_t s5) {
+      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
+          tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
+                  ord_head + l * H, ctr(l, C_G5)},
+          0, s5);
+    };
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
+      if (side) {
+        D2FT_CUDA(cudaEventRecord(side_event(2 * l), st));
+        D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(2 * l), 0));
+        g5(l, st2);
+        D2FT_CUDA(cudaEventRecord(side_event(2 * l + 1), st2));
+      }
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
@@ -587,10 +617,7 @@ struct Engine {
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
       mark(PH_G5);
-      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
-          tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
-                  ord_head + l * H, ctr(l, C_G5)},
-          0, st);
+      if (!side) g5(l, st);
       mark(PH_G7);
       launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
           tm_xn64, tm_dY1Tb,
@@ -608,6 +635,7 @@ struct Engine {
         mark(PH_EXCH);
         ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
       }
+      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(2 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
@@ -620,6 +648,13 @@ struct Engine {
     launch_bias_reduce(D, codes_exp, part_cs, part_db1, G + seg[S_B1].off, G + seg[S_B2].off, st);
   }
 
+  cudaEvent_t side_event(int i) {
+    if (side_ev.empty()) {
+      side_ev.resize(2 * D.L);
+      for (auto& e : side_ev) D2FT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return side_ev[i];
+  }
   float* cs_slot(int k) { return part_cs + (size_t)k * D.Bmax * ((D.T + 31) / 32) * D.d; }
   float* db1_slot(int l) { return part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs; }
 
