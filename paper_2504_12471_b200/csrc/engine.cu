@@ -435,12 +435,13 @@ struct Engine {
     {  // G1 epilogue bulk stores: 32 tokens x 32 feature rows (feature-major) or
        // 32 features x 32 tokens (token-major QKV), clipped at T
       CUtensorMap sm[5];
-      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, 32, 32, true);
-      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, 32, 32, true);
-      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, 32);
+      constexpr int cw = G1<208>::kChunk;
+      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, cw, 32, cw * 2);
+      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, cw, 32, cw * 2);
+      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, cw);
       // G4 epilogue: dO (token-major) and the dz rows of dY1T (feature-major)
       sm[3] = make_tmap_store_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, 32, 32);
-      sm[4] = make_tmap_store_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 32, 32, true);
+      sm[4] = make_tmap_store_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 32, 32, 64);
       D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)

@@ -535,10 +535,10 @@ inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, 
   return make_tmap_16_3d(base, d0, d1, d2, s1, s2, box_rows, false);
 }
 // fp16 map for bulk tensor STORES: box = box0 x box1 x 1; the staging tile is
-// row-major [box1][box0], plain or 64-byte swizzled (box0 * 2 == 64 bytes);
-// writes past d0/d1 are clipped.
+// row-major [box1][box0], plain or swizzled with swizzle_bytes == box0 * 2
+// (32 or 64); writes past d0/d1 are clipped.
 CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-                                   uint32_t box0, uint32_t box1, bool swizzle64 = false);
+                                   uint32_t box0, uint32_t box1, int swizzle_bytes = 0);
 
 int num_sms();
 

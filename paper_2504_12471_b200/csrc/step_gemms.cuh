@@ -73,6 +73,12 @@ struct EmbedFwd {
 // are staged and written by one TMA store per destination.  Per-lane global
 // stores (32 rows per instruction) made the LSU the limiter of this epilogue;
 // the GELU pair runs on packed fp32 (gelu_and_grad2).
+#ifndef D2FT_G1_CW
+#define D2FT_G1_CW 32  // tokens per epilogue chunk (16 or 32)
+#endif
+#ifndef D2FT_G1_BUFS
+#define D2FT_G1_BUFS 1  // staging buffers per epilogue warp
+#endif
 template <int BN>
 struct G1 {
   Dims D;
@@ -83,17 +89,19 @@ struct G1 {
   const int* act_cnt;
   const uint8_t* codes;  // expanded K x Bmax (code 1 = Full)
   const float* b1;  // block l: [H][fs]
-  const CUtensorMap* maps;  // bulk-store maps: [0] ZT, [1] OGT (32 tokens x 32 rows, 64B swizzle), [2] QKV (32 x 32)
-  static constexpr int kChunk = 32;
+  // bulk-store maps: [0] ZT, [1] OGT (CW tokens x 32 rows, CW*2-byte swizzle), [2] QKV (32 features x CW tokens)
+  const CUtensorMap* maps;
+  static constexpr int kChunk = D2FT_G1_CW;
+  static constexpr int kNC = kChunk / 8;  // 16-byte chunks per staged row
   static constexpr bool kNonEmpty = true;
-  // g tile [32 rows][32 tokens] at +0, GELU' tile at +2048 (64B-swizzled);
-  // or the QKV tile [32 tokens][32 features] at +0
-  static constexpr int kEpiStageBytes = 4096;
+  static constexpr int kBufs = D2FT_G1_BUFS;
+  static constexpr int kBufBytes = 2 * 32 * kChunk * 2;  // g tile + GELU' tile (or the QKV tile)
+  static constexpr int kEpiStageBytes = kBufs * kBufBytes;
   struct Tile {
     int nkb, s, u0, nu, r0, r1;  // r0/r1: weight rows of the two 64-row units (fixed per tile)
   };
   struct Row {
-    int valid, h, f, full;
+    int valid, h, f, full, buf;
     float bias;
     uint8_t* stage;  // this warp's staging (kEpiStageBytes)
   };
@@ -115,6 +123,10 @@ struct G1 {
     return KCoord{kb * 64, c.r0, c.r1, l, kb * 64, 0, l * D.Bmax + c.s};
   }
   __device__ void row_begin(const Tile& c, int row, Row& r) const {
+    if (kBufs > 1) {  // buffer parity restarts: the previous tile's stores must have read both buffers
+      if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read<0>();
+      r.buf = 0;
+    }
     const int u = c.u0 + (row >> 6);
     r.valid = u < c.nu;
     if (!r.valid) return;
@@ -124,65 +136,69 @@ struct G1 {
     r.full = codes[(size_t)(l * D.H + r.h) * D.Bmax + c.s] == 1;
     r.bias = (r.valid && r.f >= 3 * D.dh) ? b1[r.h * D.fs + (r.f - 3 * D.dh)] : 0.f;
   }
-  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[32], Row& r) const {
+  __device__ void chunk(const Tile& c, int, int col0, const float (&v)[kChunk], Row& r) const {
     if (!r.valid || col0 >= D.T) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
-    // the staging is single-buffered: the previous chunk's bulk stores must
-    // have read it; that wait comes after this chunk's math, which hides it
+    // the store that last used this buffer must have read it; the wait comes
+    // after this chunk's math, which hides it
     auto staging_free = [&]() {
-      if (lane == 0) ptx::bulk_wait_read<0>();
+      if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
       __syncwarp();
     };
-    const uint32_t sb = ptx::smem_u32(r.stage);
+    const int buf = kBufs > 1 ? r.buf : 0;
+    uint8_t* stp = r.stage + buf * kBufBytes;
+    const uint32_t sb = ptx::smem_u32(stp);
     const int plane = (l * D.Bmax + c.s) * D.H + r.h;
     const int f0 = r.f - lane;  // the warp's first feature row
-    if (r.f < 3 * D.dh) {  // q, k, v: staged [32 tokens][32 features]
-      uint32_t hv[16];
+    if (kBufs > 1) r.buf ^= 1;
+    if (r.f < 3 * D.dh) {  // q, k, v: staged [kChunk tokens][32 features]
+      uint32_t hv[kChunk / 2];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < kChunk / 2; ++i) {
         const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
         hv[i] = *reinterpret_cast<const uint32_t*>(&h);
       }
       staging_free();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < kChunk / 2; ++i) {
         ptx::st_shared_u16(sb + (2 * i) * 64 + lane * 2, (unsigned short)(hv[i] & 0xffffu));
         ptx::st_shared_u16(sb + (2 * i + 1) * 64 + lane * 2, (unsigned short)(hv[i] >> 16));
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::tma_store_3d(maps + 2, r.stage, f0, col0, plane);
+        ptx::tma_store_3d(maps + 2, stp, f0, col0, plane);
         ptx::bulk_commit();
       }
       return;
     }
     const int j0 = f0 - 3 * D.dh;
-    uint32_t hg[16], hz[16];  // half2 pairs of g = GELU(z) and GELU'(z), tokens 2i, 2i+1
+    uint32_t hg[kChunk / 2], hz[kChunk / 2];  // half2 pairs of g = GELU(z) and GELU'(z), tokens 2i, 2i+1
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < kChunk / 2; ++i) {
       float g0, g1, d0, d1;
       gelu_and_grad2(v[2 * i] + r.bias, v[2 * i + 1] + r.bias, g0, g1, d0, d1);
       const __half2 a = __floats2half2_rn(g0, g1), b = __floats2half2_rn(d0, d1);
       hg[i] = *reinterpret_cast<const uint32_t*>(&a);
       hz[i] = *reinterpret_cast<const uint32_t*>(&b);
     }
-    // row `lane` of a [32][32] fp16 tile is 64 B = four 16-byte chunks; the
-    // 64-byte swizzle (chunk ^ (row >> 1) & 3) keeps the 8 lanes of each
-    // store phase on distinct banks
-    const uint32_t rb = sb + lane * 64, sw = (lane >> 1) & 3;
+    // row `lane` of a [32][kChunk] fp16 tile is kNC 16-byte chunks; the
+    // (kChunk*2)-byte swizzle keeps the 8 lanes of each store phase on
+    // distinct banks
+    const uint32_t rb = sb + lane * (kChunk * 2), sw = ((lane * kNC) >> 3) & (kNC - 1);
     staging_free();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kNC; ++q) {
       const uint32_t o = ((q ^ sw) << 4);
       ptx::st_shared_v4(rb + o, hg[4 * q], hg[4 * q + 1], hg[4 * q + 2], hg[4 * q + 3]);
-      if (r.full) ptx::st_shared_v4(rb + 2048 + o, hz[4 * q], hz[4 * q + 1], hz[4 * q + 2], hz[4 * q + 3]);
+      if (r.full)
+        ptx::st_shared_v4(rb + kBufBytes / 2 + o, hz[4 * q], hz[4 * q + 1], hz[4 * q + 2], hz[4 * q + 3]);
     }
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      ptx::tma_store_3d(maps + 1, r.stage, col0, D.dh + j0, plane);
-      if (r.full) ptx::tma_store_3d(maps + 0, r.stage + 2048, col0, j0, plane);
+      ptx::tma_store_3d(maps + 1, stp, col0, D.dh + j0, plane);
+      if (r.full) ptx::tma_store_3d(maps + 0, stp + kBufBytes / 2, col0, j0, plane);
       ptx::bulk_commit();
     }
   }
