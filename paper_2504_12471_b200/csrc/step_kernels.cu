@@ -125,38 +125,56 @@ __global__ void prep_input_kernel(Dims D, const float* x, act_t* inp, act_t* inp
   write_transposed(tile, pitch, D.d, t0, D.TP, inpT + (size_t)s * D.d * D.TP);
 }
 
+// Vectorised row access: lane handles elements 4*lane + 128*q + e (q < NV/4,
+// e < 4): 16-byte fp32 / 8-byte fp16 accesses, 512 contiguous bytes per warp
+// instruction.
+__device__ __forceinline__ void ld4(const float* p, float* v) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+}
+__device__ __forceinline__ void ld4h(const act_t* p, float* v) {
+  const uint2 t = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&t.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&t.y));
+  v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+}
+__device__ __forceinline__ void st4h(act_t* p, float a, float b, float c, float d) {
+  const __half2 x = __floats2half2_rn(a, b), y = __floats2half2_rn(c, d);
+  uint2 t;
+  t.x = *reinterpret_cast<const uint32_t*>(&x);
+  t.y = *reinterpret_cast<const uint32_t*>(&y);
+  *reinterpret_cast<uint2*>(p) = t;
+}
+
 template <int NV>
-__global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
+__global__ void __launch_bounds__(512) ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
   D2FT_PDL_ENTRY();
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int nv = NV;
-  for (int r = warp; r < 32; r += 8) {
+  constexpr int NQ = NV / 4;
+  for (int r = warp; r < 32; r += blockDim.x >> 5) {
     const int t = t0 + r;
     if (t >= D.T) continue;
-    const float* row = x + ((size_t)s * D.T + t) * D.d;
+    const size_t ro = ((size_t)s * D.T + t) * D.d + 4 * lane;
     float v[NV];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) ld4(x + ro + 128 * q, v + 4 * q);
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (j < nv) {
-        v[j] = row[lane + 32 * j];
-        sum += v[j];
-      }
+    for (int j = 0; j < NV; ++j) sum += v[j];
     const float mean = warp_sum(sum) / D.d;  // linalg.cpp:136-139, two-pass
     float sq = 0.f;
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (j < nv) {
-        const float dv = v[j] - mean;
-        sq += dv * dv;
-      }
+    for (int j = 0; j < NV; ++j) {
+      const float dv = v[j] - mean;
+      sq += dv * dv;
+    }
     const float var = warp_sum(sq) / D.d;
     const float rstd = 1.0f / sqrtf(var + kLnEps);
-    act_t* out = xn + ((size_t)s * D.T + t) * D.d;
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (j < nv) out[lane + 32 * j] = to_act((v[j] - mean) * rstd);
+    for (int q = 0; q < NQ; ++q)
+      st4h(xn + ro + 128 * q, (v[4 * q] - mean) * rstd, (v[4 * q + 1] - mean) * rstd, (v[4 * q + 2] - mean) * rstd,
+           (v[4 * q + 3] - mean) * rstd);
     if (lane == 0) {
       stats[((size_t)s * D.T + t) * 2] = mean;
       stats[((size_t)s * D.T + t) * 2 + 1] = rstd;
@@ -164,66 +182,79 @@ __global__ void ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
   }
 }
 
+constexpr int kLnbWarps = 16;  // LN backward: 32 tokens per CTA, 2 rows per warp
 template <int NV>
-__global__ void ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
+__global__ void __launch_bounds__(32 * kLnbWarps) ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
                                    const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
                                    float* part_cs, const float* gmax) {
   D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
-  float* cs = reinterpret_cast<float*>(smem);  // [8][d]
+  float* cs = reinterpret_cast<float*>(smem);  // [kLnbWarps][d] per-warp column sums
   const int s = blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int nv = NV;
+  constexpr int NQ = NV / 4;
   const bool do_ln = l >= 0 && full_hcnt[s * D.L + l] > 0;  // model.cpp:508
-  float acc[NV];
+  const float S = grad_scale(gmax);  // fp16 gradient operands carry S
+  const float iS = 1.f / S;
+  float* csw = cs + warp * D.d + 4 * lane;
 #pragma unroll
-  for (int j = 0; j < NV; ++j) acc[j] = 0.f;
-  for (int r = warp; r < 32; r += 8) {
+  for (int q = 0; q < NQ; ++q) *reinterpret_cast<float4*>(csw + 128 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = warp; r < 32; r += kLnbWarps) {
     const int t = t0 + r;
     if (t >= D.T) continue;
-    const size_t ro = ((size_t)s * D.T + t) * D.d;
+    const size_t ro = ((size_t)s * D.T + t) * D.d + 4 * lane;
     float v[NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (j < nv) v[j] = dX[ro + lane + 32 * j];
+    for (int q = 0; q < NQ; ++q) ld4(dX + ro + 128 * q, v + 4 * q);
     if (do_ln) {  // linalg.cpp:153-180
       const float mean = stats_l[((size_t)s * D.T + t) * 2], rstd = stats_l[((size_t)s * D.T + t) * 2 + 1];
       float y[NV], dy[NV];
-      float s1 = 0.f, s2 = 0.f;
-      const float iS = 1.f / grad_scale(gmax);
+      // fp16 inputs (single engine): y = the stored LN output, dxn in S units
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (j < nv) {
-          // fp16 inputs (single engine): y = the stored LN output, dxn in S units
-          y[j] = xn_l ? act_to_f(xn_l[ro + lane + 32 * j]) : (x_l[ro + lane + 32 * j] - mean) * rstd;
-          dy[j] = dxn_h ? act_to_f(dxn_h[ro + lane + 32 * j]) * iS : dxn[ro + lane + 32 * j];
-          s1 += dy[j];
-          s2 += dy[j] * y[j];
+      for (int q = 0; q < NQ; ++q) {
+        if (xn_l) {
+          ld4h(xn_l + ro + 128 * q, y + 4 * q);
+        } else {
+          ld4(x_l + ro + 128 * q, y + 4 * q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) y[4 * q + e] = (y[4 * q + e] - mean) * rstd;
         }
+        if (dxn_h) {
+          ld4h(dxn_h + ro + 128 * q, dy + 4 * q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dy[4 * q + e] *= iS;
+        } else {
+          ld4(dxn + ro + 128 * q, dy + 4 * q);
+        }
+      }
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        s1 += dy[j];
+        s2 += dy[j] * y[j];
+      }
       const float dmean = warp_sum(s1) / D.d, ddot = warp_sum(s2) / D.d;
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (j < nv) v[j] += (dy[j] - dmean - y[j] * ddot) * rstd;
+      for (int j = 0; j < NV; ++j) v[j] += (dy[j] - dmean - y[j] * ddot) * rstd;
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (j < nv) dX[ro + lane + 32 * j] = v[j];
+      for (int q = 0; q < NQ; ++q)
+        *reinterpret_cast<float4*>(dX + ro + 128 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
-    const float S = grad_scale(gmax);  // fp16 gradient operands carry S
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (j < nv) {
-        dC[ro + lane + 32 * j] = to_act(v[j] * S);
-        acc[j] += v[j];
-      }
+    for (int q = 0; q < NQ; ++q)
+      st4h(dC + ro + 128 * q, v[4 * q] * S, v[4 * q + 1] * S, v[4 * q + 2] * S, v[4 * q + 3] * S);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float4 c = *reinterpret_cast<float4*>(csw + 128 * q);
+      c.x += v[4 * q], c.y += v[4 * q + 1], c.z += v[4 * q + 2], c.w += v[4 * q + 3];
+      *reinterpret_cast<float4*>(csw + 128 * q) = c;
+    }
   }
-#pragma unroll
-  for (int j = 0; j < NV; ++j)
-    if (j < nv) cs[warp * D.d + lane + 32 * j] = acc[j];
   __syncthreads();
   const int ntile = (D.T + 31) / 32;
   for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
     float c = 0.f;
-    for (int w = 0; w < 8; ++w) c += cs[w * D.d + m];
+    for (int w = 0; w < kLnbWarps; ++w) c += cs[w * D.d + m];
     part_cs[((size_t)s * ntile + blockIdx.x) * D.d + m] = c;
   }
 }
@@ -909,7 +940,7 @@ void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, c
 
 void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
-  D2FT_NV_DISPATCH(D.d, { ln_fwd_kernel<NV><<<grid, 256, 0, st>>>(D, x, xn, stats); });
+  D2FT_NV_DISPATCH(D.d, { ln_fwd_kernel<NV><<<grid, 512, 0, st>>>(D, x, xn, stats); });  // 2 rows per warp
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -918,11 +949,11 @@ void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float*
                         const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
                         float* part_cs, const float* gmax, cudaStream_t st) {
   dim3 grid((D.T + 31) / 32, D.B);
-  const size_t sm = (size_t)8 * D.d * 4;
+  const size_t sm = (size_t)kLnbWarps * D.d * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ln_bwd_prep_kernel<NV><<<grid, 256, sm, st>>>(D, l, full_hcnt, x_l, xn_l, stats_l, dxn, dxn_h, dX, dC, part_cs,
-                                                  gmax);
+    ln_bwd_prep_kernel<NV><<<grid, 32 * kLnbWarps, sm, st>>>(D, l, full_hcnt, x_l, xn_l, stats_l, dxn, dxn_h, dX, dC,
+                                                              part_cs, gmax);
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
