@@ -117,6 +117,7 @@ struct Engine {
   // opt-in (D2FT_SIDE=1): measured 5.716 vs 5.733 ms per step — the
   // persistent G5 CTAs that start in a tail hold their SMs until done
   bool use_side = getenv("D2FT_SIDE") != nullptr;
+  int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : 0;  // G5's grid on the side stream
   cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
   bool have_prefetch = false;
   int prefetch_B = 0;
@@ -142,7 +143,7 @@ struct Engine {
   bool partitioned() const { return ex && ex->world > 1; }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
                                        // (the variable-K GEMMs; uniform ones stay static)
-  enum { C_G3, C_G5, C_G7, C_G8 };
+  enum { C_G3, C_G5, C_G7, C_G8, C_G4 };
   int* ctr(int l, int kind) { return ctrs + (l < 0 ? (size_t)D.L * 8 : (size_t)l * 8) + kind; }
   uint32_t* sched_bits = nullptr;
   size_t sched_bits_words = 0;
@@ -593,7 +594,7 @@ struct Engine {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
                   ord_head + l * H, ctr(l, C_G5)},
-          0, s5);
+          s5 == st ? 0 : side_ctas, s5);
     };
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
@@ -608,7 +609,8 @@ struct Engine {
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
-                          (const act_t*)ZTl, db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps);
+                          (const act_t*)ZTl, db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps,
+                          side ? ctr(l, C_G4) : (int*)nullptr);
       mark(PH_ATTN_B);
       if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
         launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, O32T + (size_t)l * Bm * H * 64 * D.TP,

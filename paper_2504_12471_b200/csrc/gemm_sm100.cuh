@@ -276,14 +276,16 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           ptx::mbar_arrive(&kq_full[j]);
         }
       };
-      if constexpr (kDyn) {
+      bool dyn = false;
+      if constexpr (kDyn) dyn = prob.ctr != nullptr;  // a null counter selects static striding
+      if (dyn) {
         for (int i = 0;; ++i) {
           int t;
           if (rank == 0) {
             // claim only once the ring slot is free: claiming further ahead
             // than the pipeline needs unbalances the end of the launch
             ptx::mbar_wait(&ring_empty[i % kRing], ((i / kRing) & 1) ^ 1);
-            t = atomicAdd(prob.ctr, 1);
+            if constexpr (kDyn) t = atomicAdd(prob.ctr, 1);
             if (S::CLUSTER == 2) {
               const int q = i % kTileQ;
               ptx::mbar_wait_cluster(&tq_empty[q], ((i / kTileQ) & 1) ^ 1);

@@ -294,6 +294,7 @@ struct G4 {
   float* part_db1; // [EPI][Bmax][H][fs]
   const float* gmax;
   const CUtensorMap* maps;  // bulk-store maps: [3] dO (32 features x 32 tokens), [4] dY1T (32 tokens x 32 rows, 64B swizzle)
+  int* ctr;                 // non-null: dynamic tile claiming (gemm_sm100.cuh); null: static striding
   static constexpr int kChunk = 32;
   static constexpr bool kNonEmpty = true;
   static constexpr int kEpiStageBytes = 2048;
