@@ -262,24 +262,51 @@ __global__ void __launch_bounds__(32 * kLnbWarps) ln_bwd_prep_kernel(Dims D, int
 // ------------------------------------------------------------------ head
 // LN -> mean over tokens -> linear -> cross-entropy (model.cpp:342-355,
 // 400-414, 470-492); backward to dX = dL/dx_L.  One CTA per sample.
+// 4-CTA cluster per sample: each CTA takes a quarter of the tokens; the
+// partial pooled sums meet over DSMEM (fixed rank order, identical in every
+// CTA), every CTA redoes the tiny classifier + CE, and backpropagates its own
+// tokens.  One CTA per sample kept only 64 of 148 SMs busy.
+constexpr int kHeadCluster = 4;
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 template <int NV>
-__global__ void head_kernel(Dims D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                            double* loss_s, float* pooled_out, float* dlog_out, float* dX, float* gmax) {
+__global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, const int* labels, const float* Wc,
+                                                   const float* bc, float scale, double* loss_s, float* pooled_out,
+                                                   float* dlog_out, float* dX, float* gmax) {
   D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int nw = blockDim.x >> 5;
   float* part = reinterpret_cast<float*>(smem);  // [nw][d]
-  float* pooled = part + nw * D.d;               // [d]
+  float* ppart = part + nw * D.d;                // [d] this CTA's pooled partial (read by the peers)
+  float* pooled = ppart + D.d;                   // [d]
   float* dpooled = pooled + D.d;                 // [d]
   float* rowstat = dpooled + D.d;                // [T][2]
   __shared__ float logits[64], dlog[64];
-  const int s = blockIdx.x;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int s = blockIdx.x / kHeadCluster;
+  const int tq = (D.T + kHeadCluster - 1) / kHeadCluster;
+  const int ta = rank * tq, tb = min(D.T, ta + tq);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nv = NV;
   float acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.f;
-  for (int t = warp; t < D.T; t += nw) {
+  for (int t = ta + warp; t < tb; t += nw) {
     const float* row = xL + ((size_t)s * D.T + t) * D.d;
     float v[NV];
     float sum = 0.f;
@@ -310,10 +337,16 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
     float p = 0.f;
     for (int w = 0; w < nw; ++w) p += part[w * D.d + m];
-    pooled[m] = p / D.T;  // row_mean (linalg.cpp:101-105)
-    pooled_out[(size_t)s * D.d + m] = pooled[m];
+    ppart[m] = p;
   }
-  __syncthreads();
+  cluster_barrier();  // every CTA's partial is complete
+  for (int m = threadIdx.x; m < D.d; m += blockDim.x) {
+    float p = 0.f;
+    for (int r = 0; r < kHeadCluster; ++r) p += ld_cluster_f32(cluster_addr(ppart + m, r));
+    pooled[m] = p / D.T;  // row_mean (linalg.cpp:101-105)
+    if (rank == 0) pooled_out[(size_t)s * D.d + m] = pooled[m];
+  }
+  cluster_barrier();  // peers' partials read: they may proceed (and exit)
   for (int c = warp; c < D.C; c += nw) {
     float z = 0.f;
     for (int m = lane; m < D.d; m += 32) z += pooled[m] * Wc[(size_t)m * D.C + c];
@@ -327,12 +360,12 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
     for (int c = 1; c < D.C; ++c) mx = fmax(mx, (double)logits[c]);
     double sum = 0.0;
     for (int c = 0; c < D.C; ++c) sum += exp((double)logits[c] - mx);
-    loss_s[s] = log(sum) - ((double)logits[lab] - mx);
+    if (rank == 0) loss_s[s] = log(sum) - ((double)logits[lab] - mx);
     for (int c = 0; c < D.C; ++c) {
       double p = exp((double)logits[c] - mx) / sum;
       if (c == lab) p -= 1.0;
       dlog[c] = (float)(p * scale);
-      dlog_out[(size_t)s * D.C + c] = dlog[c];
+      if (rank == 0) dlog_out[(size_t)s * D.C + c] = dlog[c];
     }
   }
   __syncthreads();
@@ -345,7 +378,7 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   float dmean_l = 0.f;
   for (int m = lane; m < D.d; m += 32) dmean_l += dpooled[m];
   const float dmean = warp_sum(dmean_l) / D.d;
-  for (int t = warp; t < D.T; t += nw) {
+  for (int t = ta + warp; t < tb; t += nw) {
     const size_t ro = ((size_t)s * D.T + t) * D.d;
     const float mean = rowstat[2 * t], rstd = rowstat[2 * t + 1];
     float y[NV];
@@ -371,21 +404,26 @@ __global__ void head_kernel(Dims D, const float* xL, const int* labels, const fl
   }
 }
 
+// warp per output: lanes split the samples (fixed order: lane partials, then
+// a shuffle tree), so the B-long reductions run 32-wide
 __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                                    float* dbc, double* loss) {
   D2FT_PDL_ENTRY();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i < D.d * D.C) {
     const int m = i / D.C, c = i % D.C;
     float a = 0.f;
-    for (int s = 0; s < D.B; ++s) a += pooled[(size_t)s * D.d + m] * dlog[(size_t)s * D.C + c];
-    dWc[i] = a;
+    for (int s = lane; s < D.B; s += 32) a += pooled[(size_t)s * D.d + m] * dlog[(size_t)s * D.C + c];
+    a = warp_sum(a);
+    if (lane == 0) dWc[i] = a;
   } else if (i < D.d * D.C + D.C) {
     const int c = i - D.d * D.C;
     float a = 0.f;
-    for (int s = 0; s < D.B; ++s) a += dlog[(size_t)s * D.C + c];
-    dbc[c] = a;
-  } else if (i == D.d * D.C + D.C) {
+    for (int s = lane; s < D.B; s += 32) a += dlog[(size_t)s * D.C + c];
+    a = warp_sum(a);
+    if (lane == 0) dbc[c] = a;
+  } else if (i == D.d * D.C + D.C && lane == 0) {
     double a = 0.0;
     for (int s = 0; s < D.B; ++s) a += loss_s[s];
     *loss = a / D.B;
@@ -1003,12 +1041,23 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
-  // one CTA per sample, 16 warps (96 registers each): B (= 64) CTAs need many rows in flight each
   const int threads = 512;
-  const size_t sm = (size_t)((threads / 32 + 2) * D.d + 2 * D.T) * 4;
+  const size_t sm = (size_t)((threads / 32 + 3) * D.d + 2 * D.T) * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(head_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    head_kernel<NV><<<D.B, threads, sm, st>>>(D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(D.B * kHeadCluster);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kHeadCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    D2FT_CUDA(cudaLaunchKernelEx(&cfg, head_kernel<NV>, D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax));
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());
@@ -1016,7 +1065,7 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
 
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                         float* dbc, double* loss, cudaStream_t st) {
-  const int n = D.d * D.C + D.C + 1;
+  const int n = (D.d * D.C + D.C + 1) * 32;  // a warp per output
   head_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, loss_s, pooled, dlog, dWc, dbc, loss);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
