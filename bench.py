@@ -409,6 +409,21 @@ def run_ours(args):
         if codes is not None:
             r = cpu_baseline(codes, os.cpu_count() or 1)
             cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    prepass = None
+    if rank == 0 and world == 1:
+        # scoring pre-pass (scoring.cpp:108-151) of the same 64 samples, mbs 1,
+        # Fisher / WeightMagnitude: host buffers in, K x 64 tables out
+        try:
+            import time as _t
+            t0 = _t.perf_counter()
+            reps = 3
+            for _ in range(reps):
+                m.prepass_scores(x, y, 1, "fisher_information", "weight_magnitude")
+            dt = (_t.perf_counter() - t0) / reps
+            prepass = {"workload": f"prepass_scores ViT-B/16, {B} samples, micro-batch 1, Fisher + WeightMagnitude "
+                                   f"(host buffers, tables returned)", "samples_per_s": B / dt, "ms": dt * 1e3}
+        except Exception as e:
+            prepass = {"error": str(e)[:200]}
     vitl = None
     if rank == 0 and world == 1 and not args.no_vitl:
         try:
@@ -450,6 +465,8 @@ def run_ours(args):
             line["partition"] = part_info
         if vitl:
             line["vitl_1gpu"] = vitl
+        if prepass:
+            line["prepass"] = prepass
         print(json.dumps(line))
     m.close()
     if dist:

@@ -61,6 +61,18 @@ int d2ft_engine_step(d2ft_engine* e, const float* samples, const int32_t* labels
                      const int32_t* cap_fwd, int n_mb, int mbs, double lr, double momentum, double* loss_out,
                      uint8_t* codes_out);
 
+/* Scoring pre-pass, prepass_scores (scoring.hpp:48-54, scoring.cpp:108-151):
+ * every micro-batch of micro_batch_size samples runs forward + backward with
+ * all scheduled subnets Full and no weight update; fwd_out / bwd_out (K x
+ * num_samples/micro_batch_size, row-major = ScoreTable::forward / backward)
+ * receive the chosen metric of each head-subnet's unit gradient: 0
+ * FisherInformation (sum g^2), 1 WeightMagnitude (sum |w|), 2
+ * GradientMagnitude (sum |g|), 3 TaylorImportance (sum |w g|) — the Metric
+ * enum order.  Parameters are unchanged. */
+int d2ft_engine_prepass_scores(d2ft_engine* e, const float* samples, const int32_t* labels, int num_samples,
+                               int micro_batch_size, int fwd_metric, int bwd_metric, double* fwd_out,
+                               double* bwd_out);
+
 /* Input pipeline (a data loader's double buffering; no reference counterpart:
  * trainer.cpp:214-292 reads batches from host memory).  d2ft_engine_prefetch
  * starts the H2D copy of a batch's samples (pinned host memory) on the

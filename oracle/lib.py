@@ -274,6 +274,20 @@ class RefModel:
             raise OracleError(rc, self.lib.ref_last_error().decode())
         return loss.value, grads, eng
 
+    def prepass_scores(self, inputs, labels, mbs, fwd_metric, bwd_metric, threads=1):
+        """The reference's prepass_scores (scoring.cpp:108-151); metrics as Metric enum ints."""
+        x = np.ascontiguousarray(inputs, np.float64)
+        lab = np.ascontiguousarray(labels, np.int32)
+        units = len(lab) // mbs
+        K = self.dims[0] * self.dims[1]
+        fo = np.empty((K, units), np.float64)
+        bo = np.empty((K, units), np.float64)
+        rc = self.lib.ref_prepass_scores(C.c_void_p(self.h), _ptr(x), _ptr(lab), _I(len(lab)), _I(mbs),
+                                         _I(fwd_metric), _I(bwd_metric), _I(threads), _ptr(fo), _ptr(bo))
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+        return fo, bo
+
     def train_batch_parallel(self, inputs, labels, codes, mbs, lr, momentum, threads):
         x = np.ascontiguousarray(inputs, np.float64)
         lab = np.ascontiguousarray(labels, np.int32)

@@ -265,3 +265,38 @@ def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, lab
         velocity[a:b] = momentum * velocity[a:b] + g
         flat[a:b] -= lr * velocity[a:b]
     return batch_loss, touched
+
+
+# scoring.cpp:57-96 (non-LoRA: every tensor of the block subnet) and
+# prepass_scores, scoring.cpp:108-151: per unit, forward_backward with every
+# scheduled subnet Full, then the metric of each head-subnet's unit gradient.
+METRICS = ("fisher_information", "weight_magnitude", "gradient_magnitude", "taylor_importance")
+
+
+def metric_value(metric, w, g):
+    if metric == "fisher_information":
+        return float(np.sum(g * g))
+    if metric == "weight_magnitude":
+        return float(np.sum(np.abs(w)))
+    if metric == "gradient_magnitude":
+        return float(np.sum(np.abs(g)))
+    if metric == "taylor_importance":
+        return float(np.sum(np.abs(w * g)))
+    raise ValueError(metric)
+
+
+def prepass_scores(cfg: Config, flat, inputs, labels, mbs, fwd_metric, bwd_metric):
+    n = len(inputs)
+    assert n % mbs == 0
+    units = n // mbs
+    sl = subnet_slices(cfg)
+    fwd = np.zeros((cfg.K, units))
+    bwd = np.zeros((cfg.K, units))
+    col = np.ones(cfg.K, np.uint8)
+    for u in range(units):
+        _, g, _ = forward_backward(cfg, flat, inputs[u * mbs:(u + 1) * mbs], labels[u * mbs:(u + 1) * mbs], col)
+        for k in range(cfg.K):
+            a, b = sl[1 + k]
+            fwd[k, u] = metric_value(fwd_metric, flat[a:b], g[a:b])
+            bwd[k, u] = metric_value(bwd_metric, flat[a:b], g[a:b])
+    return fwd, bwd

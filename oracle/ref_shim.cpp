@@ -24,6 +24,7 @@
 #include "d2ft/rng.hpp"
 #include "d2ft/scheduler.hpp"
 #include "d2ft/scoring.hpp"
+#include "d2ft/scoring.hpp"
 #include "d2ft/trainer.hpp"
 
 using namespace d2ft;
@@ -286,6 +287,27 @@ int ref_forward_backward(void* h, const double* inputs, const int32_t* labels, i
         off += mat.data.size();
       });
     }
+  });
+}
+
+// prepass_scores (scoring.cpp:108-151) of the unmodified reference on a
+// dataset of n samples; fwd / bwd receive ScoreTable::forward / backward
+// (K x n/mbs, row-major).  Metrics: scoring.hpp Metric enum order.
+int ref_prepass_scores(void* h, const double* inputs, const int32_t* labels, int n, int mbs, int fwd_metric,
+                       int bwd_metric, int threads, double* fwd, double* bwd) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    Dataset ds;
+    fill_inputs(m, inputs, n, ds.samples);
+    ds.labels.assign(labels, labels + n);
+    ds.num_classes = m->model.config().num_classes;
+    ScoreTable t = prepass_scores(m->model, ds, mbs, static_cast<Metric>(fwd_metric), static_cast<Metric>(bwd_metric),
+                                  threads);
+    for (int k = 0; k < t.subnets; ++k)
+      for (int u = 0; u < t.micro_batches; ++u) {
+        fwd[static_cast<std::size_t>(k) * t.micro_batches + u] = t.fwd(k, u);
+        bwd[static_cast<std::size_t>(k) * t.micro_batches + u] = t.bwd(k, u);
+      }
   });
 }
 

@@ -547,7 +547,13 @@ struct Engine {
 
   // ---------------------------------------------------------------- the step
   // Requires codes_exp + compaction lists + plan for this batch.
-  void run_forward_backward() {
+  // scoring pre-pass mode of run_forward_backward: unit-mean loss, the weight
+  // gradient GEMMs replaced by per-unit score reductions, no embedding wgrad
+  struct ScoreMode {
+    int n_units, mbs;
+    float *p7, *p5;  // [L][n_units][H][kScoreTiles][16][3]
+  };
+  void run_forward_backward(const ScoreMode* sm = nullptr) {
     const size_t L = D.L, Bm = D.Bmax, T = D.T, d = D.d, H = D.H;
     const size_t xs = Bm * T * d;
     mark(PH_EMBED);
@@ -583,13 +589,14 @@ struct Engine {
     }
     mark(PH_HEAD);
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
-    launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off, 1.0f / (float)D.B, loss_s, pooled,
+    launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off,
+                sm ? 1.0f / (float)sm->mbs : 1.0f / (float)D.B, loss_s, pooled,
                 dlog, dX, gmax, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
-    const bool side = use_side && !profiling && !partitioned();
+    const bool side = use_side && !profiling && !partitioned() && !sm;
     auto g5 = [&](int l, cudaStream_t s5) {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
@@ -620,8 +627,23 @@ struct Engine {
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
       mark(PH_G5);
-      if (!side) g5(l, st);
+      const size_t sper = sm ? (size_t)sm->n_units * H * kScoreTiles * 16 * 3 : 0;
+      if (sm) {
+        launch_gemm<S5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
+            tm_dC64, tm_OGT,
+            S5<160>{D, l, sm->mbs, sm->n_units, P + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax, sm->p5 + l * sper},
+            0, st);
+      } else if (!side) {
+        g5(l, st);
+      }
       mark(PH_G7);
+      if (sm)
+        launch_gemm<S7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
+            tm_xn64, tm_dY1Tb,
+            S7<kG7BN>{D, l, sm->mbs, sm->n_units, P + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                      sm->p7 + l * sper},
+            0, st);
+      else
       launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
           tm_xn64, tm_dY1Tb,
           G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
@@ -644,6 +666,7 @@ struct Engine {
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
                          partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
+    if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     mark(PH_EMBED_W);
     launch_gemm<EmbedW<256>, GemmShape<256, kCG2 ? 6 : 4, 0, 4, 2, 0, 1, kCG2>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, cs_slot(L), dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
@@ -658,6 +681,43 @@ struct Engine {
     }
     return side_ev[i];
   }
+  // prepass_scores (scoring.cpp:108-151) on the staged samples/labels:
+  // n_units micro-batches of mbs samples, all head-subnets Full, no update.
+  void prepass(int n_units, int mbs, int fwd_metric, int bwd_metric, double* fwd_host, double* bwd_host) {
+    D2FT_REQUIRE(!partitioned(), kState, "prepass: not available on a head-partitioned engine");
+    const int B = n_units * mbs;
+    begin_step(B);
+    const int K = D.K();
+    const size_t per = (size_t)D.L * n_units * D.H * kScoreTiles * 16 * 3;
+    if (score_cap < per) {
+      D2FT_CUDA(cudaStreamSynchronize(st));
+      float* p = nullptr;
+      D2FT_CUDA(cudaMalloc(&p, (2 * per + (size_t)D.L * n_units * D.H * 3) * sizeof(float)));
+      owned.push_back(p);
+      score_buf = p;
+      score_cap = per;
+      double* q = nullptr;
+      D2FT_CUDA(cudaMalloc(&q, ((size_t)K + 2 * (size_t)K * D.Bmax) * sizeof(double)));
+      owned.push_back(q);
+      score_dbl = q;
+    }
+    float *p7 = score_buf, *p5 = score_buf + per, *pb = score_buf + 2 * per;
+    double *wm = score_dbl, *fo = score_dbl + K, *bo = fo + (size_t)K * D.Bmax;
+    D2FT_CUDA(cudaMemsetAsync(codes_exp, 1, (size_t)K * D.Bmax, st));  // every cell Full
+    D2FT_CUDA(cudaMemsetAsync(score_buf, 0, 2 * per * sizeof(float), st));  // unused tile slots sum as 0
+    compact_and_plan();
+    ScoreMode m{n_units, mbs, p7, p5};
+    run_forward_backward(&m);
+    launch_score_bias(D, mbs, n_units, part_db1, part_cs, P + seg[S_B1].off, P + seg[S_B2].off, pb, st);
+    launch_score_weight(D, P + seg[S_W1T].off, P + seg[S_W2T].off, P + seg[S_B1].off, P + seg[S_B2].off, wm, st);
+    launch_score_reduce(D, n_units, p7, p5, pb, wm, fwd_metric, bwd_metric, fo, bo, st);
+    D2FT_CUDA(cudaMemcpyAsync(fwd_host, fo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
+    D2FT_CUDA(cudaMemcpyAsync(bwd_host, bo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
+  }
+  float* score_buf = nullptr;
+  double* score_dbl = nullptr;
+  size_t score_cap = 0;
+
   float* cs_slot(int k) { return part_cs + (size_t)k * D.Bmax * ((D.T + 31) / 32) * D.d; }
   float* db1_slot(int l) { return part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs; }
 
@@ -969,6 +1029,30 @@ int d2ft_engine_forward_backward(d2ft_engine* h, const float* samples, const int
     E.run_forward_backward();
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
+  });
+}
+
+int d2ft_engine_prepass_scores(d2ft_engine* h, const float* samples, const int32_t* labels, int num_samples,
+                               int micro_batch_size, int fwd_metric, int bwd_metric, double* fwd_out,
+                               double* bwd_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_REQUIRE(num_samples >= 1, kInput, "prepass_scores: empty dataset");
+    D2FT_REQUIRE(micro_batch_size >= 1 && num_samples % micro_batch_size == 0, kInput,
+                 "dataset size must be a multiple of the micro-batch size");
+    D2FT_REQUIRE(num_samples <= E.D.Bmax, kSize, "prepass_scores: more samples than the engine's batch capacity");
+    D2FT_REQUIRE(fwd_metric >= 0 && fwd_metric <= 3 && bwd_metric >= 0 && bwd_metric <= 3, kConfig,
+                 "unknown metric");
+    D2FT_REQUIRE(fwd_out && bwd_out, kInput, "prepass_scores: null output");
+    validate_labels(labels, num_samples, E.D.C);
+    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, samples, (size_t)num_samples * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice,
+                              E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, num_samples * 4, cudaMemcpyHostToDevice, E.st));
+    E.prepass(num_samples / micro_batch_size, micro_batch_size, fwd_metric, bwd_metric, fwd_out, bwd_out);
+    check_status(E.finish_and_check());
+    for (size_t i = 0; i < (size_t)E.D.K() * (num_samples / micro_batch_size); ++i)
+      D2FT_REQUIRE(std::isfinite(fwd_out[i]) && std::isfinite(bwd_out[i]), kNumeric,
+                   "prepass_scores produced a non-finite score");
   });
 }
 

@@ -23,6 +23,8 @@ __device__ __forceinline__ float grad_scale(const float* gmax) {
 
 // epilogue warpgroups of the step GEMMs (GemmShape::EPI) — G4's db1 partials
 constexpr int kEpiGroups = 4;
+// scoring pre-pass: GEMM tiles per (unit, head) partial slot (>= m-tiles (d/128 <= 8) x n-tiles (2))
+constexpr int kScoreTiles = 16;
 
 // Model/step geometry (ModelConfig, model.hpp:43-57, plus the B200 layout).
 struct Dims {

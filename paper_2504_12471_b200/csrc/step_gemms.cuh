@@ -629,3 +629,149 @@ struct EmbedW {
 };
 
 }  // namespace d2ft_b200
+
+namespace d2ft_b200 {
+
+// ---------------------------------------------------------------- scoring pre-pass
+// prepass_scores (scoring.cpp:108-151): every micro-batch ("unit") runs
+// forward + backward with all subnets Full and no update; each scheduled
+// head-subnet's unit gradient is reduced to sum(g^2) (FisherInformation),
+// sum|g| (GradientMagnitude) and sum|w g| (TaylorImportance), scoring.cpp:57-96.
+// The unit gradients of the weight matrices are the G7 / G5 products with K
+// restricted to the unit's tokens; nothing is stored — the epilogue folds the
+// three sums per thread and one lane per warp writes the warp's partials:
+//   part[((u * H + h) * kScoreTiles + tile) * 16 + warp][3],  tile = mt * 2 + nt
+// (fixed-order reduction in score_reduce_kernel).
+
+struct ScoreRow {
+  float f2, fa, ft;  // sum g^2, sum |g|, sum |w g|
+  float inv;
+};
+__device__ __forceinline__ void score_row_end(float* part, size_t base, int warp, ScoreRow& r) {
+  float a = r.f2, b = r.fa, c = r.ft;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    float* p = part + (base * 16 + warp) * 3;
+    p[0] = a;
+    p[1] = b;
+    p[2] = c;
+  }
+}
+
+// unit gradients of [Wq|Wk|Wv|W1] (G7 with K = the unit's tokens): M = d, N = PQ
+template <int BN>
+struct S7 {
+  Dims D;
+  int l, mbs, n_units;
+  const float* W1T;  // block l master: [H][PQ][d]
+  const float* gmax;
+  float* part;
+  struct Tile {
+    int nkb, u, h, mt, nt;
+  };
+  using Row = ScoreRow;
+  __device__ int ntm() const { return (D.d + 127) / 128; }
+  __device__ int ntn() const { return (D.PQ + BN - 1) / BN; }
+  __device__ int ntiles() const { return n_units * D.H * mpairs(ntm()) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int per = mpairs(ntm()) * ntn();
+    c.u = t / (D.H * per);
+    c.h = (t / per) % D.H;
+    const int r = t % per;
+    c.mt = 2 * (r / ntn()) + rank;
+    c.nt = r % ntn();
+    c.nkb = D.TB * mbs;
+  }
+  __device__ int ksteps(const Tile&, int kb) const {
+    return kb % D.TB == D.TB - 1 ? (D.T - 64 * (D.TB - 1) + 15) / 16 : 4;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int s = c.u * mbs + kb / D.TB;
+    const int t0 = (kb % D.TB) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, l * D.Bmax + s, t0, c.nt * BN, s * D.H + c.h};
+  }
+  __device__ void row_begin(const Tile&, int, Row& r) const {
+    r.f2 = r.fa = r.ft = 0.f;
+    r.inv = 1.f / grad_scale(gmax);
+  }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
+    const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
+    const int f0 = c.nt * BN + col0;
+    const float* w = W1T + ((size_t)c.h * D.PQ + f0) * D.d + m;  // lanes: consecutive m
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (f0 + i < D.PQ) {
+        const float g = v[i] * r.inv;
+        r.f2 = fmaf(g, g, r.f2);
+        r.fa += fabsf(g);
+        r.ft += fabsf(g * __ldg(w + (size_t)i * D.d));
+      }
+  }
+  __device__ void row_end(const Tile& c, int, int, Row& r) const {
+    const int warp = (threadIdx.x >> 5) - 4;
+    score_row_end(part, ((size_t)c.u * D.H + c.h) * kScoreTiles + c.mt * ntn() + c.nt, warp, r);
+  }
+};
+
+// unit gradients of [Wo;W2] (G5 with K = the unit's tokens): M = d, N = PO
+template <int BN>
+struct S5 {
+  Dims D;
+  int l, mbs, n_units;
+  const float* W2T;  // block l master: [d][H*PO]
+  const float* gmax;
+  float* part;
+  struct Tile {
+    int nkb, u, h, mt, nt;
+  };
+  using Row = ScoreRow;
+  __device__ int ntn() const { return (D.PO + BN - 1) / BN; }
+  __device__ int ntiles() const { return n_units * D.H * mpairs(D.d / 128) * ntn(); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int per = mpairs(D.d / 128) * ntn();
+    c.u = t / (D.H * per);
+    c.h = (t / per) % D.H;
+    const int r = t % per;
+    c.mt = 2 * (r / ntn()) + rank;
+    c.nt = r % ntn();
+    c.nkb = D.TB * mbs;
+  }
+  __device__ int ksteps(const Tile&, int kb) const {
+    return kb % D.TB == D.TB - 1 ? (D.T - 64 * (D.TB - 1) + 15) / 16 : 4;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    const int s = c.u * mbs + kb / D.TB;
+    const int t0 = (kb % D.TB) * 64;
+    return KCoord{t0, c.mt * 128, c.mt * 128 + 64, s, t0, c.nt * BN, (l * D.Bmax + s) * D.H + c.h};
+  }
+  __device__ void row_begin(const Tile&, int, Row& r) const {
+    r.f2 = r.fa = r.ft = 0.f;
+    r.inv = 1.f / grad_scale(gmax);
+  }
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
+    const int m = c.mt * 128 + row;
+    if (m >= D.d) return;
+    const int f0 = c.nt * BN + col0;
+    const float* w = W2T + (size_t)m * D.H * D.PO + c.h * D.PO + f0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (f0 + i < D.PO) {
+        const float g = v[i] * r.inv;
+        r.f2 = fmaf(g, g, r.f2);
+        r.fa += fabsf(g);
+        r.ft += fabsf(g * __ldg(w + i));
+      }
+  }
+  __device__ void row_end(const Tile& c, int, int, Row& r) const {
+    const int warp = (threadIdx.x >> 5) - 4;
+    score_row_end(part, ((size_t)c.u * D.H + c.h) * kScoreTiles + c.mt * ntn() + c.nt, warp, r);
+  }
+};
+
+}  // namespace d2ft_b200

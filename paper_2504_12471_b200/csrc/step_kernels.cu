@@ -1106,3 +1106,130 @@ void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st) {
 }
 
 }  // namespace d2ft_b200
+
+namespace d2ft_b200 {
+
+// ---------------------------------------------------------------- scoring pre-pass
+// Bias parts of the unit gradients (b1 from G4's per-sample partials, b2 from
+// the LN backward's per-tile column sums of the gradient entering the block),
+// for every block: part[((l * n_units + u) * H + h) * 3 + {f2, fa, ft}].
+__global__ void score_bias_kernel(Dims D, int mbs, int n_units, const float* part_db1, const float* part_cs,
+                                  const float* b1, const float* b2, float* part) {
+  D2FT_PDL_ENTRY();
+  const int u = blockIdx.x, h = blockIdx.y, l = blockIdx.z;
+  const int ntile = (D.T + 31) / 32, w = D.d / D.H;
+  const float* pdb = part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs;
+  const float* pcs = part_cs + (size_t)l * D.Bmax * ntile * D.d;
+  float f2 = 0.f, fa = 0.f, ft = 0.f;
+  for (int j = threadIdx.x; j < D.fs + w; j += blockDim.x) {
+    float g = 0.f, wt;
+    if (j < D.fs) {
+      for (int s = u * mbs; s < (u + 1) * mbs; ++s)
+        for (int e = 0; e < kEpiGroups; ++e) g += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
+      wt = b1[((size_t)l * D.H + h) * D.fs + j];
+    } else {
+      const int m = h * w + (j - D.fs);
+      for (int s = u * mbs; s < (u + 1) * mbs; ++s)
+        for (int tt = 0; tt < ntile; ++tt) g += pcs[((size_t)s * ntile + tt) * D.d + m];
+      wt = b2[(size_t)l * D.d + m];
+    }
+    f2 = fmaf(g, g, f2);
+    fa += fabsf(g);
+    ft += fabsf(g * wt);
+  }
+  __shared__ float red[3][32];
+  f2 = warp_sum(f2);
+  fa = warp_sum(fa);
+  ft = warp_sum(ft);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = f2;
+    red[1][warp] = fa;
+    red[2][warp] = ft;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float a = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a += red[threadIdx.x][i];
+    part[(((size_t)l * n_units + u) * D.H + h) * 3 + threadIdx.x] = a;
+  }
+}
+
+// WeightMagnitude per scheduled head-subnet (scoring.cpp:66-72): sum |w| over
+// wq, wk, wv, wo, w1, b1, w2, b2 (fp32 masters, fp64 sum per thread).
+__global__ void score_weight_kernel(Dims D, const float* W1T, const float* W2T, const float* b1, const float* b2,
+                                    double* wm) {
+  D2FT_PDL_ENTRY();
+  const int h = blockIdx.x, l = blockIdx.y, w = D.d / D.H;
+  const float* a = W1T + ((size_t)l * D.H + h) * D.PQ * D.d;
+  const float* c = W2T + (size_t)l * D.d * D.H * D.PO + h * D.PO;
+  double s = 0.0;
+  for (size_t i = threadIdx.x; i < (size_t)D.PQ * D.d; i += blockDim.x) s += fabsf(a[i]);
+  for (size_t i = threadIdx.x; i < (size_t)D.d * D.PO; i += blockDim.x) s += fabsf(c[(i / D.PO) * D.H * D.PO + i % D.PO]);
+  for (int i = threadIdx.x; i < D.fs; i += blockDim.x) s += fabsf(b1[((size_t)l * D.H + h) * D.fs + i]);
+  for (int i = threadIdx.x; i < w; i += blockDim.x) s += fabsf(b2[(size_t)l * D.d + h * w + i]);
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    wm[l * D.H + h] = t;
+  }
+}
+
+// table[k][u] of a metric (0 Fisher, 1 WeightMagnitude, 2 GradientMagnitude,
+// 3 Taylor; scoring.hpp:19-24) from the fixed-order sum of the GEMM partials
+// (S7 then S5, tile then warp) and the bias part.
+__global__ void score_reduce_kernel(Dims D, int n_units, const float* p7, const float* p5, const float* pb,
+                                    const double* wm, int fwd_metric, int bwd_metric, double* fwd_out,
+                                    double* bwd_out) {
+  D2FT_PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = D.L * D.H;
+  if (i >= K * n_units) return;
+  const int k = i / n_units, u = i % n_units, l = k / D.H, h = k % D.H;
+  double acc[3] = {0.0, 0.0, 0.0};
+  const size_t per = (size_t)n_units * D.H * kScoreTiles * 16 * 3;  // one block's partials
+  for (int which = 0; which < 2; ++which) {
+    const float* p = (which ? p5 : p7) + l * per + (((size_t)u * D.H + h) * kScoreTiles) * 16 * 3;
+    for (int e = 0; e < kScoreTiles * 16; ++e)
+      for (int q = 0; q < 3; ++q) acc[q] += p[e * 3 + q];
+  }
+  for (int q = 0; q < 3; ++q) acc[q] += pb[(((size_t)l * n_units + u) * D.H + h) * 3 + q];
+  auto pick = [&](int metric) {
+    switch (metric) {
+      case 0: return acc[0];
+      case 1: return wm[k];
+      case 2: return acc[1];
+      default: return acc[2];
+    }
+  };
+  fwd_out[(size_t)k * n_units + u] = pick(fwd_metric);
+  bwd_out[(size_t)k * n_units + u] = pick(bwd_metric);
+}
+
+void launch_score_bias(const Dims& D, int mbs, int n_units, const float* part_db1, const float* part_cs,
+                       const float* b1, const float* b2, float* part, cudaStream_t st) {
+  score_bias_kernel<<<dim3(n_units, D.H, D.L), 256, 0, st>>>(D, mbs, n_units, part_db1, part_cs, b1, b2, part);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
+void launch_score_weight(const Dims& D, const float* W1T, const float* W2T, const float* b1, const float* b2,
+                         double* wm, cudaStream_t st) {
+  score_weight_kernel<<<dim3(D.H, D.L), 512, 0, st>>>(D, W1T, W2T, b1, b2, wm);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
+void launch_score_reduce(const Dims& D, int n_units, const float* p7, const float* p5, const float* pb,
+                         const double* wm, int fwd_metric, int bwd_metric, double* fwd_out, double* bwd_out,
+                         cudaStream_t st) {
+  const int n = D.L * D.H * n_units;
+  score_reduce_kernel<<<(n + 127) / 128, 128, 0, st>>>(D, n_units, p7, p5, pb, wm, fwd_metric, bwd_metric, fwd_out,
+                                                       bwd_out);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
+
+}  // namespace d2ft_b200

@@ -66,4 +66,14 @@ void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long l
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st);
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st);
 
+// scoring pre-pass (step_gemms.cuh S5 / S7 + these): bias parts of the unit
+// gradients, WeightMagnitude per head-subnet, and the K x n_units tables
+void launch_score_bias(const Dims& D, int mbs, int n_units, const float* part_db1, const float* part_cs,
+                       const float* b1, const float* b2, float* part, cudaStream_t st);
+void launch_score_weight(const Dims& D, const float* W1T, const float* W2T, const float* b1, const float* b2,
+                         double* wm, cudaStream_t st);
+void launch_score_reduce(const Dims& D, int n_units, const float* p7, const float* p5, const float* pb,
+                         const double* wm, int fwd_metric, int bwd_metric, double* fwd_out, double* bwd_out,
+                         cudaStream_t st);
+
 }  // namespace d2ft_b200

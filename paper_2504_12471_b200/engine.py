@@ -50,6 +50,9 @@ class ModelConfig:
                     self.num_classes, self.seed)
 
 
+# scoring.hpp:19-24 (Metric enum order; names as metric_name, scoring.cpp)
+METRICS = ("fisher_information", "weight_magnitude", "gradient_magnitude", "taylor_importance")
+
 # presets of BASELINE.json
 TINY = ModelConfig(2, 4, 128, 512, 64, 4, 1)
 VIT_B16 = ModelConfig(12, 12, 768, 3072, 197, 8, 1)
@@ -195,6 +198,29 @@ class SubnetModel:
                                      ptr(cb), ptr(i32(capacities.full)), ptr(i32(capacities.fwd)), C.c_int(n_mb),
                                      C.c_int(mbs), C.c_double(lr), C.c_double(momentum), C.byref(loss), ptr(codes)))
         return loss.value, ScheduleTable(K, n_mb, codes)
+
+    def prepass_scores(self, samples, labels, micro_batch_size=1, fwd_metric="fisher_information",
+                       bwd_metric="weight_magnitude") -> ScoreTable:
+        """prepass_scores (scoring.cpp:108-151): every micro-batch forward and
+        backward with all scheduled subnets Full and no update; the chosen
+        metric of each head-subnet's unit gradient (scoring.cpp:57-96)."""
+        x = np.ascontiguousarray(samples, np.float32)
+        y = i32(labels)
+        n = len(y)
+        if n == 0:
+            raise Error(2, "prepass_scores: empty dataset")
+        if micro_batch_size < 1 or n % micro_batch_size:
+            raise Error(2, "dataset size must be a multiple of the micro-batch size")
+        units = n // micro_batch_size
+        K = self.scheduled_count()
+        fo = np.zeros((K, units), np.float64)
+        bo = np.zeros((K, units), np.float64)
+        check(lib().d2ft_engine_prepass_scores(self._h, ptr(x), ptr(y), C.c_int(n), C.c_int(micro_batch_size),
+                                               C.c_int(METRICS.index(fwd_metric)), C.c_int(METRICS.index(bwd_metric)),
+                                               ptr(fo), ptr(bo)))
+        t = ScoreTable(K, units, fo, bo, fwd_metric, bwd_metric)
+        t.validate()
+        return t
 
     # -- bench path -------------------------------------------------------
     def stage(self, samples, labels, scores: ScoreTable, cost_model: CostModel, capacities: Capacities, mbs=1):

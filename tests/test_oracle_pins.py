@@ -200,3 +200,21 @@ def test_oracle_matches_reference_model():
     l1, g1, e1 = MO.forward_backward(cfg, p, x[:2], y[:2], col)
     l2, g2, e2 = r.forward_backward(x[:2], y[:2], col)
     assert abs(l1 - l2) < 1e-12 and np.max(np.abs(g1 - g2)) < 1e-12 and np.array_equal(e1, e2)
+
+
+@needs_ref
+@pytest.mark.parametrize("mbs", [1, 2])
+def test_oracle_prepass_matches_reference(mbs):
+    """The numpy restatement of prepass_scores / metric_value (model_oracle.py)
+    against the unmodified reference's prepass_scores (scoring.cpp:108-151),
+    all four metrics, on a perturbed model."""
+    cfg = MO.Config(2, 4, 32, 64, 16, 4)
+    r = O.RefModel(2, 4, 32, 64, 16, 4, 1)
+    p = O.partition_model(2, 4, 32, 64, 16, 4, 1) + 0.05 * np.random.default_rng(1).standard_normal(r.n)
+    r.set_params(p)
+    x, y = O.make_dataset(4, 4, 32, 16, 0.5, 7)
+    for fi, bi in ((0, 1), (2, 3)):
+        rf, rb = r.prepass_scores(x, y, mbs, fi, bi, threads=2)
+        of, ob = MO.prepass_scores(cfg, p, x, y, mbs, MO.METRICS[fi], MO.METRICS[bi])
+        assert np.allclose(of, rf, rtol=1e-10, atol=0) and np.allclose(ob, rb, rtol=1e-10, atol=0)
+    assert np.array_equal(r.params(), p)  # no update
