@@ -47,6 +47,64 @@ __device__ inline void set_err(int32_t* err, int code) {
   if (err) atomicCAS(err, 0, code);
 }
 
+// One warp (the training shapes: ViT-B 25 p_f of 64 -> 26 columns, ViT-L 102
+// of 256 -> 103): lane holds columns m = 32 j + lane, j < CW.  Column m-1
+// comes from the lane below (shuffle up) or, for lane 0, from lane 31 of the
+// previous 32-column group — registers only, no shared-memory exchange or
+// barrier per item.  Same fp64 adds in the same order and the same
+// decision-bit words (word j = columns 32 j .. 32 j + 31) as the block path.
+// All threads of the block call it (block-uniform arguments).
+template <int CW>
+__device__ double dp_row_warp(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
+                              double* s_obj) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {
+    double v[CW];
+    bool okc[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int m = 32 * j + lane;
+      v[j] = 0.0;
+      okc[j] = (wt == 0) ? (m == 0) : (m >= 1 && m <= Mp);
+    }
+    for (int i = 0; i < N; ++i) {
+      const double s = s_scores[i];
+      double prev[CW];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const double up = __shfl_up_sync(0xffffffffu, v[j], 1);
+        double wrap = 0.0;
+        if (j > 0) wrap = __shfl_sync(0xffffffffu, v[j - 1], 31);
+        prev[j] = lane > 0 ? up : wrap;
+        if (wt == 0) prev[j] = v[j];  // zero weight: take reads the same column
+      }
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const double take = __dadd_rn(prev[j], s);
+        const bool d = okc[j] && (take > v[j]);  // scheduler.cpp:167 strict >
+        if (d) v[j] = take;
+        const unsigned ball = __ballot_sync(0xffffffffu, d);
+        if (lane == 0) bits[(size_t)i * CW + j] = ball;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+      if (32 * j + lane == Mp) *s_obj = v[j];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
+    for (int i = N; i > 0; --i) {
+      const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
+      const unsigned b = (bits[(size_t)(i - 1) * CW + (col >> 5)] >> (col & 31)) & 1u;
+      sel[i - 1] = (uint8_t)b;
+      if (b && wt > 0) mm -= 1;
+    }
+  }
+  __syncthreads();
+  return *s_obj;
+}
+
 // Count-compressed 0/1 knapsack of one row (all threads of the block call it
 // with block-uniform arguments).  s_scores: the row's N scores in shared
 // memory.  Writes sel[i] in {0,1} (shared or global) and returns the
@@ -58,6 +116,19 @@ __device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, u
   const int ncols = Mp + 1;
   int nw, C;
   row_geometry(ncols, &nw, &C);
+  if (ncols <= 32 * kCMax) {
+    const int Cw = (ncols + 31) / 32;
+    switch (Cw) {  // compile-time column count: a straight-line item loop
+      case 1: return dp_row_warp<1>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 2: return dp_row_warp<2>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 3: return dp_row_warp<3>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 4: return dp_row_warp<4>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 5: return dp_row_warp<5>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 6: return dp_row_warp<6>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      case 7: return dp_row_warp<7>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+      default: return dp_row_warp<8>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    }
+  }
   const int nthr = nw * 32;
   const int words = nw * C;
   const bool active = tid < nthr;
@@ -138,6 +209,8 @@ struct KnapsackArgs {
   bool bits_in_smem;
   int words_max;
   bool validate;
+  int lists_smem_bytes;  // dynamic shared memory of the launch (staging of the table for the column lists)
+  bool cols_in_kernel;   // the last CTA builds the column lists (table staged in its shared memory)
 };
 
 // Warp 0 writes the ascending index lists of one row (codes in smem).
@@ -166,11 +239,14 @@ __device__ void row_lists(const uint8_t* s_codes, int N, int32_t* fwd_idx, int32
 __device__ void column_lists(const uint8_t* codes, int K, int N, int H, const CompactLists& L, int tid0,
                              int stride) {
   const int nb = K / H;
-  for (int cell = tid0; cell < N * nb; cell += stride) {
-    const int i = cell / nb, l = cell % nb;
+  // consecutive threads take consecutive micro-batches of one block, so each
+  // head's code loads of a warp are one contiguous 32-byte segment
+  for (int q = tid0; q < N * nb; q += stride) {
+    const int l = q / N, i = q % N;
+    const int cell = i * nb + l;
     int a = 0, f = 0;
     for (int h = 0; h < H; ++h) {
-      const uint8_t c = __ldcg(codes + (size_t)(l * H + h) * N + i);
+      const uint8_t c = codes[(size_t)(l * H + h) * N + i];
       if (c == 1 || c == 2) L.act_heads[(size_t)cell * H + a++] = h;
       if (c == 1) L.full_heads[(size_t)cell * H + f++] = h;
     }
@@ -234,6 +310,7 @@ __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
   if (threadIdx.x < 32)
     row_lists(s_codes, N, A.lists.fwd_idx + (size_t)k * N, A.lists.fwd_cnt + k, A.lists.full_idx + (size_t)k * N,
               A.lists.full_cnt + k);
+  if (!A.cols_in_kernel) return;  // large tables: compact_cols_kernel after this launch
   // last CTA to finish builds the per-(micro-batch, block) head lists
   __shared__ bool s_last;
   __threadfence();
@@ -245,7 +322,19 @@ __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    column_lists(A.codes, A.K, N, A.H, A.lists, threadIdx.x, blockDim.x);
+    // the whole K x N table into this CTA's (now free) shared memory with
+    // coalesced 16-byte loads when it fits, then every cell scans it there:
+    // the per-cell head loops were 12 strided global loads each
+    const size_t kn = (size_t)A.K * N;
+    if (kn <= (size_t)A.lists_smem_bytes && (kn & 15) == 0) {
+      uint8_t* tab = reinterpret_cast<uint8_t*>(smem);
+      for (size_t q = threadIdx.x; q < kn / 16; q += blockDim.x)
+        reinterpret_cast<uint4*>(tab)[q] = __ldcg(reinterpret_cast<const uint4*>(A.codes) + q);
+      __syncthreads();
+      column_lists(tab, A.K, N, A.H, A.lists, threadIdx.x, blockDim.x);
+    } else {
+      column_lists(A.codes, A.K, N, A.H, A.lists, threadIdx.x, blockDim.x);
+    }
     if (threadIdx.x == 0) *A.ws.done_counter = 0u;  // re-arm for the next launch
   }
 }
@@ -525,7 +614,12 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   A.ws = ws;
   A.validate = validate;
   A.words_max = (max_cols + 31) / 32 + 8;
-  const size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
+  size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
+  // room to stage the K x N table for the last CTA's column lists (<= 48 KB)
+  const size_t kn = (size_t)K * N;
+  if (lists && kn <= 48 * 1024 && kn > smem) smem = (kn + 15) & ~size_t(15);
+  A.lists_smem_bytes = (int)smem;
+  A.cols_in_kernel = kn <= smem && (kn & 15) == 0;
   if (!A.bits_in_smem)
     D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(K, N, max_cols), kState,
                  "knapsack: global decision-bit workspace too small");
@@ -538,6 +632,12 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   knapsack_kernel<<<K, kThreads, smem, stream>>>(A);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
+  if (lists && !A.cols_in_kernel) {  // column lists over many CTAs (one thread per cell)
+    const int cells = N * (K / H);
+    compact_cols_kernel<<<(cells + 127) / 128, 128, 0, stream>>>(codes, K, N, H, *lists);
+    count_launch();
+    D2FT_CUDA(cudaGetLastError());
+  }
 }
 
 void launch_dp_const(const double* scores, const int32_t* row_wt, const int32_t* caps, const int32_t* rows,
