@@ -105,32 +105,15 @@ __device__ double dp_row_warp(const double* s_scores, int N, int wt, int cap, in
   return *s_obj;
 }
 
-// Count-compressed 0/1 knapsack of one row (all threads of the block call it
-// with block-uniform arguments).  s_scores: the row's N scores in shared
-// memory.  Writes sel[i] in {0,1} (shared or global) and returns the
-// objective T[N][cap] in thread 0.
-__device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, uint32_t* bits, double* xch,
-                               uint8_t* sel, double* s_obj) {
+// Block path (more than 256 columns, up to 8 warps): columns m = j * nthr +
+// warp * 32 + lane; the boundary column of each warp crosses through a
+// double-buffered shared exchange and one named barrier per item.
+template <int CC>
+__device__ double dp_row_block(const double* s_scores, int N, int wt, int cap, int Mp, int nw, uint32_t* bits,
+                               double* xch, uint8_t* sel, double* s_obj) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int Mp = (wt == 0) ? 0 : min(cap / wt, N);  // last stored column
-  const int ncols = Mp + 1;
-  int nw, C;
-  row_geometry(ncols, &nw, &C);
-  if (ncols <= 32 * kCMax) {
-    const int Cw = (ncols + 31) / 32;
-    switch (Cw) {  // compile-time column count: a straight-line item loop
-      case 1: return dp_row_warp<1>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 2: return dp_row_warp<2>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 3: return dp_row_warp<3>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 4: return dp_row_warp<4>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 5: return dp_row_warp<5>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 6: return dp_row_warp<6>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      case 7: return dp_row_warp<7>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-      default: return dp_row_warp<8>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    }
-  }
   const int nthr = nw * 32;
-  const int words = nw * C;
+  const int words = nw * CC;
   const bool active = tid < nthr;
   double v[kCMax];
 #pragma unroll
@@ -147,8 +130,8 @@ __device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, u
       const double* xin = xch + p * (8 * kCMax);
       double* xout = xch + (p ^ 1) * (8 * kCMax);
 #pragma unroll
-      for (int j = 0; j < kCMax; ++j) {
-        if (j < C) {
+      for (int j = 0; j < CC; ++j) {
+        {
           const int m = j * nthr + warp * 32 + lane;
           double prev = __shfl_up_sync(0xffffffffu, v[j], 1);
           if (lane == 0) {
@@ -175,8 +158,8 @@ __device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, u
     }
     // objective = U[N][Mp]
 #pragma unroll
-    for (int j = 0; j < kCMax; ++j) {
-      if (j < C && j * nthr + warp * 32 + lane == Mp) *s_obj = v[j];
+    for (int j = 0; j < CC; ++j) {
+      if (j * nthr + warp * 32 + lane == Mp) *s_obj = v[j];
     }
   }
   __syncthreads();
@@ -192,6 +175,109 @@ __device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, u
   }
   __syncthreads();
   return *s_obj;
+}
+
+// Single warp, contiguous columns per lane (rows of up to 32 * 40 columns:
+// the training shapes and the 1024-item sweep): lane l holds columns
+// m = l * CL + j.  Column m-1 is the lane's own previous register except for
+// j = 0 (one shuffle per item), so an item costs one shuffle plus CL
+// independent add / compare / select — no shared-memory exchange, no barrier.
+// The same fp64 adds in the same order as the reference; decision bits are a
+// 64-bit mask per (item, lane): bits word pair 2 * (32 i + l).
+constexpr int kLaneColsMax = 40;
+template <int CL>
+__device__ double dp_row_lane(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
+                              double* s_obj) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t* mb = reinterpret_cast<uint64_t*>(bits);
+  if (warp == 0) {
+    double v[CL];
+    bool okc[CL];
+#pragma unroll
+    for (int j = 0; j < CL; ++j) {
+      const int m = lane * CL + j;
+      v[j] = 0.0;
+      okc[j] = (wt == 0) ? (m == 0) : (m >= 1 && m <= Mp);
+    }
+    for (int i = 0; i < N; ++i) {
+      const double s = s_scores[i];
+      double left = __shfl_up_sync(0xffffffffu, v[CL - 1], 1);  // column l*CL - 1, before this item
+      if (lane == 0) left = 0.0;
+      // decision bits into 4 independent accumulators (short OR chains)
+      uint64_t acc4[4] = {0, 0, 0, 0};
+      if (wt == 0) {  // zero weight: take reads the same column (only m == 0 may take)
+#pragma unroll
+        for (int j = 0; j < CL; ++j) {
+          const double take = __dadd_rn(v[j], s);
+          const bool d = okc[j] && (take > v[j]);
+          if (d) v[j] = take;
+          acc4[j & 3] |= (uint64_t)d << j;
+        }
+      } else {
+#pragma unroll
+        for (int j = CL - 1; j >= 1; --j) {  // downwards: v[j-1] is still the previous item's
+          const double take = __dadd_rn(v[j - 1], s);
+          const bool d = okc[j] && (take > v[j]);  // scheduler.cpp:167 strict >
+          if (d) v[j] = take;
+          acc4[j & 3] |= (uint64_t)d << j;
+        }
+        const double take = __dadd_rn(left, s);
+        const bool d = okc[0] && (take > v[0]);
+        if (d) v[0] = take;
+        acc4[0] |= (uint64_t)d;
+      }
+      mb[(size_t)i * 32 + lane] = (acc4[0] | acc4[1]) | (acc4[2] | acc4[3]);
+    }
+#pragma unroll
+    for (int j = 0; j < CL; ++j)
+      if (lane * CL + j == Mp) *s_obj = v[j];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
+    for (int i = N; i > 0; --i) {
+      const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
+      const unsigned b = (unsigned)((mb[(size_t)(i - 1) * 32 + col / CL] >> (col % CL)) & 1u);
+      sel[i - 1] = (uint8_t)b;
+      if (b && wt > 0) mm -= 1;
+    }
+  }
+  __syncthreads();
+  return *s_obj;
+}
+
+// Count-compressed 0/1 knapsack of one row (all threads of the block call it
+// with block-uniform arguments).  s_scores: the row's N scores in shared
+// memory.  Writes sel[i] in {0,1} (shared or global) and returns the
+// objective T[N][cap] in thread 0.
+__device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, uint32_t* bits, double* xch,
+                               uint8_t* sel, double* s_obj) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Mp = (wt == 0) ? 0 : min(cap / wt, N);  // last stored column
+  const int ncols = Mp + 1;
+  int nw, C;
+  row_geometry(ncols, &nw, &C);
+  if (ncols <= 32) return dp_row_warp<1>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+  if (ncols <= 32 * kLaneColsMax) {
+    const int c = (ncols + 31) / 32;  // columns per lane, rounded up to an instantiated width
+    if (c <= 2) return dp_row_lane<2>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    if (c <= 4) return dp_row_lane<4>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    if (c <= 8) return dp_row_lane<8>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    if (c <= 16) return dp_row_lane<16>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    if (c <= 24) return dp_row_lane<24>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    if (c <= 33) return dp_row_lane<33>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+    return dp_row_lane<kLaneColsMax>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
+  }
+  switch (C) {  // compile-time columns per thread
+    case 1: return dp_row_block<1>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 2: return dp_row_block<2>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 3: return dp_row_block<3>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 4: return dp_row_block<4>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 5: return dp_row_block<5>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 6: return dp_row_block<6>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 7: return dp_row_block<7>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    default: return dp_row_block<8>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+  }
 }
 
 struct KnapsackArgs {
@@ -575,8 +661,14 @@ void launch_brute_force(const double* bwd, const double* fwd, const int32_t* cf,
   D2FT_CUDA(cudaGetLastError());
 }
 
+// decision-bit words per item: the block path's row words, or a 64-bit mask
+// per lane for the single-warp lane path
+int bits_words_per_item(int max_cols) {
+  const int w = (max_cols + 31) / 32 + 8;
+  return max_cols <= 32 * kLaneColsMax ? (w > 64 ? w : 64) : w;
+}
 size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
-  const int words = (max_cols + 31) / 32 + 8;
+  const int words = bits_words_per_item(max_cols);
   const size_t Np = (size_t)((N + 15) & ~15);
   const size_t base = (size_t)N * 8 + 2 * 8 * kCMax * 8 + 16 + 2 * Np;
   const size_t with_bits = base + (size_t)N * words * 4;
@@ -589,7 +681,7 @@ size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
 }
 
 size_t knapsack_global_bits_words(int K, int N, int max_cols) {
-  const int words = (max_cols + 31) / 32 + 8;
+  const int words = bits_words_per_item(max_cols);
   return (size_t)K * N * words;
 }
 
@@ -613,7 +705,7 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   if (lists) A.lists = *lists;
   A.ws = ws;
   A.validate = validate;
-  A.words_max = (max_cols + 31) / 32 + 8;
+  A.words_max = bits_words_per_item(max_cols);
   size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
   // room to stage the K x N table for the last CTA's column lists (<= 48 KB)
   const size_t kn = (size_t)K * N;
@@ -629,7 +721,10 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
     D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
     attr_done = true;
   }
-  knapsack_kernel<<<K, kThreads, smem, stream>>>(A);
+  // rows that fit the single-warp DP need one warp (more CTAs per SM, the
+  // DP's registers only for 32 threads); wider rows use the 8-warp block path
+  const int threads = max_cols <= 32 * kLaneColsMax ? 32 : kThreads;
+  knapsack_kernel<<<K, threads, smem, stream>>>(A);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
   if (lists && !A.cols_in_kernel) {  // column lists over many CTAs (one thread per cell)
@@ -654,13 +749,13 @@ void launch_dp_const(const double* scores, const int32_t* row_wt, const int32_t*
   A.sel = sel;
   A.obj = obj;
   A.ws = ws;
-  A.words_max = (max_cols + 31) / 32 + 8;
+  A.words_max = bits_words_per_item(max_cols);
   const size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
   if (!A.bits_in_smem)
     D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(nrows, N, max_cols), kState,
                  "dp_search: global decision-bit workspace too small");
   D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-  dp_const_kernel<<<nrows, kThreads, smem, stream>>>(A);
+  dp_const_kernel<<<nrows, max_cols <= 32 * kLaneColsMax ? 32 : kThreads, smem, stream>>>(A);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
