@@ -21,6 +21,7 @@ int d2ft_test_gemm_planes(const uint16_t* A, const uint16_t* X, int M, int T, in
 /* Tokens as K: D[m][n] = sum_p sum_{t<T} XT[p][m][t] YT[p][n][t]; pitch TP >= T. */
 int d2ft_test_gemm_tokenk(const uint16_t* XT, const uint16_t* YT, int M, int N, int T, int TP, int P, float* D);
 /* ms per launch of a dense M x N x K GEMM (BN = 256), CUDA-event timed. */
+int d2ft_test_gemm_bench_pair(int M, int K, int variant, int iters, double* ms_per);
 int d2ft_test_gemm_bench(int M, int N, int K, int iters, double* ms_per);
 
 #ifdef __cplusplus

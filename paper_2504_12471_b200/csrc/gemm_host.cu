@@ -199,6 +199,7 @@ struct DensePairProb {
   }
   __device__ void row_begin(const Tile&, int, Row&) const {}
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    if (!D) return;  // throughput runs: accumulator drained, nothing stored
     const int m = c.mt * 128 + row;
     if (m >= M) return;
 #pragma unroll
@@ -232,6 +233,7 @@ struct DenseMNProb {
   }
   __device__ void row_begin(const Tile&, int, Row&) const {}
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    if (!D) return;
     const int m = c.mt * 128 + row;
     if (m >= M) return;
 #pragma unroll
@@ -374,6 +376,55 @@ int d2ft_test_gemm_tokenk(const uint16_t* XT, const uint16_t* YT, int M, int N, 
     launch_gemm<TokenKProb<256>, S>(a, b, TokenKProb<256>{M, N, T, P, dD.p}, 0, nullptr);
     D2FT_CUDA(cudaDeviceSynchronize());
     D2FT_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Times `iters` launches of a dense M x N x K GEMM shaped like the step's
+// tokens-as-N GEMMs (N = 208, K-major A and B, CTA pairs): variant 0 = B
+// multicast (G1's config), 1 = pair UMMA (cta_group::2); ms per launch.
+int d2ft_test_gemm_bench_pair(int M, int K, int variant, int iters, double* ms_per) {
+  return guarded([&] {
+    const int N = 208;
+    Dev<uint16_t> dA((size_t)M * K), dB((size_t)N * K);
+    Dev<float> dD((size_t)M * N);
+    D2FT_CUDA(cudaMemset(dA.p, 0x3c, (size_t)M * K * 2));
+    D2FT_CUDA(cudaMemset(dB.p, 0x3c, (size_t)N * K * 2));
+    CUtensorMap a = make_tmap_bf16_3d(dA.p, K, M, 1, (uint64_t)K * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap b = make_tmap_bf16_3d(dB.p, K, N, 1, (uint64_t)K * 2, (uint64_t)K * N * 2, 104);
+    DensePairProb<208> prob{M, N, K, (variant >= 2) ? nullptr : dD.p};
+    // 4: A MN-major ([K][M]), 5: B MN-major ([K][N]), both pair UMMA, no stores
+    CUtensorMap amn = make_tmap_bf16_3d(dA.p, M, K, 1, (uint64_t)M * 2, (uint64_t)K * M * 2, 64);
+    CUtensorMap bmn = make_tmap_bf16_3d(dB.p, N, K, 1, (uint64_t)N * 2, (uint64_t)K * N * 2, 64);
+    DenseMNProb<208> mnp{M, N, K, 1, nullptr};
+    // 6 / 7: MN-major B with N = 256 / 128 (whole 64-token blocks per CTA); 8: MN-major B multicast
+    Dev<uint16_t> dB2((size_t)256 * K);
+    D2FT_CUDA(cudaMemset(dB2.p, 0x3c, (size_t)256 * K * 2));
+    CUtensorMap bmn256 = make_tmap_bf16_3d(dB2.p, 256, K, 1, (uint64_t)256 * 2, (uint64_t)K * 256 * 2, 64);
+    DenseMNProb<256> mnp256{M, 256, K, 1, nullptr};
+    DenseMNProb<128> mnp128{M, 128, K, 1, nullptr};
+    const int v = variant;
+    auto run = [&]() {
+      if (v == 4) launch_gemm<DensePairProb<208>, GemmShape<208, 6, 1, 4, 2, 0, 1, 1>>(amn, b, prob, 0, nullptr);
+      else if (v == 5) launch_gemm<DenseMNProb<208>, GemmShape<208, 6, 1, 4, 2, 1, 0, 1>>(a, bmn, mnp, 0, nullptr);
+      else if (v == 6) launch_gemm<DenseMNProb<256>, GemmShape<256, 6, 1, 4, 2, 1, 0, 1>>(a, bmn256, mnp256, 0, nullptr);
+      else if (v == 7) launch_gemm<DenseMNProb<128>, GemmShape<128, 8, 1, 4, 2, 1, 0, 1>>(a, bmn256, mnp128, 0, nullptr);
+      else if (v == 8) launch_gemm<DenseMNProb<208>, GemmShape<208, 4, 1, 4, 2, 1, 0, 0>>(a, bmn, mnp, 0, nullptr);
+      else if (v == 1 || v == 3) launch_gemm<DensePairProb<208>, GemmShape<208, 6, 1, 4, 2, 0, 0, 1>>(a, b, prob, 0, nullptr);
+      else launch_gemm<DensePairProb<208>, GemmShape<208, 5, 1, 4, 2>>(a, b, prob, 0, nullptr);
+    };
+    for (int i = 0; i < 3; ++i) run();
+    cudaEvent_t e0, e1;
+    D2FT_CUDA(cudaEventCreate(&e0));
+    D2FT_CUDA(cudaEventCreate(&e1));
+    D2FT_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) run();
+    D2FT_CUDA(cudaEventRecord(e1));
+    D2FT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    D2FT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 
