@@ -341,6 +341,25 @@ def run_ours(args):
                      "cost_units_max_over_mean": round(unit_ratio, 4),
                      "exchange_ms_per_step": round(phases.get("exchange", 0.0), 3),
                      "exchange_bytes_per_step": 2 * L * B * T * D * 4}
+    # ---- schedule metrics of this batch on the GPU (cost_sim.cpp:109-172 with
+    # the MEASURED per-device busy time in place of the calibrated table): the
+    # rows each rank owns (head h of every block -> rank h % N) are grouped so
+    # the reference's in-order row-to-device mapping applies
+    from paper_2504_12471_b200 import cost_sim as CSIM
+    gcodes = glob if dist else codes_exp
+    order = [k for r in range(world) for k in range(K) if (k % H) % world == r]
+    profs = []
+    for r in range(world):
+        p = CSIM.DeviceProfile.standard(r)
+        p.memory_units = sum(1 for k in range(K) if (k % H) % world == r)
+        profs.append(p)
+    bm = CSIM.simulate_batch(S.ScheduleTable(K, B, gcodes[order]), profs, cm,
+                             S.Capacities(capf[order].tolist(), capo[order].tolist()),
+                             busy_ms=bl if dist else [ms_step])
+    sched_metrics = {"compute_fraction": bm.compute_fraction, "comm_fraction": bm.comm_fraction,
+                     "workload_variance": bm.workload_variance, "row_workload_variance": bm.row_workload_variance,
+                     "makespan_ms": round(bm.makespan_ms, 4), "imbalance_residual": bm.imbalance_residual,
+                     "busy": "measured per device (step minus exchange)"}
     # ---- end to end through the C-ABI with pinned host buffers
     lib.d2ft_host_alloc.restype = C.c_void_p
     nbytes = x.nbytes
@@ -461,6 +480,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cb,
         }
+        line["schedule_metrics"] = sched_metrics
         if part_info:
             line["partition"] = part_info
         if vitl:

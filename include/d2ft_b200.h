@@ -111,6 +111,94 @@ int d2ft_sched_bench(d2ft_sched* s, const double* bwd, const double* fwd, const 
 int d2ft_sched_lists(d2ft_sched* s, int32_t** fwd_idx, int32_t** fwd_cnt, int32_t** full_idx, int32_t** full_cnt,
                      int32_t** act_heads, int32_t** act_cnt, int32_t** full_heads, int32_t** full_hcnt);
 
+
+/* ------------------------------------------------------------------ schedule metrics
+ * cost_sim.hpp:57-90 (BatchMetrics, compute_cost_fraction, comm_cost_fraction,
+ * workload_variance, simulate_batch), evaluated by one CUDA kernel over the
+ * code table; bit-identical to the reference built without FMA contraction.
+ * Field order is the order of the d2ft_schedule_metrics_device out6 array. */
+typedef struct d2ft_batch_metrics {
+  double compute_fraction;      /* compute_cost_fraction (cost_sim.cpp:71-81) */
+  double comm_fraction;         /* comm_cost_fraction (cost_sim.cpp:83-93) */
+  double workload_variance;     /* simulate_batch: over devices (cost_sim.cpp:159-166); 0 without devices */
+  double makespan_ms;           /* max per-device busy time */
+  double imbalance_residual;    /* || units_p - sum(cap_full + cap_fwd) || over devices (0 without capacities) */
+  double row_workload_variance; /* workload_variance(): over schedule rows (cost_sim.cpp:95-107) */
+} d2ft_batch_metrics;
+
+/* DeviceProfile::time_ms (cost_sim.cpp:40-69): table of n entries (counts
+ * strictly increasing), exact / interpolated / extrapolated busy ms. */
+int d2ft_device_time_ms(const int32_t* counts, const double* full_ms, const double* fwd_ms, int n, int count,
+                        int full, double* out);
+
+/* simulate_batch (cost_sim.hpp:86-89, cost_sim.cpp:109-172) and the three
+ * standalone metrics in one launch.  Host pointers; synchronous.
+ *   codes K x N; cf/cb per row (CostModel::cf/cb).
+ *   n_dev devices (0: fractions and row variance only), memory_units[n_dev]
+ *   consecutive rows each (the reference's in-order row-to-device mapping).
+ *   Busy time per device: busy_ms[n_dev] MEASURED (e.g. the head partition's
+ *   per-rank busy time) when non-NULL, else the timing table of device p:
+ *   entries [table_off[p], table_off[p+1]) of table_count / table_full_ms /
+ *   table_fwd_ms (DeviceProfile::timing_table).
+ *   cap_full/cap_fwd (K, may be NULL): Capacities for the imbalance residual.
+ * Outputs: out; per_device_busy_ms[n_dev] and row_counts[K x 3] (n_full,
+ * n_fwd, n_shortcut per row; ScheduleTable::row_counts) may be NULL. */
+int d2ft_schedule_metrics(const uint8_t* codes, int K, int N, const int32_t* cf, const int32_t* cb, int n_dev,
+                          const int32_t* memory_units, const int32_t* table_off, const int32_t* table_count,
+                          const double* table_full_ms, const double* table_fwd_ms, const double* busy_ms,
+                          const int32_t* cap_full, const int32_t* cap_fwd, d2ft_batch_metrics* out,
+                          double* per_device_busy_ms, int32_t* row_counts);
+/* Same on device pointers (e.g. the scheduler context's codes), no
+ * allocation, no synchronisation: out6 = the six d2ft_batch_metrics fields
+ * in order; err_dev (zeroed by the caller) receives 2 on an invalid code.
+ * The caller validates profiles/capacities (d2ft_schedule_metrics does). */
+int d2ft_schedule_metrics_device(const uint8_t* codes, int K, int N, const int32_t* cf, const int32_t* cb, int n_dev,
+                                 const int32_t* memory_units, const int32_t* table_off, const int32_t* table_count,
+                                 const double* table_full_ms, const double* table_fwd_ms, const double* busy_ms,
+                                 const int32_t* cap_full, const int32_t* cap_fwd, double* out6,
+                                 double* per_device_busy_ms, int32_t* row_counts, int32_t* err_dev, void* stream);
+
+
+/* ------------------------------------------------------------------ artifact formats
+ * serialize.hpp:21-53 / serialize.cpp:17-222: the reference pipeline's JSON
+ * and CSV wire formats (host code; no GPU).  Text outputs go to a caller
+ * buffer of `cap` bytes, NUL-terminated; *len = text length; status 6 (size)
+ * with *len set when cap <= *len, so callers can size and retry.  JSON
+ * layout is nlohmann::json::dump(2) (sorted keys, 2-space indent, shortest
+ * round-trip doubles); metric ids are the Metric enum order of
+ * scoring.hpp:18-23 (0 fisher_information .. 3 taylor_importance).
+ * Readers take (text, n) and fail with the reference's messages. */
+int d2ft_format_double(double v, char* buf, size_t cap, size_t* len);                       /* serialize.cpp:17-21 */
+int d2ft_json_double(double v, char* buf, size_t cap, size_t* len);                         /* nlohmann layout */
+int d2ft_score_table_to_json(const double* fwd, const double* bwd, int K, int N, int fwd_metric, int bwd_metric,
+                             char* buf, size_t cap, size_t* len);                          /* serialize.cpp:66-75 */
+/* fills K, N and the metric ids, then the K x N tables if cap_cells >= K*N (else status 6) */
+int d2ft_score_table_from_json(const char* text, size_t n, int* K, int* N, int* fwd_metric, int* bwd_metric,
+                               double* fwd, double* bwd, size_t cap_cells);                /* serialize.cpp:77-88 */
+int d2ft_score_table_to_csv(const double* fwd, const double* bwd, int K, int N, char* buf, size_t cap,
+                            size_t* len);                                                  /* serialize.cpp:90-99 */
+int d2ft_schedule_table_to_json(const uint8_t* codes, int K, int N, char* buf, size_t cap,
+                                size_t* len);                                              /* serialize.cpp:101-113 */
+int d2ft_schedule_table_from_json(const char* text, size_t n, int* K, int* N, uint8_t* codes,
+                                  size_t cap_cells);                                       /* serialize.cpp:115-135 */
+int d2ft_schedule_table_to_csv(const uint8_t* codes, int K, int N, char* buf, size_t cap,
+                               size_t* len);                                               /* serialize.cpp:137-146 */
+int d2ft_batch_metrics_to_json(const d2ft_batch_metrics* m, const double* per_device_busy_ms, int n_dev,
+                               const char* run_id, const char* method, char* buf, size_t cap,
+                               size_t* len);                                               /* serialize.cpp:148-160 */
+int d2ft_batch_metrics_csv_header(char* buf, size_t cap, size_t* len);                      /* serialize.cpp:162-165 */
+int d2ft_batch_metrics_to_csv_row(const d2ft_batch_metrics* m, const char* run_id, const char* method, char* buf,
+                                  size_t cap, size_t* len);                                /* serialize.cpp:167-173 */
+/* TrainHistory (trainer.hpp:82-92) as parallel arrays of n epochs */
+int d2ft_history_to_csv(const int32_t* epoch, const double* loss, const double* top1, const double* compute_fraction,
+                        const double* comm_fraction, int n, char* buf, size_t cap, size_t* len); /* serialize.cpp:175-182 */
+int d2ft_history_to_json(const int32_t* epoch, const double* loss, const double* top1, const double* compute_fraction,
+                         const double* comm_fraction, int n, char* buf, size_t cap, size_t* len); /* serialize.cpp:184-198 */
+int d2ft_history_from_csv(const char* text, size_t n_text, int32_t* epoch, double* loss, double* top1,
+                          double* compute_fraction, double* comm_fraction, int cap, int* n); /* serialize.cpp:200-222 */
+int d2ft_atomic_write_file(const char* path, const char* data, size_t n);                  /* serialize.cpp:23-34 */
+int d2ft_read_file(const char* path, char* buf, size_t cap, size_t* len);                   /* serialize.cpp:36-42 */
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,6 +12,7 @@
 //               at proj/core/src/trainer.cpp:247-268 (composed here with the
 //               same public calls, in the same order)
 //   rng         proj/core/include/d2ft/rng.hpp:16-59
+//   cost_sim    proj/core/include/d2ft/cost_sim.hpp:18-103
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -19,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "d2ft/cost_sim.hpp"
 #include "d2ft/data.hpp"
 #include "d2ft/model.hpp"
 #include "d2ft/rng.hpp"
@@ -428,6 +430,95 @@ int ref_make_dataset(int num_samples, int C, int d, int T, double noise, uint64_
       std::memcpy(samples + static_cast<std::size_t>(i) * T * d, ds.samples[i].data.data(),
                   static_cast<std::size_t>(T) * d * sizeof(double));
       labels[i] = ds.labels[i];
+    }
+  });
+}
+
+// ---------------------------------------------------------------- cost_sim
+int ref_time_ms(const int32_t* cnt, const double* full_ms, const double* fwd_ms, int n, int count, int full,
+                double* out) {
+  return guarded([&] {
+    DeviceProfile p;
+    for (int j = 0; j < n; ++j) p.timing_table.push_back({cnt[j], full_ms[j], fwd_ms[j]});
+    p.validate();
+    *out = p.time_ms(count, full != 0);
+  });
+}
+
+// out6 = compute_fraction, comm_fraction, workload_variance (devices),
+// makespan_ms, imbalance_residual, workload_variance() over rows.
+// n_dev == 0: only the three standalone metrics.
+int ref_schedule_metrics(const uint8_t* codes, int K, int N, int cf, int cb, const int32_t* cf_dev,
+                         const int32_t* cb_dev, int n_dev, const int32_t* mu, const int32_t* toff, const int32_t* tcnt,
+                         const double* tfull, const double* tfwd, const int32_t* cap_full, const int32_t* cap_fwd,
+                         double* out6, double* busy) {
+  return guarded([&] {
+    ScheduleTable t(K, N);
+    for (size_t c = 0; c < static_cast<size_t>(K) * N; ++c) t.codes[c] = codes[c];
+    CostModel cm = make_cost(cf, cb, cf_dev, cb_dev, K);
+    out6[0] = compute_cost_fraction(t, cm);
+    out6[1] = comm_cost_fraction(t);
+    out6[5] = workload_variance(t, cm);
+    out6[2] = out6[3] = out6[4] = 0.0;
+    if (n_dev == 0) return;
+    std::vector<DeviceProfile> profiles;
+    for (int p = 0; p < n_dev; ++p) {
+      DeviceProfile d;
+      d.device_id = p;
+      d.memory_units = mu[p];
+      for (int j = toff[p]; j < toff[p + 1]; ++j) d.timing_table.push_back({tcnt[j], tfull[j], tfwd[j]});
+      profiles.push_back(std::move(d));
+    }
+    Capacities caps;
+    if (cap_full) {
+      caps.full.assign(cap_full, cap_full + K);
+      caps.fwd.assign(cap_fwd, cap_fwd + K);
+    }
+    BatchMetrics m = simulate_batch(t, profiles, cm, cap_full ? &caps : nullptr);
+    out6[0] = m.compute_fraction;
+    out6[1] = m.comm_fraction;
+    out6[2] = m.workload_variance;
+    out6[3] = m.makespan_ms;
+    out6[4] = m.imbalance_residual;
+    for (int p = 0; p < n_dev; ++p) busy[p] = m.per_device_busy_ms[p];
+  });
+}
+
+// build_hetero_profiles (cost_sim.hpp:79-81): profiles as (memory_units,
+// fast) pairs, budget overrides as (device, n_full, n_fwd) triples.
+int ref_build_hetero_profiles(int mode, int count, int units, int max_prof, int* n_prof, int32_t* mu, int32_t* fast,
+                              int32_t* ovr, int* n_ovr, int32_t* budget2) {
+  return guarded([&] {
+    HeteroSetup s = build_hetero_profiles(mode == 0 ? HeteroMode::Memory : HeteroMode::Compute, count, units);
+    *n_prof = static_cast<int>(s.profiles.size());
+    if (*n_prof > max_prof) throw size_error("too many profiles");
+    for (int p = 0; p < *n_prof; ++p) {
+      mu[p] = s.profiles[p].memory_units;
+      fast[p] = s.profiles[p].speed_class == DeviceProfile::Speed::Fast;
+    }
+    *n_ovr = static_cast<int>(s.budget.overrides.size());
+    for (int i = 0; i < *n_ovr && i < max_prof; ++i) {
+      ovr[3 * i] = s.budget.overrides[i].device;
+      ovr[3 * i + 1] = s.budget.overrides[i].n_full;
+      ovr[3 * i + 2] = s.budget.overrides[i].n_fwd;
+    }
+    budget2[0] = s.budget.n_full;
+    budget2[1] = s.budget.n_fwd;
+  });
+}
+
+// lora_{compute,comm}_reference_points (cost_sim.hpp:96-101): 3 rows of
+// (n_full, n_fwd, n_shortcut, computed_pct, nominal_pct, discrepancy).
+int ref_lora_reference_points(int comm, int32_t* counts9, double* pct6, int32_t* disc3) {
+  return guarded([&] {
+    std::vector<ReferencePoint> pts = comm ? lora_comm_reference_points() : lora_compute_reference_points();
+    for (int i = 0; i < 3; ++i) {
+      counts9[3 * i] = pts[i].n_full;
+      counts9[3 * i + 1] = pts[i].n_fwd;
+      counts9[3 * i + 2] = pts[i].n_shortcut;
+      pct6[2 * i] = pts[i].computed_pct;
+      pct6[2 * i + 1] = pts[i].nominal_pct;
+      disc3[i] = pts[i].discrepancy ? 1 : 0;
     }
   });
 }
