@@ -256,6 +256,13 @@ class RefModel:
         a = np.ascontiguousarray(flat, np.float64)
         self.lib.ref_model_set_params(self.h, _ptr(a))
 
+    def attach_lora(self, rank, scaling):
+        rc = self.lib.ref_model_attach_lora(C.c_void_p(self.h), _I(rank), _D(scaling))
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+        self.lib.ref_model_flat_count.restype = C.c_int64
+        self.n = int(self.lib.ref_model_flat_count(C.c_void_p(self.h)))
+
     def velocity(self):
         out = np.empty(self.n, np.float64)
         self.lib.ref_model_get_velocity(self.h, _ptr(out))

@@ -122,9 +122,17 @@ def softmax_rows(s):
     return e / e.sum(axis=1, keepdims=True)
 
 
-def block_contribution(cfg, blk, h, xn, cache=None):
-    """model.cpp:197-241 (h is 0-based here; b2 offset = h*d/H, model.cpp:222)."""
+def block_contribution(cfg, blk, h, xn, cache=None, ad=None, scaling=0.0):
+    """model.cpp:197-241 (h is 0-based here; b2 offset = h*d/H, model.cpp:222).
+    ad: LoRA adapters of the block subnet (model.cpp:204-211)."""
     q, k, v = xn @ blk["wq"], xn @ blk["wk"], xn @ blk["wv"]
+    if ad is not None:
+        pq, pk, pv = xn @ ad["down_q"], xn @ ad["down_k"], xn @ ad["down_v"]
+        q = q + scaling * (pq @ ad["up_q"])
+        k = k + scaling * (pk @ ad["up_k"])
+        v = v + scaling * (pv @ ad["up_v"])
+        if cache is not None:
+            cache.update(pq=pq, pk=pk, pv=pv)
     probs = softmax_rows((q @ k.T) * (1.0 / math.sqrt(cfg.dh)))
     headout = probs @ v
     contrib = headout @ blk["wo"]
@@ -139,18 +147,23 @@ def block_contribution(cfg, blk, h, xn, cache=None):
     return contrib
 
 
-def contribution_backward(cfg, blk, h, c, dc, dxn, gb):
-    """model.cpp:243-303 (non-LoRA)."""
+def contribution_backward(cfg, blk, h, c, dc, dxn, gb, ad=None, scaling=0.0, ga=None):
+    """model.cpp:243-303; with adapters (ad, gradients into ga) the base
+    tensors get no gradient (model.cpp:248-263, 273-289)."""
+    lora = ad is not None
     dg = dc @ blk["w2"].T
-    gb["w2"] += c["g"].T @ dc
     w = cfg.d // cfg.H
-    gb["b2"] += dc[:, h * w:(h + 1) * w].sum(axis=0)
+    if not lora:
+        gb["w2"] += c["g"].T @ dc
+        gb["b2"] += dc[:, h * w:(h + 1) * w].sum(axis=0)
     dz = dg * gelu_grad(c["z"])
-    gb["w1"] += c["xn"].T @ dz
-    gb["b1"] += dz.sum(axis=0)
+    if not lora:
+        gb["w1"] += c["xn"].T @ dz
+        gb["b1"] += dz.sum(axis=0)
     dxn += dz @ blk["w1"].T
     dheadout = dc @ blk["wo"].T
-    gb["wo"] += c["headout"].T @ dc
+    if not lora:
+        gb["wo"] += c["headout"].T @ dc
     dprobs = dheadout @ c["v"].T
     dv = c["probs"].T @ dheadout
     dot = (c["probs"] * dprobs).sum(axis=1, keepdims=True)
@@ -158,19 +171,35 @@ def contribution_backward(cfg, blk, h, c, dc, dxn, gb):
     sc = 1.0 / math.sqrt(cfg.dh)
     dq = (dscores @ c["k"]) * sc
     dk = (dscores.T @ c["q"]) * sc
-    for dproj, wname in ((dq, "wq"), (dk, "wk"), (dv, "wv")):
-        gb[wname] += c["xn"].T @ dproj
+    for dproj, wname, x in ((dq, "wq", "q"), (dk, "wk", "k"), (dv, "wv", "v")):
+        if lora:  # projection_backward, model.cpp:273-289
+            ga["up_" + x] += scaling * (c["p" + x].T @ dproj)
+            dp = scaling * (dproj @ ad["up_" + x].T)
+            ga["down_" + x] += c["xn"].T @ dp
+            dxn += dp @ ad["down_" + x].T
+        else:
+            gb[wname] += c["xn"].T @ dproj
         dxn += dproj @ blk[wname].T
 
 
-def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trace=None):
+def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trace=None, lora=None):
     """SubnetModel::forward_backward, model.cpp:416-520.
 
     Returns (loss, grads_flat, engaged[K+2]).  `trace`, if a dict, receives the
-    block inputs per sample (for activation-level parity checks)."""
+    block inputs per sample (for activation-level parity checks).
+    lora = (rank, scaling, adapters_flat): adapters attached (model.cpp:165-195);
+    then only the adapters get gradients and the result is
+    (loss, adapter_grads_flat, engaged)."""
     p = unpack(cfg, flat)
     grads = np.zeros_like(flat)
     g = unpack(cfg, grads)
+    ads = gads = None
+    scaling = 0.0
+    if lora is not None:
+        rank, scaling, aflat = lora
+        ads = lora_unpack(cfg, rank, aflat)
+        agrads = np.zeros_like(aflat)
+        gads = lora_unpack(cfg, rank, agrads)
     column = list(column)
     engaged = np.zeros(cfg.K + 2, dtype=np.uint8)
     engaged[0] = engaged[-1] = 1
@@ -196,7 +225,7 @@ def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trac
                 if op == 3:
                     continue
                 cache = {} if op == 1 else None
-                acc += block_contribution(cfg, p["blocks"][r], h, xn, cache)
+                acc += block_contribution(cfg, p["blocks"][r], h, xn, cache, ads[r] if ads else None, scaling)
                 caches[r] = cache
             xs.append(acc)
         if trace is not None:
@@ -228,14 +257,80 @@ def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trac
                 r = l * H + h
                 if column[r] != 1:
                     continue
-                contribution_backward(cfg, p["blocks"][r], h, caches[r], dx, dxn, g["blocks"][r])
+                contribution_backward(cfg, p["blocks"][r], h, caches[r], dx, dxn, g["blocks"][r],
+                                      ads[r] if ads else None, scaling, gads[r] if gads else None)
                 anyf = True
             if anyf:
                 dx = dx + layer_norm_backward(xin, dxn)
         g["w_embed"] += inp.T @ dx
         g["b_embed"] += dx.sum(axis=0)
         g["pos"] += dx
+    if lora is not None:
+        return loss, agrads, engaged
     return loss, grads, engaged
+
+
+# ---------------------------------------------------------------- LoRA
+def lora_block_size(cfg: Config, rank: int) -> int:
+    return 3 * (cfg.d * rank + rank * cfg.dh)
+
+
+def lora_unpack(cfg: Config, rank: int, aflat: np.ndarray):
+    """Views per block subnet in visit_tensors order (model.hpp:139-146):
+    down_q[d,r], up_q[r,dh], down_k, up_k, down_v, up_v."""
+    d, dh = cfg.d, cfg.dh
+    out, off = [], 0
+    for _ in range(cfg.K):
+        a = {}
+        for x in "qkv":
+            a["down_" + x] = aflat[off:off + d * rank].reshape(d, rank)
+            off += d * rank
+            a["up_" + x] = aflat[off:off + rank * dh].reshape(rank, dh)
+            off += rank * dh
+        out.append(a)
+    assert off == aflat.size
+    return out
+
+
+def lora_init(cfg: Config, rank: int, seed: int) -> np.ndarray:
+    """attach_lora (model.cpp:165-195): down = 0; up_q, up_k, up_v ~ N(0, 1/rank)
+    from make_rng(seed, 0x10000 + subnet index), block subnet (l,h) at index
+    1 + l*H + h (partition order, model.cpp:140-156)."""
+    from oracle import lib as O
+    aflat = np.zeros(cfg.K * lora_block_size(cfg, rank))
+    ads = lora_unpack(cfg, rank, aflat)
+    sd = 1.0 / math.sqrt(rank)
+    for r in range(cfg.K):
+        gs = O.gaussian_stream(seed, 0x10000 + 1 + r, 3 * rank * cfg.dh)
+        for i, x in enumerate("qkv"):
+            ads[r]["up_" + x][...] = (sd * gs[i * rank * cfg.dh:(i + 1) * rank * cfg.dh]).reshape(rank, cfg.dh)
+    return aflat
+
+
+def train_batch_lora(cfg: Config, flat, rank, scaling, aflat, avel, inputs, labels, codes, mbs, lr, momentum):
+    """Trainer batch body with adapters attached (trainer.cpp:247-268,
+    sgd_momentum_step over visit_trainable = adapters only, trainer.cpp:124-133);
+    updates aflat / avel in place."""
+    codes = np.asarray(codes, dtype=np.uint8).reshape(cfg.K, -1)
+    n_mb = codes.shape[1]
+    inv_mb = 1.0 / n_mb
+    accum = np.zeros_like(aflat)
+    touched = np.zeros(cfg.K, dtype=bool)
+    batch_loss = 0.0
+    for j in range(n_mb):
+        loss, ga, eng = forward_backward(cfg, flat, inputs[j * mbs:(j + 1) * mbs], labels[j * mbs:(j + 1) * mbs],
+                                         codes[:, j], lora=(rank, scaling, aflat))
+        batch_loss += loss * inv_mb
+        accum += ga * inv_mb
+        touched |= eng[1:-1].astype(bool)
+    bs = lora_block_size(cfg, rank)
+    for r in range(cfg.K):
+        if not touched[r]:
+            continue
+        a, b = r * bs, (r + 1) * bs
+        avel[a:b] = momentum * avel[a:b] + accum[a:b]
+        aflat[a:b] -= lr * avel[a:b]
+    return batch_loss, touched
 
 
 def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, labels, codes, mbs,

@@ -222,6 +222,22 @@ void ref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
 
 uint64_t ref_model_param_count(void* h) { return static_cast<RefModel*>(h)->model.parameter_count(); }
 
+// attach_lora (model.cpp:165-195); velocities are re-made so they carry the
+// adapter slots sgd_momentum_step visits in LoRA mode
+int ref_model_attach_lora(void* h, int rank, double scaling) {
+  return guarded([&] {
+    auto* m = static_cast<RefModel*>(h);
+    m->model.attach_lora(rank, scaling);
+    m->velocity.clear();
+    for (const Subnet& s : m->model.subnets()) m->velocity.push_back(zeros_like(s));
+  });
+}
+
+// doubles in the canonical flat vector, adapters included (parameter_bytes(true))
+int64_t ref_model_flat_count(void* h) {
+  return static_cast<int64_t>(static_cast<RefModel*>(h)->model.parameter_bytes(true).size() / sizeof(double));
+}
+
 // canonical order (model.hpp:117-153), identical to parameter_bytes()
 void ref_model_get_params(void* h, double* out) {
   auto* m = static_cast<RefModel*>(h);

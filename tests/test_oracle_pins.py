@@ -218,3 +218,69 @@ def test_oracle_prepass_matches_reference(mbs):
         of, ob = MO.prepass_scores(cfg, p, x, y, mbs, MO.METRICS[fi], MO.METRICS[bi])
         assert np.allclose(of, rf, rtol=1e-10, atol=0) and np.allclose(ob, rb, rtol=1e-10, atol=0)
     assert np.array_equal(r.params(), p)  # no update
+
+
+def _split_lora(cfg, rank, flat):
+    """The reference's canonical vector with adapters (visit_tensors: each
+    block's base tensors, then its six adapter matrices) -> (base, adapters)."""
+    sl = MO.subnet_slices(cfg)
+    lb = MO.lora_block_size(cfg, rank)
+    base, ad, off = [], [], 0
+    for si, (a, b) in enumerate(sl):
+        n = b - a
+        base.append(flat[off:off + n])
+        off += n
+        if 1 <= si <= cfg.K:
+            ad.append(flat[off:off + lb])
+            off += lb
+    assert off == flat.size
+    return np.concatenate(base), np.concatenate(ad)
+
+
+def _join_lora(cfg, rank, base, ad):
+    sl = MO.subnet_slices(cfg)
+    lb = MO.lora_block_size(cfg, rank)
+    parts = []
+    for si, (a, b) in enumerate(sl):
+        parts.append(base[a:b])
+        if 1 <= si <= cfg.K:
+            parts.append(ad[(si - 1) * lb:si * lb])
+    return np.concatenate(parts)
+
+
+@needs_ref
+def test_oracle_lora_matches_reference():
+    """LoRA: attach_lora's init (model.cpp:165-195), the
+    adapter forward/backward (model.cpp:204-211, 273-302) and the LoRA trainer
+    step (adapters only, trainer.cpp:124-133) of the numpy restatement against
+    the unmodified reference."""
+    cfg = MO.Config(2, 4, 32, 64, 16, 4)
+    rank, scaling = 4, 0.5
+    r = O.RefModel(2, 4, 32, 64, 16, 4, 1)
+    p = O.partition_model(2, 4, 32, 64, 16, 4, 1) + 0.05 * np.random.default_rng(2).standard_normal(r.n)
+    r.set_params(p)
+    r.attach_lora(rank, scaling)
+    base, ad = _split_lora(cfg, rank, r.params())
+    assert np.array_equal(base, p)
+    assert np.array_equal(ad, MO.lora_init(cfg, rank, 1))  # down = 0, up ~ N(0, 1/rank), same streams
+    ad = ad + 0.05 * np.random.default_rng(3).standard_normal(ad.size)  # nonzero down: every term live
+    r.set_params(_join_lora(cfg, rank, p, ad))
+    x, y = O.make_dataset(4, 4, 32, 16, 0.5, 7)
+    col = np.array([1, 2, 3, 1, 1, 1, 2, 3], np.uint8)
+    l1, ga, e1 = MO.forward_backward(cfg, p, x[:2], y[:2], col, lora=(rank, scaling, ad))
+    l2, g2, e2 = r.forward_backward(x[:2], y[:2], col)
+    gb2, ga2 = _split_lora(cfg, rank, g2)
+    assert abs(l1 - l2) < 1e-12 and np.array_equal(e1, e2)
+    assert np.max(np.abs(ga - ga2)) < 1e-12
+    assert not np.any(gb2)  # base tensors frozen: no gradient
+    codes = np.array([[1, 2], [3, 1], [1, 1], [2, 3], [3, 3], [1, 3], [2, 2], [1, 1]], np.uint8)
+    a_o, v_o = ad.copy(), np.zeros_like(ad)
+    for _ in range(2):
+        lr_ = r.train_batch(x, y, codes, 2, 0.05, 0.9)
+        lo, _ = MO.train_batch_lora(cfg, p, rank, scaling, a_o, v_o, x, y, codes, 2, 0.05, 0.9)
+        assert abs(lo - lr_) < 1e-12
+    b3, a3 = _split_lora(cfg, rank, r.params())
+    assert np.array_equal(b3, p)  # base frozen
+    assert np.max(np.abs(a3 - a_o)) < 1e-12
+    _, v3 = _split_lora(cfg, rank, r.velocity())
+    assert np.max(np.abs(v3 - v_o)) < 1e-12
