@@ -157,6 +157,27 @@ def gemm_flops(codes_exp, B):
     return fl, total_alg
 
 
+def lora_leg(x, y, fwd, bwd, capf, capo, B, steps=10, warmup=3, rank=8):
+    """§8f #3: the same ViT-B/16 batch and schedule with rank-8 LoRA adapters
+    on Q/K/V (base frozen, adapters trained; csrc/lora.cu), device-resident."""
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    from paper_2504_12471_b200 import scheduler as S
+    lib = _lib.lib()
+    K = L * H
+    m = E.SubnetModel(E.VIT_B16, B)
+    m.attach_lora(rank, 1.0)
+    m.stage(x, y, S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
+    ms, loss = C.c_double(), C.c_double()
+    _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+                                            C.c_int(warmup), C.c_int(steps), C.byref(ms), C.byref(loss)))
+    m.close()
+    ms_step = ms.value / steps
+    return {"workload": f"ViT-B/16 D2FT step with rank-{rank} LoRA on Q/K/V (adapters trained, base frozen), "
+                        f"batch {B}, same schedule", "value": B / (ms_step * 1e-3), "unit": "samples/s",
+            "ms_per_step": ms_step, "steps": steps, "warmup": warmup, "loss": loss.value}
+
+
 def vitl_leg(steps=3, warmup=2, B=256):
     """BASELINE configs[3]'s model and batch (ViT-L/16, L24 H16 d1024 ffn4096,
     batch 256) on ONE B200: device-resident steps, same schedule recipe and
@@ -443,6 +464,12 @@ def run_ours(args):
                                    f"(host buffers, tables returned)", "samples_per_s": B / dt, "ms": dt * 1e3}
         except Exception as e:
             prepass = {"error": str(e)[:200]}
+    lora = None
+    if rank == 0 and world == 1:
+        try:
+            lora = lora_leg(x, y, fwd, bwd, capf, capo, B)
+        except Exception as e:
+            lora = {"error": str(e)[:200]}
     vitl = None
     if rank == 0 and world == 1 and not args.no_vitl:
         try:
@@ -481,6 +508,8 @@ def run_ours(args):
             "cpu_baseline": cb,
         }
         line["schedule_metrics"] = sched_metrics
+        if lora:
+            line["lora"] = lora
         if part_info:
             line["partition"] = part_info
         if vitl:

@@ -40,6 +40,20 @@ int d2ft_engine_get_velocity(d2ft_engine* e, double* flat);
  * without a Full cell hold stale values (check the schedule) */
 int d2ft_engine_get_grads(d2ft_engine* e, double* flat);
 
+/* ---- LoRA: SubnetModel::attach_lora (model.cpp:165-195).
+ * Rank-r adapters on Q/K/V of every head-subnet; afterwards the step trains
+ * only the adapters (visit_trainable, model.hpp:155-172; trainer.cpp:124-133)
+ * and the base weights stay frozen.  Adapters are a flat fp64 array in
+ * visit_tensors order per block subnet (l, h): down_q [d][r], up_q [r][dh],
+ * down_k, up_k, down_v, up_v (model.hpp:139-146); initial values from
+ * d2ft_lora_init.  Errors: state (already attached), config (rank < 1 or
+ * rank > min(d, d/H)), as the reference. */
+int d2ft_engine_attach_lora(d2ft_engine* e, int rank, double scaling, const double* adapters);
+int64_t d2ft_engine_lora_count(d2ft_engine* e); /* adapter doubles (0 = none attached) */
+int d2ft_engine_set_lora(d2ft_engine* e, const double* adapters); /* also zeroes their velocity */
+/* which: 0 adapters, 1 velocity, 2 gradients of the last forward_backward / step */
+int d2ft_engine_get_lora(d2ft_engine* e, int which, double* adapters);
+
 /* SubnetModel::forward_backward (model.cpp:416-520) for n samples of one
  * micro-batch under one schedule column (K = L*H codes).  Loss = mean CE;
  * gradients (scaled 1/n) readable with d2ft_engine_get_grads. */
@@ -138,6 +152,10 @@ int d2ft_set_device(int device);
 /* partition_model (model.cpp:140-156): canonical fp64 flat initial
  * parameters, bit-identical to the reference for the same config/seed. */
 int d2ft_partition_model(const d2ft_model_config* cfg, double* out);
+/* attach_lora's initial adapters (model.cpp:174-192): down = 0, up_q/k/v
+ * ~ N(0, 1/rank) from make_rng(seed, 0x10000 + subnet index); layout as
+ * d2ft_engine_attach_lora, L*H*3*(d*r + r*dh) doubles. */
+int d2ft_lora_init(const d2ft_model_config* cfg, int rank, double* out);
 /* make_synthetic_dataset (trainer.cpp:83-111), samples returned as fp32
  * (the engine's input precision; the fp64 draws are rounded once). */
 int d2ft_make_synthetic_dataset(int num_samples, int num_classes, int token_dim, int seq_len, double noise,

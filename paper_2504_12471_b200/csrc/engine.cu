@@ -94,6 +94,13 @@ struct Engine {
   Seg seg[S_N];
   size_t nparam = 0;
   float *P = nullptr, *V = nullptr, *G = nullptr;
+  // LoRA (lora.cu): adapter arena [L][H][down_q|up_q|down_k|up_k|down_v|up_v],
+  // velocity and gradient; rank 0 = no adapters attached
+  int lora_rank = 0;
+  float lora_scaling = 0.f;
+  float *LA = nullptr, *LV = nullptr, *LG = nullptr;
+  size_t lora_per() const { return 3 * ((size_t)D.d * lora_rank + (size_t)lora_rank * D.dh); }
+  size_t lora_count() const { return (size_t)D.L * D.H * lora_per(); }
   act_t *W1T_bf, *W2T_bf, *WeT_bf;  // fp16 operand copies (G4 / G8 read W2T / W1T MN-major)
 
   // activations
@@ -496,6 +503,43 @@ struct Engine {
            d * D.C + D.C;
   }
 
+  // attach_lora (model.cpp:165-195) with the caller's initial adapters
+  void attach_lora(int rank, double scaling, const double* init) {
+    D2FT_REQUIRE(!lora_rank, kState, "lora adapters already attached");
+    D2FT_REQUIRE(!partitioned(), kState, "lora: not available on a head-partitioned engine");
+    D2FT_REQUIRE(rank >= 1, kConfig, "lora rank must be >= 1");
+    const int cap = std::min(D.d, D.dh);
+    D2FT_REQUIRE(rank <= cap, kConfig,
+                 "lora rank " + std::to_string(rank) + " exceeds min(d, d/H) = " + std::to_string(cap));
+    D2FT_REQUIRE(rank * D.dh <= 4096, kConfig, "lora: rank x head_dim above 4096 is not supported");
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    lora_rank = rank;
+    lora_scaling = (float)scaling;
+    LA = dalloc<float>(lora_count(), owned);
+    LV = dalloc<float>(lora_count(), owned);
+    LG = dalloc<float>(lora_count(), owned);
+    D2FT_CUDA(cudaMemsetAsync(LV, 0, lora_count() * 4, st));
+    D2FT_CUDA(cudaMemsetAsync(LG, 0, lora_count() * 4, st));
+    set_lora(init);
+    if (gexec) {  // the captured step has no adapter work
+      D2FT_CUDA(cudaGraphExecDestroy(gexec));
+      gexec = nullptr;
+    }
+  }
+  void set_lora(const double* flat) {
+    std::vector<float> a(lora_count());
+    for (size_t i = 0; i < a.size(); ++i) a[i] = (float)flat[i];
+    D2FT_CUDA(cudaMemcpyAsync(LA, a.data(), a.size() * 4, cudaMemcpyHostToDevice, st));
+    launch_lora_merge(D, lora_rank, lora_scaling, P + seg[S_W1T].off, LA, W1T_bf, st);
+    D2FT_CUDA(cudaStreamSynchronize(st));
+  }
+  void get_lora(const float* src, double* flat) {
+    std::vector<float> a(lora_count());
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    D2FT_CUDA(cudaMemcpy(a.data(), src, a.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < a.size(); ++i) flat[i] = a[i];
+  }
+
   void refresh_bf16_all() {
     launch_f32_to_act(P + seg[S_W1T].off, W1T_bf, seg[S_W1T].n, st);
     launch_f32_to_act(P + seg[S_W2T].off, W2T_bf, seg[S_W2T].n, st);
@@ -507,6 +551,7 @@ struct Engine {
     convert<true>(const_cast<double*>(flat), a);
     D2FT_CUDA(cudaMemcpyAsync(P, a.data(), nparam * 4, cudaMemcpyHostToDevice, st));
     refresh_bf16_all();
+    if (lora_rank) launch_lora_merge(D, lora_rank, lora_scaling, P + seg[S_W1T].off, LA, W1T_bf, st);
     D2FT_CUDA(cudaStreamSynchronize(st));
   }
   void get_arena(float* src, double* flat) {
@@ -596,7 +641,7 @@ struct Engine {
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
-    const bool side = use_side && !profiling && !partitioned() && !sm;
+    const bool side = use_side && !profiling && !partitioned() && !sm && !lora_rank;
     auto g5 = [&](int l, cudaStream_t s5) {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
@@ -633,7 +678,7 @@ struct Engine {
             tm_dC64, tm_OGT,
             S5<160>{D, l, sm->mbs, sm->n_units, P + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax, sm->p5 + l * sper},
             0, st);
-      } else if (!side) {
+      } else if (!side && !lora_rank) {  // LoRA: [Wo;W2] frozen
         g5(l, st);
       }
       mark(PH_G7);
@@ -667,6 +712,11 @@ struct Engine {
                          partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
+    if (lora_rank) {  // only the adapters train (model.hpp:155-172)
+      mark(PH_BIAS);
+      launch_lora_grad(D, lora_rank, lora_scaling, G + seg[S_W1T].off, LA, LG, lists.full_cnt, st);
+      return;
+    }
     mark(PH_EMBED_W);
     launch_gemm<EmbedW<256>, GemmShape<256, kCG2 ? 6 : 4, 0, 4, 2, 0, 1, kCG2>>(tm_dC64, tm_inpT, EmbedW<256>{D, KS, part_ew, gmax}, 0, st);
     launch_embed_reduce(D, KS, part_ew, cs_slot(L), dX, G + seg[S_WET].off, G + seg[S_BE].off, G + seg[S_POS].off, st);
@@ -685,6 +735,7 @@ struct Engine {
   // n_units micro-batches of mbs samples, all head-subnets Full, no update.
   void prepass(int n_units, int mbs, int fwd_metric, int bwd_metric, double* fwd_host, double* bwd_host) {
     D2FT_REQUIRE(!partitioned(), kState, "prepass: not available on a head-partitioned engine");
+    D2FT_REQUIRE(!lora_rank, kState, "prepass: adapter (LoRA-mode) scores are not implemented");
     const int B = n_units * mbs;
     begin_step(B);
     const int K = D.K();
@@ -724,6 +775,12 @@ struct Engine {
   void run_sgd(float lr, float mom) {
     mark(PH_SGD);
     const int* fc = lists.full_cnt;
+    if (lora_rank) {  // adapters of subnets with Full cells, then W_eff for the next step
+      const long long per = (long long)lora_per();
+      launch_sgd(LA, LV, LG, nullptr, lora_count(), (long long)D.H * per, per, D.H, fc, lr, mom, err, st);
+      launch_lora_merge(D, lora_rank, lora_scaling, P + seg[S_W1T].off, LA, W1T_bf, st);
+      return;
+    }
     auto sgd = [&](int id, act_t* pbf, const int* touch) {
       const Seg& s = seg[id];
       launch_sgd(P + s.off, V + s.off, G + s.off, pbf, s.n, s.outer, s.inner, D.H, touch, lr, mom, err, st);
@@ -963,6 +1020,36 @@ int d2ft_engine_get_velocity(d2ft_engine* e, double* flat) {
 
 int d2ft_engine_get_grads(d2ft_engine* e, double* flat) {
   return guarded([&] { e->e->get_arena(e->e->G, flat); });
+}
+
+int d2ft_engine_attach_lora(d2ft_engine* e, int rank, double scaling, const double* adapters) {
+  return guarded([&] {
+    D2FT_REQUIRE(e && e->e && adapters, kInput, "attach_lora: null argument");
+    e->e->attach_lora(rank, scaling, adapters);
+  });
+}
+
+int64_t d2ft_engine_lora_count(d2ft_engine* e) {
+  return e && e->e && e->e->lora_rank ? (int64_t)e->e->lora_count() : 0;
+}
+
+int d2ft_engine_set_lora(d2ft_engine* e, const double* adapters) {
+  return guarded([&] {
+    D2FT_REQUIRE(e && e->e && adapters, kInput, "set_lora: null argument");
+    D2FT_REQUIRE(e->e->lora_rank, kState, "set_lora: no adapters attached");
+    e->e->set_lora(adapters);
+    D2FT_CUDA(cudaMemsetAsync(e->e->LV, 0, e->e->lora_count() * 4, e->e->st));
+    D2FT_CUDA(cudaStreamSynchronize(e->e->st));
+  });
+}
+
+int d2ft_engine_get_lora(d2ft_engine* e, int which, double* adapters) {
+  return guarded([&] {
+    D2FT_REQUIRE(e && e->e && adapters, kInput, "get_lora: null argument");
+    D2FT_REQUIRE(e->e->lora_rank, kState, "get_lora: no adapters attached");
+    D2FT_REQUIRE(which >= 0 && which <= 2, kInput, "get_lora: which is 0 (params), 1 (velocity) or 2 (grads)");
+    e->e->get_lora(which == 0 ? e->e->LA : which == 1 ? e->e->LV : e->e->LG, adapters);
+  });
 }
 
 int d2ft_nccl_unique_id(uint8_t* id_out) {

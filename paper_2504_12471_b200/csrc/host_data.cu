@@ -4,7 +4,9 @@
 //   partition_model         model.cpp:91-156 (per-subnet streams make_rng(seed, index))
 //   make_synthetic_dataset  trainer.cpp:61-111
 //   make_rng / gaussian     rng.hpp:16-50 (std::mt19937_64 is fully specified by the standard)
+#include <algorithm>
 #include <cmath>
+#include <string>
 #include <cstring>
 #include <random>
 
@@ -43,6 +45,30 @@ double* zeros(double* p, size_t n) {
 using namespace d2ft_b200;
 
 extern "C" {
+
+int d2ft_lora_init(const d2ft_model_config* c, int rank, double* out) {
+  return guarded([&] {
+    D2FT_REQUIRE(c && out, kInput, "lora_init: null argument");
+    const int L = c->num_blocks, H = c->heads_per_block, d = c->model_dim;
+    D2FT_REQUIRE(L >= 1 && H >= 1 && d >= 1 && d % H == 0, kConfig, "model config: invalid dimensions");
+    const int dh = d / H;
+    D2FT_REQUIRE(rank >= 1, kConfig, "lora rank must be >= 1");
+    D2FT_REQUIRE(rank <= std::min(d, dh), kConfig,
+                 "lora rank " + std::to_string(rank) + " exceeds min(d, d/H) = " + std::to_string(std::min(d, dh)));
+    double* p = out;
+    const double sd = 1.0 / std::sqrt(rank);
+    for (int k = 0; k < L * H; ++k) {
+      auto g = stream_rng(c->seed, 0x10000u + 1u + (uint64_t)k);  // subnet index 1 + l*H + h
+      double* blk = p;
+      for (int x = 0; x < 3; ++x) {
+        p = zeros(p, (size_t)d * rank);   // down_x
+        p += (size_t)rank * dh;           // up_x, filled below in q, k, v order
+      }
+      for (int x = 0; x < 3; ++x)
+        fill(blk + (size_t)x * ((size_t)d * rank + (size_t)rank * dh) + (size_t)d * rank, (size_t)rank * dh, g, sd);
+    }
+  });
+}
 
 int d2ft_partition_model(const d2ft_model_config* c, double* out) {
   return guarded([&] {

@@ -83,6 +83,16 @@ def partition_model(cfg: ModelConfig) -> np.ndarray:
     return out
 
 
+def lora_init(cfg: ModelConfig, rank: int) -> np.ndarray:
+    """attach_lora's initial adapters (model.cpp:174-192), bit-identical to the
+    reference: per block subnet down_q[d][r] = 0, up_q[r][dh] ~ N(0, 1/r), k, v."""
+    n = cfg.num_blocks * cfg.heads_per_block * 3 * (cfg.model_dim * rank + rank * cfg.head_dim())
+    out = np.empty(n, np.float64)
+    c = cfg._c()
+    check(lib().d2ft_lora_init(C.byref(c), C.c_int(rank), ptr(out)))
+    return out
+
+
 def make_synthetic_dataset(num_samples, num_classes, token_dim, seq_len, noise_level=0.5, seed=7):
     """trainer.cpp:83-111; samples as fp32 [n][T][d], labels int32."""
     x = np.empty((num_samples, seq_len, token_dim), np.float32)
@@ -146,6 +156,41 @@ class SubnetModel:
         out = np.empty(self.n, np.float64)
         check(lib().d2ft_engine_get_grads(self._h, ptr(out)))
         return out
+
+    # ---- LoRA (model.cpp:165-195; csrc/lora.cu) ----------------------------
+    def attach_lora(self, rank: int, scaling: float, adapters: np.ndarray | None = None) -> None:
+        """SubnetModel::attach_lora: rank-r adapters on Q/K/V, base frozen.
+        adapters default to the reference's initial values (lora_init)."""
+        a = lora_init(self.config, rank) if adapters is None else f64(adapters)
+        check(lib().d2ft_engine_attach_lora(self._h, C.c_int(rank), C.c_double(scaling), ptr(a)))
+        self.lora_rank, self.lora_scaling = rank, scaling
+
+    def lora_enabled(self) -> bool:
+        return bool(getattr(self, "lora_rank", 0))
+
+    def _lora_n(self) -> int:
+        lib().d2ft_engine_lora_count.restype = C.c_int64
+        return int(lib().d2ft_engine_lora_count(self._h))
+
+    def set_lora(self, adapters) -> None:
+        a = f64(adapters)
+        if a.size != self._lora_n():
+            raise Error(3, f"set_lora: expected {self._lora_n()} values, got {a.size}")
+        check(lib().d2ft_engine_set_lora(self._h, ptr(a)))
+
+    def _get_lora(self, which: int) -> np.ndarray:
+        out = np.empty(self._lora_n(), np.float64)
+        check(lib().d2ft_engine_get_lora(self._h, C.c_int(which), ptr(out)))
+        return out
+
+    def lora_params(self) -> np.ndarray:
+        return self._get_lora(0)
+
+    def lora_velocity(self) -> np.ndarray:
+        return self._get_lora(1)
+
+    def lora_grads(self) -> np.ndarray:
+        return self._get_lora(2)
 
     def forward_backward(self, inputs, labels, schedule_column):
         """model.cpp:416-520: returns (loss, grads_flat, engaged).  Gradients of

