@@ -35,6 +35,16 @@ constexpr int kCG2 = D2FT_CG2;
 #define D2FT_CG2_BMN 1  // pair UMMA also for the MN-major-B GEMMs (G3, G8)
 #endif
 constexpr int kCG2Bmn = D2FT_CG2_BMN;
+// SGD in the G5 / G7 epilogues: opt-in.  Correct (the GPU suite passes with
+// it on) but measured slower on the ViT-B step: 7.89 vs 5.59 ms — G5's
+// row-per-thread epilogue turns the p / v read-modify-write into
+// uncoalesced scalar traffic (0.52 -> 2.87 ms) and G7's coalesced one still
+// does not hide 18 B / weight under its MMAs (0.59 -> 0.99 ms), against a
+// separate streaming SGD pass of 0.30 ms for those weights.
+#ifndef D2FT_FUSE_SGD
+#define D2FT_FUSE_SGD 0
+#endif
+constexpr bool kFuseSgd = D2FT_FUSE_SGD;
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
@@ -642,10 +652,14 @@ struct Engine {
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
     const bool side = use_side && !profiling && !partitioned() && !sm && !lora_rank;
+    // SGD in the G5 / G7 epilogues (FusedSgd) when a training step follows;
+    // G8 runs before G7 so the layer's fp16 W1 operand is updated after its
+    // last reader; not with the side stream (G5 would overlap G4's W2 reads)
+    sgd_fused = sgd_fuse_req && !side && !sm && !lora_rank;
     auto g5 = [&](int l, cudaStream_t s5) {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
-                  ord_head + l * H, ctr(l, C_G5)},
+                  ord_head + l * H, ctr(l, C_G5), fsgd(S_W2T, W2T_bf, (size_t)l * d * H * D.PO)},
           s5 == st ? 0 : side_ctas, s5);
     };
     for (int l = D.L - 1; l >= 0; --l) {
@@ -681,19 +695,6 @@ struct Engine {
       } else if (!side && !lora_rank) {  // LoRA: [Wo;W2] frozen
         g5(l, st);
       }
-      mark(PH_G7);
-      if (sm)
-        launch_gemm<S7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
-            tm_xn64, tm_dY1Tb,
-            S7<kG7BN>{D, l, sm->mbs, sm->n_units, P + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
-                      sm->p7 + l * sper},
-            0, st);
-      else
-      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
-          tm_xn64, tm_dY1Tb,
-          G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
-                    ord_head + l * H, ctr(l, C_G7)},
-          0, st);
       mark(PH_G8);
       // single engine: dxn leaves G8 as fp16 in gradient-scale units (half the
       // bytes of G8's stores and the LN backward's reads); partitioned: fp32
@@ -705,6 +706,19 @@ struct Engine {
         mark(PH_EXCH);
         ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
       }
+      mark(PH_G7);
+      if (sm)
+        launch_gemm<S7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
+            tm_xn64, tm_dY1Tb,
+            S7<kG7BN>{D, l, sm->mbs, sm->n_units, P + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                      sm->p7 + l * sper},
+            0, st);
+      else
+      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
+          tm_xn64, tm_dY1Tb,
+          G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                    ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
+          0, st);
       if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(2 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
@@ -772,6 +786,25 @@ struct Engine {
   float* cs_slot(int k) { return part_cs + (size_t)k * D.Bmax * ((D.T + 31) / 32) * D.d; }
   float* db1_slot(int l) { return part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs; }
 
+  // fused SGD (step_gemms.cuh FusedSgd): requested by train_body for the next
+  // run_forward_backward; sgd_fused records whether the GEMMs applied it
+  bool sgd_fuse_req = false, sgd_fused = false;
+  float sgd_lr = 0.f, sgd_mom = 0.f;
+  FusedSgd fsgd(int id, act_t* pbf, size_t off) const {
+    if (!sgd_fused) return FusedSgd{nullptr, nullptr, nullptr, 0.f, 0.f, nullptr};
+    return FusedSgd{P + seg[id].off + off, V + seg[id].off + off, pbf + off, sgd_lr, sgd_mom, err};
+  }
+  // forward/backward + SGD of one training step (the trainer's batch body)
+  void train_body(float lr, float mom) {
+    sgd_fuse_req = kFuseSgd;
+    sgd_lr = lr;
+    sgd_mom = mom;
+    run_forward_backward();
+    sgd_fuse_req = false;
+    run_sgd(lr, mom);
+    sgd_fused = false;
+  }
+
   void run_sgd(float lr, float mom) {
     mark(PH_SGD);
     const int* fc = lists.full_cnt;
@@ -785,9 +818,9 @@ struct Engine {
       const Seg& s = seg[id];
       launch_sgd(P + s.off, V + s.off, G + s.off, pbf, s.n, s.outer, s.inner, D.H, touch, lr, mom, err, st);
     };
-    sgd(S_W1T, W1T_bf, fc);
+    if (!sgd_fused) sgd(S_W1T, W1T_bf, fc);
     sgd(S_B1, nullptr, fc);
-    sgd(S_W2T, W2T_bf, fc);
+    if (!sgd_fused) sgd(S_W2T, W2T_bf, fc);
     sgd(S_B2, nullptr, fc);
     sgd(S_WET, WeT_bf, nullptr);
     sgd(S_BE, nullptr, nullptr);
@@ -892,8 +925,7 @@ struct Engine {
   void compute_step(int n_mb, int mbs, double lr, double momentum) {
     if (profiling || partitioned() || !use_graphs) {
       schedule_device(n_mb, mbs);
-      run_forward_backward();
-      run_sgd((float)lr, (float)momentum);
+      train_body((float)lr, (float)momentum);
       return;
     }
     if (!gexec || g_nmb != n_mb || g_mbs != mbs || g_lr != (float)lr || g_mom != (float)momentum) {
@@ -905,8 +937,7 @@ struct Engine {
       const unsigned long long n0 = d2ft_b200::launch_count();
       D2FT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       schedule_device(n_mb, mbs);
-      run_forward_backward();
-      run_sgd((float)lr, (float)momentum);
+      train_body((float)lr, (float)momentum);
       D2FT_CUDA(cudaStreamEndCapture(st, &g));
       g_kernels = d2ft_b200::launch_count() - n0;
       if (use_pdl) make_edges_programmatic(g);
@@ -1158,8 +1189,7 @@ int d2ft_engine_step_codes(d2ft_engine* h, const float* samples, const int32_t* 
     D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, codes, (size_t)E.D.K() * n_mb, cudaMemcpyHostToDevice, E.st));
     launch_expand_codes(E.codes_mb, E.D.K(), n_mb, mbs, B, E.D.Bmax, E.codes_exp, E.st);
     E.compact_and_plan();
-    E.run_forward_backward();
-    E.run_sgd((float)lr, (float)momentum);
+    E.train_body((float)lr, (float)momentum);
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
   });

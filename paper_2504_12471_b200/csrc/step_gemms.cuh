@@ -411,6 +411,32 @@ struct G4 {
   }
 };
 
+// ---------------------------------------------------------------- fused SGD
+// sgd_momentum_step (trainer.cpp:114-121) applied in the G5 / G7 epilogues
+// when a training step follows: the weight gradient never reaches HBM and the
+// separate SGD pass skips [Wq|Wk|Wv|W1]^T and [Wo;W2]^T (the bulk of the
+// parameters).  Same arithmetic as sgd_kernel (bitwise).  Tiles of heads
+// without Full samples (nkb == 0) leave p and v untouched (trainer.cpp:264-268).
+// P == nullptr: write the gradient (forward_backward API, pre-pass, LoRA).
+struct FusedSgd {
+  float* P;     // master weights of block l's segment, gradient indexing
+  float* V;     // momentum
+  act_t* Pbf;   // fp16 operand copy
+  float lr, mom;
+  int* err;
+  __device__ __forceinline__ void apply(size_t i, float g) const {
+    if (!isfinite(g)) {
+      atomicCAS(err, 0, 5);  // kNumeric (trainer.cpp:118)
+      return;
+    }
+    const float v = mom * V[i] + g;
+    const float p = P[i] - lr * v;
+    V[i] = v;
+    P[i] = p;
+    Pbf[i] = to_act(p);
+  }
+};
+
 // ---------------------------------------------------------------- G5
 // dW2T[l][m][h*PO + f] = sum_{s in Full(h)} sum_t dC[s][t][m] [O|g][s][h][t][f]
 // (model.cpp:249, 263).  A = dC read MN-major (plane s, [t][m] as [K][M]),
@@ -425,6 +451,7 @@ struct G5 {
   const float* gmax;
   const int* order;  // block l: heads by decreasing Full-sample count
   int* ctr;
+  FusedSgd sgd;
   struct Tile {
     int nkb, h, mt, nt;
   };
@@ -455,8 +482,16 @@ struct G5 {
   __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row& r) const {
     const int m = c.mt * 128 + row;
     if (m >= D.d) return;
-    float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
     const int f0 = c.nt * BN + col0;
+    if (sgd.P) {
+      if (c.nkb == 0) return;
+      const size_t o = (size_t)m * D.H * D.PO + c.h * D.PO + f0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (f0 + i < D.PO) sgd.apply(o + i, v[i] * r.inv);
+      return;
+    }
+    float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
     if (f0 + 16 <= D.PO) {  // 16 contiguous fp32 of this row: four 16-byte stores
 #pragma unroll
       for (int i = 0; i < 16; i += 4)
@@ -486,6 +521,7 @@ struct G7 {
   const float* gmax;
   const int* order;  // block l: heads by decreasing Full-sample count
   int* ctr;
+  FusedSgd sgd;
   struct Tile {
     int nkb, h, mt, nt;
   };
@@ -518,6 +554,14 @@ struct G7 {
     const int m = c.mt * 128 + row;
     if (m >= D.d) return;
     const int f0 = c.nt * BN + col0;
+    if (sgd.P) {
+      if (c.nkb == 0) return;
+      const size_t o = ((size_t)c.h * D.PQ + f0) * D.d + m;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (f0 + i < D.PQ) sgd.apply(o + (size_t)i * D.d, v[i] * r.inv);
+      return;
+    }
     // lanes hold consecutive m: each store instruction writes 128 contiguous bytes
     float* out = dW1T + ((size_t)c.h * D.PQ + f0) * D.d + m;
 #pragma unroll
