@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (S::CG2 && rank != 0) ptx::mbar_arrive_cluster(ptx::mapa(&tempty[acc], 0));  // the issuing CTA's
+          if (S::CG2 && rank != 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(&tempty[acc], 0));  // the issuing CTA's
           else ptx::mbar_arrive(&tempty[acc]);
         }
       };

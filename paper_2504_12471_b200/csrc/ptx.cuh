@@ -58,6 +58,13 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
+// Remote arrive that publishes no memory writes (e.g. an accumulator release
+// after tcgen05.wait::ld + tcgen05.fence::before_thread_sync): relaxed, so no
+// cluster-scope release fence (MEMBAR.ALL.GPU, which waits for the thread's
+// outstanding global stores) is emitted.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
