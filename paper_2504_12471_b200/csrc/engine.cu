@@ -130,11 +130,17 @@ struct Engine {
   // the forward's [O|g], so it runs beside G4 / attention backward / G7 / G8
   // and joins before the LN backward overwrites dC
   cudaStream_t st2 = nullptr;
-  std::vector<cudaEvent_t> side_ev;  // [2L]: fork, join per block
-  // opt-in (D2FT_SIDE=1): measured 5.716 vs 5.733 ms per step — the
-  // persistent G5 CTAs that start in a tail hold their SMs until done
-  bool use_side = getenv("D2FT_SIDE") != nullptr;
-  int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : 0;  // G5's grid on the side stream
+  std::vector<cudaEvent_t> side_ev;  // [4L]: G5 fork / join, G7 fork / join per block
+  // G7 (dW of [Wq|Wk|Wv|W1]) also runs on the side stream, forked after the
+  // attention backward and joined before the next block's G4 overwrites dY1T.
+  // The weight-gradient GEMMs then fill the critical path's tails (the
+  // attention backward's last round, G4 / G8 ramps): ViT-B 5.49 vs 5.57 ms
+  // per step with both, 5.54 with G5 alone (same box, tools/ab_side.sh).
+  // D2FT_NO_SIDE / D2FT_NO_SIDE_G7 turn them off; D2FT_SIDE_CTAS caps the side
+  // kernels' grids (64: 5.66 ms — fewer SMs, same long tiles).
+  bool use_side = getenv("D2FT_NO_SIDE") == nullptr;
+  int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : 0;
+  bool side_g7 = getenv("D2FT_NO_SIDE_G7") == nullptr;
   cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
   bool have_prefetch = false;
   int prefetch_B = 0;
@@ -667,11 +673,13 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       if (side) {
-        D2FT_CUDA(cudaEventRecord(side_event(2 * l), st));
-        D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(2 * l), 0));
+        D2FT_CUDA(cudaEventRecord(side_event(4 * l), st));
+        D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(4 * l), 0));
         g5(l, st2);
-        D2FT_CUDA(cudaEventRecord(side_event(2 * l + 1), st2));
+        D2FT_CUDA(cudaEventRecord(side_event(4 * l + 1), st2));
       }
+      if (side && side_g7 && l + 1 < (int)L)  // G7(l+1) read dY1T
+        D2FT_CUDA(cudaStreamWaitEvent(st, side_event(4 * (l + 1) + 3), 0));
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
@@ -685,6 +693,7 @@ struct Engine {
       else
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
+      if (side && side_g7) D2FT_CUDA(cudaEventRecord(side_event(4 * l + 2), st));
       mark(PH_G5);
       const size_t sper = sm ? (size_t)sm->n_units * H * kScoreTiles * 16 * 3 : 0;
       if (sm) {
@@ -713,18 +722,27 @@ struct Engine {
             S7<kG7BN>{D, l, sm->mbs, sm->n_units, P + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
                       sm->p7 + l * sper},
             0, st);
-      else
-      launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
-          tm_xn64, tm_dY1Tb,
-          G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
-                    ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
-          0, st);
-      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(2 * l + 1), 0));  // G5 read dC
+      else {
+        const bool s7 = side && side_g7;
+        cudaStream_t g7s = st;
+        if (s7) {
+          D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(4 * l + 2), 0));  // dY1T of block l complete
+          g7s = st2;
+        }
+        launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
+            tm_xn64, tm_dY1Tb,
+            G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
+                      ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
+            s7 ? side_ctas : 0, g7s);
+        if (s7) D2FT_CUDA(cudaEventRecord(side_event(4 * l + 3), st2));
+      }
+      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(4 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
                          partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
+    if (side && side_g7) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(3), 0));  // G7 of block 0
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     if (lora_rank) {  // only the adapters train (model.hpp:155-172)
       mark(PH_BIAS);
@@ -740,7 +758,7 @@ struct Engine {
 
   cudaEvent_t side_event(int i) {
     if (side_ev.empty()) {
-      side_ev.resize(2 * D.L);
+      side_ev.resize(4 * D.L);
       for (auto& e : side_ev) D2FT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return side_ev[i];

@@ -557,6 +557,7 @@ void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int 
   }
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (max_ctas < 0) grid = -max_ctas;  // explicit grid (may exceed the SM count: non-persistent)
   grid -= grid % S::CLUSTER;
   if (grid < S::CLUSTER) grid = S::CLUSTER;
   if (S::CLUSTER == 1) {
