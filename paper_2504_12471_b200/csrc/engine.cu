@@ -130,12 +130,14 @@ struct Engine {
   // the forward's [O|g], so it runs beside G4 / attention backward / G7 / G8
   // and joins before the LN backward overwrites dC
   cudaStream_t st2 = nullptr;
-  std::vector<cudaEvent_t> side_ev;  // [4L]: G5 fork / join, G7 fork / join per block
+  std::vector<cudaEvent_t> side_ev;  // [5L+1]: G5 fork / join, G7 fork / join, G8 done per block; final join
   // G7 (dW of [Wq|Wk|Wv|W1]) also runs on the side stream, forked after the
   // attention backward and joined before the next block's G4 overwrites dY1T.
   // The weight-gradient GEMMs then fill the critical path's tails (the
-  // attention backward's last round, G4 / G8 ramps): ViT-B 5.49 vs 5.57 ms
-  // per step with both, 5.54 with G5 alone (same box, tools/ab_side.sh).
+  // attention backward's last round, G4 / G8 ramps), and each block's weight
+  // SGD follows its G7 there instead of ending the step: ViT-B 5.25 vs
+  // 5.47 ms per step (5.49 before the per-block SGD; G5 alone 5.46; same box,
+  // tools/ab_side.sh).
   // D2FT_NO_SIDE / D2FT_NO_SIDE_G7 turn them off; D2FT_SIDE_CTAS caps the side
   // kernels' grids (64: 5.66 ms — fewer SMs, same long tiles).
   bool use_side = getenv("D2FT_NO_SIDE") == nullptr;
@@ -662,6 +664,10 @@ struct Engine {
     // G8 runs before G7 so the layer's fp16 W1 operand is updated after its
     // last reader; not with the side stream (G5 would overlap G4's W2 reads)
     sgd_fused = sgd_fuse_req && !side && !sm && !lora_rank;
+    // training step with both weight-gradient GEMMs on the side stream: each
+    // block's weight SGD follows its G7 there (after G8, the block's last
+    // reader of the fp16 operands), overlapping the lower blocks' backward
+    sgd_layer = step_train && side && side_g7 && !sm && !lora_rank && !sgd_fused;
     auto g5 = [&](int l, cudaStream_t s5) {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
@@ -673,13 +679,13 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       if (side) {
-        D2FT_CUDA(cudaEventRecord(side_event(4 * l), st));
-        D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(4 * l), 0));
+        D2FT_CUDA(cudaEventRecord(side_event(5 * l), st));
+        D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l), 0));
         g5(l, st2);
-        D2FT_CUDA(cudaEventRecord(side_event(4 * l + 1), st2));
+        D2FT_CUDA(cudaEventRecord(side_event(5 * l + 1), st2));
       }
       if (side && side_g7 && l + 1 < (int)L)  // G7(l+1) read dY1T
-        D2FT_CUDA(cudaStreamWaitEvent(st, side_event(4 * (l + 1) + 3), 0));
+        D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * (l + 1) + 3), 0));
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
       gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
@@ -693,7 +699,7 @@ struct Engine {
       else
         launch_attn_bwd(D, l, lists.full_heads, lists.full_hcnt, QKVl, OGTl, dO, lse + (size_t)l * Bm * H * T, dY1T,
                         st);
-      if (side && side_g7) D2FT_CUDA(cudaEventRecord(side_event(4 * l + 2), st));
+      if (side && side_g7) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 2), st));
       mark(PH_G5);
       const size_t sper = sm ? (size_t)sm->n_units * H * kScoreTiles * 16 * 3 : 0;
       if (sm) {
@@ -715,6 +721,7 @@ struct Engine {
         mark(PH_EXCH);
         ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
       }
+      if (sgd_layer) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 4), st));  // last reader of W1T_bf[l] / W2T_bf[l]
       mark(PH_G7);
       if (sm)
         launch_gemm<S7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
@@ -726,7 +733,7 @@ struct Engine {
         const bool s7 = side && side_g7;
         cudaStream_t g7s = st;
         if (s7) {
-          D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(4 * l + 2), 0));  // dY1T of block l complete
+          D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l + 2), 0));  // dY1T of block l complete
           g7s = st2;
         }
         launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
@@ -734,15 +741,23 @@ struct Engine {
             G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
                       ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
             s7 ? side_ctas : 0, g7s);
-        if (s7) D2FT_CUDA(cudaEventRecord(side_event(4 * l + 3), st2));
+        if (s7) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 3), st2));
+        if (sgd_layer) {  // this block's [Wq|Wk|Wv|W1]^T and [Wo;W2]^T SGD, off the critical path
+          D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l + 4), 0));
+          sgd_block(S_W1T, W1T_bf, l, st2);
+          sgd_block(S_W2T, W2T_bf, l, st2);
+        }
       }
-      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(4 * l + 1), 0));  // G5 read dC
+      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
                          partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
-    if (side && side_g7) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(3), 0));  // G7 of block 0
+    if (side) {  // everything on the side stream (G5, G7, per-block SGD) before what follows
+      D2FT_CUDA(cudaEventRecord(side_event(5 * (int)L), st2));
+      D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * (int)L), 0));
+    }
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     if (lora_rank) {  // only the adapters train (model.hpp:155-172)
       mark(PH_BIAS);
@@ -758,7 +773,7 @@ struct Engine {
 
   cudaEvent_t side_event(int i) {
     if (side_ev.empty()) {
-      side_ev.resize(4 * D.L);
+      side_ev.resize(5 * D.L + 1);
       for (auto& e : side_ev) D2FT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return side_ev[i];
@@ -807,6 +822,7 @@ struct Engine {
   // fused SGD (step_gemms.cuh FusedSgd): requested by train_body for the next
   // run_forward_backward; sgd_fused records whether the GEMMs applied it
   bool sgd_fuse_req = false, sgd_fused = false;
+  bool step_train = false, sgd_layer = false;  // train_body in progress / per-block side-stream SGD applied
   float sgd_lr = 0.f, sgd_mom = 0.f;
   FusedSgd fsgd(int id, act_t* pbf, size_t off) const {
     if (!sgd_fused) return FusedSgd{nullptr, nullptr, nullptr, 0.f, 0.f, nullptr};
@@ -815,12 +831,22 @@ struct Engine {
   // forward/backward + SGD of one training step (the trainer's batch body)
   void train_body(float lr, float mom) {
     sgd_fuse_req = kFuseSgd;
+    step_train = true;
     sgd_lr = lr;
     sgd_mom = mom;
     run_forward_backward();
     sgd_fuse_req = false;
+    step_train = false;
     run_sgd(lr, mom);
     sgd_fused = false;
+    sgd_layer = false;
+  }
+  // sgd_momentum_step on block l's part of a per-block segment
+  void sgd_block(int id, act_t* pbf, int l, cudaStream_t s) {
+    const Seg& g = seg[id];
+    const size_t o = g.off + (size_t)l * g.outer;
+    launch_sgd(P + o, V + o, G + o, pbf + (size_t)l * g.outer, (size_t)g.outer, g.outer, g.inner, D.H,
+               lists.full_cnt + l * D.H, sgd_lr, sgd_mom, err, s);
   }
 
   void run_sgd(float lr, float mom) {
@@ -836,9 +862,9 @@ struct Engine {
       const Seg& s = seg[id];
       launch_sgd(P + s.off, V + s.off, G + s.off, pbf, s.n, s.outer, s.inner, D.H, touch, lr, mom, err, st);
     };
-    if (!sgd_fused) sgd(S_W1T, W1T_bf, fc);
+    if (!sgd_fused && !sgd_layer) sgd(S_W1T, W1T_bf, fc);
     sgd(S_B1, nullptr, fc);
-    if (!sgd_fused) sgd(S_W2T, W2T_bf, fc);
+    if (!sgd_fused && !sgd_layer) sgd(S_W2T, W2T_bf, fc);
     sgd(S_B2, nullptr, fc);
     sgd(S_WET, WeT_bf, nullptr);
     sgd(S_BE, nullptr, nullptr);
