@@ -754,10 +754,12 @@ struct Engine {
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
                          partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
     }
-    if (side) {  // everything on the side stream (G5, G7, per-block SGD) before what follows
-      D2FT_CUDA(cudaEventRecord(side_event(5 * (int)L), st2));
-      D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * (int)L), 0));
-    }
+    // everything on the side stream (G5, G7, per-block SGD) joins here, or —
+    // in a training step — after the remaining SGD (train_body), so the embed
+    // / bias gradients and the small SGD segments overlap the side stream's
+    // last G7 and block SGD (they touch none of its buffers)
+    side_pending = side;
+    if (side && !step_train) join_side();
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     if (lora_rank) {  // only the adapters train (model.hpp:155-172)
       mark(PH_BIAS);
@@ -838,8 +840,15 @@ struct Engine {
     sgd_fuse_req = false;
     step_train = false;
     run_sgd(lr, mom);
+    if (side_pending) join_side();
     sgd_fused = false;
     sgd_layer = false;
+  }
+  bool side_pending = false;
+  void join_side() {
+    D2FT_CUDA(cudaEventRecord(side_event(5 * D.L), st2));
+    D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * D.L), 0));
+    side_pending = false;
   }
   // sgd_momentum_step on block l's part of a per-block segment
   void sgd_block(int id, act_t* pbf, int l, cudaStream_t s) {
