@@ -659,7 +659,7 @@ struct Engine {
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
-    const bool side = use_side && !profiling && !partitioned() && !sm && !lora_rank;
+    const bool side = use_side && !profiling && !partitioned() && !sm;  // LoRA: G7 only ([Wo;W2] frozen)
     // SGD in the G5 / G7 epilogues (FusedSgd) when a training step follows;
     // G8 runs before G7 so the layer's fp16 W1 operand is updated after its
     // last reader; not with the side stream (G5 would overlap G4's W2 reads)
@@ -678,7 +678,7 @@ struct Engine {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       const act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
-      if (side) {
+      if (side && !lora_rank) {
         D2FT_CUDA(cudaEventRecord(side_event(5 * l), st));
         D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l), 0));
         g5(l, st2);
@@ -748,7 +748,7 @@ struct Engine {
           sgd_block(S_W2T, W2T_bf, l, st2);
         }
       }
-      if (side) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * l + 1), 0));  // G5 read dC
+      if (side && !lora_rank) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
       launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
                          partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
@@ -759,7 +759,7 @@ struct Engine {
     // / bias gradients and the small SGD segments overlap the side stream's
     // last G7 and block SGD (they touch none of its buffers)
     side_pending = side;
-    if (side && !step_train) join_side();
+    if (side && (!step_train || lora_rank)) join_side();  // lora_grad reads G7's output
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     if (lora_rank) {  // only the adapters train (model.hpp:155-172)
       mark(PH_BIAS);
