@@ -35,6 +35,10 @@ constexpr int kCG2 = D2FT_CG2;
 #define D2FT_CG2_BMN 1  // pair UMMA also for the MN-major-B GEMMs (G3, G8)
 #endif
 constexpr int kCG2Bmn = D2FT_CG2_BMN;
+#ifndef D2FT_EPI_WIDE_STAGES
+#define D2FT_EPI_WIDE_STAGES 3  // pipeline stages of a staged-epilogue GEMM with > 2 epilogue warpgroups
+#endif
+constexpr int kEpiWideStages = D2FT_EPI_WIDE_STAGES;
 // SGD in the G5 / G7 epilogues: opt-in.  Correct (the GPU suite passes with
 // it on) but measured slower on the ViT-B step: 7.89 vs 5.59 ms — G5's
 // row-per-thread epilogue turns the p / v read-modify-write into
@@ -592,18 +596,18 @@ struct Engine {
     constexpr int CG = !PAIR_UMMA ? 0 : (BMN ? kCG2Bmn : kCG2);
     switch (BNt) {
       case 64:
-        launch_gemm<Prob<64>, GemmShape<64, 8, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<64>{args...}, 0, st);
+        launch_gemm<Prob<64>, GemmShape<64, (!CG && EPI > 2 && epi_stage_bytes<Prob<64>>::value) ? kEpiWideStages : 8, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<64>{args...}, 0, st);
         break;
       case 128:
-        launch_gemm<Prob<128>, GemmShape<128, CG ? 8 : 6, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<128>{args...}, 0, st);
+        launch_gemm<Prob<128>, GemmShape<128, (!CG && EPI > 2 && epi_stage_bytes<Prob<128>>::value) ? kEpiWideStages : (CG ? 8 : 6), 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<128>{args...}, 0, st);
         break;
       case 208:
         // multicast B: 4 stages when the B blocks are MN-major or the epilogue stages bulk stores
-        launch_gemm<Prob<208>, GemmShape<208, CG ? 6 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? 4 : 5), 0, EPI, 2,
+        launch_gemm<Prob<208>, GemmShape<208, CG ? 6 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? (EPI > 2 ? kEpiWideStages : 4) : 5), 0, EPI, 2,
                                          BMN, AMN, CG>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
-        launch_gemm<Prob<256>, GemmShape<256, CG ? 5 : 4, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<256>{args...}, 0, st);
+        launch_gemm<Prob<256>, GemmShape<256, (!CG && EPI > 2 && epi_stage_bytes<Prob<256>>::value) ? kEpiWideStages : (CG ? 5 : 4), 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<256>{args...}, 0, st);
         break;
     }
   }
