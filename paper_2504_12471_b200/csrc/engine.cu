@@ -35,6 +35,10 @@ constexpr int kCG2 = D2FT_CG2;
 #define D2FT_CG2_BMN 1  // pair UMMA also for the MN-major-B GEMMs (G3, G8)
 #endif
 constexpr int kCG2Bmn = D2FT_CG2_BMN;
+#ifndef D2FT_BMN_ROUND
+#define D2FT_BMN_ROUND 0
+#endif
+constexpr int kBmnRound = D2FT_BMN_ROUND;
 #ifndef D2FT_EPI_WIDE_STAGES
 #define D2FT_EPI_WIDE_STAGES 3  // pipeline stages of a staged-epilogue GEMM with > 2 epilogue warpgroups
 #endif
@@ -594,7 +598,13 @@ struct Engine {
     // multicast: its epilogue is the limiter and the pair UMMA couples the two
     // CTAs' epilogues through one accumulator release (0.91 vs 0.95 ms).
     constexpr int CG = !PAIR_UMMA ? 0 : (BMN ? kCG2Bmn : kCG2);
-    switch (BNt) {
+    // Pair UMMA with MN-major B: each CTA holds BN/2 token columns of B as
+    // 64-wide swizzle blocks; a partial last block (208/2 = 104) costs a third
+    // of the mainloop rate (dense core bench), so D2FT_BMN_ROUND=1 rounds the
+    // tile up to whole blocks (the epilogue skips the columns past T).
+    int bn = BNt;
+    if (BMN && CG && kBmnRound) bn = (BNt + 127) / 128 * 128;
+    switch (bn) {
       case 64:
         launch_gemm<Prob<64>, GemmShape<64, (!CG && EPI > 2 && epi_stage_bytes<Prob<64>>::value) ? kEpiWideStages : 8, 0, EPI, 2, BMN, AMN, CG>>(a, b, Prob<64>{args...}, 0, st);
         break;

@@ -99,6 +99,12 @@ template <class P, class = void>
 struct chunk_cols : std::integral_constant<int, 16> {};
 template <class P>
 struct chunk_cols<P, std::void_t<decltype(P::kChunk)>> : std::integral_constant<int, P::kChunk> {};
+// Optional P::ncols(tile): accumulator columns that carry data (e.g. T tokens
+// of a BN-wide tile); the epilogue neither loads nor drains chunks past it.
+template <class P, class = void>
+struct has_ncols : std::false_type {};
+template <class P>
+struct has_ncols<P, std::void_t<decltype(&P::ncols)>> : std::true_type {};
 template <class P, class = void>
 struct non_empty : std::false_type {};
 template <class P>
@@ -461,7 +467,9 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       // as soon as the warp's last TMEM load has landed.
       constexpr int CW = chunk_cols<P>::value;
       const bool have = non_empty<P>::value || c.nkb > 0;
-      const int nch = (S::BN - CW * e + CW * S::EPI - 1) / (CW * S::EPI);
+      int ncol = S::BN;
+      if constexpr (has_ncols<P>::value) ncol = min(ncol, prob.ncols(c));
+      const int nch = ncol > CW * e ? (ncol - CW * e + CW * S::EPI - 1) / (CW * S::EPI) : 0;
       auto col_of = [&](int i) { return CW * e + i * CW * S::EPI; };
       typename P::Row st;
       if constexpr (epi_stage_bytes<P>::value > 0) st.stage = epi_stage + (warp - 4) * epi_stage_bytes<P>::value;

@@ -232,6 +232,7 @@ struct G3 {
     float xi[16];  // residual of the warp's next chunk (prefetched one chunk ahead)
   };
   __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ int ncols(const Tile&) const { return D.T; }
   __device__ void tile(int t, int rank, Tile& c) const {
     c.s = order[t / mpairs(D.d / 128)];
     c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
@@ -593,6 +594,7 @@ struct G8 {
     float inv;
   };
   __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ int ncols(const Tile&) const { return D.T; }
   __device__ void tile(int t, int rank, Tile& c) const {
     c.s = order[t / mpairs(D.d / 128)];
     c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
