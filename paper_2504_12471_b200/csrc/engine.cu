@@ -53,6 +53,12 @@ constexpr int kEpiWideStages = D2FT_EPI_WIDE_STAGES;
 #define D2FT_FUSE_SGD 0
 #endif
 constexpr bool kFuseSgd = D2FT_FUSE_SGD;
+#ifndef D2FT_G3_EPI
+#define D2FT_G3_EPI 4  // epilogue warpgroups of G3 / G8 (experiment builds vary them)
+#endif
+#ifndef D2FT_G8_EPI
+#define D2FT_G8_EPI 4
+#endif
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
@@ -657,7 +663,7 @@ struct Engine {
       mark(PH_G3);
       // partitioned: partial block output, residual added once (rank 0), then summed across ranks
       const float* xres = partitioned() && ex->rank != 0 ? nullptr : x + l * xs;
-      gemm_tokN<G3, 1>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
+      gemm_tokN<G3, 1, 0, D2FT_G3_EPI>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
                        P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
       if (partitioned()) {
         mark(PH_EXCH);
@@ -729,7 +735,7 @@ struct Engine {
       // bytes of G8's stores and the LN backward's reads); partitioned: fp32
       // for the cross-rank sum
       act_t* dxn_h = partitioned() ? nullptr : reinterpret_cast<act_t*>(dxn);
-      gemm_tokN<G8, 1, 1>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, dxn_h, (const float*)gmax,
+      gemm_tokN<G8, 1, 1, D2FT_G8_EPI>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, dxn_h, (const float*)gmax,
                           ord_full + l * Bm, ctr(l, C_G8));
       if (partitioned()) {
         mark(PH_EXCH);
