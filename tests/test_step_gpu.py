@@ -207,3 +207,29 @@ def test_vitl_batch_step_properties():
     assert np.array_equal(outs[0][1], O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd))
     assert np.isfinite(outs[0][0]) and outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_side_stream_schedule_is_bitwise_neutral(monkeypatch):
+    """The weight-gradient GEMMs and per-block SGD on the side stream
+    (engine default) change only the execution order: two ViT-B D2FT steps
+    give bitwise the same weights, momentum and losses as the single-stream
+    engine (D2FT_NO_SIDE)."""
+    cfg = E.VIT_B16
+    B = 16
+    x, y = E.make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    K = cfg.scheduled_subnet_count()
+    b, f = O.bench_scores(K, B, 1)
+    nb = (2 * B) // 5
+    caps = P.Capacities([nb * 5] * K, [nb * 2] * K)
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("D2FT_NO_SIDE", env)
+        else:
+            monkeypatch.delenv("D2FT_NO_SIDE", raising=False)
+        m = E.SubnetModel(cfg, B)
+        losses = [m.d2ft_step(x, y, P.ScoreTable(K, B, f, b), P.CostModel(), caps, 1, 0.05, 0.9)[0] for _ in range(2)]
+        out.append((losses, m.params(), m.velocity()))
+        m.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
