@@ -148,3 +148,16 @@ def test_lora_vitb_forward_backward_two_samples():
     bad = compare_tensors(got, rga, sl, GRAD_TOL)
     assert not bad, bad[:8]
     print("max normwise adapter-gradient error", max(normwise(got[a:b], rga[a:b]) for _, a, b in sl))
+
+
+@pytest.mark.gpu
+def test_lora_prepass_is_refused():
+    """Adapter-only pre-pass scores (visit_trainable in LoRA mode) are not
+    implemented: the engine refuses instead of returning base-tensor scores."""
+    cfg = SMALL
+    m = E.SubnetModel(cfg, 4)
+    m.attach_lora(2, 1.0)
+    x, y = E.make_synthetic_dataset(4, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    with pytest.raises(P.Error) as e:
+        m.prepass_scores(x, y, 1)
+    assert e.value.kind == "state"

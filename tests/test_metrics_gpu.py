@@ -175,3 +175,16 @@ def test_device_entry_matches_host_entry():
     assert o.tolist() == [host.compute_fraction, host.comm_fraction, host.workload_variance, host.makespan_ms,
                           host.imbalance_residual, host.row_workload_variance]
     assert busy.cpu().numpy().tolist() == host.per_device_busy_ms
+
+
+def test_empty_tables():  # cost_sim.cpp: zero cells -> 0 fractions, zero rows -> 0 variance
+    cm = CostModel()
+    m = CS._metrics(ScheduleTable(0, 0), cm)
+    assert (m.compute_fraction, m.comm_fraction, m.row_workload_variance) == (0.0, 0.0, 0.0)
+    m = CS._metrics(ScheduleTable(3, 0), cm)
+    assert (m.compute_fraction, m.comm_fraction, m.row_workload_variance) == (0.0, 0.0, 0.0)
+    assert m.row_counts.tolist() == [[0, 0, 0]] * 3
+    zero = CostModel(forward_cost=0, backward_cost=0)
+    t = ScheduleTable(2, 4, [[1, 2, 3, 1], [3, 3, 3, 3]])
+    assert CS.compute_cost_fraction(t, zero) == CO.compute_cost_fraction(t.codes, [0, 0], [0, 0]) == 0.0
+    assert CS.workload_variance(t, zero) == 0.0
