@@ -53,8 +53,14 @@ constexpr int kEpiWideStages = D2FT_EPI_WIDE_STAGES;
 #define D2FT_FUSE_SGD 0
 #endif
 constexpr bool kFuseSgd = D2FT_FUSE_SGD;
-#ifndef D2FT_G3_EPI
-#define D2FT_G3_EPI 4  // epilogue warpgroups of G3 / G8 (experiment builds vary them)
+#ifndef D2FT_G5_EPI
+#define D2FT_G5_EPI 4
+#endif
+#ifndef D2FT_G7_EPI
+#define D2FT_G7_EPI 4
+#endif
+#ifndef D2FT_G4_PAIR
+#define D2FT_G4_PAIR 1
 #endif
 #ifndef D2FT_G8_EPI
 #define D2FT_G8_EPI 4
@@ -387,7 +393,7 @@ struct Engine {
     // backward loop: part_cs slot l = column sums of the gradient entering
     // block l (slot L: entering the embedding), part_db1 slot l = G4 partials
     part_cs = dalloc<float>((L + 1) * Bm * ntile * d, owned);
-    part_db1 = dalloc<float>(L * (size_t)kEpiGroups * Bm * H * fs, owned);
+    part_db1 = dalloc<float>(L * (size_t)kG4Epi * Bm * H * fs, owned);
     part_ew = dalloc<float>((size_t)KS * d * d, owned);
     dC = dalloc<act_t>(Bm * T * d, owned);
     dO = dalloc<act_t>(Bm * H * T * D.dh, owned);
@@ -663,7 +669,7 @@ struct Engine {
       mark(PH_G3);
       // partitioned: partial block output, residual added once (rank 0), then summed across ranks
       const float* xres = partitioned() && ex->rank != 0 ? nullptr : x + l * xs;
-      gemm_tokN<G3, 1, 0, D2FT_G3_EPI>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
+      gemm_tokN<G3, 1, 0, kG3Epi>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
                        P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
       if (partitioned()) {
         mark(PH_EXCH);
@@ -689,7 +695,7 @@ struct Engine {
     // reader of the fp16 operands), overlapping the lower blocks' backward
     sgd_layer = step_train && side && side_g7 && !sm && !lora_rank && !sgd_fused;
     auto g5 = [&](int l, cudaStream_t s5) {
-      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, 4, 2, 0, 1, kCG2>>(
+      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, D2FT_G5_EPI, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
                   ord_head + l * H, ctr(l, C_G5), fsgd(S_W2T, W2T_bf, (size_t)l * d * H * D.PO)},
           s5 == st ? 0 : side_ctas, s5);
@@ -708,7 +714,7 @@ struct Engine {
         D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * (l + 1) + 3), 0));
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
-      gemm_tokN<G4, 0, 1>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
+      gemm_tokN<G4, 0, 1, kG4Epi, D2FT_G4_PAIR>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
                           (const act_t*)ZTl, db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps,
                           side ? ctr(l, C_G4) : (int*)nullptr);
       mark(PH_ATTN_B);
@@ -756,7 +762,7 @@ struct Engine {
           D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l + 2), 0));  // dY1T of block l complete
           g7s = st2;
         }
-        launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, 4, 2, 0, 1, kCG2>>(
+        launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, D2FT_G7_EPI, 2, 0, 1, kCG2>>(
             tm_xn64, tm_dY1Tb,
             G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
                       ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
@@ -839,7 +845,7 @@ struct Engine {
   size_t score_cap = 0;
 
   float* cs_slot(int k) { return part_cs + (size_t)k * D.Bmax * ((D.T + 31) / 32) * D.d; }
-  float* db1_slot(int l) { return part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs; }
+  float* db1_slot(int l) { return part_db1 + (size_t)l * kG4Epi * D.Bmax * D.H * D.fs; }
 
   // fused SGD (step_gemms.cuh FusedSgd): requested by train_body for the next
   // run_forward_backward; sgd_fused records whether the GEMMs applied it

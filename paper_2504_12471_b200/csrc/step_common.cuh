@@ -22,7 +22,17 @@ __device__ __forceinline__ float grad_scale(const float* gmax) {
 }
 
 // epilogue warpgroups of the step GEMMs (GemmShape::EPI) — G4's db1 partials
-constexpr int kEpiGroups = 4;
+// Epilogue warpgroups of G3 and G4 (their prefetch strides and G4's db1
+// partial-sum slots depend on them; engine.cu instantiates the GEMMs with the
+// same values).  G4 with 2: 0.515 vs 0.64 ms per step at 4 (ViT-B).
+#ifndef D2FT_G3_EPI
+#define D2FT_G3_EPI 4
+#endif
+#ifndef D2FT_G4_EPI
+#define D2FT_G4_EPI 2
+#endif
+constexpr int kG3Epi = D2FT_G3_EPI;
+constexpr int kG4Epi = D2FT_G4_EPI;
 // scoring pre-pass: GEMM tiles per (unit, head) partial slot (>= m-tiles (d/128 <= 8) x n-tiles (2))
 constexpr int kScoreTiles = 16;
 

@@ -270,7 +270,7 @@ struct G3 {
     float xi[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) xi[i] = r.xi[i];
-    prefetch(c, row, col0 + 16 * kEpiGroups, r);
+    prefetch(c, row, col0 + 16 * kG3Epi, r);
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (col0 + i < D.T) xout[o0 + (size_t)i * D.d] = xi[i] + v[i] + r.bias;
@@ -382,7 +382,7 @@ struct G4 {
       gz[4 * q + 2] = r.gp[q].z;
       gz[4 * q + 3] = r.gp[q].w;
     }
-    prefetch(c, row, col0 + 32 * kEpiGroups, r);
+    prefetch(c, row, col0 + 32 * kG4Epi, r);
     uint32_t hz[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

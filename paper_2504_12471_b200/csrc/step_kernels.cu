@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, const uint8_t
   const int ntile = (D.T + 31) / 32;
   const int nout = D.d + D.H * D.fs;
   const float* pcs = part_cs + (size_t)l * D.Bmax * ntile * D.d;
-  const float* pdb = part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs;
+  const float* pdb = part_db1 + (size_t)l * kG4Epi * D.Bmax * D.H * D.fs;
   float a = 0.f;
   if (i < nout) {
     if (i < D.d) {
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(1024) bias_reduce_kernel(Dims D, const uint8_t
       for (int s = warp; s < D.B; s += 32)
         if (row[s] == 1)
 #pragma unroll
-          for (int e = 0; e < kEpiGroups; ++e) a += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
+          for (int e = 0; e < kG4Epi; ++e) a += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
     }
   }
   red[warp][lane] = a;
@@ -1118,14 +1118,14 @@ __global__ void score_bias_kernel(Dims D, int mbs, int n_units, const float* par
   D2FT_PDL_ENTRY();
   const int u = blockIdx.x, h = blockIdx.y, l = blockIdx.z;
   const int ntile = (D.T + 31) / 32, w = D.d / D.H;
-  const float* pdb = part_db1 + (size_t)l * kEpiGroups * D.Bmax * D.H * D.fs;
+  const float* pdb = part_db1 + (size_t)l * kG4Epi * D.Bmax * D.H * D.fs;
   const float* pcs = part_cs + (size_t)l * D.Bmax * ntile * D.d;
   float f2 = 0.f, fa = 0.f, ft = 0.f;
   for (int j = threadIdx.x; j < D.fs + w; j += blockDim.x) {
     float g = 0.f, wt;
     if (j < D.fs) {
       for (int s = u * mbs; s < (u + 1) * mbs; ++s)
-        for (int e = 0; e < kEpiGroups; ++e) g += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
+        for (int e = 0; e < kG4Epi; ++e) g += pdb[(((size_t)e * D.Bmax + s) * D.H + h) * D.fs + j];
       wt = b1[((size_t)l * D.H + h) * D.fs + j];
     } else {
       const int m = h * w + (j - D.fs);
