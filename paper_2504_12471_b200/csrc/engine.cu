@@ -35,6 +35,10 @@ constexpr int kCG2 = D2FT_CG2;
 #define D2FT_CG2_BMN 1  // pair UMMA also for the MN-major-B GEMMs (G3, G8)
 #endif
 constexpr int kCG2Bmn = D2FT_CG2_BMN;
+#ifndef D2FT_CG_STAGES_208
+#define D2FT_CG_STAGES_208 6  // pipeline stages of the pair-UMMA N = 208 GEMMs (G3, G4, G8)
+#endif
+constexpr int kCGStages208 = D2FT_CG_STAGES_208;
 #ifndef D2FT_BMN_ROUND
 #define D2FT_BMN_ROUND 0
 #endif
@@ -625,7 +629,7 @@ struct Engine {
         break;
       case 208:
         // multicast B: 4 stages when the B blocks are MN-major or the epilogue stages bulk stores
-        launch_gemm<Prob<208>, GemmShape<208, CG ? 6 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? (EPI > 2 ? kEpiWideStages : 4) : 5), 0, EPI, 2,
+        launch_gemm<Prob<208>, GemmShape<208, CG ? kCGStages208 : ((BMN || epi_stage_bytes<Prob<208>>::value) ? (EPI > 2 ? kEpiWideStages : 4) : 5), 0, EPI, 2,
                                          BMN, AMN, CG>>(a, b, Prob<208>{args...}, 0, st);
         break;
       default:
