@@ -94,7 +94,10 @@ typedef struct d2ft_sched d2ft_sched;
 int d2ft_sched_create(int K, int N, int H, int max_cols, d2ft_sched** out);
 int d2ft_sched_destroy(d2ft_sched* s);
 /* Device pointers; lists may be NULL.  err_dev (int32, may be NULL) receives
- * the first validation failure (numeric/input/config) seen on the device. */
+ * the first validation failure seen on the device: per row, in the
+ * reference's order numeric (scores) > input (capacities) > config (costs),
+ * then size (a row needing more DP columns than max_cols of the context; the
+ * row is written as all-shortcut instead of being solved). */
 int d2ft_sched_run_device(d2ft_sched* s, const double* bwd, const double* fwd, const int32_t* cf,
                           const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, uint8_t* codes,
                           int with_lists, int32_t* err_dev, void* stream);

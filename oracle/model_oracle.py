@@ -362,6 +362,66 @@ def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, lab
     return batch_loss, touched
 
 
+_PAR = {}
+
+
+def _par_chunk(js):
+    """Worker of train_batch_parallel: the micro-batches js in order, summed
+    as the trainer does (accum += grads * (1/n_mb))."""
+    from threadpoolctl import threadpool_limits
+    a = _PAR
+    with threadpool_limits(1):
+        acc = np.zeros_like(a["flat"])
+        losses, touched = [], np.zeros(a["cfg"].K + 2, dtype=bool)
+        for j in js:
+            mbs = a["mbs"]
+            loss, gr, eng = forward_backward(a["cfg"], a["flat"], a["inputs"][j * mbs:(j + 1) * mbs],
+                                             a["labels"][j * mbs:(j + 1) * mbs], a["codes"][:, j])
+            acc += gr * a["inv_mb"]
+            losses.append(loss)
+            touched |= eng.astype(bool)
+    return losses, acc, touched
+
+
+def train_batch_parallel(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, labels, codes, mbs, lr,
+                         momentum, workers=8):
+    """train_batch with the micro-batches split over `workers` forked
+    processes (test infrastructure for batch-64 ViT parity runs).  Each worker
+    sums a contiguous run of micro-batches in order and the runs are summed in
+    order, so the gradient differs from the serial trainer's left-to-right sum
+    only by fp64 re-association (~1e-16 relative); the loss is summed in the
+    serial order.  Updates flat / velocity in place like train_batch."""
+    import multiprocessing as mp
+    codes = np.asarray(codes, dtype=np.uint8).reshape(cfg.K, -1)
+    n_mb = codes.shape[1]
+    workers = max(1, min(workers, n_mb))
+    _PAR.clear()
+    _PAR.update(cfg=cfg, flat=flat, inputs=np.asarray(inputs, np.float64), labels=np.asarray(labels), codes=codes,
+                mbs=mbs, inv_mb=1.0 / n_mb)
+    bounds = np.linspace(0, n_mb, workers + 1).astype(int)
+    runs = [list(range(bounds[i], bounds[i + 1])) for i in range(workers)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        parts = pool.map(_par_chunk, runs)
+    _PAR.clear()
+    accum = np.zeros_like(flat)
+    touched = np.zeros(cfg.K + 2, dtype=bool)
+    batch_loss = 0.0
+    for losses, acc, t in parts:
+        for loss in losses:
+            batch_loss += loss * (1.0 / n_mb)
+        accum += acc
+        touched |= t
+    for si, (a, b) in enumerate(subnet_slices(cfg)):
+        if not touched[si]:
+            continue
+        g = accum[a:b]
+        if not np.all(np.isfinite(g)):
+            raise FloatingPointError("sgd: non-finite gradient")
+        velocity[a:b] = momentum * velocity[a:b] + g
+        flat[a:b] -= lr * velocity[a:b]
+    return batch_loss, touched
+
+
 # scoring.cpp:57-96 (non-LoRA: every tensor of the block subnet) and
 # prepass_scores, scoring.cpp:108-151: per unit, forward_backward with every
 # scheduled subnet Full, then the metric of each head-subnet's unit gradient.

@@ -476,10 +476,9 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_bwd_tc_smem(D.TQ);
   D2FT_REQUIRE(attn_bwd_tc_fits(D.TQ), kConfig, "tcgen05 attention backward: shared memory");
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 223 * 1024));
-    attr = true;
   }
   dim3 grid(D.H, D.B);
   attn_bwd_tc_kernel<<<grid, 32 * kBwdWarps, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, O32T, lse, dY1T});
@@ -492,10 +491,9 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
                         const uint8_t* codes, float* O32T, cudaStream_t st) {
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_tc_smem(D.TQ);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max_attn()));
-    attr = true;
   }
   attn_fwd_tc_kernel<<<num_sms(), 384, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse, codes, O32T});
   count_launch();

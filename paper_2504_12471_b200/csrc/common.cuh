@@ -80,6 +80,17 @@ int guarded(F&& f) {
   }
 }
 
+// cudaFuncSetAttribute is per device: a call site keeps one bit per device
+// it has configured (`static unsigned long long mask; if (first_on_device(mask))`)
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
 }  // namespace d2ft_b200

@@ -929,6 +929,9 @@ struct Engine {
   void ensure_sched(int max_cols) {
     if (max_cols <= sched_max_cols) return;
     sched_max_cols = max_cols;
+    // the captured step baked in the knapsack launch's geometry (threads,
+    // shared memory, decision-bit buffer): capture again
+    drop_graph();
     bool in_smem = true;
     knapsack_smem_bytes(D.Bmax, max_cols, &in_smem);
     if (!in_smem) {
@@ -1034,6 +1037,14 @@ struct Engine {
       d2ft_b200::add_launches(g_kernels);
     }
     D2FT_CUDA(cudaGraphLaunch(gexec, st));
+  }
+
+  void drop_graph() {
+    if (gexec) {
+      D2FT_CUDA(cudaStreamSynchronize(st));
+      D2FT_CUDA(cudaGraphExecDestroy(gexec));
+      gexec = nullptr;
+    }
   }
 
   void begin_step(int B) {

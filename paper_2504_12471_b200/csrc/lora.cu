@@ -133,10 +133,9 @@ void launch_lora_merge(const Dims& D, int rank, float scaling, const float* W1T,
 void launch_lora_grad(const Dims& D, int rank, float scaling, const float* G1T, const float* A, float* AG,
                       const int* full_cnt, cudaStream_t st) {
   const int smem = (rank * D.dh + kLoraI * (D.dh + 1) + kLoraI * rank) * 4;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     D2FT_CUDA(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
   }
   lora_grad_kernel<<<D.L * D.H * 3, 256, smem, st>>>(D, rank, scaling, G1T, A, AG, full_cnt);
   count_launch();

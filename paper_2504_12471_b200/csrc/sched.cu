@@ -294,6 +294,7 @@ struct KnapsackArgs {
   SchedWorkspace ws;
   bool bits_in_smem;
   int words_max;
+  int max_cols;  // DP columns per row the launch is sized for
   bool validate;
   int lists_smem_bytes;  // dynamic shared memory of the launch (staging of the table for the column lists)
   bool cols_in_kernel;   // the last CTA builds the column lists (table staged in its shared memory)
@@ -353,24 +354,42 @@ __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
   uint8_t* s_sel = s_codes + ((N + 15) & ~15);
   uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + ((N + 15) & ~15))
                                   : A.ws.bits_global + (size_t)k * N * A.words_max;
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
+  // validation outcome: one bit per category, resolved after the barrier in
+  // the reference's order (ScoreTable::validate -> numeric, Capacities ->
+  // input, CostModel -> config; scheduler.cpp:24-43, scoring.cpp:30-47), then
+  // this launch's own column limit (size)
+  __shared__ int s_flags, s_bad;
+  if (threadIdx.x == 0) s_flags = 0;
   __syncthreads();
 
   const int cfk = A.cf[k], cbk = A.cb[k];
   if (A.validate) {
+    bool bad = false;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const double b = A.bwd[(size_t)k * N + i], f = A.fwd[(size_t)k * N + i];
-      if (!isfinite(b) || !isfinite(f) || b < 0.0 || f < 0.0) s_bad = kNumeric;  // scoring.cpp:38-41
+      bad |= !isfinite(b) || !isfinite(f) || b < 0.0 || f < 0.0;  // scoring.cpp:38-41
     }
-    if (threadIdx.x == 0 && (A.cap_full[k] < 0 || A.cap_fwd[k] < 0)) s_bad = kInput;
-    if (threadIdx.x == 0 && (cfk < 0 || cbk < 0)) s_bad = kConfig;
-    __syncthreads();
-    if (s_bad) {
-      if (threadIdx.x == 0) set_err(A.ws.err_flag, s_bad);
-      for (int i = threadIdx.x; i < N; i += blockDim.x) A.codes[(size_t)k * N + i] = 3;
-      // fall through to the compaction epilogue with an all-shortcut row
-    }
+    if (bad) atomicOr(&s_flags, 1);
+    if (threadIdx.x == 0 && (A.cap_full[k] < 0 || A.cap_fwd[k] < 0)) atomicOr(&s_flags, 2);
+    if (threadIdx.x == 0 && (cfk < 0 || cbk < 0)) atomicOr(&s_flags, 4);
+  }
+  if (threadIdx.x == 0) {
+    // device-resident capacities are not seen by the host: a row whose
+    // count-compressed DP needs more columns than this launch was sized for
+    // (thread count, decision-bit words) is refused instead of run
+    auto cols = [N](int wt, int cap) { return wt <= 0 ? 1 : min(max(cap, 0) / wt, N) + 1; };
+    if (cols(cfk + cbk, A.cap_full[k]) > A.max_cols || cols(cfk, A.cap_fwd[k]) > A.max_cols) atomicOr(&s_flags, 8);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int f = s_flags;
+    s_bad = (f & 1) ? kNumeric : (f & 2) ? kInput : (f & 4) ? kConfig : (f & 8) ? kSize : 0;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) set_err(A.ws.err_flag, s_bad);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) A.codes[(size_t)k * N + i] = 3;
+    // fall through to the compaction epilogue with an all-shortcut row
   }
   if (!s_bad) {
     // pass 1: Full pool on backward scores, weight cf+cb (scheduler.cpp:233)
@@ -706,6 +725,7 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   A.ws = ws;
   A.validate = validate;
   A.words_max = bits_words_per_item(max_cols);
+  A.max_cols = max_cols;
   size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
   // room to stage the K x N table for the last CTA's column lists (<= 48 KB)
   const size_t kn = (size_t)K * N;
@@ -715,11 +735,10 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   if (!A.bits_in_smem)
     D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(K, N, max_cols), kState,
                  "knapsack: global decision-bit workspace too small");
-  static bool attr_done = false;
-  if (!attr_done) {
+  static unsigned long long attr_done = 0;
+  if (first_on_device(attr_done)) {
     D2FT_CUDA(cudaFuncSetAttribute(knapsack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
     D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-    attr_done = true;
   }
   // rows that fit the single-warp DP need one warp (more CTAs per SM, the
   // DP's registers only for 32 threads); wider rows use the 8-warp block path

@@ -196,11 +196,12 @@ class SubnetModel:
         """model.cpp:416-520: returns (loss, grads_flat, engaged).  Gradients of
         subnets that are not engaged are zeroed here, mirroring the reference's
         disengaged optionals."""
-        x = np.ascontiguousarray(inputs, np.float32)
-        y = i32(labels)
         col = u8(schedule_column)
         if col.size != self.scheduled_count():
             raise Error(2, "schedule column must have one operation per scheduled subnet")
+        if len(inputs) == 0 or len(inputs) != len(labels):
+            raise Error(2, "micro-batch inputs and labels must be non-empty and aligned")  # model.cpp:424
+        x, y = self._batch(inputs, labels, len(labels))
         loss = C.c_double()
         check(lib().d2ft_engine_forward_backward(self._h, ptr(x), ptr(y), C.c_int(len(y)), ptr(col), C.byref(loss)))
         g = self.grads()
@@ -214,14 +215,30 @@ class SubnetModel:
 
     def step_codes(self, samples, labels, codes, mbs=1, lr=0.05, momentum=0.9) -> float:
         """Trainer batch with an explicit K x n_mb schedule table."""
-        x = np.ascontiguousarray(samples, np.float32)
-        y = i32(labels)
         c = u8(codes.codes if isinstance(codes, ScheduleTable) else codes)
+        if c.ndim != 2 or c.shape[0] != self.scheduled_count():
+            raise Error(2, f"step_codes: schedule table must be {self.scheduled_count()} x n_mb, got {c.shape}")
         n_mb = c.shape[1]
+        x, y = self._batch(samples, labels, n_mb * mbs)
         loss = C.c_double()
         check(lib().d2ft_engine_step_codes(self._h, ptr(x), ptr(y), ptr(c), C.c_int(n_mb), C.c_int(mbs),
                                            C.c_double(lr), C.c_double(momentum), C.byref(loss)))
         return loss.value
+
+    def _batch(self, samples, labels, B):
+        """Samples [B][T][d] fp32 and B labels of one batch (the C entry
+        points read exactly B of each)."""
+        x = np.ascontiguousarray(samples, np.float32)
+        y = i32(labels)
+        cfg = self.config
+        if y.ndim != 1 or y.size != B:
+            raise Error(2, f"batch of {B} units needs {B} labels, got {y.size}")
+        if x.shape != (B, cfg.seq_len, cfg.model_dim):
+            raise Error(2, f"batch of {B} units needs samples of shape {(B, cfg.seq_len, cfg.model_dim)}, "
+                           f"got {x.shape}")
+        if B > self.max_batch:
+            raise Error(6, f"batch of {B} units exceeds the engine capacity {self.max_batch}")
+        return x, y
 
     def d2ft_step(self, samples, labels, scores: ScoreTable, cost_model: CostModel, capacities: Capacities,
                   mbs=1, lr=0.05, momentum=0.9):
@@ -230,13 +247,14 @@ class SubnetModel:
         Returns (batch_loss, ScheduleTable)."""
         K, n_mb = scores.subnets, scores.micro_batches
         if K != self.scheduled_count():
-            raise Error(2, "knapsack_schedule: capacities device count mismatch")
+            raise Error(2, f"d2ft_step: score table has {K} rows, the model schedules {self.scheduled_count()} subnets")
         scores.validate()
         capacities.validate()
+        if len(capacities.full) != K or len(capacities.fwd) != K:
+            raise Error(2, "knapsack_schedule: capacities device count mismatch")
         cost_model.validate()
         cf, cb = cost_model.row_arrays(K)
-        x = np.ascontiguousarray(samples, np.float32)
-        y = i32(labels)
+        x, y = self._batch(samples, labels, n_mb * mbs)
         codes = np.zeros((K, n_mb), np.uint8)
         loss = C.c_double()
         check(lib().d2ft_engine_step(self._h, ptr(x), ptr(y), ptr(scores.backward), ptr(scores.forward), ptr(cf),
@@ -270,9 +288,11 @@ class SubnetModel:
     # -- bench path -------------------------------------------------------
     def stage(self, samples, labels, scores: ScoreTable, cost_model: CostModel, capacities: Capacities, mbs=1):
         K, n_mb = scores.subnets, scores.micro_batches
+        if K != self.scheduled_count() or len(capacities.full) != K or len(capacities.fwd) != K:
+            raise Error(2, "knapsack_schedule: capacities device count mismatch")
         cf, cb = cost_model.row_arrays(K)
-        x = np.ascontiguousarray(samples, np.float32)
-        check(lib().d2ft_engine_stage_device(self._h, ptr(x), ptr(i32(labels)), ptr(scores.backward),
+        x, y = self._batch(samples, labels, n_mb * mbs)
+        check(lib().d2ft_engine_stage_device(self._h, ptr(x), ptr(y), ptr(scores.backward),
                                              ptr(scores.forward), ptr(cf), ptr(cb), ptr(i32(capacities.full)),
                                              ptr(i32(capacities.fwd)), C.c_int(n_mb), C.c_int(mbs)))
         self._staged = (n_mb, mbs)

@@ -284,3 +284,22 @@ def test_oracle_lora_matches_reference():
     assert np.max(np.abs(a3 - a_o)) < 1e-12
     _, v3 = _split_lora(cfg, rank, r.velocity())
     assert np.max(np.abs(v3 - v_o)) < 1e-12
+
+
+def test_parallel_trainer_matches_serial():
+    """train_batch_parallel (the forked-worker oracle of the batch-64 ViT-B
+    parity test) equals the serial trainer body up to fp64 re-association."""
+    cfg = MO.Config(2, 2, 16, 32, 8, 4)
+    rng = np.random.default_rng(5)
+    flat = rng.standard_normal(MO.param_count(cfg)) * 0.3
+    x = rng.standard_normal((12, cfg.T, cfg.d))
+    y = np.arange(12) % cfg.C
+    codes = rng.integers(1, 4, (cfg.K, 6)).astype(np.uint8)
+    codes[1, :] = 3
+    p1, v1 = flat.copy(), np.zeros_like(flat)
+    p2, v2 = flat.copy(), np.zeros_like(flat)
+    for _ in range(2):
+        l1, t1 = MO.train_batch(cfg, p1, v1, x, y, codes, 2, 0.05, 0.9)
+        l2, t2 = MO.train_batch_parallel(cfg, p2, v2, x, y, codes, 2, 0.05, 0.9, workers=3)
+        assert l1 == l2 and np.array_equal(t1, t2)
+    assert np.max(np.abs(p1 - p2)) <= 1e-13 and np.max(np.abs(v1 - v2)) <= 1e-13

@@ -187,3 +187,52 @@ def test_brute_force_vs_oracle_and_dominance():
     with pytest.raises(P.Error) as e:
         P.brute_force_schedule(P.ScoreTable(1, 15, np.ones((1, 15)), np.ones((1, 15))), cm, P.Capacities([10], [2]))
     assert e.value.kind == "size"
+
+
+def test_device_capacities_beyond_context_width_are_refused():
+    """device-resident capacities bypass the host width check; a row
+    needing more DP columns than the context's max_cols must come back as a
+    size error with an all-shortcut row (not a hang or a wrong schedule), and
+    the reference's category order must win when several checks fail."""
+    import ctypes as C
+    import torch
+    from paper_2504_12471_b200._lib import lib
+    K, N, H = 4, 1600, 4
+    h = C.c_void_p()
+    assert lib().d2ft_sched_create(K, N, H, 32, C.byref(h)) == 0
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(1)
+    b = torch.tensor(rng.uniform(0, 10, (K, N)), device=dev, dtype=torch.float64)
+    f = torch.tensor(rng.uniform(0, 10, (K, N)), device=dev, dtype=torch.float64)
+    cf = torch.full((K,), 2, device=dev, dtype=torch.int32)
+    cb = torch.full((K,), 3, device=dev, dtype=torch.int32)
+    capf = torch.tensor([5 * 10, 5 * 1500, 5 * 10, 5 * 10], device=dev, dtype=torch.int32)  # row 1: 1501 columns
+    capo = torch.full((K,), 2 * 10, device=dev, dtype=torch.int32)
+    codes = torch.zeros((K, N), device=dev, dtype=torch.uint8)
+    err = torch.zeros(1, device=dev, dtype=torch.int32)
+
+    def run():
+        err.zero_()
+        rc = lib().d2ft_sched_run_device(h, C.c_void_p(b.data_ptr()), C.c_void_p(f.data_ptr()),
+                                         C.c_void_p(cf.data_ptr()), C.c_void_p(cb.data_ptr()),
+                                         C.c_void_p(capf.data_ptr()), C.c_void_p(capo.data_ptr()),
+                                         C.c_void_p(codes.data_ptr()), 0, C.c_void_p(err.data_ptr()), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        return int(err.item()), codes.cpu().numpy()
+
+    e, c = run()
+    assert e == 6 and np.all(c[1] == 3)  # kSize, row refused
+    ref = O.knapsack_schedule(b.cpu().numpy(), f.cpu().numpy(), 2, 3, capf.cpu().numpy(), capo.cpu().numpy())
+    for k in (0, 2, 3):
+        assert np.array_equal(c[k], ref[k])
+    # several failures in one row: numeric (scores) is reported before input (capacities)
+    capf[1] = -5
+    b[1, 7] = float("nan")
+    e, c = run()
+    assert e == 5 and np.all(c[1] == 3)
+    b[1, 7] = 1.0
+    cf[1] = -1
+    e, _ = run()
+    assert e == 2  # input (negative capacity) before config (negative cost)
+    lib().d2ft_sched_destroy(h)
