@@ -397,3 +397,60 @@ def ref_shuffle_iota(seed, stream, n):
     out = np.empty(n, np.int32)
     ref_lib().ref_shuffle_iota(_U64(seed), _U64(stream), _I(n), _ptr(out))
     return out
+
+
+# ------------------------------------------------------------------ reference artifact formats
+# (oracle/ref_serialize_shim.cpp over the unmodified serialize.cpp)
+def _ref_text(fn, *args):
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        n = C.c_size_t()
+        rc = fn(*args, buf, C.c_size_t(cap), C.byref(n))
+        if rc == 6 and n.value + 1 > cap:
+            cap = n.value + 1
+            continue
+        if rc:
+            ref_lib().ref_ser_last_error.restype = C.c_char_p
+            raise OracleError(rc, ref_lib().ref_ser_last_error().decode())
+        return buf.raw[:n.value].decode()
+
+
+def ref_format_double(v):
+    return _ref_text(ref_lib().ref_ser_format_double, _D(v))
+
+
+def ref_score_table_text(fwd, bwd, fwd_metric, bwd_metric, fmt):
+    f = np.ascontiguousarray(fwd, np.float64)
+    b = np.ascontiguousarray(bwd, np.float64).reshape(f.shape)
+    K, N = f.shape
+    if f.size == 0:
+        f = b = np.zeros(1)
+    return _ref_text(ref_lib().ref_ser_score_table, _I(K), _I(N), _ptr(f), _ptr(b), _I(fwd_metric), _I(bwd_metric),
+                     _I(fmt))
+
+
+def ref_schedule_table_text(codes, fmt):
+    c = np.ascontiguousarray(codes, np.uint8)
+    K, N = c.shape
+    return _ref_text(ref_lib().ref_ser_schedule_table, _I(K), _I(N), _ptr(c), _I(fmt))
+
+
+def ref_batch_metrics_text(m5, busy, run_id, method, fmt):
+    m = np.ascontiguousarray(m5, np.float64)
+    b = np.ascontiguousarray(busy if len(busy) else [0.0], np.float64)
+    return _ref_text(ref_lib().ref_ser_batch_metrics, _ptr(m), _ptr(b), _I(len(busy)), run_id.encode(),
+                     method.encode(), _I(fmt))
+
+
+def ref_history_text(epochs, fmt):
+    n = len(epochs)
+    cols = [np.ascontiguousarray([e[i] for e in epochs] or [0], np.int32 if i == 0 else np.float64) for i in range(5)]
+    return _ref_text(ref_lib().ref_ser_history, _I(n), *[_ptr(c) for c in cols], _I(fmt))
+
+
+def ref_reparse(kind, text):
+    """kind: 'score' / 'schedule' (re-emitted as JSON) or 'history' (as CSV)."""
+    fn = {"score": ref_lib().ref_ser_score_table_reparse, "schedule": ref_lib().ref_ser_schedule_table_reparse,
+          "history": ref_lib().ref_ser_history_reparse}[kind]
+    return _ref_text(fn, text.encode())

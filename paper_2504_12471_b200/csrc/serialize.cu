@@ -8,9 +8,8 @@
 // nlohmann::json::dump(2): keys in sorted order, two-space indent, one array
 // element per line, doubles as the shortest round-trip digits laid out by
 // nlohmann's format (1.0, 0.001, 1e-05, 1.5e+20, non-finite -> null).  This
-// writer reproduces that layout; digits come from std::to_chars (shortest
-// round trip), which equals nlohmann's Grisu2 output except in the rare cases
-// where Grisu2 is not shortest (the value still round-trips identically).
+// writer reproduces that layout and nlohmann's Grisu2 digits (json_double);
+// byte-compared with the compiled reference in tests/test_artifacts_vs_ref_cpu.py.
 // CSV doubles use format_double = std::to_chars, as the reference does.
 #include <array>
 #include <charconv>
@@ -37,7 +36,191 @@ std::string format_double(double v) {
   return std::string(buf, r.ptr);
 }
 
-// nlohmann::detail::to_chars layout for a finite double
+// ---- JSON doubles: nlohmann::json 3.11 dump() digits (Grisu2) and layout.
+// nlohmann prints a double with Grisu2 (Loitsch, "Printing Floating-Point
+// Numbers Quickly and Accurately with Integers", PLDI 2010): digits of the
+// upper boundary M+ of the value's rounding interval (conservatively shrunk
+// by one unit at 64-bit precision) until the rest fits the interval, then
+// one weeding step toward the value.  The result is usually but not always
+// the shortest round-trip string, so std::to_chars cannot stand in for it.
+// Restated here: 64-bit "diy" floats, the cached powers 10^k (k = -300 + 8i,
+// significands rounded to nearest; tools/gen_pow10_table.py), exponent window
+// [-60, -32].
+struct DiyFp {
+  uint64_t f;
+  int e;
+};
+
+DiyFp diy_mul(DiyFp a, DiyFp b) {  // upper 64 bits of the product, rounded half up
+  unsigned __int128 p = (unsigned __int128)a.f * b.f;
+  p += (unsigned __int128)1 << 63;
+  return DiyFp{(uint64_t)(p >> 64), a.e + b.e + 64};
+}
+
+DiyFp diy_normalize(DiyFp x) {
+  while (!(x.f >> 63)) {
+    x.f <<= 1;
+    --x.e;
+  }
+  return x;
+}
+
+struct Pow10 {
+  uint64_t f;
+  int e, k;
+};
+constexpr Pow10 kPow10[79] = {
+    {0xAB70FE17C79AC6CAull, -1060, -300},
+    {0xFF77B1FCBEBCDC4Full, -1034, -292},
+    {0xBE5691EF416BD60Cull, -1007, -284},
+    {0x8DD01FAD907FFC3Cull, -980, -276},
+    {0xD3515C2831559A83ull, -954, -268},
+    {0x9D71AC8FADA6C9B5ull, -927, -260},
+    {0xEA9C227723EE8BCBull, -901, -252},
+    {0xAECC49914078536Dull, -874, -244},
+    {0x823C12795DB6CE57ull, -847, -236},
+    {0xC21094364DFB5637ull, -821, -228},
+    {0x9096EA6F3848984Full, -794, -220},
+    {0xD77485CB25823AC7ull, -768, -212},
+    {0xA086CFCD97BF97F4ull, -741, -204},
+    {0xEF340A98172AACE5ull, -715, -196},
+    {0xB23867FB2A35B28Eull, -688, -188},
+    {0x84C8D4DFD2C63F3Bull, -661, -180},
+    {0xC5DD44271AD3CDBAull, -635, -172},
+    {0x936B9FCEBB25C996ull, -608, -164},
+    {0xDBAC6C247D62A584ull, -582, -156},
+    {0xA3AB66580D5FDAF6ull, -555, -148},
+    {0xF3E2F893DEC3F126ull, -529, -140},
+    {0xB5B5ADA8AAFF80B8ull, -502, -132},
+    {0x87625F056C7C4A8Bull, -475, -124},
+    {0xC9BCFF6034C13053ull, -449, -116},
+    {0x964E858C91BA2655ull, -422, -108},
+    {0xDFF9772470297EBDull, -396, -100},
+    {0xA6DFBD9FB8E5B88Full, -369, -92},
+    {0xF8A95FCF88747D94ull, -343, -84},
+    {0xB94470938FA89BCFull, -316, -76},
+    {0x8A08F0F8BF0F156Bull, -289, -68},
+    {0xCDB02555653131B6ull, -263, -60},
+    {0x993FE2C6D07B7FACull, -236, -52},
+    {0xE45C10C42A2B3B06ull, -210, -44},
+    {0xAA242499697392D3ull, -183, -36},
+    {0xFD87B5F28300CA0Eull, -157, -28},
+    {0xBCE5086492111AEBull, -130, -20},
+    {0x8CBCCC096F5088CCull, -103, -12},
+    {0xD1B71758E219652Cull, -77, -4},
+    {0x9C40000000000000ull, -50, 4},
+    {0xE8D4A51000000000ull, -24, 12},
+    {0xAD78EBC5AC620000ull, 3, 20},
+    {0x813F3978F8940984ull, 30, 28},
+    {0xC097CE7BC90715B3ull, 56, 36},
+    {0x8F7E32CE7BEA5C70ull, 83, 44},
+    {0xD5D238A4ABE98068ull, 109, 52},
+    {0x9F4F2726179A2245ull, 136, 60},
+    {0xED63A231D4C4FB27ull, 162, 68},
+    {0xB0DE65388CC8ADA8ull, 189, 76},
+    {0x83C7088E1AAB65DBull, 216, 84},
+    {0xC45D1DF942711D9Aull, 242, 92},
+    {0x924D692CA61BE758ull, 269, 100},
+    {0xDA01EE641A708DEAull, 295, 108},
+    {0xA26DA3999AEF774Aull, 322, 116},
+    {0xF209787BB47D6B85ull, 348, 124},
+    {0xB454E4A179DD1877ull, 375, 132},
+    {0x865B86925B9BC5C2ull, 402, 140},
+    {0xC83553C5C8965D3Dull, 428, 148},
+    {0x952AB45CFA97A0B3ull, 455, 156},
+    {0xDE469FBD99A05FE3ull, 481, 164},
+    {0xA59BC234DB398C25ull, 508, 172},
+    {0xF6C69A72A3989F5Cull, 534, 180},
+    {0xB7DCBF5354E9BECEull, 561, 188},
+    {0x88FCF317F22241E2ull, 588, 196},
+    {0xCC20CE9BD35C78A5ull, 614, 204},
+    {0x98165AF37B2153DFull, 641, 212},
+    {0xE2A0B5DC971F303Aull, 667, 220},
+    {0xA8D9D1535CE3B396ull, 694, 228},
+    {0xFB9B7CD9A4A7443Cull, 720, 236},
+    {0xBB764C4CA7A44410ull, 747, 244},
+    {0x8BAB8EEFB6409C1Aull, 774, 252},
+    {0xD01FEF10A657842Cull, 800, 260},
+    {0x9B10A4E5E9913129ull, 827, 268},
+    {0xE7109BFBA19C0C9Dull, 853, 276},
+    {0xAC2820D9623BF429ull, 880, 284},
+    {0x80444B5E7AA7CF85ull, 907, 292},
+    {0xBF21E44003ACDD2Dull, 933, 300},
+    {0x8E679C2F5E44FF8Full, 960, 308},
+    {0xD433179D9C8CB841ull, 986, 316},
+    {0x9E19DB92B4E31BA9ull, 1013, 324},
+};
+
+// Digits of the positive finite double v: v ~= digits * 10^dexp.
+void grisu2_digits(double v, std::string& digits, int& dexp) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  const uint64_t E = bits >> 52, F = bits & ((1ull << 52) - 1);
+  const DiyFp w0 = E == 0 ? DiyFp{F, -1074} : DiyFp{F + (1ull << 52), (int)E - 1075};
+  // rounding interval [m-, m+] around v; the lower neighbour is closer when v
+  // is a power of two above the smallest normal
+  const DiyFp mp0{2 * w0.f + 1, w0.e - 1};
+  const DiyFp mm0 = (F == 0 && E > 1) ? DiyFp{4 * w0.f - 1, w0.e - 2} : DiyFp{2 * w0.f - 1, w0.e - 1};
+  const DiyFp mp = diy_normalize(mp0);
+  const DiyFp mm{mm0.f << (mm0.e - mp.e), mp.e};
+  const DiyFp w = diy_normalize(w0);
+  // cached power c ~= 10^-k with -60 <= e(w * c) <= -32
+  const int fe = -60 - mp.e - 1;
+  const int kk = (fe * 78913) / (1 << 18) + (fe > 0 ? 1 : 0);
+  const Pow10 c = kPow10[(300 + kk + 7) / 8];
+  const DiyFp cw{c.f, c.e};
+  const DiyFp W = diy_mul(w, cw), Wm = diy_mul(mm, cw), Wp = diy_mul(mp, cw);
+  const DiyFp Mm{Wm.f + 1, Wm.e}, Mp{Wp.f - 1, Wp.e};
+  dexp = -c.k;
+  uint64_t delta = Mp.f - Mm.f, dist = Mp.f - W.f;
+  const int sh = -Mp.e;
+  const uint64_t one = 1ull << sh;
+  uint32_t p1 = (uint32_t)(Mp.f >> sh);
+  uint64_t p2 = Mp.f & (one - 1);
+  digits.clear();
+  // weed the last digit toward w while it stays inside the interval
+  auto round_last = [&](uint64_t rest, uint64_t ten_k) {
+    while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+      digits.back()--;
+      rest += ten_k;
+    }
+  };
+  uint32_t pow10 = 1;
+  int n = 1;
+  while (n < 10 && p1 >= pow10 * 10u) {
+    pow10 *= 10u;
+    ++n;
+  }
+  // integral part
+  while (n > 0) {
+    digits.push_back((char)('0' + p1 / pow10));
+    p1 %= pow10;
+    --n;
+    const uint64_t rest = ((uint64_t)p1 << sh) + p2;
+    if (rest <= delta) {
+      dexp += n;
+      round_last(rest, (uint64_t)pow10 << sh);
+      return;
+    }
+    pow10 /= 10u;
+  }
+  // fractional part
+  int m = 0;
+  for (;;) {
+    p2 *= 10;
+    digits.push_back((char)('0' + (p2 >> sh)));
+    p2 &= one - 1;
+    ++m;
+    delta *= 10;
+    dist *= 10;
+    if (p2 <= delta) break;
+  }
+  dexp -= m;
+  round_last(p2, one);
+}
+
+// nlohmann::detail::to_chars layout of a finite double: fixed notation for
+// 10^-4 <= |v| < 10^15 (".0" on integral values), else d.ddde[+-]XX
 std::string json_double(double v) {
   if (!std::isfinite(v)) return "null";
   std::string out;
@@ -46,14 +229,11 @@ std::string json_double(double v) {
     v = -v;
   }
   if (v == 0.0) return out + "0.0";
-  char sci[64];
-  auto r = std::to_chars(sci, sci + sizeof(sci), v, std::chars_format::scientific);
-  std::string s(sci, r.ptr);  // d[.ddd]e[+-]XX
-  const size_t epos = s.find('e');
-  std::string digits = s.substr(0, 1) + (epos > 2 ? s.substr(2, epos - 2) : "");
-  const int e10 = std::atoi(s.c_str() + epos + 1);
+  std::string digits;
+  int dexp = 0;
+  grisu2_digits(v, digits, dexp);
   const int k = (int)digits.size();
-  const int n = e10 + 1;  // value = 0.digits * 10^n
+  const int n = k + dexp;  // value = 0.digits * 10^n
   constexpr int kMinExp = -4, kMaxExp = 15;
   if (k <= n && n <= kMaxExp) return out + digits + std::string(n - k, '0') + ".0";
   if (0 < n && n <= kMaxExp) return out + digits.substr(0, n) + "." + digits.substr(n);
