@@ -30,6 +30,51 @@ namespace {
 
 constexpr int kQTile = 128;
 
+// Experiment builds (-DD2FT_ATTN_TRACE): per-CTA event stamps (SM clock) of
+// the attention kernels of one layer, read back with d2ft_debug_attn_trace.
+#ifdef D2FT_ATTN_TRACE
+// stamps go to shared memory (one 64-entry ring per warp, written by lane 0:
+// no global round trip inside the timed phases) and are copied out at exit
+constexpr int kTrCtas = 16, kTrWarps = 16, kTrPer = 96, kTrLayer = 6;
+__device__ unsigned long long g_attn_trace[2][kTrCtas][kTrWarps * kTrPer];
+__device__ int g_attn_trace_n[2][kTrCtas];
+#define ATR_DECL(nw)                                \
+  __shared__ unsigned long long tr_buf[nw][kTrPer]; \
+  int tr_n = 0;                                     \
+  constexpr int tr_nw = nw;
+#define ATR(kind, code, item)                                                                          \
+  do {                                                                                                 \
+    if ((threadIdx.x & 31) == 0 && tr_n < kTrPer && (threadIdx.x >> 5) < tr_nw)                        \
+      tr_buf[threadIdx.x >> 5][tr_n++] = ((unsigned long long)(code) << 56) |                          \
+                                         ((unsigned long long)((item) & 255) << 48) |                   \
+                                         ((unsigned long long)clock64() & 0xFFFFFFFFFFull);           \
+  } while (0)
+#define ATR_FLUSH(kind)                                                                                \
+  do {                                                                                                 \
+    const int b_ = blockIdx.x + blockIdx.y * gridDim.x, w_ = threadIdx.x >> 5;                         \
+    if (a.l == kTrLayer && b_ < kTrCtas && (threadIdx.x & 31) == 0 && w_ < tr_nw) {                    \
+      for (int i_ = 0; i_ < kTrPer; ++i_)                                                              \
+        g_attn_trace[kind][b_][w_ * kTrPer + i_] = i_ < tr_n ? tr_buf[w_][i_] | ((unsigned long long)w_ << 40) : 0ull; \
+      atomicAdd(&g_attn_trace_n[kind][b_], tr_n);                                                      \
+    }                                                                                                  \
+  } while (0)
+#define ATR_Q(kind, code, item) \
+  do {                          \
+    if (q4 == 0) ATR(kind, code, item); \
+  } while (0)
+#else
+#define ATR_DECL(nw)
+#define ATR_FLUSH(kind) \
+  do {                  \
+  } while (0)
+#define ATR_Q(kind, code, item) \
+  do {                          \
+  } while (0)
+#define ATR(kind, code, item) \
+  do {                        \
+  } while (0)
+#endif
+
 // 2^x on the SFU (ex2.approx.ftz: ~2 ulp; P is rounded to fp16 right after)
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
@@ -37,6 +82,47 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 constexpr float kLog2eF = 1.4426950408889634f;
+
+// 2^x for x <= 0 on the FMA pipe: round-to-nearest split x = j + f
+// (|f| <= 1/2) by the 1.5 * 2^23 shifter, 2^f by a degree-4 fit (Chebyshev
+// nodes on [-1/2, 1/2], relative error 3.5e-6 — below the fp16 rounding P
+// gets next), j added to the exponent field.  x is clamped at -125 (P rounds
+// to 0 in fp16 far above that).
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(0.00966637f, f, 0.05592198f);
+  p = fmaf(p, f, 0.24022349f);
+  p = fmaf(p, f, 0.69312105f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// Forward softmax variants (experiment builds; defaults = the measured best):
+//   D2FT_ATTN_POLY   exponentials per 16 computed by exp2_poly (the rest on the SFU)
+//   D2FT_AF_FREE     release the O accumulator's TMEM columns after its last load
+//   D2FT_AF_SKIPDEAD warps whose 32 queries all lie past T skip the softmax
+//   D2FT_AF_SINGLE   one read of the scores against a running reference max
+#ifndef D2FT_ATTN_POLY
+#define D2FT_ATTN_POLY 0
+#endif
+#ifndef D2FT_AF_FREE
+#define D2FT_AF_FREE 0
+#endif
+#ifndef D2FT_AF_SKIPDEAD
+#define D2FT_AF_SKIPDEAD 0
+#endif
+#ifndef D2FT_AF_SINGLE
+#define D2FT_AF_SINGLE 0
+#endif
+constexpr int kPolyExp = D2FT_ATTN_POLY;
+constexpr bool kFreeEarly = D2FT_AF_FREE, kSkipDead = D2FT_AF_SKIPDEAD;
+constexpr int kFwdSmWarps = 4;  // softmax warps per query tile (one per TMEM lane quarter)
+constexpr int kFwdThreads = 128 + 2 * 32 * kFwdSmWarps;
+// largest excess of a later chunk's max over the running reference before
+// the stored P is rescaled: P <= 2^8, well inside fp16
+constexpr float kRescaleGap = 8.f;
 
 struct AttnFwdArgs {
   Dims D;
@@ -48,6 +134,7 @@ struct AttnFwdArgs {
   float* lse;  // block l
   const uint8_t* codes;  // expanded K x Bmax (code 1 = Full)
   float* O32T;           // block l: [Bmax][H][64][TP] fp32 O of Full cells (the backward's D)
+  float gap;             // softmax rescale threshold (kRescaleGap; D2FT_ATTN_RESCALE_GAP overrides, tests)
 };
 
 __host__ __device__ inline int attn_fwd_stage_bytes(int TQ) {
@@ -60,10 +147,11 @@ __host__ __device__ inline int attn_tc_smem(int TQ) { return 2 * attn_fwd_stage_
 // warp 2 TMEM allocator, warps 4-7 / 8-11 = softmax+epilogue of query tile
 // 0 / 1 (TMEM columns [0,256) / [256,512)), so both tiles of an item run in
 // parallel and the next item's operands land during the current one.
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const AttnFwdArgs a) {
   pdl_trigger();
+  ATR_DECL(12)
   const Dims& D = a.D;
   const int TQ = D.TQ, T = D.T;
   const int nkv = (TQ + 63) / 64, nqt = (T + kQTile - 1) / kQTile;
@@ -83,9 +171,9 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&load_full[i], 1);
       ptx::mbar_init(&load_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&p_full[i], kFwdSmWarps);
       ptx::mbar_init(&o_full[i], 1);
-      ptx::mbar_init(&tfree[i], 4);
+      ptx::mbar_init(&tfree[i], kFwdSmWarps);
     }
     ptx::fence_barrier_init();
   }
@@ -107,6 +195,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
         const int buf = it & 1;
         ptx::mbar_wait(&load_empty[buf], ((it >> 1) & 1) ^ 1);
+        ATR(0, 0, it);
         int s, h;
         decode(i, s, h);
         const int plane = (a.l * D.Bmax + s) * D.H + h;
@@ -126,11 +215,13 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
       const int buf = it & 1;
       ptx::mbar_wait(&load_full[buf], (it >> 1) & 1);
+      if (lane == 0) ATR(0, 1, it);
       ptx::tc_fence_after();
       const uint32_t qb = ptx::smem_u32(smem + buf * stage);
       const uint32_t kb = qb + 2 * kQTile * 128, vb = kb + TQ * 128;
       for (int t = 0; t < nqt; ++t) {
         ptx::mbar_wait(&tfree[t], (it & 1) ^ 1);
+        if (lane == 0) ATR(0, 2 + t, it);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           const uint64_t qd = ptx::desc_sw128(qb + t * kQTile * 128), kd = ptx::desc_sw128(kb);
@@ -143,6 +234,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       for (int t = 0; t < nqt; ++t) {
         ptx::mbar_wait(&p_full[t], it & 1);
+        if (lane == 0) ATR(0, 4 + t, it);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           for (int kk = 0; kk < TQ / 16; ++kk)
@@ -155,59 +247,78 @@ __global__ void __launch_bounds__(384, 1)
       if (ptx::elect_one()) ptx::umma_commit(&load_empty[buf]);
       __syncwarp();
     }
+#if D2FT_AF_SINGLE == 0
   } else if (warp >= 4 && (warp - 4) / 4 < nqt) {
+    // One warp per TMEM lane quarter of each query tile; thread = query row:
+    // row max, then P = 2^(s*sl2 - max) as fp16 pairs written back over S,
+    // then O / rowsum out of TMEM.
     const int t = (warp - 4) / 4, q4 = warp & 3;
     const uint32_t base = tmem + 256 * t + ((uint32_t)(q4 * 32) << 16);
     const float sl2 = kLog2eF * 0.125f;  // log2(e) / sqrt(64)
     const int cfull = T & ~15;           // chunks [0, cfull) hold valid keys only
     const int row = t * kQTile + q4 * 32 + lane;  // query
+    // a warp whose 32 queries all lie past T has nothing to compute: its P
+    // rows only feed O rows that are never stored (MMA rows are independent)
+    const bool live = !kSkipDead || t * kQTile + q4 * 32 < T;
     for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
       int s, h;
       decode(i, s, h);
       const size_t sh = (size_t)s * D.H + h;
       ptx::mbar_wait(&s_full[t], it & 1);
+      ATR_Q(0, 10 + 8 * t, it);
       ptx::tc_fence_after();
-      float mx = -INFINITY;
-      for (int c0 = 0; c0 < TQ; c0 += 16) {
-        float v[16];
-        ptx::tmem_ld16(base + c0, v);
-        if (c0 < cfull) {
+      float mx = -INFINITY, sum = 0.f;
+      if (live) {
+        for (int c0 = 0; c0 < TQ; c0 += 16) {
+          float v[16];
+          ptx::tmem_ld16(base + c0, v);
+          if (c0 < cfull) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v[j]);
-        } else {
+            for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v[j]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < T) mx = fmaxf(mx, v[j]);
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < T) mx = fmaxf(mx, v[j]);
+          }
         }
+        mx *= sl2;
+        ATR_Q(0, 11 + 8 * t, it);
+        for (int c0 = 0; c0 < TQ; c0 += 16) {
+          float v[16];
+          if (it == 1) ATR_Q(0, 30, c0 >> 4);
+          ptx::tmem_ld16(base + c0, v);
+          if (it == 1) ATR_Q(0, 31, c0 >> 4);
+          float p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x = fmaf(v[j], sl2, -mx);
+            p[j] = j < kPolyExp ? exp2_poly(x) : fast_exp2(x);
+          }
+          if (it == 1) ATR_Q(0, 32, c0 >> 4);
+          if (c0 >= cfull) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j >= T) p[j] = 0.f;
+          }
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            sum += p[2 * j] + p[2 * j + 1];
+            __half2 hp = __floats2half2_rn(p[2 * j], p[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&hp);
+          }
+          ptx::tmem_st8(base + (c0 >> 1), pk);
+          if (it == 1) ATR_Q(0, 33, c0 >> 4);
+        }
+        ptx::tmem_st_wait();
       }
-      mx *= sl2;
-      float sum = 0.f;
-      for (int c0 = 0; c0 < TQ; c0 += 16) {
-        float v[16];
-        ptx::tmem_ld16(base + c0, v);
-        float p[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) p[j] = fast_exp2(fmaf(v[j], sl2, -mx));
-        if (c0 >= cfull) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j >= T) p[j] = 0.f;
-        }
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sum += p[2 * j] + p[2 * j + 1];
-          __half2 hp = __floats2half2_rn(p[2 * j], p[2 * j + 1]);
-          pk[j] = *reinterpret_cast<uint32_t*>(&hp);
-        }
-        ptx::tmem_st8(base + (c0 >> 1), pk);
-      }
-      ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      ATR_Q(0, 12 + 8 * t, it);
       if (row < T) a.lse[sh * T + row] = mx + log2f(sum);
       ptx::mbar_wait(&o_full[t], it & 1);
+      ATR_Q(0, 13 + 8 * t, it);
       ptx::tc_fence_after();
       const float inv = 1.f / sum;
       act_t* o = a.OGT + sh * D.PO * D.TP + row;
@@ -217,26 +328,189 @@ __global__ void __launch_bounds__(384, 1)
       // the wq/wk gradients at ViT-L)
       const bool full = a.codes[(size_t)(a.l * D.H + h) * D.Bmax + s] == 1;
       float* o32 = a.O32T + sh * 64 * D.TP + row;
+      if (live) {
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        float v[16];
-        ptx::tmem_ld16(base + 128 + c0, v);
-        if (row < T) {
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          float v[16];
+          ptx::tmem_ld16(base + 128 + c0, v);
+          if (kFreeEarly && c0 == 48) {  // the accumulator is in registers: release its columns
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+          }
+          if (row < T) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) o[(size_t)(c0 + j) * D.TP] = to_act(v[j] * inv);
-          if (full) {
+            for (int j = 0; j < 16; ++j) o[(size_t)(c0 + j) * D.TP] = to_act(v[j] * inv);
+            if (full) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) o32[(size_t)(c0 + j) * D.TP] = v[j] * inv;
+              for (int j = 0; j < 16; ++j) o32[(size_t)(c0 + j) * D.TP] = v[j] * inv;
+            }
           }
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+      if (!kFreeEarly || !live) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+      }
+      ATR_Q(0, 14 + 8 * t, it);
     }
   }
+#else  // D2FT_AF_SINGLE: single read of the scores against a running reference max
+  } else if (warp >= 4 && (warp - 4) / 4 < nqt) {
+    // One warp per TMEM lane quarter of each query tile; thread = query row.
+    // TMEM reads bound this loop, so each score is read once:
+    // the row's reference max m comes from its first 64 columns (kept in
+    // registers), every later chunk is exponentiated against m, and a chunk
+    // whose max exceeds m by more than kRescaleGap (P would leave the fp16
+    // range) rescales the P already stored by 2^(m - m') first (rare).
+    // lse = m + log2(sum) holds for any m, so no second pass is needed.
+    const int t = (warp - 4) / 4, q4 = warp & 3;
+    const uint32_t base = tmem + 256 * t + ((uint32_t)(q4 * 32) << 16);
+    const float sl2 = kLog2eF * 0.125f;  // log2(e) / sqrt(64)
+    const int row = t * kQTile + q4 * 32 + lane;  // query
+    // a warp whose 32 queries all lie past T has nothing to compute: its P
+    // rows only feed O rows that are never stored (MMA rows are independent)
+    const bool live = t * kQTile + q4 * 32 < T;
+    const int nch = TQ / 16, npre = nch < 4 ? nch : 4;
+    for (int i = blockIdx.x, it = 0; i < nitems; i += gridDim.x, ++it) {
+      int s, h;
+      decode(i, s, h);
+      const size_t sh = (size_t)s * D.H + h;
+      // Full cells also keep O in fp32 (the backward's D = rowsum(dO . O) must be
+      // consistent with its dP = dO V^T to the fp32 level: the softmax backward
+      // dP - D cancels strongly when tokens are alike; an fp16 O costs ~1e-2 on
+      // the wq/wk gradients at ViT-L).  Loaded before the waits.
+      const bool full = a.codes[(size_t)(a.l * D.H + h) * D.Bmax + s] == 1;
+      ptx::mbar_wait(&s_full[t], it & 1);
+      ATR_Q(0, 10 + 8 * t, it);
+      ptx::tc_fence_after();
+      float m = 0.f, sum = 0.f;
+      if (live) {
+        auto exp_chunk = [&](const uint32_t (&v)[16], int c0) {
+          float p[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float x = fmaf(__uint_as_float(v[e]), sl2, -m);
+            p[e] = e < kPolyExp ? exp2_poly(x) : fast_exp2(x);
+          }
+          if (c0 + 16 > T) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (c0 + e >= T) p[e] = 0.f;
+          }
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            sum += p[2 * e] + p[2 * e + 1];
+            __half2 hp = __floats2half2_rn(p[2 * e], p[2 * e + 1]);
+            pk[e] = *reinterpret_cast<uint32_t*>(&hp);
+          }
+          ptx::tmem_st8(base + (c0 >> 1), pk);
+        };
+        auto chunk_max = [&](const uint32_t (&v)[16], int c0) {
+          float x = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (c0 + e < T) x = fmaxf(x, __uint_as_float(v[e]));
+          return x * sl2;
+        };
+        uint32_t pre[4][16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < npre) ptx::tmem_ld16_async(base + 16 * j, pre[j]);
+        ptx::tmem_ld_wait(pre[0]);
+        ptx::tmem_ld_wait(pre[1]);
+        ptx::tmem_ld_wait(pre[2]);
+        ptx::tmem_ld_wait(pre[3]);
+        m = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < npre) m = fmaxf(m, chunk_max(pre[j], 16 * j));
+        uint32_t cur[16], nxt[16];
+        if (npre < nch) ptx::tmem_ld16_async(base + 16 * npre, cur);  // in flight during the prologue's math
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < npre) exp_chunk(pre[j], 16 * j);
+        ATR_Q(0, 11 + 8 * t, it);
+        if (npre < nch) ptx::tmem_ld_wait(cur);
+        for (int j = npre; j < nch; ++j) {
+          const int c0 = 16 * j;
+          if (j + 1 < nch) ptx::tmem_ld16_async(base + c0 + 16, nxt);
+          const float cm = chunk_max(cur, c0);
+          if (__any_sync(0xffffffffu, cm > m + a.gap)) {
+            // rare: P of chunks [0, j) to the new reference (lanes that do not
+            // need it scale by 1)
+            const float mn = fmaxf(m, cm);
+            const float f = fast_exp2(m - mn);
+            const __half2 f2 = __float2half2_rn(f);
+            ptx::tmem_st_wait();
+            for (int jj = 0; jj < j; ++jj) {
+              uint32_t q[8];
+              ptx::tmem_ld8_async(base + 8 * jj, q);
+              ptx::tmem_ld_wait(q);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                __half2 hv = __hmul2(*reinterpret_cast<__half2*>(&q[e]), f2);
+                q[e] = *reinterpret_cast<uint32_t*>(&hv);
+              }
+              ptx::tmem_st8(base + 8 * jj, q);
+            }
+            sum *= f;
+            m = mn;
+          }
+          exp_chunk(cur, c0);
+          if (j + 1 < nch) {
+            ptx::tmem_ld_wait(nxt);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) cur[e] = nxt[e];
+          }
+        }
+        ptx::tmem_st_wait();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      ATR_Q(0, 12 + 8 * t, it);
+      if (live && row < T) a.lse[sh * T + row] = m + log2f(sum);
+      const float inv = 1.f / sum;
+      ptx::mbar_wait(&o_full[t], it & 1);
+      ATR_Q(0, 13 + 8 * t, it);
+      ptx::tc_fence_after();
+      if (live) {
+        act_t* og = a.OGT + sh * D.PO * D.TP + row;
+        float* o32 = a.O32T + sh * 64 * D.TP + row;
+        uint32_t o[16];
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          ptx::tmem_ld16_async(base + 128 + c0, o);
+          ptx::tmem_ld_wait(o);
+          if (c0 == 48) {  // the accumulator is in registers: release the columns
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+          }
+          if (row < T) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) og[(size_t)(c0 + e) * D.TP] = to_act(__uint_as_float(o[e]) * inv);
+            if (full) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o32[(size_t)(c0 + e) * D.TP] = __uint_as_float(o[e]) * inv;
+            }
+          }
+        }
+      } else {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tfree[t]);
+      }
+      ATR_Q(0, 14 + 8 * t, it);
+    }
+  }
+#endif
   ptx::tc_fence_before();
   __syncthreads();
+  ATR_FLUSH(0);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
@@ -279,6 +553,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmdO,
                        const AttnBwdArgs a) {
   D2FT_PDL_ENTRY();
+  ATR_DECL(1)
   const Dims& D = a.D;
   const int s = blockIdx.y, slot = blockIdx.x;
   if (s >= D.B || slot >= a.full_hcnt[s * D.L + a.l]) return;
@@ -314,6 +589,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (threadIdx.x == 0) ATR(1, 0, slot);
   if (threadIdx.x == 0) {
     ptx::mbar_arrive_expect_tx(&bar[0], 4 * tile_bytes);
     ptx::tma_load_3d(sQ, &tmQKV, &bar[0], 0, 0, plane);
@@ -348,6 +624,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     if (hf == 0 && q < TQ) Dv[q] = acc;
   }
   __syncthreads();
+  if (threadIdx.x == 0) ATR(1, 1, slot);
 
   const float sl2 = kLog2eF * 0.125f;
   const float scale = 0.125f;  // 1 / sqrt(64)
@@ -374,6 +651,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       ptx::umma_commit(&bar[1]);
     }
     ptx::mbar_wait(&bar[1], kt & 1);
+    if (threadIdx.x == 0) ATR(1, 2 + 4 * kt, slot);
     ptx::tc_fence_after();
     const int k = kt * kQTile + q4 * 32 + lane;  // this thread's key (TMEM lane)
     const bool kv = k < T;
@@ -410,6 +688,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) ATR(1, 3 + 4 * kt, slot);
     if (threadIdx.x == 0) {
       ptx::tc_fence_after();
       for (int kk = 0; kk < TQ / 16; ++kk) {
@@ -421,6 +700,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       ptx::umma_commit(&bar[2]);
     }
     ptx::mbar_wait(&bar[2], kt & 1);
+    if (threadIdx.x == 0) ATR(1, 4 + 4 * kt, slot);
     ptx::tc_fence_after();
     {
       const int c0 = 16 * cg;  // this warp's 16 of the 64 dV / dK columns
@@ -437,6 +717,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();  // TMEM regions free for the next key tile
+    if (threadIdx.x == 0) ATR(1, 5 + 4 * kt, slot);
   }
   // dQ = dS K: query tiles of 128 (two 64-wide MN-major blocks of dS^T each)
   if (threadIdx.x == 0) {
@@ -450,6 +731,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     ptx::umma_commit(&bar[3]);
   }
   ptx::mbar_wait(&bar[3], 0);
+  if (threadIdx.x == 0) ATR(1, 20, slot);
   ptx::tc_fence_after();
   for (int qt = 0; qt < nkt; ++qt) {
     const int q = qt * kQTile + q4 * 32 + lane;
@@ -463,6 +745,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATR(1, 21, slot);
+  ATR_FLUSH(1);
   if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
@@ -495,12 +779,36 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
   if (first_on_device(attr)) {
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max_attn()));
   }
-  attn_fwd_tc_kernel<<<num_sms(), 384, sm, st>>>(tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse, codes, O32T});
+  const char* g = getenv("D2FT_ATTN_RESCALE_GAP");  // tests force the rescale path with a small gap
+  const float gap = g ? (float)atof(g) : kRescaleGap;
+  attn_fwd_tc_kernel<<<num_sms(), kFwdThreads, sm, st>>>(
+      tmQ, tmK, tmV, AttnFwdArgs{D, l, items, count, act_heads, OGT, lse, codes, O32T, gap});
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 int sm_max_attn() { return attn_tc_smem(256); }
+
+}  // namespace d2ft_b200
+
+#ifdef D2FT_ATTN_TRACE
+// experiment builds: copy the trace (kind 0 forward, 1 backward) of one launch
+// of layer kTrLayer; out = [kTrCtas][kTrWarps * kTrPer] u64 stamps
+// (code << 56 | item << 48 | warp << 40 | 40-bit SM clock), counts = [kTrCtas]; clears it
+extern "C" int d2ft_debug_attn_trace(int kind, unsigned long long* out, int* counts) {
+  using namespace d2ft_b200;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace[0]), kind * sizeof(g_attn_trace[0]));
+  static unsigned long long zt[kTrCtas][kTrWarps * kTrPer] = {};
+  cudaMemcpyToSymbol(g_attn_trace, zt, sizeof(zt), kind * sizeof(zt));
+  cudaMemcpyFromSymbol(counts, g_attn_trace_n, sizeof(g_attn_trace_n[0]), kind * sizeof(g_attn_trace_n[0]));
+  static int zero[kTrCtas] = {};
+  cudaMemcpyToSymbol(g_attn_trace_n, zero, sizeof(zero), kind * sizeof(zero));
+  return (int)cudaGetLastError();
+}
+#endif
+
+namespace d2ft_b200 {
 bool attn_bwd_tc_fits(int TQ) { return attn_bwd_tc_smem(TQ) + 4096 <= 227 * 1024; }  // + static shared
 
 }  // namespace d2ft_b200
