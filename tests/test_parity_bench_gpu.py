@@ -174,27 +174,3 @@ def test_dh64_d2ft_step_graph(mbs):
     bad = compare_tensors(vg, vr, sl, GRAD_TOL)
     assert not bad, bad[:8]
 
-
-@pytest.mark.parametrize("gap", ["0", "-1"])
-def test_attention_rescale_path(monkeypatch, gap):
-    """The forward softmax reads each score once against a running reference
-    max and rescales the stored P when a later chunk exceeds it by more than
-    a gap (csrc/attn_sm100.cu).  With the gap forced to 0 / -1 the rescale
-    path runs on most chunks; the results must stay within the step
-    tolerances of the fp64 oracle (T = 197: 13 score chunks per row)."""
-    monkeypatch.setenv("D2FT_ATTN_RESCALE_GAP", gap)
-    cfg = MID64
-    oc, sl = _cfgs(cfg)
-    p = _perturbed(cfg)
-    x, y = E.make_synthetic_dataset(8, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
-    x, y = x[:3], y[:3]
-    K = cfg.scheduled_subnet_count()
-    col = np.array([(1, 2, 3, 1)[k % 4] for k in range(K)], np.uint8)
-    m = E.SubnetModel(cfg, 3, p)
-    loss, g, eng = m.forward_backward(x, y, col)
-    m.close()
-    rl, rg, reng = MO.forward_backward(oc, p, x.astype(np.float64), y, col)
-    assert np.array_equal(eng, reng)
-    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
-    bad = compare_tensors(g, rg, sl, GRAD_TOL)
-    assert not bad, bad[:8]
