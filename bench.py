@@ -56,7 +56,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-vitl", action="store_true", help="skip the ViT-L/16 batch-256 1-GPU leg")
+    ap.add_argument("--no-vitl", action="store_true", help="skip the ViT-L/16 batch-256 leg")
+    ap.add_argument("--mapping", default="heads", choices=["heads", "contiguous"],
+                    help="N > 1: row -> GPU mapping (head-interleaved, or the SPEC-literal contiguous one)")
+    ap.add_argument("--exchange-chunks", type=int, default=2, help="N > 1: sample chunks of the per-block exchange")
+    ap.add_argument("--uniform-caps", action="store_true",
+                    help="N > 1: the same budget on every rank (no BudgetSpec rebalancing)")
     return ap.parse_args()
 
 
@@ -66,35 +71,72 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    """SM clock and throttle-reason sampling DURING the timed region
+    (B200_PROFILING.md clocks line).  The device-resident step train lasts
+    ~50-100 ms, shorter than nvidia-smi's sampling period, so the samples come
+    from NVML (pynvml, the library nvidia-smi queries) polled every ~2 ms on a
+    thread while the timed C call runs (ctypes releases the GIL); nvidia-smi
+    is the fallback when pynvml is missing."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu):
         self.gpu = gpu
-        self.rows = []
+        self.rows = []  # (sm_mhz, sm_max_mhz, [active reason flags x4])
         self._stop = threading.Event()
+        self._first = threading.Event()
+        self.source = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        try:
+            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            self.source = "nvml"
+            while not self._stop.is_set():
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, mx, [bool(r & b) for b in bits]))
+                self._first.set()
+                time.sleep(0.002)
+        finally:
+            N.nvmlShutdown()
+
+    def _run_smi(self):
         try:
             p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, text=True)
+                                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
         except Exception:
+            self._first.set()
             return
         self.proc = p
+        self.source = "nvidia-smi"
         for line in p.stdout:
             if self._stop.is_set():
                 break
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+            if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]), [x.lower() == "active" for x in parts[3:7]]))
+                self._first.set()
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
+        self._first.set()
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
-        time.sleep(0.3)
+        self._first.wait(timeout=5.0)  # the sampler is live before the timed region starts
+        self.rows.clear()
         return self
 
     def __exit__(self, *a):
@@ -106,16 +148,15 @@ class Clocks:
                 p.wait(timeout=2)
             except Exception:
                 p.kill()
+        self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        rows = list(self.rows)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[2][i]})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "source": self.source}
 
 
 def workload(B):
@@ -178,11 +219,13 @@ def lora_leg(x, y, fwd, bwd, capf, capo, B, steps=10, warmup=3, rank=8):
             "ms_per_step": ms_step, "steps": steps, "warmup": warmup, "loss": loss.value}
 
 
-def vitl_leg(steps=3, warmup=2, B=256):
+def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
     """BASELINE configs[3]'s model and batch (ViT-L/16, L24 H16 d1024 ffn4096,
-    batch 256) on ONE B200: device-resident steps, same schedule recipe and
-    data generators as the headline.  The config names 8 B200 (head partition,
-    --gpus 8); this leg reports what a single GPU does with that batch."""
+    batch 256): device-resident steps, same schedule recipe and data
+    generators as the headline.  world == 1: what one B200 does with that
+    batch; world > 1 (the config's 8 B200): the head partition over all ranks
+    (16 heads / 8 = 2 per block per rank, NCCL exchange), the batch fixed at
+    256 (strong scaling), time = max over ranks."""
     from paper_2504_12471_b200 import _lib
     from paper_2504_12471_b200 import engine as E
     from paper_2504_12471_b200 import scheduler as S
@@ -199,10 +242,20 @@ def vitl_leg(steps=3, warmup=2, B=256):
     nb = (2 * B) // 5
     capf, capo = np.full(K, nb * 5, np.int32), np.full(K, nb * 2, np.int32)
     m = E.SubnetModel(cfg, B)
+    if dist:
+        from paper_2504_12471_b200 import partition as PT
+        PT.join_nccl(m, PT.HeadPartition(Hq, rank, world, args.mapping, Lq), chunks=args.exchange_chunks)
     m.stage(x, y, S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
     ms, loss = C.c_double(), C.c_double()
+    if dist:
+        dist.barrier()
     _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
                                             C.c_int(warmup), C.c_int(steps), C.byref(ms), C.byref(loss)))
+    if dist:
+        import torch
+        t = torch.tensor([ms.value], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = C.c_double(float(t.item()))
     codes = np.zeros((K, B), np.uint8)
     _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes)))
     m.close()
@@ -212,12 +265,25 @@ def vitl_leg(steps=3, warmup=2, B=256):
     alg = 3 * Fk * full + Fk * (act - full) + 4.0 * T * Dq * Dq * B
     ms_step = ms.value / steps
     tf = alg / (ms_step * 1e-3) / 1e12
-    peak = PEAKS["bf16_tflops_sustained"]
+    peak = PEAKS["bf16_tflops_sustained"] * world
+    if dist:  # this rank's rows only: the global table's FLOPs
+        full = float(sum(dist_sum(full, dist)))
+        act = float(sum(dist_sum(act, dist)))
+        alg = 3 * Fk * full + Fk * (act - full) + 4.0 * T * Dq * Dq * B
+    where = f"{world} B200, head partition (NCCL)" if dist else "1 B200 (BASELINE configs[3] names 8 B200)"
     return {"workload": f"ViT-L/16 (L24 H16 d1024 ffn4096 T197, {K} head-subnets) D2FT step, batch {B}, "
-                        f"per-sample schedule, 1 B200 (BASELINE configs[3] names 8 B200)",
+                        f"per-sample schedule, {where}",
             "value": B / (ms_step * 1e-3), "unit": "samples/s", "ms_per_step": ms_step, "steps": steps,
             "warmup": warmup, "loss": loss.value, "tflop_per_step": alg / 1e12, "achieved_tflops": round(tf, 1),
             "frac": round(tf / peak, 4)}
+
+
+def dist_sum(v, dist):
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(o.item()) for o in out]
 
 
 def ref_workload(B):
@@ -382,10 +448,17 @@ def run_ours(args):
     cfg = E.VIT_B16
     m = E.SubnetModel(cfg, B)
     part = None
+    budget = None
     if dist:
         from paper_2504_12471_b200 import partition as PT
-        part = PT.HeadPartition(H, rank, world)
-        PT.join_nccl(m, part)
+        part = PT.HeadPartition(H, rank, world, args.mapping, L)
+        PT.join_nccl(m, part, chunks=args.exchange_chunks)
+        if not args.uniform_caps:  # per-rank budgets (BudgetSpec overrides) balance the mapping
+            nb = (2 * B) // 5
+            spec, caps_r = PT.rank_capacities(part, L, B, nb, nb)
+            capf, capo = np.array(caps_r.full, np.int32), np.array(caps_r.fwd, np.int32)
+            budget = {"base": [nb, nb], "per_rank": sorted({(spec.n_full_for(k), spec.n_fwd_for(k))
+                                                            for k in range(K)})}
     cm = S.CostModel()
     st = S.ScoreTable(K, B, fwd, bwd)
     caps = S.Capacities(capf.tolist(), capo.tolist())
@@ -430,25 +503,32 @@ def run_ours(args):
     fl, alg_total = gemm_flops(codes_exp, B)
     if dist:
         glob = global_codes(bwd, fwd, capf, capo, B)
-        _, unit_ratio = PT.busy_units(glob, H, world)
-        part_info = {"mapping": "head h -> rank h % N (tensor parallel over heads)",
-                     "heads_per_rank": [len(PT.HeadPartition(H, r, world).owned_heads()) for r in range(world)],
+        owners = part.row_owners(L)
+        _, unit_ratio = PT.busy_units(glob, H, world, owners=owners)
+        xcalls, xbytes = PT.exchange_stats(m)
+        part_info = {"mapping": ("head h -> rank h % N (tensor parallel over heads)" if args.mapping == "heads" else
+                                 "contiguous rows per rank (cost_sim.cpp:138-152)"),
+                     "rows_per_rank": np.bincount(owners, minlength=world).tolist(),
+                     "budget": budget or "uniform",
                      "busy_ms_per_rank": [round(b, 3) for b in bl],
                      "busy_max_over_mean": round(max(bl) / (sum(bl) / len(bl)), 4),
                      "cost_units_max_over_mean": round(unit_ratio, 4),
                      "exchange_ms_per_step": round(phases.get("exchange", 0.0), 3),
-                     "exchange_bytes_per_step": 2 * L * B * T * D * 4}
+                     "exchange_chunks": args.exchange_chunks,
+                     "exchange_bytes_per_step": 2 * L * B * T * D * 4,
+                     "exchange_calls_total": xcalls, "exchange_bytes_total": xbytes}
     # ---- schedule metrics of this batch on the GPU (cost_sim.cpp:109-172 with
     # the MEASURED per-device busy time in place of the calibrated table): the
     # rows each rank owns (head h of every block -> rank h % N) are grouped so
     # the reference's in-order row-to-device mapping applies
     from paper_2504_12471_b200 import cost_sim as CSIM
     gcodes = glob if dist else codes_exp
-    order = [k for r in range(world) for k in range(K) if (k % H) % world == r]
+    own = part.row_owners(L) if dist else np.zeros(K, np.int32)
+    order = [k for r in range(world) for k in range(K) if own[k] == r]
     profs = []
     for r in range(world):
         p = CSIM.DeviceProfile.standard(r)
-        p.memory_units = sum(1 for k in range(K) if (k % H) % world == r)
+        p.memory_units = int((own == r).sum())
         profs.append(p)
     bm = CSIM.simulate_batch(S.ScheduleTable(K, B, gcodes[order]), profs, cm,
                              S.Capacities(capf[order].tolist(), capo[order].tolist()),
@@ -563,9 +643,9 @@ def run_ours(args):
         except Exception as e:
             lora = {"error": str(e)[:200]}
     vitl = None
-    if rank == 0 and world == 1 and not args.no_vitl:
+    if not args.no_vitl and (world == 1 or world == 8):
         try:
-            vitl = vitl_leg()
+            vitl = vitl_leg(rank=rank, world=world, dist=dist, args=args)
         except Exception as e:  # reported, never fatal for the headline line
             vitl = {"error": str(e)[:200]}
     if rank == 0:
@@ -609,7 +689,7 @@ def run_ours(args):
         if part_info:
             line["partition"] = part_info
         if vitl:
-            line["vitl_1gpu"] = vitl
+            line["vitl_1gpu" if world == 1 else f"vitl_{world}gpu"] = vitl
         if prepass:
             line["prepass"] = prepass
         print(json.dumps(line))

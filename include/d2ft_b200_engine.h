@@ -146,6 +146,18 @@ int d2ft_engine_partition_nccl(d2ft_engine* e, int rank, int world, const uint8_
 int d2ft_local_group_create(int world, d2ft_local_group** out);
 int d2ft_local_group_destroy(d2ft_local_group* g);
 int d2ft_engine_partition_local(d2ft_engine* e, d2ft_local_group* g, int rank);
+/* row -> rank mapping of a partitioned engine: owner[k] for every scheduled
+ * subnet row k = l*H + h (default after joining: h % world, head-interleaved;
+ * partition.py also builds the SPEC-literal contiguous mapping of
+ * cost_sim.cpp:138-152, memory_units consecutive rows per device) */
+int d2ft_engine_set_row_owner(d2ft_engine* e, const int32_t* owner, int K);
+/* the per-block exchanges run per sample chunk (1..8, default 2 or
+ * $D2FT_EXCH_CHUNKS) on an exchange stream, overlapping the next chunk's
+ * G3 / G8 and the previous chunk's LayerNorm */
+int d2ft_engine_set_exchange_chunks(d2ft_engine* e, int chunks);
+/* all-reduce calls issued by this rank so far and their payload bytes
+ * (graph replays included) */
+int d2ft_engine_exchange_stats(d2ft_engine* e, unsigned long long* calls, unsigned long long* bytes);
 
 /* select the CUDA device for subsequent engine/scheduler creation on this thread */
 int d2ft_set_device(int device);

@@ -189,11 +189,55 @@ struct Engine {
   std::unique_ptr<Exchange> ex;
   CUtensorMap* store_maps;  // device copies of the epilogue bulk-store maps: [0] ZT, [1] OGT, [2] QKV (G1), [3] dO, [4] dY1T (G4)
   int* full_any;  // [B][L] Full heads of the sample in the block over ALL ranks (LN-backward gate)
-  bool partitioned() const { return ex && ex->world > 1; }
+  // Partitioned whenever an exchange is attached, world 1 included: the
+  // partition's data path (owner mask, fp32 partial sums, the all-reduce
+  // call) then runs on a one-GPU box as well.
+  bool partitioned() const { return ex != nullptr; }
+  int* row_owner = nullptr;  // [K] rank owning scheduled row k (partition mapping, partition.py)
+  // Exchange stream and chunks: G3 / G8 run per sample chunk [c*B/C, (c+1)*B/C)
+  // and each chunk's all-reduce runs on xst while the next chunk computes;
+  // the LayerNorm of a chunk waits only for that chunk's sum.
+  static constexpr int kMaxXChunks = 8;
+  cudaStream_t xst = nullptr;
+  int xchunks = getenv("D2FT_EXCH_CHUNKS") ? atoi(getenv("D2FT_EXCH_CHUNKS")) : 2;
+  std::vector<cudaEvent_t> xev;  // [dir][L][chunk][ready, done]
+  int active_chunks() const {
+    if (!partitioned() || profiling) return 1;
+    return std::max(1, std::min(std::min(xchunks, kMaxXChunks), D.B));
+  }
+  int chunk_lo(int c, int C) const { return (int)((long long)c * D.B / C); }
+  bool async_exchange() const { return partitioned() && !profiling; }
+  cudaEvent_t xevent(int dir, int l, int c, int kind) {
+    if (xev.empty()) {
+      xev.resize((size_t)2 * D.L * kMaxXChunks * 2);
+      for (auto& e : xev) D2FT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return xev[(((size_t)dir * D.L + l) * kMaxXChunks + c) * 2 + kind];
+  }
+  // exchange of rows [lo, lo+n) of a [B][T][d] fp32 buffer after the producer
+  // (on st) finished them: on xst with events, or inline when profiling
+  void exchange_chunk(int dir, int l, int c, float* buf, int lo, int n) {
+    const size_t row = (size_t)D.T * D.d;
+    if (!async_exchange()) {
+      mark(PH_EXCH);
+      ex->allreduce_sum(buf + (size_t)lo * row, (size_t)n * row, st);
+      return;
+    }
+    D2FT_CUDA(cudaEventRecord(xevent(dir, l, c, 0), st));
+    D2FT_CUDA(cudaStreamWaitEvent(xst, xevent(dir, l, c, 0), 0));
+    ex->allreduce_sum(buf + (size_t)lo * row, (size_t)n * row, xst);
+    D2FT_CUDA(cudaEventRecord(xevent(dir, l, c, 1), xst));
+  }
+  void wait_exchange(int dir, int l, int c) {
+    if (async_exchange()) D2FT_CUDA(cudaStreamWaitEvent(st, xevent(dir, l, c, 1), 0));
+  }
   int* ctrs;                           // dynamic tile counters: [L][8] + 8, zeroed per pass
-                                       // (the variable-K GEMMs; uniform ones stay static)
+                                       // (the variable-K GEMMs; uniform ones stay static),
+                                       // then [L][2][kMaxXChunks] for the chunked G3 / G8
   enum { C_G3, C_G5, C_G7, C_G8, C_G4 };
   int* ctr(int l, int kind) { return ctrs + (l < 0 ? (size_t)D.L * 8 : (size_t)l * 8) + kind; }
+  int* xctr(int l, int dir, int c) { return ctrs + (size_t)(D.L + 1) * 8 + ((size_t)l * 2 + dir) * kMaxXChunks + c; }
+  size_t ctr_count() const { return (size_t)(D.L + 1) * 8 + (size_t)D.L * 2 * kMaxXChunks; }
   uint32_t* sched_bits = nullptr;
   size_t sched_bits_words = 0;
   unsigned int* sched_counter;
@@ -227,6 +271,7 @@ struct Engine {
   int g_nmb = -1, g_mbs = -1;
   float g_lr = 0.f, g_mom = 0.f;
   unsigned long long g_kernels = 0;  // kernels per replay (for d2ft_launch_count)
+  unsigned long long g_xcalls = 0, g_xbytes = 0;  // exchange calls / bytes per replay (partitioned)
   bool use_graphs = getenv("D2FT_NO_GRAPH") == nullptr;
   // opt-in (D2FT_PDL=1): measured slower on the ViT-B step (6.13 / 5.96 ms with
   // early / implicit trigger vs 5.88 ms plain graph edges)
@@ -348,6 +393,9 @@ struct Engine {
     if (ev_stage_free) cudaEventDestroy(ev_stage_free);
     if (cst) cudaStreamDestroy(cst);
     for (auto e : side_ev) cudaEventDestroy(e);
+    for (auto e : xev) cudaEventDestroy(e);
+    ex.reset();  // the communicator before its stream
+    if (xst) cudaStreamDestroy(xst);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
@@ -441,7 +489,8 @@ struct Engine {
     ord_act = dalloc<int>(L * Bm, owned);
     ord_full = dalloc<int>(L * Bm, owned);
     ord_head = dalloc<int>(L * H, owned);
-    ctrs = dalloc<int>((L + 1) * 8, owned);
+    ctrs = dalloc<int>(ctr_count(), owned);
+    row_owner = dalloc<int>(L * H, owned);
     full_any = dalloc<int>(L * Bm, owned);
     store_maps = dalloc<CUtensorMap>(8, owned);
     af_items = dalloc<int>(L * Bm * H, owned);
@@ -650,12 +699,22 @@ struct Engine {
     const size_t L = D.L, Bm = D.Bmax, T = D.T, d = D.d, H = D.H;
     const size_t xs = Bm * T * d;
     mark(PH_EMBED);
-    D2FT_CUDA(cudaMemsetAsync(ctrs, 0, (L + 1) * 8 * sizeof(int), st));
+    D2FT_CUDA(cudaMemsetAsync(ctrs, 0, ctr_count() * sizeof(int), st));
     launch_prep_input(D, samples_dev, inp, inpT, st);
     gemm_tokN<EmbedFwd>(tm_WeT, tm_inp, D, P + seg[S_BE].off, P + seg[S_POS].off, x);
+    const int XC = active_chunks();
     for (int l = 0; l < D.L; ++l) {
       mark(PH_LN);
-      launch_ln_fwd(D, x + l * xs, xn + l * xs, stats + (size_t)l * Bm * T * 2, st);
+      if (l == 0 || !partitioned()) {
+        launch_ln_fwd(D, x + l * xs, xn + l * xs, stats + (size_t)l * Bm * T * 2, st);
+      } else {  // chunk c of x_l as soon as its exchange is done
+        for (int c = 0; c < XC; ++c) {
+          const int lo = chunk_lo(c, XC), n = chunk_lo(c + 1, XC) - lo;
+          if (!n) continue;
+          wait_exchange(0, l - 1, c);
+          launch_ln_fwd(D, x + l * xs, xn + l * xs, stats + (size_t)l * Bm * T * 2, st, lo, n);
+        }
+      }
       mark(PH_G1);
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
@@ -671,15 +730,23 @@ struct Engine {
       else
         launch_attn_fwd(D, l, lists.act_heads, lists.act_cnt, QKVl, OGTl, lse + (size_t)l * Bm * H * T, st);
       mark(PH_G3);
-      // partitioned: partial block output, residual added once (rank 0), then summed across ranks
+      // partitioned: partial block output, residual added once (rank 0), then
+      // summed across ranks chunk by chunk (the sum of chunk c overlaps G3 of c+1)
       const float* xres = partitioned() && ex->rank != 0 ? nullptr : x + l * xs;
-      gemm_tokN<G3, 1, 0, kG3Epi>(tm_W2T, tm_OGT64, D, l, lists.act_heads, lists.act_cnt, codes_exp,
-                       P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm, ctr(l, C_G3));
-      if (partitioned()) {
-        mark(PH_EXCH);
-        ex->allreduce_sum(x + (l + 1) * xs, (size_t)D.B * T * d, st);
+      for (int c = 0; c < XC; ++c) {
+        const int lo = chunk_lo(c, XC), n = chunk_lo(c + 1, XC) - lo;
+        if (!n) continue;
+        Dims Dc = D;
+        Dc.B = n;  // G3's tiles: the chunk's samples in ord_act[lo, lo+n)
+        gemm_tokN<G3, 1, 0, kG3Epi>(tm_W2T, tm_OGT64, Dc, l, lists.act_heads, lists.act_cnt, codes_exp,
+                         P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm + lo,
+                         XC > 1 ? xctr(l, 0, c) : ctr(l, C_G3));
+        if (partitioned()) exchange_chunk(0, l, c, x + (l + 1) * xs, lo, n);
       }
     }
+    if (partitioned())
+      for (int c = 0; c < XC; ++c)
+        if (chunk_lo(c + 1, XC) > chunk_lo(c, XC)) wait_exchange(0, (int)L - 1, c);
     mark(PH_HEAD);
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
     launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off,
@@ -689,7 +756,7 @@ struct Engine {
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
-    const bool side = use_side && !profiling && !partitioned() && !sm;  // LoRA: G7 only ([Wo;W2] frozen)
+    const bool side = use_side && !profiling && !sm;  // LoRA: G7 only ([Wo;W2] frozen)
     // SGD in the G5 / G7 epilogues (FusedSgd) when a training step follows;
     // G8 runs before G7 so the layer's fp16 W1 operand is updated after its
     // last reader; not with the side stream (G5 would overlap G4's W2 reads)
@@ -745,11 +812,15 @@ struct Engine {
       // bytes of G8's stores and the LN backward's reads); partitioned: fp32
       // for the cross-rank sum
       act_t* dxn_h = partitioned() ? nullptr : reinterpret_cast<act_t*>(dxn);
-      gemm_tokN<G8, 1, 1, D2FT_G8_EPI>(tm_W1T, tm_dY1T, D, l, lists.full_heads, lists.full_hcnt, dxn, dxn_h, (const float*)gmax,
-                          ord_full + l * Bm, ctr(l, C_G8));
-      if (partitioned()) {
-        mark(PH_EXCH);
-        ex->allreduce_sum(dxn, (size_t)D.B * T * d, st);
+      for (int c = 0; c < XC; ++c) {  // per exchange chunk, as G3
+        const int lo = chunk_lo(c, XC), n = chunk_lo(c + 1, XC) - lo;
+        if (!n) continue;
+        Dims Dc = D;
+        Dc.B = n;
+        gemm_tokN<G8, 1, 1, D2FT_G8_EPI>(tm_W1T, tm_dY1T, Dc, l, lists.full_heads, lists.full_hcnt, dxn, dxn_h,
+                                         (const float*)gmax, ord_full + l * Bm + lo,
+                                         XC > 1 ? xctr(l, 1, c) : ctr(l, C_G8));
+        if (partitioned()) exchange_chunk(1, l, c, dxn, lo, n);
       }
       if (sgd_layer) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 4), st));  // last reader of W1T_bf[l] / W2T_bf[l]
       mark(PH_G7);
@@ -780,9 +851,15 @@ struct Engine {
       }
       if (side && !lora_rank) D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * l + 1), 0));  // G5 read dC
       mark(PH_LN_BWD);
-      launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
-                         partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
-                         partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st);
+      for (int c = 0; c < XC; ++c) {
+        const int lo = chunk_lo(c, XC), n = chunk_lo(c + 1, XC) - lo;
+        if (!n) continue;
+        if (partitioned()) wait_exchange(1, l, c);
+        launch_ln_bwd_prep(D, l, partitioned() ? full_any : lists.full_hcnt, x + l * xs,
+                           partitioned() ? nullptr : xn + l * xs, stats + (size_t)l * Bm * T * 2,
+                           partitioned() ? dxn : nullptr, dxn_h, dX, dC, cs_slot(l == 0 ? (int)L : l - 1), gmax, st,
+                           lo, n);
+      }
     }
     // everything on the side stream (G5, G7, per-block SGD) joins here, or —
     // in a training step — after the remaining SGD (train_body), so the embed
@@ -918,12 +995,12 @@ struct Engine {
       launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
       D2FT_CUDA(cudaMemcpyAsync(full_any, lists.full_hcnt, (size_t)D.L * D.Bmax * sizeof(int),
                                 cudaMemcpyDeviceToDevice, st));
-      launch_mask_rows(codes_exp, D.K(), D.Bmax, D.H, ex->rank, ex->world, st);
+      launch_mask_rows(codes_exp, D.K(), D.Bmax, row_owner, ex->rank, st);
     }
     launch_compact(codes_exp, D.K(), D.Bmax, D.H, lists, st);
     launch_plan(D, lists.act_cnt, lists.full_hcnt, lists.full_cnt,
                 Plan{g1_tiles, g1_count, g4_tiles, g4_count, ord_act, ord_full, ord_head, af_items, af_count, ab_items,
-                     ab_count}, st);
+                     ab_count, active_chunks()}, st);
   }
 
   void ensure_sched(int max_cols) {
@@ -1009,7 +1086,7 @@ struct Engine {
 
   // schedule + forward/backward + SGD on the staged device inputs (after begin_step)
   void compute_step(int n_mb, int mbs, double lr, double momentum) {
-    if (profiling || partitioned() || !use_graphs) {
+    if (profiling || (partitioned() && !ex->capturable()) || !use_graphs) {
       schedule_device(n_mb, mbs);
       train_body((float)lr, (float)momentum);
       return;
@@ -1021,11 +1098,14 @@ struct Engine {
       }
       cudaGraph_t g = nullptr;
       const unsigned long long n0 = d2ft_b200::launch_count();
+      const unsigned long long xc0 = ex ? ex->calls : 0, xb0 = ex ? ex->bytes : 0;
       D2FT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       schedule_device(n_mb, mbs);
       train_body((float)lr, (float)momentum);
       D2FT_CUDA(cudaStreamEndCapture(st, &g));
       g_kernels = d2ft_b200::launch_count() - n0;
+      g_xcalls = ex ? ex->calls - xc0 : 0;
+      g_xbytes = ex ? ex->bytes - xb0 : 0;
       if (use_pdl) make_edges_programmatic(g);
       D2FT_CUDA(cudaGraphInstantiate(&gexec, g, 0));
       D2FT_CUDA(cudaGraphDestroy(g));
@@ -1035,8 +1115,33 @@ struct Engine {
       g_mom = (float)momentum;
     } else {
       d2ft_b200::add_launches(g_kernels);
+      if (ex) {  // the replay issues the captured all-reduces again
+        ex->calls += g_xcalls;
+        ex->bytes += g_xbytes;
+      }
     }
     D2FT_CUDA(cudaGraphLaunch(gexec, st));
+  }
+
+  // a partition was attached: exchange stream, default head-interleaved
+  // mapping (row k = l*H + h -> rank h % world), the captured step is stale
+  void on_partition() {
+    drop_graph();
+    if (!xst) {
+      int least = 0, greatest = 0;
+      D2FT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      D2FT_CUDA(cudaStreamCreateWithPriority(&xst, cudaStreamNonBlocking, greatest));
+    }
+    std::vector<int> own(D.K());
+    for (int k = 0; k < D.K(); ++k) own[k] = (k % D.H) % ex->world;
+    set_row_owner(own.data());
+  }
+  void set_row_owner(const int* owner) {
+    D2FT_REQUIRE(ex, kState, "row owner: the engine is not partitioned");
+    for (int k = 0; k < D.K(); ++k)
+      D2FT_REQUIRE(owner[k] >= 0 && owner[k] < ex->world, kConfig, "row owner: rank out of range");
+    drop_graph();
+    D2FT_CUDA(cudaMemcpy(row_owner, owner, (size_t)D.K() * sizeof(int), cudaMemcpyHostToDevice));
   }
 
   void drop_graph() {
@@ -1191,6 +1296,7 @@ int d2ft_engine_partition_nccl(d2ft_engine* h, int rank, int world, const uint8_
     Engine& E = *h->e;
     D2FT_CUDA(cudaStreamSynchronize(E.st));
     E.ex = make_nccl_exchange(rank, world, id);
+    E.on_partition();
   });
 }
 
@@ -1220,6 +1326,7 @@ int d2ft_engine_partition_local(d2ft_engine* h, d2ft_local_group* g, int rank) {
     Engine& E = *h->e;
     D2FT_CUDA(cudaStreamSynchronize(E.st));
     E.ex = make_local_exchange(g->g, rank);
+    E.on_partition();
   });
 }
 
@@ -1470,6 +1577,33 @@ int d2ft_engine_sync(d2ft_engine* h, double* loss_out) {
 }
 
 void* d2ft_engine_stream(d2ft_engine* h) { return h && h->e ? (void*)h->e->st : nullptr; }
+
+int d2ft_engine_set_row_owner(d2ft_engine* h, const int32_t* owner, int K) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && owner, kInput, "set_row_owner: null argument");
+    D2FT_REQUIRE(K == h->e->D.K(), kInput, "set_row_owner: one owner per scheduled subnet");
+    D2FT_CUDA(cudaStreamSynchronize(h->e->st));
+    h->e->set_row_owner(owner);
+  });
+}
+
+int d2ft_engine_set_exchange_chunks(d2ft_engine* h, int chunks) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e, kInput, "set_exchange_chunks: null argument");
+    D2FT_REQUIRE(chunks >= 1 && chunks <= Engine::kMaxXChunks, kConfig, "exchange chunks: 1..8");
+    h->e->drop_graph();
+    h->e->xchunks = chunks;
+  });
+}
+
+int d2ft_engine_exchange_stats(d2ft_engine* h, unsigned long long* calls, unsigned long long* bytes) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && calls && bytes, kInput, "exchange_stats: null argument");
+    D2FT_CUDA(cudaStreamSynchronize(h->e->st));
+    *calls = h->e->ex ? h->e->ex->calls : 0;
+    *bytes = h->e->ex ? h->e->ex->bytes : 0;
+  });
+}
 
 int d2ft_engine_set_profiling(d2ft_engine* h, int on) {
   return guarded([&] {

@@ -56,9 +56,12 @@ struct NcclExchange final : Exchange {
     if (comm) nccl().comm_destroy(comm);
   }
   void allreduce_sum(float* buf, size_t n, cudaStream_t st) override {
-    if (world == 1 || n == 0) return;
+    if (n == 0) return;
     D2FT_NCCL(nccl().all_reduce(buf, buf, n, ncclFloat32, ncclSum, comm, st));
+    ++calls;
+    bytes += n * sizeof(float);
   }
+  bool capturable() const override { return true; }
 };
 }  // namespace
 
@@ -132,8 +135,12 @@ struct LocalExchange final : Exchange {
   ~LocalExchange() override {
     if (tmp) cudaFree(tmp);
   }
+  bool capturable() const override { return false; }  // host-side barrier between the ranks
   void allreduce_sum(float* buf, size_t n, cudaStream_t st) override {
-    if (world == 1 || n == 0) return;
+    if (n == 0) return;
+    ++calls;
+    bytes += n * sizeof(float);
+    if (world == 1) return;  // the sum over one rank is the buffer itself
     if (n > cap) {
       if (tmp) D2FT_CUDA(cudaFree(tmp));
       D2FT_CUDA(cudaMalloc(&tmp, n * sizeof(float)));
@@ -153,12 +160,12 @@ struct LocalExchange final : Exchange {
   }
 };
 
-__global__ void mask_rows_kernel(uint8_t* codes, int K, int Bmax, int H, int rank, int world) {
+__global__ void mask_rows_kernel(uint8_t* codes, int K, int Bmax, const int* owner, int rank) {
   D2FT_PDL_ENTRY();
   const size_t n = (size_t)K * Bmax;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / Bmax);
-    if ((k % H) % world != rank) codes[i] = 3;
+    if (owner[k] != rank) codes[i] = 3;
   }
 }
 }  // namespace
@@ -172,11 +179,11 @@ std::unique_ptr<Exchange> make_local_exchange(LocalGroup* g, int rank) {
   return x;
 }
 
-void launch_mask_rows(uint8_t* codes, int K, int Bmax, int H, int rank, int world, cudaStream_t st) {
+void launch_mask_rows(uint8_t* codes, int K, int Bmax, const int* owner, int rank, cudaStream_t st) {
   const size_t n = (size_t)K * Bmax;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  mask_rows_kernel<<<blocks, 256, 0, st>>>(codes, K, Bmax, H, rank, world);
+  mask_rows_kernel<<<blocks, 256, 0, st>>>(codes, K, Bmax, owner, rank);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

@@ -16,9 +16,14 @@ namespace d2ft_b200 {
 
 struct Exchange {
   int rank = 0, world = 1;
+  unsigned long long calls = 0, bytes = 0;  // all-reduces issued and their payload bytes (this rank)
   virtual ~Exchange() = default;
-  // in place: buf[i] <- sum over ranks of buf[i]; stream-ordered on `st`
+  // in place: buf[i] <- sum over ranks of buf[i]; stream-ordered on `st`.
+  // Every call is issued, world 1 included (the NCCL data path runs on a
+  // one-GPU box too).
   virtual void allreduce_sum(float* buf, size_t n, cudaStream_t st) = 0;
+  // stream-ordered without host synchronisation (can be captured in a CUDA graph)
+  virtual bool capturable() const = 0;
 };
 
 void nccl_unique_id(uint8_t out[128]);
@@ -29,7 +34,7 @@ LocalGroup* local_group_create(int world);
 void local_group_destroy(LocalGroup* g);
 std::unique_ptr<Exchange> make_local_exchange(LocalGroup* g, int rank);
 
-// codes[k][s] = 3 (skip) for the rows k whose head (k % H) another rank owns
-void launch_mask_rows(uint8_t* codes, int K, int Bmax, int H, int rank, int world, cudaStream_t st);
+// codes[k][s] = 3 (skip) for the scheduled rows k another rank owns (owner[k] != rank)
+void launch_mask_rows(uint8_t* codes, int K, int Bmax, const int* owner, int rank, cudaStream_t st);
 
 }  // namespace d2ft_b200

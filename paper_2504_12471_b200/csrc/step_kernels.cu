@@ -31,6 +31,17 @@ __device__ __forceinline__ int desc_rank(const int* v, int n, int i) {
   for (int j = 0; j < n; ++j) r += (v[j] > x) | ((v[j] == x) & (j < i));
   return r;
 }
+// the same within i's sample chunk [c*n/C, (c+1)*n/C) (exchange chunks of a
+// head partition): position = chunk start + rank in the chunk
+__device__ __forceinline__ int desc_rank_chunked(const int* v, int n, int chunks, int i) {
+  if (chunks <= 1) return desc_rank(v, n, i);
+  int lo = 0, hi = n;
+  for (int c = 0; c < chunks; ++c) {
+    const int a = (int)((long long)c * n / chunks), b = (int)((long long)(c + 1) * n / chunks);
+    if (i >= a && i < b) lo = a, hi = b;
+  }
+  return lo + desc_rank(v + lo, hi - lo, i - lo);
+}
 
 __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, Plan pl) {
   D2FT_PDL_ENTRY();
@@ -53,8 +64,8 @@ __global__ void plan_kernel(Dims D, const int* act_cnt, const int* full_hcnt, co
   // cost orders of the dynamically scheduled GEMMs: samples by active / Full
   // head count (G3, G8), heads by Full sample count (G5, G7), largest first
   if (s < D.B) {
-    pl.ord_act[l * D.Bmax + desc_rank(va, D.B, s)] = s;
-    pl.ord_full[l * D.Bmax + desc_rank(vf, D.B, s)] = s;
+    pl.ord_act[l * D.Bmax + desc_rank_chunked(va, D.B, pl.chunks, s)] = s;
+    pl.ord_full[l * D.Bmax + desc_rank_chunked(vf, D.B, pl.chunks, s)] = s;
   }
   if (s < D.H) pl.ord_head[l * D.H + desc_rank(vh, D.H, s)] = s;
   for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scans
@@ -147,9 +158,9 @@ __device__ __forceinline__ void st4h(act_t* p, float a, float b, float c, float 
 }
 
 template <int NV>
-__global__ void __launch_bounds__(512) ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats) {
+__global__ void __launch_bounds__(512) ln_fwd_kernel(Dims D, const float* x, act_t* xn, float* stats, int s0) {
   D2FT_PDL_ENTRY();
-  const int s = blockIdx.y, t0 = blockIdx.x * 32;
+  const int s = s0 + blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NQ = NV / 4;
   for (int r = warp; r < 32; r += blockDim.x >> 5) {
@@ -186,11 +197,11 @@ constexpr int kLnbWarps = 16;  // LN backward: 32 tokens per CTA, 2 rows per war
 template <int NV>
 __global__ void __launch_bounds__(32 * kLnbWarps) ln_bwd_prep_kernel(Dims D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
                                    const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
-                                   float* part_cs, const float* gmax) {
+                                   float* part_cs, const float* gmax, int s0) {
   D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   float* cs = reinterpret_cast<float*>(smem);  // [kLnbWarps][d] per-warp column sums
-  const int s = blockIdx.y, t0 = blockIdx.x * 32;
+  const int s = s0 + blockIdx.y, t0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NQ = NV / 4;
   const bool do_ln = l >= 0 && full_hcnt[s * D.L + l] > 0;  // model.cpp:508
@@ -976,22 +987,26 @@ void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, c
   D2FT_CUDA(cudaGetLastError());
 }
 
-void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st) {
-  dim3 grid((D.T + 31) / 32, D.B);
-  D2FT_NV_DISPATCH(D.d, { ln_fwd_kernel<NV><<<grid, 512, 0, st>>>(D, x, xn, stats); });  // 2 rows per warp
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st, int s0, int ns) {
+  if (ns < 0) ns = D.B;
+  if (ns == 0) return;
+  dim3 grid((D.T + 31) / 32, ns);
+  D2FT_NV_DISPATCH(D.d, { ln_fwd_kernel<NV><<<grid, 512, 0, st>>>(D, x, xn, stats, s0); });  // 2 rows per warp
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
 
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
                         const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
-                        float* part_cs, const float* gmax, cudaStream_t st) {
-  dim3 grid((D.T + 31) / 32, D.B);
+                        float* part_cs, const float* gmax, cudaStream_t st, int s0, int ns) {
+  if (ns < 0) ns = D.B;
+  if (ns == 0) return;
+  dim3 grid((D.T + 31) / 32, ns);
   const size_t sm = (size_t)kLnbWarps * D.d * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(ln_bwd_prep_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     ln_bwd_prep_kernel<NV><<<grid, 32 * kLnbWarps, sm, st>>>(D, l, full_hcnt, x_l, xn_l, stats_l, dxn, dxn_h, dX, dC,
-                                                              part_cs, gmax);
+                                                              part_cs, gmax, s0);
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());

@@ -19,13 +19,15 @@ struct Plan {
   int* ord_head;  // [L][H] heads by decreasing Full-sample count (G5, G7)
   int *af_items, *af_count;  // [L][Bmax*H] (sample << 8 | active slot) of the attention forward
   int *ab_items, *ab_count;  // [L][Bmax*H] (sample << 8 | Full slot) of the attention backward
+  int chunks = 1;  // ord_act / ord_full sorted within sample chunks [c*B/C, (c+1)*B/C) (head-partition exchange)
 };
 void launch_plan(const Dims& D, const int* act_cnt, const int* full_hcnt, const int* full_cnt, const Plan& pl,
                  cudaStream_t st);
 // fp32 samples [B][T][d] -> act_t token-major + feature-major copies
 void launch_prep_input(const Dims& D, const float* x, act_t* inp, act_t* inpT, cudaStream_t st);
-// LayerNorm (no affine, eps 1e-5) of x -> xn (token-major fp16), stats (mean, rstd)
-void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st);
+// LayerNorm (no affine, eps 1e-5) of x -> xn (token-major fp16), stats (mean, rstd);
+// samples [s0, s0 + ns) (ns < 0: the whole batch D.B)
+void launch_ln_fwd(const Dims& D, const float* x, act_t* xn, float* stats, cudaStream_t st, int s0 = 0, int ns = -1);
 // attention forward / backward (one CTA per (sample, active|Full head) slot)
 // (O feature-major into OGT rows 0..dh-1; dq|dk|dv feature-major into dY1T rows 0..3dh-1)
 void launch_attn_fwd(const Dims& D, int l, const int* act_heads, const int* act_cnt, const act_t* Y1, act_t* OGT,
@@ -54,7 +56,7 @@ void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled
 // x_l (fp32) or xn_l (the stored fp16 LN output) for y; dxn (fp32) or dxn_h (fp16, gradient-scale units)
 void launch_ln_bwd_prep(const Dims& D, int l, const int* full_hcnt, const float* x_l, const act_t* xn_l,
                         const float* stats_l, const float* dxn, const act_t* dxn_h, float* dX, act_t* dC,
-                        float* part_cs, const float* gmax, cudaStream_t st);
+                        float* part_cs, const float* gmax, cudaStream_t st, int s0 = 0, int ns = -1);
 void launch_bias_reduce(const Dims& D, const uint8_t* codes, const float* part_cs, const float* part_db1, float* db1,
                         float* db2, cudaStream_t st);
 void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* part_cs, const float* dX, float* dWeT,

@@ -5,8 +5,12 @@ exchange is a fixed-order device sum) and step the same batch from host
 threads.  The owner-merged parameters, the velocity and the loss must match
 the whole-model engine and the fp64 oracle trainer to the step tolerances
 (tests/step_util.py); the schedule each rank derives is bit-identical to the
-oracle's.  The NCCL exchange is exercised at world 1 (the driver's boxes have
-one GPU); its multi-rank path shares every line but the all-reduce call."""
+oracle's — for both row mappings (head-interleaved, SPEC-contiguous) and 1-3
+exchange chunks.  The NCCL exchange runs at world 1 (the driver's boxes have
+one GPU): the partitioned data path (owner mask, fp32 partial sums, one
+ncclAllReduce per block, direction and chunk on the exchange stream, captured
+in the step's CUDA graph) executes and is compared with the whole-model
+engine and the oracle."""
 import os
 import socket
 
@@ -33,8 +37,9 @@ def _setup(cfg, B, seed=3):
     return p, x, y
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_local_partition_step_codes_matches_oracle(world):
+@pytest.mark.parametrize("world,mapping,chunks", [(2, "heads", 1), (2, "heads", 2), (3, "heads", 3),
+                                                  (2, "contiguous", 2), (3, "contiguous", 1)])
+def test_local_partition_step_codes_matches_oracle(world, mapping, chunks):
     cfg = SMALL
     oc = MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len, cfg.num_classes)
     sl = tensor_slices(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
@@ -44,7 +49,7 @@ def test_local_partition_step_codes_matches_oracle(world):
     p, x, y = _setup(cfg, B)
     K = cfg.scheduled_subnet_count()
     codes = np.random.default_rng(world).integers(1, 4, (K, n_mb)).astype(np.uint8)
-    g = PT.LocalGroup([E.SubnetModel(cfg, B, p) for _ in range(world)])
+    g = PT.LocalGroup([E.SubnetModel(cfg, B, p) for _ in range(world)], mapping, chunks)
     try:
         losses = []
         pr, vr = p.copy(), np.zeros_like(p)
@@ -54,8 +59,12 @@ def test_local_partition_step_codes_matches_oracle(world):
             assert len(set(ls)) == 1, ls  # every rank sees the same exchanged activations
             assert abs(ls[0] - rl) <= FP32_TOL * abs(rl), (step, ls[0], rl)
             losses.append(ls[0])
-        merged = PT.merge_owned(cfg, [m.params() for m in g.models])
-        vel = PT.merge_owned(cfg, [m.velocity() for m in g.models])
+        merged = PT.merge_owned(cfg, [m.params() for m in g.models], g.partition)
+        vel = PT.merge_owned(cfg, [m.velocity() for m in g.models], g.partition)
+        # 2 steps x L blocks x 2 directions x the non-empty chunks
+        calls, nbytes = PT.exchange_stats(g.models[0])
+        assert calls == 2 * cfg.num_blocks * 2 * min(chunks, B)
+        assert nbytes == 2 * cfg.num_blocks * 2 * B * cfg.seq_len * cfg.model_dim * 4
         p32 = p.astype(np.float32).astype(np.float64)
         assert normwise(merged, pr) <= FP32_TOL
         bad = compare_tensors(merged - p32, pr - p, sl, GRAD_TOL)
@@ -96,7 +105,13 @@ def test_local_partition_matches_whole_model_engine():
         whole.close()
 
 
-def test_nccl_partition_world1_is_the_whole_model():
+def test_nccl_partition_world1_runs_the_exchange():
+    """An NCCL partition of one rank: every block's partial output and dxn go
+    through ncclAllReduce (eager step_codes, then d2ft_step, whose CUDA graph
+    captures the all-reduces and replays them).  Results agree with the
+    whole-model engine to fp32 summation-order noise (the partitioned path
+    keeps dxn in fp32) and with the fp64 oracle trainer at the step
+    tolerances."""
     import torch.distributed as dist
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -105,19 +120,62 @@ def test_nccl_partition_world1_is_the_whole_model():
     dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
     try:
         cfg = SMALL
+        oc = MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
+                       cfg.num_classes)
+        sl = tensor_slices(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
+                           cfg.num_classes)
         B = 4
         p, x, y = _setup(cfg, B)
         K = cfg.scheduled_subnet_count()
         codes = np.random.default_rng(9).integers(1, 4, (K, B)).astype(np.uint8)
         a = E.SubnetModel(cfg, B, p)
         m = E.SubnetModel(cfg, B, p)
-        PT.join_nccl(m, PT.HeadPartition(cfg.heads_per_block, 0, 1))
+        part = PT.HeadPartition(cfg.heads_per_block, 0, 1)
+        PT.join_nccl(m, part, chunks=2)
         la = a.step_codes(x, y, codes, 1, 0.05, 0.9)
         lm = m.step_codes(x, y, codes, 1, 0.05, 0.9)
-        assert la == lm
-        assert np.array_equal(a.params(), m.params())
+        calls, nbytes = PT.exchange_stats(m)
+        assert calls == cfg.num_blocks * 2 * 2 and nbytes == cfg.num_blocks * 2 * B * cfg.seq_len * cfg.model_dim * 4
+        assert abs(la - lm) <= 1e-6 * abs(la)
+        p32 = p.astype(np.float32).astype(np.float64)
+        assert normwise(m.params() - p32, a.params() - p32) <= 1e-3
+        rl, _ = MO.train_batch(oc, p.copy(), np.zeros_like(p), x.astype(np.float64), y, codes, 1, 0.05, 0.9)
+        assert abs(lm - rl) <= FP32_TOL * abs(rl)
         assert np.array_equal(PT.gather_params(m, m.partition), m.params())
+        # graph path: the knapsack schedule + step captured once, replayed
+        b, f = O.bench_scores(K, B, 1)
+        nb = (2 * B) // 5
+        caps = Capacities([nb * 5] * K, [nb * 2] * K)
+        st = ScoreTable(K, B, f, b)
+        for i in range(3):
+            lw, tw = a.d2ft_step(x, y, st, CostModel(), caps, 1, 0.05, 0.9)
+            lp, tp = m.d2ft_step(x, y, st, CostModel(), caps, 1, 0.05, 0.9)
+            assert np.array_equal(tw.codes, tp.codes)
+            assert abs(lw - lp) <= 1e-4 * abs(lw), (i, lw, lp)
+        calls2, _ = PT.exchange_stats(m)
+        assert calls2 == calls + 3 * cfg.num_blocks * 2 * 2
+        assert normwise(m.params() - p32, a.params() - p32) <= 1e-3
         a.close()
         m.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_local_partition_graphless_chunks_match_single_chunk():
+    """Exchange chunking only reorders when the sums run, never what they
+    add: chunks 1 and 3 give bit-identical parameters (ViT-shaped dh 64)."""
+    cfg = E.ModelConfig(2, 4, 256, 512, 197, 4, 1)
+    B = 8
+    p, x, y = _setup(cfg, B, 13)
+    K = cfg.scheduled_subnet_count()
+    codes = np.random.default_rng(4).integers(1, 4, (K, B)).astype(np.uint8)
+    res = []
+    for chunks in (1, 3):
+        g = PT.LocalGroup([E.SubnetModel(cfg, B, p) for _ in range(2)], "heads", chunks)
+        try:
+            ls = g.run(lambda r, m: m.step_codes(x, y, codes, 1, 0.05, 0.9))
+            res.append((ls[0], PT.merge_owned(cfg, [m.params() for m in g.models], g.partition)))
+        finally:
+            g.close()
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
