@@ -145,6 +145,8 @@ int d2ft_engine_partition_nccl(d2ft_engine* e, int rank, int world, const uint8_
  * host threads; exchange = fixed-order device sum (single-GPU test harness) */
 int d2ft_local_group_create(int world, d2ft_local_group** out);
 int d2ft_local_group_destroy(d2ft_local_group* g);
+/* a rank failed: every rank waiting in the group's exchange returns a state error */
+int d2ft_local_group_abort(d2ft_local_group* g);
 int d2ft_engine_partition_local(d2ft_engine* e, d2ft_local_group* g, int rank);
 /* row -> rank mapping of a partitioned engine: owner[k] for every scheduled
  * subnet row k = l*H + h (default after joining: h % world, head-interleaved;

@@ -761,9 +761,9 @@ void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const
   const int sm = attn_bwd_tc_smem(D.TQ);
   D2FT_REQUIRE(attn_bwd_tc_fits(D.TQ), kConfig, "tcgen05 attention backward: shared memory");
   static unsigned long long attr = 0;
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     D2FT_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 223 * 1024));
-  }
+  });
   dim3 grid(D.H, D.B);
   attn_bwd_tc_kernel<<<grid, 32 * kBwdWarps, sm, st>>>(tmQKV, tmdO, AttnBwdArgs{D, l, full_heads, full_hcnt, O32T, lse, dY1T});
   count_launch();
@@ -776,9 +776,9 @@ void launch_attn_fwd_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CU
   D2FT_REQUIRE(D.dh == 64 && D.TQ <= 256, kConfig, "tcgen05 attention: head_dim 64, T <= 256");
   const int sm = attn_tc_smem(D.TQ);
   static unsigned long long attr = 0;
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     D2FT_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max_attn()));
-  }
+  });
   const char* g = getenv("D2FT_ATTN_RESCALE_GAP");  // tests force the rescale path with a small gap
   const float gap = g ? (float)atof(g) : kRescaleGap;
   attn_fwd_tc_kernel<<<num_sms(), kFwdThreads, sm, st>>>(

@@ -1,5 +1,6 @@
 // Shared helpers for the d2ft B200 library (sm_100a only).
 #pragma once
+#include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -81,14 +82,26 @@ int guarded(F&& f) {
 }
 
 // cudaFuncSetAttribute is per device: a call site keeps one bit per device
-// it has configured (`static unsigned long long mask; if (first_on_device(mask))`)
-inline bool first_on_device(unsigned long long& mask) {
+// it has configured (`static unsigned long long mask; once_per_device(mask,
+// [&] { cudaFuncSetAttribute(...); })`).  Thread-safe: the bit is published
+// only after `set` ran, under one process-wide mutex, so a second host thread
+// (the engines of an in-process partition, or two engines stepped
+// concurrently) never launches a kernel before its shared-memory limit took
+// effect (it used to see the bit first and fail the launch).
+inline std::mutex& func_attr_mutex() {
+  static std::mutex m;
+  return m;
+}
+template <class F>
+inline void once_per_device(unsigned long long& mask, F&& set) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   const unsigned long long bit = 1ull << (dev & 63);
-  if (mask & bit) return false;
-  mask |= bit;
-  return true;
+  if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return;
+  std::lock_guard<std::mutex> lk(func_attr_mutex());
+  if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return;
+  set();
+  __atomic_fetch_or(&mask, bit, __ATOMIC_RELEASE);
 }
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

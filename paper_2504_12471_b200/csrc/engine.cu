@@ -1320,6 +1320,13 @@ int d2ft_local_group_destroy(d2ft_local_group* g) {
   });
 }
 
+int d2ft_local_group_abort(d2ft_local_group* g) {
+  return guarded([&] {
+    D2FT_REQUIRE(g, kInput, "local_group_abort: null argument");
+    local_group_abort(g->g);
+  });
+}
+
 int d2ft_engine_partition_local(d2ft_engine* h, d2ft_local_group* g, int rank) {
   return guarded([&] {
     D2FT_REQUIRE(h && h->e && g, kInput, "partition: null argument");

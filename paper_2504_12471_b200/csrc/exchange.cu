@@ -104,17 +104,25 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0;
   unsigned gen = 0;
+  bool aborted = false;  // a rank failed outside the exchange: the others must not wait for it
   std::vector<float*> bufs;
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
+    D2FT_REQUIRE(!aborted, kState, "local group: aborted by a failing rank");
     const unsigned g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      D2FT_REQUIRE(gen != g, kState, "local group: aborted by a failing rank");
     }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    aborted = true;
+    cv.notify_all();
   }
 };
 
@@ -126,6 +134,7 @@ LocalGroup* local_group_create(int world) {
   return g;
 }
 void local_group_destroy(LocalGroup* g) { delete g; }
+void local_group_abort(LocalGroup* g) { g->abort(); }
 
 namespace {
 struct LocalExchange final : Exchange {

@@ -32,6 +32,8 @@ std::unique_ptr<Exchange> make_nccl_exchange(int rank, int world, const uint8_t 
 struct LocalGroup;
 LocalGroup* local_group_create(int world);
 void local_group_destroy(LocalGroup* g);
+// wake every rank waiting in the group's exchange with a state error (a peer failed)
+void local_group_abort(LocalGroup* g);
 std::unique_ptr<Exchange> make_local_exchange(LocalGroup* g, int rank);
 
 // codes[k][s] = 3 (skip) for the scheduled rows k another rank owns (owner[k] != rank)

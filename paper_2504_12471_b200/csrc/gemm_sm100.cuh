@@ -558,10 +558,10 @@ template <class P, class S>
 void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const P& prob, int max_ctas, cudaStream_t stream) {
   static_assert(gemm_smem_bytes<P, S>() <= 227 * 1024, "shared memory (stages + epilogue staging)");
   static unsigned long long attr = 0;
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     D2FT_CUDA(cudaFuncSetAttribute(gemm_sm100_kernel<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    gemm_smem_bytes<P, S>()));
-  }
+  });
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (max_ctas < 0) grid = -max_ctas;  // explicit grid (may exceed the SM count: non-persistent)

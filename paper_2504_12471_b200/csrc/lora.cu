@@ -134,9 +134,9 @@ void launch_lora_grad(const Dims& D, int rank, float scaling, const float* G1T, 
                       const int* full_cnt, cudaStream_t st) {
   const int smem = (rank * D.dh + kLoraI * (D.dh + 1) + kLoraI * rank) * 4;
   static unsigned long long attr = 0;
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     D2FT_CUDA(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-  }
+  });
   lora_grad_kernel<<<D.L * D.H * 3, 256, smem, st>>>(D, rank, scaling, G1T, A, AG, full_cnt);
   count_launch();
   D2FT_CUDA(cudaGetLastError());

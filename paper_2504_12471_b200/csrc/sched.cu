@@ -736,10 +736,10 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
     D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(K, N, max_cols), kState,
                  "knapsack: global decision-bit workspace too small");
   static unsigned long long attr_done = 0;
-  if (first_on_device(attr_done)) {
+  once_per_device(attr_done, [&] {
     D2FT_CUDA(cudaFuncSetAttribute(knapsack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
     D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-  }
+  });
   // rows that fit the single-warp DP need one warp (more CTAs per SM, the
   // DP's registers only for 32 threads); wider rows use the 8-warp block path
   const int threads = max_cols <= 32 * kLaneColsMax ? 32 : kThreads;

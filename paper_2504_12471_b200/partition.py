@@ -237,15 +237,17 @@ class LocalGroup:
                 out[r] = fn(r, self.models[r])
             except BaseException as e:  # re-raised on the caller's thread
                 err[r] = e
+                lib().d2ft_local_group_abort(self._g)  # peers waiting in the exchange fail instead of hanging
 
         ts = [threading.Thread(target=body, args=(r,)) for r in range(self.world)]
         for t in ts:
             t.start()
         for t in ts:
             t.join()
-        for e in err:
-            if e is not None:
-                raise e
+        first = next((e for e in err if e is not None and "aborted by a failing rank" not in str(e)), None)
+        first = first or next((e for e in err if e is not None), None)
+        if first is not None:  # the root cause, not a peer's abort
+            raise first
         return out
 
     def close(self):

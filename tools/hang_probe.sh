@@ -9,6 +9,7 @@ for i in $(seq 1 $WAIT); do sleep 1; kill -0 $PID 2>/dev/null || break; done
 if kill -0 $PID 2>/dev/null; then
   echo "HUNG after $WAIT s" > $OUT
   which gdb >> $OUT 2>&1
+  nvidia-smi --query-gpu=utilization.gpu,power.draw,clocks.sm --format=csv >> $OUT 2>&1
   if which gdb > /dev/null 2>&1; then
     gdb -p $PID -batch -ex "thread apply all bt 25" >> $OUT 2>&1
   else
