@@ -15,9 +15,11 @@ weights partition_model(seed 1), data make_synthetic_dataset(noise 0.5, seed 7).
 value : samples/s with inputs resident in HBM, CUDA-event timed on the engine
         stream (max over ranks).  The step's working set (weights, activations,
         >4 GB) exceeds the 126 MB L2, so no explicit flush is needed.
-e2e   : the same metric through the C-ABI host-buffer call d2ft_engine_step
-        (H2D of samples/labels/scores from pinned memory, D2H of loss+codes,
-        host sync, every step).
+e2e   : the same metric through the C-ABI Dataset call d2ft_engine_step_units
+        (the reference's fp64 per-sample matrices gathered H2D and converted on
+        the device, labels and score slice gathered, D2H of loss+codes, host
+        sync, every step); e2e.fp32_pinned = the pre-converted pinned-buffer
+        call d2ft_engine_step.
 --impl reference: the unmodified reference (oracle/_ref, built from
         /root/reference) on the host cores, a bounded sample per step.
 """
@@ -563,14 +565,39 @@ def run_ours(args):
             m._h, _lib.ptr(px), _lib.ptr(py), _lib.ptr(pb), _lib.ptr(pf), _lib.ptr(pc[0]), _lib.ptr(pc[1]),
             _lib.ptr(pc[2]), _lib.ptr(pc[3]), C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
             C.c_int(1), C.c_int(args.steps), C.byref(ms_e2e), C.byref(loss)))
-    e2e_step = ms_e2e.value / args.steps
+    e2e_pinned_step = ms_e2e.value / args.steps
+    h2d_pinned = x.nbytes + y.nbytes + 2 * bwd.nbytes + 4 * 4 * K
+    d2h = 8 + K * B
+    # ---- end to end through the Dataset path (the headline e2e): the
+    # reference's fp64 vector<Matrix> dataset (data.hpp), every batch's units
+    # gathered H2D as fp64 and converted on the device, its score slice cut
+    # from the whole pre-pass table (slice_scores), the next batch prefetched
+    # while this one computes (d2ft_engine_bench_e2e_units)
+    n_units = 4 * B
+    dset = E.make_synthetic_dataset_f64(n_units, NCLS, D, T, 0.5, 7)
+    uu = np.empty(2 * K * n_units)
+    _lib.check(lib.d2ft_uniform_stream(C.c_uint64(1), C.c_uint64(0), C.c_int(uu.size), _lib.ptr(uu)))
+    uu = uu.reshape(K, n_units, 2) * 10.0
+    tfwd, tbwd = np.ascontiguousarray(uu[:, :, 0]), np.ascontiguousarray(uu[:, :, 1])
+    n_batches = 1 + args.steps
+    rng = np.random.default_rng(3)
+    order = np.concatenate([rng.permutation(n_units) for _ in range((n_batches * B) // n_units + 1)])
+    order = np.ascontiguousarray(order[:n_batches * B], np.int32)
+    ms_ds = C.c_double()
+    if dist:
+        dist.barrier()
+    _lib.check(lib.d2ft_engine_bench_e2e_units(
+        m._h, dset.handle(), _lib.ptr(order), C.c_int(B), C.c_int(1), _lib.ptr(tbwd), _lib.ptr(tfwd),
+        C.c_int(n_units), _lib.ptr(pc[0]), _lib.ptr(pc[1]), _lib.ptr(pc[2]), _lib.ptr(pc[3]), C.c_double(0.05),
+        C.c_double(0.9), C.c_int(1), C.c_int(args.steps), C.byref(ms_ds), C.byref(loss)))
+    e2e_step = ms_ds.value / args.steps
     if dist:
         import torch
-        t = torch.tensor([e2e_step], device="cuda")
+        t = torch.tensor([e2e_step, e2e_pinned_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
-    h2d = x.nbytes + y.nbytes + 2 * bwd.nbytes + 4 * 4 * K
-    d2h = 8 + K * B
+        e2e_step, e2e_pinned_step = float(t[0].item()), float(t[1].item())
+    h2d = B * T * D * 8 + B * 4 + 2 * K * B * 8 + 4 * 4 * K
+    dset.close()
     # ---- scheduler latency: the training shapes and the 144 x 1024 sweep
     # (GPU, device-resident scores and host round trip) beside the
     # reference's knapsack_schedule on this host at threads 1 and nproc
@@ -663,7 +690,15 @@ def run_ours(args):
                        "l2": "working set > 126 MB L2 (no flush needed)"},
             "loss": loss.value,
             "e2e": {"value": B / (e2e_step * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step,
+                    "path": f"d2ft_engine_step_units over the fp64 Dataset ({n_units} samples, page-locked): per "
+                            "step the batch's fp64 samples gathered H2D + converted on the device (next batch "
+                            "prefetched), labels and score slice gathered on the host, schedule + step, loss "
+                            "and codes D2H, host sync",
+                    "fp32_pinned": {"value": B / (e2e_pinned_step * 1e-3), "ms_per_step": e2e_pinned_step,
+                                    "h2d_bytes_per_step": h2d_pinned,
+                                    "path": "d2ft_engine_step_pipelined, pre-converted fp32 samples in pinned "
+                                            "memory"}},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": "G1 grouped tcgen05 GEMM ([Wq|Wk|Wv|W1] x xn, active heads)",
                          "achieved": round(g1_tflops, 1), "peak": peak, "unit": "TFLOP/s",

@@ -99,6 +99,45 @@ int d2ft_engine_step_pipelined(d2ft_engine* e, const float* samples_next, const 
                                const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb, int mbs,
                                double lr, double momentum, double* loss_out, uint8_t* codes_out);
 
+/* The reference's Dataset (data.hpp:18-42): num_samples fp64 seq_len x
+ * token_dim row-major matrices (Matrix::data of dataset.samples[i]) and their
+ * labels.  The sample pointers are borrowed — the caller's vector<Matrix>
+ * stays the owner and must outlive the handle; labels are copied.  pin != 0
+ * page-locks every sample (cudaHostRegister; undone by destroy) so the
+ * per-batch gather runs at DMA speed. */
+typedef struct d2ft_dataset d2ft_dataset;
+int d2ft_dataset_create(const double* const* samples, const int32_t* labels, int num_samples, int num_classes,
+                        int seq_len, int token_dim, int pin, d2ft_dataset** out);
+int d2ft_dataset_destroy(d2ft_dataset* ds);
+
+/* The D2FT batch body of train() over dataset units (trainer.cpp:214-268):
+ * the batch is units[0..n_mb) (unit u = samples [u*mbs, (u+1)*mbs),
+ * Dataset::unit_inputs / unit_labels), scores are the whole pre-pass
+ * ScoreTable (K x total_units row-major backward / forward) sliced per batch
+ * as slice_scores (trainer.cpp:139-154).  The fp64 samples are gathered H2D
+ * and converted on the device; units_next != NULL gathers the next batch on
+ * the copy stream while this one computes (the next call must pass those
+ * units).  loss_out = batch loss (trainer.cpp:254); codes_out (K x n_mb, may
+ * be NULL) = the schedule. */
+int d2ft_engine_step_units(d2ft_engine* e, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
+                           const int32_t* units_next, const double* bwd_scores, const double* fwd_scores,
+                           int total_units, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                           const int32_t* cap_fwd, double lr, double momentum, double* loss_out, uint8_t* codes_out);
+/* The same batch body under an explicit K x n_mb schedule table (codes
+ * {1,2,3}; the Standard / Random / Scaler / pruning policies of
+ * trainer.cpp:220-243). */
+int d2ft_engine_step_units_codes(d2ft_engine* e, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
+                                 const int32_t* units_next, const uint8_t* codes, double lr, double momentum,
+                                 double* loss_out);
+/* bench.py's end-to-end leg over the Dataset path: warmup + steps batches,
+ * batch i = order[i*n_mb .. (i+1)*n_mb); ms_out = CUDA-event time of the
+ * timed steps (fp64 gather, score slicing, schedule, step, loss/codes D2H and
+ * host sync of every step inside). */
+int d2ft_engine_bench_e2e_units(d2ft_engine* e, const d2ft_dataset* ds, const int32_t* order, int n_mb, int mbs,
+                                const double* bwd_scores, const double* fwd_scores, int total_units,
+                                const int32_t* cf, const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd,
+                                double lr, double momentum, int warmup, int steps, double* ms_out, double* loss_out);
+
 /* Benchmark path: stage inputs once on the device, then run device-resident
  * steps (asynchronous on d2ft_engine_stream) and d2ft_engine_sync. */
 int d2ft_engine_stage_device(d2ft_engine* e, const float* samples, const int32_t* labels, const double* bwd_scores,
@@ -174,6 +213,9 @@ int d2ft_lora_init(const d2ft_model_config* cfg, int rank, double* out);
  * (the engine's input precision; the fp64 draws are rounded once). */
 int d2ft_make_synthetic_dataset(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
                                 uint64_t seed, float* samples, int32_t* labels);
+/* the same draws kept in fp64: Dataset::samples of the reference bit for bit */
+int d2ft_make_synthetic_dataset_f64(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
+                                    uint64_t seed, double* samples, int32_t* labels);
 
 #ifdef __cplusplus
 }

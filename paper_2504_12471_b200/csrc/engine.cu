@@ -9,6 +9,7 @@
 // Parameters live as fp32 masters in an arena laid out for the GEMMs (see
 // DESIGN.md §3); the canonical fp64 flat vector of the reference
 // (model.hpp:117-153) is the interchange format at the C-ABI.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -149,6 +150,7 @@ struct Engine {
   // input pipeline: the next batch's samples are copied H2D on a copy stream
   // into samples_stage while the current batch computes (d2ft_engine_prefetch)
   float* samples_stage = nullptr;
+  double* stage64 = nullptr;  // fp64 Dataset samples of the next batch, gathered H2D (prefetch_units)
   cudaStream_t cst = nullptr;
   // side stream: G5 (dW of [Wo;W2]) only needs the incoming gradient dC and
   // the forward's [O|g], so it runs beside G4 / attention backward / G7 / G8
@@ -170,6 +172,7 @@ struct Engine {
   cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
   bool have_prefetch = false;
   int prefetch_B = 0;
+  std::vector<int32_t> prefetched_units;  // the units of a Dataset prefetch (empty: a host-buffer prefetch)
   int* labels_dev;
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
@@ -1074,6 +1077,31 @@ struct Engine {
     D2FT_CUDA(cudaEventRecord(ev_copied, cst));
     have_prefetch = true;
     prefetch_B = B;
+    prefetched_units.clear();
+  }
+  // The data.hpp Dataset path (trainer.cpp:247-253 reads
+  // dataset.unit_inputs(units[j], mbs), fp64 Matrix samples): the batch's
+  // samples are gathered H2D as fp64 in batch order on the copy stream (one
+  // DMA per sample; page-locked by d2ft_dataset_create for full speed), then
+  // converted to fp32 into samples_stage on the same stream.  Overlaps the
+  // engine stream's current step; consume_prefetch picks it up.
+  void prefetch_units(const double* const* samples, const int32_t* units, int n_mb, int mbs) {
+    const int B = n_mb * mbs;
+    D2FT_REQUIRE(B >= 1 && B <= D.Bmax, kSize, "prefetch: batch exceeds the engine capacity");
+    const size_t per = (size_t)D.T * D.d;
+    if (!stage64) stage64 = dalloc<double>((size_t)D.Bmax * per, owned);
+    D2FT_CUDA(cudaStreamWaitEvent(cst, ev_stage_free, 0));
+    for (int j = 0; j < n_mb; ++j)
+      for (int i = 0; i < mbs; ++i) {
+        const size_t s = (size_t)units[j] * mbs + i;
+        D2FT_CUDA(cudaMemcpyAsync(stage64 + ((size_t)j * mbs + i) * per, samples[s], per * 8,
+                                  cudaMemcpyHostToDevice, cst));
+      }
+    launch_f64_to_f32(stage64, samples_stage, (size_t)B * per, cst);
+    D2FT_CUDA(cudaEventRecord(ev_copied, cst));
+    have_prefetch = true;
+    prefetch_B = B;
+    prefetched_units.assign(units, units + n_mb);
   }
   // prefetched samples -> samples_dev on the engine stream (device copy, ~12 us at ViT-B)
   void consume_prefetch(int B) {
@@ -1175,6 +1203,15 @@ using namespace d2ft_b200;
 
 struct d2ft_engine {
   Engine* e;
+};
+
+// data.hpp:18-42 Dataset: borrowed fp64 sample pointers (the caller's
+// vector<Matrix> owns them), labels, optionally page-locked.
+struct d2ft_dataset {
+  std::vector<const double*> samples;
+  std::vector<int32_t> labels;
+  std::vector<void*> pinned;  // cudaHostRegister'ed sample buffers (unregistered on destroy)
+  int num_classes = 0, T = 0, d = 0;
 };
 
 namespace {
@@ -1444,6 +1481,184 @@ int d2ft_engine_step_pipelined(d2ft_engine* h, const float* samples_next, const 
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
     if (codes_out) std::memcpy(codes_out, E.h_codes, (size_t)K * n_mb);
+  });
+}
+
+int d2ft_dataset_create(const double* const* samples, const int32_t* labels, int num_samples, int num_classes,
+                        int seq_len, int token_dim, int pin, d2ft_dataset** out) {
+  return guarded([&] {
+    D2FT_REQUIRE(samples && labels && out, kInput, "dataset: null argument");
+    D2FT_REQUIRE(num_samples >= 1 && num_classes >= 1 && seq_len >= 1 && token_dim >= 1, kInput,
+                 "dataset: sizes must be positive");
+    for (int i = 0; i < num_samples; ++i) {
+      D2FT_REQUIRE(samples[i], kInput, "dataset: null sample");
+      D2FT_REQUIRE(labels[i] >= 0 && labels[i] < num_classes, kInput, "dataset: label out of range");
+    }
+    auto ds = std::make_unique<d2ft_dataset>();
+    ds->samples.assign(samples, samples + num_samples);
+    ds->labels.assign(labels, labels + num_samples);
+    ds->num_classes = num_classes;
+    ds->T = seq_len;
+    ds->d = token_dim;
+    if (pin) {
+      const size_t bytes = (size_t)seq_len * token_dim * sizeof(double);
+      for (int i = 0; i < num_samples; ++i) {
+        void* p = const_cast<double*>(samples[i]);
+        // best effort: a sample sharing pages with an already registered
+        // range (small heap matrices) stays pageable; its copy is staged by
+        // the driver instead (slower, same bytes)
+        if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess) ds->pinned.push_back(p);
+        else cudaGetLastError();
+      }
+    }
+    *out = ds.release();
+  });
+}
+
+int d2ft_dataset_destroy(d2ft_dataset* ds) {
+  return guarded([&] {
+    if (!ds) return;
+    for (void* p : ds->pinned) cudaHostUnregister(p);
+    delete ds;
+  });
+}
+
+namespace {
+// the units of one batch: in range, the dataset matches the engine
+void validate_units(const Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs) {
+  D2FT_REQUIRE(ds && units, kInput, "step_units: null argument");
+  D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
+  D2FT_REQUIRE(ds->T == E.D.T && ds->d == E.D.d, kInput, "train sample: shape does not match the model");
+  const int total = (int)ds->samples.size() / mbs;
+  D2FT_REQUIRE((int)ds->samples.size() % mbs == 0, kInput, "dataset size must be a multiple of the micro-batch size");
+  for (int j = 0; j < n_mb; ++j) D2FT_REQUIRE(units[j] >= 0 && units[j] < total, kInput, "step_units: unit out of range");
+}
+
+// one batch of the Dataset path (trainer.cpp:214-268): labels gathered as
+// dataset.unit_labels, the score slice as slice_scores (trainer.cpp:139-154)
+// from the full K x total_units table, the samples as prefetched fp64.
+void units_step(Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs, const int32_t* units_next,
+                const double* bwd_scores, const double* fwd_scores, int total_units, const int32_t* cf,
+                const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, double lr, double momentum) {
+  const int K = E.D.K();
+  const int B = n_mb * mbs;
+  for (int j = 0; j < n_mb; ++j)
+    for (int i = 0; i < mbs; ++i) E.h_labels[j * mbs + i] = ds->labels[(size_t)units[j] * mbs + i];
+  validate_labels(E.h_labels, B, E.D.C);
+  double* sb = E.h_scores;
+  double* sf = E.h_scores + (size_t)K * n_mb;
+  for (int k = 0; k < K; ++k)
+    for (int j = 0; j < n_mb; ++j) {
+      sb[(size_t)k * n_mb + j] = bwd_scores[(size_t)k * total_units + units[j]];
+      sf[(size_t)k * n_mb + j] = fwd_scores[(size_t)k * total_units + units[j]];
+    }
+  validate_sched_inputs(sb, sf, cf, cb, cap_full, cap_fwd, K, n_mb);
+  E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
+  if (!E.have_prefetch) E.prefetch_units(ds->samples.data(), units, n_mb, mbs);
+  E.host_step(nullptr, E.h_labels, sb, sf, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
+  if (units_next) E.prefetch_units(ds->samples.data(), units_next, n_mb, mbs);
+}
+}  // namespace
+
+int d2ft_engine_step_units(d2ft_engine* h, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
+                           const int32_t* units_next, const double* bwd_scores, const double* fwd_scores,
+                           int total_units, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,
+                           const int32_t* cap_fwd, double lr, double momentum, double* loss_out, uint8_t* codes_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    validate_units(E, ds, units, n_mb, mbs);
+    if (units_next) validate_units(E, ds, units_next, n_mb, mbs);
+    D2FT_REQUIRE(bwd_scores && fwd_scores && cf && cb && cap_full && cap_fwd && loss_out, kInput,
+                 "step_units: null argument");
+    D2FT_REQUIRE(total_units == (int)ds->samples.size() / mbs, kInput,
+                 "step_units: score table columns must equal the dataset's micro-batch units");
+    D2FT_REQUIRE(!E.have_prefetch || (E.prefetch_B == n_mb * mbs &&
+                                      std::equal(units, units + n_mb, E.prefetched_units.begin(),
+                                                 E.prefetched_units.end())),
+                 kState, "step_units: the prefetched batch holds other units");
+    units_step(E, ds, units, n_mb, mbs, units_next, bwd_scores, fwd_scores, total_units, cf, cb, cap_full, cap_fwd, lr,
+               momentum);
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+    if (codes_out) std::memcpy(codes_out, E.h_codes, (size_t)E.D.K() * n_mb);
+  });
+}
+
+// The batch body for a given schedule table (Standard / Random / Scaler /
+// pruning policies, trainer.cpp:220-243 then :247-268) over dataset units.
+int d2ft_engine_step_units_codes(d2ft_engine* h, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
+                                 const int32_t* units_next, const uint8_t* codes, double lr, double momentum,
+                                 double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    validate_units(E, ds, units, n_mb, mbs);
+    if (units_next) validate_units(E, ds, units_next, n_mb, mbs);
+    D2FT_REQUIRE(codes && loss_out, kInput, "step_units: null argument");
+    const int B = n_mb * mbs;
+    D2FT_REQUIRE(B <= E.D.Bmax, kSize, "step: batch exceeds the engine capacity");
+    for (size_t c = 0; c < (size_t)E.D.K() * n_mb; ++c)
+      D2FT_REQUIRE(codes[c] >= 1 && codes[c] <= 3, kInput, "schedule table: code out of range");
+    D2FT_REQUIRE(!E.have_prefetch || (E.prefetch_B == B && std::equal(units, units + n_mb, E.prefetched_units.begin(),
+                                                                      E.prefetched_units.end())),
+                 kState, "step_units: the prefetched batch holds other units");
+    for (int j = 0; j < n_mb; ++j)
+      for (int i = 0; i < mbs; ++i) E.h_labels[j * mbs + i] = ds->labels[(size_t)units[j] * mbs + i];
+    validate_labels(E.h_labels, B, E.D.C);
+    std::memcpy(E.h_codes, codes, (size_t)E.D.K() * n_mb);
+    if (!E.have_prefetch) E.prefetch_units(ds->samples.data(), units, n_mb, mbs);
+    E.begin_step(B);
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, E.h_labels, B * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, E.h_codes, (size_t)E.D.K() * n_mb, cudaMemcpyHostToDevice, E.st));
+    E.consume_prefetch(B);
+    launch_expand_codes(E.codes_mb, E.D.K(), n_mb, mbs, B, E.D.Bmax, E.codes_exp, E.st);
+    E.compact_and_plan();
+    E.train_body((float)lr, (float)momentum);
+    if (units_next) E.prefetch_units(ds->samples.data(), units_next, n_mb, mbs);
+    check_status(E.finish_and_check());
+    *loss_out = *E.h_loss;
+  });
+}
+
+// bench.py's e2e leg through the Dataset path: `steps` batches whose units
+// are order[i*n_mb .. (i+1)*n_mb) (the trainer's shuffled unit order), every
+// step gathering its fp64 samples H2D (prefetched while the previous batch
+// computes), slicing its scores, and reading loss + codes back with a host
+// sync.  CUDA events on the engine stream; the first gather is inside.
+int d2ft_engine_bench_e2e_units(d2ft_engine* h, const d2ft_dataset* ds, const int32_t* order, int n_mb, int mbs,
+                                const double* bwd_scores, const double* fwd_scores, int total_units,
+                                const int32_t* cf, const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd,
+                                double lr, double momentum, int warmup, int steps, double* ms_out, double* loss_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_REQUIRE(warmup >= 0 && steps >= 1, kInput, "bench: steps must be positive");
+    D2FT_REQUIRE(total_units == (int)ds->samples.size() / mbs, kInput,
+                 "step_units: score table columns must equal the dataset's micro-batch units");
+    for (int i = 0; i < warmup + steps; ++i) validate_units(E, ds, order + (size_t)i * n_mb, n_mb, mbs);
+    D2FT_REQUIRE(!E.have_prefetch, kState, "bench: a prefetched batch is pending");
+    for (int i = 0; i < warmup; ++i) {
+      units_step(E, ds, order + (size_t)i * n_mb, n_mb, mbs, nullptr, bwd_scores, fwd_scores, total_units, cf, cb,
+                 cap_full, cap_fwd, lr, momentum);
+      check_status(E.finish_and_check());
+    }
+    cudaEvent_t e0, e1;
+    D2FT_CUDA(cudaEventCreate(&e0));
+    D2FT_CUDA(cudaEventCreate(&e1));
+    D2FT_CUDA(cudaEventRecord(e0, E.st));
+    D2FT_CUDA(cudaStreamWaitEvent(E.cst, e0, 0));  // the first gather is inside the timed region
+    const int32_t* ord = order + (size_t)warmup * n_mb;
+    for (int i = 0; i < steps; ++i) {
+      units_step(E, ds, ord + (size_t)i * n_mb, n_mb, mbs, i + 1 < steps ? ord + (size_t)(i + 1) * n_mb : nullptr,
+                 bwd_scores, fwd_scores, total_units, cf, cb, cap_full, cap_fwd, lr, momentum);
+      check_status(E.finish_and_check());
+    }
+    D2FT_CUDA(cudaEventRecord(e1, E.st));
+    D2FT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    D2FT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms;
+    if (loss_out) *loss_out = *E.h_loss;
   });
 }
 

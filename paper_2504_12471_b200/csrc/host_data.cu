@@ -118,26 +118,41 @@ int d2ft_set_device(int device) {
   return guarded([&] { D2FT_CUDA(cudaSetDevice(device)); });
 }
 
+}  // extern "C"
+
+namespace {
+template <typename T>
+void synth(int num_samples, int num_classes, int token_dim, int seq_len, double noise, uint64_t seed, T* samples,
+           int32_t* labels) {
+  D2FT_REQUIRE(num_samples >= 1 && num_classes >= 1 && token_dim >= 1 && seq_len >= 1, kInput,
+               "dataset spec: degenerate dimensions");
+  D2FT_REQUIRE(noise >= 0.0 && std::isfinite(noise), kInput, "dataset spec: noise_level must be nonnegative and finite");
+  D2FT_REQUIRE(num_samples % num_classes == 0, kInput, "dataset spec: num_samples must be a multiple of num_classes");
+  std::vector<double> means((size_t)num_classes * token_dim);
+  auto mg = stream_rng(seed, 0);
+  for (double& v : means) v = normal(mg);
+  for (int i = 0; i < num_samples; ++i) {
+    const int label = i % num_classes;
+    auto g = stream_rng(seed, 1 + (uint64_t)i);
+    T* x = samples + (size_t)i * seq_len * token_dim;
+    for (int t = 0; t < seq_len; ++t)
+      for (int j = 0; j < token_dim; ++j)
+        x[(size_t)t * token_dim + j] = (T)(means[(size_t)label * token_dim + j] + noise * normal(g));
+    labels[i] = label;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int d2ft_make_synthetic_dataset(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
                                 uint64_t seed, float* samples, int32_t* labels) {
-  return guarded([&] {
-    D2FT_REQUIRE(num_samples >= 1 && num_classes >= 1 && token_dim >= 1 && seq_len >= 1, kInput,
-                 "dataset spec: degenerate dimensions");
-    D2FT_REQUIRE(noise >= 0.0 && std::isfinite(noise), kInput, "dataset spec: noise_level must be nonnegative and finite");
-    D2FT_REQUIRE(num_samples % num_classes == 0, kInput, "dataset spec: num_samples must be a multiple of num_classes");
-    std::vector<double> means((size_t)num_classes * token_dim);
-    auto mg = stream_rng(seed, 0);
-    for (double& v : means) v = normal(mg);
-    for (int i = 0; i < num_samples; ++i) {
-      const int label = i % num_classes;
-      auto g = stream_rng(seed, 1 + (uint64_t)i);
-      float* x = samples + (size_t)i * seq_len * token_dim;
-      for (int t = 0; t < seq_len; ++t)
-        for (int j = 0; j < token_dim; ++j)
-          x[(size_t)t * token_dim + j] = (float)(means[(size_t)label * token_dim + j] + noise * normal(g));
-      labels[i] = label;
-    }
-  });
+  return guarded([&] { synth(num_samples, num_classes, token_dim, seq_len, noise, seed, samples, labels); });
+}
+
+int d2ft_make_synthetic_dataset_f64(int num_samples, int num_classes, int token_dim, int seq_len, double noise,
+                                    uint64_t seed, double* samples, int32_t* labels) {
+  return guarded([&] { synth(num_samples, num_classes, token_dim, seq_len, noise, seed, samples, labels); });
 }
 
 }  // extern "C"

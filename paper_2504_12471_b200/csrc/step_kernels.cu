@@ -585,6 +585,16 @@ __global__ void sgd_kernel(float* p, float* v, const float* g, act_t* pbf, size_
   }
 }
 
+// Dataset::samples (fp64 Matrix, data.hpp:18-20) -> the engine's fp32 input:
+// the batch's samples arrive H2D as fp64 in batch order; two doubles per thread
+// per iteration (n is even: every sample is T x d with d a multiple of 128).
+__global__ void f64_to_f32_kernel(const double2* __restrict__ in, float2* __restrict__ out, size_t n2) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(in + i);
+    out[i] = make_float2((float)v.x, (float)v.y);
+  }
+}
+
 __global__ void f32_to_bf16_kernel(const float* in, act_t* out, size_t n) {
   D2FT_PDL_ENTRY();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -1113,6 +1123,13 @@ void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long l
   D2FT_CUDA(cudaGetLastError());
 }
 
+
+void launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st) {
+  f64_to_f32_kernel<<<grid_for(n / 2, 256), 256, 0, st>>>(reinterpret_cast<const double2*>(in),
+                                                           reinterpret_cast<float2*>(out), n / 2);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
 
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);

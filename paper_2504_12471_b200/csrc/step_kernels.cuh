@@ -67,6 +67,7 @@ void launch_embed_reduce(const Dims& D, int KS, const float* part, const float* 
 void launch_sgd(float* p, float* v, const float* g, act_t* pbf, size_t n, long long outer, long long inner, int H,
                 const int* full_cnt, float lr, float mom, int* err, cudaStream_t st);
 void launch_f32_to_act(const float* in, act_t* out, size_t n, cudaStream_t st);
+void launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
 // LoRA (lora.cu): W_eff = W + s D U into the fp16 q/k/v operand rows; adapter
 // gradients from G7's q/k/v weight gradient
 void launch_lora_merge(const Dims& D, int rank, float scaling, const float* W1T, const float* A, act_t* W1T_bf,

@@ -103,6 +103,83 @@ def make_synthetic_dataset(num_samples, num_classes, token_dim, seq_len, noise_l
     return x, y
 
 
+def _aligned_f64(shape) -> np.ndarray:
+    """A fresh page-aligned fp64 array (one Matrix allocation of the reference's
+    vector<Matrix>; page alignment lets d2ft_dataset_create page-lock each
+    sample on its own)."""
+    n = int(np.prod(shape))
+    raw = np.empty(n + 512, np.float64)
+    off = (-raw.ctypes.data % 4096) // 8
+    return raw[off:off + n].reshape(shape)
+
+
+class Dataset:
+    """data.hpp:18-42: `samples` is a list of fp64 [seq_len][token_dim] arrays
+    (one per sample, as vector<Matrix>), `labels` ints, `num_classes`.  The
+    device handle (d2ft_dataset_create) borrows the arrays and page-locks them
+    for the per-batch gather of d2ft_engine_step_units."""
+
+    def __init__(self, samples, labels, num_classes: int):
+        self.samples = [np.ascontiguousarray(s, np.float64) for s in samples]
+        self.labels = i32(labels)
+        self.num_classes = int(num_classes)
+        if len(self.samples) != self.labels.size:
+            raise Error(2, "dataset: samples and labels must align")
+        self._h = None
+
+    def size(self) -> int:
+        return len(self.samples)
+
+    def micro_batch_count(self, micro_batch_size: int) -> int:
+        if micro_batch_size < 1 or self.size() % micro_batch_size:
+            raise Error(2, "dataset size must be a multiple of the micro-batch size")  # data.hpp:26-28
+        return self.size() // micro_batch_size
+
+    def unit_inputs(self, unit: int, micro_batch_size: int):
+        return self.samples[unit * micro_batch_size:(unit + 1) * micro_batch_size]
+
+    def unit_labels(self, unit: int, micro_batch_size: int):
+        return self.labels[unit * micro_batch_size:(unit + 1) * micro_batch_size]
+
+    def handle(self, pin: bool = True):
+        if self._h is None:
+            T, d = self.samples[0].shape
+            if any(s.shape != (T, d) for s in self.samples):
+                raise Error(2, "dataset: samples must share one shape")
+            ptrs = (C.c_void_p * self.size())(*[s.ctypes.data for s in self.samples])
+            h = C.c_void_p()
+            check(lib().d2ft_dataset_create(ptrs, ptr(self.labels), C.c_int(self.size()), C.c_int(self.num_classes),
+                                            C.c_int(T), C.c_int(d), C.c_int(1 if pin else 0), C.byref(h)))
+            self._h = h
+        return self._h
+
+    def close(self):
+        if self._h is not None:
+            lib().d2ft_dataset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_synthetic_dataset_f64(num_samples, num_classes, token_dim, seq_len, noise_level=0.5, seed=7) -> Dataset:
+    """trainer.cpp:83-111 as the reference's fp64 Dataset (bit-identical samples)."""
+    flat = np.empty((num_samples, seq_len, token_dim), np.float64)
+    y = np.empty(num_samples, np.int32)
+    check(lib().d2ft_make_synthetic_dataset_f64(C.c_int(num_samples), C.c_int(num_classes), C.c_int(token_dim),
+                                                C.c_int(seq_len), C.c_double(noise_level), C.c_uint64(seed),
+                                                ptr(flat), ptr(y)))
+    samples = []
+    for i in range(num_samples):
+        a = _aligned_f64((seq_len, token_dim))
+        a[...] = flat[i]
+        samples.append(a)
+    return Dataset(samples, y, num_classes)
+
+
 class SubnetModel:
     """Device-resident subnet model + optimizer state on one B200."""
 
@@ -262,6 +339,40 @@ class SubnetModel:
                                      C.c_int(mbs), C.c_double(lr), C.c_double(momentum), C.byref(loss), ptr(codes)))
         return loss.value, ScheduleTable(K, n_mb, codes)
 
+    def step_units(self, dataset: Dataset, units, scores: ScoreTable, cost_model: CostModel,
+                   capacities: Capacities, mbs=1, lr=0.05, momentum=0.9, units_next=None):
+        """trainer.cpp:214-268 over dataset units: the batch is `units` (unit u =
+        samples [u*mbs, (u+1)*mbs)), `scores` the whole pre-pass table
+        (K x micro_batch_count), sliced per batch (slice_scores,
+        trainer.cpp:139-154).  The fp64 samples are gathered on the device;
+        `units_next` prefetches the next batch (pass it as `units` next call).
+        Returns (batch_loss, ScheduleTable)."""
+        K = self.scheduled_count()
+        u = i32(units)
+        n_mb = u.size
+        total = dataset.micro_batch_count(mbs)
+        if scores.subnets != K or scores.micro_batches != total:
+            raise Error(2, f"step_units: score table must be {K} x {total}, got {scores.subnets} x {scores.micro_batches}")
+        if len(capacities.full) != K or len(capacities.fwd) != K:
+            raise Error(2, "knapsack_schedule: capacities device count mismatch")
+        if n_mb * mbs > self.max_batch:
+            raise Error(6, f"batch of {n_mb * mbs} units exceeds the engine capacity {self.max_batch}")
+        un = None
+        if units_next is not None:
+            un = i32(units_next)
+            if un.size != n_mb:
+                raise Error(2, "step_units: the next batch must have as many units")
+        cost_model.validate()
+        cf, cb = cost_model.row_arrays(K)
+        codes = np.zeros((K, n_mb), np.uint8)
+        loss = C.c_double()
+        check(lib().d2ft_engine_step_units(self._h, dataset.handle(), ptr(u), C.c_int(n_mb), C.c_int(mbs),
+                                           ptr(un) if un is not None else None, ptr(scores.backward),
+                                           ptr(scores.forward), C.c_int(total), ptr(cf), ptr(cb),
+                                           ptr(i32(capacities.full)), ptr(i32(capacities.fwd)), C.c_double(lr),
+                                           C.c_double(momentum), C.byref(loss), ptr(codes)))
+        return loss.value, ScheduleTable(K, n_mb, codes)
+
     def prepass_scores(self, samples, labels, micro_batch_size=1, fwd_metric="fisher_information",
                        bwd_metric="weight_magnitude") -> ScoreTable:
         """prepass_scores (scoring.cpp:108-151): every micro-batch forward and
@@ -325,27 +436,29 @@ class SubnetModel:
 
 
 def smoke_step() -> None:
-    """__graft_entry__.smoke(): one tiny D2FT step on cuda:0 vs the fp64 oracle."""
+    """__graft_entry__.smoke(): one tiny D2FT step on cuda:0 vs the fp64 oracle,
+    at the BASELINE tiny shape (dh = 32, mma.sync attention) and at dh = 64
+    (the tcgen05 attention kernels the ViT configs run)."""
     from oracle import lib as O
     from oracle import model_oracle as MO
-    cfg = ModelConfig(2, 4, 128, 256, 64, 4, 1)
-    B = 8
-    x, y = make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
-    K = cfg.scheduled_subnet_count()
-    b, f = O.bench_scores(K, B, 3)
-    caps = Capacities([(2 * B // 5) * 5] * K, [(2 * B // 5) * 2] * K)
-    m = SubnetModel(cfg, B)
-    p0 = m.params()
-    loss, table = m.d2ft_step(x, y, ScoreTable(K, B, f, b), CostModel(), caps, 1, 0.05, 0.9)
-    ref_codes = O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd)
-    assert np.array_equal(table.codes, ref_codes), "smoke: GPU schedule differs from the oracle"
-    oc = MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
-                   cfg.num_classes)
-    pr = p0.copy()
-    v = np.zeros_like(pr)
-    ref_loss, _ = MO.train_batch(oc, pr, v, x.astype(np.float64), y, ref_codes, 1, 0.05, 0.9)
-    assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss), (loss, ref_loss)
-    dp, dr = m.params() - p0.astype(np.float32).astype(np.float64), pr - p0
-    rel = np.max(np.abs(dp - dr)) / np.max(np.abs(dr))
-    assert rel <= 1e-2, rel
-    m.close()
+    for cfg in (ModelConfig(2, 4, 128, 256, 64, 4, 1), ModelConfig(2, 2, 128, 256, 64, 4, 1)):
+        B = 8
+        x, y = make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+        K = cfg.scheduled_subnet_count()
+        b, f = O.bench_scores(K, B, 3)
+        caps = Capacities([(2 * B // 5) * 5] * K, [(2 * B // 5) * 2] * K)
+        m = SubnetModel(cfg, B)
+        p0 = m.params()
+        loss, table = m.d2ft_step(x, y, ScoreTable(K, B, f, b), CostModel(), caps, 1, 0.05, 0.9)
+        ref_codes = O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd)
+        assert np.array_equal(table.codes, ref_codes), "smoke: GPU schedule differs from the oracle"
+        oc = MO.Config(cfg.num_blocks, cfg.heads_per_block, cfg.model_dim, cfg.ffn_hidden, cfg.seq_len,
+                       cfg.num_classes)
+        pr = p0.copy()
+        v = np.zeros_like(pr)
+        ref_loss, _ = MO.train_batch(oc, pr, v, x.astype(np.float64), y, ref_codes, 1, 0.05, 0.9)
+        assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss), (loss, ref_loss)
+        dp, dr = m.params() - p0.astype(np.float32).astype(np.float64), pr - p0
+        rel = np.max(np.abs(dp - dr)) / np.max(np.abs(dr))
+        assert rel <= 1e-2, rel
+        m.close()

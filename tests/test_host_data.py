@@ -24,3 +24,22 @@ def test_slices_cover_param_vector():
     cfg = E.TINY
     s = E.subnet_slices(cfg)
     assert s[0][0] == 0 and s[-1][1] == E.param_count(cfg) and len(s) == cfg.subnet_count()
+
+
+def test_synthetic_dataset_f64_bit_identical_to_reference_dataset():
+    """The fp64 Dataset (data.hpp) the step_units path ingests: every sample is
+    the reference's Matrix bit for bit (golden data_x from the reference), each
+    its own page-aligned allocation."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "rng_init.npz"))
+    ds = E.make_synthetic_dataset_f64(8, 4, 32, 16, 0.5, 7)
+    assert ds.size() == 8 and ds.num_classes == 4
+    assert np.array_equal(np.stack(ds.samples), g["data_x"]) and np.array_equal(ds.labels, g["data_y"])
+    assert all(s.ctypes.data % 4096 == 0 for s in ds.samples)
+    assert ds.micro_batch_count(2) == 4
+    assert np.array_equal(np.stack(ds.unit_inputs(1, 2)), g["data_x"][2:4])
+    try:
+        ds.micro_batch_count(3)
+        raise AssertionError("expected input_error")
+    except E.Error as e:
+        assert e.kind == "input"

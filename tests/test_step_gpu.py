@@ -233,3 +233,36 @@ def test_side_stream_schedule_is_bitwise_neutral(monkeypatch):
         m.close()
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+
+
+@pytest.mark.parametrize("cfg", [SMALL, SMALL64], ids=["dh32", "dh64"])
+def test_nonfinite_gradient_is_numeric_error(cfg):
+    """trainer.cpp:118: a non-finite gradient makes the step fail with a
+    numeric error (the reference throws from sgd_momentum_step; its model is
+    then partially updated, here every finite element is — in both cases the
+    caller restores the parameters).  After set_params the engine steps
+    exactly like a fresh one."""
+    K = cfg.scheduled_subnet_count()
+    B = 4
+    x, y = E.make_synthetic_dataset(B, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    b, f = O.bench_scores(K, B, 2)
+    st = P.ScoreTable(K, B, f, b)
+    caps = P.Capacities([10] * K, [4] * K)
+    m = E.SubnetModel(cfg, B)
+    p0 = m.params()
+    bad = x.copy()
+    bad[1, 3, 5] = np.nan
+    with pytest.raises(E.Error) as e:
+        m.d2ft_step(bad, y, st, P.CostModel(), caps)
+    assert e.value.kind == "numeric"
+    bad[1, 3, 5] = np.inf
+    with pytest.raises(E.Error) as e:
+        m.step_codes(bad, y, np.ones((K, B), np.uint8), 1)
+    assert e.value.kind == "numeric"
+    m.set_params(p0)
+    fresh = E.SubnetModel(cfg, B)
+    la, ta = m.d2ft_step(x, y, st, P.CostModel(), caps)
+    lb, tb = fresh.d2ft_step(x, y, st, P.CostModel(), caps)
+    assert la == lb and np.array_equal(ta.codes, tb.codes) and np.array_equal(m.params(), fresh.params())
+    m.close()
+    fresh.close()
