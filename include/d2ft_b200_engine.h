@@ -60,6 +60,12 @@ int d2ft_engine_get_lora(d2ft_engine* e, int which, double* adapters);
 int d2ft_engine_forward_backward(d2ft_engine* e, const float* samples, const int32_t* labels, int n,
                                  const uint8_t* column, double* loss_out);
 
+/* SubnetModel::logits (model.cpp logits, every subnet active) for n <= max
+ * batch samples: logits_out n x num_classes.  No parameter changes; the
+ * gradient buffers are clobbered.  evaluate() (trainer.cpp:307-319) is the
+ * argmax over these. */
+int d2ft_engine_logits(d2ft_engine* e, const float* samples, int n, double* logits_out);
+
 /* One trainer batch with an explicit K x n_mb schedule table (Standard policy
  * = all 1).  samples: (n_mb*mbs) x T x d fp32 in micro-batch order; loss_out
  * = batch loss as trainer.cpp:254. */

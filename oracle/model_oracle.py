@@ -455,3 +455,24 @@ def prepass_scores(cfg: Config, flat, inputs, labels, mbs, fwd_metric, bwd_metri
             fwd[k, u] = metric_value(fwd_metric, flat[a:b], g[a:b])
             bwd[k, u] = metric_value(bwd_metric, flat[a:b], g[a:b])
     return fwd, bwd
+
+
+def prepass_scores_lora(cfg: Config, flat, rank, scaling, aflat, inputs, labels, mbs, fwd_metric, bwd_metric):
+    """prepass_scores with adapters attached (scoring.cpp:129-148 with
+    lora_enabled(): metric_value walks visit_trainable = the six adapter
+    tensors of each block subnet, model.hpp:155-172)."""
+    n = len(inputs)
+    assert n % mbs == 0
+    units = n // mbs
+    bs = lora_block_size(cfg, rank)
+    fwd = np.zeros((cfg.K, units))
+    bwd = np.zeros((cfg.K, units))
+    col = np.ones(cfg.K, np.uint8)
+    for u in range(units):
+        _, ga, _ = forward_backward(cfg, flat, inputs[u * mbs:(u + 1) * mbs], labels[u * mbs:(u + 1) * mbs], col,
+                                    lora=(rank, scaling, aflat))
+        for k in range(cfg.K):
+            a, b = k * bs, (k + 1) * bs
+            fwd[k, u] = metric_value(fwd_metric, aflat[a:b], ga[a:b])
+            bwd[k, u] = metric_value(bwd_metric, aflat[a:b], ga[a:b])
+    return fwd, bwd

@@ -540,8 +540,13 @@ struct AttnBwdArgs {
   act_t* dY1T;        // [Bmax][H][PQ][TP]
 };
 
+// Q, K, V, dO tiles + 4 dS^T query blocks.  The S^T / dP^T UMMAs read K and V
+// as M = 128 A operands: with TQ < 128 they read past their tile into the
+// following ones (rows past T only feed TMEM lanes of keys >= T, never
+// stored), so the allocation must cover sV + 128 rows for short sequences.
 __host__ __device__ inline int attn_bwd_tc_smem(int TQ) {
-  return 4 * TQ * 128 + 4 * TQ * 128 + 1024;
+  const int tiles = 8 * TQ * 128, v_extent = 2 * TQ * 128 + kQTile * 128;
+  return (tiles > v_extent ? tiles : v_extent) + 1024;
 }
 
 // 16 warps: warp w owns TMEM lane quarter w % 4 (its 32 keys / queries) and

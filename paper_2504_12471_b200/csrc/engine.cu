@@ -174,6 +174,7 @@ struct Engine {
   int prefetch_B = 0;
   std::vector<int32_t> prefetched_units;  // the units of a Dataset prefetch (empty: a host-buffer prefetch)
   int* labels_dev;
+  float* logits_dev;  // [Bmax][C] head logits of the last forward (d2ft_engine_logits)
   // backward scratch
   float *dX, *dxn, *part_cs, *part_db1, *part_ew;
   act_t *dC, *dO, *dY1T;  // dC: G4's B, G5's / EmbedW's A (read MN-major)
@@ -457,6 +458,7 @@ struct Engine {
     loss = dalloc<double>(1, owned);
     pooled = dalloc<float>(Bm * d, owned);
     dlog = dalloc<float>(Bm * D.C, owned);
+    logits_dev = dalloc<float>(Bm * D.C, owned);
 
     const size_t K = (size_t)D.K();
     bwd_dev = dalloc<double>(K * Bm, owned);
@@ -754,7 +756,7 @@ struct Engine {
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
     launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off,
                 sm ? 1.0f / (float)sm->mbs : 1.0f / (float)D.B, loss_s, pooled,
-                dlog, dX, gmax, st);
+                dlog, dX, gmax, logits_dev, st);
     launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
@@ -894,7 +896,7 @@ struct Engine {
   // n_units micro-batches of mbs samples, all head-subnets Full, no update.
   void prepass(int n_units, int mbs, int fwd_metric, int bwd_metric, double* fwd_host, double* bwd_host) {
     D2FT_REQUIRE(!partitioned(), kState, "prepass: not available on a head-partitioned engine");
-    D2FT_REQUIRE(!lora_rank, kState, "prepass: adapter (LoRA-mode) scores are not implemented");
+    if (lora_rank) return prepass_lora(n_units, mbs, fwd_metric, bwd_metric, fwd_host, bwd_host);
     const int B = n_units * mbs;
     begin_step(B);
     const int K = D.K();
@@ -924,6 +926,33 @@ struct Engine {
     D2FT_CUDA(cudaMemcpyAsync(fwd_host, fo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
     D2FT_CUDA(cudaMemcpyAsync(bwd_host, bo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
   }
+  // LoRA mode (scoring.cpp:129-148 with lora_enabled): the metric runs over
+  // the adapter gradients of each unit's own forward/backward (all Full), so
+  // the units run one after another on the staged samples; the weight sums
+  // use the adapters (visit_trainable).  Parameters and velocities untouched.
+  void prepass_lora(int n_units, int mbs, int fwd_metric, int bwd_metric, double* fwd_host, double* bwd_host) {
+    const int B = n_units * mbs, K = D.K();
+    const size_t per = (size_t)D.T * D.d;
+    if (!lab_stage) lab_stage = dalloc<int>(D.Bmax, owned);
+    if (!lora_scores) lora_scores = dalloc<double>(2 * (size_t)K * D.Bmax, owned);
+    double *fo = lora_scores, *bo = lora_scores + (size_t)K * n_units;
+    D2FT_CUDA(cudaMemcpyAsync(samples_stage, samples_dev, (size_t)B * per * 4, cudaMemcpyDeviceToDevice, st));
+    D2FT_CUDA(cudaMemcpyAsync(lab_stage, labels_dev, (size_t)B * 4, cudaMemcpyDeviceToDevice, st));
+    for (int u = 0; u < n_units; ++u) {
+      begin_step(mbs);
+      D2FT_CUDA(cudaMemcpyAsync(samples_dev, samples_stage + (size_t)u * mbs * per, (size_t)mbs * per * 4,
+                                cudaMemcpyDeviceToDevice, st));
+      D2FT_CUDA(cudaMemcpyAsync(labels_dev, lab_stage + (size_t)u * mbs, (size_t)mbs * 4, cudaMemcpyDeviceToDevice, st));
+      D2FT_CUDA(cudaMemsetAsync(codes_exp, 1, (size_t)K * D.Bmax, st));  // every cell Full
+      compact_and_plan();
+      run_forward_backward();
+      launch_lora_score(D, lora_rank, LA, LG, fwd_metric, bwd_metric, u, n_units, fo, bo, st);
+    }
+    D2FT_CUDA(cudaMemcpyAsync(fwd_host, fo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
+    D2FT_CUDA(cudaMemcpyAsync(bwd_host, bo, (size_t)K * n_units * 8, cudaMemcpyDeviceToHost, st));
+  }
+  int* lab_stage = nullptr;
+  double* lora_scores = nullptr;
   float* score_buf = nullptr;
   double* score_dbl = nullptr;
   size_t score_cap = 0;
@@ -1392,6 +1421,30 @@ int d2ft_engine_forward_backward(d2ft_engine* h, const float* samples, const int
     E.run_forward_backward();
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
+  });
+}
+
+int d2ft_engine_logits(d2ft_engine* h, const float* samples, int n, double* logits_out) {
+  return guarded([&] {
+    Engine& E = *h->e;
+    D2FT_REQUIRE(samples && logits_out, kInput, "logits: null argument");
+    D2FT_REQUIRE(n >= 1 && n <= E.D.Bmax, kSize, "logits: batch exceeds the engine capacity");
+    // every subnet active (model.cpp logits): a forward-only column runs the
+    // identical forward; no block backward, no update
+    std::vector<uint8_t> col(E.D.K(), 2);
+    std::vector<int32_t> lab(n, 0);
+    E.begin_step(n);
+    const size_t xs = (size_t)n * E.D.T * E.D.d;
+    D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, samples, xs * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, lab.data(), n * 4, cudaMemcpyHostToDevice, E.st));
+    D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, col.data(), E.D.K(), cudaMemcpyHostToDevice, E.st));
+    launch_expand_codes(E.codes_mb, E.D.K(), 1, n, n, E.D.Bmax, E.codes_exp, E.st);
+    E.compact_and_plan();
+    E.run_forward_backward();
+    std::vector<float> lg((size_t)n * E.D.C);
+    D2FT_CUDA(cudaMemcpyAsync(lg.data(), E.logits_dev, lg.size() * 4, cudaMemcpyDeviceToHost, E.st));
+    check_status(E.finish_and_check());
+    for (size_t i = 0; i < lg.size(); ++i) logits_out[i] = lg[i];
   });
 }
 

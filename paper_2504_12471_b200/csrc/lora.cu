@@ -119,7 +119,46 @@ __global__ void __launch_bounds__(256) lora_grad_kernel(Dims D, int rank, float 
   }
 }
 
+// LoRA-mode pre-pass scores (scoring.cpp:57-96 with lora_mode: visit_trainable
+// walks only the six adapter tensors of a block subnet): one CTA per (l, h),
+// fp64 sums in a fixed order (per-thread strided partials, then a tree), the
+// chosen metric of the unit's adapter gradient -> fo / bo [K][n_units].
+__global__ void __launch_bounds__(256) lora_score_kernel(Dims D, int rank, const float* A, const float* AG, int fm,
+                                                         int bm, int unit, int n_units, double* fo, double* bo) {
+  const int lh = blockIdx.x;
+  const size_t per = 3 * ((size_t)D.d * rank + (size_t)rank * D.dh);
+  const float* w = A + lh * per;
+  const float* g = AG + lh * per;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // fisher, |w|, |g|, |w g| (Metric enum order)
+  for (size_t i = threadIdx.x; i < per; i += blockDim.x) {
+    const double gv = g[i], wv = w[i];
+    acc[0] += gv * gv;
+    acc[1] += fabs(wv);
+    acc[2] += fabs(gv);
+    acc[3] += fabs(wv * gv);
+  }
+  __shared__ double red[4][256];
+  for (int m = 0; m < 4; ++m) red[m][threadIdx.x] = acc[m];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int m = 0; m < 4; ++m) red[m][threadIdx.x] += red[m][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    fo[(size_t)lh * n_units + unit] = red[fm][0];
+    bo[(size_t)lh * n_units + unit] = red[bm][0];
+  }
+}
+
 }  // namespace
+
+void launch_lora_score(const Dims& D, int rank, const float* A, const float* AG, int fwd_metric, int bwd_metric,
+                       int unit, int n_units, double* fo, double* bo, cudaStream_t st) {
+  lora_score_kernel<<<D.L * D.H, 256, 0, st>>>(D, rank, A, AG, fwd_metric, bwd_metric, unit, n_units, fo, bo);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
 
 void launch_lora_merge(const Dims& D, int rank, float scaling, const float* W1T, const float* A, act_t* W1T_bf,
                        cudaStream_t st) {

@@ -297,7 +297,7 @@ __device__ __forceinline__ void cluster_barrier() {
 template <int NV>
 __global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, const int* labels, const float* Wc,
                                                    const float* bc, float scale, double* loss_s, float* pooled_out,
-                                                   float* dlog_out, float* dX, float* gmax) {
+                                                   float* dlog_out, float* dX, float* gmax, float* logits_out) {
   D2FT_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int nw = blockDim.x >> 5;
@@ -362,7 +362,10 @@ __global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, cons
     float z = 0.f;
     for (int m = lane; m < D.d; m += 32) z += pooled[m] * Wc[(size_t)m * D.C + c];
     z = warp_sum(z);
-    if (lane == 0) logits[c] = z + bc[c];
+    if (lane == 0) {
+      logits[c] = z + bc[c];
+      if (rank == 0) logits_out[(size_t)s * D.C + c] = logits[c];  // SubnetModel::logits (evaluate)
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // cross_entropy, model.cpp:400-414 (fp64 reduction)
@@ -1064,7 +1067,7 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 }
 
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st) {
+                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, float* logits, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
   const int threads = 512;
   const size_t sm = (size_t)((threads / 32 + 3) * D.d + 2 * D.T) * 4;
@@ -1082,7 +1085,8 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    D2FT_CUDA(cudaLaunchKernelEx(&cfg, head_kernel<NV>, D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax));
+    D2FT_CUDA(cudaLaunchKernelEx(&cfg, head_kernel<NV>, D, xL, labels, Wc, bc, scale, loss_s, pooled, dlog, dX, gmax,
+                                 logits));
   });
   count_launch();
   D2FT_CUDA(cudaGetLastError());

@@ -46,9 +46,9 @@ int sm_max_attn();
 void launch_attn_bwd_tc(const CUtensorMap& tmQKV, const CUtensorMap& tmdO, const Dims& D, int l, const int* full_heads,
                         const int* full_hcnt, const float* O32T, const float* lse, act_t* dY1T, cudaStream_t st);
 bool attn_bwd_tc_fits(int TQ);
-// head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, dlogits, and dX = dL/dx_L
+// head: LN -> mean-pool -> linear -> CE; writes loss_s, pooled, logits, dlogits, and dX = dL/dx_L
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
-                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, cudaStream_t st);
+                 double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, float* logits, cudaStream_t st);
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
                         float* dbc, double* loss, cudaStream_t st);
 // dX += LN_bwd(x_l, dxn) for samples with a Full head in block l (if l >= 0), then
@@ -72,6 +72,8 @@ void launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
 // gradients from G7's q/k/v weight gradient
 void launch_lora_merge(const Dims& D, int rank, float scaling, const float* W1T, const float* A, act_t* W1T_bf,
                        cudaStream_t st);
+void launch_lora_score(const Dims& D, int rank, const float* A, const float* AG, int fwd_metric, int bwd_metric,
+                       int unit, int n_units, double* fo, double* bo, cudaStream_t st);
 void launch_lora_grad(const Dims& D, int rank, float scaling, const float* G1T, const float* A, float* AG,
                       const int* full_cnt, cudaStream_t st);
 

@@ -286,6 +286,28 @@ def test_oracle_lora_matches_reference():
     assert np.max(np.abs(v3 - v_o)) < 1e-12
 
 
+@needs_ref
+def test_oracle_lora_prepass_matches_reference():
+    """prepass_scores in LoRA mode (scoring.cpp:108-151 with lora_enabled():
+    the metrics walk the adapter tensors only) of the numpy restatement
+    against the unmodified reference, every metric pair."""
+    cfg = MO.Config(2, 4, 32, 64, 16, 4)
+    rank, scaling = 4, 0.5
+    r = O.RefModel(2, 4, 32, 64, 16, 4, 1)
+    p = O.partition_model(2, 4, 32, 64, 16, 4, 1) + 0.05 * np.random.default_rng(2).standard_normal(r.n)
+    r.set_params(p)
+    r.attach_lora(rank, scaling)
+    _, ad = _split_lora(cfg, rank, r.params())
+    ad = ad + 0.05 * np.random.default_rng(4).standard_normal(ad.size)
+    r.set_params(_join_lora(cfg, rank, p, ad))
+    x, y = O.make_dataset(4, 4, 32, 16, 0.5, 7)
+    for mbs in (1, 2):
+        for fi, bi in ((0, 1), (2, 3)):
+            rf, rb = r.prepass_scores(x, y, mbs, fi, bi)
+            of, ob = MO.prepass_scores_lora(cfg, p, rank, scaling, ad, x, y, mbs, MO.METRICS[fi], MO.METRICS[bi])
+            assert np.allclose(of, rf, rtol=1e-10, atol=0) and np.allclose(ob, rb, rtol=1e-10, atol=0)
+
+
 def test_parallel_trainer_matches_serial():
     """train_batch_parallel (the forked-worker oracle of the batch-64 ViT-B
     parity test) equals the serial trainer body up to fp64 re-association."""

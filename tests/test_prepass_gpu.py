@@ -60,3 +60,30 @@ def test_prepass_feeds_the_step():
     assert np.isfinite(loss)
     assert np.array_equal(table.codes, S.knapsack_schedule(t, S.CostModel(), caps).codes)
     m.close()
+
+
+@pytest.mark.parametrize("cfg", [SMALL, SMALL64], ids=["dh32", "dh64"])
+@pytest.mark.parametrize("mbs", [1, 2])
+def test_prepass_lora_matches_oracle(cfg, mbs):
+    """LoRA-mode pre-pass (scoring.cpp:108-151 with lora_enabled(): metrics
+    over the adapter tensors, oracle pinned to the reference in
+    test_oracle_pins.py::test_oracle_lora_prepass_matches_reference)."""
+    rank, scaling = 4, 0.5
+    p = E.partition_model(cfg) + 0.02 * np.random.default_rng(5).standard_normal(E.param_count(cfg))
+    ad = E.lora_init(cfg, rank) + 0.05 * np.random.default_rng(6).standard_normal(
+        E.lora_init(cfg, rank).size)
+    n = 4
+    x, y = E.make_synthetic_dataset(8, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    x, y = x[:n], y[:n]
+    m = E.SubnetModel(cfg, n, p)
+    m.attach_lora(rank, scaling, ad)
+    before, abefore = m.params(), m.lora_params()
+    for fm, bm in (("fisher_information", "weight_magnitude"), ("gradient_magnitude", "taylor_importance")):
+        t = m.prepass_scores(x, y, mbs, fm, bm)
+        rf, rb = MO.prepass_scores_lora(_oc(cfg), p, rank, scaling, ad, x.astype(np.float64), y, mbs, fm, bm)
+        for got, ref, metric in ((t.forward, rf, fm), (t.backward, rb, bm)):
+            tol = 1e-5 if metric == "weight_magnitude" else 2e-2
+            rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
+            assert rel.max() <= tol, (metric, rel.max(), np.unravel_index(rel.argmax(), rel.shape))
+    assert np.array_equal(m.params(), before) and np.array_equal(m.lora_params(), abefore)
+    m.close()

@@ -29,3 +29,21 @@ def test_reference_scheduler_suite_on_reference_cpu():
         pytest.skip("oracle/_ref/test_scheduler_ref not built")
     r = subprocess.run([REF], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "failed: 0" in r.stdout, r.stdout[-3000:]
+
+
+TRAINER = os.path.join(ROOT, "oracle", "_ref", "test_b200_model_trainer")
+
+
+@pytest.mark.gpu
+def test_reference_operator_and_trainer_cases_on_b200():
+    """The reference's test_model.cpp / test_trainer.cpp cases (adapted to the
+    B200 tile sizes, integration/tests/test_b200_model_trainer.cpp) through the
+    operator / trainer binding (integration/d2ft_b200_trainer.cpp): device
+    forward_backward, logits / evaluate, the train() loop for every policy,
+    update locality, cost fractions, LoRA freezing, failure before mutation."""
+    if not os.path.exists(TRAINER):
+        pytest.skip("oracle/_ref/test_b200_model_trainer not built (needs /root/reference at build time)")
+    r = subprocess.run([TRAINER], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "failed: 0" in r.stdout

@@ -54,6 +54,29 @@ def test_forward_backward_parity(cfg, colkind):
     assert not bad, bad[:8]
 
 
+@pytest.mark.parametrize("T", [1, 8, 16, 24])
+@pytest.mark.parametrize("H", [2, 4], ids=["dh64", "dh32"])
+def test_short_sequences_vs_oracle(T, H):
+    """Sequences shorter than one 128-row UMMA tile (the tcgen05 attention
+    reads its K / V tiles as M = 128 operands): forward/backward parity."""
+    cfg = E.ModelConfig(2, H, 128, 256, T, 4, 17)
+    oc, sl = _cfgs(cfg)
+    p = _perturbed_params(cfg)
+    x, y = E.make_synthetic_dataset(4, cfg.num_classes, cfg.model_dim, cfg.seq_len, 0.5, 7)
+    K = cfg.scheduled_subnet_count()
+    col = np.array([(1, 2, 1, 3)[k % 4] for k in range(K)], np.uint8)
+    m = E.SubnetModel(cfg, 4, p)
+    loss, g, eng = m.forward_backward(x[:3], y[:3], col)
+    rl, rg, reng = MO.forward_backward(oc, p, x[:3].astype(np.float64), y[:3], col)
+    assert np.array_equal(eng, reng)
+    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
+    # T = 1: softmax over one key is constant, dWq / dWk are exactly 0 in the
+    # reference and fp32 cancellation residue (~1e-8) here: absolute check
+    bad = compare_tensors(g, rg, sl, GRAD_TOL, skip_zero_ref=False)
+    assert not bad, bad[:8]
+    m.close()
+
+
 def test_forward_only_keeps_loss_and_drops_grads():
     # test_model.cpp:326-369: p_o changes no loss vs p_f; grads only for Full
     cfg = SMALL
