@@ -221,6 +221,31 @@ def lora_leg(x, y, fwd, bwd, capf, capo, B, steps=10, warmup=3, rank=8):
             "ms_per_step": ms_step, "steps": steps, "warmup": warmup, "loss": loss.value}
 
 
+def surrogate_leg(x, y, fwd, bwd, capf, capo, B, steps=10, warmup=3, rank=16):
+    """North_star's "skip-with-linear-surrogate" p_s (opt-in, off in the
+    headline): the same batch and schedule with rank-16 surrogates on every
+    head-subnet — the p_s cells (14 of 64 per row here) add LN(x).down.up
+    through two small dense GEMMs per block (step_gemms.cuh Sur1 / Sur2)."""
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    from paper_2504_12471_b200 import scheduler as S
+    lib = _lib.lib()
+    K = L * H
+    m = E.SubnetModel(E.VIT_B16, B)
+    m.set_surrogate(rank, 0.02 * np.random.default_rng(1).standard_normal(K * 2 * D * rank))
+    m.stage(x, y, S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
+    ms, loss = C.c_double(), C.c_double()
+    _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+                                            C.c_int(warmup), C.c_int(steps), C.byref(ms), C.byref(loss)))
+    m.close()
+    ms_step = ms.value / steps
+    flops = 2 * 2 * B * T * D * H * rank * L  # Sur1 + Sur2, dense over the batch
+    return {"workload": f"ViT-B/16 D2FT step with rank-{rank} linear surrogates on the p_s cells, batch {B}, "
+                        f"same schedule", "value": B / (ms_step * 1e-3), "unit": "samples/s",
+            "ms_per_step": ms_step, "steps": steps, "warmup": warmup, "loss": loss.value,
+            "surrogate_gflop_per_step": flops / 1e9}
+
+
 def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
     """BASELINE configs[3]'s model and batch (ViT-L/16, L24 H16 d1024 ffn4096,
     batch 256): device-resident steps, same schedule recipe and data
@@ -669,6 +694,12 @@ def run_ours(args):
             lora = lora_leg(x, y, fwd, bwd, capf, capo, B)
         except Exception as e:
             lora = {"error": str(e)[:200]}
+    surr = None
+    if rank == 0 and world == 1:
+        try:
+            surr = surrogate_leg(x, y, fwd, bwd, capf, capo, B)
+        except Exception as e:
+            surr = {"error": str(e)[:200]}
     vitl = None
     if not args.no_vitl and (world == 1 or world == 8):
         try:
@@ -721,6 +752,8 @@ def run_ours(args):
         line["schedule_metrics"] = sched_metrics
         if lora:
             line["lora"] = lora
+        if surr:
+            line["surrogate"] = surr
         if part_info:
             line["partition"] = part_info
         if vitl:

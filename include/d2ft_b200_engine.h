@@ -54,6 +54,16 @@ int d2ft_engine_set_lora(d2ft_engine* e, const double* adapters); /* also zeroes
 /* which: 0 adapters, 1 velocity, 2 gradients of the last forward_backward / step */
 int d2ft_engine_get_lora(d2ft_engine* e, int which, double* adapters);
 
+/* Opt-in p_s surrogate ("skip with a linear surrogate", BASELINE north_star /
+ * PAPER.md:25-26; the reference's p_s is a pure bypass, model.cpp:326-328,
+ * 458, which rank 0 — the default — keeps bit for bit).  With rank R > 0 a
+ * shortcut cell (sample s, head-subnet (l,h)) adds LN(x_l)_s . down . up to
+ * the block output: factors per block subnet in scheduled order (l-major,
+ * h-minor), down [d][R] then up [R][d], fp64 (stored fp16).  Frozen: no
+ * gradient flows through a surrogate (as p_o, model.cpp:501).  R a multiple
+ * of 8 in [8, 64]; state error on a head-partitioned engine. */
+int d2ft_engine_set_surrogate(d2ft_engine* e, int rank, const double* factors);
+
 /* SubnetModel::forward_backward (model.cpp:416-520) for n samples of one
  * micro-batch under one schedule column (K = L*H codes).  Loss = mean CE;
  * gradients (scaled 1/n) readable with d2ft_engine_get_grads. */

@@ -182,15 +182,25 @@ def contribution_backward(cfg, blk, h, c, dc, dxn, gb, ad=None, scaling=0.0, ga=
         dxn += dproj @ blk[wname].T
 
 
-def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trace=None, lora=None):
+def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trace=None, lora=None, surrogate=None):
     """SubnetModel::forward_backward, model.cpp:416-520.
 
     Returns (loss, grads_flat, engaged[K+2]).  `trace`, if a dict, receives the
     block inputs per sample (for activation-level parity checks).
     lora = (rank, scaling, adapters_flat): adapters attached (model.cpp:165-195);
     then only the adapters get gradients and the result is
-    (loss, adapter_grads_flat, engaged)."""
+    (loss, adapter_grads_flat, engaged).
+    surrogate = (rank, factors_flat): the opt-in p_s surrogate of the B200
+    engine (d2ft_engine_set_surrogate; not a reference feature): a shortcut
+    cell adds xn . down . up (per block subnet: down [d][R], up [R][d]),
+    stop-gradient like p_o."""
     p = unpack(cfg, flat)
+    sur = None
+    if surrogate is not None:
+        sr, sflat = surrogate
+        per = 2 * cfg.d * sr
+        sur = [(sflat[k * per:k * per + cfg.d * sr].reshape(cfg.d, sr),
+                sflat[k * per + cfg.d * sr:(k + 1) * per].reshape(sr, cfg.d)) for k in range(cfg.K)]
     grads = np.zeros_like(flat)
     g = unpack(cfg, grads)
     ads = gads = None
@@ -223,6 +233,8 @@ def forward_backward(cfg: Config, flat: np.ndarray, inputs, labels, column, trac
                 r = l * H + h
                 op = column[r]
                 if op == 3:
+                    if sur is not None:
+                        acc += (xn @ sur[r][0]) @ sur[r][1]
                     continue
                 cache = {} if op == 1 else None
                 acc += block_contribution(cfg, p["blocks"][r], h, xn, cache, ads[r] if ads else None, scaling)
@@ -334,7 +346,7 @@ def train_batch_lora(cfg: Config, flat, rank, scaling, aflat, avel, inputs, labe
 
 
 def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, labels, codes, mbs,
-                lr, momentum):
+                lr, momentum, surrogate=None):
     """Trainer batch body, trainer.cpp:247-268, updating flat/velocity in place.
 
     inputs: n_mb*mbs samples in unit order; codes: K x n_mb table."""
@@ -347,7 +359,7 @@ def train_batch(cfg: Config, flat: np.ndarray, velocity: np.ndarray, inputs, lab
     for j in range(n_mb):
         xs = inputs[j * mbs:(j + 1) * mbs]
         ls = labels[j * mbs:(j + 1) * mbs]
-        loss, gr, eng = forward_backward(cfg, flat, xs, ls, codes[:, j])
+        loss, gr, eng = forward_backward(cfg, flat, xs, ls, codes[:, j], surrogate=surrogate)
         batch_loss += loss * inv_mb
         accum += gr * inv_mb
         touched |= eng.astype(bool)

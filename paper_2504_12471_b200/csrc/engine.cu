@@ -137,6 +137,11 @@ struct Engine {
   size_t lora_per() const { return 3 * ((size_t)D.d * lora_rank + (size_t)lora_rank * D.dh); }
   size_t lora_count() const { return (size_t)D.L * D.H * lora_per(); }
   act_t *W1T_bf, *W2T_bf, *WeT_bf;  // fp16 operand copies (G4 / G8 read W2T / W1T MN-major)
+  // opt-in p_s surrogate (step_gemms.cuh Sur1 / Sur2): rank 0 = the
+  // reference's pure bypass; SurA [L][H*R][d], SurB [L][d][H*R], U [Bmax][H*R][TP]
+  int sur_rank = 0;
+  act_t *SurA = nullptr, *SurB = nullptr, *SurU = nullptr;
+  CUtensorMap tm_SA, tm_SB, tm_U64;
 
   // activations
   float* x;       // [L+1][Bmax][T][d]
@@ -642,6 +647,49 @@ struct Engine {
     launch_f32_to_act(P + seg[S_WET].off, WeT_bf, seg[S_WET].n, st);
   }
 
+  // factors per block subnet (l, h) in scheduled order: down [d][R], up [R][d]
+  void set_surrogate(int rank, const double* factors) {
+    D2FT_REQUIRE(!partitioned(), kState, "surrogate: not available on a head-partitioned engine");
+    D2FT_REQUIRE(rank == 0 || (rank >= 8 && rank <= 64 && rank % 8 == 0), kConfig,
+                 "surrogate rank must be 0 (off) or a multiple of 8 in [8, 64]");
+    D2FT_REQUIRE(rank == 0 || factors, kInput, "surrogate: null factors");
+    drop_graph();
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    if (rank == 0) {
+      sur_rank = 0;
+      return;
+    }
+    const size_t L = D.L, H = D.H, d = D.d, R = rank, HR = H * R;
+    if (rank != sur_rank) {
+      for (act_t* q : {SurA, SurB, SurU})
+        if (q) {
+          owned.erase(std::find(owned.begin(), owned.end(), (void*)q));
+          cudaFree(q);
+        }
+      SurA = dalloc<act_t>(L * HR * d, owned);
+      SurB = dalloc<act_t>(L * d * HR, owned);
+      SurU = dalloc<act_t>((size_t)D.Bmax * HR * D.TP, owned);
+      D2FT_CUDA(cudaMemset(SurU, 0, (size_t)D.Bmax * HR * D.TP * sizeof(act_t)));
+      tm_SA = make_tmap_f16_3d(SurA, d, HR, L, d * 2, HR * d * 2, 64);
+      tm_SB = make_tmap_f16_3d(SurB, HR, d, L, HR * 2, d * HR * 2, 64);
+      tm_U64 = make_tmap_f16_3d(SurU, D.T, HR, D.Bmax, (uint64_t)D.TP * 2, HR * D.TP * 2, 64);
+    }
+    std::vector<act_t> a(L * HR * d), b(L * d * HR);
+    for (size_t l = 0; l < L; ++l)
+      for (size_t h = 0; h < H; ++h) {
+        const double* down = factors + (l * H + h) * 2 * d * R;
+        const double* up = down + d * R;
+        for (size_t i = 0; i < d; ++i)
+          for (size_t r = 0; r < R; ++r) {
+            a[(l * HR + h * R + r) * d + i] = __float2half_rn((float)down[i * R + r]);
+            b[(l * d + i) * HR + h * R + r] = __float2half_rn((float)up[r * d + i]);
+          }
+      }
+    D2FT_CUDA(cudaMemcpy(SurA, a.data(), a.size() * sizeof(act_t), cudaMemcpyHostToDevice));
+    D2FT_CUDA(cudaMemcpy(SurB, b.data(), b.size() * sizeof(act_t), cudaMemcpyHostToDevice));
+    sur_rank = rank;
+  }
+
   void set_params(const double* flat) {
     std::vector<float> a(nparam, 0.f);
     convert<true>(const_cast<double*>(flat), a);
@@ -747,6 +795,11 @@ struct Engine {
                          P + seg[S_B2].off + (size_t)l * d, xres, x + (l + 1) * xs, ord_act + l * Bm + lo,
                          XC > 1 ? xctr(l, 0, c) : ctr(l, C_G3));
         if (partitioned()) exchange_chunk(0, l, c, x + (l + 1) * xs, lo, n);
+      }
+      if (sur_rank) {  // p_s cells add their linear surrogate (off in parity mode)
+        const int HR = D.H * sur_rank;
+        gemm_tokN<Sur1>(tm_SA, tm_xn, D, l, HR, sur_rank, (const int*)lists.act_cnt, (const uint8_t*)codes_exp, SurU);
+        gemm_tokN<Sur2, 1>(tm_SB, tm_U64, D, l, HR, (const int*)lists.act_cnt, x + (l + 1) * xs);
       }
     }
     if (partitioned())
@@ -1316,6 +1369,13 @@ int d2ft_engine_get_velocity(d2ft_engine* e, double* flat) {
 
 int d2ft_engine_get_grads(d2ft_engine* e, double* flat) {
   return guarded([&] { e->e->get_arena(e->e->G, flat); });
+}
+
+int d2ft_engine_set_surrogate(d2ft_engine* e, int rank, const double* factors) {
+  return guarded([&] {
+    D2FT_REQUIRE(e && e->e, kInput, "set_surrogate: null engine");
+    e->e->set_surrogate(rank, factors);
+  });
 }
 
 int d2ft_engine_attach_lora(d2ft_engine* e, int rank, double scaling, const double* adapters) {

@@ -820,4 +820,82 @@ struct S5 {
   }
 };
 
+// ---------------------------------------------------------------- surrogate (opt-in p_s)
+// p_s as "skip with a linear surrogate" (north_star) instead
+// of the reference's pure bypass (model.cpp:326-328, 458): a shortcut cell
+// (s, l, h) adds xn_s . A_{l,h} . B_{l,h} (rank-R factors, frozen, no
+// gradient — like p_o it never runs backward, model.cpp:501).  Off (rank 0)
+// in every parity run; two small dense GEMMs per block when on:
+//   Sur1: U[s] = xn_s . [A_{l,1} .. A_{l,H}]   (M = H*R features, N = tokens, K = d)
+//         epilogue keeps a head's R columns only where the cell is p_s -> U [Bmax][H*R][TP] fp16
+//   Sur2: x_{l+1}[s] += U[s] . [B_{l,1}; ..; B_{l,H}]   (M = d, N = tokens, K = H*R, B read MN-major)
+// A operands: SurA [L][H*R][d] (A^T), SurB [L][d][H*R] (B^T), fp16.  Samples
+// without a p_s cell in the block skip both (nkb = 0).
+template <int BN>
+struct Sur1 {
+  Dims D;
+  int l, HR, R;
+  const int* act_cnt;    // [Bmax][L]
+  const uint8_t* codes;  // expanded K x Bmax
+  act_t* U;              // [Bmax][HR][TP]
+  struct Tile {
+    int nkb, s, mt;
+  };
+  using Row = NoRow;
+  __device__ int ntiles() const { return D.B * mpairs((HR + 127) / 128); }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    const int mp = mpairs((HR + 127) / 128);
+    c.s = t / mp;
+    c.mt = 2 * (t % mp) + rank;
+    c.nkb = act_cnt[c.s * D.L + l] < D.H ? D.d / 64 : 0;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, l, kb * 64, 0, l * D.Bmax + c.s};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int f = c.mt * 128 + row;
+    if (c.nkb == 0 || f >= HR || col0 >= D.T) return;
+    const bool ps = codes[(size_t)(l * D.H + f / R) * D.Bmax + c.s] == 3;
+    act_t* u = U + ((size_t)c.s * HR + f) * D.TP + col0;
+#pragma unroll
+    for (int i = 0; i < 16; i += 2)
+      if (col0 + i < D.TP)
+        *reinterpret_cast<__half2*>(u + i) = __floats2half2_rn(ps ? v[i] : 0.f, ps ? v[i + 1] : 0.f);
+  }
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
+};
+
+template <int BN>
+struct Sur2 {
+  Dims D;
+  int l, HR;
+  const int* act_cnt;
+  float* xout;  // x_{l+1}, already holding x_l + the active heads (G3)
+  struct Tile {
+    int nkb, s, mt;
+  };
+  using Row = NoRow;
+  __device__ int ntiles() const { return D.B * mpairs(D.d / 128); }
+  __device__ int ncols(const Tile&) const { return D.T; }
+  __device__ void tile(int t, int rank, Tile& c) const {
+    c.s = t / mpairs(D.d / 128);
+    c.mt = 2 * (t % mpairs(D.d / 128)) + rank;
+    c.nkb = act_cnt[c.s * D.L + l] < D.H ? (HR + 63) / 64 : 0;
+  }
+  __device__ KCoord kcoord(const Tile& c, int kb) const {
+    return KCoord{kb * 64, c.mt * 128, c.mt * 128 + 64, l, 0, kb * 64, c.s};
+  }
+  __device__ void row_begin(const Tile&, int, Row&) const {}
+  __device__ void chunk(const Tile& c, int row, int col0, const float (&v)[16], Row&) const {
+    const int m = c.mt * 128 + row;
+    if (c.nkb == 0 || m >= D.d || col0 >= D.T) return;
+    float* x = xout + ((size_t)c.s * D.T + col0) * D.d + m;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col0 + i < D.T) x[(size_t)i * D.d] += v[i];
+  }
+  __device__ void row_end(const Tile&, int, int, Row&) const {}
+};
+
 }  // namespace d2ft_b200

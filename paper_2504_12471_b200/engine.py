@@ -234,6 +234,22 @@ class SubnetModel:
         check(lib().d2ft_engine_get_grads(self._h, ptr(out)))
         return out
 
+    # ---- opt-in p_s surrogate (d2ft_engine_set_surrogate) ------------------
+    def set_surrogate(self, rank: int, factors=None) -> None:
+        """p_s as "skip with a linear surrogate" (BASELINE north_star): a
+        shortcut cell adds LN(x)_s . down . up; factors per block subnet in
+        scheduled order, down [d][rank] then up [rank][d].  rank 0 restores the
+        reference's pure bypass (the default; every parity run)."""
+        cfg = self.config
+        n = cfg.scheduled_subnet_count() * 2 * cfg.model_dim * rank
+        a = None
+        if rank:
+            a = f64(factors)
+            if a.size != n:
+                raise Error(3, f"set_surrogate: expected {n} values, got {a.size}")
+        check(lib().d2ft_engine_set_surrogate(self._h, C.c_int(rank), ptr(a) if a is not None else None))
+        self.surrogate_rank = rank
+
     # ---- LoRA (model.cpp:165-195; csrc/lora.cu) ----------------------------
     def attach_lora(self, rank: int, scaling: float, adapters: np.ndarray | None = None) -> None:
         """SubnetModel::attach_lora: rank-r adapters on Q/K/V, base frozen.
