@@ -607,7 +607,6 @@ struct Engine {
   // attach_lora (model.cpp:165-195) with the caller's initial adapters
   void attach_lora(int rank, double scaling, const double* init) {
     D2FT_REQUIRE(!lora_rank, kState, "lora adapters already attached");
-    D2FT_REQUIRE(!partitioned(), kState, "lora: not available on a head-partitioned engine");
     D2FT_REQUIRE(rank >= 1, kConfig, "lora rank must be >= 1");
     const int cap = std::min(D.d, D.dh);
     D2FT_REQUIRE(rank <= cap, kConfig,

@@ -134,6 +134,18 @@ def merge_owned(cfg, flats_by_rank, part: HeadPartition | None = None) -> np.nda
     return out
 
 
+def merge_owned_lora(cfg, rank: int, flats_by_rank, part: HeadPartition) -> np.ndarray:
+    """LoRA adapters (d2ft_engine_attach_lora layout: per block subnet k, in
+    scheduled order) assembled from each subnet's owner — under a head
+    partition only the owner trains a head's adapters (its Full cells)."""
+    per = 3 * (cfg.model_dim * rank + rank * cfg.head_dim())
+    owners = part.row_owners(cfg.num_blocks)
+    out = np.array(flats_by_rank[0], np.float64, copy=True)
+    for k, r in enumerate(owners):
+        out[k * per:(k + 1) * per] = flats_by_rank[int(r)][k * per:(k + 1) * per]
+    return out
+
+
 def rank_capacities(part: HeadPartition, num_blocks: int, micro_batches: int, n_full: int, n_fwd: int,
                     cost_model=None, balance: bool = True):
     """Per-rank knapsack capacities through BudgetSpec overrides
