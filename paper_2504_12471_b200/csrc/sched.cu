@@ -47,6 +47,56 @@ __device__ inline void set_err(int32_t* err, int code) {
   if (err) atomicCAS(err, 0, code);
 }
 
+// Backtrack of one row (scheduler.cpp:176-183): from item N down, the column
+// is min(cap/wt - taken so far, i) and the decision bit says take.  Serial by
+// nature; the bit read of step i decides the address of step i-1.  Bits in
+// shared memory: one thread walks them.  Bits in global memory (large N): the
+// walk would pay a dependent L2 round trip per item (~0.4 ms for 2 x 1024
+// items), so warp 0 stages the decision words of the next 32 items (whole
+// rows, coalesced) into shared memory `stage` and lane 0 walks those.
+// bit_of(row_words, col) reads a column's bit in the path's word layout.
+template <class BitOf>
+__device__ void backtrack_row(const uint32_t* bits, int words, int N, int wt, int cap, uint8_t* sel,
+                              uint32_t* stage, BitOf bit_of) {
+  // called by one whole warp
+  const int lane = threadIdx.x & 31;
+  if (!stage) {
+    if (lane == 0) {
+      long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
+      for (int i = N; i > 0; --i) {
+        const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
+        const unsigned b = bit_of(bits + (size_t)(i - 1) * words, col);
+        sel[i - 1] = (uint8_t)b;
+        if (b && wt > 0) mm -= 1;
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
+  for (int i1 = N; i1 > 0; i1 -= 32) {
+    const int i0 = i1 > 32 ? i1 - 32 : 0;
+    const int n = (i1 - i0) * words;
+    const uint32_t* src = bits + (size_t)i0 * words;
+    for (int q = lane; q < n; q += 32) stage[q] = __ldcg(src + q);
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = i1; i > i0; --i) {
+        const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
+        const unsigned b = bit_of(stage + (size_t)(i - 1 - i0) * words, col);
+        sel[i - 1] = (uint8_t)b;
+        if (b && wt > 0) mm -= 1;
+      }
+    }
+    mm = __shfl_sync(0xffffffffu, mm, 0);
+    __syncwarp();
+  }
+}
+
+struct BitOfWords {  // column c -> word c / 32, bit c % 32 (warp and block paths)
+  __device__ unsigned operator()(const uint32_t* row, int col) const { return (row[col >> 5] >> (col & 31)) & 1u; }
+};
+
 // One warp (the training shapes: ViT-B 25 p_f of 64 -> 26 columns, ViT-L 102
 // of 256 -> 103): lane holds columns m = 32 j + lane, j < CW.  Column m-1
 // comes from the lane below (shuffle up) or, for lane 0, from lane 31 of the
@@ -54,11 +104,12 @@ __device__ inline void set_err(int32_t* err, int code) {
 // barrier per item.  Same fp64 adds in the same order and the same
 // decision-bit words (word j = columns 32 j .. 32 j + 31) as the block path.
 // All threads of the block call it (block-uniform arguments).
+// Run by warp `wsel` alone (no block barrier): DP, objective, backtrack.
 template <int CW>
-__device__ double dp_row_warp(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
-                              double* s_obj) {
+__device__ void dp_row_warp(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
+                            double* s_obj, uint32_t* stage, int wsel) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (warp == 0) {
+  if (warp == wsel) {
     double v[CW];
     bool okc[CW];
 #pragma unroll
@@ -90,27 +141,17 @@ __device__ double dp_row_warp(const double* s_scores, int N, int wt, int cap, in
 #pragma unroll
     for (int j = 0; j < CW; ++j)
       if (32 * j + lane == Mp) *s_obj = v[j];
+    __syncwarp();
+    backtrack_row(bits, CW, N, wt, cap, sel, stage, BitOfWords{});
   }
-  __syncthreads();
-  if (tid == 0) {
-    long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
-    for (int i = N; i > 0; --i) {
-      const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
-      const unsigned b = (bits[(size_t)(i - 1) * CW + (col >> 5)] >> (col & 31)) & 1u;
-      sel[i - 1] = (uint8_t)b;
-      if (b && wt > 0) mm -= 1;
-    }
-  }
-  __syncthreads();
-  return *s_obj;
 }
 
 // Block path (more than 256 columns, up to 8 warps): columns m = j * nthr +
 // warp * 32 + lane; the boundary column of each warp crosses through a
 // double-buffered shared exchange and one named barrier per item.
 template <int CC>
-__device__ double dp_row_block(const double* s_scores, int N, int wt, int cap, int Mp, int nw, uint32_t* bits,
-                               double* xch, uint8_t* sel, double* s_obj) {
+__device__ void dp_row_block(const double* s_scores, int N, int wt, int cap, int Mp, int nw, uint32_t* bits,
+                             double* xch, uint8_t* sel, double* s_obj, uint32_t* stage) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = nw * 32;
   const int words = nw * CC;
@@ -163,18 +204,8 @@ __device__ double dp_row_block(const double* s_scores, int N, int wt, int cap, i
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    long long m = (wt == 0) ? 0 : (long long)(cap / wt);
-    for (int i = N; i > 0; --i) {
-      const long long colll = (wt == 0) ? 0 : (m < i ? m : i);
-      const int col = (int)colll;
-      const unsigned b = (bits[(size_t)(i - 1) * words + (col >> 5)] >> (col & 31)) & 1u;
-      sel[i - 1] = (uint8_t)b;
-      if (b && wt > 0) m -= 1;
-    }
-  }
+  if (warp == 0) backtrack_row(bits, words, N, wt, cap, sel, stage, BitOfWords{});
   __syncthreads();
-  return *s_obj;
 }
 
 // Single warp, contiguous columns per lane (rows of up to 32 * 40 columns:
@@ -183,14 +214,23 @@ __device__ double dp_row_block(const double* s_scores, int N, int wt, int cap, i
 // j = 0 (one shuffle per item), so an item costs one shuffle plus CL
 // independent add / compare / select — no shared-memory exchange, no barrier.
 // The same fp64 adds in the same order as the reference; decision bits are a
-// 64-bit mask per (item, lane): bits word pair 2 * (32 i + l).
+// CL-bit mask per (item, lane): one 32-bit word (CL <= 32: rows of up to
+// 1024 columns, 128 B per item, so the 1024-item sweep keeps its bits in
+// shared memory) or a word pair (CL > 32), at (32 i + l).
 constexpr int kLaneColsMax = 40;
 template <int CL>
-__device__ double dp_row_lane(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
-                              double* s_obj) {
+struct BitOfLane {  // column c -> lane c / CL, bit c % CL
+  __device__ unsigned operator()(const uint32_t* row, int col) const {
+    if constexpr (CL <= 32) return (row[col / CL] >> (col % CL)) & 1u;
+    else return (unsigned)((reinterpret_cast<const uint64_t*>(row)[col / CL] >> (col % CL)) & 1u);
+  }
+};
+template <int CL>
+__device__ void dp_row_lane(const double* s_scores, int N, int wt, int cap, int Mp, uint32_t* bits, uint8_t* sel,
+                            double* s_obj, uint32_t* stage, int wsel) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint64_t* mb = reinterpret_cast<uint64_t*>(bits);
-  if (warp == 0) {
+  constexpr int kWords = CL <= 32 ? 32 : 64;  // decision words per item
+  if (warp == wsel) {
     double v[CL];
     bool okc[CL];
 #pragma unroll
@@ -214,69 +254,78 @@ __device__ double dp_row_lane(const double* s_scores, int N, int wt, int cap, in
           acc4[j & 3] |= (uint64_t)d << j;
         }
       } else {
+        // all takes from the previous item's values first, then the compares,
+        // then the updates: CL independent chains the scheduler can interleave
+        // (the fused per-column form issued DADD -> DSETP -> FSEL serially,
+        // ~25 cycles a column).  Columns past Mp may update freely (nothing at
+        // or below Mp reads them, the backtrack never visits them); column 0
+        // (lane 0) never takes: its left neighbour is -inf.
+        double t[CL];
+        t[0] = __dadd_rn(lane == 0 ? -INFINITY : left, s);
 #pragma unroll
-        for (int j = CL - 1; j >= 1; --j) {  // downwards: v[j-1] is still the previous item's
-          const double take = __dadd_rn(v[j - 1], s);
-          const bool d = okc[j] && (take > v[j]);  // scheduler.cpp:167 strict >
-          if (d) v[j] = take;
-          acc4[j & 3] |= (uint64_t)d << j;
+        for (int j = 1; j < CL; ++j) t[j] = __dadd_rn(v[j - 1], s);
+        bool d[CL];
+#pragma unroll
+        for (int j = 0; j < CL; ++j) d[j] = t[j] > v[j];  // scheduler.cpp:167 strict >
+#pragma unroll
+        for (int j = 0; j < CL; ++j) {
+          acc4[j & 3] |= (uint64_t)d[j] << j;
+          v[j] = d[j] ? t[j] : v[j];
         }
-        const double take = __dadd_rn(left, s);
-        const bool d = okc[0] && (take > v[0]);
-        if (d) v[0] = take;
-        acc4[0] |= (uint64_t)d;
       }
-      mb[(size_t)i * 32 + lane] = (acc4[0] | acc4[1]) | (acc4[2] | acc4[3]);
+      const uint64_t m = (acc4[0] | acc4[1]) | (acc4[2] | acc4[3]);
+      if constexpr (CL <= 32) bits[(size_t)i * 32 + lane] = (uint32_t)m;
+      else reinterpret_cast<uint64_t*>(bits)[(size_t)i * 32 + lane] = m;
     }
 #pragma unroll
     for (int j = 0; j < CL; ++j)
       if (lane * CL + j == Mp) *s_obj = v[j];
+    __syncwarp();
+    backtrack_row(bits, kWords, N, wt, cap, sel, stage, BitOfLane<CL>{});
   }
-  __syncthreads();
-  if (tid == 0) {
-    long long mm = (wt == 0) ? 0 : (long long)(cap / wt);
-    for (int i = N; i > 0; --i) {
-      const int col = (wt == 0) ? 0 : (int)(mm < i ? mm : i);
-      const unsigned b = (unsigned)((mb[(size_t)(i - 1) * 32 + col / CL] >> (col % CL)) & 1u);
-      sel[i - 1] = (uint8_t)b;
-      if (b && wt > 0) mm -= 1;
-    }
-  }
-  __syncthreads();
-  return *s_obj;
+}
+
+// Rows of up to 32 * kLaneColsMax count-compressed columns run on one warp
+// (`wsel`; the other warps of the block are free for the other pool).
+__device__ void dp_row_small(const double* s_scores, int N, int wt, int cap, uint32_t* bits, uint8_t* sel,
+                             double* s_obj, uint32_t* stage, int wsel) {
+  const int Mp = (wt == 0) ? 0 : min(cap / wt, N);  // last stored column
+  const int ncols = Mp + 1;
+  if (ncols <= 32) return dp_row_warp<1>(s_scores, N, wt, cap, Mp, bits, sel, s_obj, stage, wsel);
+  const int c = (ncols + 31) / 32;  // columns per lane, rounded up to an instantiated width
+#define D2FT_LANE(W) \
+  if (c <= W) return dp_row_lane<W>(s_scores, N, wt, cap, Mp, bits, sel, s_obj, stage, wsel);
+  D2FT_LANE(2) D2FT_LANE(4) D2FT_LANE(6) D2FT_LANE(8) D2FT_LANE(10) D2FT_LANE(12) D2FT_LANE(14) D2FT_LANE(16)
+  D2FT_LANE(18) D2FT_LANE(20) D2FT_LANE(24) D2FT_LANE(26) D2FT_LANE(28) D2FT_LANE(32)  // 32-bit masks
+  D2FT_LANE(33) D2FT_LANE(36)
+#undef D2FT_LANE
+  return dp_row_lane<kLaneColsMax>(s_scores, N, wt, cap, Mp, bits, sel, s_obj, stage, wsel);
 }
 
 // Count-compressed 0/1 knapsack of one row (all threads of the block call it
 // with block-uniform arguments).  s_scores: the row's N scores in shared
-// memory.  Writes sel[i] in {0,1} (shared or global) and returns the
-// objective T[N][cap] in thread 0.
-__device__ double dp_row_const(const double* s_scores, int N, int wt, int cap, uint32_t* bits, double* xch,
-                               uint8_t* sel, double* s_obj) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// memory.  Writes sel[i] in {0,1} (shared or global) and the objective
+// T[N][cap] to *s_obj, both visible to the block on return.
+__device__ void dp_row_const(const double* s_scores, int N, int wt, int cap, uint32_t* bits, double* xch,
+                             uint8_t* sel, double* s_obj, uint32_t* stage) {
   const int Mp = (wt == 0) ? 0 : min(cap / wt, N);  // last stored column
   const int ncols = Mp + 1;
+  if (ncols <= 32 * kLaneColsMax) {
+    dp_row_small(s_scores, N, wt, cap, bits, sel, s_obj, stage, 0);
+    __syncthreads();
+    return;
+  }
   int nw, C;
   row_geometry(ncols, &nw, &C);
-  if (ncols <= 32) return dp_row_warp<1>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-  if (ncols <= 32 * kLaneColsMax) {
-    const int c = (ncols + 31) / 32;  // columns per lane, rounded up to an instantiated width
-    if (c <= 2) return dp_row_lane<2>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    if (c <= 4) return dp_row_lane<4>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    if (c <= 8) return dp_row_lane<8>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    if (c <= 16) return dp_row_lane<16>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    if (c <= 24) return dp_row_lane<24>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    if (c <= 33) return dp_row_lane<33>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-    return dp_row_lane<kLaneColsMax>(s_scores, N, wt, cap, Mp, bits, sel, s_obj);
-  }
   switch (C) {  // compile-time columns per thread
-    case 1: return dp_row_block<1>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 2: return dp_row_block<2>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 3: return dp_row_block<3>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 4: return dp_row_block<4>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 5: return dp_row_block<5>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 6: return dp_row_block<6>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    case 7: return dp_row_block<7>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
-    default: return dp_row_block<8>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj);
+    case 1: return dp_row_block<1>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 2: return dp_row_block<2>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 3: return dp_row_block<3>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 4: return dp_row_block<4>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 5: return dp_row_block<5>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 6: return dp_row_block<6>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    case 7: return dp_row_block<7>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
+    default: return dp_row_block<8>(s_scores, N, wt, cap, Mp, nw, bits, xch, sel, s_obj, stage);
   }
 }
 
@@ -298,6 +347,7 @@ struct KnapsackArgs {
   bool validate;
   int lists_smem_bytes;  // dynamic shared memory of the launch (staging of the table for the column lists)
   bool cols_in_kernel;   // the last CTA builds the column lists (table staged in its shared memory)
+  bool two_pools;        // every row fits one warp: the two pools run concurrently (2 warps)
 };
 
 // Warp 0 writes the ascending index lists of one row (codes in smem).
@@ -347,13 +397,24 @@ __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int k = blockIdx.x;
   const int N = A.N;
+  // layout (sched_smem_layout): scores of the two pools, the block path's
+  // exchange, objectives, codes, the two pools' selections, then the two
+  // pools' decision bits (shared) or backtrack staging (bits in global)
+  const int Np = (N + 15) & ~15;
   double* s_scores = reinterpret_cast<double*>(smem);
-  double* xch = s_scores + N;                    // 2 x 8 x kCMax
-  double* s_obj = xch + 2 * 8 * kCMax;           // 1 (+pad)
-  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 2);
-  uint8_t* s_sel = s_codes + ((N + 15) & ~15);
-  uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + ((N + 15) & ~15))
-                                  : A.ws.bits_global + (size_t)k * N * A.words_max;
+  double* s_scores2 = s_scores + N;              // Forward pool (two-pool launches)
+  double* xch = s_scores2 + N;                   // 2 x 8 x kCMax
+  double* s_obj = xch + 2 * 8 * kCMax;           // [2] (+pad)
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 4);
+  uint8_t* s_sel = s_codes + Np;
+  uint8_t* s_sel2 = s_sel + Np;
+  uint32_t* bits_base = reinterpret_cast<uint32_t*>(s_sel2 + Np);
+  const size_t pool_words = A.bits_in_smem ? (size_t)N * A.words_max : (size_t)32 * A.words_max;
+  uint32_t* bits = A.bits_in_smem ? bits_base : A.ws.bits_global + (size_t)2 * k * N * A.words_max;
+  uint32_t* bits2 = A.bits_in_smem ? bits_base + pool_words : bits + (size_t)N * A.words_max;
+  // global bits: the backtrack's staging words sit where the bits would
+  uint32_t* stage = A.bits_in_smem ? nullptr : bits_base;
+  uint32_t* stage2 = A.bits_in_smem ? nullptr : bits_base + pool_words;
   // validation outcome: one bit per category, resolved after the barrier in
   // the reference's order (ScoreTable::validate -> numeric, Capacities ->
   // input, CostModel -> config; scheduler.cpp:24-43, scoring.cpp:30-47), then
@@ -391,16 +452,34 @@ __global__ void __launch_bounds__(kThreads) knapsack_kernel(KnapsackArgs A) {
     for (int i = threadIdx.x; i < N; i += blockDim.x) A.codes[(size_t)k * N + i] = 3;
     // fall through to the compaction epilogue with an all-shortcut row
   }
-  if (!s_bad) {
+  if (!s_bad && A.two_pools) {
+    // the two pools are independent DPs (scheduler.cpp:233-234): warp 0
+    // runs the Full pool on the backward scores (weight cf+cb), warp 1 the
+    // Forward pool on the forward scores (weight cf), concurrently
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      s_scores[i] = A.bwd[(size_t)k * N + i];
+      s_scores2[i] = A.fwd[(size_t)k * N + i];
+    }
+    __syncthreads();
+    dp_row_small(s_scores, N, cfk + cbk, A.cap_full[k], bits, s_sel, s_obj, stage, 0);
+    dp_row_small(s_scores2, N, cfk, A.cap_fwd[k], bits2, s_sel2, s_obj + 1, stage2, 1);
+    __syncthreads();
+    // merge (scheduler.cpp:205-216): full wins, then forward, else shortcut
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const uint8_t c = s_sel[i] ? 1 : (s_sel2[i] ? 2 : 3);
+      s_codes[i] = c;
+      A.codes[(size_t)k * N + i] = c;
+    }
+  } else if (!s_bad) {
     // pass 1: Full pool on backward scores, weight cf+cb (scheduler.cpp:233)
     for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.bwd[(size_t)k * N + i];
     __syncthreads();
-    dp_row_const(s_scores, N, cfk + cbk, A.cap_full[k], bits, xch, s_sel, s_obj);
+    dp_row_const(s_scores, N, cfk + cbk, A.cap_full[k], bits, xch, s_sel, s_obj, stage);
     for (int i = threadIdx.x; i < N; i += blockDim.x) s_codes[i] = s_sel[i] ? 1 : 3;
     // pass 2: Forward pool on forward scores, weight cf (scheduler.cpp:234)
     for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.fwd[(size_t)k * N + i];
     __syncthreads();
-    dp_row_const(s_scores, N, cfk, A.cap_fwd[k], bits, xch, s_sel, s_obj);
+    dp_row_const(s_scores, N, cfk, A.cap_fwd[k], bits, xch, s_sel, s_obj, stage);
     // merge (scheduler.cpp:205-216): full wins, then forward, else shortcut
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const uint8_t c = s_codes[i] == 1 ? 1 : (s_sel[i] ? 2 : 3);
@@ -462,16 +541,20 @@ __global__ void __launch_bounds__(kThreads) dp_const_kernel(DpConstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int k = A.rows[blockIdx.x];
   const int N = A.N;
+  // single-pool layout of sched_smem_layout(pools = 1)
+  const int Np = (N + 15) & ~15;
   double* s_scores = reinterpret_cast<double*>(smem);
   double* xch = s_scores + N;
   double* s_obj = xch + 2 * 8 * kCMax;
-  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 2);
-  uint8_t* s_sel = s_codes + ((N + 15) & ~15);
-  uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + ((N + 15) & ~15))
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(s_obj + 4);
+  uint8_t* s_sel = s_codes + Np;
+  uint32_t* bits = A.bits_in_smem ? reinterpret_cast<uint32_t*>(s_sel + Np)
                                   : A.ws.bits_global + (size_t)blockIdx.x * N * A.words_max;
+  uint32_t* stage = A.bits_in_smem ? nullptr : reinterpret_cast<uint32_t*>(s_sel + Np);
   for (int i = threadIdx.x; i < N; i += blockDim.x) s_scores[i] = A.scores[(size_t)k * N + i];
   __syncthreads();
-  const double obj = dp_row_const(s_scores, N, A.row_wt[k], A.caps[k], bits, xch, s_sel, s_obj);
+  dp_row_const(s_scores, N, A.row_wt[k], A.caps[k], bits, xch, s_sel, s_obj, stage);
+  const double obj = *s_obj;
   for (int i = threadIdx.x; i < N; i += blockDim.x) A.sel[(size_t)k * N + i] = s_sel[i];
   if (threadIdx.x == 0) A.obj[k] = obj;
 }
@@ -684,24 +767,34 @@ void launch_brute_force(const double* bwd, const double* fwd, const int32_t* cf,
 // per lane for the single-warp lane path
 int bits_words_per_item(int max_cols) {
   const int w = (max_cols + 31) / 32 + 8;
-  return max_cols <= 32 * kLaneColsMax ? (w > 64 ? w : 64) : w;
+  if (max_cols <= 32 * 32) return w > 32 ? w : 32;            // lane path, 32-bit masks
+  if (max_cols <= 32 * kLaneColsMax) return w > 64 ? w : 64;  // lane path, 64-bit masks
+  return w;
 }
-size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
+// pools = 2: the knapsack launch whose rows all fit one warp (both pools
+// concurrently, each with its own scores / selection / bits); 1: one pool at
+// a time (dp_search rows, and knapsack rows on the 8-warp block path).
+int knapsack_pools(int max_cols) { return max_cols <= 32 * kLaneColsMax ? 2 : 1; }
+size_t sched_smem_layout(int N, int max_cols, int pools, bool* bits_in_smem) {
   const int words = bits_words_per_item(max_cols);
   const size_t Np = (size_t)((N + 15) & ~15);
-  const size_t base = (size_t)N * 8 + 2 * 8 * kCMax * 8 + 16 + 2 * Np;
-  const size_t with_bits = base + (size_t)N * words * 4;
+  // scores of both pools always reserved (the kernel's layout is fixed)
+  const size_t base = (size_t)2 * N * 8 + 2 * 8 * kCMax * 8 + 32 + 3 * Np;
+  const size_t with_bits = base + (size_t)pools * N * words * 4;
   if (with_bits <= kSmemCap) {
     *bits_in_smem = true;
     return with_bits;
   }
   *bits_in_smem = false;
-  return base;
+  return base + (size_t)pools * 32 * words * 4;  // the backtrack's staging of 32 items per pool
+}
+size_t knapsack_smem_bytes(int N, int max_cols, bool* bits_in_smem) {
+  return sched_smem_layout(N, max_cols, knapsack_pools(max_cols), bits_in_smem);
 }
 
 size_t knapsack_global_bits_words(int K, int N, int max_cols) {
   const int words = bits_words_per_item(max_cols);
-  return (size_t)K * N * words;
+  return (size_t)2 * K * N * words;  // both pools of every row
 }
 
 void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_t* cf, const int32_t* cb,
@@ -726,6 +819,7 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   A.validate = validate;
   A.words_max = bits_words_per_item(max_cols);
   A.max_cols = max_cols;
+  A.two_pools = knapsack_pools(max_cols) == 2;
   size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
   // room to stage the K x N table for the last CTA's column lists (<= 48 KB)
   const size_t kn = (size_t)K * N;
@@ -742,7 +836,7 @@ void launch_knapsack_schedule(const double* bwd, const double* fwd, const int32_
   });
   // rows that fit the single-warp DP need one warp (more CTAs per SM, the
   // DP's registers only for 32 threads); wider rows use the 8-warp block path
-  const int threads = max_cols <= 32 * kLaneColsMax ? 32 : kThreads;
+  const int threads = A.two_pools ? 64 : kThreads;
   knapsack_kernel<<<K, threads, smem, stream>>>(A);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
@@ -769,9 +863,9 @@ void launch_dp_const(const double* scores, const int32_t* row_wt, const int32_t*
   A.obj = obj;
   A.ws = ws;
   A.words_max = bits_words_per_item(max_cols);
-  const size_t smem = knapsack_smem_bytes(N, max_cols, &A.bits_in_smem);
+  const size_t smem = sched_smem_layout(N, max_cols, 1, &A.bits_in_smem);
   if (!A.bits_in_smem)
-    D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= knapsack_global_bits_words(nrows, N, max_cols), kState,
+    D2FT_REQUIRE(ws.bits_global && ws.bits_global_words >= (size_t)nrows * N * A.words_max, kState,
                  "dp_search: global decision-bit workspace too small");
   D2FT_CUDA(cudaFuncSetAttribute(dp_const_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
   dp_const_kernel<<<nrows, max_cols <= 32 * kLaneColsMax ? 32 : kThreads, smem, stream>>>(A);
