@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--exchange-chunks", type=int, default=2, help="N > 1: sample chunks of the per-block exchange")
     ap.add_argument("--uniform-caps", action="store_true",
                     help="N > 1: the same budget on every rank (no BudgetSpec rebalancing)")
+    ap.add_argument("--no-dp-leg", action="store_true",
+                    help="N > 1: skip the data-parallel leg beside the head-partition headline")
     return ap.parse_args()
 
 
@@ -244,6 +246,43 @@ def surrogate_leg(x, y, fwd, bwd, capf, capo, B, steps=10, warmup=3, rank=16):
                         f"same schedule", "value": B / (ms_step * 1e-3), "unit": "samples/s",
             "ms_per_step": ms_step, "steps": steps, "warmup": warmup, "loss": loss.value,
             "surrogate_gflop_per_step": flops / 1e9}
+
+
+def dp_leg(rank, local, world, dist, steps=10, warmup=3, B_per=64):
+    """N > 1: data parallelism over the same global batch (64 N samples,
+    weak scaling): every rank stages its 64 samples and the GLOBAL score table,
+    runs the same knapsack, its samples' forward/backward, and the weight
+    gradients are all-reduced over NCCL inside the step graph before the SGD
+    (d2ft_engine_data_parallel_nccl)."""
+    from paper_2504_12471_b200 import _lib
+    from paper_2504_12471_b200 import engine as E
+    from paper_2504_12471_b200 import partition as PT
+    from paper_2504_12471_b200 import scheduler as S
+    lib = _lib.lib()
+    B = B_per * world
+    K = L * H
+    x, y, bwd, fwd, capf, capo = workload(B)
+    lo, hi = PT.dp_slice(B, 1, rank, world)
+    m = E.SubnetModel(E.VIT_B16, hi - lo)
+    PT.join_nccl_dp(m, rank, world)
+    m.stage(x[lo:hi], y[lo:hi], S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
+    ms, loss = C.c_double(), C.c_double()
+    dist.barrier()
+    _lib.check(lib.d2ft_engine_bench_device(m._h, C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+                                            C.c_int(warmup), C.c_int(steps), C.byref(ms), C.byref(loss)))
+    import torch
+    t = torch.tensor([ms.value / steps, loss.value], device="cuda", dtype=torch.float64)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t)
+    xcalls, xbytes = PT.exchange_stats(m)
+    m.close()
+    ms_step = float(mx[0].item())
+    return {"workload": f"ViT-B/16 D2FT step, global batch {B} ({B_per} per GPU), data parallel over {world} GPUs: "
+                        f"global knapsack on every rank, NCCL all-reduce of the weight gradients in the step graph",
+            "value": B / (ms_step * 1e-3), "unit": "samples/s", "ms_per_step": ms_step, "steps": steps,
+            "warmup": warmup, "loss": float(t[1].item()), "scaling": "weak",
+            "allreduce_bytes_per_step": xbytes // max(1, xcalls) if xcalls else 0}
 
 
 def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
@@ -694,6 +733,12 @@ def run_ours(args):
             lora = lora_leg(x, y, fwd, bwd, capf, capo, B)
         except Exception as e:
             lora = {"error": str(e)[:200]}
+    dpl = None
+    if dist and not args.no_dp_leg:
+        try:
+            dpl = dp_leg(rank, local, world, dist, steps=args.steps, warmup=args.warmup, B_per=args.batch)
+        except Exception as e:
+            dpl = {"error": str(e)[:200]}
     surr = None
     if rank == 0 and world == 1:
         try:
@@ -754,6 +799,8 @@ def run_ours(args):
             line["lora"] = lora
         if surr:
             line["surrogate"] = surr
+        if dpl:
+            line["data_parallel"] = dpl
         if part_info:
             line["partition"] = part_info
         if vitl:

@@ -203,6 +203,23 @@ int d2ft_local_group_destroy(d2ft_local_group* g);
 /* a rank failed: every rank waiting in the group's exchange returns a state error */
 int d2ft_local_group_abort(d2ft_local_group* g);
 int d2ft_engine_partition_local(d2ft_engine* e, d2ft_local_group* g, int rank);
+/* Data parallelism over the GLOBAL batch (an alternative to the head
+ * partition): rank r of `world` holds micro-batches [r*n_mb/world,
+ * (r+1)*n_mb/world) of every batch.  After joining, the step entry points
+ * (d2ft_engine_step, _step_pipelined, _step_codes, _stage_device /
+ * _step_resident / _bench_device / _bench_e2e) take n_mb = the global
+ * micro-batch count, the global K x n_mb score (or code) table, and THIS
+ * rank's samples and labels only; every rank runs the same knapsack over the
+ * global table, computes its samples' forward/backward with the global 1/B
+ * loss weight, and the weight gradients are all-reduced (NCCL, captured in
+ * the step graph) before the SGD, whose touched-subnet rule uses the global
+ * Full counts — trainer.cpp:247-268 for the global batch.  loss_out is this
+ * rank's share of the batch loss (sum over ranks = the batch loss).  State
+ * errors: an engine already partitioned / data parallel, LoRA adapters,
+ * the Dataset path.  n_mb must divide evenly over the ranks (config). */
+int d2ft_engine_data_parallel_nccl(d2ft_engine* e, int rank, int world, const uint8_t* id);
+int d2ft_engine_data_parallel_local(d2ft_engine* e, d2ft_local_group* g, int rank);
+
 /* row -> rank mapping of a partitioned engine: owner[k] for every scheduled
  * subnet row k = l*H + h (default after joining: h % world, head-interleaved;
  * partition.py also builds the SPEC-literal contiguous mapping of

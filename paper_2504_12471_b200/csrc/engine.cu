@@ -202,6 +202,50 @@ struct Engine {
   // partition's data path (owner mask, fp32 partial sums, the all-reduce
   // call) then runs on a one-GPU box as well.
   bool partitioned() const { return ex != nullptr; }
+  // data parallelism (d2ft_engine_data_parallel_*): rank r of W holds micro-
+  // batches [r*n_mb/W, (r+1)*n_mb/W) of the GLOBAL batch, every rank runs the
+  // same knapsack over the global score table, and the weight gradients are
+  // all-reduced before the SGD — the global batch's trainer step
+  // (trainer.cpp:247-268) with the per-sample work split across GPUs.
+  std::unique_ptr<Exchange> dpx;
+  int dp_mb0 = 0;      // first global micro-batch of this rank (current step)
+  int B_glob = 0;      // samples of the global batch (the 1/B loss weight)
+  int Nmax = 0;        // micro-batch columns the score / code tables hold (Bmax; world x Bmax when data parallel)
+  // (re)size the K x Nmax score and code tables (device and pinned host)
+  void size_tables(int nmax) {
+    D2FT_CUDA(cudaStreamSynchronize(st));
+    const size_t K = (size_t)D.K();
+    for (void* q : {(void*)bwd_dev, (void*)fwd_dev, (void*)codes_mb})
+      if (q) {
+        owned.erase(std::find(owned.begin(), owned.end(), q));
+        cudaFree(q);
+      }
+    if (h_scores) cudaFreeHost(h_scores);
+    if (h_codes) cudaFreeHost(h_codes);
+    bwd_dev = dalloc<double>(K * nmax, owned);
+    fwd_dev = dalloc<double>(K * nmax, owned);
+    codes_mb = dalloc<uint8_t>(K * nmax, owned);
+    D2FT_CUDA(cudaMallocHost(&h_scores, 2 * K * nmax * sizeof(double)));
+    D2FT_CUDA(cudaMallocHost(&h_codes, K * nmax));
+    Nmax = nmax;
+    sched_max_cols = 0;  // decision-bit workspace sized again for the new tables
+    drop_graph();
+  }
+  int* full_cnt_glob = nullptr;  // [K] Full cells per row over the global batch (SGD touch rule)
+  bool data_parallel() const { return dpx != nullptr; }
+  // samples this rank holds for a global batch of n_mb micro-batches of mbs
+  int local_B(int n_mb, int mbs) {
+    D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
+    B_glob = n_mb * mbs;
+    if (!dpx) {
+      dp_mb0 = 0;
+      return n_mb * mbs;
+    }
+    D2FT_REQUIRE(n_mb % dpx->world == 0, kConfig,
+                 "data parallel: the micro-batches of a batch must divide evenly over the ranks");
+    dp_mb0 = dpx->rank * (n_mb / dpx->world);
+    return n_mb / dpx->world * mbs;
+  }
   int* row_owner = nullptr;  // [K] rank owning scheduled row k (partition mapping, partition.py)
   // Exchange stream and chunks: G3 / G8 run per sample chunk [c*B/C, (c+1)*B/C)
   // and each chunk's all-reduce runs on xst while the next chunk computes;
@@ -468,6 +512,7 @@ struct Engine {
     const size_t K = (size_t)D.K();
     bwd_dev = dalloc<double>(K * Bm, owned);
     fwd_dev = dalloc<double>(K * Bm, owned);
+    Nmax = (int)Bm;
     cf_dev = dalloc<int32_t>(K, owned);
     cb_dev = dalloc<int32_t>(K, owned);
     capf_dev = dalloc<int32_t>(K, owned);
@@ -607,6 +652,7 @@ struct Engine {
   // attach_lora (model.cpp:165-195) with the caller's initial adapters
   void attach_lora(int rank, double scaling, const double* init) {
     D2FT_REQUIRE(!lora_rank, kState, "lora adapters already attached");
+    D2FT_REQUIRE(!data_parallel(), kState, "lora: not available on a data-parallel engine");
     D2FT_REQUIRE(rank >= 1, kConfig, "lora rank must be >= 1");
     const int cap = std::min(D.d, D.dh);
     D2FT_REQUIRE(rank <= cap, kConfig,
@@ -807,9 +853,10 @@ struct Engine {
     mark(PH_HEAD);
     D2FT_CUDA(cudaMemsetAsync(gmax, 0, sizeof(float), st));
     launch_head(D, x + L * xs, labels_dev, P + seg[S_WC].off, P + seg[S_BC].off,
-                sm ? 1.0f / (float)sm->mbs : 1.0f / (float)D.B, loss_s, pooled,
+                sm ? 1.0f / (float)sm->mbs : 1.0f / (float)(data_parallel() ? B_glob : D.B), loss_s, pooled,
                 dlog, dX, gmax, logits_dev, st);
-    launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st);
+    launch_head_reduce(D, loss_s, pooled, dlog, G + seg[S_WC].off, G + seg[S_BC].off, loss, st,
+                       data_parallel() ? B_glob : 0);
     mark(PH_LN_BWD);
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
@@ -821,7 +868,7 @@ struct Engine {
     // training step with both weight-gradient GEMMs on the side stream: each
     // block's weight SGD follows its G7 there (after G8, the block's last
     // reader of the fp16 operands), overlapping the lower blocks' backward
-    sgd_layer = step_train && side && side_g7 && !sm && !lora_rank && !sgd_fused;
+    sgd_layer = step_train && side && side_g7 && !sm && !lora_rank && !sgd_fused && !data_parallel();
     auto g5 = [&](int l, cudaStream_t s5) {
       launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, D2FT_G5_EPI, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
@@ -1023,13 +1070,18 @@ struct Engine {
   }
   // forward/backward + SGD of one training step (the trainer's batch body)
   void train_body(float lr, float mom) {
-    sgd_fuse_req = kFuseSgd;
+    sgd_fuse_req = kFuseSgd && !data_parallel();
     step_train = true;
     sgd_lr = lr;
     sgd_mom = mom;
     run_forward_backward();
     sgd_fuse_req = false;
     step_train = false;
+    if (data_parallel()) {  // the global batch's gradient: sum of every rank's (already 1/B_glob-weighted) share
+      if (side_pending) join_side();
+      mark(PH_EXCH);
+      dpx->allreduce_sum(G, nparam, st);
+    }
     run_sgd(lr, mom);
     if (side_pending) join_side();
     sgd_fused = false;
@@ -1051,7 +1103,7 @@ struct Engine {
 
   void run_sgd(float lr, float mom) {
     mark(PH_SGD);
-    const int* fc = lists.full_cnt;
+    const int* fc = data_parallel() ? full_cnt_glob : lists.full_cnt;
     if (lora_rank) {  // adapters of subnets with Full cells, then W_eff for the next step
       const long long per = (long long)lora_per();
       launch_sgd(LA, LV, LG, nullptr, lora_count(), (long long)D.H * per, per, D.H, fc, lr, mom, err, st);
@@ -1094,9 +1146,9 @@ struct Engine {
     // shared memory, decision-bit buffer): capture again
     drop_graph();
     bool in_smem = true;
-    knapsack_smem_bytes(D.Bmax, max_cols, &in_smem);
+    knapsack_smem_bytes(Nmax, max_cols, &in_smem);
     if (!in_smem) {
-      const size_t w = knapsack_global_bits_words(D.K(), D.Bmax, max_cols);
+      const size_t w = knapsack_global_bits_words(D.K(), Nmax, max_cols);
       if (w > sched_bits_words) {
         D2FT_CUDA(cudaStreamSynchronize(st));
         void* p = nullptr;
@@ -1118,8 +1170,18 @@ struct Engine {
     ws.err_flag = err;
     launch_knapsack_schedule(bwd_dev, fwd_dev, cf_dev, cb_dev, capf_dev, capo_dev, D.K(), n_mb, D.H, sched_max_cols,
                              codes_mb, nullptr, ws, true, st);
-    launch_expand_codes(codes_mb, D.K(), n_mb, mbs, D.B, D.Bmax, codes_exp, st);
+    expand_and_plan(n_mb, mbs);
+  }
+  // codes_mb (K x n_mb, the whole batch) -> this rank's per-sample codes,
+  // compaction, plan; data parallel: the global Full counts and zeroed
+  // gradient rows this rank does not touch (their all-reduce input)
+  void expand_and_plan(int n_mb, int mbs) {
+    launch_expand_codes(codes_mb, D.K(), n_mb, mbs, D.B, D.Bmax, codes_exp, st, dp_mb0);
     compact_and_plan();
+    if (data_parallel()) {
+      launch_row_full_count(codes_mb, D.K(), n_mb, full_cnt_glob, st);
+      launch_zero_untouched(D, lists.full_cnt, G, seg[S_W1T].off, seg[S_B1].off, seg[S_W2T].off, seg[S_B2].off, st);
+    }
   }
 
   // One D2FT batch from host buffers (pinned for full-speed DMA): H2D of the
@@ -1128,7 +1190,7 @@ struct Engine {
                  const int32_t* cf, const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int n_mb,
                  int mbs, double lr, double momentum, const float* samples_next = nullptr) {
     const int K = D.K();
-    const int B = n_mb * mbs;
+    const int B = local_B(n_mb, mbs);
     begin_step(B);
     const size_t KN = (size_t)K * n_mb;
     // the small H2D copies go first: the host->device copy engine serves
@@ -1195,7 +1257,7 @@ struct Engine {
 
   // schedule + forward/backward + SGD on the staged device inputs (after begin_step)
   void compute_step(int n_mb, int mbs, double lr, double momentum) {
-    if (profiling || (partitioned() && !ex->capturable()) || !use_graphs) {
+    if (profiling || (partitioned() && !ex->capturable()) || (data_parallel() && !dpx->capturable()) || !use_graphs) {
       schedule_device(n_mb, mbs);
       train_body((float)lr, (float)momentum);
       return;
@@ -1207,14 +1269,15 @@ struct Engine {
       }
       cudaGraph_t g = nullptr;
       const unsigned long long n0 = d2ft_b200::launch_count();
-      const unsigned long long xc0 = ex ? ex->calls : 0, xb0 = ex ? ex->bytes : 0;
+      Exchange* xx = ex ? ex.get() : dpx.get();  // the engine's collective (partition or data parallel)
+      const unsigned long long xc0 = xx ? xx->calls : 0, xb0 = xx ? xx->bytes : 0;
       D2FT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       schedule_device(n_mb, mbs);
       train_body((float)lr, (float)momentum);
       D2FT_CUDA(cudaStreamEndCapture(st, &g));
       g_kernels = d2ft_b200::launch_count() - n0;
-      g_xcalls = ex ? ex->calls - xc0 : 0;
-      g_xbytes = ex ? ex->bytes - xb0 : 0;
+      g_xcalls = xx ? xx->calls - xc0 : 0;
+      g_xbytes = xx ? xx->bytes - xb0 : 0;
       if (use_pdl) make_edges_programmatic(g);
       D2FT_CUDA(cudaGraphInstantiate(&gexec, g, 0));
       D2FT_CUDA(cudaGraphDestroy(g));
@@ -1224,9 +1287,9 @@ struct Engine {
       g_mom = (float)momentum;
     } else {
       d2ft_b200::add_launches(g_kernels);
-      if (ex) {  // the replay issues the captured all-reduces again
-        ex->calls += g_xcalls;
-        ex->bytes += g_xbytes;
+      if (Exchange* xx = ex ? ex.get() : dpx.get()) {  // the replay issues the captured all-reduces again
+        xx->calls += g_xcalls;
+        xx->bytes += g_xbytes;
       }
     }
     D2FT_CUDA(cudaGraphLaunch(gexec, st));
@@ -1419,6 +1482,7 @@ int d2ft_engine_partition_nccl(d2ft_engine* h, int rank, int world, const uint8_
     D2FT_REQUIRE(h && h->e && id, kInput, "partition: null argument");
     D2FT_REQUIRE(world >= 1 && rank >= 0 && rank < world, kConfig, "partition: rank out of range");
     Engine& E = *h->e;
+    D2FT_REQUIRE(!E.data_parallel(), kState, "partition: the engine is data parallel");
     D2FT_CUDA(cudaStreamSynchronize(E.st));
     E.ex = make_nccl_exchange(rank, world, id);
     E.on_partition();
@@ -1456,9 +1520,37 @@ int d2ft_engine_partition_local(d2ft_engine* h, d2ft_local_group* g, int rank) {
   return guarded([&] {
     D2FT_REQUIRE(h && h->e && g, kInput, "partition: null argument");
     Engine& E = *h->e;
+    D2FT_REQUIRE(!E.data_parallel(), kState, "partition: the engine is data parallel");
     D2FT_CUDA(cudaStreamSynchronize(E.st));
     E.ex = make_local_exchange(g->g, rank);
     E.on_partition();
+  });
+}
+
+namespace {
+void join_data_parallel(Engine& E, std::unique_ptr<Exchange> x) {
+  D2FT_REQUIRE(!E.partitioned() && !E.data_parallel(), kState, "data parallel: the engine already joined a group");
+  D2FT_REQUIRE(!E.lora_rank, kState, "data parallel: not available with LoRA adapters attached");
+  D2FT_CUDA(cudaStreamSynchronize(E.st));
+  E.drop_graph();
+  if (!E.full_cnt_glob) E.full_cnt_glob = dalloc<int>(E.D.K(), E.owned);
+  E.size_tables(x->world * E.D.Bmax);  // the global batch's table: up to world x Bmax micro-batches
+  E.dpx = std::move(x);
+}
+}  // namespace
+
+int d2ft_engine_data_parallel_nccl(d2ft_engine* h, int rank, int world, const uint8_t* id) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && id, kInput, "data parallel: null argument");
+    D2FT_REQUIRE(world >= 1 && rank >= 0 && rank < world, kConfig, "data parallel: rank out of range");
+    join_data_parallel(*h->e, make_nccl_exchange(rank, world, id));
+  });
+}
+
+int d2ft_engine_data_parallel_local(d2ft_engine* h, d2ft_local_group* g, int rank) {
+  return guarded([&] {
+    D2FT_REQUIRE(h && h->e && g, kInput, "data parallel: null argument");
+    join_data_parallel(*h->e, make_local_exchange(g->g, rank));
   });
 }
 
@@ -1535,8 +1627,7 @@ int d2ft_engine_step_codes(d2ft_engine* h, const float* samples, const int32_t* 
                            int n_mb, int mbs, double lr, double momentum, double* loss_out) {
   return guarded([&] {
     Engine& E = *h->e;
-    D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
-    const int B = n_mb * mbs;
+    const int B = E.local_B(n_mb, mbs);  // data parallel: n_mb and codes cover the global batch
     for (size_t c = 0; c < (size_t)E.D.K() * n_mb; ++c)
       D2FT_REQUIRE(codes[c] >= 1 && codes[c] <= 3, kInput, "schedule table: code out of range");
     validate_labels(labels, B, E.D.C);
@@ -1544,8 +1635,7 @@ int d2ft_engine_step_codes(d2ft_engine* h, const float* samples, const int32_t* 
     D2FT_CUDA(cudaMemcpyAsync(E.samples_dev, samples, (size_t)B * E.D.T * E.D.d * 4, cudaMemcpyHostToDevice, E.st));
     D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, labels, B * 4, cudaMemcpyHostToDevice, E.st));
     D2FT_CUDA(cudaMemcpyAsync(E.codes_mb, codes, (size_t)E.D.K() * n_mb, cudaMemcpyHostToDevice, E.st));
-    launch_expand_codes(E.codes_mb, E.D.K(), n_mb, mbs, B, E.D.Bmax, E.codes_exp, E.st);
-    E.compact_and_plan();
+    E.expand_and_plan(n_mb, mbs);
     E.train_body((float)lr, (float)momentum);
     check_status(E.finish_and_check());
     *loss_out = *E.h_loss;
@@ -1561,7 +1651,7 @@ int d2ft_engine_step(d2ft_engine* h, const float* samples, const int32_t* labels
     const int K = E.D.K();
     D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
-    validate_labels(labels, n_mb * mbs, E.D.C);
+    validate_labels(labels, E.local_B(n_mb, mbs), E.D.C);
     E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
     E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
     check_status(E.finish_and_check());
@@ -1586,7 +1676,7 @@ int d2ft_engine_step_pipelined(d2ft_engine* h, const float* samples_next, const 
     const int K = E.D.K();
     D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
-    validate_labels(labels, n_mb * mbs, E.D.C);
+    validate_labels(labels, E.local_B(n_mb, mbs), E.D.C);
     E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
     E.host_step(nullptr, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum,
                 samples_next);
@@ -1639,6 +1729,7 @@ namespace {
 // the units of one batch: in range, the dataset matches the engine
 void validate_units(const Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs) {
   D2FT_REQUIRE(ds && units, kInput, "step_units: null argument");
+  D2FT_REQUIRE(!E.data_parallel(), kState, "step_units: not available on a data-parallel engine");
   D2FT_REQUIRE(n_mb >= 1 && mbs >= 1, kConfig, "train: batch_size must be a positive multiple of micro_batch_size");
   D2FT_REQUIRE(ds->T == E.D.T && ds->d == E.D.d, kInput, "train sample: shape does not match the model");
   const int total = (int)ds->samples.size() / mbs;
@@ -1785,12 +1876,12 @@ int d2ft_engine_bench_e2e(d2ft_engine* h, const float* samples, const int32_t* l
     Engine& E = *h->e;
     const int K = E.D.K();
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
-    validate_labels(labels, n_mb * mbs, E.D.C);
+    validate_labels(labels, E.local_B(n_mb, mbs), E.D.C);
     E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
     // Every step copies its own samples H2D; the copy of batch i+1 runs on the
     // copy stream while batch i computes (the data-loader pipeline of
     // d2ft_engine_prefetch + d2ft_engine_step(samples = NULL, samples_next)).
-    const int B = n_mb * mbs;
+    const int B = E.local_B(n_mb, mbs);
     for (int i = 0; i < warmup; ++i) {
       E.host_step(samples, labels, bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
       check_status(E.finish_and_check());
@@ -1846,7 +1937,7 @@ int d2ft_engine_bench_device(d2ft_engine* h, int n_mb, int mbs, double lr, doubl
   return guarded([&] {
     Engine& E = *h->e;
     for (int i = 0; i < warmup; ++i) {
-      E.begin_step(n_mb * mbs);
+      E.begin_step(E.local_B(n_mb, mbs));
       E.compute_step(n_mb, mbs, lr, momentum);
     }
     check_status(E.finish_and_check());
@@ -1855,7 +1946,7 @@ int d2ft_engine_bench_device(d2ft_engine* h, int n_mb, int mbs, double lr, doubl
     D2FT_CUDA(cudaEventCreate(&e1));
     D2FT_CUDA(cudaEventRecord(e0, E.st));
     for (int i = 0; i < steps; ++i) {
-      E.begin_step(n_mb * mbs);
+      E.begin_step(E.local_B(n_mb, mbs));
       E.compute_step(n_mb, mbs, lr, momentum);
     }
     D2FT_CUDA(cudaEventRecord(e1, E.st));
@@ -1876,7 +1967,7 @@ int d2ft_engine_stage_device(d2ft_engine* h, const float* samples, const int32_t
   return guarded([&] {
     Engine& E = *h->e;
     const int K = E.D.K();
-    const int B = n_mb * mbs;
+    const int B = E.local_B(n_mb, mbs);
     D2FT_REQUIRE(B >= 1 && B <= E.D.Bmax, kSize, "stage: batch exceeds the engine capacity");
     validate_sched_inputs(bwd_scores, fwd_scores, cf, cb, cap_full, cap_fwd, K, n_mb);
     validate_labels(labels, B, E.D.C);
@@ -1897,7 +1988,7 @@ int d2ft_engine_stage_device(d2ft_engine* h, const float* samples, const int32_t
 int d2ft_engine_step_resident(d2ft_engine* h, int n_mb, int mbs, double lr, double momentum) {
   return guarded([&] {
     Engine& E = *h->e;
-    E.begin_step(n_mb * mbs);
+    E.begin_step(E.local_B(n_mb, mbs));
     E.compute_step(n_mb, mbs, lr, momentum);
   });
 }
@@ -1934,8 +2025,9 @@ int d2ft_engine_exchange_stats(d2ft_engine* h, unsigned long long* calls, unsign
   return guarded([&] {
     D2FT_REQUIRE(h && h->e && calls && bytes, kInput, "exchange_stats: null argument");
     D2FT_CUDA(cudaStreamSynchronize(h->e->st));
-    *calls = h->e->ex ? h->e->ex->calls : 0;
-    *bytes = h->e->ex ? h->e->ex->bytes : 0;
+    const Exchange* xx = h->e->ex ? h->e->ex.get() : h->e->dpx.get();
+    *calls = xx ? xx->calls : 0;
+    *bytes = xx ? xx->bytes : 0;
   });
 }
 

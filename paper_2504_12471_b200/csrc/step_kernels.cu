@@ -15,13 +15,49 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ------------------------------------------------------------------ codes / plan
-__global__ void expand_codes_kernel(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out) {
+__global__ void expand_codes_kernel(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
+                                    int mb0) {
   D2FT_PDL_ENTRY();
   const size_t n = (size_t)K * Bmax;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / Bmax), s = (int)(i % Bmax);
-    out[i] = s < B ? codes[(size_t)k * n_mb + s / mbs] : (uint8_t)3;
+    out[i] = s < B ? codes[(size_t)k * n_mb + mb0 + s / mbs] : (uint8_t)3;
   }
+}
+
+// data parallel: Full cells per row over the whole batch's table (K x n_mb)
+__global__ void row_full_count_kernel(const uint8_t* codes, int n_mb, int* out) {
+  const int k = blockIdx.x;
+  int c = 0;
+  for (int i = threadIdx.x; i < n_mb; i += blockDim.x) c += codes[(size_t)k * n_mb + i] == 1;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ int part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    out[k] = t;
+  }
+}
+
+// data parallel: a head-subnet with no Full cell among THIS rank's samples
+// gets no gradient writes from this rank's GEMMs (its rows keep old values);
+// zero them so the all-reduce sums only real contributions.  Row k = (l, h):
+// [Wq|Wk|Wv|W1]^T rows (contiguous), b1 slice, [Wo;W2]^T columns h*PO.. of
+// every output row (strided), b2 slice.
+__global__ void zero_untouched_kernel(Dims D, const int* full_cnt, float* G, size_t o_w1, size_t o_b1, size_t o_w2,
+                                      size_t o_b2) {
+  const int k = blockIdx.x;
+  if (full_cnt[k] != 0) return;
+  const int l = k / D.H, h = k % D.H;
+  float* w1 = G + o_w1 + (size_t)k * D.PQ * D.d;
+  for (size_t i = threadIdx.x; i < (size_t)D.PQ * D.d; i += blockDim.x) w1[i] = 0.f;
+  for (int i = threadIdx.x; i < D.fs; i += blockDim.x) G[o_b1 + (size_t)k * D.fs + i] = 0.f;
+  float* w2 = G + o_w2 + (size_t)l * D.d * D.H * D.PO + (size_t)h * D.PO;
+  for (size_t i = threadIdx.x; i < (size_t)D.d * D.PO; i += blockDim.x)
+    w2[(i / D.PO) * D.H * D.PO + i % D.PO] = 0.f;
+  for (int i = threadIdx.x; i < D.d / D.H; i += blockDim.x) G[o_b2 + (size_t)l * D.d + h * (D.d / D.H) + i] = 0.f;
 }
 
 // rank of v[i] in decreasing order, ties by index (a stable counting rank)
@@ -421,7 +457,7 @@ __global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, cons
 // warp per output: lanes split the samples (fixed order: lane partials, then
 // a shuffle tree), so the B-long reductions run 32-wide
 __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
-                                   float* dbc, double* loss) {
+                                   float* dbc, double* loss, int loss_div) {
   D2FT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -440,7 +476,7 @@ __global__ void head_reduce_kernel(Dims D, const double* loss_s, const float* po
   } else if (i == D.d * D.C + D.C && lane == 0) {
     double a = 0.0;
     for (int s = 0; s < D.B; ++s) a += loss_s[s];
-    *loss = a / D.B;
+    *loss = a / loss_div;  // batch loss = sum of CE / B (this rank's share under data parallelism)
   }
 }
 
@@ -970,8 +1006,21 @@ int grid_for(size_t n, int threads) {
 }  // namespace
 
 void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
-                         cudaStream_t st) {
-  expand_codes_kernel<<<grid_for((size_t)K * Bmax, 256), 256, 0, st>>>(codes, K, n_mb, mbs, B, Bmax, out);
+                         cudaStream_t st, int mb0) {
+  expand_codes_kernel<<<grid_for((size_t)K * Bmax, 256), 256, 0, st>>>(codes, K, n_mb, mbs, B, Bmax, out, mb0);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_row_full_count(const uint8_t* codes, int K, int n_mb, int* out, cudaStream_t st) {
+  row_full_count_kernel<<<K, 128, 0, st>>>(codes, n_mb, out);
+  count_launch();
+  D2FT_CUDA(cudaGetLastError());
+}
+
+void launch_zero_untouched(const Dims& D, const int* full_cnt, float* G, size_t o_w1, size_t o_b1, size_t o_w2,
+                           size_t o_b2, cudaStream_t st) {
+  zero_untouched_kernel<<<D.K(), 256, 0, st>>>(D, full_cnt, G, o_w1, o_b1, o_w2, o_b2);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }
@@ -1093,9 +1142,10 @@ void launch_head(const Dims& D, const float* xL, const int* labels, const float*
 }
 
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
-                        float* dbc, double* loss, cudaStream_t st) {
+                        float* dbc, double* loss, cudaStream_t st, int loss_div) {
   const int n = (D.d * D.C + D.C + 1) * 32;  // a warp per output
-  head_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, loss_s, pooled, dlog, dWc, dbc, loss);
+  head_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(D, loss_s, pooled, dlog, dWc, dbc, loss,
+                                                      loss_div > 0 ? loss_div : D.B);
   count_launch();
   D2FT_CUDA(cudaGetLastError());
 }

@@ -8,8 +8,13 @@
 namespace d2ft_b200 {
 
 // codes [K][n_mb] -> per-sample codes [K][Bmax] (sample s uses column s / mbs; s >= B -> 3)
+// codes_exp[k][s] = codes[k][mb0 + s / mbs] for the B samples (mb0: first
+// micro-batch of this data-parallel rank), 3 past B
 void launch_expand_codes(const uint8_t* codes, int K, int n_mb, int mbs, int B, int Bmax, uint8_t* out,
-                         cudaStream_t st);
+                         cudaStream_t st, int mb0 = 0);
+void launch_row_full_count(const uint8_t* codes, int K, int n_mb, int* out, cudaStream_t st);
+void launch_zero_untouched(const Dims& D, const int* full_cnt, float* G, size_t o_w1, size_t o_b1, size_t o_w2,
+                           size_t o_b2, cudaStream_t st);
 // Per-block GEMM plan of one batch: G1 / G4 tile lists over (sample, 64-row
 // unit pair) and the cost orders of the dynamically scheduled GEMMs.
 struct Plan {
@@ -50,7 +55,8 @@ bool attn_bwd_tc_fits(int TQ);
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, float* logits, cudaStream_t st);
 void launch_head_reduce(const Dims& D, const double* loss_s, const float* pooled, const float* dlog, float* dWc,
-                        float* dbc, double* loss, cudaStream_t st);
+                        float* dbc, double* loss, cudaStream_t st,
+                        int loss_div = 0);
 // dX += LN_bwd(x_l, dxn) for samples with a Full head in block l (if l >= 0), then
 // emit dC (act_t token-major) and per-tile column sums.
 // x_l (fp32) or xn_l (the stored fp16 LN output) for y; dxn (fp32) or dxn_h (fp16, gradient-scale units)

@@ -187,6 +187,7 @@ class SubnetModel:
         self.config = config
         self.max_batch = max_batch
         self.partition = None  # partition.HeadPartition once joined to a head partition
+        self.data_parallel = None  # (rank, world) once joined to a data-parallel group
         self._h = C.c_void_p()
         c = config._c()
         L = lib()
@@ -294,7 +295,7 @@ class SubnetModel:
             raise Error(2, "schedule column must have one operation per scheduled subnet")
         if len(inputs) == 0 or len(inputs) != len(labels):
             raise Error(2, "micro-batch inputs and labels must be non-empty and aligned")  # model.cpp:424
-        x, y = self._batch(inputs, labels, len(labels))
+        x, y = self._batch(inputs, labels, len(labels), global_batch=False)
         loss = C.c_double()
         check(lib().d2ft_engine_forward_backward(self._h, ptr(x), ptr(y), C.c_int(len(y)), ptr(col), C.byref(loss)))
         g = self.grads()
@@ -318,12 +319,15 @@ class SubnetModel:
                                            C.c_double(lr), C.c_double(momentum), C.byref(loss)))
         return loss.value
 
-    def _batch(self, samples, labels, B):
+    def _batch(self, samples, labels, B, global_batch=True):
         """Samples [B][T][d] fp32 and B labels of one batch (the C entry
-        points read exactly B of each)."""
+        points read exactly B of each); on a data-parallel engine a batch
+        step's B is the global batch and the caller passes this rank's slice."""
         x = np.ascontiguousarray(samples, np.float32)
         y = i32(labels)
         cfg = self.config
+        if global_batch and self.data_parallel is not None:  # this rank holds its slice of the global batch
+            B //= self.data_parallel[1]
         if y.ndim != 1 or y.size != B:
             raise Error(2, f"batch of {B} units needs {B} labels, got {y.size}")
         if x.shape != (B, cfg.seq_len, cfg.model_dim):

@@ -222,16 +222,42 @@ def exchange_stats(model) -> tuple[int, int]:
     return calls.value, nbytes.value
 
 
+# ---------------------------------------------------------------- data parallel
+def dp_slice(n_mb: int, mbs: int, rank: int, world: int) -> tuple[int, int]:
+    """Samples [lo, hi) of the global batch rank `rank` holds under data
+    parallelism: micro-batches [rank*n_mb/world, (rank+1)*n_mb/world)."""
+    if n_mb % world:
+        raise Error(1, "data parallel: the micro-batches of a batch must divide evenly over the ranks")
+    per = n_mb // world
+    return rank * per * mbs, (rank + 1) * per * mbs
+
+
+def join_nccl_dp(model, rank: int, world: int, group=None) -> None:
+    """Make `model` rank `rank` of an NCCL data-parallel group (collective
+    over the torch.distributed group): afterwards its steps take the global
+    score table and this rank's slice of the batch (`dp_slice`)."""
+    uid = share_unique_id(rank, group)
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    check(lib().d2ft_engine_data_parallel_nccl(model._h, C.c_int(rank), C.c_int(world), buf))
+    model.data_parallel = (rank, world)
+
+
 class LocalGroup:
     """`world` engines on one device forming a head partition (single-GPU test
     harness; the exchange is a fixed-order device sum).  `run(fn)` calls
     fn(rank, model) on one host thread per rank and returns the results."""
 
-    def __init__(self, models, mapping: str = "heads", chunks: int | None = None):
+    def __init__(self, models, mapping: str = "heads", chunks: int | None = None, data_parallel: bool = False):
         self.models = list(models)
         self.world = len(self.models)
         self._g = C.c_void_p()
         check(lib().d2ft_local_group_create(C.c_int(self.world), C.byref(self._g)))
+        if data_parallel:  # engines of one data-parallel group (gradient all-reduce)
+            for r, m in enumerate(self.models):
+                check(lib().d2ft_engine_data_parallel_local(m._h, self._g, C.c_int(r)))
+                m.data_parallel = (r, self.world)
+            self.partition = None
+            return
         for r, m in enumerate(self.models):
             check(lib().d2ft_engine_partition_local(m._h, self._g, C.c_int(r)))
             _apply_mapping(m, HeadPartition(m.config.heads_per_block, r, self.world, mapping,
