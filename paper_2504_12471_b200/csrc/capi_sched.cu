@@ -36,7 +36,11 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   void upload(const T* h, size_t count) {
-    if (count) D2FT_CUDA(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    if (!count) return;
+    D2FT_CUDA(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    // from pageable memory cudaMemcpy returns once the bytes are staged, not
+    // landed; the kernels run on non-blocking streams, so wait for the DMA
+    D2FT_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   }
   void download(T* h, size_t count) const {
     if (count) D2FT_CUDA(cudaMemcpy(h, p, count * sizeof(T), cudaMemcpyDeviceToHost));

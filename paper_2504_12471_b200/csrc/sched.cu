@@ -78,7 +78,7 @@ __device__ void backtrack_row(const uint32_t* bits, int words, int N, int wt, in
     const int i0 = i1 > 32 ? i1 - 32 : 0;
     const int n = (i1 - i0) * words;
     const uint32_t* src = bits + (size_t)i0 * words;
-    for (int q = lane; q < n; q += 32) stage[q] = __ldcg(src + q);
+    for (int q = lane; q < n; q += 32) stage[q] = src[q];
     __syncwarp();
     if (lane == 0) {
       for (int i = i1; i > i0; --i) {
@@ -141,6 +141,7 @@ __device__ void dp_row_warp(const double* s_scores, int N, int wt, int cap, int 
 #pragma unroll
     for (int j = 0; j < CW; ++j)
       if (32 * j + lane == Mp) *s_obj = v[j];
+    __threadfence_block();  // every lane's decision words (shared or global) before lane 0 reads them
     __syncwarp();
     backtrack_row(bits, CW, N, wt, cap, sel, stage, BitOfWords{});
   }
@@ -280,6 +281,7 @@ __device__ void dp_row_lane(const double* s_scores, int N, int wt, int cap, int 
 #pragma unroll
     for (int j = 0; j < CL; ++j)
       if (lane * CL + j == Mp) *s_obj = v[j];
+    __threadfence_block();  // every lane's decision words (shared or global) before lane 0 reads them
     __syncwarp();
     backtrack_row(bits, kWords, N, wt, cap, sel, stage, BitOfLane<CL>{});
   }
