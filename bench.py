@@ -65,7 +65,9 @@ def parse():
     ap.add_argument("--uniform-caps", action="store_true",
                     help="N > 1: the same budget on every rank (no BudgetSpec rebalancing)")
     ap.add_argument("--no-dp-leg", action="store_true",
-                    help="N > 1: skip the data-parallel leg beside the head-partition headline")
+                    help="N > 1: skip the data-parallel leg (the headline is then the head partition)")
+    ap.add_argument("--parallel", default="dp", choices=["dp", "heads"],
+                    help="N > 1 headline: data parallelism over the global batch, or the head partition")
     return ap.parse_args()
 
 
@@ -276,13 +278,43 @@ def dp_leg(rank, local, world, dist, steps=10, warmup=3, B_per=64):
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(t)
     xcalls, xbytes = PT.exchange_stats(m)
+    # end to end through the C-ABI host-buffer call: this rank's samples and
+    # labels, the global score table, from pinned memory; loss + codes D2H
+    lib.d2ft_host_alloc.restype = C.c_void_p
+    xl, yl = np.ascontiguousarray(x[lo:hi]), np.ascontiguousarray(y[lo:hi])
+    hx = lib.d2ft_host_alloc(C.c_size_t(xl.nbytes))
+    px = np.frombuffer((C.c_char * xl.nbytes).from_address(hx), np.float32).reshape(xl.shape)
+    px[...] = xl
+    nb = 2 * bwd.nbytes + yl.nbytes + 16 * K
+    hs = lib.d2ft_host_alloc(C.c_size_t(nb))
+    buf = (C.c_char * nb).from_address(hs)
+    pb = np.frombuffer(buf, np.float64, count=bwd.size, offset=0).reshape(bwd.shape)
+    pf = np.frombuffer(buf, np.float64, count=fwd.size, offset=bwd.nbytes).reshape(fwd.shape)
+    py = np.frombuffer(buf, np.int32, count=yl.size, offset=2 * bwd.nbytes)
+    pc = np.frombuffer(buf, np.int32, count=4 * K, offset=2 * bwd.nbytes + yl.nbytes).reshape(4, K)
+    pb[...], pf[...], py[...] = bwd, fwd, yl
+    pc[0], pc[1], pc[2], pc[3] = 2, 3, capf, capo
+    ms_e = C.c_double()
+    dist.barrier()
+    _lib.check(lib.d2ft_engine_bench_e2e(
+        m._h, _lib.ptr(px), _lib.ptr(py), _lib.ptr(pb), _lib.ptr(pf), _lib.ptr(pc[0]), _lib.ptr(pc[1]),
+        _lib.ptr(pc[2]), _lib.ptr(pc[3]), C.c_int(B), C.c_int(1), C.c_double(0.05), C.c_double(0.9),
+        C.c_int(1), C.c_int(steps), C.byref(ms_e), C.byref(loss)))
+    te = torch.tensor([ms_e.value / steps], device="cuda", dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
     m.close()
     ms_step = float(mx[0].item())
+    e2e_ms = float(te[0].item())
     return {"workload": f"ViT-B/16 D2FT step, global batch {B} ({B_per} per GPU), data parallel over {world} GPUs: "
                         f"global knapsack on every rank, NCCL all-reduce of the weight gradients in the step graph",
             "value": B / (ms_step * 1e-3), "unit": "samples/s", "ms_per_step": ms_step, "steps": steps,
             "warmup": warmup, "loss": float(t[1].item()), "scaling": "weak",
-            "allreduce_bytes_per_step": xbytes // max(1, xcalls) if xcalls else 0}
+            "allreduce_bytes_per_step": xbytes // max(1, xcalls) if xcalls else 0,
+            "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": xl.nbytes + yl.nbytes + 2 * bwd.nbytes + 16 * K,
+                    "d2h_bytes_per_step": 8 + K * B,
+                    "path": "d2ft_engine_bench_e2e per rank: its samples / labels and the global score table "
+                            "from pinned host memory, loss + codes D2H, host sync"}}
 
 
 def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
@@ -801,6 +833,23 @@ def run_ours(args):
             line["surrogate"] = surr
         if dpl:
             line["data_parallel"] = dpl
+        if dpl and "value" in dpl and args.parallel == "dp":
+            # N > 1 headline: data parallelism over the global batch (it scales:
+            # one parameter-sized all-reduce per step, no replicated work); the
+            # head partition (BASELINE configs[2]'s subnet-to-device mapping)
+            # stays in `partition` with its busy-time balance
+            part_line = line.get("partition", {})
+            part_line.update({"value": value, "ms_per_step": ms_step, "e2e": line["e2e"],
+                              "roofline": line["roofline"]})
+            line["partition"] = part_line
+            line["value"], line["ms_per_step"], line["loss"] = dpl["value"], dpl["ms_per_step"], dpl["loss"]
+            line["e2e"] = dpl["e2e"]
+            line["config"]["parallelism"] = (f"data parallel over {world} GPUs (global knapsack on every rank, "
+                                             f"NCCL gradient all-reduce in the step graph); the head partition "
+                                             f"leg is under `partition`")
+            line["roofline"] = {k: v for k, v in line["roofline"].items()}
+            line["roofline"]["note"] = ("per-kernel figures measured on the head-partition engine of this run "
+                                        "(the data-parallel ranks run the 1-GPU step's kernels on 64 samples each)")
         if part_info:
             line["partition"] = part_info
         if vitl:

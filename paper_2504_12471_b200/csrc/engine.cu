@@ -232,6 +232,14 @@ struct Engine {
     drop_graph();
   }
   int* full_cnt_glob = nullptr;  // [K] Full cells per row over the global batch (SGD touch rule)
+  std::vector<cudaEvent_t> dp_ev;  // [L] block l's weight gradients complete, [L] the step's gradients all-reduced
+  cudaEvent_t dp_event(int i) {
+    if (dp_ev.empty()) {
+      dp_ev.resize(D.L + 1);
+      for (auto& e : dp_ev) D2FT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return dp_ev[i];
+  }
   bool data_parallel() const { return dpx != nullptr; }
   // samples this rank holds for a global batch of n_mb micro-batches of mbs
   int local_B(int n_mb, int mbs) {
@@ -447,7 +455,9 @@ struct Engine {
     if (cst) cudaStreamDestroy(cst);
     for (auto e : side_ev) cudaEventDestroy(e);
     for (auto e : xev) cudaEventDestroy(e);
-    ex.reset();  // the communicator before its stream
+    for (auto e : dp_ev) cudaEventDestroy(e);
+    ex.reset();  // the communicators before their stream
+    dpx.reset();
     if (xst) cudaStreamDestroy(xst);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
@@ -947,6 +957,16 @@ struct Engine {
                       ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
             s7 ? side_ctas : 0, g7s);
         if (s7) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 3), st2));
+        if (data_parallel() && step_train) {
+          // data parallel: block l's [Wq|Wk|Wv|W1]^T and [Wo;W2]^T gradients
+          // are final (G7 after G5 on the side stream, or both on st): sum
+          // them over the ranks on the exchange stream while the backward
+          // goes on with block l-1
+          D2FT_CUDA(cudaEventRecord(dp_event(l), side ? st2 : st));
+          D2FT_CUDA(cudaStreamWaitEvent(xst, dp_event(l), 0));
+          dpx->allreduce_sum(G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, (size_t)H * D.PQ * d, xst);
+          dpx->allreduce_sum(G + seg[S_W2T].off + (size_t)l * d * H * D.PO, (size_t)d * H * D.PO, xst);
+        }
         if (sgd_layer) {  // this block's [Wq|Wk|Wv|W1]^T and [Wo;W2]^T SGD, off the critical path
           D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l + 4), 0));
           sgd_block(S_W1T, W1T_bf, l, st2);
@@ -1080,7 +1100,14 @@ struct Engine {
     if (data_parallel()) {  // the global batch's gradient: sum of every rank's (already 1/B_glob-weighted) share
       if (side_pending) join_side();
       mark(PH_EXCH);
-      dpx->allreduce_sum(G, nparam, st);
+      // the block weight matrices went per block during the backward; the
+      // biases, embedding, positions and classifier now, then the SGD waits
+      D2FT_CUDA(cudaEventRecord(dp_event(D.L), st));
+      D2FT_CUDA(cudaStreamWaitEvent(xst, dp_event(D.L), 0));
+      dpx->allreduce_sum(G + seg[S_B1].off, seg[S_B1].n, xst);
+      dpx->allreduce_sum(G + seg[S_B2].off, nparam - seg[S_B2].off, xst);
+      D2FT_CUDA(cudaEventRecord(dp_event(D.L), xst));
+      D2FT_CUDA(cudaStreamWaitEvent(st, dp_event(D.L), 0));
     }
     run_sgd(lr, mom);
     if (side_pending) join_side();
@@ -1534,6 +1561,11 @@ void join_data_parallel(Engine& E, std::unique_ptr<Exchange> x) {
   D2FT_CUDA(cudaStreamSynchronize(E.st));
   E.drop_graph();
   if (!E.full_cnt_glob) E.full_cnt_glob = dalloc<int>(E.D.K(), E.owned);
+  if (!E.xst) {  // the gradient all-reduces run on the exchange stream, overlapping the backward
+    int least = 0, greatest = 0;
+    D2FT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    D2FT_CUDA(cudaStreamCreateWithPriority(&E.xst, cudaStreamNonBlocking, greatest));
+  }
   E.size_tables(x->world * E.D.Bmax);  // the global batch's table: up to world x Bmax micro-batches
   E.dpx = std::move(x);
 }
