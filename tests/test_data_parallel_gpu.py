@@ -71,6 +71,9 @@ def test_local_data_parallel_d2ft_step(cfg, world, mbs):
             assert np.array_equal(q, ps[0])  # one all-reduced gradient, one SGD: identical on every rank
         assert np.array_equal(g.models[0].velocity(), g.models[-1].velocity())
         p32 = p.astype(np.float32).astype(np.float64)
+        bad_w = compare_tensors(whole.params() - p32, pr - p, sl, GRAD_TOL)
+        bad_d = compare_tensors(ps[0] - p32, pr - p, sl, GRAD_TOL)
+        assert not bad_w and not bad_d, ("whole vs oracle", bad_w[:4], "dp vs oracle", bad_d[:4])
         # vs one engine on the whole batch: each rank's fp16 gradient operands
         # carry its own power-of-two scale (its samples' max |dX|) and the
         # all-reduce sums in another order; the wq / wk updates amplify such
