@@ -1881,10 +1881,18 @@ int d2ft_engine_bench_e2e_units(d2ft_engine* h, const d2ft_dataset* ds, const in
     D2FT_CUDA(cudaEventRecord(e0, E.st));
     D2FT_CUDA(cudaStreamWaitEvent(E.cst, e0, 0));  // the first gather is inside the timed region
     const int32_t* ord = order + (size_t)warmup * n_mb;
+    const bool trace = getenv("D2FT_E2E_TRACE") != nullptr;  // host enqueue / sync split per step (stderr)
     for (int i = 0; i < steps; ++i) {
+      const auto h0 = std::chrono::steady_clock::now();
       units_step(E, ds, ord + (size_t)i * n_mb, n_mb, mbs, i + 1 < steps ? ord + (size_t)(i + 1) * n_mb : nullptr,
                  bwd_scores, fwd_scores, total_units, cf, cb, cap_full, cap_fwd, lr, momentum);
+      const auto h1 = std::chrono::steady_clock::now();
       check_status(E.finish_and_check());
+      const auto h2 = std::chrono::steady_clock::now();
+      if (trace)
+        fprintf(stderr, "e2e units step %d: enqueue %.3f ms, sync %.3f ms\n", i,
+                std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                std::chrono::duration<double, std::milli>(h2 - h1).count());
     }
     D2FT_CUDA(cudaEventRecord(e1, E.st));
     D2FT_CUDA(cudaEventSynchronize(e1));
