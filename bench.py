@@ -339,11 +339,20 @@ def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
     fwd, bwd = np.ascontiguousarray(u[:, :, 0]), np.ascontiguousarray(u[:, :, 1])
     nb = (2 * B) // 5
     capf, capo = np.full(K, nb * 5, np.int32), np.full(K, nb * 2, np.int32)
-    m = E.SubnetModel(cfg, B)
+    dp = bool(dist) and args is not None and args.parallel == "dp"
+    lo, hi = 0, B
+    if dp:  # data parallel over the global batch of 256: B / N samples per rank
+        from paper_2504_12471_b200 import partition as PT
+        lo, hi = PT.dp_slice(B, 1, rank, world)
+    m = E.SubnetModel(cfg, hi - lo)
     if dist:
         from paper_2504_12471_b200 import partition as PT
-        PT.join_nccl(m, PT.HeadPartition(Hq, rank, world, args.mapping, Lq), chunks=args.exchange_chunks)
-    m.stage(x, y, S.ScoreTable(K, B, fwd, bwd), S.CostModel(), S.Capacities(capf.tolist(), capo.tolist()))
+        if dp:
+            PT.join_nccl_dp(m, rank, world)
+        else:
+            PT.join_nccl(m, PT.HeadPartition(Hq, rank, world, args.mapping, Lq), chunks=args.exchange_chunks)
+    m.stage(x[lo:hi], y[lo:hi], S.ScoreTable(K, B, fwd, bwd), S.CostModel(),
+            S.Capacities(capf.tolist(), capo.tolist()))
     ms, loss = C.c_double(), C.c_double()
     if dist:
         dist.barrier()
@@ -354,21 +363,21 @@ def vitl_leg(steps=3, warmup=2, B=256, rank=0, world=1, dist=None, args=None):
         t = torch.tensor([ms.value], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = C.c_double(float(t.item()))
-    codes = np.zeros((K, B), np.uint8)
+    codes = np.zeros((K, hi - lo), np.uint8)
     _lib.check(lib.d2ft_engine_codes(m._h, _lib.ptr(codes)))
     m.close()
     full = float((codes == 1).sum())
     act = float(((codes == 1) | (codes == 2)).sum())
     Fk = 2.0 * T * (4 * Dq * dh + 2 * T * dh + 2 * Dq * fs)
+    if dist:  # this rank's rows (head partition) or samples (data parallel) only: the global table's FLOPs
+        full = float(sum(dist_sum(full, dist)))
+        act = float(sum(dist_sum(act, dist)))
     alg = 3 * Fk * full + Fk * (act - full) + 4.0 * T * Dq * Dq * B
     ms_step = ms.value / steps
     tf = alg / (ms_step * 1e-3) / 1e12
     peak = PEAKS["bf16_tflops_sustained"] * world
-    if dist:  # this rank's rows only: the global table's FLOPs
-        full = float(sum(dist_sum(full, dist)))
-        act = float(sum(dist_sum(act, dist)))
-        alg = 3 * Fk * full + Fk * (act - full) + 4.0 * T * Dq * Dq * B
-    where = f"{world} B200, head partition (NCCL)" if dist else "1 B200 (BASELINE configs[3] names 8 B200)"
+    where = ((f"{world} B200, data parallel (NCCL gradient all-reduce)" if dp else
+              f"{world} B200, head partition (NCCL)") if dist else "1 B200 (BASELINE configs[3] names 8 B200)")
     return {"workload": f"ViT-L/16 (L24 H16 d1024 ffn4096 T197, {K} head-subnets) D2FT step, batch {B}, "
                         f"per-sample schedule, {where}",
             "value": B / (ms_step * 1e-3), "unit": "samples/s", "ms_per_step": ms_step, "steps": steps,

@@ -240,6 +240,8 @@ TEST_CASE("standard policy reproduces the reference trainer") {  // test_trainer
   TrainHistory ours = b200::train(gpu_model, ds, tc);
   REQUIRE(ours.epochs.size() == ref.epochs.size());
   for (size_t e = 0; e < ref.epochs.size(); ++e) {
+    if (std::abs(ours.epochs[e].loss - ref.epochs[e].loss) > 1e-3 * std::abs(ref.epochs[e].loss))
+      std::printf("  epoch %zu: loss %.9g, reference %.9g\n", e, ours.epochs[e].loss, ref.epochs[e].loss);
     CHECK(std::abs(ours.epochs[e].loss - ref.epochs[e].loss) <= 1e-3 * std::abs(ref.epochs[e].loss));
     CHECK(ours.epochs[e].compute_fraction == 1.0);
     CHECK(ours.epochs[e].comm_fraction == 1.0);

@@ -871,6 +871,7 @@ struct Engine {
     launch_ln_bwd_prep(D, -1, lists.full_hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, dX, dC, cs_slot(L - 1),
                        gmax, st);
     const bool side = use_side && !profiling && !sm;  // LoRA: G7 only ([Wo;W2] frozen)
+    bool forked = false;  // work went to the side stream in this pass
     // SGD in the G5 / G7 epilogues (FusedSgd) when a training step follows;
     // G8 runs before G7 so the layer's fp16 W1 operand is updated after its
     // last reader; not with the side stream (G5 would overlap G4's W2 reads)
@@ -892,6 +893,7 @@ struct Engine {
       if (side && !lora_rank) {
         D2FT_CUDA(cudaEventRecord(side_event(5 * l), st));
         D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l), 0));
+        forked = true;
         g5(l, st2);
         D2FT_CUDA(cudaEventRecord(side_event(5 * l + 1), st2));
       }
@@ -949,6 +951,7 @@ struct Engine {
         cudaStream_t g7s = st;
         if (s7) {
           D2FT_CUDA(cudaStreamWaitEvent(st2, side_event(5 * l + 2), 0));  // dY1T of block l complete
+          forked = true;
           g7s = st2;
         }
         launch_gemm<G7<kG7BN>, GemmShape<kG7BN, kCG2 ? 7 : 5, 0, D2FT_G7_EPI, 2, 0, 1, kCG2>>(
@@ -989,8 +992,11 @@ struct Engine {
     // in a training step — after the remaining SGD (train_body), so the embed
     // / bias gradients and the small SGD segments overlap the side stream's
     // last G7 and block SGD (they touch none of its buffers)
-    side_pending = side;
-    if (side && (!step_train || lora_rank)) join_side();  // lora_grad reads G7's output
+    // join only a side stream that received work in this pass (LoRA with G7
+    // on the main stream forks nothing: joining an empty side stream inside
+    // a graph capture is an error)
+    side_pending = forked;
+    if (forked && (!step_train || lora_rank)) join_side();  // lora_grad reads G7's output
     if (sm) return;  // the pre-pass scores only the scheduled head-subnets
     if (lora_rank) {  // only the adapters train (model.hpp:155-172)
       mark(PH_BIAS);
@@ -1109,6 +1115,10 @@ struct Engine {
       D2FT_CUDA(cudaEventRecord(dp_event(D.L), xst));
       D2FT_CUDA(cudaStreamWaitEvent(st, dp_event(D.L), 0));
     }
+    // the remaining SGD may overlap the side stream only when the side
+    // stream already updated (and alone writes) the block weight matrices'
+    // gradients; otherwise run_sgd reads what G5 / G7 there still write
+    if (side_pending && !sgd_layer) join_side();
     run_sgd(lr, mom);
     if (side_pending) join_side();
     sgd_fused = false;
@@ -1735,14 +1745,22 @@ int d2ft_dataset_create(const double* const* samples, const int32_t* labels, int
     ds->T = seq_len;
     ds->d = token_dim;
     if (pin) {
+      // Page-lock only samples that start on a page boundary (the caller
+      // allocated them page-aligned, so the pages they touch are theirs): a
+      // registration that covers pages shared with other allocations — heap
+      // neighbours of small matrices — makes later copies of those
+      // neighbours straddle a registered range (the driver then refuses them
+      // or DMAs unlocked bytes).  Every other sample stays pageable: its copy
+      // is staged by the driver (slower, same bytes).
       const size_t bytes = (size_t)seq_len * token_dim * sizeof(double);
+      const size_t pg = 4096;
       for (int i = 0; i < num_samples; ++i) {
         void* p = const_cast<double*>(samples[i]);
-        // best effort: a sample sharing pages with an already registered
-        // range (small heap matrices) stays pageable; its copy is staged by
-        // the driver instead (slower, same bytes)
-        if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess) ds->pinned.push_back(p);
-        else cudaGetLastError();
+        if (reinterpret_cast<uintptr_t>(p) % pg) continue;
+        if (cudaHostRegister(p, (bytes + pg - 1) / pg * pg, cudaHostRegisterDefault) == cudaSuccess)
+          ds->pinned.push_back(p);
+        else
+          cudaGetLastError();
       }
     }
     *out = ds.release();

@@ -108,7 +108,9 @@ def _aligned_f64(shape) -> np.ndarray:
     vector<Matrix>; page alignment lets d2ft_dataset_create page-lock each
     sample on its own)."""
     n = int(np.prod(shape))
-    raw = np.empty(n + 512, np.float64)
+    # 8 KB of slack: the aligned start (<= 4 KB in) plus the page-rounded end
+    # the registration covers both stay inside this allocation
+    raw = np.empty(n + 1024, np.float64)
     off = (-raw.ctypes.data % 4096) // 8
     return raw[off:off + n].reshape(shape)
 

@@ -12,4 +12,7 @@ dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cu
 import bench
 r = bench.dp_leg(0, 0, 1, dist, steps=5, warmup=2, B_per=64)
 print(json.dumps(r))
+import argparse
+args = argparse.Namespace(parallel="dp", mapping="heads", exchange_chunks=2)
+print(json.dumps(bench.vitl_leg(steps=2, warmup=1, rank=0, world=1, dist=dist, args=args)))
 dist.destroy_process_group()
