@@ -11,6 +11,8 @@
 //      the same fp64 operations in the same order; columns beyond i are equal
 //      to column i, so only min(cap/wt, N)+1 columns are needed.
 // Every fp64 operation is an add (__dadd_rn) or a compare: no contraction.
+#include <type_traits>
+
 #include "common.cuh"
 #include "sched.cuh"
 
@@ -247,14 +249,15 @@ __device__ void dp_row_lane(const double* s_scores, int N, int wt, int cap, int 
       double left = __shfl_up_sync(0xffffffffu, v[CL - 1], 1);  // column l*CL - 1, before this item
       if (lane == 0) left = 0.0;
       // decision bits into 4 independent accumulators (short OR chains)
-      uint64_t acc4[4] = {0, 0, 0, 0};
+      using MaskT = std::conditional_t<(CL <= 32), uint32_t, uint64_t>;  // one decision bit per column
+      MaskT acc4[4] = {0, 0, 0, 0};
       if (wt == 0) {  // zero weight: take reads the same column (only m == 0 may take)
 #pragma unroll
         for (int j = 0; j < CL; ++j) {
           const double take = __dadd_rn(v[j], s);
           const bool d = okc[j] && (take > v[j]);
           if (d) v[j] = take;
-          acc4[j & 3] |= (uint64_t)d << j;
+          acc4[j & 3] |= (MaskT)d << j;
         }
       } else {
         // all takes from the previous item's values first, then the compares,
@@ -272,11 +275,11 @@ __device__ void dp_row_lane(const double* s_scores, int N, int wt, int cap, int 
         for (int j = 0; j < CL; ++j) d[j] = t[j] > v[j];  // scheduler.cpp:167 strict >
 #pragma unroll
         for (int j = 0; j < CL; ++j) {
-          acc4[j & 3] |= (uint64_t)d[j] << j;
+          acc4[j & 3] |= (MaskT)d[j] << j;
           v[j] = d[j] ? t[j] : v[j];
         }
       }
-      const uint64_t m = (acc4[0] | acc4[1]) | (acc4[2] | acc4[3]);
+      const MaskT m = (acc4[0] | acc4[1]) | (acc4[2] | acc4[3]);
       if constexpr (CL <= 32) bits[(size_t)i * 32 + lane] = (uint32_t)m;
       else reinterpret_cast<uint64_t*>(bits)[(size_t)i * 32 + lane] = m;
     }
