@@ -14,9 +14,20 @@ SRCS     := $(wildcard $(CSRC)/*.cu)
 OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/d2ft_b200.h
 LIB      ?= $(PKG)/libd2ft_b200.so
+# GEMM self-test hooks (include/d2ft_b200_testing.h): a separate library for
+# tests/test_gemm_gpu.py, linked against the product library
+TESTLIB  := $(PKG)/libd2ft_b200_testing.so
 
 .PHONY: all ref oracle clean
-all: $(LIB) oracle
+all: $(LIB) $(TESTLIB) oracle
+
+$(OBJDIR)/testing/%.o: $(CSRC)/testing/%.cu $(HDRS) include/d2ft_b200_testing.h
+	@mkdir -p $(OBJDIR)/testing
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/testing/$*.ptxas.log || (cat $(OBJDIR)/testing/$*.ptxas.log; exit 1)
+
+$(TESTLIB): $(OBJDIR)/testing/gemm_testing.o $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJDIR)/testing/gemm_testing.o -L$(PKG) -ld2ft_b200 -lcuda \
+	    -Xlinker -rpath -Xlinker '$$ORIGIN'
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -32,5 +43,5 @@ ref: all
 	$(MAKE) -s -j8 -C oracle ref
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(TESTLIB)
 	$(MAKE) -s -C oracle clean

@@ -20,8 +20,22 @@ def bf16(x):
     return r, back
 
 
+_TESTING = None
+
+
+def _testing():
+    """The GEMM self-test hooks live in libd2ft_b200_testing.so (not in the
+    product library); errors come back through the product's d2ft_last_error."""
+    global _TESTING
+    if _TESTING is None:
+        import os
+        _lib.lib()  # the product library first (the hooks link against it)
+        _TESTING = C.CDLL(os.path.join(os.path.dirname(_lib.LIB_PATH), "libd2ft_b200_testing.so"))
+    return _TESTING
+
+
 def _call(name, *args):
-    fn = getattr(_lib.lib(), name)
+    fn = getattr(_testing(), name)
     _lib.check(fn(*args))
 
 

@@ -10,9 +10,11 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared():
+def _declared(testing=False):
     names = set()
     for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        if h.endswith("_testing.h") != testing:
+            continue
         src = open(h).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         names |= set(re.findall(r"\b(d2ft_[a-z0-9_]+)\s*\(", src))
@@ -31,6 +33,11 @@ def test_library_exports_every_declared_symbol():
         pytest.fail("libd2ft_b200.so not built — run __graft_entry__.build()")
     lib = ctypes.CDLL(_lib.LIB_PATH)
     missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+    # the GEMM self-test hooks are NOT in the product library, but in the testing one
+    assert not any(hasattr(lib, n) for n in _declared(testing=True))
+    tlib = ctypes.CDLL(os.path.join(os.path.dirname(_lib.LIB_PATH), "libd2ft_b200_testing.so"))
+    missing = [n for n in _declared(testing=True) if not hasattr(tlib, n)]
     assert not missing, missing
 
 

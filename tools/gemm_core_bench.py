@@ -1,9 +1,11 @@
 """Dense GEMM core throughput at the step's tile shapes (CTA pairs): B
 multicast vs pair UMMA, with / without output stores, MN-major A or B."""
-import ctypes as C, os, sys
+import ctypes as C
+import os, sys
 sys.path.insert(0, os.getcwd())
 from paper_2504_12471_b200 import _lib
-lib = _lib.lib()
+_lib.lib()
+lib = C.CDLL(os.path.join(os.path.dirname(_lib.LIB_PATH), "libd2ft_b200_testing.so"))  # the GEMM self-test hooks
 names = ["multicast N208", "pair N208", "multicast N208 nostore", "pair N208 nostore", "pair A-MN N208 nostore",
          "pair B-MN N208 nostore", "pair B-MN N256 nostore", "pair B-MN N128 nostore", "multicast B-MN N208 nostore"]
 nn = [208, 208, 208, 208, 208, 208, 256, 128, 208]
