@@ -66,6 +66,7 @@ def parse():
                     help="N > 1: the same budget on every rank (no BudgetSpec rebalancing)")
     ap.add_argument("--no-dp-leg", action="store_true",
                     help="N > 1: skip the data-parallel leg (the headline is then the head partition)")
+    ap.add_argument("--force-dist", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--parallel", default="dp", choices=["dp", "heads"],
                     help="N > 1 headline: data parallelism over the global batch, or the head partition")
     return ap.parse_args()
@@ -540,11 +541,13 @@ def run_ours(args):
     lib = _lib.lib()
     _lib.check(lib.d2ft_set_device(C.c_int(local)))
     dist = None
-    if world > 1:
+    if world > 1 or args.force_dist:  # --force-dist: the N > 1 code path at world 1 (a check on a 1-GPU box)
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         dist = tdist
     # N > 1: head partition (partition.py), weak scaling: the
     # global batch grows with N so each rank's share of head-sample cells stays
