@@ -389,10 +389,24 @@ __device__ void column_lists(const uint8_t* codes, int K, int N, int H, const Co
     const int l = q / N, i = q % N;
     const int cell = i * nb + l;
     int a = 0, f = 0;
-    for (int h = 0; h < H; ++h) {
-      const uint8_t c = codes[(size_t)(l * H + h) * N + i];
-      if (c == 1 || c == 2) L.act_heads[(size_t)cell * H + a++] = h;
-      if (c == 1) L.full_heads[(size_t)cell * H + f++] = h;
+    if (H <= 16) {
+      // every head's code first: the list stores below may alias `codes` as
+      // far as the compiler knows (byte pointer), which serialised one L2
+      // round trip per head
+      uint8_t cc[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) cc[h] = h < H ? codes[(size_t)(l * H + h) * N + i] : 0;  // shared or global table
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        if (cc[h] == 1 || cc[h] == 2) L.act_heads[(size_t)cell * H + a++] = h;
+        if (cc[h] == 1) L.full_heads[(size_t)cell * H + f++] = h;
+      }
+    } else {
+      for (int h = 0; h < H; ++h) {
+        const uint8_t c = codes[(size_t)(l * H + h) * N + i];
+        if (c == 1 || c == 2) L.act_heads[(size_t)cell * H + a++] = h;
+        if (c == 1) L.full_heads[(size_t)cell * H + f++] = h;
+      }
     }
     L.act_cnt[cell] = a;
     L.full_hcnt[cell] = f;

@@ -667,6 +667,13 @@ struct EmbedW {
     if (m >= D.d) return;
     float* out = part + ((size_t)c.ks * D.d + m) * D.d;
     const int n0 = c.nt * BN + col0;
+    if (n0 + 16 <= D.d) {  // the row's 16 contiguous floats as four 16-byte stores (scalar stores: LSU-throttled)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(out + n0 + 4 * q) =
+            make_float4(v[4 * q] * r.inv, v[4 * q + 1] * r.inv, v[4 * q + 2] * r.inv, v[4 * q + 3] * r.inv);
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (n0 + i < D.d) out[n0 + i] = v[i] * r.inv;

@@ -331,7 +331,7 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 template <int NV>
-__global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, const int* labels, const float* Wc,
+__global__ void __launch_bounds__(256, 2) head_kernel(Dims D, const float* xL, const int* labels, const float* Wc,
                                                    const float* bc, float scale, double* loss_s, float* pooled_out,
                                                    float* dlog_out, float* dX, float* gmax, float* logits_out) {
   D2FT_PDL_ENTRY();
@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, cons
   float* dpooled = pooled + D.d;                 // [d]
   float* rowstat = dpooled + D.d;                // [T][2]
   __shared__ float logits[64], dlog[64];
+  __shared__ double ex[64];
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int s = blockIdx.x / kHeadCluster;
@@ -404,15 +405,23 @@ __global__ void __launch_bounds__(512) head_kernel(Dims D, const float* xL, cons
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // cross_entropy, model.cpp:400-414 (fp64 reduction)
-    const int lab = labels[s];
-    double mx = logits[0];
-    for (int c = 1; c < D.C; ++c) mx = fmax(mx, (double)logits[c]);
+  if (warp == 0) {  // cross_entropy, model.cpp:400-414 (fp64 reduction)
+    // the exps on the lanes, the sum serially in class order (lane 0)
+    double mx = -INFINITY;
+    for (int c = lane; c < D.C; c += 32) mx = fmax(mx, (double)logits[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int c = lane; c < D.C; c += 32) ex[c] = exp((double)logits[c] - mx);
+    __syncwarp();
     double sum = 0.0;
-    for (int c = 0; c < D.C; ++c) sum += exp((double)logits[c] - mx);
-    if (rank == 0) loss_s[s] = log(sum) - ((double)logits[lab] - mx);
-    for (int c = 0; c < D.C; ++c) {
-      double p = exp((double)logits[c] - mx) / sum;
+    if (lane == 0) {
+      for (int c = 0; c < D.C; ++c) sum += ex[c];
+      if (rank == 0) loss_s[s] = log(sum) - ((double)logits[labels[s]] - mx);
+    }
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    const int lab = labels[s];
+    for (int c = lane; c < D.C; c += 32) {
+      double p = ex[c] / sum;
       if (c == lab) p -= 1.0;
       dlog[c] = (float)(p * scale);
       if (rank == 0) dlog_out[(size_t)s * D.C + c] = dlog[c];
@@ -1118,7 +1127,9 @@ void launch_attn_bwd(const Dims& D, int l, const int* full_heads, const int* ful
 void launch_head(const Dims& D, const float* xL, const int* labels, const float* Wc, const float* bc, float scale,
                  double* loss_s, float* pooled, float* dlog, float* dX, float* gmax, float* logits, cudaStream_t st) {
   D2FT_REQUIRE(D.C <= 64, kConfig, "head: at most 64 classes");
-  const int threads = 512;
+  // 8 warps: two CTAs per SM (registers), so the B x 4 CTAs of ViT-B run as
+  // one wave (512-thread CTAs ran one per SM, 1.94 waves)
+  const int threads = 256;
   const size_t sm = (size_t)((threads / 32 + 3) * D.d + 2 * D.T) * 4;
   D2FT_NV_DISPATCH(D.d, {
     D2FT_CUDA(cudaFuncSetAttribute(head_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
