@@ -95,6 +95,40 @@ def test_vitb_bench_step_vs_oracle(B):
     assert not bad, bad[:8]
 
 
+def test_vitl_step_vs_oracle():
+    """BASELINE configs[3]'s model (ViT-L/16: 24 blocks x 16 heads, d = 1024,
+    ffn 4096, T = 197) through the graph path with a ragged bench-style
+    schedule (U[0,10) scores, floor(2B/5) p_f + p_o per row), batch 8, one
+    step against the oracle trainer body."""
+    cfg = E.VIT_L16
+    oc, sl = _cfgs(cfg)
+    B = 8
+    x, y, b, f, caps = _bench_inputs(cfg, B)
+    K = cfg.scheduled_subnet_count()
+    p0 = E.partition_model(cfg)
+    ref_codes = O.knapsack_schedule(b, f, 2, 3, caps.full, caps.fwd)
+    assert (ref_codes == 1).any() and (ref_codes == 2).any() and (ref_codes == 3).any()
+    pr, vr = p0.copy(), np.zeros_like(p0)
+    workers = max(1, min(B, _workers() * 2 // 7))  # ~9 GB of fp64 buffers per ViT-L worker
+    rl, _ = MO.train_batch_parallel(oc, pr, vr, x.astype(np.float64), y, ref_codes, 1, 0.05, 0.9, workers=workers)
+    m = E.SubnetModel(cfg, B)
+    loss, table = m.d2ft_step(x, y, P.ScoreTable(K, B, f, b), P.CostModel(), caps, 1, 0.05, 0.9)
+    assert np.array_equal(table.codes, ref_codes)
+    pg, vg = m.params(), m.velocity()
+    m.close()
+    assert abs(loss - rl) <= FP32_TOL * abs(rl), (loss, rl)
+    p32 = p0.astype(np.float32).astype(np.float64)
+    rep = {"loss_rel": abs(loss - rl) / abs(rl), "params_normwise": normwise(pg, pr),
+           "update": error_report(pg - p32, pr - p0, sl), "velocity": error_report(vg, vr, sl),
+           "cells": {"full": int((ref_codes == 1).sum()), "fwd": int((ref_codes == 2).sum())}}
+    write_report("vitl_step_B8", rep)
+    assert normwise(pg, pr) <= FP32_TOL
+    bad = compare_tensors(pg - p32, pr - p0, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+    bad = compare_tensors(vg, vr, sl, GRAD_TOL)
+    assert not bad, bad[:8]
+
+
 SMALL64 = E.ModelConfig(2, 2, 128, 256, 50, 4, 5)    # dh = 64 (tcgen05 attention), ragged T
 MID64 = E.ModelConfig(3, 4, 256, 1024, 197, 8, 9)    # dh = 64, T = 197 as ViT-B
 
