@@ -133,8 +133,10 @@ int d2ft_dataset_destroy(d2ft_dataset* ds);
  * as slice_scores (trainer.cpp:139-154).  The fp64 samples are gathered H2D
  * and converted on the device; units_next != NULL gathers the next batch on
  * the copy stream while this one computes (the next call must pass those
- * units).  loss_out = batch loss (trainer.cpp:254); codes_out (K x n_mb, may
- * be NULL) = the schedule. */
+ * units) and stages its labels and score slice on the host (the next call
+ * must pass the same dataset and unmodified score table; other arguments are
+ * re-checked).  loss_out = batch loss (trainer.cpp:254); codes_out (K x n_mb,
+ * may be NULL) = the schedule. */
 int d2ft_engine_step_units(d2ft_engine* e, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
                            const int32_t* units_next, const double* bwd_scores, const double* fwd_scores,
                            int total_units, const int32_t* cf, const int32_t* cb, const int32_t* cap_full,

@@ -215,15 +215,15 @@ struct Engine {
   void size_tables(int nmax) {
     D2FT_CUDA(cudaStreamSynchronize(st));
     const size_t K = (size_t)D.K();
-    for (void* q : {(void*)bwd_dev, (void*)fwd_dev, (void*)codes_mb})
+    for (void* q : {(void*)bwd_dev, (void*)codes_mb})
       if (q) {
         owned.erase(std::find(owned.begin(), owned.end(), q));
         cudaFree(q);
       }
     if (h_scores) cudaFreeHost(h_scores);
     if (h_codes) cudaFreeHost(h_codes);
-    bwd_dev = dalloc<double>(K * nmax, owned);
-    fwd_dev = dalloc<double>(K * nmax, owned);
+    bwd_dev = dalloc<double>(2 * K * nmax, owned);
+    fwd_dev = bwd_dev + K * nmax;
     codes_mb = dalloc<uint8_t>(K * nmax, owned);
     D2FT_CUDA(cudaMallocHost(&h_scores, 2 * K * nmax * sizeof(double)));
     D2FT_CUDA(cudaMallocHost(&h_codes, K * nmax));
@@ -309,6 +309,29 @@ struct Engine {
   float* h_samples = nullptr;
   int* h_labels = nullptr;
   double* h_scores = nullptr;
+  // Dataset-path staging, double-buffered: batch i+1's labels, score slice
+  // (bwd at 0, fwd at K * Nmax, as on the device) and cost / capacity rows
+  // are gathered and validated while batch i computes (units_step)
+  int* u_lab[2] = {nullptr, nullptr};
+  double* u_sc[2] = {nullptr, nullptr};
+  int32_t* u_caps[2] = {nullptr, nullptr};
+  struct UnitsPrep {
+    bool valid = false;
+    int buf = 0, n_mb = 0, mbs = 0, total_units = 0;
+    const void* ds = nullptr;
+    const double *bwd = nullptr, *fwd = nullptr;
+    std::vector<int32_t> units;
+  } prep;
+  int ubuf = 0;
+  void ensure_units_staging() {
+    if (u_lab[0]) return;
+    const size_t K = (size_t)D.K();
+    for (int b = 0; b < 2; ++b) {
+      D2FT_CUDA(cudaMallocHost(&u_lab[b], (size_t)D.Bmax * sizeof(int)));
+      D2FT_CUDA(cudaMallocHost(&u_sc[b], 2 * K * Nmax * sizeof(double)));
+      D2FT_CUDA(cudaMallocHost(&u_caps[b], 4 * K * sizeof(int32_t)));
+    }
+  }
   double* h_loss = nullptr;
   int* h_err = nullptr;
   uint8_t* h_codes = nullptr;
@@ -446,6 +469,11 @@ struct Engine {
     if (h_samples) cudaFreeHost(h_samples);
     if (h_labels) cudaFreeHost(h_labels);
     if (h_scores) cudaFreeHost(h_scores);
+    for (int b = 0; b < 2; ++b) {
+      if (u_lab[b]) cudaFreeHost(u_lab[b]);
+      if (u_sc[b]) cudaFreeHost(u_sc[b]);
+      if (u_caps[b]) cudaFreeHost(u_caps[b]);
+    }
     if (h_loss) cudaFreeHost(h_loss);
     if (h_err) cudaFreeHost(h_err);
     if (h_codes) cudaFreeHost(h_codes);
@@ -520,13 +548,15 @@ struct Engine {
     logits_dev = dalloc<float>(Bm * D.C, owned);
 
     const size_t K = (size_t)D.K();
-    bwd_dev = dalloc<double>(K * Bm, owned);
-    fwd_dev = dalloc<double>(K * Bm, owned);
+    // the two score tables and the four per-row cost / capacity vectors are
+    // one allocation each, so a staged batch reaches the device in two copies
+    bwd_dev = dalloc<double>(2 * K * Bm, owned);
+    fwd_dev = bwd_dev + K * Bm;
     Nmax = (int)Bm;
-    cf_dev = dalloc<int32_t>(K, owned);
-    cb_dev = dalloc<int32_t>(K, owned);
-    capf_dev = dalloc<int32_t>(K, owned);
-    capo_dev = dalloc<int32_t>(K, owned);
+    cf_dev = dalloc<int32_t>(4 * K, owned);
+    cb_dev = cf_dev + K;
+    capf_dev = cf_dev + 2 * K;
+    capo_dev = cf_dev + 3 * K;
     codes_mb = dalloc<uint8_t>(K * Bm, owned);
     codes_exp = dalloc<uint8_t>(K * Bm, owned);
     const size_t cells = Bm * L;
@@ -1787,29 +1817,89 @@ void validate_units(const Engine& E, const d2ft_dataset* ds, const int32_t* unit
   for (int j = 0; j < n_mb; ++j) D2FT_REQUIRE(units[j] >= 0 && units[j] < total, kInput, "step_units: unit out of range");
 }
 
-// one batch of the Dataset path (trainer.cpp:214-268): labels gathered as
-// dataset.unit_labels, the score slice as slice_scores (trainer.cpp:139-154)
-// from the full K x total_units table, the samples as prefetched fp64.
-void units_step(Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs, const int32_t* units_next,
-                const double* bwd_scores, const double* fwd_scores, int total_units, const int32_t* cf,
-                const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, double lr, double momentum) {
+// One batch of the Dataset path (trainer.cpp:214-268), gathered into pinned
+// staging set `buf`: labels as dataset.unit_labels, the score slice as
+// slice_scores (trainer.cpp:139-154) from the full K x total_units table, the
+// cost / capacity rows; validated in the reference's order.
+void units_prepare(Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs,
+                   const double* bwd_scores, const double* fwd_scores, int total_units, const int32_t* cf,
+                   const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, int buf) {
+  E.prep.valid = false;
+  E.ensure_units_staging();
   const int K = E.D.K();
   const int B = n_mb * mbs;
+  int* lab = E.u_lab[buf];
   for (int j = 0; j < n_mb; ++j)
-    for (int i = 0; i < mbs; ++i) E.h_labels[j * mbs + i] = ds->labels[(size_t)units[j] * mbs + i];
-  validate_labels(E.h_labels, B, E.D.C);
-  double* sb = E.h_scores;
-  double* sf = E.h_scores + (size_t)K * n_mb;
+    for (int i = 0; i < mbs; ++i) lab[j * mbs + i] = ds->labels[(size_t)units[j] * mbs + i];
+  validate_labels(lab, B, E.D.C);
+  double* sb = E.u_sc[buf];
+  double* sf = sb + (size_t)K * E.Nmax;
   for (int k = 0; k < K; ++k)
     for (int j = 0; j < n_mb; ++j) {
       sb[(size_t)k * n_mb + j] = bwd_scores[(size_t)k * total_units + units[j]];
       sf[(size_t)k * n_mb + j] = fwd_scores[(size_t)k * total_units + units[j]];
     }
   validate_sched_inputs(sb, sf, cf, cb, cap_full, cap_fwd, K, n_mb);
+  int32_t* caps = E.u_caps[buf];
+  std::memcpy(caps, cf, (size_t)K * 4);
+  std::memcpy(caps + K, cb, (size_t)K * 4);
+  std::memcpy(caps + 2 * K, cap_full, (size_t)K * 4);
+  std::memcpy(caps + 3 * K, cap_fwd, (size_t)K * 4);
+  E.prep.buf = buf;
+  E.prep.n_mb = n_mb;
+  E.prep.mbs = mbs;
+  E.prep.total_units = total_units;
+  E.prep.ds = ds;
+  E.prep.bwd = bwd_scores;
+  E.prep.fwd = fwd_scores;
+  E.prep.units.assign(units, units + n_mb);
+  E.prep.valid = true;
+}
+
+// One batch of the Dataset path: the staged batch (prepared while the
+// previous one computed, or now) goes up in three copies (labels, both score
+// slices, the cost / capacity rows), then the step; the next batch's fp64
+// samples are prefetched and its host inputs staged behind this step.  A
+// validation error of the next batch is raised by its own step.
+void units_step(Engine& E, const d2ft_dataset* ds, const int32_t* units, int n_mb, int mbs, const int32_t* units_next,
+                const double* bwd_scores, const double* fwd_scores, int total_units, const int32_t* cf,
+                const int32_t* cb, const int32_t* cap_full, const int32_t* cap_fwd, double lr, double momentum) {
+  const int K = E.D.K();
+  const int B = n_mb * mbs;
+  const size_t KN = (size_t)K * n_mb;
+  // the staged batch is used when it is this one: same units, dataset and
+  // score table (which the caller keeps unmodified, as for the prefetched
+  // samples) and the same cost / capacity rows (compared here)
+  const auto same_rows = [&](int buf) {
+    const int32_t* c = E.u_caps[buf];
+    return !std::memcmp(c, cf, (size_t)K * 4) && !std::memcmp(c + K, cb, (size_t)K * 4) &&
+           !std::memcmp(c + 2 * K, cap_full, (size_t)K * 4) && !std::memcmp(c + 3 * K, cap_fwd, (size_t)K * 4);
+  };
+  if (!(E.prep.valid && E.prep.n_mb == n_mb && E.prep.mbs == mbs && E.prep.ds == ds && E.prep.bwd == bwd_scores &&
+        E.prep.fwd == fwd_scores && E.prep.total_units == total_units &&
+        std::equal(units, units + n_mb, E.prep.units.begin(), E.prep.units.end()) && same_rows(E.prep.buf)))
+    units_prepare(E, ds, units, n_mb, mbs, bwd_scores, fwd_scores, total_units, cf, cb, cap_full, cap_fwd, E.ubuf);
+  const int buf = E.prep.buf;
+  E.prep.valid = false;
   E.ensure_sched(max_cols_of(cf, cb, cap_full, cap_fwd, K, n_mb));
   if (!E.have_prefetch) E.prefetch_units(ds->samples.data(), units, n_mb, mbs);
-  E.host_step(nullptr, E.h_labels, sb, sf, cf, cb, cap_full, cap_fwd, n_mb, mbs, lr, momentum);
-  if (units_next) E.prefetch_units(ds->samples.data(), units_next, n_mb, mbs);
+  E.begin_step(B);
+  D2FT_CUDA(cudaMemcpyAsync(E.labels_dev, E.u_lab[buf], (size_t)B * 4, cudaMemcpyHostToDevice, E.st));
+  D2FT_CUDA(cudaMemcpyAsync(E.bwd_dev, E.u_sc[buf], ((size_t)K * E.Nmax + KN) * 8, cudaMemcpyHostToDevice, E.st));
+  D2FT_CUDA(cudaMemcpyAsync(E.cf_dev, E.u_caps[buf], (size_t)K * 16, cudaMemcpyHostToDevice, E.st));
+  E.consume_prefetch(B);
+  E.compute_step(n_mb, mbs, lr, momentum);
+  D2FT_CUDA(cudaMemcpyAsync(E.h_codes, E.codes_mb, KN, cudaMemcpyDeviceToHost, E.st));
+  E.ubuf = buf ^ 1;
+  if (units_next) {
+    E.prefetch_units(ds->samples.data(), units_next, n_mb, mbs);
+    try {
+      units_prepare(E, ds, units_next, n_mb, mbs, bwd_scores, fwd_scores, total_units, cf, cb, cap_full, cap_fwd,
+                    buf ^ 1);
+    } catch (...) {
+      E.prep.valid = false;  // prepared again (and the error raised) by the next batch's step
+    }
+  }
 }
 }  // namespace
 

@@ -393,6 +393,9 @@ class SubnetModel:
                                            ptr(scores.forward), C.c_int(total), ptr(cf), ptr(cb),
                                            ptr(i32(capacities.full)), ptr(i32(capacities.fwd)), C.c_double(lr),
                                            C.c_double(momentum), C.byref(loss), ptr(codes)))
+        # the engine staged the next batch's labels / score slice from these
+        # tables and recognises them by address: keep them alive until then
+        self._staged = (dataset, scores.backward, scores.forward) if un is not None else None
         return loss.value, ScheduleTable(K, n_mb, codes)
 
     def prepass_scores(self, samples, labels, micro_batch_size=1, fwd_metric="fisher_information",

@@ -107,3 +107,30 @@ def test_step_units_unaligned_heap_samples():
     assert la == lb and np.array_equal(a.params(), b.params())
     for x in (a, b, ds, ds0):
         x.close()
+
+
+def test_step_units_staged_batch_follows_the_call():
+    """units_next also stages the next batch's labels / score slice on the
+    host; the next call uses that staging only for the same dataset, score
+    table and cost / capacity rows — changed capacities or another score
+    table give exactly the unstaged engine's step."""
+    ds, scores = _setup(16, 1)
+    _, scores2 = _setup(16, 1, seed=9)
+    K = CFG.scheduled_subnet_count()
+    n_mb = 4
+    caps = P.Capacities([(2 * n_mb // 5 + 1) * 5] * K, [(2 * n_mb // 5) * 2] * K)
+    caps2 = P.Capacities([5] * K, [2] * K)
+    u0, u1, u2 = [0, 5, 2, 7], [1, 3, 4, 6], [8, 9, 10, 11]
+    a = E.SubnetModel(CFG, n_mb)
+    b = E.SubnetModel(CFG, n_mb)
+    seq = [(u0, scores, caps, u1), (u1, scores, caps2, u2), (u2, scores2, caps, None)]
+    for units, sc, cp, nxt in seq:
+        la, ta = a.step_units(ds, units, sc, P.CostModel(), cp, 1, 0.05, 0.9, units_next=nxt)
+        lb, tb = b.step_units(ds, units, sc, P.CostModel(), cp, 1, 0.05, 0.9)
+        ref = O.knapsack_schedule(sc.backward[:, units], sc.forward[:, units], 2, 3, cp.full, cp.fwd)
+        assert np.array_equal(ta.codes, ref) and np.array_equal(tb.codes, ref)
+        assert la == lb
+    assert np.array_equal(a.params(), b.params())
+    for m in (a, b):
+        m.close()
+    ds.close()
