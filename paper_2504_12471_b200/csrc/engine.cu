@@ -630,9 +630,15 @@ struct Engine {
        // 32 features x 32 tokens (token-major QKV), clipped at T
       CUtensorMap sm[5];
       constexpr int cw = G1<208>::kChunk;
+#ifndef D2FT_EXP_G1_HALFBOX
       sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, cw, 32, cw * 2);
       sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, cw, 32, cw * 2);
       sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, cw);
+#else  // experiment: same store count, half the bytes (results wrong; timing only)
+      sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, cw / 2, 32, cw);
+      sm[1] = make_tmap_store_f16_3d(OGT, T, PO, L * Bm * H, TP * 2, PO * TP * 2, cw / 2, 32, cw);
+      sm[2] = make_tmap_store_f16_3d(QKV, 3 * D.dh, T, L * Bm * H, 3 * D.dh * 2, T * 3 * D.dh * 2, 32, cw / 2);
+#endif
       // G4 epilogue: dO (token-major) and the dz rows of dY1T (feature-major)
       sm[3] = make_tmap_store_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, 32, 32);
       sm[4] = make_tmap_store_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 32, 32, 64);

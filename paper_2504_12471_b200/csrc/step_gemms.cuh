@@ -167,7 +167,9 @@ struct G1 {
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
+#ifndef D2FT_EXP_G1_NOSTORE
         ptx::tma_store_3d(maps + 2, stp, f0, col0, plane);
+#endif
         ptx::bulk_commit();
       }
       return;
@@ -177,7 +179,11 @@ struct G1 {
 #pragma unroll
     for (int i = 0; i < kChunk / 2; ++i) {
       float g0, g1, d0, d1;
+#ifndef D2FT_EXP_G1_NOMATH
       gelu_and_grad2(v[2 * i] + r.bias, v[2 * i + 1] + r.bias, g0, g1, d0, d1);
+#else
+      g0 = v[2 * i] + r.bias, g1 = v[2 * i + 1] + r.bias, d0 = g1, d1 = g0;  // experiment: no GELU math
+#endif
       const __half2 a = __floats2half2_rn(g0, g1), b = __floats2half2_rn(d0, d1);
       hg[i] = *reinterpret_cast<const uint32_t*>(&a);
       hz[i] = *reinterpret_cast<const uint32_t*>(&b);
@@ -197,8 +203,10 @@ struct G1 {
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
+#ifndef D2FT_EXP_G1_NOSTORE
       ptx::tma_store_3d(maps + 1, stp, col0, D.dh + j0, plane);
       if (r.full) ptx::tma_store_3d(maps + 0, stp + kBufBytes / 2, col0, j0, plane);
+#endif
       ptx::bulk_commit();
     }
   }
