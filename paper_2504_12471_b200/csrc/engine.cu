@@ -73,6 +73,17 @@ constexpr bool kFuseSgd = D2FT_FUSE_SGD;
 #ifndef D2FT_G1_EPI
 #define D2FT_G1_EPI 2  // epilogue warpgroups of the G1 GEMM (experiment builds vary it)
 #endif
+// G1 with the sample's xn resident in shared memory across its unit groups
+// (GemmShape RES, pair UMMA): d = 768 (12 k-blocks) and T <= 208 only.
+// Opt-in: correct (step parity suite) but slower — 156 KB of resident B
+// leaves room for only 2 weight stages (G1 1.16 vs 0.95 ms per step) or 3
+// with 16-token epilogue chunks (0.99), DESIGN.md §10.
+#ifndef D2FT_G1_RESB
+#define D2FT_G1_RESB 0
+#endif
+#ifndef D2FT_G1_RES_STAGES
+#define D2FT_G1_RES_STAGES 2
+#endif
 
 namespace d2ft_b200 {
 
@@ -864,9 +875,16 @@ struct Engine {
       act_t* ZTl = ZT + (size_t)l * Bm * H * D.fs * D.TP;
       act_t* OGTl = OGT + (size_t)l * Bm * H * D.PO * D.TP;
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
-      gemm_tokN<G1, 0, 0, D2FT_G1_EPI, 0>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads,
-                                       lists.act_cnt, (const uint8_t*)codes_exp, P + seg[S_B1].off + (size_t)l * H * D.fs,
-                                       (const CUtensorMap*)store_maps);
+      if (D2FT_G1_RESB && BNt == 208 && D.d == 12 * 64)
+        launch_gemm<G1<208>, GemmShape<208, D2FT_G1_RES_STAGES, 0, D2FT_G1_EPI, 2, 0, 0, 1, 12>>(
+            tm_W1T, tm_xn,
+            G1<208>{D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt, (const uint8_t*)codes_exp,
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, (const CUtensorMap*)store_maps},
+            0, st);
+      else
+        gemm_tokN<G1, 0, 0, D2FT_G1_EPI, 0>(tm_W1T, tm_xn, D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads,
+                                         lists.act_cnt, (const uint8_t*)codes_exp, P + seg[S_B1].off + (size_t)l * H * D.fs,
+                                         (const CUtensorMap*)store_maps);
       mark(PH_ATTN_F);
       if (D.dh == 64 && D.TQ <= 256)
         launch_attn_fwd_tc(tm_Q, tm_K, tm_V, D, l, af_items + l * Bm * H, af_count + l, lists.act_heads, OGTl,

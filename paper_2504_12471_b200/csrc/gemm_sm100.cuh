@@ -122,8 +122,10 @@ constexpr int kKQ = 16;
 template <class P>
 struct alignas(16) RingEntry {
   int t;
+  int flags;  // resident-B mode: kNewB (first tile of its B plane) | kLastB (last one)
   typename P::Tile c;
 };
+constexpr int kNewB = 1, kLastB = 2;
 struct alignas(16) KRec {
   KCoord k;
   int nk;  // 16-wide K steps of the k-block that carry data (P::ksteps)
@@ -136,7 +138,7 @@ struct SchedSmem {
 };
 template <class P, class S>
 constexpr int gemm_sched_offset() {  // after the epilogue staging
-  return S::STAGES * S::STAGE_BYTES + 512 + 4 * S::EPI * epi_stage_bytes<P>::value;
+  return S::MAIN_BYTES + 512 + 4 * S::EPI * epi_stage_bytes<P>::value;
 }
 
 template <class P, class S>
@@ -152,12 +154,20 @@ constexpr int gemm_smem_bytes() {
 // multicast, so a stage is A + B/2 bytes per CTA and more stages fit; the even
 // CTA issues the MMAs for both, its mbarriers count both CTAs' TMA bytes, and
 // its commits arrive on both CTAs' barriers.  K-major B only.
+// RES > 0: resident B (pair UMMA, K-major B, static tile ranges only).  The
+// CTA's half of B for all RES k-blocks of a plane stays in shared memory
+// across the consecutive tiles that share the plane (a sample's unit groups
+// in G1), so only A streams through the STAGES ring.  Per k-block barriers:
+// the MMA of the first tile of a plane waits bfull[kb]; the MMA of the last
+// tile commits bempty[kb] after its k-block kb, and the producer of the next
+// plane reloads block kb behind it.
 template <int BN_, int STAGES_, int FMT_ = 0, int EPI_ = 4, int CLUSTER_ = 1, int BMN_ = 0, int AMN_ = 0,
-          int CG2_ = 0>
+          int CG2_ = 0, int RES_ = 0>
 struct GemmShape {
   static constexpr int BM = 128, BK = 64, BN = BN_, STAGES = STAGES_, FMT = FMT_, EPI = EPI_, CLUSTER = CLUSTER_;
-  static constexpr int BMN = BMN_, AMN = AMN_, CG2 = CG2_;
+  static constexpr int BMN = BMN_, AMN = AMN_, CG2 = CG2_, RES = RES_;
   static_assert(!CG2 || CLUSTER == 2, "pair UMMA needs a CTA pair");
+  static_assert(!RES || (CG2 && !BMN && RES <= 16), "resident B: pair UMMA, K-major B, <= 16 k-blocks");
   // MN-major B: 64-wide N blocks held per CTA (pair UMMA: of this CTA's N/2)
   static constexpr int NBLK = CG2 ? (BN / 2 + 63) / 64 : (BN + 63) / 64;
   static constexpr int THREADS = 128 + 128 * EPI;
@@ -165,8 +175,10 @@ struct GemmShape {
   // B bytes held per CTA and stage (CG2: this CTA's N/2 rows)
   static constexpr int B_BYTES = BMN ? NBLK * 64 * BK * 2 : (CG2 ? BN * BK : BN * BK * 2);
   static constexpr int B_PART = CG2 ? B_BYTES : B_BYTES / CLUSTER;  // bytes of B each CTA loads (K-major)
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
+  static constexpr int STAGE_BYTES = RES ? A_BYTES : A_BYTES + B_BYTES;  // bytes a stage's TMA brings per CTA
+  static constexpr int B_SLOTS = RES ? RES : STAGES;  // B blocks held: resident plane or one per stage
+  static constexpr int MAIN_BYTES = STAGES * A_BYTES + B_SLOTS * B_BYTES;
+  static constexpr int SMEM_BYTES = MAIN_BYTES + 1024 + 512;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
   static_assert(BMN || (B_BYTES % 1024 == 0 && B_PART % 1024 == 0),
                 "B stage parts must keep 1024-byte swizzle alignment");
@@ -181,16 +193,18 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::STAGES * S::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S::B_SLOTS * S::B_BYTES);
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* tq_full = tempty + 2;        // rank 0 -> rank 1 tile-id queue (dynamic scheduling)
   uint64_t* tq_empty = tq_full + kTileQ;
-  int* tq = reinterpret_cast<int*>(tq_empty + kTileQ);
+  uint64_t* bfull = tq_empty + kTileQ;   // resident B, per k-block (RES)
+  uint64_t* bempty = bfull + S::RES;
+  int* tq = reinterpret_cast<int*>(bempty + S::RES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kTileQ);
   // per-epilogue-warp staging (epi_stage_bytes), 128-byte aligned, after the barriers
-  uint8_t* epi_stage = sB + S::STAGES * S::B_BYTES + 512;
+  uint8_t* epi_stage = sB + S::B_SLOTS * S::B_BYTES + 512;
   SchedSmem<P>& sch = *reinterpret_cast<SchedSmem<P>*>(smem + gemm_sched_offset<P, S>());
   RingEntry<P>* ring = sch.ring;
   uint64_t* ring_full = sch.ring_full;
@@ -216,6 +230,10 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 4 * S::EPI * (S::CG2 ? 2 : 1));  // pair UMMA: both CTAs' epilogues
+    }
+    for (int i = 0; i < S::RES; ++i) {
+      ptx::mbar_init(&bfull[i], 1);
+      ptx::mbar_init(&bempty[i], 1);  // the even CTA's commit, multicast to both
     }
     for (int i = 0; i < kTileQ; ++i) {
       ptx::mbar_init(&tq_full[i], 1);
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       const int q = i % kRing;
       ptx::mbar_wait(&ring_full[q], (i / kRing) & 1);
       if (ring[q].t >= ntiles) break;
-      body(static_cast<const typename P::Tile&>(ring[q].c));
+      body(static_cast<const typename P::Tile&>(ring[q].c), ring[q].flags);
       __syncwarp(__activemask());
       if (leader) ptx::mbar_arrive(&ring_empty[q]);
     }
@@ -262,12 +280,13 @@ __global__ void __launch_bounds__(S::THREADS, 1)
   if (warp == 3) {
     if (lane == 0) {
       int kqi = 0;
-      auto push = [&](int i, int t) {
+      auto push = [&](int i, int t, int flags = 0) {
         const int q = i % kRing;
         typename P::Tile c{};
         if (t < ntiles) prob.tile(t, rank, c);  // global loads resolve before the slot is needed
         ptx::mbar_wait(&ring_empty[q], ((i / kRing) & 1) ^ 1);
         ring[q].t = t;
+        ring[q].flags = flags;
         ring[q].c = c;
         ptx::mbar_arrive(&ring_full[q]);
         if (t >= ntiles) return;
@@ -307,6 +326,26 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           push(i, t);
           if (t >= ntiles) break;
         }
+      } else if (S::RES) {
+        // contiguous tile range per slot; a tile's B plane = its k-block 0 coordinate
+        const int t0 = (int)((long long)slot0 * ntiles / nslots), t1 = (int)((long long)(slot0 + 1) * ntiles / nslots);
+        auto plane = [&](int t) {
+          typename P::Tile c{};
+          prob.tile(t, rank, c);
+          return prob.kcoord(c, 0).bz;
+        };
+        int cur = t0 < t1 ? plane(t0) : -1, prev = -1;
+        for (int i = 0;; ++i) {
+          const int t = t0 + i;
+          if (t >= t1) {
+            push(i, ntiles);
+            break;
+          }
+          const int nxt = t + 1 < t1 ? plane(t + 1) : -1;
+          push(i, t, (cur != prev ? kNewB : 0) | (nxt != cur ? kLastB : 0));
+          prev = cur;
+          cur = nxt;
+        }
       } else {
         for (int i = 0;; ++i) {
           const int t = slot0 + i * nslots;
@@ -320,7 +359,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int kqi = 0;
-      for_each_tile(true, [&](const typename P::Tile& c) {
+      uint32_t bph = 0;  // resident B: loads of the plane so far (parity)
+      for_each_tile(true, [&](const typename P::Tile& c, int flags) {
         const int nkb = c.nkb;
         for (int kb = 0; kb < nkb; ++kb, ++kqi) {
           const int j = kqi % kKQ;
@@ -332,6 +372,14 @@ __global__ void __launch_bounds__(S::THREADS, 1)
             // both CTAs' bytes complete on the even CTA's full barrier
             const uint32_t fb = ptx::mapa(&full[stage], 0);
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+            if constexpr (S::RES) {
+              if (flags & kNewB) {  // block kb of the new plane, once the last tile of the old one read it
+                ptx::mbar_wait(&bempty[kb], bph ^ 1);
+                if (rank == 0) ptx::mbar_arrive_expect_tx(&bfull[kb], 2 * S::B_BYTES);
+                ptx::tma_load_3d_cg2(sB + kb * S::B_BYTES, &tmB, ptx::mapa(&bfull[kb], 0), k.bx,
+                                     k.by + rank * (S::BN / 2), k.bz);
+              }
+            }
             if constexpr (S::AMN) {
               ptx::tma_load_3d_cg2(a, &tmA, fb, k.ay0, k.ax, k.az);
               ptx::tma_load_3d_cg2(a + S::A_BYTES / 2, &tmA, fb, k.ay1, k.ax, k.az);
@@ -339,7 +387,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
               ptx::tma_load_3d_cg2(a, &tmA, fb, k.ax, k.ay0, k.az);
               ptx::tma_load_3d_cg2(a + S::A_BYTES / 2, &tmA, fb, k.ax, k.ay1, k.az);
             }
-            if constexpr (S::BMN) {  // this CTA's N/2 tokens from k.bx + rank * BN/2, 64 per box
+            if constexpr (S::RES) {
+            } else if constexpr (S::BMN) {  // this CTA's N/2 tokens from k.bx + rank * BN/2, 64 per box
               for (int j2 = 0; j2 < S::NBLK; ++j2)
                 ptx::tma_load_3d_cg2(sB + stage * S::B_BYTES + j2 * (64 * S::BK * 2), &tmB, fb,
                                      k.bx + rank * (S::BN / 2) + 64 * j2, k.by, k.bz);
@@ -379,6 +428,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
             phase ^= 1;
           }
         }
+        if (S::RES && (flags & kNewB)) bph ^= 1;
       });
     }
   } else if (warp == 1) {
@@ -390,8 +440,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     // pair UMMA: the odd CTA's MMA warp only keeps the ring / k-block queue flowing
     const bool issuer = !S::CG2 || rank == 0;
     int stage = 0, acc = 0, kqm = 0;
-    uint32_t phase = 0, acc_phase = 0;
-    for_each_tile(lane == 0, [&](const typename P::Tile& cref) {
+    uint32_t phase = 0, acc_phase = 0, bph = 0;
+    for_each_tile(lane == 0, [&](const typename P::Tile& cref, int flags) {
       const typename P::Tile c = cref;  // registers (smem reads would be re-done around every store)
       if (!issuer) {
         if constexpr (has_ksteps<P>::value) {
@@ -412,7 +462,11 @@ __global__ void __launch_bounds__(S::THREADS, 1)
         ptx::tc_fence_after();
         const uint32_t as = ptx::smem_u32(sA + stage * S::A_BYTES);
         const uint64_t ad = S::AMN ? ptx::desc_sw128_mn(as, S::A_BYTES / 2) : ptx::desc_sw128(as);
-        const uint32_t bs = ptx::smem_u32(sB + stage * S::B_BYTES);
+        if (S::RES && (flags & kNewB)) {
+          ptx::mbar_wait(&bfull[kb], bph);
+          ptx::tc_fence_after();
+        }
+        const uint32_t bs = ptx::smem_u32(sB + (S::RES ? kb : stage) * S::B_BYTES);
         const uint64_t bd = S::BMN ? ptx::desc_sw128_mn(bs, 64 * S::BK * 2) : ptx::desc_sw128(bs);
         // K step of 16: +32 B along a K-major row, or +16 rows (2 KB) of an MN-major block
         constexpr uint64_t astep = S::AMN ? (16 * 128) >> 4 : 2;
@@ -438,6 +492,8 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           if constexpr (S::CG2) ptx::umma_commit_cg2_mc(&empty[stage], kPair);
           else if (S::CLUSTER == 2) ptx::umma_commit_mc(&empty[stage], kPair);
           else ptx::umma_commit(&empty[stage]);
+          // the plane's last tile has read B block kb: both producers may reload it
+          if (S::RES && (flags & kLastB)) ptx::umma_commit_cg2_mc(&bempty[kb], kPair);
         }
         __syncwarp();
         if (++stage == S::STAGES) {
@@ -445,6 +501,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
           phase ^= 1;
         }
       }
+      if (S::RES && (flags & kNewB)) bph ^= 1;
       if (ptx::elect_one()) {
         if constexpr (S::CG2) ptx::umma_commit_cg2_mc(&tfull[acc], kPair);  // both CTAs' epilogues
         else ptx::umma_commit(&tfull[acc]);
@@ -459,7 +516,7 @@ __global__ void __launch_bounds__(S::THREADS, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for_each_tile(lane == 0, [&](const typename P::Tile& cref) {
+    for_each_tile(lane == 0, [&](const typename P::Tile& cref, int) {
       const typename P::Tile c = cref;
       // Chunks of this warp: 16*e + i*16*EPI.  Row state and the first
       // chunk's epilogue operands are loaded before the accumulator wait (they
