@@ -84,6 +84,15 @@ constexpr bool kFuseSgd = D2FT_FUSE_SGD;
 #ifndef D2FT_G1_RES_STAGES
 #define D2FT_G1_RES_STAGES 2
 #endif
+// G1 on pair UMMA (B split between the pair instead of multicast, 6 stages
+// instead of 4) at T <= 208: G1 0.875-0.885 vs 0.906-0.909 ms per step on one
+// box (two A/B runs), step -0.4%.  0 = the multicast pair of gemm_tokN.
+#ifndef D2FT_G1_PAIR
+#define D2FT_G1_PAIR 1
+#endif
+#ifndef D2FT_G1_PAIR_STAGES
+#define D2FT_G1_PAIR_STAGES 6
+#endif
 
 namespace d2ft_b200 {
 
@@ -814,9 +823,9 @@ struct Engine {
   template <template <int> class Prob, int BMN = 0, int AMN = 0, int EPI = 4, int PAIR_UMMA = 1, class... Args>
   void gemm_tokN(const CUtensorMap& a, const CUtensorMap& b, Args... args) {
     // K-major B: pair UMMA (cta_group::2, B split across the pair, deeper
-    // pipeline); MN-major B: B multicast to both CTAs of the pair.  G1 keeps
-    // multicast: its epilogue is the limiter and the pair UMMA couples the two
-    // CTAs' epilogues through one accumulator release (0.91 vs 0.95 ms).
+    // pipeline); MN-major B: B multicast to both CTAs of the pair.  (G1 at
+    // T <= 208 launches its pair-UMMA shape directly, D2FT_G1_PAIR; other
+    // token tiles keep multicast here.)
     constexpr int CG = !PAIR_UMMA ? 0 : (BMN ? kCG2Bmn : kCG2);
     // Pair UMMA with MN-major B: each CTA holds BN/2 token columns of B as
     // 64-wide swizzle blocks; a partial last block (208/2 = 104) costs a third
@@ -877,6 +886,12 @@ struct Engine {
       const size_t g1cap = Bm * ((D.UQ * H + 1) / 2);
       if (D2FT_G1_RESB && BNt == 208 && D.d == 12 * 64)
         launch_gemm<G1<208>, GemmShape<208, D2FT_G1_RES_STAGES, 0, D2FT_G1_EPI, 2, 0, 0, 1, 12>>(
+            tm_W1T, tm_xn,
+            G1<208>{D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt, (const uint8_t*)codes_exp,
+                    P + seg[S_B1].off + (size_t)l * H * D.fs, (const CUtensorMap*)store_maps},
+            0, st);
+      else if (D2FT_G1_PAIR && BNt == 208)
+        launch_gemm<G1<208>, GemmShape<208, D2FT_G1_PAIR_STAGES, 0, D2FT_G1_EPI, 2, 0, 0, 1>>(
             tm_W1T, tm_xn,
             G1<208>{D, l, g1_tiles + l * g1cap, g1_count + l, lists.act_heads, lists.act_cnt, (const uint8_t*)codes_exp,
                     P + seg[S_B1].off + (size_t)l * H * D.fs, (const CUtensorMap*)store_maps},
