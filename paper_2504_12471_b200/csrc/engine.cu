@@ -648,7 +648,7 @@ struct Engine {
     }
     {  // G1 epilogue bulk stores: 32 tokens x 32 feature rows (feature-major) or
        // 32 features x 32 tokens (token-major QKV), clipped at T
-      CUtensorMap sm[5];
+      CUtensorMap sm[6];
       constexpr int cw = G1<208>::kChunk;
 #ifndef D2FT_EXP_G1_HALFBOX
       sm[0] = make_tmap_store_f16_3d(ZT, T, D.fs, L * Bm * H, TP * 2, D.fs * TP * 2, cw, 32, cw * 2);
@@ -662,6 +662,9 @@ struct Engine {
       // G4 epilogue: dO (token-major) and the dz rows of dY1T (feature-major)
       sm[3] = make_tmap_store_f16_3d(dO, D.dh, T, Bm * H, D.dh * 2, T * D.dh * 2, 32, 32);
       sm[4] = make_tmap_store_f16_3d(dY1T, T, PQ, Bm * H, TP * 2, PQ * TP * 2, 32, 32, 64);
+      // G5 epilogue: the [Wo;W2] weight-gradient rows (fp32, [L][d][H*PO])
+      sm[5] = make_tmap_store_f32_3d(G + seg[S_W2T].off, (uint64_t)H * PO, d, L, (uint64_t)H * PO * 4,
+                                     (uint64_t)d * H * PO * 4, 16, 32, 64);
       D2FT_CUDA(cudaMemcpy(store_maps, sm, sizeof(sm), cudaMemcpyHostToDevice));
     }
     // B operands, tokens as N read MN-major from feature-major buffers (64 x 64 boxes)
@@ -950,9 +953,11 @@ struct Engine {
     // reader of the fp16 operands), overlapping the lower blocks' backward
     sgd_layer = step_train && side && side_g7 && !sm && !lora_rank && !sgd_fused && !data_parallel();
     auto g5 = [&](int l, cudaStream_t s5) {
-      launch_gemm<G5<160>, GemmShape<160, kCG2 ? 8 : 6, 0, D2FT_G5_EPI, 2, 0, 1, kCG2>>(
+      // the bulk-store staging of the G5 epilogue (16 warps x 2 KB) costs one stage
+      launch_gemm<G5<160>, GemmShape<160, kCG2 ? (D2FT_G5_TMA ? 7 : 8) : 6, 0, D2FT_G5_EPI, 2, 0, 1, kCG2>>(
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
-                  ord_head + l * H, ctr(l, C_G5), fsgd(S_W2T, W2T_bf, (size_t)l * d * H * D.PO)},
+                  ord_head + l * H, ctr(l, C_G5), fsgd(S_W2T, W2T_bf, (size_t)l * d * H * D.PO),
+                  (const CUtensorMap*)store_maps},
           s5 == st ? 0 : side_ctas, s5);
     };
     for (int l = D.L - 1; l >= 0; --l) {

@@ -47,15 +47,16 @@ CUtensorMap make_tmap_16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t
   return m;
 }
 
-CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-                                   uint32_t box0, uint32_t box1, int swizzle_bytes) {
+static CUtensorMap make_tmap_store_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                                      uint64_t s2, uint32_t box0, uint32_t box1, int swizzle_bytes, int esize) {
   CUtensorMap m;
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {s1, s2};
   const cuuint32_t box[3] = {box0, box1, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  D2FT_REQUIRE(s1 % 16 == 0 && s2 % 16 == 0 && (box0 * 2) % 16 == 0, kInput, "store tensor map: 16-byte granularity");
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+  D2FT_REQUIRE(s1 % 16 == 0 && s2 % 16 == 0 && (box0 * esize) % 16 == 0, kInput,
+               "store tensor map: 16-byte granularity");
+  const CUresult r = encode_fn()(&m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box,
                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  swizzle_bytes == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
                                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
@@ -63,6 +64,14 @@ CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, u
                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   D2FT_REQUIRE(r == CUDA_SUCCESS, kCuda, "cuTensorMapEncodeTiled (store) failed (" + std::to_string((int)r) + ")");
   return m;
+}
+CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                                   uint32_t box0, uint32_t box1, int swizzle_bytes) {
+  return make_tmap_store_3d(base, d0, d1, d2, s1, s2, box0, box1, swizzle_bytes, 2);
+}
+CUtensorMap make_tmap_store_f32_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                                   uint32_t box0, uint32_t box1, int swizzle_bytes) {
+  return make_tmap_store_3d(base, d0, d1, d2, s1, s2, box0, box1, swizzle_bytes, 4);
 }
 
 int num_sms() {

@@ -606,6 +606,9 @@ inline CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, 
 // (32 or 64); writes past d0/d1 are clipped.
 CUtensorMap make_tmap_store_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
                                    uint32_t box0, uint32_t box1, int swizzle_bytes = 0);
+// fp32 variant (box0 fp32 elements per row; swizzle_bytes == box0 * 4)
+CUtensorMap make_tmap_store_f32_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                                   uint32_t box0, uint32_t box1, int swizzle_bytes = 0);
 
 int num_sms();
 

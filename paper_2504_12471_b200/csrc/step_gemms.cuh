@@ -450,6 +450,14 @@ struct FusedSgd {
 // dW2T[l][m][h*PO + f] = sum_{s in Full(h)} sum_t dC[s][t][m] [O|g][s][h][t][f]
 // (model.cpp:249, 263).  A = dC read MN-major (plane s, [t][m] as [K][M]),
 // B = OGT (plane (l*Bmax+s)*H+h).
+// Epilogue: per-lane 16-byte stores (16 contiguous fp32 of the thread's row).
+// D2FT_G5_TMA=1 (opt-in): each warp stages its 32 rows x 16 fp32 (64-byte
+// swizzle) and writes them with one bulk tensor store ([5] of the store maps)
+// — G5 0.526 -> 0.496 ms per step, but the G7 that follows it 0.563 -> 0.608
+// (same box, two runs), the step neutral; not adopted.
+#ifndef D2FT_G5_TMA
+#define D2FT_G5_TMA 0
+#endif
 template <int BN>
 struct G5 {
   Dims D;
@@ -461,11 +469,14 @@ struct G5 {
   const int* order;  // block l: heads by decreasing Full-sample count
   int* ctr;
   FusedSgd sgd;
+  const CUtensorMap* maps;  // [5]: dW2T bulk-store map (fp32, 16 x 32 box, 64B swizzle)
+  static constexpr int kEpiStageBytes = D2FT_G5_TMA ? 32 * 16 * 4 : 0;
   struct Tile {
     int nkb, h, mt, nt;
   };
   struct Row {
     float inv;
+    uint8_t* stage;
   };
   __device__ int ntn() const { return (D.PO + BN - 1) / BN; }
   // slot = (head, m-tile pair, n-tile): the pair shares B = [O|g]^T of (s, h)
@@ -499,6 +510,26 @@ struct G5 {
       for (int i = 0; i < 16; ++i)
         if (f0 + i < D.PO) sgd.apply(o + i, v[i] * r.inv);
       return;
+    }
+    if constexpr (D2FT_G5_TMA > 0) {
+      if (f0 + 16 <= D.PO && (m - (int)(threadIdx.x & 31)) + 32 <= D.d) {  // warp-uniform
+        const int lane = threadIdx.x & 31;
+        const uint32_t sb = ptx::smem_u32(r.stage), rb = sb + lane * 64, sw = (lane >> 1) & 3;
+        if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's store has read the staging
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ptx::st_shared_v4(rb + ((q ^ sw) << 4), __float_as_uint(v[4 * q] * r.inv),
+                            __float_as_uint(v[4 * q + 1] * r.inv), __float_as_uint(v[4 * q + 2] * r.inv),
+                            __float_as_uint(v[4 * q + 3] * r.inv));
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(maps + 5, r.stage, c.h * D.PO + f0, m - lane, l);
+          ptx::bulk_commit();
+        }
+        return;
+      }
     }
     float* out = dW2T + (size_t)m * D.H * D.PO + c.h * D.PO;
     if (f0 + 16 <= D.PO) {  // 16 contiguous fp32 of this row: four 16-byte stores
