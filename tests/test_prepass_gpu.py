@@ -1,8 +1,13 @@
 """GPU scoring pre-pass (prepass_scores, scoring.cpp:108-151) against the fp64
 oracle restatement (oracle/model_oracle.prepass_scores): every metric of every
-scheduled head-subnet and unit.  Tolerance: 2e-2 relative per entry for the
-gradient metrics (fp16 GEMM operands, per-unit gradients — not averaged over a
-batch), 1e-5 for WeightMagnitude (fp32 masters)."""
+scheduled head-subnet and unit.  Tolerance: 1e-2 relative per entry for the
+gradient metrics (north_star's gradient bar; fp16 GEMM operands, per-unit
+gradients — not averaged over a batch; achieved <= 1.7e-3, LoRA Fisher the
+largest, profiles/r2_prepass_errors.jsonl), 1e-5 for WeightMagnitude (fp32
+masters)."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -13,6 +18,16 @@ pytestmark = pytest.mark.gpu
 
 SMALL = E.ModelConfig(2, 4, 128, 256, 64, 4, 1)      # dh = 32 (mma.sync attention)
 SMALL64 = E.ModelConfig(2, 2, 128, 256, 50, 4, 5)    # dh = 64 (tcgen05 attention), ragged T
+
+
+def _report(case, metric, rel):
+    """Achieved error beside the assertion (gpurun_out/prepass_errors.jsonl)."""
+    rec = {"case": case, "metric": metric, "max_rel": float(rel.max()), "p99": float(np.percentile(rel, 99))}
+    print(json.dumps(rec))
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if os.path.isdir(d):
+        with open(os.path.join(d, "prepass_errors.jsonl"), "a") as f:
+            f.write(json.dumps(rec) + "\n")
 
 
 def _oc(cfg):
@@ -30,8 +45,9 @@ def _check(cfg, n, mbs, nsamp_data=8):
         t = m.prepass_scores(x, y, mbs, fm, bm)
         rf, rb = MO.prepass_scores(_oc(cfg), p, x.astype(np.float64), y, mbs, fm, bm)
         for got, ref, metric in ((t.forward, rf, fm), (t.backward, rb, bm)):
-            tol = 1e-5 if metric == "weight_magnitude" else 2e-2
+            tol = 1e-5 if metric == "weight_magnitude" else 1e-2
             rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
+            _report(f"L{cfg.num_blocks}H{cfg.heads_per_block}d{cfg.model_dim}T{cfg.seq_len} n{n} mbs{mbs}", metric, rel)
             assert rel.max() <= tol, (metric, rel.max(), np.unravel_index(rel.argmax(), rel.shape))
     assert np.array_equal(m.params(), before)  # no update (scoring.hpp:46-47)
     m.close()
@@ -82,8 +98,9 @@ def test_prepass_lora_matches_oracle(cfg, mbs):
         t = m.prepass_scores(x, y, mbs, fm, bm)
         rf, rb = MO.prepass_scores_lora(_oc(cfg), p, rank, scaling, ad, x.astype(np.float64), y, mbs, fm, bm)
         for got, ref, metric in ((t.forward, rf, fm), (t.backward, rb, bm)):
-            tol = 1e-5 if metric == "weight_magnitude" else 2e-2
+            tol = 1e-5 if metric == "weight_magnitude" else 1e-2
             rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
+            _report(f"lora L{cfg.num_blocks}H{cfg.heads_per_block}d{cfg.model_dim} mbs{mbs}", metric, rel)
             assert rel.max() <= tol, (metric, rel.max(), np.unravel_index(rel.argmax(), rel.shape))
     assert np.array_equal(m.params(), before) and np.array_equal(m.lora_params(), abefore)
     m.close()
