@@ -743,13 +743,23 @@ def run_ours(args):
                     "frac": round(fl[k] / (phases[k] * 1e-3) / 1e12 / peak, 4)}
                 for k in gemm_keys + ["attn_fwd", "attn_bwd"] if phases.get(k, 0) > 0}
     step_tf = alg_total / (ms_step * 1e-3) / 1e12
-    traffic = None
+    traffic, l2 = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("G1_dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("G1_dram_bytes_per_launch")
+            if tj.get("G1_l2_read_bytes") and phases["G1"] > 0:
+                # G1's binding roof is the L2 path: its L2 bytes per launch
+                # (ncu) over the live per-launch time, against ~6.3 KB/clk of LTS throughput
+                # (microarchitecture notes, measured on B300) at the max SM clock
+                l2b = tj["G1_l2_read_bytes"] + tj.get("G1_l2_bulk_store_bytes", 0)
+                l2_tbs = l2b / (phases["G1"] / L * 1e-3) / 1e12
+                cap = 6300 * (ck.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+                l2 = {"bytes_per_launch": l2b, "achieved_tbs": round(l2_tbs, 2), "lts_cap_tbs_est": round(cap, 2),
+                      "frac": round(l2_tbs / cap, 3)}
         except Exception:
-            traffic = None
+            traffic, l2 = None, None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_baseline(os.cpu_count() or 1, B=B)
@@ -822,7 +832,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": "G1 grouped tcgen05 GEMM ([Wq|Wk|Wv|W1] x xn, active heads)",
                          "achieved": round(g1_tflops, 1), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(g1_tflops / peak, 4), "traffic": traffic,
+                         "frac": round(g1_tflops / peak, 4), "traffic": traffic, "l2_path": l2,
                          "frac_of_sustained": round(g1_tflops / PEAKS["bf16_tflops_sustained"], 4),
                          "peak_source": f"{PEAK_SRC} bf16 dense {'burst' if at_max else 'sustained'} "
                                         f"(SM clock {ck.get('sm_mhz')} of {ck.get('sm_max_mhz')} MHz in the timed "
