@@ -90,6 +90,12 @@ constexpr bool kFuseSgd = D2FT_FUSE_SGD;
 #ifndef D2FT_G1_PAIR
 #define D2FT_G1_PAIR 1
 #endif
+// G4 in the resident-B mode (the sample's dC half kept in shared memory
+// across its unit groups, static contiguous tile ranges): opt-in; correct on
+// the step parity suite, but 3 stages fit: G4 0.634 vs 0.546 ms per step
+#ifndef D2FT_G4_RESB
+#define D2FT_G4_RESB 0
+#endif
 #ifndef D2FT_G1_PAIR_STAGES
 #define D2FT_G1_PAIR_STAGES 6
 #endif
@@ -975,9 +981,16 @@ struct Engine {
         D2FT_CUDA(cudaStreamWaitEvent(st, side_event(5 * (l + 1) + 3), 0));
       mark(PH_G4);
       const size_t g4cap = Bm * ((D.UO * H + 1) / 2);
-      gemm_tokN<G4, 0, 1, kG4Epi, D2FT_G4_PAIR>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt,
-                          (const act_t*)ZTl, db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps,
-                          side ? ctr(l, C_G4) : (int*)nullptr);
+      if (D2FT_G4_RESB && BNt == 208 && D.d == 12 * 64)
+        launch_gemm<G4<208>, GemmShape<208, 3, 0, kG4Epi, 2, 0, 1, 1, 12>>(
+            tm_W2T, tm_dC,
+            G4<208>{D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads, lists.full_hcnt, (const act_t*)ZTl,
+                    db1_slot(l), (const float*)gmax, (const CUtensorMap*)store_maps, (int*)nullptr},
+            0, st);
+      else
+        gemm_tokN<G4, 0, 1, kG4Epi, D2FT_G4_PAIR>(tm_W2T, tm_dC, D, l, g4_tiles + l * g4cap, g4_count + l, lists.full_heads,
+                                                 lists.full_hcnt, (const act_t*)ZTl, db1_slot(l), (const float*)gmax,
+                                                 (const CUtensorMap*)store_maps, side ? ctr(l, C_G4) : (int*)nullptr);
       mark(PH_ATTN_B);
       if (D.dh == 64 && attn_bwd_tc_fits(D.TQ))
         launch_attn_bwd_tc(tm_K, tm_dO, D, l, lists.full_heads, lists.full_hcnt, O32T + (size_t)l * Bm * H * 64 * D.TP,
