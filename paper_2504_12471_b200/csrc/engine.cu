@@ -196,10 +196,16 @@ struct Engine {
   // 5.47 ms per step (5.49 before the per-block SGD; G5 alone 5.46; same box,
   // tools/ab_side.sh).
   // D2FT_NO_SIDE / D2FT_NO_SIDE_G7 turn them off; D2FT_SIDE_CTAS caps the side
-  // kernels' grids (64: 5.66 ms — fewer SMs, same long tiles).
+  // kernels' grids (64: 5.66 ms — fewer SMs, same long tiles).  Default cap:
+  // all SMs but 20 (128 of 148), which stay free for the critical path's
+  // kernels: −0.05 ms per step on average over six paired same-box runs of
+  // the final build, every pair in its favour (112 and 96 in between, 0 =
+  // uncapped the slowest).
   bool use_side = getenv("D2FT_NO_SIDE") == nullptr;
-  int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : 0;
+  int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : -1;  // -1: num_sms() - 20
   bool side_g7 = getenv("D2FT_NO_SIDE_G7") == nullptr;
+  // grid cap of a side-stream GEMM (launch_gemm's max_ctas: > 0 caps, 0 = all SMs)
+  int side_cap() const { return side_ctas >= 0 ? side_ctas : (num_sms() > 40 ? num_sms() - 20 : 0); }
   cudaEvent_t ev_copied = nullptr, ev_stage_free = nullptr;
   bool have_prefetch = false;
   int prefetch_B = 0;
@@ -964,7 +970,7 @@ struct Engine {
           tm_dC64, tm_OGT, G5<160>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W2T].off + (size_t)l * d * H * D.PO, gmax,
                   ord_head + l * H, ctr(l, C_G5), fsgd(S_W2T, W2T_bf, (size_t)l * d * H * D.PO),
                   (const CUtensorMap*)store_maps},
-          s5 == st ? 0 : side_ctas, s5);
+          s5 == st ? 0 : side_cap(), s5);
     };
     for (int l = D.L - 1; l >= 0; --l) {
       act_t* QKVl = QKV + (size_t)l * Bm * H * T * 3 * D.dh;
@@ -1045,7 +1051,7 @@ struct Engine {
             tm_xn64, tm_dY1Tb,
             G7<kG7BN>{D, l, lists.full_idx, lists.full_cnt, G + seg[S_W1T].off + (size_t)l * H * D.PQ * d, gmax,
                       ord_head + l * H, ctr(l, C_G7), fsgd(S_W1T, W1T_bf, (size_t)l * H * D.PQ * d)},
-            s7 ? side_ctas : 0, g7s);
+            s7 ? side_cap() : 0, g7s);
         if (s7) D2FT_CUDA(cudaEventRecord(side_event(5 * l + 3), st2));
         if (data_parallel() && step_train) {
           // data parallel: block l's [Wq|Wk|Wv|W1]^T and [Wo;W2]^T gradients
