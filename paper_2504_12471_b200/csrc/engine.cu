@@ -200,7 +200,7 @@ struct Engine {
   // all SMs but 20 (128 of 148), which stay free for the critical path's
   // kernels: −0.05 ms per step on average over six paired same-box runs of
   // the final build, every pair in its favour (112 and 96 in between, 0 =
-  // uncapped the slowest).
+  // uncapped the slowest; 120-144 within run-to-run noise of 128).
   bool use_side = getenv("D2FT_NO_SIDE") == nullptr;
   int side_ctas = getenv("D2FT_SIDE_CTAS") ? atoi(getenv("D2FT_SIDE_CTAS")) : -1;  // -1: num_sms() - 20
   bool side_g7 = getenv("D2FT_NO_SIDE_G7") == nullptr;
